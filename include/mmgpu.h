@@ -1,0 +1,269 @@
+/*
+ * mmgpu.h — C ABI of the B200 metric + move-method engine (libmmgpu.so).
+ *
+ * This is the drop-in boundary for the reference library's hot path
+ * (/root/reference/proj/include/modmetrics/{metrics,parallel,suggest}.hpp).
+ * Plain C: fixed-width integers, raw pointers and sizes, no C++ or torch
+ * types, no exception crosses it. Every entry point returns an mm_status;
+ * the status codes map one-to-one onto the exception types the reference
+ * throws (see MM_E_RANGE / MM_E_ARG below), and include/modmetrics/gpu.hpp
+ * rethrows exactly those types for C++ callers.
+ *
+ * Each function cites the reference interface it replaces (file:line, paths
+ * relative to /root/reference/proj/include/modmetrics/).
+ *
+ * Threading: one mm_ctx == one CUDA device + one CUDA stream. A context is
+ * not thread-safe; distinct contexts (one per GPU) may be driven from
+ * distinct host threads or processes.
+ */
+#ifndef MMGPU_H
+#define MMGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MMGPU_ABI_VERSION 1
+
+typedef enum mm_status {
+    MM_OK = 0,
+    MM_E_RANGE = 1,       /* std::out_of_range  (metrics.hpp:97-100, suggest.hpp:89-90, model.hpp:66-67) */
+    MM_E_ARG = 2,         /* std::invalid_argument (suggest.hpp:91-96, :313, parallel.hpp:29, generate.hpp:97-100) */
+    MM_E_CUDA = 3,        /* CUDA runtime failure (no device, launch error, ...) */
+    MM_E_OOM = 4,         /* device allocation failed */
+    MM_E_STATE = 5,       /* call order violated (e.g. sweep before upload) */
+    MM_E_UNSUPPORTED = 6, /* outside this engine's scope (e.g. Criterion::Similarity) */
+    MM_E_CAPACITY = 7     /* caller buffer too small; *n_out holds the needed count */
+} mm_status;
+
+/* Criterion bits: bit (1 << Criterion) with Criterion as in suggest.hpp:17
+ * (Similarity = 0, Cohesion = 1, Coupling = 2). */
+#define MM_CRIT_SIMILARITY (1u << 0)
+#define MM_CRIT_COHESION (1u << 1)
+#define MM_CRIT_COUPLING (1u << 2)
+
+/* Combine, suggest.hpp:296 */
+#define MM_COMBINE_UNION 0
+#define MM_COMBINE_INTERSECTION 1
+
+/*
+ * A system snapshot in CSR form: SystemModel + DependencyTable
+ * (model.hpp:19-53) with every vector<vector<u32>> flattened to
+ * (offsets, values). Host memory; mm_upload copies it.
+ *
+ * Preconditions are the reference's: the model passes validate()
+ * (model.hpp:113-212): ids dense, membership partitions each id space and
+ * agrees with the owner tables, every member/dependency list sorted unique,
+ * no self-calls. mm_upload range-checks every id on the device and fails
+ * with MM_E_ARG instead of faulting; the sorted/unique/partition invariants
+ * are the caller's contract exactly as in the reference.
+ * Edge counts are limited to < 2^32 per table (u32 offsets).
+ */
+typedef struct mm_system {
+    uint32_t n_classes;
+    uint32_t n_methods;
+    uint32_t n_attributes;
+    uint32_t reserved;
+    const uint32_t* method_owner;     /* [n_methods]      SystemModel::method_owner (model.hpp:35) */
+    const uint32_t* attribute_owner;  /* [n_attributes]   SystemModel::attribute_owner (model.hpp:36) */
+    const uint32_t* class_method_off; /* [n_classes + 1]  ClassRecord::method_ids, concatenated (model.hpp:23) */
+    const uint32_t* class_methods;    /* [n_methods] */
+    const uint32_t* class_attr_off;   /* [n_classes + 1]  ClassRecord::attribute_ids, concatenated (model.hpp:22) */
+    const uint32_t* class_attrs;      /* [n_attributes] */
+    const uint32_t* call_off;         /* [n_methods + 1]  DependencyTable::calls (model.hpp:49) */
+    const uint32_t* call_tgt;         /* [call_off[n_methods]] */
+    const uint32_t* acc_off;          /* [n_methods + 1]  DependencyTable::accesses (model.hpp:50) */
+    const uint32_t* acc_tgt;          /* [acc_off[n_methods]] */
+} mm_system;
+
+/* WhatIfMetrics, suggest.hpp:72-85 (same field order and types). */
+typedef struct mm_whatif {
+    double lcom_origin_before;
+    double lcom_origin_after;
+    double lcom_dest_before;
+    double lcom_dest_after;
+    uint32_t cbo_origin_before;
+    uint32_t cbo_origin_after;
+    uint32_t cbo_dest_before;
+    uint32_t cbo_dest_after;
+    uint8_t origin_degenerate_after;
+    uint8_t dest_degenerate_after;
+    uint8_t pad[6];
+} mm_whatif; /* 56 bytes */
+
+/* MoveSuggestion, suggest.hpp:124-132: 64-byte record. `criteria` is the
+ * sorted-unique criteria vector as a bit set of MM_CRIT_* bits. */
+typedef struct mm_suggestion {
+    double lcom_origin_before;
+    double lcom_origin_after;
+    double lcom_dest_before;
+    double lcom_dest_after;
+    uint32_t method;
+    uint32_t origin;
+    uint32_t destination;
+    uint32_t cbo_origin_before;
+    uint32_t cbo_origin_after;
+    uint32_t cbo_dest_before;
+    uint32_t cbo_dest_after;
+    uint8_t criteria;
+    uint8_t origin_degenerate_after;
+    uint8_t dest_degenerate_after;
+    uint8_t pad;
+} mm_suggestion; /* 64 bytes */
+
+/* ThresholdOverrides / Thresholds, suggest.hpp:28-41. has_* = optional engaged. */
+typedef struct mm_overrides {
+    uint8_t has_similarity, has_lcom, has_cbo, pad;
+    double similarity;
+    double lcom;
+    double cbo;
+} mm_overrides;
+
+typedef struct mm_thresholds {
+    double similarity;
+    double lcom;
+    double cbo;
+    uint8_t explicit_mode;
+    uint8_t pad[7];
+} mm_thresholds;
+
+/* Parameters of one candidate sweep: suggest_all (suggest.hpp:303) over
+ * criteria ⊆ {Cohesion, Coupling}, or a single suggest_by_* when one bit is
+ * set. `class_begin/class_end` restrict the sweep to origins in that class
+ * range (the multi-GPU shard); [0, n_classes) is the whole system.
+ * top_k: 0 or 1 = the reference's best-only mode; k > 1 keeps the k best
+ * passing destinations per (criterion, method) (an extension; ordered like
+ * all_candidates output). all_candidates = SuggestOptions::all_candidates
+ * (suggest.hpp:134-138) and overrides top_k. */
+typedef struct mm_sweep_params {
+    uint32_t criteria;       /* MM_CRIT_* bits */
+    uint32_t combine;        /* MM_COMBINE_* */
+    uint32_t all_candidates; /* 0/1 */
+    uint32_t top_k;          /* 0/1 = best only */
+    double thr_lcom;         /* Thresholds::lcom  (gate: lcom[c] > thr_lcom, suggest.hpp:246) */
+    double thr_cbo;          /* Thresholds::cbo   (gate: (double)cbo[c] > thr_cbo, suggest.hpp:273) */
+    uint32_t class_begin;
+    uint32_t class_end;      /* 0 == n_classes */
+    uint32_t threshold_source; /* MM_THR_EXPLICIT: thr_lcom/thr_cbo above;
+                                  MM_THR_DEVICE_MEANS: the means computed on the device by the
+                                  last mm_compute_metrics (compute_thresholds with no overrides),
+                                  read without a host round trip */
+    uint32_t pad;
+} mm_sweep_params;
+
+#define MM_THR_EXPLICIT 0
+#define MM_THR_DEVICE_MEANS 1
+
+typedef struct mm_sweep_stats {
+    uint64_t candidates;     /* (method, destination) pairs scored, ungated: Σ|used_classes(u)| */
+    uint64_t gated_whatifs;  /* what-ifs the reference would evaluate: per criterion, gated classes only */
+    uint64_t suggestions;    /* records emitted */
+    uint64_t methods;        /* methods swept */
+} mm_sweep_stats;
+
+typedef struct mm_kernel_stat {
+    char name[32];
+    uint64_t launches;
+    double total_ms; /* CUDA-event time summed over launches (profiling on) */
+} mm_kernel_stat;
+
+typedef struct mm_ctx mm_ctx;
+
+/* ---- context ---------------------------------------------------------- */
+mm_status mm_ctx_create(int device, mm_ctx** out);
+void mm_ctx_destroy(mm_ctx* ctx);
+const char* mm_last_error(const mm_ctx* ctx); /* never NULL */
+int mm_abi_version(void);
+/* Run all work on this cudaStream_t (e.g. torch's current stream). NULL = the ctx's own stream. */
+mm_status mm_ctx_set_stream(mm_ctx* ctx, void* cuda_stream);
+mm_status mm_ctx_synchronize(mm_ctx* ctx);
+/* Per-kernel CUDA-event timing (adds two event records per launch). */
+mm_status mm_ctx_set_profiling(mm_ctx* ctx, int on);
+mm_status mm_kernel_stats(mm_ctx* ctx, mm_kernel_stat* out, int cap, int* n_out);
+mm_status mm_reset_kernel_stats(mm_ctx* ctx);
+
+/* ---- model upload (replaces passing const SystemModel&, const DependencyTable&) ---- */
+mm_status mm_upload(mm_ctx* ctx, const mm_system* sys);
+/* Bytes of the uploaded CSR (what one H2D of the system costs). */
+uint64_t mm_system_bytes(const mm_system* sys);
+
+/* ---- class metric pass ------------------------------------------------ */
+/* Device-resident recompute of per-class LCOM (normalized), LCOM-CK, CBO and
+ * the class×class use-count table. Replaces full_report's class loop
+ * (metrics.hpp:253-261) / parallel_class_metrics (parallel.hpp:149) +
+ * parallel_lcom_ck (parallel.hpp:164). No host copy. */
+mm_status mm_compute_metrics(mm_ctx* ctx);
+/* Copies results (any pointer may be NULL). Runs mm_compute_metrics first if
+ * the model changed since the last pass.
+ *   lcom    == lcom_normalized per class (metrics.hpp:128)
+ *   lcom_ck == lcom_ck per class         (metrics.hpp:159)
+ *   cbo     == cbo per class             (metrics.hpp:187) */
+mm_status mm_class_metrics(mm_ctx* ctx, double* lcom, uint64_t* lcom_ck, uint32_t* cbo);
+/* Single-class accessors with the reference's error behaviour
+ * (out_of_range on a bad id, metrics.hpp:97-100). */
+mm_status mm_lcom_normalized(mm_ctx* ctx, uint32_t cls, double* out);
+mm_status mm_lcom_ck(mm_ctx* ctx, uint32_t cls, uint64_t* out);
+mm_status mm_cbo(mm_ctx* ctx, uint32_t cls, uint32_t* out);
+
+/* ---- thresholds (compute_thresholds, suggest.hpp:46-61) --------------- */
+/* Means of the device-resident per-class lcom/cbo, bit-identical to the
+ * reference's sequential double sums (computed on the device by the metric
+ * pass; this call copies 24 bytes back and applies the overrides).
+ * similarity is out of scope for this engine (no similarity table): it is
+ * the override when given, else 0. */
+mm_status mm_compute_thresholds(mm_ctx* ctx, const mm_overrides* ov, mm_thresholds* out);
+/* ---- what-if (what_if_move, suggest.hpp:87-122) ----------------------- */
+mm_status mm_what_if(mm_ctx* ctx, uint32_t method, uint32_t origin, uint32_t destination,
+                     mm_whatif* out);
+
+/* ---- candidate sweep (suggest_by_cohesion/coupling, suggest_all) ------- */
+/* Runs the sweep on the device; the ordered result stays resident.
+ * n_out (may be NULL) receives the record count (a D2H of 8 bytes). */
+mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out);
+/* Device pointer to the last sweep's records (mm_suggestion[n]), for
+ * device-side exchange (NCCL all-gather) without a host round trip. */
+mm_status mm_sweep_device_result(mm_ctx* ctx, const void** dev_records, uint64_t* n);
+mm_status mm_sweep_stats_get(mm_ctx* ctx, mm_sweep_stats* out);
+/* Copies the last sweep's records to host memory; MM_E_CAPACITY (with
+ * *n_out = needed) when cap is too small. */
+mm_status mm_copy_suggestions(mm_ctx* ctx, mm_suggestion* out, uint64_t cap, uint64_t* n_out);
+/* mm_sweep + mm_copy_suggestions: the reference-facing one-call form of
+ * suggest_all(model, deps, report, thresholds, criteria, combine, opts). */
+mm_status mm_suggest(mm_ctx* ctx, const mm_sweep_params* p, mm_suggestion* out, uint64_t cap,
+                     uint64_t* n_out);
+
+/* ---- host-side helpers (no GPU needed) --------------------------------- */
+/* Contiguous class ranges balanced by sweep cost (Σ over members of
+ * 1 + |calls| + |accesses|), the GPU analogue of plan_partition
+ * (parallel.hpp:28-41). bounds has n_shards + 1 entries. n_shards == 0 ->
+ * MM_E_ARG like plan_partition's zero-worker check. */
+mm_status mm_plan_shards(const mm_system* sys, uint32_t n_shards, uint32_t* bounds);
+
+/* Synthetic systems. mm_gen_config mirrors GeneratorConfig (generate.hpp:39-47);
+ * zipf_s > 0 selects the skewed-size variant:
+ * class sizes ∝ 1/rank^s, ids shuffled over classes by SplitMix64, deps drawn
+ * exactly as generate.hpp:124-161. */
+typedef struct mm_gen_config {
+    uint64_t seed;
+    uint32_t n_classes;
+    uint32_t n_methods;
+    uint32_t n_attributes;
+    uint32_t k_max_calls;
+    uint32_t k_max_accesses;
+    uint32_t pad;
+    double intra_class_bias;
+    double zipf_s; /* 0 = reference round-robin generate() */
+} mm_gen_config;
+
+typedef struct mm_host_system mm_host_system;
+mm_status mm_generate(const mm_gen_config* cfg, mm_host_system** out);
+const mm_system* mm_host_system_view(const mm_host_system* h);
+void mm_host_system_free(mm_host_system* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMGPU_H */

@@ -1,0 +1,221 @@
+"""ctypes bindings to the CPU oracle (liboracle.so) and the compiled reference (_ref/libmmref.so).
+
+TEST INFRASTRUCTURE ONLY. Importable solely from tests/, __graft_entry__.smoke()
+and bench.py's CPU-baseline / --impl reference leg — as the checker or the
+timed CPU baseline, never as the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from paper_1308_4011_b200 import abi
+from paper_1308_4011_b200.system import System
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle.so"
+REF_SO = HERE / "_ref" / "libmmref.so"
+_or = None
+_ref = None
+
+
+def oracle_lib():
+    global _or
+    if _or is None:
+        l = C.CDLL(str(ORACLE_SO))
+        S = C.POINTER(abi.mm_system)
+        l.or_class_metrics.argtypes = [S, C.c_void_p, C.c_void_p, C.c_void_p]
+        l.or_thresholds.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                    C.POINTER(abi.mm_overrides), C.POINTER(abi.mm_thresholds)]
+        l.or_what_if.argtypes = [S, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(abi.mm_whatif)]
+        l.or_suggest.argtypes = [S, C.c_void_p, C.c_void_p, C.POINTER(abi.mm_sweep_params), C.c_void_p,
+                                 C.c_uint64, C.POINTER(C.c_uint64)]
+        _or = l
+    return _or
+
+
+def ref_available() -> bool:
+    return REF_SO.exists()
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        l = C.CDLL(str(REF_SO))
+        S = C.POINTER(abi.mm_system)
+        l.ref_model_create.argtypes = [S]
+        l.ref_model_create.restype = C.c_void_p
+        l.ref_model_free.argtypes = [C.c_void_p]
+        l.ref_validate.argtypes = [C.c_void_p]
+        l.ref_generate.argtypes = [C.POINTER(abi.mm_gen_config)]
+        l.ref_generate.restype = C.c_void_p
+        l.ref_model_view.argtypes = [C.c_void_p]
+        l.ref_model_view.restype = S
+        l.ref_class_metrics.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p, C.c_void_p]
+        l.ref_single_metric.argtypes = [C.c_void_p, C.c_int, C.c_uint32, C.POINTER(C.c_double),
+                                        C.POINTER(C.c_uint64)]
+        l.ref_thresholds.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                     C.POINTER(abi.mm_overrides), C.POINTER(abi.mm_thresholds)]
+        l.ref_what_if.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(abi.mm_whatif)]
+        l.ref_suggest.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(abi.mm_sweep_params), C.c_void_p,
+                                  C.c_uint64, C.POINTER(C.c_uint64)]
+        l.ref_suggest_by.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p,
+                                     C.POINTER(abi.mm_sweep_params), C.c_void_p, C.c_uint64,
+                                     C.POINTER(C.c_uint64)]
+        l.ref_sweep_sample.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_uint32,
+                                       C.c_uint32, C.c_uint, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        _ref = l
+    return _ref
+
+
+def _overrides(ov):
+    o = abi.mm_overrides()
+    if ov:
+        for k, v in ov.items():
+            if v is not None:
+                setattr(o, "has_" + k, 1)
+                setattr(o, k, float(v))
+    return o
+
+
+def _params(criteria_mask, combine=0, all_candidates=False, top_k=1, thr_lcom=0.0, thr_cbo=0.0,
+            class_range=None):
+    p = abi.mm_sweep_params(criteria=criteria_mask, combine=combine, all_candidates=int(all_candidates),
+                            top_k=top_k, thr_lcom=thr_lcom, thr_cbo=thr_cbo)
+    if class_range:
+        p.class_begin, p.class_end = class_range
+    return p
+
+
+# ---- oracle (C restatement) ----------------------------------------------
+
+def class_metrics(sys_: System):
+    s = sys_.as_c()
+    n = sys_.n_classes
+    lcom, ck, cbo = np.empty(n, np.float64), np.empty(n, np.uint64), np.empty(n, np.uint32)
+    oracle_lib().or_class_metrics(C.byref(s), lcom.ctypes.data, ck.ctypes.data, cbo.ctypes.data)
+    return lcom, ck, cbo
+
+
+def thresholds(lcom, cbo, similarity=None, overrides=None):
+    lcom = np.ascontiguousarray(lcom, np.float64)
+    cbo = np.ascontiguousarray(cbo, np.uint32)
+    sim = np.ascontiguousarray(similarity if similarity is not None else [], np.float64)
+    t = abi.mm_thresholds()
+    o = _overrides(overrides)
+    oracle_lib().or_thresholds(lcom.ctypes.data, cbo.ctypes.data, len(lcom), sim.ctypes.data, len(sim),
+                               C.byref(o), C.byref(t))
+    return t
+
+
+def what_if(sys_: System, u, o, d):
+    s = sys_.as_c()
+    w = abi.mm_whatif()
+    st = oracle_lib().or_what_if(C.byref(s), u, o, d, C.byref(w))
+    return st, w
+
+
+def suggest(sys_: System, lcom_gate, cbo_gate, criteria_mask, combine=0, all_candidates=False, top_k=1,
+            thr_lcom=0.0, thr_cbo=0.0, class_range=None):
+    s = sys_.as_c()
+    lg = np.ascontiguousarray(lcom_gate, np.float64)
+    cg = np.ascontiguousarray(cbo_gate, np.uint32)
+    p = _params(criteria_mask, combine, all_candidates, top_k, thr_lcom, thr_cbo, class_range)
+    n = C.c_uint64()
+    st = oracle_lib().or_suggest(C.byref(s), lg.ctypes.data, cg.ctypes.data, C.byref(p), None, 0, C.byref(n))
+    out = np.zeros(n.value, dtype=abi.SUGGESTION_DTYPE)
+    if n.value:
+        st = oracle_lib().or_suggest(C.byref(s), lg.ctypes.data, cg.ctypes.data, C.byref(p), out.ctypes.data,
+                                     n.value, C.byref(n))
+    if st:
+        raise RuntimeError(f"or_suggest status {st}")
+    return out
+
+
+# ---- the reference itself (compiled headers) -----------------------------
+
+class RefModel:
+    def __init__(self, sys_: System = None, handle=None):
+        self._keep = sys_
+        self.h = handle if handle is not None else ref_lib().ref_model_create(C.byref(sys_.as_c()))
+        self.n_classes = ref_lib().ref_model_view(self.h).contents.n_classes if handle is not None else sys_.n_classes
+
+    def close(self):
+        if self.h:
+            ref_lib().ref_model_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def validate(self) -> int:
+        return ref_lib().ref_validate(self.h)
+
+    def class_metrics(self, n_workers=0):
+        n = self.n_classes
+        lcom, ck, cbo = np.empty(n, np.float64), np.empty(n, np.uint64), np.empty(n, np.uint32)
+        st = ref_lib().ref_class_metrics(self.h, n_workers, lcom.ctypes.data, ck.ctypes.data, cbo.ctypes.data)
+        if st:
+            raise RuntimeError(f"ref_class_metrics status {st}")
+        return lcom, ck, cbo
+
+    def what_if(self, u, o, d):
+        w = abi.mm_whatif()
+        st = ref_lib().ref_what_if(self.h, u, o, d, C.byref(w))
+        return st, w
+
+    def suggest(self, lcom_gate, cbo_gate, criteria_mask, combine=0, all_candidates=False, thr_lcom=0.0,
+                thr_cbo=0.0, by=None):
+        lg = np.ascontiguousarray(lcom_gate, np.float64)
+        cg = np.ascontiguousarray(cbo_gate, np.uint32)
+        p = _params(criteria_mask, combine, all_candidates, 1, thr_lcom, thr_cbo)
+        n = C.c_uint64()
+        L = ref_lib()
+
+        def call(out, cap):
+            if by is None:
+                return L.ref_suggest(self.h, lg.ctypes.data, cg.ctypes.data, C.byref(p), out, cap, C.byref(n))
+            return L.ref_suggest_by(self.h, by, lg.ctypes.data, cg.ctypes.data, C.byref(p), out, cap, C.byref(n))
+
+        st = call(None, 0)
+        if st not in (0, abi.MM_E_CAPACITY):
+            return st, None
+        out = np.zeros(n.value, dtype=abi.SUGGESTION_DTYPE)
+        if n.value:
+            st = call(out.ctypes.data, n.value)
+        return st, out
+
+    def sweep_sample(self, lcom_gate, cbo_gate, thr_lcom, thr_cbo, class_begin, class_end, n_workers):
+        lg = np.ascontiguousarray(lcom_gate, np.float64)
+        cg = np.ascontiguousarray(cbo_gate, np.uint32)
+        ns, nc = C.c_uint64(), C.c_uint64()
+        st = ref_lib().ref_sweep_sample(self.h, lg.ctypes.data, cg.ctypes.data, thr_lcom, thr_cbo, class_begin,
+                                        class_end, n_workers, C.byref(ns), C.byref(nc))
+        if st:
+            raise RuntimeError(f"ref_sweep_sample status {st}")
+        return ns.value, nc.value
+
+
+def ref_generate(**cfg) -> System:
+    c = abi.mm_gen_config(**cfg)
+    h = ref_lib().ref_generate(C.byref(c))
+    try:
+        return System.from_view(ref_lib().ref_model_view(h).contents)
+    finally:
+        ref_lib().ref_model_free(h)
+
+
+def ref_thresholds(lcom, cbo, similarity=None, overrides=None):
+    lcom = np.ascontiguousarray(lcom, np.float64)
+    cbo = np.ascontiguousarray(cbo, np.uint32)
+    sim = np.ascontiguousarray(similarity if similarity is not None else [], np.float64)
+    t = abi.mm_thresholds()
+    o = _overrides(overrides)
+    ref_lib().ref_thresholds(lcom.ctypes.data, cbo.ctypes.data, len(lcom), sim.ctypes.data, len(sim), C.byref(o),
+                             C.byref(t))
+    return t

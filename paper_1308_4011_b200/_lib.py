@@ -1,0 +1,91 @@
+"""Loader for the in-tree libmmgpu.so. Fails loudly: there is no fallback."""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from . import abi
+
+_LIB_PATH = Path(__file__).resolve().parent / "libmmgpu.so"
+_lib = None
+
+
+class MMError(RuntimeError):
+    """A non-OK mm_status. `.status` holds the code."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{abi.STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class MMRangeError(MMError, IndexError):
+    """MM_E_RANGE — the reference throws std::out_of_range here."""
+
+
+class MMArgError(MMError, ValueError):
+    """MM_E_ARG — the reference throws std::invalid_argument here."""
+
+
+def _exc_for(status: int):
+    return {abi.MM_E_RANGE: MMRangeError, abi.MM_E_ARG: MMArgError}.get(status, MMError)
+
+
+_SIGS = {
+    "mm_abi_version": (C.c_int, []),
+    "mm_last_error": (C.c_char_p, [C.c_void_p]),
+    "mm_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "mm_ctx_destroy": (None, [C.c_void_p]),
+    "mm_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "mm_ctx_synchronize": (C.c_int, [C.c_void_p]),
+    "mm_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
+    "mm_kernel_stats": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_kernel_stat), C.c_int, C.POINTER(C.c_int)]),
+    "mm_reset_kernel_stats": (C.c_int, [C.c_void_p]),
+    "mm_upload": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_system)]),
+    "mm_system_bytes": (C.c_uint64, [C.POINTER(abi.mm_system)]),
+    "mm_compute_metrics": (C.c_int, [C.c_void_p]),
+    "mm_class_metrics": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mm_lcom_normalized": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_double)]),
+    "mm_lcom_ck": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]),
+    "mm_cbo": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "mm_compute_thresholds": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_overrides), C.POINTER(abi.mm_thresholds)]),
+    "mm_what_if": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(abi.mm_whatif)]),
+    "mm_sweep": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_params), C.POINTER(C.c_uint64)]),
+    "mm_sweep_device_result": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
+    "mm_sweep_stats_get": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_stats)]),
+    "mm_copy_suggestions": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
+    "mm_suggest": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_params), C.c_void_p, C.c_uint64,
+                             C.POINTER(C.c_uint64)]),
+    "mm_plan_shards": (C.c_int, [C.POINTER(abi.mm_system), C.c_uint32, C.POINTER(C.c_uint32)]),
+    "mm_generate": (C.c_int, [C.POINTER(abi.mm_gen_config), C.POINTER(C.c_void_p)]),
+    "mm_host_system_view": (C.POINTER(abi.mm_system), [C.c_void_p]),
+    "mm_host_system_free": (None, [C.c_void_p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def lib() -> C.CDLL:
+    """The loaded libmmgpu.so. Raises if it has not been built — never falls back."""
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise RuntimeError(
+                f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(this engine has no CPU fallback)")
+        l = C.CDLL(str(_LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(l, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = l
+    return _lib
+
+
+def check(status: int, ctx, what: str) -> None:
+    if status != abi.MM_OK:
+        msg = lib().mm_last_error(ctx).decode() if ctx else what
+        raise _exc_for(status)(status, f"{what}: {msg}")

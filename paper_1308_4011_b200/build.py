@@ -1,0 +1,70 @@
+"""Build the in-tree native libraries.
+
+    libmmgpu.so  (paper_1308_4011_b200/)  the product: CUDA kernels for sm_100a + the C ABI
+    oracle/liboracle.so, oracle/_ref/libmmref.so  test/baseline infrastructure (oracle/Makefile)
+
+Everything is compiled explicitly with nvcc / gcc into the source tree so the
+built .so files travel with the repo snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libmmgpu.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-fmad=false",          # IEEE mul/add everywhere; the fp64 metric paths also use _rn intrinsics
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+    "-Xptxas", "-v",
+    "--expt-relaxed-constexpr",
+]
+
+
+def _sources():
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def build_lib(force: bool = False, verbose: bool = False) -> Path:
+    deps = _sources() + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "mmgpu.h"]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-o", str(LIB), *map(str, _sources())]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    log = PKG / "build.log"
+    log.write_text(" ".join(cmd) + "\n\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"nvcc failed building {LIB.name} (see {log})")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    return LIB
+
+
+def build_oracle() -> None:
+    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
+
+
+def build_all(force: bool = False) -> None:
+    build_lib(force=force)
+    build_oracle()
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)
+    print("built", LIB)

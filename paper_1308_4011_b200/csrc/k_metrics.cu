@@ -1,0 +1,448 @@
+// k_metrics.cu — the class metric pass (LCOM normalized, LCOM-CK, CBO + the
+// class×class use-count rows U) and the threshold means.
+//
+// Replaces the per-class loop of full_report (metrics.hpp:253-261) and
+// parallel_class_metrics / parallel_lcom_ck (parallel.hpp:149-174). Results
+// are bit-identical to the reference:
+//   lcom    : H = Σ_p |acc(p) ∩ attrs(c)| counted as accesses whose owner is c
+//             (same integer as intersection_count, metrics.hpp:121-123 for a
+//             validated model), then the reference's single-division formula.
+//   lcom_ck : Q = #pairs (i<j) whose own-attribute sets intersect; with
+//             P = C(M,2) - Q the reference returns P > Q ? P - Q : 0
+//             (metrics.hpp:147-156).
+//   cbo     : |{owner(t) : t ∈ calls ∪ accesses of members} \ {c}|
+//             (metrics.hpp:167-185), built as the sorted U row with counts.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mm_device.cuh"
+#include "mm_kernels.h"
+
+namespace mmg {
+
+// ---------------------------------------------------------------------------
+// upload-time: range validation and class planning
+// ---------------------------------------------------------------------------
+
+__global__ void k_validate_ids(const uint32_t* __restrict__ v, uint64_t n, uint32_t bound,
+                               uint32_t* __restrict__ bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        if (v[i] >= bound) atomicOr(bad, 1u);
+}
+
+// offsets must be non-decreasing, start at 0 and end at `total`
+__global__ void k_validate_offsets(const uint32_t* __restrict__ off, uint64_t n_plus_1, uint32_t total,
+                                   uint32_t* __restrict__ bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_plus_1;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (i == 0 && off[0] != 0) atomicOr(bad, 2u);
+        if (i + 1 == n_plus_1 && off[i] != total) atomicOr(bad, 2u);
+        if (i + 1 < n_plus_1 && off[i] > off[i + 1]) atomicOr(bad, 2u);
+    }
+}
+
+// Per class: member/attribute counts, Σ degree, max degree, foreign-edge
+// count; classify into the warp path (small) or the CTA path (large).
+__global__ void k_plan_classes(DevModel s, uint8_t* __restrict__ kind, uint32_t* __restrict__ large_list,
+                               uint32_t* __restrict__ n_large, uint32_t* __restrict__ max_deg,
+                               uint32_t* __restrict__ foreign) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= s.C) return;
+    const uint32_t mb = s.cls_moff[c], me = s.cls_moff[c + 1];
+    const uint32_t A = s.cls_aoff[c + 1] - s.cls_aoff[c];
+    uint32_t mdeg = 0, fr = 0;
+    for (uint32_t i = mb; i < me; ++i) {
+        const uint32_t p = s.cls_methods[i];
+        const uint32_t cb = s.call_off[p], ce = s.call_off[p + 1];
+        const uint32_t ab = s.acc_off[p], ae = s.acc_off[p + 1];
+        mdeg = max(mdeg, (ce - cb) + (ae - ab));
+        for (uint32_t e = cb; e < ce; ++e) fr += s.method_owner[s.call_tgt[e]] != c;
+        for (uint32_t e = ab; e < ae; ++e) fr += s.attribute_owner[s.acc_tgt[e]] != c;
+    }
+    foreign[c] = fr;
+    const bool small = (me - mb) <= kSmallMaxMembers && A <= kSmallMaxAttrs && mdeg <= kSmallMaxDeg;
+    kind[c] = small ? 0 : 1;
+    if (!small) large_list[atomicAdd(n_large, 1u)] = c;
+    atomicMax(max_deg, mdeg);
+}
+
+// attr_local[t] = index of attribute t in its class's sorted attribute list
+__global__ void k_attr_local(DevModel s, uint32_t* __restrict__ attr_local) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < s.A; j += gridDim.x * blockDim.x) {
+        const uint32_t t = s.cls_attrs[j];
+        attr_local[t] = j - s.cls_aoff[s.attribute_owner[t]];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// warp path: one warp per class, one lane per member (M ≤ 32, A ≤ 64, deg ≤ 16)
+// ---------------------------------------------------------------------------
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kSmallEntries = kSmallMaxMembers * kSmallMaxDeg;  // 512
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) { return __reduce_add_sync(0xffffffffu, v); }
+
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, int lane) {
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    return x - v;
+}
+
+// ascending bitonic sort of buf[0, N) (N a power of two ≥ 2), one warp
+__device__ __forceinline__ void warp_bitonic_u32(uint32_t* buf, int N, int lane) {
+    for (int k = 2; k <= N; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < N; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint32_t a = buf[i], b = buf[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) { buf[i] = b; buf[ixj] = a; }
+                }
+            }
+            __syncwarp();
+        }
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+k_class_small(DevModel s, const uint8_t* __restrict__ kind, const uint32_t* __restrict__ attr_local,
+              ClassRec* __restrict__ rec, double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out,
+              uint32_t* __restrict__ cbo_out, uint32_t* __restrict__ ux, uint32_t* __restrict__ un,
+              uint32_t* __restrict__ ucursor) {
+    __shared__ uint32_t sbuf[kWarpsPerBlock][kSmallEntries];
+    __shared__ uint16_t shead[kWarpsPerBlock][kSmallEntries + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t c = blockIdx.x * kWarpsPerBlock + warp;
+    if (c >= s.C || kind[c] != 0) return;  // warp-uniform exit
+    const uint32_t mb = s.cls_moff[c];
+    const uint32_t M = s.cls_moff[c + 1] - mb;
+    const uint32_t A = s.cls_aoff[c + 1] - s.cls_aoff[c];
+
+    UsedList<kSmallMaxDeg> L;
+    L.clear();
+    uint64_t mask = 0;  // own-attribute set as bits of attr_local
+    uint32_t hown = 0;  // |acc(p) ∩ attrs(c)|
+    if (lane < (int)M) {
+        const uint32_t p = s.cls_methods[mb + lane];
+        const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
+        for (uint32_t e = cb; e < ce; ++e) L.insert(__ldg(s.method_owner + __ldg(s.call_tgt + e)), 0);
+        const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+        for (uint32_t e = ab; e < ae; ++e) {
+            const uint32_t t = __ldg(s.acc_tgt + e);
+            const uint32_t o = __ldg(s.attribute_owner + t);
+            L.insert(o, 1);
+            if (o == c) {
+                mask |= 1ull << __ldg(attr_local + t);
+                ++hown;
+            }
+        }
+    }
+    const uint32_t H = warp_sum(hown);
+
+    // LCOM-CK: Q = #pairs (i<j) with intersecting own sets
+    uint32_t q = 0;
+    for (uint32_t k = 0; k < M; ++k) {
+        const uint64_t mk = __shfl_sync(0xffffffffu, mask, k);
+        if ((uint32_t)lane < k && (mask & mk)) ++q;
+    }
+    const uint32_t Q = warp_sum(q);
+
+    // U row: multiset union of members' used classes other than c
+    const uint32_t has_c = L.has(c) ? 1u : 0u;
+    const uint32_t cnt = lane < (int)M ? (uint32_t)L.n - has_c : 0u;
+    const uint32_t off = warp_excl_scan(cnt, lane);
+    const uint32_t T = __shfl_sync(0xffffffffu, off + cnt, 31);
+    uint32_t* buf = sbuf[warp];
+    {
+        uint32_t w = off;
+#pragma unroll
+        for (int k = 0; k < kSmallMaxDeg; ++k)
+            if (k < L.n && L.X[k] != c) buf[w++] = L.X[k];
+    }
+    int N = 32;
+    while (N < (int)T) N <<= 1;
+    for (int i = (int)T + lane; i < N; i += 32) buf[i] = kNone;
+    __syncwarp();
+    warp_bitonic_u32(buf, N, lane);
+
+    uint16_t* heads = shead[warp];
+    uint32_t nh = 0;
+    for (uint32_t base = 0; base < T; base += 32) {
+        const uint32_t i = base + lane;
+        const bool head = i < T && (i == 0 || buf[i] != buf[i - 1]);
+        const uint32_t b = __ballot_sync(0xffffffffu, head);
+        if (head) heads[nh + __popc(b & ((1u << lane) - 1))] = (uint16_t)i;
+        nh += __popc(b);
+    }
+    if (lane == 0) heads[nh] = (uint16_t)T;
+    __syncwarp();
+    const uint32_t cbo = nh;
+    uint32_t ubase = 0;
+    if (lane == 0 && cbo) ubase = atomicAdd(ucursor, cbo);  // slot reservation
+    ubase = __shfl_sync(0xffffffffu, ubase, 0);
+    for (uint32_t k = lane; k < cbo; k += 32) {
+        ux[ubase + k] = buf[heads[k]];
+        un[ubase + k] = (uint32_t)heads[k + 1] - heads[k];
+    }
+    if (lane == 0) {
+        const double l = lcom_of(A, M, H);
+        const uint64_t pairs = (uint64_t)M * (M - 1) / 2;
+        const uint64_t P = pairs - Q;
+        ClassRec r;
+        r.A = A; r.M = M; r.H = H; r.cbo = cbo; r.ubase = ubase; r.pad = 0; r.lcom = l;
+        rec[c] = r;
+        lcom_out[c] = l;
+        ck_out[c] = P > Q ? P - Q : 0;
+        cbo_out[c] = cbo;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CTA path: one CTA per large class (any M, A, degree)
+// ---------------------------------------------------------------------------
+
+constexpr int kLargeThreads = 256;
+
+__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(0xffffffffu, v, d);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    uint64_t t = 0;
+    for (int w = 0; w < kLargeThreads / 32; ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
+// exclusive block scan of one u32 per thread; returns total in *total
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* red, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t inc = warp_excl_scan(v, lane) + v;
+    __syncthreads();
+    if (lane == 31) red[warp] = inc;
+    __syncthreads();
+    uint32_t before = 0, all = 0;
+    for (int w = 0; w < kLargeThreads / 32; ++w) {
+        if (w < warp) before += red[w];
+        all += red[w];
+    }
+    __syncthreads();
+    *total = all;
+    return before + inc - v;
+}
+
+__device__ void block_bitonic_u64(uint64_t* buf, uint32_t N) {
+    for (uint32_t k = 2; k <= N; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
+                const uint32_t ixj = i ^ j;
+                if (ixj > i) {
+                    const uint64_t a = buf[i], b = buf[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) { buf[i] = b; buf[ixj] = a; }
+                }
+            }
+            __syncthreads();
+        }
+}
+
+__global__ void __launch_bounds__(kLargeThreads)
+k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* __restrict__ plan,
+              const uint32_t* __restrict__ attr_local, ClassRec* __restrict__ rec,
+              double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
+              uint32_t* __restrict__ ux, uint32_t* __restrict__ un, uint32_t* __restrict__ ucursor,
+              uint64_t* __restrict__ gkeys, uint32_t* __restrict__ grows) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    __shared__ uint64_t red64[kLargeThreads / 32];
+    __shared__ uint32_t red32[kLargeThreads / 32];
+    __shared__ uint32_t s_nk, s_ubase;
+    const uint32_t c = large_list[blockIdx.x];
+    const LargePlan pl = plan[blockIdx.x];
+    uint64_t* keys = pl.keys_in_smem ? reinterpret_cast<uint64_t*>(dsm) : gkeys + pl.keys_off;
+    uint32_t* rows = pl.rows_in_smem
+                         ? reinterpret_cast<uint32_t*>(dsm + (pl.keys_in_smem ? 8ull * pl.keys_cap : 0))
+                         : grows + pl.rows_off;
+    const uint32_t mb = s.cls_moff[c];
+    const uint32_t M = s.cls_moff[c + 1] - mb;
+    const uint32_t A = s.cls_aoff[c + 1] - s.cls_aoff[c];
+    const uint32_t W = (M + 31) / 32;
+    const uint64_t nrow_words = (uint64_t)A * W;
+    if (threadIdx.x == 0) s_nk = 0;
+    for (uint64_t i = threadIdx.x; i < nrow_words; i += blockDim.x) rows[i] = 0;
+    __syncthreads();
+
+    // phase 1: foreign (X, member) keys, own-attribute bits, H
+    uint64_t hown = 0;
+    for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) {
+        const uint32_t p = s.cls_methods[mb + i];
+        const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
+        for (uint32_t e = cb; e < ce; ++e) {
+            const uint32_t o = __ldg(s.method_owner + __ldg(s.call_tgt + e));
+            if (o != c) keys[atomicAdd(&s_nk, 1u)] = ((uint64_t)o << 32) | i;
+        }
+        const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+        for (uint32_t e = ab; e < ae; ++e) {
+            const uint32_t t = __ldg(s.acc_tgt + e);
+            const uint32_t o = __ldg(s.attribute_owner + t);
+            if (o != c) {
+                keys[atomicAdd(&s_nk, 1u)] = ((uint64_t)o << 32) | i;
+            } else {
+                const uint32_t a = __ldg(attr_local + t);
+                atomicOr(rows + (uint64_t)a * W + (i >> 5), 1u << (i & 31));
+                ++hown;
+            }
+        }
+    }
+    const uint64_t H = block_sum_u64(hown, red64);  // includes a __syncthreads
+    const uint32_t nk = s_nk;
+    uint32_t N = 1;
+    while (N < nk) N <<= 1;
+    for (uint32_t i = nk + threadIdx.x; i < N; i += blockDim.x) keys[i] = ~0ull;
+    __syncthreads();
+    if (N > 1) block_bitonic_u64(keys, N);
+
+    // phase 2: distinct X (cbo) and per-X distinct members (U counts)
+    uint32_t nx = 0;
+    for (uint32_t b = 0; b < nk; b += blockDim.x) {
+        const uint32_t k = b + threadIdx.x;
+        const bool xh = k < nk && (k == 0 || (keys[k] >> 32) != (keys[k - 1] >> 32));
+        uint32_t tot;
+        block_excl_scan(xh ? 1u : 0u, red32, &tot);
+        nx += tot;
+    }
+    if (threadIdx.x == 0) s_ubase = nx ? atomicAdd(ucursor, nx) : 0u;
+    __syncthreads();
+    const uint32_t ubase = s_ubase;
+    uint32_t xcarry = 0;
+    for (uint32_t b = 0; b < nk; b += blockDim.x) {
+        const uint32_t k = b + threadIdx.x;
+        const bool xh = k < nk && (k == 0 || (keys[k] >> 32) != (keys[k - 1] >> 32));
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(xh ? 1u : 0u, red32, &tot);
+        if (xh) {
+            ux[ubase + xcarry + ex] = (uint32_t)(keys[k] >> 32);
+            un[ubase + xcarry + ex] = 0;
+        }
+        xcarry += tot;
+    }
+    __syncthreads();
+    xcarry = 0;
+    for (uint32_t b = 0; b < nk; b += blockDim.x) {
+        const uint32_t k = b + threadIdx.x;
+        const bool xh = k < nk && (k == 0 || (keys[k] >> 32) != (keys[k - 1] >> 32));
+        const bool ph = k < nk && (k == 0 || keys[k] != keys[k - 1]);
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(xh ? 1u : 0u, red32, &tot);
+        // run index of position k = (#X heads at or before k) - 1
+        if (ph) atomicAdd(un + ubase + xcarry + ex + (xh ? 1u : 0u) - 1u, 1u);
+        xcarry += tot;
+    }
+
+    // phase 3: LCOM-CK via per-attribute member bitmaps (rows[a] = methods using a)
+    uint64_t q = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t i = warp; i < M; i += kLargeThreads / 32) {
+        const uint32_t p = s.cls_methods[mb + i];
+        const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+        for (uint32_t wb = 0; wb < W; wb += 32) {
+            const uint32_t w = wb + lane;
+            uint32_t acc = 0;
+            if (w < W && w >= (i >> 5)) {
+                for (uint32_t e = ab; e < ae; ++e) {
+                    const uint32_t t = __ldg(s.acc_tgt + e);
+                    if (__ldg(s.attribute_owner + t) == c) acc |= rows[(uint64_t)__ldg(attr_local + t) * W + w];
+                }
+                if (w == (i >> 5)) acc &= ((i & 31) == 31) ? 0u : (~0u << ((i & 31) + 1));
+            }
+            q += __popc(acc);
+        }
+    }
+    const uint64_t Q = block_sum_u64(q, red64);
+    if (threadIdx.x == 0) {
+        const double l = lcom_of(A, M, H);
+        const uint64_t pairs = (uint64_t)M * (M - 1) / 2;
+        const uint64_t P = pairs - Q;
+        ClassRec r;
+        r.A = A; r.M = M; r.H = (uint32_t)H; r.cbo = nx; r.ubase = ubase; r.pad = 0; r.lcom = l;
+        rec[c] = r;
+        lcom_out[c] = l;
+        ck_out[c] = P > Q ? P - Q : 0;
+        cbo_out[c] = nx;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// threshold means (compute_thresholds, suggest.hpp:46-61)
+// ---------------------------------------------------------------------------
+
+// Serial reference semantics: one thread, class order, round-to-nearest adds.
+__global__ void k_thresholds_serial(const double* __restrict__ lcom, const uint32_t* __restrict__ cbo,
+                                    uint32_t n, DevThresholds* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double sl = 0.0;
+    uint64_t sc = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        sl = __dadd_rn(sl, lcom[i]);
+        sc += cbo[i];  // exact; (double)Σ == the reference's double sum while Σ < 2^53
+    }
+    out->lcom = n ? __ddiv_rn(sl, (double)n) : 0.0;
+    out->cbo = n ? __ddiv_rn((double)sc, (double)n) : 0.0;
+    out->fast_path_ok = 0;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t* bad, cudaStream_t st) {
+    if (!n) return;
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+    k_validate_ids<<<blocks, 256, 0, st>>>(v, n, bound, bad);
+}
+void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st) {
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((n1 + 255) / 256, 148 * 16);
+    k_validate_offsets<<<blocks, 256, 0, st>>>(off, n1, total, bad);
+}
+void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list, uint32_t* n_large,
+                         uint32_t* max_deg, uint32_t* foreign, cudaStream_t st) {
+    if (!s.C) return;
+    k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, kind, large_list, n_large, max_deg, foreign);
+}
+void launch_attr_local(const DevModel& s, uint32_t* attr_local, cudaStream_t st) {
+    if (!s.A) return;
+    const uint32_t blocks = std::min<uint32_t>((s.A + 255) / 256, 148 * 16);
+    k_attr_local<<<blocks, 256, 0, st>>>(s, attr_local);
+}
+void launch_class_small(const DevModel& s, const uint8_t* kind, const uint32_t* attr_local, ClassRec* rec,
+                        double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,
+                        uint32_t* ucursor, cudaStream_t st) {
+    if (!s.C) return;
+    k_class_small<<<(s.C + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(
+        s, kind, attr_local, rec, lcom, ck, cbo, ux, un, ucursor);
+}
+void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
+                        uint32_t smem_bytes, const uint32_t* attr_local, ClassRec* rec, double* lcom,
+                        uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
+                        uint64_t* gkeys, uint32_t* grows, cudaStream_t st) {
+    if (!n_large) return;
+    k_class_large<<<n_large, kLargeThreads, smem_bytes, st>>>(s, large_list, plan, attr_local, rec, lcom, ck,
+                                                              cbo, ux, un, ucursor, gkeys, grows);
+}
+cudaError_t set_class_large_smem(uint32_t bytes) {
+    return cudaFuncSetAttribute(k_class_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+void launch_thresholds_serial(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
+                              cudaStream_t st) {
+    k_thresholds_serial<<<1, 32, 0, st>>>(lcom, cbo, n, out);
+}
+
+}  // namespace mmg

@@ -1,0 +1,610 @@
+// mm_api.cu — the C ABI (include/mmgpu.h): context, upload, metric pass,
+// thresholds, what-if, sweep. Host orchestration only; all arithmetic on the
+// hot path runs in the kernels of k_metrics.cu / k_sweep.cu. There is no CPU
+// fallback: without a usable CUDA device every compute entry point fails
+// with MM_E_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstddef>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/mmgpu.h"
+#include "mm_device.cuh"
+#include "mm_kernels.h"
+
+using namespace mmg;
+
+namespace {
+
+struct Ctl {  // small device-resident control block
+    uint32_t bad;
+    uint32_t n_large;
+    uint32_t max_deg;
+    uint32_t ucursor;
+    uint32_t tile_counter;
+    uint32_t err;
+    uint32_t pad[2];
+    unsigned long long stats[4];
+    DevThresholds thr;
+};
+
+struct KStat {
+    uint64_t launches = 0;
+    double total_ms = 0.0;
+};
+
+struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+};
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t alloc(size_t count) {
+        release();
+        n = count;
+        if (count == 0) return cudaSuccess;
+        return cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T));
+    }
+    cudaError_t ensure(size_t count) { return count <= n && p ? cudaSuccess : alloc(count); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+}  // namespace
+
+struct mm_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    bool profiling = false;
+    std::vector<Pending> pending;
+    std::map<std::string, KStat> kstats;
+
+    // model
+    bool have_model = false;
+    bool metrics_valid = false;
+    uint32_t C = 0, M = 0, A = 0;
+    uint64_t Ec = 0, Ea = 0;
+    std::vector<uint32_t> h_method_owner, h_cls_moff;
+    DBuf<uint32_t> method_owner, attribute_owner, cls_moff, cls_methods, cls_aoff, cls_attrs, call_off, call_tgt,
+        acc_off, acc_tgt;
+    // plan
+    uint32_t n_large = 0, max_deg = 0, large_smem = 0;
+    DBuf<uint8_t> kind;
+    DBuf<uint32_t> large_list, foreign;
+    DBuf<LargePlan> plans;
+    DBuf<uint64_t> gkeys;
+    DBuf<uint32_t> grows;
+    // derived
+    DBuf<uint32_t> attr_local, cbo, ux, un;
+    DBuf<ClassRec> rec;
+    DBuf<double> lcom;
+    DBuf<uint64_t> ck;
+    // control / sweep
+    DBuf<Ctl> ctl;
+    DBuf<unsigned long long> tile_state;
+    DBuf<mm_suggestion> out;
+    DBuf<mm_whatif> whatif;
+    bool sweep_valid = false;
+
+    DevModel dev() const {
+        DevModel s;
+        s.C = C; s.M = M; s.A = A;
+        s.method_owner = method_owner.p; s.attribute_owner = attribute_owner.p;
+        s.cls_moff = cls_moff.p; s.cls_methods = cls_methods.p;
+        s.cls_aoff = cls_aoff.p; s.cls_attrs = cls_attrs.p;
+        s.call_off = call_off.p; s.call_tgt = call_tgt.p;
+        s.acc_off = acc_off.p; s.acc_tgt = acc_tgt.p;
+        return s;
+    }
+};
+
+namespace {
+
+mm_status fail(mm_ctx* ctx, mm_status st, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return st;
+}
+
+mm_status cuda_fail(mm_ctx* ctx, cudaError_t e, const char* where) {
+    return fail(ctx, e == cudaErrorMemoryAllocation ? MM_E_OOM : MM_E_CUDA,
+                std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define MM_CUDA(ctx, call)                                   \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+template <class F>
+mm_status run(mm_ctx* ctx, const char* name, F&& launch) {
+    Pending pe;
+    if (ctx->profiling) {
+        cudaEventCreate(&pe.a);
+        cudaEventCreate(&pe.b);
+        cudaEventRecord(pe.a, ctx->stream);
+    }
+    launch();
+    const cudaError_t e = cudaGetLastError();
+    if (ctx->profiling) {
+        cudaEventRecord(pe.b, ctx->stream);
+        pe.name = name;
+        ctx->pending.push_back(pe);
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, name);
+    return MM_OK;
+}
+
+void resolve_pending(mm_ctx* ctx) {
+    for (Pending& p : ctx->pending) {
+        cudaEventSynchronize(p.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        KStat& k = ctx->kstats[p.name];
+        ++k.launches;
+        k.total_ms += ms;
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    ctx->pending.clear();
+}
+
+void free_model(mm_ctx* c) {
+    for (DBuf<uint32_t>* b : {&c->method_owner, &c->attribute_owner, &c->cls_moff, &c->cls_methods, &c->cls_aoff,
+                              &c->cls_attrs, &c->call_off, &c->call_tgt, &c->acc_off, &c->acc_tgt,
+                              &c->large_list, &c->foreign, &c->grows, &c->attr_local, &c->cbo, &c->ux, &c->un})
+        b->release();
+    c->kind.release();
+    c->plans.release();
+    c->gkeys.release();
+    c->rec.release();
+    c->lcom.release();
+    c->ck.release();
+    c->have_model = c->metrics_valid = c->sweep_valid = false;
+}
+
+mm_status set_device(mm_ctx* ctx) {
+    MM_CUDA(ctx, cudaSetDevice(ctx->device));
+    return MM_OK;
+}
+
+template <class T>
+mm_status upload_array(mm_ctx* ctx, DBuf<T>& d, const T* h, size_t n, const char* what) {
+    if (n && !h) return fail(ctx, MM_E_ARG, std::string("mm_upload: NULL ") + what);
+    MM_CUDA(ctx, d.alloc(n));
+    if (n) MM_CUDA(ctx, cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    return MM_OK;
+}
+
+uint32_t next_pow2(uint32_t v) {
+    uint32_t n = 1;
+    while (n < v) n <<= 1;
+    return n;
+}
+
+mm_status ensure_metrics(mm_ctx* ctx) {
+    if (!ctx->have_model) return fail(ctx, MM_E_STATE, "no model uploaded");
+    if (mm_status st = set_device(ctx)) return st;
+    if (!ctx->metrics_valid) return mm_compute_metrics(ctx);
+    return MM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mm_abi_version(void) { return MMGPU_ABI_VERSION; }
+
+const char* mm_last_error(const mm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+mm_status mm_ctx_create(int device, mm_ctx** out) {
+    if (!out) return MM_E_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return MM_E_CUDA;
+    if (device < 0 || device >= n) return MM_E_RANGE;
+    mm_ctx* ctx = new (std::nothrow) mm_ctx();
+    if (!ctx) return MM_E_OOM;
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess ||
+        ctx->ctl.alloc(1) != cudaSuccess || ctx->whatif.alloc(1) != cudaSuccess) {
+        delete ctx;
+        return MM_E_CUDA;
+    }
+    ctx->stream = ctx->own;
+    *out = ctx;
+    return MM_OK;
+}
+
+void mm_ctx_destroy(mm_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    resolve_pending(ctx);
+    free_model(ctx);
+    ctx->ctl.release();
+    ctx->whatif.release();
+    ctx->tile_state.release();
+    ctx->out.release();
+    if (ctx->own) cudaStreamDestroy(ctx->own);
+    delete ctx;
+}
+
+mm_status mm_ctx_set_stream(mm_ctx* ctx, void* s) {
+    if (!ctx) return MM_E_ARG;
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+    return MM_OK;
+}
+
+mm_status mm_ctx_synchronize(mm_ctx* ctx) {
+    if (!ctx) return MM_E_ARG;
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+mm_status mm_ctx_set_profiling(mm_ctx* ctx, int on) {
+    if (!ctx) return MM_E_ARG;
+    ctx->profiling = on != 0;
+    return MM_OK;
+}
+
+mm_status mm_kernel_stats(mm_ctx* ctx, mm_kernel_stat* out, int cap, int* n_out) {
+    if (!ctx || !n_out) return MM_E_ARG;
+    resolve_pending(ctx);
+    int i = 0;
+    for (const auto& kv : ctx->kstats) {
+        if (out && i < cap) {
+            std::memset(&out[i], 0, sizeof out[i]);
+            std::strncpy(out[i].name, kv.first.c_str(), sizeof(out[i].name) - 1);
+            out[i].launches = kv.second.launches;
+            out[i].total_ms = kv.second.total_ms;
+        }
+        ++i;
+    }
+    *n_out = i;
+    return (out && cap < i) ? MM_E_CAPACITY : MM_OK;
+}
+
+mm_status mm_reset_kernel_stats(mm_ctx* ctx) {
+    if (!ctx) return MM_E_ARG;
+    resolve_pending(ctx);
+    ctx->kstats.clear();
+    return MM_OK;
+}
+
+uint64_t mm_system_bytes(const mm_system* s) {
+    if (!s) return 0;
+    const uint64_t Ec = s->call_off ? s->call_off[s->n_methods] : 0;
+    const uint64_t Ea = s->acc_off ? s->acc_off[s->n_methods] : 0;
+    return 4ull * (2ull * s->n_methods + 2ull * s->n_attributes + 2ull * (s->n_classes + 1) +
+                   2ull * (s->n_methods + 1) + Ec + Ea);
+}
+
+mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
+    if (!ctx || !s) return MM_E_ARG;
+    if (mm_status st = set_device(ctx)) return st;
+    free_model(ctx);
+    if (!s->call_off || !s->acc_off || !s->class_method_off || !s->class_attr_off)
+        return fail(ctx, MM_E_ARG, "mm_upload: NULL offsets");
+    const uint32_t C = s->n_classes, M = s->n_methods, A = s->n_attributes;
+    const uint64_t Ec = s->call_off[M], Ea = s->acc_off[M];
+    ctx->C = C; ctx->M = M; ctx->A = A; ctx->Ec = Ec; ctx->Ea = Ea;
+    if (mm_status st = upload_array(ctx, ctx->method_owner, s->method_owner, M, "method_owner")) return st;
+    if (mm_status st = upload_array(ctx, ctx->attribute_owner, s->attribute_owner, A, "attribute_owner")) return st;
+    if (mm_status st = upload_array(ctx, ctx->cls_moff, s->class_method_off, C + 1ull, "class_method_off")) return st;
+    if (mm_status st = upload_array(ctx, ctx->cls_methods, s->class_methods, M, "class_methods")) return st;
+    if (mm_status st = upload_array(ctx, ctx->cls_aoff, s->class_attr_off, C + 1ull, "class_attr_off")) return st;
+    if (mm_status st = upload_array(ctx, ctx->cls_attrs, s->class_attrs, A, "class_attrs")) return st;
+    if (mm_status st = upload_array(ctx, ctx->call_off, s->call_off, M + 1ull, "call_off")) return st;
+    if (mm_status st = upload_array(ctx, ctx->call_tgt, s->call_tgt, Ec, "call_tgt")) return st;
+    if (mm_status st = upload_array(ctx, ctx->acc_off, s->acc_off, M + 1ull, "acc_off")) return st;
+    if (mm_status st = upload_array(ctx, ctx->acc_tgt, s->acc_tgt, Ea, "acc_tgt")) return st;
+    ctx->h_method_owner.assign(s->method_owner, s->method_owner + M);
+    ctx->h_cls_moff.assign(s->class_method_off, s->class_method_off + C + 1);
+
+    // device-side range validation: offsets first (totals come from the
+    // host arrays), then every id against its id space
+    Ctl* ctl = ctx->ctl.p;
+    MM_CUDA(ctx, cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx->stream));
+    uint32_t* bad = &ctl->bad;
+    mm_status st = run(ctx, "validate", [&] {
+        launch_validate_offsets(ctx->cls_moff.p, C + 1ull, M, bad, ctx->stream);
+        launch_validate_offsets(ctx->cls_aoff.p, C + 1ull, A, bad, ctx->stream);
+        launch_validate_offsets(ctx->call_off.p, M + 1ull, (uint32_t)Ec, bad, ctx->stream);
+        launch_validate_offsets(ctx->acc_off.p, M + 1ull, (uint32_t)Ea, bad, ctx->stream);
+        launch_validate_ids(ctx->method_owner.p, M, C, bad, ctx->stream);
+        launch_validate_ids(ctx->attribute_owner.p, A, C, bad, ctx->stream);
+        launch_validate_ids(ctx->cls_methods.p, M, M, bad, ctx->stream);
+        launch_validate_ids(ctx->cls_attrs.p, A, A, bad, ctx->stream);
+        launch_validate_ids(ctx->call_tgt.p, Ec, M, bad, ctx->stream);
+        launch_validate_ids(ctx->acc_tgt.p, Ea, A, bad, ctx->stream);
+    });
+    if (st) return st;
+    Ctl h{};
+    MM_CUDA(ctx, cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h.bad) {
+        free_model(ctx);
+        return fail(ctx, MM_E_ARG, (h.bad & 2u) ? "mm_upload: malformed offsets" : "mm_upload: id out of range");
+    }
+
+    // class plan: warp path vs CTA path, scratch for the CTA path
+    MM_CUDA(ctx, ctx->kind.alloc(C ? C : 1));
+    MM_CUDA(ctx, ctx->large_list.alloc(C ? C : 1));
+    MM_CUDA(ctx, ctx->foreign.alloc(C ? C : 1));
+    const DevModel dm = ctx->dev();
+    st = run(ctx, "plan", [&] {
+        launch_plan_classes(dm, ctx->kind.p, ctx->large_list.p, &ctl->n_large, &ctl->max_deg, ctx->foreign.p,
+                            ctx->stream);
+    });
+    if (st) return st;
+    MM_CUDA(ctx, cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->n_large = h.n_large;
+    ctx->max_deg = h.max_deg;
+    if (ctx->n_large) {
+        std::vector<uint32_t> list(ctx->n_large), fr(C);
+        MM_CUDA(ctx, cudaMemcpy(list.data(), ctx->large_list.p, 4ull * ctx->n_large, cudaMemcpyDeviceToHost));
+        MM_CUDA(ctx, cudaMemcpy(fr.data(), ctx->foreign.p, 4ull * C, cudaMemcpyDeviceToHost));
+        std::sort(list.begin(), list.end());
+        int dev_smem = 0;
+        cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+        const uint64_t budget = std::min<uint64_t>(dev_smem > 0 ? (uint64_t)dev_smem - 4096 : 48 * 1024, 160 * 1024);
+        std::vector<LargePlan> plans(ctx->n_large);
+        uint64_t koff = 0, roff = 0, smem_need = 0;
+        for (uint32_t i = 0; i < ctx->n_large; ++i) {
+            const uint32_t c = list[i];
+            const uint32_t Mc = s->class_method_off[c + 1] - s->class_method_off[c];
+            const uint32_t Ac = s->class_attr_off[c + 1] - s->class_attr_off[c];
+            LargePlan& pl = plans[i];
+            std::memset(&pl, 0, sizeof pl);
+            pl.keys_cap = next_pow2(std::max<uint32_t>(fr[c], 1));
+            const uint64_t kbytes = 8ull * pl.keys_cap;
+            const uint64_t rbytes = 4ull * Ac * ((Mc + 31) / 32);
+            uint64_t used = 0;
+            if (kbytes <= budget) { pl.keys_in_smem = 1; used = kbytes; }
+            else { pl.keys_off = koff; koff += pl.keys_cap; }
+            if (used + rbytes <= budget) { pl.rows_in_smem = 1; used += rbytes; }
+            else { pl.rows_off = roff; roff += Ac * ((Mc + 31) / 32); }
+            smem_need = std::max(smem_need, used);
+        }
+        MM_CUDA(ctx, ctx->large_list.alloc(ctx->n_large));
+        MM_CUDA(ctx, cudaMemcpy(ctx->large_list.p, list.data(), 4ull * ctx->n_large, cudaMemcpyHostToDevice));
+        MM_CUDA(ctx, ctx->plans.alloc(ctx->n_large));
+        MM_CUDA(ctx, cudaMemcpy(ctx->plans.p, plans.data(), sizeof(LargePlan) * ctx->n_large,
+                                cudaMemcpyHostToDevice));
+        MM_CUDA(ctx, ctx->gkeys.alloc(koff ? koff : 1));
+        MM_CUDA(ctx, ctx->grows.alloc(roff ? roff : 1));
+        ctx->large_smem = (uint32_t)((smem_need + 15) & ~15ull);
+        MM_CUDA(ctx, set_class_large_smem(ctx->large_smem));
+    }
+    // derived tables
+    MM_CUDA(ctx, ctx->attr_local.alloc(A ? A : 1));
+    MM_CUDA(ctx, ctx->rec.alloc(C ? C : 1));
+    MM_CUDA(ctx, ctx->lcom.alloc(C ? C : 1));
+    MM_CUDA(ctx, ctx->ck.alloc(C ? C : 1));
+    MM_CUDA(ctx, ctx->cbo.alloc(C ? C : 1));
+    MM_CUDA(ctx, ctx->ux.alloc(Ec + Ea + 1));
+    MM_CUDA(ctx, ctx->un.alloc(Ec + Ea + 1));
+    ctx->have_model = true;
+    ctx->metrics_valid = false;
+    ctx->sweep_valid = false;
+    return MM_OK;
+}
+
+mm_status mm_compute_metrics(mm_ctx* ctx) {
+    if (!ctx) return MM_E_ARG;
+    if (!ctx->have_model) return fail(ctx, MM_E_STATE, "mm_compute_metrics: no model uploaded");
+    if (mm_status st = set_device(ctx)) return st;
+    Ctl* ctl = ctx->ctl.p;
+    MM_CUDA(ctx, cudaMemsetAsync(&ctl->ucursor, 0, sizeof(uint32_t), ctx->stream));
+    const DevModel dm = ctx->dev();
+    mm_status st = run(ctx, "attr_local", [&] { launch_attr_local(dm, ctx->attr_local.p, ctx->stream); });
+    if (st) return st;
+    st = run(ctx, "class_small", [&] {
+        launch_class_small(dm, ctx->kind.p, ctx->attr_local.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p,
+                           ctx->ux.p, ctx->un.p, &ctl->ucursor, ctx->stream);
+    });
+    if (st) return st;
+    if (ctx->n_large) {
+        st = run(ctx, "class_large", [&] {
+            launch_class_large(dm, ctx->n_large, ctx->large_list.p, ctx->plans.p, ctx->large_smem,
+                               ctx->attr_local.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
+                               ctx->un.p, &ctl->ucursor, ctx->gkeys.p, ctx->grows.p, ctx->stream);
+        });
+        if (st) return st;
+    }
+    st = run(ctx, "thresholds", [&] {
+        launch_thresholds_serial(ctx->lcom.p, ctx->cbo.p, ctx->C, &ctl->thr, ctx->stream);
+    });
+    if (st) return st;
+    ctx->metrics_valid = true;
+    ctx->sweep_valid = false;
+    return MM_OK;
+}
+
+
+mm_status mm_class_metrics(mm_ctx* ctx, double* lcom, uint64_t* lcom_ck, uint32_t* cbo) {
+    if (!ctx) return MM_E_ARG;
+    if (mm_status st = ensure_metrics(ctx)) return st;
+    const size_t C = ctx->C;
+    if (C && lcom) MM_CUDA(ctx, cudaMemcpyAsync(lcom, ctx->lcom.p, 8 * C, cudaMemcpyDeviceToHost, ctx->stream));
+    if (C && lcom_ck) MM_CUDA(ctx, cudaMemcpyAsync(lcom_ck, ctx->ck.p, 8 * C, cudaMemcpyDeviceToHost, ctx->stream));
+    if (C && cbo) MM_CUDA(ctx, cudaMemcpyAsync(cbo, ctx->cbo.p, 4 * C, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+static mm_status single(mm_ctx* ctx, uint32_t cls, void* dst, const void* src, size_t sz) {
+    if (!ctx || !dst) return MM_E_ARG;
+    if (mm_status st = ensure_metrics(ctx)) return st;
+    if (cls >= ctx->C) return fail(ctx, MM_E_RANGE, "unknown class id " + std::to_string(cls));  // metrics.hpp:97-100
+    MM_CUDA(ctx, cudaMemcpyAsync(dst, static_cast<const char*>(src) + sz * cls, sz, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+mm_status mm_lcom_normalized(mm_ctx* ctx, uint32_t cls, double* out) {
+    return single(ctx, cls, out, ctx ? ctx->lcom.p : nullptr, 8);
+}
+mm_status mm_lcom_ck(mm_ctx* ctx, uint32_t cls, uint64_t* out) {
+    return single(ctx, cls, out, ctx ? ctx->ck.p : nullptr, 8);
+}
+mm_status mm_cbo(mm_ctx* ctx, uint32_t cls, uint32_t* out) {
+    return single(ctx, cls, out, ctx ? ctx->cbo.p : nullptr, 4);
+}
+
+mm_status mm_compute_thresholds(mm_ctx* ctx, const mm_overrides* ov, mm_thresholds* out) {
+    if (!ctx || !out) return MM_E_ARG;
+    if (mm_status st = ensure_metrics(ctx)) return st;
+    DevThresholds t{};
+    MM_CUDA(ctx, cudaMemcpyAsync(&t, &ctx->ctl.p->thr, sizeof t, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memset(out, 0, sizeof *out);
+    out->similarity = (ov && ov->has_similarity) ? ov->similarity : 0.0;
+    out->lcom = (ov && ov->has_lcom) ? ov->lcom : t.lcom;
+    out->cbo = (ov && ov->has_cbo) ? ov->cbo : t.cbo;
+    out->explicit_mode = (uint8_t)(ov && (ov->has_similarity || ov->has_lcom || ov->has_cbo));
+    return MM_OK;
+}
+
+mm_status mm_what_if(mm_ctx* ctx, uint32_t method, uint32_t origin, uint32_t destination, mm_whatif* out) {
+    if (!ctx || !out) return MM_E_ARG;
+    if (!ctx->have_model) return fail(ctx, MM_E_STATE, "mm_what_if: no model uploaded");
+    // error order of what_if_move, suggest.hpp:89-96
+    if (origin >= ctx->C || destination >= ctx->C) return fail(ctx, MM_E_RANGE, "what_if_move: unknown class id");
+    if (origin == destination) return fail(ctx, MM_E_ARG, "what_if_move: origin and destination coincide");
+    if (method >= ctx->M || ctx->h_method_owner[method] != origin)
+        return fail(ctx, MM_E_ARG, "what_if_move: method " + std::to_string(method) +
+                                       " is not a member of class " + std::to_string(origin));
+    if (mm_status st = ensure_metrics(ctx)) return st;
+    const DevModel dm = ctx->dev();
+    mm_status st = run(ctx, "what_if", [&] {
+        launch_what_if(dm, ctx->rec.p, ctx->ux.p, ctx->un.p, method, origin, destination, ctx->whatif.p,
+                       ctx->stream);
+    });
+    if (st) return st;
+    MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->whatif.p, sizeof *out, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
+    if (!ctx || !p) return MM_E_ARG;
+    const uint32_t sel = p->criteria & (MM_CRIT_SIMILARITY | MM_CRIT_COHESION | MM_CRIT_COUPLING);
+    if (sel == 0) return fail(ctx, MM_E_ARG, "suggest_all: no criteria selected");  // suggest.hpp:313
+    if (sel & MM_CRIT_SIMILARITY)
+        return fail(ctx, MM_E_UNSUPPORTED, "Criterion::Similarity is outside this engine (needs the O(m^2) table)");
+    if (p->combine > MM_COMBINE_INTERSECTION) return fail(ctx, MM_E_ARG, "mm_sweep: bad combine");
+    if (!p->all_candidates && p->top_k > 8) return fail(ctx, MM_E_UNSUPPORTED, "mm_sweep: top_k > 8");
+    if (mm_status st = ensure_metrics(ctx)) return st;
+    const uint32_t cb = p->class_begin, ce = p->class_end ? p->class_end : ctx->C;
+    if (cb > ce || ce > ctx->C) return fail(ctx, MM_E_RANGE, "mm_sweep: class range outside the model");
+    const uint32_t pb = ctx->h_cls_moff[cb], pe = ctx->h_cls_moff[ce];
+    const uint64_t npos = pe - pb;
+    const uint32_t mode = p->all_candidates ? 2u : (p->top_k > 1 ? 1u : 0u);
+    const uint64_t per = mode == 0 ? 2ull : (mode == 1 ? 2ull * p->top_k : ~0ull);
+    const uint64_t Etot = ctx->Ec + ctx->Ea;
+    const uint64_t cap = std::max<uint64_t>(1, mode == 2 ? Etot : std::min(per * npos, Etot));
+    MM_CUDA(ctx, ctx->out.ensure(cap));
+    const uint32_t n_tiles = (uint32_t)((npos + kSweepTile - 1) / kSweepTile);
+    MM_CUDA(ctx, ctx->tile_state.ensure(n_tiles ? n_tiles : 1));
+    Ctl* ctl = ctx->ctl.p;
+    if (n_tiles) MM_CUDA(ctx, cudaMemsetAsync(ctx->tile_state.p, 0, 8ull * n_tiles, ctx->stream));
+    // tile_counter, err, pad, stats
+    MM_CUDA(ctx, cudaMemsetAsync(&ctl->tile_counter, 0, offsetof(Ctl, thr) - offsetof(Ctl, tile_counter),
+                                 ctx->stream));
+    SweepArgs a{};
+    a.s = ctx->dev();
+    a.rec = ctx->rec.p;
+    a.ux = ctx->ux.p;
+    a.un = ctx->un.p;
+    a.dthr = &ctl->thr;
+    a.thr_lcom = p->thr_lcom;
+    a.thr_cbo = p->thr_cbo;
+    a.thr_device = p->threshold_source == MM_THR_DEVICE_MEANS ? 1u : 0u;
+    a.crit = sel;
+    a.combine = p->combine;
+    a.mode = mode;
+    a.topk = mode == 1 ? p->top_k : 1u;
+    a.pos_begin = pb;
+    a.pos_end = pe;
+    a.maxdeg_fast = ctx->max_deg <= 8 ? 8u : 16u;  // higher degrees take the streaming path
+    a.out = ctx->out.p;
+    a.tile_state = ctx->tile_state.p;
+    a.tile_counter = &ctl->tile_counter;
+    a.stats = ctl->stats;
+    a.err = &ctl->err;
+    mm_status st = run(ctx, "sweep", [&] { launch_sweep(a, n_tiles, ctx->stream); });
+    if (st) return st;
+    ctx->sweep_valid = true;
+    if (n_out) {
+        mm_sweep_stats ss;
+        if (mm_status s2 = mm_sweep_stats_get(ctx, &ss)) return s2;
+        *n_out = ss.suggestions;
+    }
+    return MM_OK;
+}
+
+mm_status mm_sweep_stats_get(mm_ctx* ctx, mm_sweep_stats* out) {
+    if (!ctx || !out) return MM_E_ARG;
+    if (!ctx->sweep_valid) return fail(ctx, MM_E_STATE, "no sweep has run");
+    Ctl h{};
+    MM_CUDA(ctx, cudaMemcpyAsync(&h, ctx->ctl.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h.err & 2u)
+        return fail(ctx, MM_E_UNSUPPORTED, "a method uses more than 64 classes (all/top-k mode limit)");
+    out->candidates = h.stats[0];
+    out->gated_whatifs = h.stats[1];
+    out->suggestions = h.stats[2];
+    out->methods = h.stats[3];
+    return MM_OK;
+}
+
+mm_status mm_sweep_device_result(mm_ctx* ctx, const void** dev_records, uint64_t* n) {
+    if (!ctx || !dev_records) return MM_E_ARG;
+    if (!ctx->sweep_valid) return fail(ctx, MM_E_STATE, "no sweep has run");
+    *dev_records = ctx->out.p;
+    if (n) {
+        mm_sweep_stats ss;
+        if (mm_status st = mm_sweep_stats_get(ctx, &ss)) return st;
+        *n = ss.suggestions;
+    }
+    return MM_OK;
+}
+
+mm_status mm_copy_suggestions(mm_ctx* ctx, mm_suggestion* out, uint64_t cap, uint64_t* n_out) {
+    if (!ctx || !n_out) return MM_E_ARG;
+    mm_sweep_stats ss;
+    if (mm_status st = mm_sweep_stats_get(ctx, &ss)) return st;
+    *n_out = ss.suggestions;
+    if (!ss.suggestions) return MM_OK;
+    if (!out || cap < ss.suggestions) return fail(ctx, MM_E_CAPACITY, "output buffer too small");
+    MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->out.p, sizeof(mm_suggestion) * ss.suggestions, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+mm_status mm_suggest(mm_ctx* ctx, const mm_sweep_params* p, mm_suggestion* out, uint64_t cap, uint64_t* n_out) {
+    if (mm_status st = mm_sweep(ctx, p, nullptr)) return st;
+    return mm_copy_suggestions(ctx, out, cap, n_out);
+}
+
+}  // extern "C"

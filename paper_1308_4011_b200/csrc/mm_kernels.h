@@ -1,0 +1,62 @@
+// mm_kernels.h — host-visible launchers of the CUDA kernels (libmmgpu internals).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mm_device.cuh"
+
+namespace mmg {
+
+// Per large class (CTA path) scratch placement, planned on the host at upload.
+struct LargePlan {
+    uint64_t keys_off;   // u64 element offset into the global key scratch
+    uint64_t rows_off;   // u32 element offset into the global row scratch
+    uint32_t keys_cap;   // power of two ≥ foreign edge count
+    uint8_t keys_in_smem;
+    uint8_t rows_in_smem;
+    uint8_t pad[2];
+};
+
+struct SweepArgs {
+    DevModel s;
+    const ClassRec* rec;
+    const uint32_t* ux;
+    const uint32_t* un;
+    const DevThresholds* dthr;  // used when thr_device != 0
+    double thr_lcom, thr_cbo;
+    uint32_t thr_device;
+    uint32_t crit;       // MM_CRIT_COHESION | MM_CRIT_COUPLING subset
+    uint32_t combine;    // MM_COMBINE_*
+    uint32_t mode;       // 0 best-only, 1 top-k, 2 all candidates
+    uint32_t topk;       // mode 1: 2..8
+    uint32_t pos_begin, pos_end;  // class-ordered method positions
+    uint32_t maxdeg_fast;         // methods with degree ≤ this take the register path
+    mm_suggestion* out;
+    unsigned long long* tile_state;
+    uint32_t* tile_counter;
+    unsigned long long* stats;  // [candidates, gated, suggestions, methods]
+    uint32_t* err;              // bit 1: distinct-class overflow in all/top-k mode
+};
+
+void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t* bad, cudaStream_t st);
+void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st);
+void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list, uint32_t* n_large,
+                         uint32_t* max_deg, uint32_t* foreign, cudaStream_t st);
+void launch_attr_local(const DevModel& s, uint32_t* attr_local, cudaStream_t st);
+void launch_class_small(const DevModel& s, const uint8_t* kind, const uint32_t* attr_local, ClassRec* rec,
+                        double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,
+                        uint32_t* ucursor, cudaStream_t st);
+void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
+                        uint32_t smem_bytes, const uint32_t* attr_local, ClassRec* rec, double* lcom,
+                        uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
+                        uint64_t* gkeys, uint32_t* grows, cudaStream_t st);
+cudaError_t set_class_large_smem(uint32_t bytes);
+void launch_thresholds_serial(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
+                              cudaStream_t st);
+void launch_sweep(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
+constexpr uint32_t kSweepTile = 256;
+void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un,
+                    uint32_t u, uint32_t o, uint32_t d, mm_whatif* out, cudaStream_t st);
+
+}  // namespace mmg

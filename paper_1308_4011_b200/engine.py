@@ -1,0 +1,280 @@
+"""Python mirror of the reference's metric + suggestion API over libmmgpu.so.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/modmetrics/{metrics,parallel,suggest}.hpp:
+
+=====================================  ==========================================
+reference (C++)                        here
+=====================================  ==========================================
+parallel_class_metrics (parallel:149)  Engine.parallel_class_metrics / module fn
+parallel_lcom_ck (parallel:164)        Engine.parallel_lcom_ck / module fn
+lcom_normalized / lcom_ck / cbo        Engine.lcom_normalized / .lcom_ck_of / .cbo
+compute_thresholds (suggest:46)        Engine.compute_thresholds
+what_if_move (suggest:87)              Engine.what_if_move / module fn
+suggest_by_cohesion / _coupling        Engine.suggest_by_cohesion / _coupling
+suggest_all (suggest:303)              Engine.suggest_all / module fn
+=====================================  ==========================================
+
+std::out_of_range -> MMRangeError (an IndexError); std::invalid_argument ->
+MMArgError (a ValueError). Everything computes on the GPU; a missing library
+or device raises (no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+from . import abi
+from ._lib import MMArgError, check, lib
+from .system import System
+
+
+class Criterion(enum.IntEnum):  # suggest.hpp:17
+    Similarity = 0
+    Cohesion = 1
+    Coupling = 2
+
+
+class Combine(enum.IntEnum):  # suggest.hpp:296
+    Union = 0
+    Intersection = 1
+
+
+@dataclass(frozen=True)
+class Thresholds:  # suggest.hpp:35-41
+    similarity: float = 0.0
+    lcom: float = 0.0
+    cbo: float = 0.0
+    explicit_mode: bool = False
+
+
+@dataclass(frozen=True)
+class ThresholdOverrides:  # suggest.hpp:28-32
+    similarity: Optional[float] = None
+    lcom: Optional[float] = None
+    cbo: Optional[float] = None
+
+
+@dataclass(frozen=True)
+class ClassMetrics:  # parallel.hpp:139-144
+    lcom: np.ndarray
+    cbo: np.ndarray
+
+
+def criteria_mask(criteria: Iterable) -> int:
+    m = 0
+    for c in criteria:
+        m |= 1 << int(c)
+    return m
+
+
+def criteria_of_mask(mask: int) -> list:
+    return [c for c in Criterion if mask & (1 << int(c))]
+
+
+class Engine:
+    """One GPU context (`mm_ctx`) holding one uploaded system."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        self._ctx = C.c_void_p()
+        check(lib().mm_ctx_create(device, C.byref(self._ctx)), None, f"mm_ctx_create(device={device})")
+        if stream is not None:
+            self.set_stream(stream)
+        self.system: Optional[System] = None
+
+    # ---- context ------------------------------------------------------
+    def close(self) -> None:
+        if self._ctx:
+            lib().mm_ctx_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int, what: str) -> None:
+        check(st, self._ctx, what)
+
+    def set_stream(self, stream_handle: Optional[int]) -> None:
+        self._check(lib().mm_ctx_set_stream(self._ctx, C.c_void_p(stream_handle or 0)), "mm_ctx_set_stream")
+
+    def synchronize(self) -> None:
+        self._check(lib().mm_ctx_synchronize(self._ctx), "mm_ctx_synchronize")
+
+    def set_profiling(self, on: bool) -> None:
+        self._check(lib().mm_ctx_set_profiling(self._ctx, int(on)), "mm_ctx_set_profiling")
+
+    def kernel_stats(self) -> dict:
+        n = C.c_int()
+        lib().mm_kernel_stats(self._ctx, None, 0, C.byref(n))
+        arr = (abi.mm_kernel_stat * max(1, n.value))()
+        self._check(lib().mm_kernel_stats(self._ctx, arr, n.value, C.byref(n)), "mm_kernel_stats")
+        return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms)) for i in range(n.value)}
+
+    def reset_kernel_stats(self) -> None:
+        self._check(lib().mm_reset_kernel_stats(self._ctx), "mm_reset_kernel_stats")
+
+    # ---- model --------------------------------------------------------
+    def upload(self, system: System) -> "Engine":
+        s = system.as_c()
+        self._check(lib().mm_upload(self._ctx, C.byref(s)), "mm_upload")
+        self.system = system
+        return self
+
+    # ---- metric pass --------------------------------------------------
+    def compute_metrics(self) -> None:
+        self._check(lib().mm_compute_metrics(self._ctx), "mm_compute_metrics")
+
+    def class_metrics_all(self):
+        """(lcom f64[c], lcom_ck u64[c], cbo u32[c]) — full_report's class fields."""
+        n = self.system.n_classes
+        lcom = np.empty(n, np.float64)
+        ck = np.empty(n, np.uint64)
+        cbo = np.empty(n, np.uint32)
+        self._check(lib().mm_class_metrics(self._ctx, lcom.ctypes.data, ck.ctypes.data, cbo.ctypes.data),
+                    "mm_class_metrics")
+        return lcom, ck, cbo
+
+    def parallel_class_metrics(self, n_workers: int = 1) -> ClassMetrics:
+        if n_workers == 0:
+            raise MMArgError(abi.MM_E_ARG, "plan_partition: zero workers")  # parallel.hpp:29
+        lcom, _, cbo = self.class_metrics_all()
+        return ClassMetrics(lcom, cbo)
+
+    def parallel_lcom_ck(self, n_workers: int = 1) -> np.ndarray:
+        if n_workers == 0:
+            raise MMArgError(abi.MM_E_ARG, "plan_partition: zero workers")
+        return self.class_metrics_all()[1]
+
+    def lcom_normalized(self, cls: int) -> float:
+        v = C.c_double()
+        self._check(lib().mm_lcom_normalized(self._ctx, cls, C.byref(v)), "lcom_normalized")
+        return v.value
+
+    def lcom_ck_of(self, cls: int) -> int:
+        v = C.c_uint64()
+        self._check(lib().mm_lcom_ck(self._ctx, cls, C.byref(v)), "lcom_ck")
+        return v.value
+
+    def cbo(self, cls: int) -> int:
+        v = C.c_uint32()
+        self._check(lib().mm_cbo(self._ctx, cls, C.byref(v)), "cbo")
+        return v.value
+
+    # ---- thresholds ---------------------------------------------------
+    def compute_thresholds(self, overrides: Optional[ThresholdOverrides] = None) -> Thresholds:
+        ov = abi.mm_overrides()
+        if overrides is not None:
+            for name in ("similarity", "lcom", "cbo"):
+                v = getattr(overrides, name)
+                if v is not None:
+                    setattr(ov, "has_" + name, 1)
+                    setattr(ov, name, float(v))
+        t = abi.mm_thresholds()
+        self._check(lib().mm_compute_thresholds(self._ctx, C.byref(ov), C.byref(t)), "compute_thresholds")
+        return Thresholds(t.similarity, t.lcom, t.cbo, bool(t.explicit_mode))
+
+    # ---- what-if ------------------------------------------------------
+    def what_if_move(self, method: int, origin: int, destination: int) -> dict:
+        w = abi.mm_whatif()
+        self._check(lib().mm_what_if(self._ctx, method, origin, destination, C.byref(w)), "what_if_move")
+        return {f: (bool(getattr(w, f)) if f.endswith("degenerate_after") else getattr(w, f))
+                for f in abi.WHATIF_FIELDS}
+
+    # ---- sweep --------------------------------------------------------
+    def sweep(self, criteria=(Criterion.Cohesion, Criterion.Coupling), combine=Combine.Union,
+              thresholds: Optional[Thresholds] = None, all_candidates: bool = False, top_k: int = 1,
+              class_range: Optional[tuple] = None, want_count: bool = True) -> Optional[int]:
+        """Device-resident sweep. thresholds=None uses the device-computed means."""
+        p = abi.mm_sweep_params(criteria=criteria_mask(criteria), combine=int(combine),
+                                all_candidates=int(bool(all_candidates)), top_k=int(top_k))
+        if thresholds is None:
+            p.threshold_source = abi.MM_THR_DEVICE_MEANS
+        else:
+            p.threshold_source = abi.MM_THR_EXPLICIT
+            p.thr_lcom = float(thresholds.lcom)
+            p.thr_cbo = float(thresholds.cbo)
+        if class_range is not None:
+            p.class_begin, p.class_end = int(class_range[0]), int(class_range[1])
+        n = C.c_uint64()
+        self._check(lib().mm_sweep(self._ctx, C.byref(p), C.byref(n) if want_count else None), "mm_sweep")
+        return n.value if want_count else None
+
+    def sweep_stats(self) -> dict:
+        s = abi.mm_sweep_stats()
+        self._check(lib().mm_sweep_stats_get(self._ctx, C.byref(s)), "mm_sweep_stats_get")
+        return {"candidates": s.candidates, "gated_whatifs": s.gated_whatifs, "suggestions": s.suggestions,
+                "methods": s.methods}
+
+    def device_result(self):
+        """(device pointer, count) of the last sweep's mm_suggestion records."""
+        ptr = C.c_void_p()
+        n = C.c_uint64()
+        self._check(lib().mm_sweep_device_result(self._ctx, C.byref(ptr), C.byref(n)), "mm_sweep_device_result")
+        return ptr.value, n.value
+
+    def suggestions(self) -> np.ndarray:
+        n = C.c_uint64()
+        lib().mm_copy_suggestions(self._ctx, None, 0, C.byref(n))
+        out = np.zeros(n.value, dtype=abi.SUGGESTION_DTYPE)
+        if n.value:
+            self._check(lib().mm_copy_suggestions(self._ctx, out.ctypes.data, n.value, C.byref(n)),
+                        "mm_copy_suggestions")
+        return out
+
+    def suggest_all(self, thresholds: Thresholds, criteria: Sequence = (Criterion.Cohesion, Criterion.Coupling),
+                    combine: Combine = Combine.Union, all_candidates: bool = False, top_k: int = 1,
+                    class_range: Optional[tuple] = None) -> np.ndarray:
+        """suggest_all (suggest.hpp:303): ordered by (origin, method, destination)."""
+        self.sweep(criteria, combine, thresholds, all_candidates, top_k, class_range, want_count=False)
+        return self.suggestions()
+
+    def suggest_by_cohesion(self, thresholds: Thresholds, all_candidates: bool = False) -> np.ndarray:
+        """suggest_by_cohesion (suggest.hpp:239) — as a set; ordered (origin, method, dest)."""
+        return self.suggest_all(thresholds, [Criterion.Cohesion], Combine.Union, all_candidates)
+
+    def suggest_by_coupling(self, thresholds: Thresholds, all_candidates: bool = False) -> np.ndarray:
+        return self.suggest_all(thresholds, [Criterion.Coupling], Combine.Union, all_candidates)
+
+
+# ---- free functions with the reference's call shapes ---------------------
+
+def plan_shards(system: System, n_shards: int) -> np.ndarray:
+    """Cost-balanced contiguous class ranges (bounds, len n_shards + 1)."""
+    b = np.zeros(n_shards + 1, dtype=np.uint32)
+    s = system.as_c()
+    check(lib().mm_plan_shards(C.byref(s), n_shards, b.ctypes.data_as(abi.U32P)), None, "mm_plan_shards")
+    return b
+
+
+def parallel_class_metrics(system: System, n_workers: int = 1, device: int = 0) -> ClassMetrics:
+    with Engine(device) as e:
+        return e.upload(system).parallel_class_metrics(n_workers)
+
+
+def parallel_lcom_ck(system: System, n_workers: int = 1, device: int = 0) -> np.ndarray:
+    with Engine(device) as e:
+        return e.upload(system).parallel_lcom_ck(n_workers)
+
+
+def what_if_move(method: int, origin: int, destination: int, system: System, device: int = 0) -> dict:
+    with Engine(device) as e:
+        return e.upload(system).what_if_move(method, origin, destination)
+
+
+def suggest_all(system: System, thresholds: Thresholds, criteria: Sequence, combine: Combine = Combine.Union,
+                all_candidates: bool = False, device: int = 0) -> np.ndarray:
+    with Engine(device) as e:
+        return e.upload(system).suggest_all(thresholds, criteria, combine, all_candidates)

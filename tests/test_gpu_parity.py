@@ -1,0 +1,227 @@
+"""GPU parity: libmmgpu.so (sm_100a) against the reference's golden outputs and the oracle.
+
+Bar: bit-exact — lcom doubles compared as raw bits, every integer equal, the
+ordered suggestion list equal record by record (all 64 bytes but padding).
+All calls go through the C ABI (paper_1308_4011_b200.Engine is a ctypes shim).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import first_diff, golden_names, golden_records, golden_system, load_golden, records_equal, unhex
+from paper_1308_4011_b200 import Combine, Criterion, Engine, MMArgError, MMError, MMRangeError, System, Thresholds, abi
+
+pytestmark = pytest.mark.gpu
+
+COH, COUP = abi.MM_CRIT_COHESION, abi.MM_CRIT_COUPLING
+CRIT = {COH: [Criterion.Cohesion], COUP: [Criterion.Coupling], COH | COUP: [Criterion.Cohesion, Criterion.Coupling]}
+
+
+def gpu_metrics(e: Engine, s: System):
+    e.upload(s)
+    return e.class_metrics_all()
+
+
+def assert_metrics_equal(got, want, ctx=""):
+    gl, gk, gc = got
+    wl, wk, wc = want
+    assert gl.tobytes() == np.ascontiguousarray(wl, np.float64).tobytes(), f"lcom differs {ctx}"
+    assert np.array_equal(gk, np.asarray(wk, np.uint64)), f"lcom_ck differs {ctx}"
+    assert np.array_equal(gc, np.asarray(wc, np.uint32)), f"cbo differs {ctx}"
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_gpu_matches_reference_golden(gpu_engine, name):
+    case = load_golden(name)
+    s = golden_system(case)
+    got = gpu_metrics(gpu_engine, s)
+    assert_metrics_equal(got, ([unhex(h) for h in case["lcom"]], case["lcom_ck"], case["cbo"]), name)
+    t = gpu_engine.compute_thresholds()
+    assert t.lcom == unhex(case["thresholds_mean"]["lcom"]) and t.cbo == unhex(case["thresholds_mean"]["cbo"])
+    for run in case["suggest"]:
+        thr = Thresholds(0.0, unhex(run["thr_lcom"]), unhex(run["thr_cbo"]), run["thresholds"] == "explicit")
+        out = gpu_engine.suggest_all(thr, CRIT[run["criteria"]], Combine(run["combine"]), run["all_candidates"])
+        want = golden_records(run["suggestions"])
+        assert records_equal(out, want), (name, run["criteria"], run["combine"], first_diff(out, want))
+    for w in case.get("what_if", []):
+        if w["status"]:
+            exc = MMRangeError if w["status"] == abi.MM_E_RANGE else MMArgError
+            with pytest.raises(exc):
+                gpu_engine.what_if_move(w["u"], w["o"], w["d"])
+            continue
+        wm = gpu_engine.what_if_move(w["u"], w["o"], w["d"])
+        for f, v in w["w"].items():
+            assert (wm[f] == unhex(v)) if f.startswith("lcom") else (int(wm[f]) == v), (name, w, f)
+
+
+def test_device_threshold_source_equals_explicit(gpu_engine):
+    s = System.generate(seed=1, n_classes=1000, n_methods=10000, n_attributes=20000)
+    gpu_engine.upload(s)
+    t = gpu_engine.compute_thresholds()
+    a = gpu_engine.suggest_all(t)
+    gpu_engine.sweep(thresholds=None)
+    b = gpu_engine.suggestions()
+    assert records_equal(a, b) and len(a) == 955  # C2 -> 955 suggestions
+
+
+def random_cfg(rng, seed, big=False):
+    if big:  # acceptance.cpp:139-153 ranges (m 10-2000, c 2-200)
+        m = int(10 + rng.integers(0, 1991))
+        c = int(2 + rng.integers(0, 199))
+        a = int(1 + rng.integers(0, max(1, m // 2)))
+    else:
+        m, c, a = int(rng.integers(4, 120)), int(rng.integers(2, 30)), int(rng.integers(1, 60))
+    return dict(seed=seed, n_classes=c, n_methods=m, n_attributes=a, k_max_calls=int(rng.integers(0, 5)),
+                k_max_accesses=int(rng.integers(0, 5)), intra_class_bias=float(rng.random()))
+
+
+def check_against_oracle(e, s, ctx, modes=None, top_ks=(1,)):
+    got = gpu_metrics(e, s)
+    want = oracle.class_metrics(s)
+    assert_metrics_equal(got, want, ctx)
+    lcom, ck, cbo = want
+    t_or = oracle.thresholds(lcom, cbo)
+    t = e.compute_thresholds()
+    assert (t.lcom, t.cbo) == (t_or.lcom, t_or.cbo), ctx
+    for mask, comb, allc in modes or ((COH | COUP, 0, False), (COH | COUP, 1, False), (COH, 0, False),
+                                     (COUP, 0, False), (COH | COUP, 0, True), (COH | COUP, 1, True)):
+        for k in top_ks:
+            g = e.suggest_all(t, CRIT[mask], Combine(comb), allc, top_k=k)
+            o = oracle.suggest(s, lcom, cbo, mask, comb, allc, k, t.lcom, t.cbo)
+            assert records_equal(g, o), (ctx, mask, comb, allc, k, first_diff(g, o))
+
+
+def test_gpu_random_small_systems(gpu_engine):
+    for seed in range(40):
+        s = System.generate(**random_cfg(np.random.default_rng(seed), seed))
+        check_against_oracle(gpu_engine, s, f"seed {seed}", top_ks=(1, 3))
+
+
+def test_gpu_random_acceptance_sized(gpu_engine):
+    # acceptance criterion 2/3 sizes: 50 systems, m in [10, 2000], c in [2, 200]
+    for seed in range(50):
+        s = System.generate(**random_cfg(np.random.default_rng(7000 + seed), seed, big=True))
+        check_against_oracle(gpu_engine, s, f"acc seed {seed}", modes=((COH | COUP, 0, False), (COH | COUP, 1, True)))
+
+
+def test_gpu_what_if_every_pair_random(gpu_engine):
+    # what_if_move for every (method, destination), including non-candidate destinations
+    for seed in range(8):
+        s = System.generate(**random_cfg(np.random.default_rng(300 + seed), seed))
+        gpu_engine.upload(s)
+        for u in range(s.n_methods):
+            o = int(s.method_owner[u])
+            for d in range(s.n_classes):
+                st, w = oracle.what_if(s, u, o, d)
+                if st:
+                    with pytest.raises(MMError):
+                        gpu_engine.what_if_move(u, o, d)
+                    continue
+                g = gpu_engine.what_if_move(u, o, d)
+                for f in abi.WHATIF_FIELDS:
+                    assert g[f] == getattr(w, f), (seed, u, o, d, f)
+
+
+def test_gpu_large_class_paths(gpu_engine):
+    # classes with > 32 members, > 64 attributes and methods of degree > 16
+    # exercise the CTA path of the metric pass and the streaming sweep path
+    cfgs = [
+        dict(seed=3, n_classes=20, n_methods=10000, n_attributes=1280, k_max_calls=4, k_max_accesses=32,
+             intra_class_bias=0.9),   # C5-like: 500 methods and 64 attributes per class
+        dict(seed=5, n_classes=7, n_methods=700, n_attributes=2000, k_max_calls=12, k_max_accesses=12,
+             intra_class_bias=0.3),
+        dict(seed=11, n_classes=300, n_methods=3000, n_attributes=6000, k_max_calls=4, k_max_accesses=4,
+             intra_class_bias=0.5, zipf_s=1.0),  # C3-like Zipf skew
+        dict(seed=12, n_classes=1, n_methods=300, n_attributes=40, k_max_calls=20, k_max_accesses=20,
+             intra_class_bias=0.7),   # single class
+    ]
+    for cfg in cfgs:
+        s = System.generate(**cfg)
+        check_against_oracle(gpu_engine, s, str(cfg), modes=((COH | COUP, 0, False), (COH | COUP, 0, True),
+                                                             (COH | COUP, 1, False)), top_ks=(1, 4))
+
+
+def test_gpu_explicit_thresholds_and_degenerate(gpu_engine):
+    # empty classes, classes without attributes, isolated methods
+    s = System.build([([], [0, 1]), ([0, 1], []), ([2], [2, 3, 4]), ([], [])],
+                     [[2], [], [0, 1], [], [3]], [[0, 2], [1], [2], [], [0]])
+    check_against_oracle(gpu_engine, s, "degenerate")
+    gpu_engine.upload(s)
+    for thr in (Thresholds(0, -1.0, -1.0), Thresholds(0, 2.0, 99.0), Thresholds(0, 0.0, 0.0)):
+        lcom, ck, cbo = oracle.class_metrics(s)
+        g = gpu_engine.suggest_all(thr)
+        o = oracle.suggest(s, lcom, cbo, COH | COUP, 0, False, 1, thr.lcom, thr.cbo)
+        assert records_equal(g, o)
+
+
+def test_gpu_empty_system(gpu_engine):
+    s = System.build([([], [])], [], [])
+    gpu_engine.upload(s)
+    lcom, ck, cbo = gpu_engine.class_metrics_all()
+    assert lcom.tolist() == [0.0] and ck.tolist() == [0] and cbo.tolist() == [0]
+    assert len(gpu_engine.suggest_all(gpu_engine.compute_thresholds())) == 0
+
+
+def test_gpu_errors(gpu_engine):
+    s = System.build([([0, 1], [0, 1]), ([2, 3], [2])], [[2], [], []], [[2, 3], [0, 1], [2]])
+    gpu_engine.upload(s)
+    with pytest.raises(MMArgError):
+        gpu_engine.what_if_move(0, 0, 0)
+    with pytest.raises(MMArgError):
+        gpu_engine.what_if_move(2, 0, 1)
+    with pytest.raises(MMRangeError):
+        gpu_engine.what_if_move(0, 0, 9)
+    with pytest.raises(MMRangeError):
+        gpu_engine.what_if_move(0, 7, 1)
+    with pytest.raises(MMRangeError):
+        gpu_engine.lcom_normalized(5)
+    with pytest.raises(MMArgError):
+        gpu_engine.suggest_all(Thresholds(), [])
+    with pytest.raises(MMError) as ei:
+        gpu_engine.suggest_all(Thresholds(), [Criterion.Similarity])
+    assert ei.value.status == abi.MM_E_UNSUPPORTED
+    with pytest.raises(MMRangeError):
+        gpu_engine.suggest_all(Thresholds(), class_range=(0, 9))
+    # malformed input is rejected on upload instead of faulting
+    bad = System.build([([0, 1], [0, 1]), ([2, 3], [2])], [[2], [], []], [[2, 3], [0, 1], [2]])
+    bad.acc_tgt[0] = 99
+    with pytest.raises(MMArgError):
+        gpu_engine.upload(bad)
+
+
+def test_gpu_shards_concatenate_to_full_list(gpu_engine):
+    from paper_1308_4011_b200 import plan_shards
+    s = System.generate(seed=2, n_classes=500, n_methods=6000, n_attributes=9000, k_max_calls=5, k_max_accesses=5,
+                        intra_class_bias=0.4)
+    gpu_engine.upload(s)
+    t = gpu_engine.compute_thresholds()
+    full = gpu_engine.suggest_all(t)
+    for n in (2, 3, 8):
+        b = plan_shards(s, n)
+        parts = [gpu_engine.suggest_all(t, class_range=(int(b[i]), int(b[i + 1]))) for i in range(n)]
+        assert records_equal(np.concatenate(parts), full)
+
+
+@pytest.mark.slow
+def test_gpu_config_c4_metrics_and_sampled_sweep(gpu_engine):
+    """C4 (100k classes / 1M methods): every class value vs the oracle; the sweep
+    vs the oracle on class ranges; size-independent properties on the full list."""
+    s = System.generate(seed=1, n_classes=100000, n_methods=1000000, n_attributes=2000000)
+    got = gpu_metrics(gpu_engine, s)
+    want = oracle.class_metrics(s)
+    assert_metrics_equal(got, want, "C4")
+    t = gpu_engine.compute_thresholds()
+    t_or = oracle.thresholds(want[0], want[2])
+    assert (t.lcom, t.cbo) == (t_or.lcom, t_or.cbo)
+    full = gpu_engine.suggest_all(t)
+    stats = gpu_engine.sweep_stats()
+    assert stats["candidates"] == s.n_candidates() == 1998056
+    assert len(full) == 86684                                     # BASELINE.md §3 (reference, C4)
+    assert stats["gated_whatifs"] == 960003 + 1236116
+    key = (full["origin"].astype(np.uint64) << np.uint64(40)) | (full["method"].astype(np.uint64) << np.uint64(20)) \
+        | full["destination"].astype(np.uint64)
+    assert np.all(np.diff(key.astype(np.int64)) > 0)  # strictly (origin, method, destination) ordered
+    for lo, hi in ((0, 1000), (50000, 50500), (99000, 100000)):
+        o = oracle.suggest(s, want[0], want[2], COH | COUP, 0, False, 1, t.lcom, t.cbo, class_range=(lo, hi))
+        sel = (full["origin"] >= lo) & (full["origin"] < hi)
+        assert records_equal(full[sel], o), (lo, hi)
