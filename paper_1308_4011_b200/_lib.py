@@ -48,6 +48,8 @@ _SIGS = {
     "mm_lcom_ck": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]),
     "mm_cbo": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32)]),
     "mm_compute_thresholds": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_overrides), C.POINTER(abi.mm_thresholds)]),
+    "mm_sequential_mean": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_double),
+                                     C.POINTER(C.c_int)]),
     "mm_what_if": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(abi.mm_whatif)]),
     "mm_sweep": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_params), C.POINTER(C.c_uint64)]),
     "mm_sweep_device_result": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),

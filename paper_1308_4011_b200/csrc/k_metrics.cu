@@ -381,25 +381,6 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
 }
 
 // ---------------------------------------------------------------------------
-// threshold means (compute_thresholds, suggest.hpp:46-61)
-// ---------------------------------------------------------------------------
-
-// Serial reference semantics: one thread, class order, round-to-nearest adds.
-__global__ void k_thresholds_serial(const double* __restrict__ lcom, const uint32_t* __restrict__ cbo,
-                                    uint32_t n, DevThresholds* __restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double sl = 0.0;
-    uint64_t sc = 0;
-    for (uint32_t i = 0; i < n; ++i) {
-        sl = __dadd_rn(sl, lcom[i]);
-        sc += cbo[i];  // exact; (double)Σ == the reference's double sum while Σ < 2^53
-    }
-    out->lcom = n ? __ddiv_rn(sl, (double)n) : 0.0;
-    out->cbo = n ? __ddiv_rn((double)sc, (double)n) : 0.0;
-    out->fast_path_ok = 0;
-}
-
-// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 
@@ -439,10 +420,6 @@ void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* lar
 }
 cudaError_t set_class_large_smem(uint32_t bytes) {
     return cudaFuncSetAttribute(k_class_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-}
-void launch_thresholds_serial(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
-                              cudaStream_t st) {
-    k_thresholds_serial<<<1, 32, 0, st>>>(lcom, cbo, n, out);
 }
 
 }  // namespace mmg

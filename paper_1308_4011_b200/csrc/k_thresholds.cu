@@ -1,0 +1,491 @@
+// k_thresholds.cu — compute_thresholds' means (suggest.hpp:46-61) with the
+// reference's SEQUENTIAL double-sum semantics, computed in parallel.
+//
+// The reference sums per-class lcom left to right in double precision:
+// s_{i+1} = RN(s_i + x_i). Reassociating would change the last bits, so a
+// plain tree reduction is not bit-exact. A serial loop on the GPU is exact but
+// costs ~3 ms for 100k classes (one dependent fp64 add chain). Instead:
+//
+// * Every lcom value is k·2^-53 with k ∈ [0, 2^53] (1 − q with q ∈ [0,1]:
+//   exact when q ≥ 1/2 by Sterbenz, else rounded in [1/2, 1] whose ulp is
+//   2^-53). So the state is an exact integer T = s·2^53 (< 2^85) and one step
+//   is T' = RNE53(T + X): round to 53 significant bits, ties to even.
+// * While the exact sum stays in one binade (granularity g = 2^e), a step on a
+//   state that is a multiple of g is T' = T + g·inc where inc depends on X and
+//   only on the PARITY of T/g (ties to even). Each element is therefore a
+//   function on one bit of state — {p -> (inc_p, p'_p)} — and those compose
+//   associatively: a segmented block scan yields, for every chunk of elements,
+//   the composed function since its binade segment began. The first element
+//   of each segment (where g doubles) is applied exactly; segments are at
+//   most ~34, chained by one thread.
+// * That gives every chunk's starting state S_t. Each thread then replays its
+//   chunk with exact RNE arithmetic from S_t, and the result is accepted only
+//   if every chunk's end state equals the next chunk's S_{t+1} (induction from
+//   S_0 = 0): the answer is then provably the sequential sum, bit for bit.
+//   Any violated precondition or mismatch falls back to the serial loop in
+//   the same kernel.
+//
+// cbo's mean sums integers: exact in u64, and (double)Σ equals the
+// reference's running double sum while Σ < 2^53 (checked; else serial).
+#include <cuda_runtime.h>
+
+#include <cooperative_groups.h>
+
+#include <cstdint>
+
+#include "mm_device.cuh"
+#include "mm_kernels.h"
+
+namespace mmg {
+
+namespace {
+
+typedef unsigned __int128 u128;
+constexpr int kThrThreads = 1024;
+constexpr int kMaxSegs = 64;
+
+__device__ __forceinline__ int bitlen128(u128 v) {
+    const uint64_t hi = (uint64_t)(v >> 64), lo = (uint64_t)v;
+    return hi ? 128 - __clzll((long long)hi) : (lo ? 64 - __clzll((long long)lo) : 0);
+}
+
+__device__ __forceinline__ int gran_exp(u128 v) {  // e with ulp(v·2^-53) = 2^e units
+    const int b = bitlen128(v);
+    return b > 53 ? b - 53 : 0;
+}
+
+__device__ __forceinline__ u128 rne53(u128 v) {
+    const int e = gran_exp(v);
+    if (e == 0) return v;
+    const u128 g = (u128)1 << e, half = g >> 1, r = v & (g - 1);
+    u128 q = v >> e;
+    if (r > half || (r == half && (q & 1))) q += 1;
+    return q << e;
+}
+
+// element function on one bit of state: p -> (inc[p], par bit (p' of p) in bits)
+struct Fn {
+    uint64_t inc0, inc1;
+    uint32_t bits;  // bit0: p'(0), bit1: p'(1), bit2: segment-start flag (scan carrier)
+};
+
+__device__ __forceinline__ Fn fn_id() { return {0, 0, 0b10u}; }
+
+__device__ __forceinline__ Fn fn_elem(uint64_t X, int e) {
+    uint64_t i0, i1;
+    if (e == 0) {
+        i0 = i1 = X;
+    } else {
+        const uint64_t q = X >> e, r = X & ((1ull << e) - 1), half = 1ull << (e - 1);
+        if (r < half) i0 = i1 = q;
+        else if (r > half) i0 = i1 = q + 1;
+        else {  // tie: the result multiple must be even
+            i0 = (q & 1) ? q + 1 : q;        // p = 0
+            i1 = (q & 1) ? q : q + 1;        // p = 1
+        }
+    }
+    return {i0, i1, (uint32_t)((0 + i0) & 1) | ((uint32_t)((1 + i1) & 1) << 1)};
+}
+
+__device__ __forceinline__ int fpar(const Fn& f, int p) { return (f.bits >> p) & 1; }
+__device__ __forceinline__ uint64_t finc(const Fn& f, int p) { return p ? f.inc1 : f.inc0; }
+
+// a then b (flags: the result carries a's|b's flag; segmented combine handled by caller)
+__device__ __forceinline__ Fn compose(const Fn& a, const Fn& b) {
+    const int a0 = fpar(a, 0), a1 = fpar(a, 1);
+    Fn c;
+    c.inc0 = a.inc0 + finc(b, a0);
+    c.inc1 = a.inc1 + finc(b, a1);
+    c.bits = (uint32_t)fpar(b, a0) | ((uint32_t)fpar(b, a1) << 1);
+    return c;
+}
+
+// segmented combine of (L, R): flag = L|R; F = R.flag ? R.F : L.F ∘ R.F
+__device__ __forceinline__ Fn seg_combine(const Fn& L, const Fn& R) {
+    Fn c = (R.bits & 4u) ? R : compose(L, R);
+    c.bits = (c.bits & 3u) | ((L.bits | R.bits) & 4u);
+    return c;
+}
+
+__device__ __forceinline__ Fn shfl_up_fn(const Fn& f, int d) {
+    Fn o;
+    o.inc0 = __shfl_up_sync(0xffffffffu, f.inc0, d);
+    o.inc1 = __shfl_up_sync(0xffffffffu, f.inc1, d);
+    o.bits = __shfl_up_sync(0xffffffffu, f.bits, d);
+    return o;
+}
+
+__device__ __forceinline__ u128 shfl_up_u128(u128 v, int d) {
+    const uint64_t lo = __shfl_up_sync(0xffffffffu, (uint64_t)v, d);
+    const uint64_t hi = __shfl_up_sync(0xffffffffu, (uint64_t)(v >> 64), d);
+    return ((u128)hi << 64) | lo;
+}
+
+__device__ __forceinline__ bool lcom_units(double x, uint64_t& X) {
+    if (!(x >= 0.0 && x <= 1.0)) return false;
+    const double y = x * 0x1p53;  // exact (power-of-two scaling)
+    X = (uint64_t)y;
+    return (double)X == y;
+}
+
+constexpr int kTT = 256;                  // threads per CTA
+constexpr int kItems = 8;                 // consecutive elements per thread
+constexpr int kTile = kTT * kItems;       // 2048 elements: one tile per CTA
+constexpr int kSlot = kMaxSegs + 1;       // piece slots per tile
+
+// A tile's run of one binade: the continuation piece (first = 0: its function
+// covers elements from the tile start) or a real segment piece (first = 1:
+// X of its first element is applied exactly, the function covers the rest).
+struct Piece {
+    Fn f;
+    uint64_t x_first;
+    int e;
+    int first;
+};
+
+struct Scratch {              // global scratch, sized for the grid
+    u128* tile_sum;           // [tiles] exact Σ X
+    u128* tile_entry;         // [tiles] chained entry state
+    u128* tile_exit;          // [tiles] replayed exit state
+    Piece* pieces;            // [tiles * kSlot]
+    int* n_pieces;            // [tiles]
+    unsigned long long* cbo_sum;
+    int* bad;
+};
+
+struct TileShared {
+    u128 warp_u128[kTT / 32];
+    Fn warp_fn[kTT / 32];
+    u128 start_state[kTT];
+    u128 end_state[kTT];
+    uint32_t seg_pos[kMaxSegs];
+    int seg_e[kMaxSegs];
+    uint64_t seg_x[kMaxSegs];
+    Fn seg_total[kMaxSegs + 1];
+    u128 seg_first[kMaxSegs];
+    u128 seg_end[kMaxSegs + 1];
+    u128 entry;
+    u128 prefix;
+    int n_segs;
+};
+
+__device__ __forceinline__ u128 blk_excl_u128(u128 v, TileShared& sh, u128* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u128 inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const u128 y = shfl_up_u128(inc, d);
+        if (lane >= d) inc += y;
+    }
+    if (lane == 31) sh.warp_u128[warp] = inc;
+    __syncthreads();
+    u128 pre = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kTT / 32; ++w) {
+        if (w < warp) pre += sh.warp_u128[w];
+        all += sh.warp_u128[w];
+    }
+    *total = all;
+    __syncthreads();
+    return pre + inc - v;
+}
+
+__device__ __forceinline__ Fn blk_excl_fn(const Fn& agg, TileShared& sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Fn x = agg;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const Fn y = shfl_up_fn(x, d);
+        if (lane >= d) x = seg_combine(y, x);
+    }
+    if (lane == 31) sh.warp_fn[warp] = x;
+    const Fn xin = shfl_up_fn(x, 1);
+    __syncthreads();
+    Fn wp = fn_id();
+#pragma unroll
+    for (int w = 0; w < kTT / 32; ++w)
+        if (w < warp) wp = seg_combine(wp, sh.warp_fn[w]);
+    __syncthreads();
+    return lane == 0 ? wp : seg_combine(wp, xin);
+}
+
+// Cooperative kernel: one 2048-element tile per CTA, three grid-wide phases.
+__global__ void __launch_bounds__(kTT)
+k_thresholds_coop(const double* __restrict__ lcom, const uint32_t* __restrict__ cbo, uint32_t n,
+                  Scratch g, DevThresholds* __restrict__ out) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ TileShared sh;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t tile = blockIdx.x, n_tiles = gridDim.x;
+    const uint32_t base = tile * kTile;
+    const uint32_t my = base + (uint32_t)t * kItems;
+    const int cnt = my < n ? (int)min((uint32_t)kItems, n - my) : 0;
+    const uint32_t tile_end = min(n, base + kTile);
+
+    // ---- phase 1: load, preconditions, exact tile sum, cbo sum
+    uint64_t X[kItems];
+    int bad = 0;
+    uint64_t cs = 0;
+    if (cnt == kItems && ((reinterpret_cast<uintptr_t>(lcom + my) & 15) == 0)) {
+        const double2* p2 = reinterpret_cast<const double2*>(lcom + my);
+#pragma unroll
+        for (int j = 0; j < kItems / 2; ++j) {
+            const double2 v = p2[j];
+            bad |= !lcom_units(v.x, X[2 * j]);
+            bad |= !lcom_units(v.y, X[2 * j + 1]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            X[j] = 0;
+            if (j < cnt) bad |= !lcom_units(lcom[my + j], X[j]);
+        }
+    }
+    if (cbo) {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j)
+            if (j < cnt) cs += cbo[my + j];
+    }
+    if (bad) atomicOr(g.bad, 1);
+    u128 S = 0;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) S += X[j];
+    u128 tsum;
+    const u128 excl_sum = blk_excl_u128(S, sh, &tsum);
+    {
+        unsigned long long cw = cs;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) cw += __shfl_down_sync(0xffffffffu, cw, d);
+        if (lane == 0 && cw) atomicAdd(g.cbo_sum, cw);
+    }
+    if (t == 0) g.tile_sum[tile] = tsum;
+    grid.sync();
+
+    // ---- phase 2: exact prefix, binade segments, per-thread compositions, tile pieces
+    {
+        u128 part = 0;
+        for (uint32_t j = t; j < tile; j += kTT) part += g.tile_sum[j];
+        u128 dummy;
+        const u128 ex = blk_excl_u128(part, sh, &dummy);
+        (void)ex;
+        if (t == 0) { sh.prefix = dummy; sh.n_segs = 0; }
+        __syncthreads();
+    }
+    const u128 P_tile = sh.prefix;
+    const u128 P_my = P_tile + excl_sum;
+    const int e_cont = base == 0 ? -1 : gran_exp(P_tile);
+    int e_el[kItems];
+    uint32_t starts = 0;
+    Fn agg = fn_id();
+    {
+        u128 P = P_my;
+        int e_prev = my == 0 ? -1 : gran_exp(P_my);
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            e_el[j] = 0;
+            if (j < cnt) {
+                P += X[j];
+                const int e = gran_exp(P);
+                e_el[j] = e;
+                if (e != e_prev) {
+                    starts |= 1u << j;
+                    const int k = atomicAdd(&sh.n_segs, 1);
+                    if (k < kMaxSegs) { sh.seg_pos[k] = my + j; sh.seg_e[k] = e; sh.seg_x[k] = X[j]; }
+                    agg = fn_id();
+                    agg.bits |= 4u;
+                } else {
+                    const uint32_t fl = agg.bits & 4u;
+                    agg = compose(agg, fn_elem(X[j], e));
+                    agg.bits |= fl;
+                }
+                e_prev = e;
+            }
+        }
+    }
+    const Fn excl = blk_excl_fn(agg, sh);
+    if (t == 0) {
+        if (sh.n_segs > kMaxSegs) atomicOr(g.bad, 4);
+        const int ns = min(sh.n_segs, kMaxSegs);
+        for (int a = 1; a < ns; ++a)
+            for (int b = a; b > 0 && sh.seg_pos[b - 1] > sh.seg_pos[b]; --b) {
+                const uint32_t tp = sh.seg_pos[b]; sh.seg_pos[b] = sh.seg_pos[b - 1]; sh.seg_pos[b - 1] = tp;
+                const int te = sh.seg_e[b]; sh.seg_e[b] = sh.seg_e[b - 1]; sh.seg_e[b - 1] = te;
+                const uint64_t tx = sh.seg_x[b]; sh.seg_x[b] = sh.seg_x[b - 1]; sh.seg_x[b - 1] = tx;
+            }
+        sh.seg_total[0] = fn_id();
+    }
+    __syncthreads();
+    const int ns = min(sh.n_segs, kMaxSegs);
+    int kb = -1;  // local segment active just before `my` (-1: continuation)
+    for (int k = 0; k < ns; ++k)
+        if (sh.seg_pos[k] < my) kb = k;
+    if (cnt > 0) {
+        Fn run = excl;
+        int k = kb;
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+            if (j < cnt) {
+                if (starts & (1u << j)) {
+                    if (k + 1 <= kMaxSegs) sh.seg_total[k + 1] = run;
+                    ++k;
+                    run = fn_id();
+                } else {
+                    run = compose(run, fn_elem(X[j], e_el[j]));
+                }
+            }
+        }
+        if (my + cnt == tile_end && k + 1 <= kMaxSegs) sh.seg_total[k + 1] = run;
+    }
+    __syncthreads();
+    const bool has_cont = !(ns > 0 && sh.seg_pos[0] == base);
+    if (t == 0) {
+        Piece* pc = g.pieces + (size_t)tile * kSlot;
+        int np = 0;
+        if (has_cont) pc[np++] = Piece{sh.seg_total[0], 0, e_cont, 0};
+        for (int k = 0; k < ns; ++k) pc[np++] = Piece{sh.seg_total[k + 1], sh.seg_x[k], sh.seg_e[k], 1};
+        g.n_pieces[tile] = np;
+    }
+    grid.sync();
+
+    // ---- phase 3: chain all earlier pieces -> tile entry state; derive chunk
+    // starts; exact replay; verify chunk joins
+    if (t == 0) {
+        u128 T = 0;
+        for (uint32_t b = 0; b < tile; ++b) {
+            const Piece* pc = g.pieces + (size_t)b * kSlot;
+            const int np = g.n_pieces[b];
+            for (int i = 0; i < np; ++i) {
+                const Piece q = pc[i];
+                if (q.first) T = rne53(T + q.x_first);
+                if (q.e >= 0) T += (u128)finc(q.f, (int)((T >> q.e) & 1)) << q.e;
+            }
+        }
+        sh.entry = T;
+        g.tile_entry[tile] = T;
+        // this tile's segment states
+        if (has_cont && e_cont >= 0) T += (u128)finc(sh.seg_total[0], (int)((T >> e_cont) & 1)) << e_cont;
+        sh.seg_end[0] = T;
+        for (int k = 0; k < ns; ++k) {
+            const int e = sh.seg_e[k];
+            T = rne53(T + sh.seg_x[k]);
+            sh.seg_first[k] = T;
+            T += (u128)finc(sh.seg_total[k + 1], (int)((T >> e) & 1)) << e;
+            sh.seg_end[k + 1] = T;
+        }
+    }
+    __syncthreads();
+    const u128 T_entry = sh.entry;
+    u128 S0 = T_entry;
+    if (cnt > 0) {
+        if (starts & 1u) {
+            S0 = sh.seg_end[kb + 1];
+        } else if (kb >= 0) {
+            const int e = sh.seg_e[kb];
+            const u128 F = sh.seg_first[kb];
+            S0 = F + ((u128)finc(excl, (int)((F >> e) & 1)) << e);
+        } else if (e_cont >= 0) {
+            S0 = T_entry + ((u128)finc(excl, (int)((T_entry >> e_cont) & 1)) << e_cont);
+        }
+    }
+    sh.start_state[t] = S0;
+    u128 T = S0;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j)
+        if (j < cnt) T = rne53(T + X[j]);
+    sh.end_state[t] = T;
+    __syncthreads();
+    if (cnt > 0) {
+        if (my == base && S0 != T_entry) atomicOr(g.bad, 2);
+        const bool last = my + cnt == tile_end;
+        if (!last && sh.start_state[t + 1] != T) atomicOr(g.bad, 2);
+        if (last) g.tile_exit[tile] = T;
+    }
+    grid.sync();
+
+    // ---- phase 4: tile joins, final mean (or the serial fallback)
+    if (tile == 0 && t == 0) {
+        int b = *g.bad;
+        for (uint32_t j = 1; j < n_tiles; ++j)
+            if (g.tile_exit[j - 1] != g.tile_entry[j]) b |= 2;
+        double mean_l;
+        uint32_t fast = 1;
+        if (b || n == 0) {
+            fast = 0;
+            double s = 0.0;
+            for (uint32_t i = 0; i < n; ++i) s = __dadd_rn(s, lcom[i]);
+            mean_l = n ? __ddiv_rn(s, (double)n) : 0.0;
+        } else {
+            const u128 Tn = g.tile_exit[n_tiles - 1];
+            const int bl = bitlen128(Tn);
+            const int sft = bl > 53 ? bl - 53 : 0;
+            mean_l = __ddiv_rn(ldexp((double)(uint64_t)(Tn >> sft), sft - 53), (double)n);
+        }
+        const unsigned long long csum = *g.cbo_sum;
+        double mean_c;
+        if (csum < (1ull << 53)) {
+            mean_c = n ? __ddiv_rn((double)csum, (double)n) : 0.0;
+        } else {
+            fast = 0;
+            double sc = 0.0;
+            for (uint32_t i = 0; i < n; ++i) sc = __dadd_rn(sc, cbo ? (double)cbo[i] : 0.0);
+            mean_c = n ? __ddiv_rn(sc, (double)n) : 0.0;
+        }
+        out->lcom = mean_l;
+        out->cbo = mean_c;
+        out->fast_path_ok = fast;
+    }
+}
+
+// Serial fallback kernel (n too large for one co-resident tile per CTA).
+__global__ void k_thresholds_serial(const double* __restrict__ lcom, const uint32_t* __restrict__ cbo, uint32_t n,
+                                    DevThresholds* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double sl = 0.0, sc = 0.0;
+    for (uint32_t i = 0; i < n; ++i) {
+        sl = __dadd_rn(sl, lcom[i]);
+        sc = __dadd_rn(sc, cbo ? (double)cbo[i] : 0.0);
+    }
+    out->lcom = n ? __ddiv_rn(sl, (double)n) : 0.0;
+    out->cbo = n ? __ddiv_rn(sc, (double)n) : 0.0;
+    out->fast_path_ok = 0;
+}
+
+}  // namespace
+
+size_t thresholds_scratch_bytes(uint32_t n) {
+    const size_t tiles = (n + kTile - 1) / kTile;
+    return tiles * (3 * sizeof(u128) + kSlot * sizeof(Piece) + sizeof(int)) + 64;
+}
+
+cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
+                              void* scratch, size_t scratch_bytes, cudaStream_t st) {
+    const uint32_t tiles = (n + kTile - 1) / kTile;
+    static int max_coresident = -1;
+    if (max_coresident < 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_thresholds_coop, kTT, 0);
+        max_coresident = sms * per_sm;
+    }
+    if (n == 0 || tiles > (uint32_t)max_coresident || scratch_bytes < thresholds_scratch_bytes(n)) {
+        k_thresholds_serial<<<1, 32, 0, st>>>(lcom, cbo, n, out);
+        return cudaGetLastError();
+    }
+    char* p = static_cast<char*>(scratch);
+    Scratch g;
+    g.tile_sum = reinterpret_cast<u128*>(p);
+    g.tile_entry = g.tile_sum + tiles;
+    g.tile_exit = g.tile_entry + tiles;
+    g.pieces = reinterpret_cast<Piece*>(g.tile_exit + tiles);
+    g.n_pieces = reinterpret_cast<int*>(g.pieces + (size_t)tiles * kSlot);
+    g.cbo_sum = reinterpret_cast<unsigned long long*>(
+        (reinterpret_cast<uintptr_t>(g.n_pieces + tiles) + 15) & ~uintptr_t(15));
+    g.bad = reinterpret_cast<int*>(g.cbo_sum + 1);
+    cudaMemsetAsync(g.cbo_sum, 0, 16, st);
+    void* args[] = {(void*)&lcom, (void*)&cbo, (void*)&n, (void*)&g, (void*)&out};
+    return cudaLaunchCooperativeKernel((const void*)k_thresholds_coop, dim3(tiles), dim3(kTT), args, 0, st);
+}
+
+}  // namespace mmg

@@ -98,6 +98,7 @@ struct mm_ctx {
     DBuf<unsigned long long> tile_state;
     DBuf<mm_suggestion> out;
     DBuf<mm_whatif> whatif;
+    DBuf<char> thr_scratch;
     bool sweep_valid = false;
 
     DevModel dev() const {
@@ -239,6 +240,7 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     free_model(ctx);
     ctx->ctl.release();
     ctx->whatif.release();
+    ctx->thr_scratch.release();
     ctx->tile_state.release();
     ctx->out.release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -399,6 +401,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, ctx->lcom.alloc(C ? C : 1));
     MM_CUDA(ctx, ctx->ck.alloc(C ? C : 1));
     MM_CUDA(ctx, ctx->cbo.alloc(C ? C : 1));
+    MM_CUDA(ctx, ctx->thr_scratch.ensure(thresholds_scratch_bytes(C)));
     MM_CUDA(ctx, ctx->ux.alloc(Ec + Ea + 1));
     MM_CUDA(ctx, ctx->un.alloc(Ec + Ea + 1));
     ctx->have_model = true;
@@ -429,10 +432,13 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
         });
         if (st) return st;
     }
+    cudaError_t te = cudaSuccess;
     st = run(ctx, "thresholds", [&] {
-        launch_thresholds_serial(ctx->lcom.p, ctx->cbo.p, ctx->C, &ctl->thr, ctx->stream);
+        te = launch_thresholds(ctx->lcom.p, ctx->cbo.p, ctx->C, &ctl->thr, ctx->thr_scratch.p, ctx->thr_scratch.n,
+                               ctx->stream);
     });
     if (st) return st;
+    if (te != cudaSuccess) return cuda_fail(ctx, te, "thresholds");
     ctx->metrics_valid = true;
     ctx->sweep_valid = false;
     return MM_OK;
@@ -599,6 +605,34 @@ mm_status mm_copy_suggestions(mm_ctx* ctx, mm_suggestion* out, uint64_t cap, uin
     MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->out.p, sizeof(mm_suggestion) * ss.suggestions, cudaMemcpyDeviceToHost,
                                  ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+mm_status mm_sequential_mean(mm_ctx* ctx, const double* values, uint64_t n, double* out, int* fast_path) {
+    if (!ctx || !out || (n && !values)) return MM_E_ARG;
+    if (n >= 0xffffffffull) return fail(ctx, MM_E_RANGE, "mm_sequential_mean: n too large");
+    if (mm_status st = set_device(ctx)) return st;
+    DBuf<double> d;
+    MM_CUDA(ctx, d.alloc(n ? n : 1));
+    if (n) MM_CUDA(ctx, cudaMemcpyAsync(d.p, values, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+    DevThresholds* dt = &ctx->ctl.p->thr;
+    DBuf<char> scratch;
+    MM_CUDA(ctx, scratch.alloc(thresholds_scratch_bytes((uint32_t)n)));
+    cudaError_t te = cudaSuccess;
+    mm_status st = run(ctx, "thresholds", [&] {
+        te = launch_thresholds(d.p, nullptr, (uint32_t)n, dt, scratch.p, scratch.n, ctx->stream);
+    });
+    if (st) return st;
+    if (te != cudaSuccess) return cuda_fail(ctx, te, "thresholds");
+    DevThresholds h{};
+    MM_CUDA(ctx, cudaMemcpyAsync(&h, dt, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    d.release();
+    scratch.release();
+    ctx->metrics_valid = false;  // the control block's thresholds were overwritten
+    *out = h.lcom;
+    if (fast_path) *fast_path = (int)h.fast_path_ok;
     return MM_OK;
 }
 

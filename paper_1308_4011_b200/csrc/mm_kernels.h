@@ -52,8 +52,10 @@ void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* lar
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
                         uint64_t* gkeys, uint32_t* grows, cudaStream_t st);
 cudaError_t set_class_large_smem(uint32_t bytes);
-void launch_thresholds_serial(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
-                              cudaStream_t st);
+// means with sequential-sum semantics; cbo may be NULL (treated as zeros)
+size_t thresholds_scratch_bytes(uint32_t n);
+cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
+                              void* scratch, size_t scratch_bytes, cudaStream_t st);
 void launch_sweep(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 constexpr uint32_t kSweepTile = 256;
 void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un,

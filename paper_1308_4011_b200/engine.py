@@ -186,6 +186,14 @@ class Engine:
         self._check(lib().mm_compute_thresholds(self._ctx, C.byref(ov), C.byref(t)), "compute_thresholds")
         return Thresholds(t.similarity, t.lcom, t.cbo, bool(t.explicit_mode))
 
+    def sequential_mean(self, values) -> tuple:
+        """(mean, fast_path) of values with the reference's sequential double-sum semantics."""
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        out, fast = C.c_double(), C.c_int()
+        self._check(lib().mm_sequential_mean(self._ctx, v.ctypes.data, len(v), C.byref(out), C.byref(fast)),
+                    "mm_sequential_mean")
+        return out.value, bool(fast.value)
+
     # ---- what-if ------------------------------------------------------
     def what_if_move(self, method: int, origin: int, destination: int) -> dict:
         w = abi.mm_whatif()

@@ -225,3 +225,42 @@ def test_gpu_config_c4_metrics_and_sampled_sweep(gpu_engine):
         o = oracle.suggest(s, want[0], want[2], COH | COUP, 0, False, 1, t.lcom, t.cbo, class_range=(lo, hi))
         sel = (full["origin"] >= lo) & (full["origin"] < hi)
         assert records_equal(full[sel], o), (lo, hi)
+
+
+def _seq_mean(vals):
+    s = 0.0
+    for v in vals:
+        s += float(v)  # IEEE double round-to-nearest, left to right (suggest.hpp:48-53)
+    return s / len(vals) if len(vals) else 0.0
+
+
+def test_gpu_sequential_mean_adversarial(gpu_engine):
+    rng = np.random.default_rng(0)
+    u = 2.0 ** -53
+    cases = []
+    for n in (1, 2, 3, 31, 1000, 1024, 1025, 4097, 100000, 333333):
+        cases.append(rng.integers(0, 2 ** 53 + 1, n).astype(np.float64) * u)            # uniform grid values
+        cases.append(np.round(rng.random(n) * 8) / 8)                                    # dyadic -> exact ties
+        cases.append(0.5 + rng.integers(0, 4, n) * 2.0 ** -53)                           # ties at every binade
+        cases.append(np.where(rng.random(n) < 0.5, 1.0, 0.0))                            # exact binade hits
+        cases.append(1.0 - rng.integers(1, 1 << 20, n) * u)                              # near-1 values
+    cases.append(np.zeros(5000))
+    for vals in cases:
+        got, fast = gpu_engine.sequential_mean(vals)
+        assert got == _seq_mean(vals), (len(vals), vals[:4])
+        assert fast, "fast path should accept grid values"
+    # outside the fast path's precondition: still exact (device serial fallback)
+    for vals in (rng.random(3000) * 0.3, -rng.random(100), rng.random(2000) * 3):
+        got, fast = gpu_engine.sequential_mean(vals)
+        assert got == _seq_mean(vals) and not fast
+
+
+def test_gpu_threshold_fast_path_on_systems(gpu_engine):
+    for cfg in (dict(seed=1, n_classes=100000, n_methods=300000, n_attributes=200000),
+                dict(seed=4, n_classes=77777, n_methods=500000, n_attributes=100000, k_max_accesses=9)):
+        s = System.generate(**cfg)
+        gpu_engine.upload(s)
+        lcom, ck, cbo = gpu_engine.class_metrics_all()
+        t = gpu_engine.compute_thresholds()
+        assert t.lcom == _seq_mean(lcom) and t.cbo == _seq_mean(cbo.astype(np.float64))
+        assert gpu_engine.sequential_mean(lcom) == (t.lcom, True)
