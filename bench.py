@@ -70,19 +70,29 @@ def dist_env():
 
 
 def algorithmic_bytes(sys_, nnz_u: int, n_sugg: int, rank_share: float = 1.0) -> dict:
-    """SURVEY.md §8d compulsory u32 traffic (bytes).
-    B_in  = 4[2(m+1) + E_c + E_a + m + a]      call/access CSR + owner maps
-    B_cls = 4[(c+1) + m + (c+1) + a] + 24c     class segments + per-class table
-    B_U   = 4(c+1) + 8 nnz(U)                  class x class use-count rows
-    metric pass = B_in + B_cls + B_U + 20c ; sweep = B_in + B_cls + B_U + 64|S|"""
+    """Compulsory bytes per launch of each kernel: every array the kernel must
+    touch, read or written once (DESIGN.md §4 derives each line). m, c, a =
+    methods, classes, attributes; E = call + access edges; nnz = Σ cbo (U row
+    entries); S = emitted suggestion records; the sweep kernels scale with the
+    rank's share of methods."""
     m, c, a = sys_.n_methods, sys_.n_classes, sys_.n_attributes
-    Ec, Ea = sys_.n_calls, sys_.n_accesses
-    b_in = 4 * (2 * (m + 1) + Ec + Ea + m + a)
+    E = sys_.n_calls + sys_.n_accesses
+    ms = int(m * rank_share)
+    k = {
+        "layout": 8 * m + 12 * a + 4 * c,
+        "method": 60 * m + 8 * a + 4 * E,
+        "class_small": 44 * m + 61 * c + 8 * nnz_u,
+        "thresholds": 12 * c,
+        "score": 56 * ms + 32 * c + 4 * nnz_u,
+        "emit": 20 * ms + 12 * c + 96 * n_sugg,
+    }
+    # SURVEY.md §8d layout-independent totals, for reference
+    b_in = 4 * (2 * (m + 1) + E + m + a)
     b_cls = 4 * ((c + 1) + m + (c + 1) + a) + 24 * c
     b_u = 4 * (c + 1) + 8 * nnz_u
-    return {"metric": b_in + b_cls + b_u + 20 * c,
-            "sweep": int(rank_share * b_in) + b_cls + b_u + 64 * n_sugg,
-            "B_in": b_in, "B_cls": b_cls, "B_U": b_u}
+    k["survey_metric_pass"] = b_in + b_cls + b_u + 20 * c
+    k["survey_sweep"] = int(rank_share * b_in) + b_cls + b_u + 64 * n_sugg
+    return k
 
 
 class ClockSampler:
@@ -300,8 +310,8 @@ def run_ours(args) -> None:
     ab = algorithmic_bytes(s, nnz_u, n_sugg_local, share)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    dom = max(("sweep", "class_small"), key=lambda k: kern.get(k, {}).get("avg_us", 0.0))
-    dom_bytes = ab["sweep"] if dom == "sweep" else ab["metric"]
+    dom = max((k for k in kern if k in ab), key=lambda k: kern[k]["avg_us"])
+    dom_bytes = ab[dom]
     dom_us = kern[dom]["avg_us"]
     achieved = dom_bytes / (dom_us * 1e-6) / 1e9
     traffic = args.traffic_bytes
@@ -312,8 +322,8 @@ def run_ours(args) -> None:
                 "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s"}
-    recompute_us = sum(kern.get(k, {}).get("avg_us", 0.0) for k in ("attr_local", "class_small", "class_large",
-                                                                     "thresholds"))
+    recompute_us = sum(kern.get(k, {}).get("avg_us", 0.0) for k in ("layout", "method", "class_small",
+                                                                     "class_large", "thresholds"))
 
     # e2e through the public API: pinned host CSR -> H2D upload -> pass -> sweep -> D2H results
     e2e = None
@@ -339,7 +349,7 @@ def run_ours(args) -> None:
             "gpu_launches": gpu_launches,
             "clocks": clocks.summary(),
             "recompute_ms": recompute_us / 1e3,
-            "sweep_ms": kern.get("sweep", {}).get("avg_us", 0.0) / 1e3,
+            "sweep_ms": sum(kern.get(k, {}).get("avg_us", 0.0) for k in ("score", "emit")) / 1e3,
             "suggestions": int(n_sugg_local) if world == 1 else None,
             "kernels": kern,
             "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),

@@ -14,6 +14,7 @@
 //             (metrics.hpp:167-185), built as the sorted U row with counts.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "mm_device.cuh"
@@ -68,12 +69,68 @@ __global__ void k_plan_classes(DevModel s, uint8_t* __restrict__ kind, uint32_t*
     atomicMax(max_deg, mdeg);
 }
 
-// attr_local[t] = index of attribute t in its class's sorted attribute list
-__global__ void k_attr_local(DevModel s, uint32_t* __restrict__ attr_local) {
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < s.A; j += gridDim.x * blockDim.x) {
-        const uint32_t t = s.cls_attrs[j];
-        attr_local[t] = j - s.cls_aoff[s.attribute_owner[t]];
+// Layout pass: inv[p] = class-order position of method p (inverse of the
+// concatenated ClassRecord::method_ids) and attr_local[t] = index of
+// attribute t inside its class's sorted attribute list.
+__global__ void k_layout(DevModel s, uint32_t* __restrict__ inv, uint32_t* __restrict__ attr_local) {
+    const uint32_t n = max(s.M, s.A);
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        if (j < s.M) inv[s.cls_methods[j]] = j;
+        if (j < s.A) {
+            const uint32_t t = s.cls_attrs[j];
+            attr_local[t] = j - s.cls_aoff[s.attribute_owner[t]];
+        }
     }
+}
+
+// Method pass, method-id order (coalesced CSR reads, owner gathers hit L2):
+// each method's sorted used list with per-class access counts, packed into a
+// 32-byte MethRec at its class-order position, plus its own-attribute bit
+// mask (attr_local bits, meaningful for classes with ≤ 64 attributes).
+template <int K>
+__global__ void __launch_bounds__(256)
+k_method(DevModel s, const uint32_t* __restrict__ inv, const uint32_t* __restrict__ attr_local,
+         MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask, uint32_t* __restrict__ pos_owner) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= s.M) return;
+    const uint32_t own = __ldg(s.method_owner + p);
+    const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
+    const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+    uint32_t hdr = kRecOverflow;
+    uint32_t ent[kRecMaxEnt];
+#pragma unroll
+    for (int k = 0; k < kRecMaxEnt; ++k) ent[k] = 0;
+    uint64_t mask = 0;
+    if ((ce - cb) + (ae - ab) <= (uint32_t)K) {
+        UsedList<K> L;
+        L.clear();
+        uint32_t hown = 0;
+        for (uint32_t e = cb; e < ce; ++e) L.insert(__ldg(s.method_owner + __ldg(s.call_tgt + e)), 0);
+        for (uint32_t e = ab; e < ae; ++e) {
+            const uint32_t t = __ldg(s.acc_tgt + e);
+            const uint32_t o = __ldg(s.attribute_owner + t);
+            L.insert(o, 1);
+            if (o == own) {
+                const uint32_t loc = __ldg(attr_local + t);
+                if (loc < 64) mask |= 1ull << loc;
+                ++hown;
+            }
+        }
+        bool fits = L.n <= kRecMaxEnt && hown < 256;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (k < L.n) {
+                fits = fits && L.X[k] < (1u << 24) && L.h[k] < 256;
+                if (k < kRecMaxEnt) ent[k] = (L.X[k] << 8) | L.h[k];
+            }
+        if (fits) hdr = (uint32_t)L.n | (hown << kRecHownShift);
+    }
+    const uint32_t pos = __ldg(inv + p);
+    uint4* dst = reinterpret_cast<uint4*>(recs + pos);
+    dst[0] = make_uint4(hdr, ent[0], ent[1], ent[2]);
+    dst[1] = make_uint4(ent[3], ent[4], ent[5], ent[6]);
+    own_mask[pos] = mask;
+    pos_owner[pos] = own;
 }
 
 // ---------------------------------------------------------------------------
@@ -111,29 +168,56 @@ __device__ __forceinline__ void warp_bitonic_u32(uint32_t* buf, int N, int lane)
         }
 }
 
+__device__ __forceinline__ int smem_find(const uint32_t* row, int n, uint32_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (row[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < n && row[lo] == x) ? lo : -1;
+}
+
+// One warp per class, one lane per member. Members' used lists come from the
+// method pass records (coalesced: a class's members are contiguous in class
+// order); a member whose list overflowed its record is rebuilt from the CSR.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_class_small(DevModel s, const uint8_t* __restrict__ kind, const uint32_t* __restrict__ attr_local,
-              ClassRec* __restrict__ rec, double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out,
-              uint32_t* __restrict__ cbo_out, uint32_t* __restrict__ ux, uint32_t* __restrict__ un,
-              uint32_t* __restrict__ ucursor) {
+              MethRec* __restrict__ recs, const uint64_t* __restrict__ own_mask, ClassRec* __restrict__ rec,
+              double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
+              uint32_t* __restrict__ ux, uint32_t* __restrict__ un, uint32_t* __restrict__ ucursor) {
     __shared__ uint32_t sbuf[kWarpsPerBlock][kSmallEntries];
-    __shared__ uint16_t shead[kWarpsPerBlock][kSmallEntries + 1];
+    __shared__ uint32_t scnt[kWarpsPerBlock][kSmallEntries];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t c = blockIdx.x * kWarpsPerBlock + warp;
     if (c >= s.C || kind[c] != 0) return;  // warp-uniform exit
     const uint32_t mb = s.cls_moff[c];
     const uint32_t M = s.cls_moff[c + 1] - mb;
     const uint32_t A = s.cls_aoff[c + 1] - s.cls_aoff[c];
+    const bool active = lane < (int)M;
+    const uint32_t pos = mb + lane;
 
-    UsedList<kSmallMaxDeg> L;
+    UsedList<kSmallMaxDeg> L;  // only for overflowed records
     L.clear();
-    uint64_t mask = 0;  // own-attribute set as bits of attr_local
-    uint32_t hown = 0;  // |acc(p) ∩ attrs(c)|
-    if (lane < (int)M) {
-        const uint32_t p = s.cls_methods[mb + lane];
+    uint4 r0 = make_uint4(kRecOverflow, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
+    uint64_t mask = 0;
+    uint32_t hown = 0;
+    if (active) {
+        const uint4* src = reinterpret_cast<const uint4*>(recs + pos);
+        r0 = src[0];
+        r1 = src[1];
+        mask = own_mask[pos];
+    }
+    const bool ovf = active && (r0.x & kRecOverflow);
+    const uint32_t ent[kRecMaxEnt] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    uint32_t nent = active && !ovf ? rec_n(r0.x) : 0;
+    if (active && !ovf) hown = rec_hown(r0.x);
+    if (ovf) {
+        const uint32_t p = s.cls_methods[pos];
         const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
         for (uint32_t e = cb; e < ce; ++e) L.insert(__ldg(s.method_owner + __ldg(s.call_tgt + e)), 0);
         const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+        mask = 0;
         for (uint32_t e = ab; e < ae; ++e) {
             const uint32_t t = __ldg(s.acc_tgt + e);
             const uint32_t o = __ldg(s.attribute_owner + t);
@@ -154,49 +238,117 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind, const uint32_t* __re
     }
     const uint32_t Q = warp_sum(q);
 
-    // U row: multiset union of members' used classes other than c
-    const uint32_t has_c = L.has(c) ? 1u : 0u;
-    const uint32_t cnt = lane < (int)M ? (uint32_t)L.n - has_c : 0u;
+    // U row: multiset union of the members' used classes other than c
+    uint32_t cnt = 0;
+    if (ovf) cnt = (uint32_t)L.n - (L.has(c) ? 1u : 0u);
+    else
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k) cnt += (k < (int)nent && (ent[k] >> 8) != c);
     const uint32_t off = warp_excl_scan(cnt, lane);
     const uint32_t T = __shfl_sync(0xffffffffu, off + cnt, 31);
     uint32_t* buf = sbuf[warp];
     {
         uint32_t w = off;
+        if (ovf) {
 #pragma unroll
-        for (int k = 0; k < kSmallMaxDeg; ++k)
-            if (k < L.n && L.X[k] != c) buf[w++] = L.X[k];
+            for (int k = 0; k < kSmallMaxDeg; ++k)
+                if (k < L.n && L.X[k] != c) buf[w++] = L.X[k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < kRecMaxEnt; ++k)
+                if (k < (int)nent && (ent[k] >> 8) != c) buf[w++] = ent[k] >> 8;
+        }
     }
-    int N = 32;
-    while (N < (int)T) N <<= 1;
-    for (int i = (int)T + lane; i < N; i += 32) buf[i] = kNone;
     __syncwarp();
-    warp_bitonic_u32(buf, N, lane);
-
-    uint16_t* heads = shead[warp];
-    uint32_t nh = 0;
-    for (uint32_t base = 0; base < T; base += 32) {
-        const uint32_t i = base + lane;
-        const bool head = i < T && (i == 0 || buf[i] != buf[i - 1]);
-        const uint32_t b = __ballot_sync(0xffffffffu, head);
-        if (head) heads[nh + __popc(b & ((1u << lane) - 1))] = (uint16_t)i;
-        nh += __popc(b);
+    uint32_t* row = sbuf[warp];
+    uint32_t* rcnt = scnt[warp];
+    uint32_t cbo = 0;
+    uint64_t sig = 0;
+    if (T <= 32) {
+        // register bitonic sort across the warp, run-length encode with ballots
+        uint32_t v = lane < (int)T ? buf[lane] : kNone;
+        __syncwarp();
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+                const bool up = (lane & k) == 0;
+                const bool lower = (lane & j) == 0;
+                v = (lower == up) ? min(v, o) : max(v, o);
+            }
+        const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
+        const bool head = lane < (int)T && (lane == 0 || v != prev);
+        const uint32_t hb = __ballot_sync(0xffffffffu, head);
+        cbo = __popc(hb);
+        if (head) {
+            const uint32_t idx = __popc(hb & ((1u << lane) - 1));
+            const uint32_t above = hb & ~((2u << lane) - 1);  // heads after this lane
+            const uint32_t next = above ? __ffs(above) - 1 : T;
+            row[idx] = v;
+            rcnt[idx] = next - lane;
+            sig |= 1ull << uhash(v);
+        }
+    } else {
+        int N = 64;
+        while (N < (int)T) N <<= 1;
+        for (int i = (int)T + lane; i < N; i += 32) buf[i] = kNone;
+        __syncwarp();
+        warp_bitonic_u32(buf, N, lane);
+        uint32_t nh = 0;
+        for (uint32_t base = 0; base < T; base += 32) {  // heads compacted into rcnt (positions)
+            const uint32_t i = base + lane;
+            const bool head = i < T && (i == 0 || buf[i] != buf[i - 1]);
+            const uint32_t b = __ballot_sync(0xffffffffu, head);
+            if (head) {
+                rcnt[nh + __popc(b & ((1u << lane) - 1))] = i;
+                sig |= 1ull << uhash(buf[i]);
+            }
+            nh += __popc(b);
+        }
+        __syncwarp();
+        cbo = nh;
+        // (X, count) into row/rcnt in place: heads are increasing, so slot k ≤ head k
+        for (uint32_t k0 = 0; k0 < cbo; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            uint32_t x = 0, cn = 0;
+            if (k < cbo) {
+                const uint32_t h0 = rcnt[k];
+                const uint32_t h1 = k + 1 < cbo ? rcnt[k + 1] : T;
+                x = buf[h0];
+                cn = h1 - h0;
+            }
+            __syncwarp();
+            if (k < cbo) { row[k] = x; rcnt[k] = cn; }
+            __syncwarp();
+        }
     }
-    if (lane == 0) heads[nh] = (uint16_t)T;
     __syncwarp();
-    const uint32_t cbo = nh;
+    sig = __reduce_or_sync(0xffffffffu, (uint32_t)sig) | ((uint64_t)__reduce_or_sync(0xffffffffu, (uint32_t)(sig >> 32)) << 32);
     uint32_t ubase = 0;
     if (lane == 0 && cbo) ubase = atomicAdd(ucursor, cbo);  // slot reservation
     ubase = __shfl_sync(0xffffffffu, ubase, 0);
     for (uint32_t k = lane; k < cbo; k += 32) {
-        ux[ubase + k] = buf[heads[k]];
-        un[ubase + k] = (uint32_t)heads[k + 1] - heads[k];
+        ux[ubase + k] = row[k];
+        un[ubase + k] = rcnt[k];
+    }
+    // per member: #{X ≠ c : U[c][X] == 1} — the sweep's cbo_origin_after
+    if (active && !ovf) {
+        uint32_t removed = 0;
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k)
+            if (k < (int)nent && (ent[k] >> 8) != c) {
+                const int at = smem_find(row, (int)cbo, ent[k] >> 8);
+                removed += (at >= 0 && rcnt[at] == 1u);
+            }
+        recs[pos].hdr = r0.x | (removed << kRecRemovedShift) | kRecRemovedValid;
     }
     if (lane == 0) {
         const double l = lcom_of(A, M, H);
         const uint64_t pairs = (uint64_t)M * (M - 1) / 2;
         const uint64_t P = pairs - Q;
         ClassRec r;
-        r.A = A; r.M = M; r.H = H; r.cbo = cbo; r.ubase = ubase; r.pad = 0; r.lcom = l;
+        r.A = A; r.M = M; r.H = H; r.cbo = cbo; r.ubase = ubase; r.pad = 0; r.sig = sig;
         rec[c] = r;
         lcom_out[c] = l;
         ck_out[c] = P > Q ? P - Q : 0;
@@ -257,7 +409,7 @@ __device__ void block_bitonic_u64(uint64_t* buf, uint32_t N) {
 
 __global__ void __launch_bounds__(kLargeThreads)
 k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* __restrict__ plan,
-              const uint32_t* __restrict__ attr_local, ClassRec* __restrict__ rec,
+              const uint32_t* __restrict__ attr_local, MethRec* __restrict__ recs, ClassRec* __restrict__ rec,
               double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
               uint32_t* __restrict__ ux, uint32_t* __restrict__ un, uint32_t* __restrict__ ucursor,
               uint64_t* __restrict__ gkeys, uint32_t* __restrict__ grows) {
@@ -265,6 +417,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     __shared__ uint64_t red64[kLargeThreads / 32];
     __shared__ uint32_t red32[kLargeThreads / 32];
     __shared__ uint32_t s_nk, s_ubase;
+    __shared__ unsigned long long s_sig;
     const uint32_t c = large_list[blockIdx.x];
     const LargePlan pl = plan[blockIdx.x];
     uint64_t* keys = pl.keys_in_smem ? reinterpret_cast<uint64_t*>(dsm) : gkeys + pl.keys_off;
@@ -276,7 +429,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     const uint32_t A = s.cls_aoff[c + 1] - s.cls_aoff[c];
     const uint32_t W = (M + 31) / 32;
     const uint64_t nrow_words = (uint64_t)A * W;
-    if (threadIdx.x == 0) s_nk = 0;
+    if (threadIdx.x == 0) { s_nk = 0; s_sig = 0; }
     for (uint64_t i = threadIdx.x; i < nrow_words; i += blockDim.x) rows[i] = 0;
     __syncthreads();
 
@@ -331,6 +484,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         if (xh) {
             ux[ubase + xcarry + ex] = (uint32_t)(keys[k] >> 32);
             un[ubase + xcarry + ex] = 0;
+            atomicOr(&s_sig, 1ull << uhash((uint32_t)(keys[k] >> 32)));
         }
         xcarry += tot;
     }
@@ -345,6 +499,22 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         // run index of position k = (#X heads at or before k) - 1
         if (ph) atomicAdd(un + ubase + xcarry + ex + (xh ? 1u : 0u) - 1u, 1u);
         xcarry += tot;
+    }
+
+    __syncthreads();
+    // per member: #{X ≠ c : U[c][X] == 1} into its method record (the sweep's cbo_origin_after)
+    for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) {
+        MethRec* r = recs + mb + i;
+        const uint32_t hdr = r->hdr;
+        if (hdr & kRecOverflow) continue;
+        uint32_t removed = 0;
+        for (uint32_t k = 0; k < rec_n(hdr); ++k) {
+            const uint32_t X = r->ent[k] >> 8;
+            if (X == c) continue;
+            const int at = urow_find(ux, ubase, nx, X);
+            removed += (at >= 0 && un[ubase + at] == 1u);
+        }
+        r->hdr = hdr | (removed << kRecRemovedShift) | kRecRemovedValid;
     }
 
     // phase 3: LCOM-CK via per-attribute member bitmaps (rows[a] = methods using a)
@@ -372,7 +542,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         const uint64_t pairs = (uint64_t)M * (M - 1) / 2;
         const uint64_t P = pairs - Q;
         ClassRec r;
-        r.A = A; r.M = M; r.H = (uint32_t)H; r.cbo = nx; r.ubase = ubase; r.pad = 0; r.lcom = l;
+        r.A = A; r.M = M; r.H = (uint32_t)H; r.cbo = nx; r.ubase = ubase; r.pad = 0; r.sig = s_sig;
         rec[c] = r;
         lcom_out[c] = l;
         ck_out[c] = P > Q ? P - Q : 0;
@@ -398,24 +568,32 @@ void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list,
     if (!s.C) return;
     k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, kind, large_list, n_large, max_deg, foreign);
 }
-void launch_attr_local(const DevModel& s, uint32_t* attr_local, cudaStream_t st) {
-    if (!s.A) return;
-    const uint32_t blocks = std::min<uint32_t>((s.A + 255) / 256, 148 * 16);
-    k_attr_local<<<blocks, 256, 0, st>>>(s, attr_local);
+void launch_layout(const DevModel& s, uint32_t* inv, uint32_t* attr_local, cudaStream_t st) {
+    const uint32_t n = std::max(s.M, s.A);
+    if (!n) return;
+    const uint32_t blocks = std::min<uint32_t>((n + 255) / 256, 148 * 16);
+    k_layout<<<blocks, 256, 0, st>>>(s, inv, attr_local);
 }
-void launch_class_small(const DevModel& s, const uint8_t* kind, const uint32_t* attr_local, ClassRec* rec,
-                        double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,
-                        uint32_t* ucursor, cudaStream_t st) {
+void launch_method(const DevModel& s, uint32_t maxdeg, const uint32_t* inv, const uint32_t* attr_local,
+                   MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner, cudaStream_t st) {
+    if (!s.M) return;
+    const uint32_t blocks = (s.M + 255) / 256;
+    if (maxdeg <= 8) k_method<8><<<blocks, 256, 0, st>>>(s, inv, attr_local, recs, own_mask, pos_owner);
+    else k_method<16><<<blocks, 256, 0, st>>>(s, inv, attr_local, recs, own_mask, pos_owner);
+}
+void launch_class_small(const DevModel& s, const uint8_t* kind, const uint32_t* attr_local, MethRec* recs,
+                        const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo,
+                        uint32_t* ux, uint32_t* un, uint32_t* ucursor, cudaStream_t st) {
     if (!s.C) return;
     k_class_small<<<(s.C + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(
-        s, kind, attr_local, rec, lcom, ck, cbo, ux, un, ucursor);
+        s, kind, attr_local, recs, own_mask, rec, lcom, ck, cbo, ux, un, ucursor);
 }
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
-                        uint32_t smem_bytes, const uint32_t* attr_local, ClassRec* rec, double* lcom,
+                        uint32_t smem_bytes, const uint32_t* attr_local, MethRec* recs, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
                         uint64_t* gkeys, uint32_t* grows, cudaStream_t st) {
     if (!n_large) return;
-    k_class_large<<<n_large, kLargeThreads, smem_bytes, st>>>(s, large_list, plan, attr_local, rec, lcom, ck,
+    k_class_large<<<n_large, kLargeThreads, smem_bytes, st>>>(s, large_list, plan, attr_local, recs, rec, lcom, ck,
                                                               cbo, ux, un, ucursor, gkeys, grows);
 }
 cudaError_t set_class_large_smem(uint32_t bytes) {

@@ -91,9 +91,11 @@ struct StreamEnum {
 };
 
 struct Origin {
-    double lo_b, lo_a;
+    ClassRec ro;
+    double lo_b, lo_a;   // exact doubles (always filled; cheap: once per method)
     uint32_t co_b, co_a;
     bool odeg;
+    bool coh_ok;         // lcom_origin_after < lcom_origin_before
 };
 
 struct Dest {
@@ -102,24 +104,49 @@ struct Dest {
     bool ddeg;
 };
 
+constexpr uint64_t kExact53 = 1ull << 53;
+
+// lcom(A, M−1, H−ho) < lcom(A, M, H) as the reference compares the doubles
+// (suggest.hpp:189-192). Exact-rational pre-test: the rounded map q -> lcom is
+// monotone, so q_after ≤ q_before already decides "false" without division.
+__device__ __forceinline__ Origin make_origin(const ClassRec& ro, uint32_t ho, uint32_t removed) {
+    Origin g;
+    g.ro = ro;
+    g.lo_b = lcom_of(ro.A, ro.M, ro.H);
+    g.lo_a = lcom_of(ro.A, (uint64_t)ro.M - 1, (uint64_t)ro.H - ho);
+    g.coh_ok = g.lo_a < g.lo_b;
+    g.co_b = ro.cbo;
+    g.co_a = ro.cbo - removed;
+    g.odeg = ro.M <= 1 || ro.A == 0;  // origin_after.empty() || attrs empty (suggest.hpp:118-120)
+    return g;
+}
+
+// lcom(A_d, M_d+1, H_d+h) < lcom(A_d, M_d, H_d): integer pre-test h·M > H
+// (q_after > q_before), doubles only when it holds.
+__device__ __forceinline__ bool coh_dest(const ClassRec& rd, uint32_t h, double& ld_a) {
+    if (rd.A == 0 || rd.M == 0) return false;  // before is 0.0 (degenerate): nothing is < 0
+    const bool exact_denoms = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
+    if (exact_denoms && !((uint64_t)h * rd.M > rd.H)) return false;
+    ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + h);
+    return ld_a < lcom_of(rd.A, rd.M, rd.H);
+}
+
+// X ∈ U[d]? Bloom signature first (a clear bit proves absence), then the row.
+__device__ __forceinline__ bool in_urow(const ClassRec& rd, const uint32_t* __restrict__ ux, uint32_t X) {
+    if (!((rd.sig >> uhash(X)) & 1ull)) return false;
+    return urow_find(ux, rd.ubase, rd.cbo, X) >= 0;
+}
+
+// coupling predicate for destination d given co_a < co_b: cd_after <= cd_before
+// ⟺ every X ∈ used(u) \ {d} is already in U[d] (miss == 0).
 template <class E>
-__device__ __forceinline__ Origin eval_origin(const ClassRec& ro, const uint32_t* __restrict__ ux,
-                                              const uint32_t* __restrict__ un, const E& en, uint32_t o) {
-    Origin r;
-    const uint32_t ho = en.hits(o);
-    r.lo_b = ro.lcom;
-    r.lo_a = lcom_of(ro.A, (uint64_t)ro.M - 1, (uint64_t)ro.H - ho);
-    uint32_t removed = 0;
+__device__ __forceinline__ bool coup_dest(const ClassRec& rd, const uint32_t* __restrict__ ux, const E& en,
+                                          uint32_t d) {
+    bool ok = true;
     en.each([&](int, uint32_t X, uint32_t) {
-        if (X != o) {
-            const int pos = urow_find(ux, ro.ubase, ro.cbo, X);
-            if (pos >= 0 && __ldg(un + ro.ubase + pos) == 1u) ++removed;
-        }
+        if (ok && X != d && !in_urow(rd, ux, X)) ok = false;
     });
-    r.co_b = ro.cbo;
-    r.co_a = ro.cbo - removed;
-    r.odeg = ro.M <= 1 || ro.A == 0;  // origin_after.empty() || attrs empty (suggest.hpp:118-120)
-    return r;
+    return ok;
 }
 
 template <class E>
@@ -127,16 +154,72 @@ __device__ __forceinline__ Dest eval_dest(const ClassRec* __restrict__ rec, cons
                                           const E& en, uint32_t d, uint32_t hd) {
     const ClassRec rd = load_rec(rec, d);
     Dest r;
-    r.ld_b = rd.lcom;
+    r.ld_b = lcom_of(rd.A, rd.M, rd.H);
     r.ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
     uint32_t miss = 0;
     en.each([&](int, uint32_t X, uint32_t) {
-        if (X != d && urow_find(ux, rd.ubase, rd.cbo, X) < 0) ++miss;
+        if (X != d && !in_urow(rd, ux, X)) ++miss;
     });
     r.cd_b = rd.cbo;
     r.cd_a = rd.cbo + miss;
     r.ddeg = rd.A == 0;
     return r;
+}
+
+// #{X ∈ used(u) \ {o} : U[o][X] == 1} from the rows (methods whose record
+// could not carry it)
+template <class E>
+__device__ __forceinline__ uint32_t removed_count(const ClassRec& ro, const uint32_t* __restrict__ ux,
+                                                  const uint32_t* __restrict__ un, const E& en, uint32_t o) {
+    uint32_t removed = 0;
+    en.each([&](int, uint32_t X, uint32_t) {
+        if (X != o) {
+            const int pos = urow_find(ux, ro.ubase, ro.cbo, X);
+            if (pos >= 0 && __ldg(un + ro.ubase + pos) == 1u) ++removed;
+        }
+    });
+    return removed;
+}
+
+// Both predicates and keys of one candidate (the shared core of the modes).
+template <class E>
+__device__ __forceinline__ void score(const SweepArgs& a, const E& en, const Origin& org, uint32_t d, uint32_t hd,
+                                      bool& pcoh, double& kcoh, bool& pcoup, uint32_t& kcoup) {
+    pcoh = pcoup = false;
+    if (!org.coh_ok && org.co_a >= org.co_b) return;  // neither criterion can pass
+    const ClassRec rd = load_rec(a.rec, d);
+    double ld_a;
+    if (org.coh_ok && coh_dest(rd, hd, ld_a)) {
+        pcoh = true;
+        kcoh = __dadd_rn(org.lo_a, ld_a);  // lcom_key, suggest.hpp:194-196
+    }
+    if (org.co_a < org.co_b && coup_dest(rd, a.ux, en, d)) {
+        pcoup = true;
+        kcoup = rd.cbo;  // cbo_dest_after == cbo_dest_before when it passes
+    }
+}
+
+// the next passing (key, index) strictly above (pk, pi) in lexicographic
+// order for one criterion (top-k extension; k ≤ 8 rounds)
+template <class E>
+__device__ __forceinline__ int select_next(const SweepArgs& a, const E& en, uint32_t o, const Origin& org,
+                                           bool coh, bool have_prev, double pk, int pi, double& out_key) {
+    int best = -1;
+    double bk = 0.0;
+    en.each([&](int k, uint32_t d, uint32_t hd) {
+        if (d == o) return;
+        bool pc, pp;
+        double kc = 0.0;
+        uint32_t kp = 0;
+        score(a, en, org, d, hd, pc, kc, pp, kp);
+        const bool pass = coh ? pc : pp;
+        const double key = coh ? kc : (double)kp;
+        if (!pass) return;
+        if (have_prev && !(key > pk || (key == pk && k > pi))) return;
+        if (best < 0 || key < bk) { best = k; bk = key; }
+    });
+    out_key = bk;
+    return best;
 }
 
 struct MethodResult {
@@ -146,34 +229,6 @@ struct MethodResult {
     uint32_t bd_coh, bd_coup;             // best-only mode
     unsigned long long m_coh, m_coup;     // top-k / all mode (bits over list index)
 };
-
-// k-th smallest passing (key, index) for one criterion, found by selection:
-// the next (key, idx) strictly above (pk, pi) in lexicographic order. Used by
-// the top-k extension only; keys are recomputed (k ≤ 8 rounds).
-template <class E>
-__device__ __forceinline__ int select_next(const SweepArgs& a, const E& en, uint32_t o, const Origin& org,
-                                           bool coh, bool have_prev, double pk, int pi, double& out_key) {
-    int best = -1;
-    double bk = 0.0;
-    en.each([&](int k, uint32_t d, uint32_t hd) {
-        if (d == o) return;
-        const Dest dv = eval_dest(a.rec, a.ux, en, d, hd);
-        bool pass;
-        double key;
-        if (coh) {
-            pass = org.lo_a < org.lo_b && dv.ld_a < dv.ld_b;
-            key = __dadd_rn(org.lo_a, dv.ld_a);
-        } else {
-            pass = org.co_a < org.co_b && dv.cd_a <= dv.cd_b;
-            key = (double)dv.cd_a;
-        }
-        if (!pass) return;
-        if (have_prev && !(key > pk || (key == pk && k > pi))) return;
-        if (best < 0 || key < bk) { best = k; bk = key; }
-    });
-    out_key = bk;
-    return best;
-}
 
 template <class E>
 __device__ __forceinline__ MethodResult evaluate(const SweepArgs& a, const E& en, uint32_t o,
@@ -189,13 +244,13 @@ __device__ __forceinline__ MethodResult evaluate(const SweepArgs& a, const E& en
     en.each([&](int k, uint32_t d, uint32_t hd) {
         if (d == o) return;
         ++cands;
-        const Dest dv = eval_dest(a.rec, a.ux, en, d, hd);
-        const bool pcoh = org.lo_a < org.lo_b && dv.ld_a < dv.ld_b;    // suggest.hpp:189-192
-        const bool pcoup = org.co_a < org.co_b && dv.cd_a <= dv.cd_b;  // :285-287
-        const double kc = __dadd_rn(org.lo_a, dv.ld_a);                // :194-196
-        // argmin over (key, d), d ascending, strict < : lowest d wins ties (:180-184)
+        bool pcoh, pcoup;
+        double kc = 0.0;
+        uint32_t kp = 0;
+        score(a, en, org, d, hd, pcoh, kc, pcoup, kp);
+        // argmin over (key, d), d ascending, strict < : lowest d wins ties (suggest.hpp:180-184)
         if (pcoh && (r.bd_coh == kNone || kc < best_coh)) { r.bd_coh = d; best_coh = kc; }
-        if (pcoup && (r.bd_coup == kNone || dv.cd_a < best_coup)) { r.bd_coup = d; best_coup = dv.cd_a; }
+        if (pcoup && (r.bd_coup == kNone || kp < best_coup)) { r.bd_coup = d; best_coup = kp; }
         if (a.mode == 2 && k < 64) {
             if (pcoh) r.m_coh |= 1ull << k;
             if (pcoup) r.m_coup |= 1ull << k;
@@ -285,6 +340,16 @@ __device__ __forceinline__ void emit(const SweepArgs& a, const E& en, uint32_t p
     });
 }
 
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -294,13 +359,84 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
     return v;
 }
 
+// Fills `ren` (shared-memory list) or `sen` (streaming) with method p's used
+// list and returns the origin-side values. Record path when the method pass
+// could pack the list; CSR otherwise.
 template <int K>
-__global__ void __launch_bounds__(kSweepTile) k_sweep(SweepArgs a) {
+__device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, uint32_t p, uint32_t o,
+                                            SmemEnum& ren, StreamEnum& sen, Origin& org) {
+    const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
+    const uint4 r0 = rp[0], r1 = rp[1];
+    const ClassRec ro = load_rec(a.rec, o);
+    if (!(r0.x & kRecOverflow)) {
+        const uint32_t ent[kRecMaxEnt] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        const uint32_t n = rec_n(r0.x);
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k)
+            if (k < (int)n) { ren.X[k * kSweepTile] = ent[k] >> 8; ren.H[k * kSweepTile] = ent[k] & 0xffu; }
+        ren.n = (int)n;
+        const uint32_t removed = (r0.x & kRecRemovedValid) ? rec_removed(r0.x)
+                                                            : removed_count(ro, a.ux, a.un, ren, o);
+        org = make_origin(ro, rec_hown(r0.x), removed);
+        return true;
+    }
+    const uint32_t deg = (__ldg(a.s.call_off + p + 1) - __ldg(a.s.call_off + p)) +
+                         (__ldg(a.s.acc_off + p + 1) - __ldg(a.s.acc_off + p));
+    if (deg <= (uint32_t)K) {
+        ren.build(a.s, p);
+        org = make_origin(ro, ren.hits(o), removed_count(ro, a.ux, a.un, ren, o));
+        return true;
+    }
+    sen.S.init(a.s, p);
+    org = make_origin(ro, sen.hits(o), removed_count(ro, a.ux, a.un, sen, o));
+    return false;
+}
+
+// Pass 1: score every candidate of every method (ungated, both criteria) and
+// keep the per-method best / top-k / all-passing destinations. One thread per
+// method, no block barriers, independent of the thresholds (so it overlaps
+// the threshold kernel on another stream).
+template <int K>
+__global__ void __launch_bounds__(kSweepTile, 2) k_score(SweepArgs a) {
+    __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];  // K >= kRecMaxEnt
+    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
+    const bool valid = pos < a.pos_end;
+    uint32_t cands = 0;
+    if (valid) {
+        const uint32_t p = __ldg(a.s.cls_methods + pos);
+        const uint32_t o = __ldg(a.pos_owner + pos);
+        SmemEnum ren;
+        ren.X = s_X + threadIdx.x;
+        ren.H = s_H + threadIdx.x;
+        ren.n = 0;
+        StreamEnum sen;
+        Origin org;
+        MethodResult r;
+        if (load_method<K>(a, (uint32_t)pos, p, o, ren, sen, org)) r = evaluate(a, ren, o, org, true, true);
+        else r = evaluate(a, sen, o, org, true, true);
+        cands = r.cands;
+        uint4 out;
+        if (a.mode == 0) out = make_uint4(r.bd_coh, r.bd_coup, r.cands, 0);
+        else {
+            if ((r.m_coh | r.m_coup) >> 32) atomicOr(a.err, 2u);
+            out = make_uint4((uint32_t)r.m_coh, (uint32_t)r.m_coup, r.cands, 0);
+        }
+        a.res[pos] = out;
+    }
+    const uint32_t wc = __reduce_add_sync(0xffffffffu, cands);
+    if ((threadIdx.x & 31) == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
+}
+
+// Pass 2: apply the class gates (suggest.hpp:246, :273), merge the criteria
+// (union / intersection, :315-341), and write the records in (origin,
+// method, destination) order at offsets from a decoupled look-back scan.
+template <int K>
+__global__ void __launch_bounds__(kSweepTile) k_emit(SweepArgs a) {
     __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_warp[kSweepTile / 32];
     __shared__ unsigned long long s_excl;
-    __shared__ unsigned long long s_red[3][kSweepTile / 32];
+    __shared__ unsigned long long s_red[2][kSweepTile / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
     __syncthreads();
@@ -311,39 +447,41 @@ __global__ void __launch_bounds__(kSweepTile) k_sweep(SweepArgs a) {
     double thr_l = a.thr_lcom, thr_c = a.thr_cbo;
     if (a.thr_device) { thr_l = a.dthr->lcom; thr_c = a.dthr->cbo; }
 
-    uint32_t p = 0, o = 0;
-    bool fast = true;
-    SmemEnum ren;
-    ren.X = s_X + threadIdx.x;
-    ren.H = s_H + threadIdx.x;
-    ren.n = 0;
-    StreamEnum sen;
-    Origin org{};
+    const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
+    const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
+    uint32_t o = 0, count = 0, gated = 0;
     MethodResult res{};
     if (valid) {
-        p = __ldg(a.s.cls_methods + pos);
-        o = __ldg(a.s.method_owner + p);
-        const uint32_t deg = (__ldg(a.s.call_off + p + 1) - __ldg(a.s.call_off + p)) +
-                             (__ldg(a.s.acc_off + p + 1) - __ldg(a.s.acc_off + p));
-        fast = deg <= (uint32_t)K;
-        const ClassRec ro = load_rec(a.rec, o);
-        // gates: lcom[c] > thr.lcom (suggest.hpp:246), (double)cbo[c] > thr.cbo (:273)
-        const bool gcoh = (a.crit & MM_CRIT_COHESION) && ro.lcom > thr_l;
-        const bool gcoup = (a.crit & MM_CRIT_COUPLING) && (double)ro.cbo > thr_c;
-        if (fast) {
-            ren.build(a.s, p);
-            org = eval_origin(ro, a.ux, a.un, ren, o);
-            res = evaluate(a, ren, o, org, gcoh, gcoup);
+        const uint4 r = a.res[pos];
+        o = __ldg(a.pos_owner + pos);
+        const bool gcoh = (a.crit & MM_CRIT_COHESION) && __ldg(a.lcom + o) > thr_l;
+        const bool gcoup = (a.crit & MM_CRIT_COUPLING) && (double)__ldg(a.cbo + o) > thr_c;
+        gated = r.z * ((gcoh ? 1u : 0u) + (gcoup ? 1u : 0u));
+        if (a.mode == 0) {
+            res.bd_coh = gcoh ? r.x : kNone;
+            res.bd_coup = gcoup ? r.y : kNone;
+            const bool same = res.bd_coh != kNone && res.bd_coh == res.bd_coup;
+            count = inter ? (same ? 1u : 0u)
+                          : (uint32_t)(res.bd_coh != kNone) + (uint32_t)(res.bd_coup != kNone) - (same ? 1u : 0u);
         } else {
-            sen.S.init(a.s, p);
-            org = eval_origin(ro, a.ux, a.un, sen, o);
-            res = evaluate(a, sen, o, org, gcoh, gcoup);
+            res.m_coh = gcoh ? r.x : 0u;
+            res.m_coup = gcoup ? r.y : 0u;
+            count = __popcll(inter ? (res.m_coh & res.m_coup) : (res.m_coh | res.m_coup));
         }
     }
 
     // tile-wide exclusive scan of record counts
-    const uint32_t inc = warp_incl_scan(res.count, lane);
+    const uint32_t inc = warp_incl_scan(count, lane);
     if (lane == 31) s_warp[warp] = inc;
+    {
+        unsigned long long g0 = gated, g1 = valid ? 1ull : 0ull;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            g0 += __shfl_down_sync(0xffffffffu, g0, d);
+            g1 += __shfl_down_sync(0xffffffffu, g1, d);
+        }
+        if (lane == 0) { s_red[0][warp] = g0; s_red[1][warp] = g1; }
+    }
     __syncthreads();
     uint32_t before = 0, agg = 0;
 #pragma unroll
@@ -351,54 +489,55 @@ __global__ void __launch_bounds__(kSweepTile) k_sweep(SweepArgs a) {
         if (w < warp) before += s_warp[w];
         agg += s_warp[w];
     }
-    const uint32_t texcl = before + inc - res.count;
+    const uint32_t texcl = before + inc - count;
 
-    // decoupled look-back for the tile's global offset
-    if (threadIdx.x == 0) {
+    // decoupled look-back: warp 0 inspects 32 predecessor tiles per step
+    // (relaxed gpu-scope loads; flag and value share one 64-bit word)
+    if (warp == 0) {
         unsigned long long excl = 0;
         if (tile == 0) {
-            __threadfence();
-            atomicExch(a.tile_state, kFlagPrefix | agg);
+            if (lane == 0) st_relaxed_u64(a.tile_state, kFlagPrefix | agg);
         } else {
-            __threadfence();
-            atomicExch(a.tile_state + tile, kFlagAgg | agg);
-            int j = (int)tile - 1;
+            if (lane == 0) st_relaxed_u64(a.tile_state + tile, kFlagAgg | agg);
+            int base = (int)tile - 1;
             while (true) {
-                const unsigned long long v = *reinterpret_cast<volatile unsigned long long*>(a.tile_state + j);
+                const int j = base - lane;
+                const unsigned long long v = j >= 0 ? ld_relaxed_u64(a.tile_state + j) : kFlagPrefix;
                 const unsigned long long f = v & ~kValMask;
-                if (f == 0) continue;
-                excl += v & kValMask;
-                if (f == kFlagPrefix) break;
-                --j;
-            }
-            __threadfence();
-            atomicExch(a.tile_state + tile, kFlagPrefix | (excl + agg));
-        }
-        s_excl = excl;
-    }
-    // stats (one atomic per tile per counter)
-    {
-        unsigned long long c0 = res.cands, c1 = res.gated, c2 = valid ? 1ull : 0ull;
+                const uint32_t bP = __ballot_sync(0xffffffffu, f == kFlagPrefix);
+                const uint32_t bZ = __ballot_sync(0xffffffffu, f == 0);
+                const int lim = bP ? __ffs(bP) - 1 : 31;
+                const uint32_t need = lim == 31 ? 0xffffffffu : ((2u << lim) - 1);
+                if (bZ & need) continue;
+                unsigned long long part = lane <= lim ? (v & kValMask) : 0ull;
 #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            c0 += __shfl_down_sync(0xffffffffu, c0, d);
-            c1 += __shfl_down_sync(0xffffffffu, c1, d);
-            c2 += __shfl_down_sync(0xffffffffu, c2, d);
+                for (int d = 16; d > 0; d >>= 1) part += __shfl_down_sync(0xffffffffu, part, d);
+                excl += __shfl_sync(0xffffffffu, part, 0);
+                if (bP) break;
+                base -= 32;
+            }
+            if (lane == 0) st_relaxed_u64(a.tile_state + tile, kFlagPrefix | (excl + agg));
         }
-        if (lane == 0) { s_red[0][warp] = c0; s_red[1][warp] = c1; s_red[2][warp] = c2; }
+        if (lane == 0) {
+            s_excl = excl;
+            unsigned long long t0 = 0, t1 = 0;
+            for (int w = 0; w < kSweepTile / 32; ++w) { t0 += s_red[0][w]; t1 += s_red[1][w]; }
+            atomicAdd(a.stats + 1, t0);
+            atomicAdd(a.stats + 2, (unsigned long long)agg);
+            atomicAdd(a.stats + 3, t1);
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long t0 = 0, t1 = 0, t2 = 0;
-        for (int w = 0; w < kSweepTile / 32; ++w) { t0 += s_red[0][w]; t1 += s_red[1][w]; t2 += s_red[2][w]; }
-        atomicAdd(a.stats + 0, t0);
-        atomicAdd(a.stats + 1, t1);
-        atomicAdd(a.stats + 2, (unsigned long long)agg);
-        atomicAdd(a.stats + 3, t2);
-    }
-    if (valid && res.count) {
+    if (valid && count) {
+        const uint32_t p = __ldg(a.s.cls_methods + pos);
+        SmemEnum ren;
+        ren.X = s_X + threadIdx.x;
+        ren.H = s_H + threadIdx.x;
+        ren.n = 0;
+        StreamEnum sen;
+        Origin org;
         const uint64_t at = s_excl + texcl;
-        if (fast) emit(a, ren, p, o, org, res, at);
+        if (load_method<K>(a, (uint32_t)pos, p, o, ren, sen, org)) emit(a, ren, p, o, org, res, at);
         else emit(a, sen, p, o, org, res, at);
     }
 }
@@ -410,7 +549,7 @@ __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const ui
     StreamEnum en;
     en.S.init(s, u);
     const ClassRec ro = load_rec(rec, o);
-    const Origin org = eval_origin(ro, ux, un, en, o);
+    const Origin org = make_origin(ro, en.hits(o), removed_count(ro, ux, un, en, o));
     const Dest dv = eval_dest(rec, ux, en, d, en.hits(d));
     mm_whatif w;
     w.lcom_origin_before = org.lo_b;
@@ -429,10 +568,16 @@ __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const ui
 
 }  // namespace
 
-void launch_sweep(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
+void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     if (!n_tiles) return;
-    if (a.maxdeg_fast <= 8) k_sweep<8><<<n_tiles, kSweepTile, 0, st>>>(a);
-    else k_sweep<16><<<n_tiles, kSweepTile, 0, st>>>(a);
+    if (a.maxdeg_fast <= 8) k_score<8><<<n_tiles, kSweepTile, 0, st>>>(a);
+    else k_score<16><<<n_tiles, kSweepTile, 0, st>>>(a);
+}
+
+void launch_emit(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
+    if (!n_tiles) return;
+    if (a.maxdeg_fast <= 8) k_emit<8><<<n_tiles, kSweepTile, 0, st>>>(a);
+    else k_emit<16><<<n_tiles, kSweepTile, 0, st>>>(a);
 }
 
 void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un, uint32_t u,

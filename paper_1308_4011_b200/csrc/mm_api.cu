@@ -68,6 +68,9 @@ struct mm_ctx {
     int device = 0;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;       // threshold means run here, overlapping the candidate scoring
+    cudaEvent_t ev_metrics = nullptr;  // class tables ready (main -> side)
+    cudaEvent_t ev_thr = nullptr;      // threshold means ready (side -> main)
     std::string err;
     bool profiling = false;
     std::vector<Pending> pending;
@@ -89,7 +92,11 @@ struct mm_ctx {
     DBuf<uint64_t> gkeys;
     DBuf<uint32_t> grows;
     // derived
-    DBuf<uint32_t> attr_local, cbo, ux, un;
+    DBuf<uint32_t> attr_local, inv, cbo, ux, un;
+    DBuf<MethRec> recs;
+    DBuf<uint64_t> own_mask;
+    DBuf<uint32_t> pos_owner;
+    DBuf<uint4> res;
     DBuf<ClassRec> rec;
     DBuf<double> lcom;
     DBuf<uint64_t> ck;
@@ -132,21 +139,33 @@ mm_status cuda_fail(mm_ctx* ctx, cudaError_t e, const char* where) {
     } while (0)
 
 template <class F>
-mm_status run(mm_ctx* ctx, const char* name, F&& launch) {
+mm_status run_on(mm_ctx* ctx, cudaStream_t st, const char* name, F&& launch) {
     Pending pe;
     if (ctx->profiling) {
         cudaEventCreate(&pe.a);
         cudaEventCreate(&pe.b);
-        cudaEventRecord(pe.a, ctx->stream);
+        cudaEventRecord(pe.a, st);
     }
     launch();
     const cudaError_t e = cudaGetLastError();
     if (ctx->profiling) {
-        cudaEventRecord(pe.b, ctx->stream);
+        cudaEventRecord(pe.b, st);
         pe.name = name;
         ctx->pending.push_back(pe);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, name);
+    return MM_OK;
+}
+
+template <class F>
+mm_status run(mm_ctx* ctx, const char* name, F&& launch) {
+    return run_on(ctx, ctx->stream, name, launch);
+}
+
+// main stream waits for the side stream's threshold means
+mm_status join_thresholds(mm_ctx* ctx) {
+    const cudaError_t e = cudaStreamWaitEvent(ctx->stream, ctx->ev_thr, 0);
+    if (e != cudaSuccess) return fail(ctx, MM_E_CUDA, std::string("join_thresholds: ") + cudaGetErrorString(e));
     return MM_OK;
 }
 
@@ -167,8 +186,12 @@ void resolve_pending(mm_ctx* ctx) {
 void free_model(mm_ctx* c) {
     for (DBuf<uint32_t>* b : {&c->method_owner, &c->attribute_owner, &c->cls_moff, &c->cls_methods, &c->cls_aoff,
                               &c->cls_attrs, &c->call_off, &c->call_tgt, &c->acc_off, &c->acc_tgt,
-                              &c->large_list, &c->foreign, &c->grows, &c->attr_local, &c->cbo, &c->ux, &c->un})
+                              &c->large_list, &c->foreign, &c->grows, &c->attr_local, &c->inv, &c->cbo, &c->ux,
+                              &c->un})
         b->release();
+    c->recs.release();
+    c->own_mask.release();
+    c->pos_owner.release();
     c->kind.release();
     c->plans.release();
     c->gkeys.release();
@@ -223,6 +246,10 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     ctx->device = device;
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_metrics, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_thr, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ctx->ev_thr, ctx->side) != cudaSuccess ||
         ctx->ctl.alloc(1) != cudaSuccess || ctx->whatif.alloc(1) != cudaSuccess) {
         delete ctx;
         return MM_E_CUDA;
@@ -236,6 +263,7 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->side);
     resolve_pending(ctx);
     free_model(ctx);
     ctx->ctl.release();
@@ -243,7 +271,11 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     ctx->thr_scratch.release();
     ctx->tile_state.release();
     ctx->out.release();
+    ctx->res.release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->ev_metrics) cudaEventDestroy(ctx->ev_metrics);
+    if (ctx->ev_thr) cudaEventDestroy(ctx->ev_thr);
     delete ctx;
 }
 
@@ -255,6 +287,7 @@ mm_status mm_ctx_set_stream(mm_ctx* ctx, void* s) {
 
 mm_status mm_ctx_synchronize(mm_ctx* ctx) {
     if (!ctx) return MM_E_ARG;
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->side));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return MM_OK;
 }
@@ -300,6 +333,8 @@ uint64_t mm_system_bytes(const mm_system* s) {
 mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     if (!ctx || !s) return MM_E_ARG;
     if (mm_status st = set_device(ctx)) return st;
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->side));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     free_model(ctx);
     if (!s->call_off || !s->acc_off || !s->class_method_off || !s->class_attr_off)
         return fail(ctx, MM_E_ARG, "mm_upload: NULL offsets");
@@ -397,6 +432,10 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     }
     // derived tables
     MM_CUDA(ctx, ctx->attr_local.alloc(A ? A : 1));
+    MM_CUDA(ctx, ctx->inv.alloc(M ? M : 1));
+    MM_CUDA(ctx, ctx->recs.alloc(M ? M : 1));
+    MM_CUDA(ctx, ctx->own_mask.alloc(M ? M : 1));
+    MM_CUDA(ctx, ctx->pos_owner.alloc(M ? M : 1));
     MM_CUDA(ctx, ctx->rec.alloc(C ? C : 1));
     MM_CUDA(ctx, ctx->lcom.alloc(C ? C : 1));
     MM_CUDA(ctx, ctx->ck.alloc(C ? C : 1));
@@ -417,28 +456,38 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
     Ctl* ctl = ctx->ctl.p;
     MM_CUDA(ctx, cudaMemsetAsync(&ctl->ucursor, 0, sizeof(uint32_t), ctx->stream));
     const DevModel dm = ctx->dev();
-    mm_status st = run(ctx, "attr_local", [&] { launch_attr_local(dm, ctx->attr_local.p, ctx->stream); });
+    mm_status st = run(ctx, "layout", [&] { launch_layout(dm, ctx->inv.p, ctx->attr_local.p, ctx->stream); });
+    if (st) return st;
+    st = run(ctx, "method", [&] {
+        launch_method(dm, ctx->max_deg, ctx->inv.p, ctx->attr_local.p, ctx->recs.p, ctx->own_mask.p,
+                      ctx->pos_owner.p, ctx->stream);
+    });
     if (st) return st;
     st = run(ctx, "class_small", [&] {
-        launch_class_small(dm, ctx->kind.p, ctx->attr_local.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p,
-                           ctx->ux.p, ctx->un.p, &ctl->ucursor, ctx->stream);
+        launch_class_small(dm, ctx->kind.p, ctx->attr_local.p, ctx->recs.p, ctx->own_mask.p, ctx->rec.p, ctx->lcom.p,
+                           ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p, &ctl->ucursor, ctx->stream);
     });
     if (st) return st;
     if (ctx->n_large) {
         st = run(ctx, "class_large", [&] {
             launch_class_large(dm, ctx->n_large, ctx->large_list.p, ctx->plans.p, ctx->large_smem,
-                               ctx->attr_local.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
+                               ctx->attr_local.p, ctx->recs.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
                                ctx->un.p, &ctl->ucursor, ctx->gkeys.p, ctx->grows.p, ctx->stream);
         });
         if (st) return st;
     }
+    // threshold means on the side stream: they overlap the candidate scoring,
+    // only the emission pass of the sweep waits for them
+    MM_CUDA(ctx, cudaEventRecord(ctx->ev_metrics, ctx->stream));
+    MM_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_metrics, 0));
     cudaError_t te = cudaSuccess;
-    st = run(ctx, "thresholds", [&] {
+    st = run_on(ctx, ctx->side, "thresholds", [&] {
         te = launch_thresholds(ctx->lcom.p, ctx->cbo.p, ctx->C, &ctl->thr, ctx->thr_scratch.p, ctx->thr_scratch.n,
-                               ctx->stream);
+                               ctx->side);
     });
     if (st) return st;
     if (te != cudaSuccess) return cuda_fail(ctx, te, "thresholds");
+    MM_CUDA(ctx, cudaEventRecord(ctx->ev_thr, ctx->side));
     ctx->metrics_valid = true;
     ctx->sweep_valid = false;
     return MM_OK;
@@ -479,6 +528,7 @@ mm_status mm_cbo(mm_ctx* ctx, uint32_t cls, uint32_t* out) {
 mm_status mm_compute_thresholds(mm_ctx* ctx, const mm_overrides* ov, mm_thresholds* out) {
     if (!ctx || !out) return MM_E_ARG;
     if (mm_status st = ensure_metrics(ctx)) return st;
+    if (mm_status st = join_thresholds(ctx)) return st;
     DevThresholds t{};
     MM_CUDA(ctx, cudaMemcpyAsync(&t, &ctx->ctl.p->thr, sizeof t, cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -531,6 +581,7 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     MM_CUDA(ctx, ctx->out.ensure(cap));
     const uint32_t n_tiles = (uint32_t)((npos + kSweepTile - 1) / kSweepTile);
     MM_CUDA(ctx, ctx->tile_state.ensure(n_tiles ? n_tiles : 1));
+    MM_CUDA(ctx, ctx->res.ensure(npos ? npos : 1));
     Ctl* ctl = ctx->ctl.p;
     if (n_tiles) MM_CUDA(ctx, cudaMemsetAsync(ctx->tile_state.p, 0, 8ull * n_tiles, ctx->stream));
     // tile_counter, err, pad, stats
@@ -539,6 +590,11 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     SweepArgs a{};
     a.s = ctx->dev();
     a.rec = ctx->rec.p;
+    a.recs = ctx->recs.p;
+    a.pos_owner = ctx->pos_owner.p;
+    a.lcom = ctx->lcom.p;
+    a.cbo = ctx->cbo.p;
+    a.res = ctx->res.p - pb;  // indexed by absolute position
     a.ux = ctx->ux.p;
     a.un = ctx->un.p;
     a.dthr = &ctl->thr;
@@ -557,7 +613,11 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     a.tile_counter = &ctl->tile_counter;
     a.stats = ctl->stats;
     a.err = &ctl->err;
-    mm_status st = run(ctx, "sweep", [&] { launch_sweep(a, n_tiles, ctx->stream); });
+    mm_status st = run(ctx, "score", [&] { launch_score(a, n_tiles, ctx->stream); });
+    if (st) return st;
+    if (a.thr_device)
+        if (mm_status s2 = join_thresholds(ctx)) return s2;
+    st = run(ctx, "emit", [&] { launch_emit(a, n_tiles, ctx->stream); });
     if (st) return st;
     ctx->sweep_valid = true;
     if (n_out) {
@@ -575,7 +635,7 @@ mm_status mm_sweep_stats_get(mm_ctx* ctx, mm_sweep_stats* out) {
     MM_CUDA(ctx, cudaMemcpyAsync(&h, ctx->ctl.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     if (h.err & 2u)
-        return fail(ctx, MM_E_UNSUPPORTED, "a method uses more than 64 classes (all/top-k mode limit)");
+        return fail(ctx, MM_E_UNSUPPORTED, "a method uses more than 32 classes (all/top-k mode limit)");
     out->candidates = h.stats[0];
     out->gated_whatifs = h.stats[1];
     out->suggestions = h.stats[2];
@@ -615,6 +675,7 @@ mm_status mm_sequential_mean(mm_ctx* ctx, const double* values, uint64_t n, doub
     DBuf<double> d;
     MM_CUDA(ctx, d.alloc(n ? n : 1));
     if (n) MM_CUDA(ctx, cudaMemcpyAsync(d.p, values, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+    if (mm_status st2 = join_thresholds(ctx)) return st2;
     DevThresholds* dt = &ctx->ctl.p->thr;
     DBuf<char> scratch;
     MM_CUDA(ctx, scratch.alloc(thresholds_scratch_bytes((uint32_t)n)));

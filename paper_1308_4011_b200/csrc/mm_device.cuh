@@ -45,8 +45,31 @@ struct __align__(32) ClassRec {
     uint32_t cbo;    // |U row|
     uint32_t ubase;  // U row start in ux/un
     uint32_t pad;
-    double lcom;     // lcom(A, M, H)
+    uint64_t sig;    // 64-bit Bloom signature of the U row (bit uhash(X)): a clear bit proves X ∉ U[c]
 };
+
+__device__ __forceinline__ uint32_t uhash(uint32_t x) {  // bit index 0..63
+    return (x * 0x9E3779B1u) >> 26;
+}
+
+// Compact per-method record, stored at the method's class-order position by
+// the method pass (one 32-byte sector): the sorted used list (owner classes
+// of calls ∪ accesses, own class included) packed as X << 8 | h, with h the
+// number of accesses owned by X.
+struct __align__(32) MethRec {
+    uint32_t hdr;      // see kRec* below
+    uint32_t ent[7];
+};
+constexpr uint32_t kRecN = 0xfu;            // bits 0-3   number of entries (≤ 7)
+constexpr int kRecHownShift = 8;            // bits 8-15  |acc(p) ∩ attrs(own)|
+constexpr int kRecRemovedShift = 16;        // bits 16-23 #{X ≠ own : U[own][X] == 1} (class pass)
+constexpr uint32_t kRecOverflow = 1u << 24; // list not representable: consumers use the CSR
+constexpr uint32_t kRecRemovedValid = 1u << 25;
+constexpr int kRecMaxEnt = 7;
+
+__device__ __forceinline__ uint32_t rec_n(uint32_t hdr) { return hdr & kRecN; }
+__device__ __forceinline__ uint32_t rec_hown(uint32_t hdr) { return (hdr >> kRecHownShift) & 0xffu; }
+__device__ __forceinline__ uint32_t rec_removed(uint32_t hdr) { return (hdr >> kRecRemovedShift) & 0xffu; }
 static_assert(sizeof(ClassRec) == 32, "ClassRec must be one 32-byte sector");
 
 struct DevThresholds {
@@ -165,9 +188,23 @@ struct StreamUsed {
     }
 };
 
-// Position of X in U row [base, base+len) (sorted), or -1.
+// Position of X in U row [base, base+len) (sorted), or -1. Short rows are
+// scanned with independent loads (one memory round trip per 8 entries instead
+// of one per binary-search probe); long rows are binary searched.
 __device__ __forceinline__ int urow_find(const uint32_t* __restrict__ ux, uint32_t base, uint32_t len,
                                          uint32_t X) {
+    if (len <= 48) {
+        for (uint32_t k0 = 0; k0 < len; k0 += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = (k0 + j < len) ? __ldg(ux + base + k0 + j) : kNone;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (v[j] == X) return (int)(k0 + j);
+            if (v[7] > X) return -1;  // sorted: passed the slot
+        }
+        return -1;
+    }
     uint32_t lo = 0, hi = len;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
@@ -184,7 +221,7 @@ __device__ __forceinline__ ClassRec load_rec(const ClassRec* __restrict__ rec, u
     ClassRec r;
     r.A = a.x; r.M = a.y; r.H = a.z; r.cbo = a.w;
     r.ubase = b.x; r.pad = b.y;
-    r.lcom = __hiloint2double(static_cast<int>(b.w), static_cast<int>(b.z));
+    r.sig = ((uint64_t)b.w << 32) | b.z;
     return r;
 }
 
