@@ -49,18 +49,27 @@ __global__ void k_validate_offsets(const uint32_t* __restrict__ off, uint64_t n_
 __global__ void k_plan_classes(DevModel s, uint8_t* __restrict__ kind, uint32_t* __restrict__ large_list,
                                uint32_t* __restrict__ n_large, uint32_t* __restrict__ max_deg,
                                uint32_t* __restrict__ foreign) {
+    // every index is bounds-checked: this runs before the validation result is known
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= s.C) return;
-    const uint32_t mb = s.cls_moff[c], me = s.cls_moff[c + 1];
+    const uint32_t mb = min(s.cls_moff[c], s.M), me = min(max(s.cls_moff[c + 1], mb), s.M);
     const uint32_t A = s.cls_aoff[c + 1] - s.cls_aoff[c];
+    const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
     uint32_t mdeg = 0, fr = 0;
     for (uint32_t i = mb; i < me; ++i) {
         const uint32_t p = s.cls_methods[i];
-        const uint32_t cb = s.call_off[p], ce = s.call_off[p + 1];
-        const uint32_t ab = s.acc_off[p], ae = s.acc_off[p + 1];
+        if (p >= s.M) continue;
+        const uint32_t cb = min(s.call_off[p], Ec), ce = min(max(s.call_off[p + 1], cb), Ec);
+        const uint32_t ab = min(s.acc_off[p], Ea), ae = min(max(s.acc_off[p + 1], ab), Ea);
         mdeg = max(mdeg, (ce - cb) + (ae - ab));
-        for (uint32_t e = cb; e < ce; ++e) fr += s.method_owner[s.call_tgt[e]] != c;
-        for (uint32_t e = ab; e < ae; ++e) fr += s.attribute_owner[s.acc_tgt[e]] != c;
+        for (uint32_t e = cb; e < ce; ++e) {
+            const uint32_t t = s.call_tgt[e];
+            fr += t >= s.M || s.method_owner[t] != c;
+        }
+        for (uint32_t e = ab; e < ae; ++e) {
+            const uint32_t t = s.acc_tgt[e];
+            fr += t >= s.A || s.attribute_owner[t] != c;
+        }
     }
     foreign[c] = fr;
     const bool small = (me - mb) <= kSmallMaxMembers && A <= kSmallMaxAttrs && mdeg <= kSmallMaxDeg;

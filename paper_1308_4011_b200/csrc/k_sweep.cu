@@ -546,6 +546,12 @@ __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const ui
                           const uint32_t* __restrict__ un, uint32_t u, uint32_t o, uint32_t d,
                           mm_whatif* __restrict__ out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (s.method_owner[u] != o) {  // not a member of the origin: invalid_argument (suggest.hpp:93-96)
+        mm_whatif w{};
+        w.pad[0] = 1;
+        *out = w;
+        return;
+    }
     StreamEnum en;
     en.S.init(s, u);
     const ClassRec ro = load_rec(rec, o);

@@ -81,7 +81,7 @@ struct mm_ctx {
     bool metrics_valid = false;
     uint32_t C = 0, M = 0, A = 0;
     uint64_t Ec = 0, Ea = 0;
-    std::vector<uint32_t> h_method_owner, h_cls_moff;
+    std::vector<uint32_t> h_cls_moff;
     DBuf<uint32_t> method_owner, attribute_owner, cls_moff, cls_methods, cls_aoff, cls_attrs, call_off, call_tgt,
         acc_off, acc_tgt;
     // plan
@@ -209,7 +209,7 @@ mm_status set_device(mm_ctx* ctx) {
 template <class T>
 mm_status upload_array(mm_ctx* ctx, DBuf<T>& d, const T* h, size_t n, const char* what) {
     if (n && !h) return fail(ctx, MM_E_ARG, std::string("mm_upload: NULL ") + what);
-    MM_CUDA(ctx, d.alloc(n));
+    MM_CUDA(ctx, d.ensure(n ? n : 1));
     if (n) MM_CUDA(ctx, cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
     return MM_OK;
 }
@@ -335,7 +335,8 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     if (mm_status st = set_device(ctx)) return st;
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->side));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    free_model(ctx);
+    // device buffers are reused across uploads (grown on demand, never shrunk)
+    ctx->have_model = ctx->metrics_valid = ctx->sweep_valid = false;
     if (!s->call_off || !s->acc_off || !s->class_method_off || !s->class_attr_off)
         return fail(ctx, MM_E_ARG, "mm_upload: NULL offsets");
     const uint32_t C = s->n_classes, M = s->n_methods, A = s->n_attributes;
@@ -351,7 +352,6 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     if (mm_status st = upload_array(ctx, ctx->call_tgt, s->call_tgt, Ec, "call_tgt")) return st;
     if (mm_status st = upload_array(ctx, ctx->acc_off, s->acc_off, M + 1ull, "acc_off")) return st;
     if (mm_status st = upload_array(ctx, ctx->acc_tgt, s->acc_tgt, Ea, "acc_tgt")) return st;
-    ctx->h_method_owner.assign(s->method_owner, s->method_owner + M);
     ctx->h_cls_moff.assign(s->class_method_off, s->class_method_off + C + 1);
 
     // device-side range validation: offsets first (totals come from the
@@ -372,26 +372,22 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         launch_validate_ids(ctx->acc_tgt.p, Ea, A, bad, ctx->stream);
     });
     if (st) return st;
-    Ctl h{};
-    MM_CUDA(ctx, cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
-    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    if (h.bad) {
-        free_model(ctx);
-        return fail(ctx, MM_E_ARG, (h.bad & 2u) ? "mm_upload: malformed offsets" : "mm_upload: id out of range");
-    }
 
-    // class plan: warp path vs CTA path, scratch for the CTA path
-    MM_CUDA(ctx, ctx->kind.alloc(C ? C : 1));
-    MM_CUDA(ctx, ctx->large_list.alloc(C ? C : 1));
-    MM_CUDA(ctx, ctx->foreign.alloc(C ? C : 1));
+    // class plan (bounds-checked, so it is safe on a model validation rejects):
+    // warp path vs CTA path, scratch for the CTA path. One sync for both.
+    MM_CUDA(ctx, ctx->kind.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->large_list.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->foreign.ensure(C ? C : 1));
     const DevModel dm = ctx->dev();
     st = run(ctx, "plan", [&] {
         launch_plan_classes(dm, ctx->kind.p, ctx->large_list.p, &ctl->n_large, &ctl->max_deg, ctx->foreign.p,
                             ctx->stream);
     });
     if (st) return st;
+    Ctl h{};
     MM_CUDA(ctx, cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h.bad) return fail(ctx, MM_E_ARG, (h.bad & 2u) ? "mm_upload: malformed offsets" : "mm_upload: id out of range");
     ctx->n_large = h.n_large;
     ctx->max_deg = h.max_deg;
     if (ctx->n_large) {
@@ -420,29 +416,28 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             else { pl.rows_off = roff; roff += Ac * ((Mc + 31) / 32); }
             smem_need = std::max(smem_need, used);
         }
-        MM_CUDA(ctx, ctx->large_list.alloc(ctx->n_large));
         MM_CUDA(ctx, cudaMemcpy(ctx->large_list.p, list.data(), 4ull * ctx->n_large, cudaMemcpyHostToDevice));
-        MM_CUDA(ctx, ctx->plans.alloc(ctx->n_large));
+        MM_CUDA(ctx, ctx->plans.ensure(ctx->n_large));
         MM_CUDA(ctx, cudaMemcpy(ctx->plans.p, plans.data(), sizeof(LargePlan) * ctx->n_large,
                                 cudaMemcpyHostToDevice));
-        MM_CUDA(ctx, ctx->gkeys.alloc(koff ? koff : 1));
-        MM_CUDA(ctx, ctx->grows.alloc(roff ? roff : 1));
+        MM_CUDA(ctx, ctx->gkeys.ensure(koff ? koff : 1));
+        MM_CUDA(ctx, ctx->grows.ensure(roff ? roff : 1));
         ctx->large_smem = (uint32_t)((smem_need + 15) & ~15ull);
         MM_CUDA(ctx, set_class_large_smem(ctx->large_smem));
     }
     // derived tables
-    MM_CUDA(ctx, ctx->attr_local.alloc(A ? A : 1));
-    MM_CUDA(ctx, ctx->inv.alloc(M ? M : 1));
-    MM_CUDA(ctx, ctx->recs.alloc(M ? M : 1));
-    MM_CUDA(ctx, ctx->own_mask.alloc(M ? M : 1));
-    MM_CUDA(ctx, ctx->pos_owner.alloc(M ? M : 1));
-    MM_CUDA(ctx, ctx->rec.alloc(C ? C : 1));
-    MM_CUDA(ctx, ctx->lcom.alloc(C ? C : 1));
-    MM_CUDA(ctx, ctx->ck.alloc(C ? C : 1));
-    MM_CUDA(ctx, ctx->cbo.alloc(C ? C : 1));
+    MM_CUDA(ctx, ctx->attr_local.ensure(A ? A : 1));
+    MM_CUDA(ctx, ctx->inv.ensure(M ? M : 1));
+    MM_CUDA(ctx, ctx->recs.ensure(M ? M : 1));
+    MM_CUDA(ctx, ctx->own_mask.ensure(M ? M : 1));
+    MM_CUDA(ctx, ctx->pos_owner.ensure(M ? M : 1));
+    MM_CUDA(ctx, ctx->rec.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->lcom.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->ck.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->cbo.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->thr_scratch.ensure(thresholds_scratch_bytes(C)));
-    MM_CUDA(ctx, ctx->ux.alloc(Ec + Ea + 1));
-    MM_CUDA(ctx, ctx->un.alloc(Ec + Ea + 1));
+    MM_CUDA(ctx, ctx->ux.ensure(Ec + Ea + 1));
+    MM_CUDA(ctx, ctx->un.ensure(Ec + Ea + 1));
     ctx->have_model = true;
     ctx->metrics_valid = false;
     ctx->sweep_valid = false;
@@ -546,9 +541,9 @@ mm_status mm_what_if(mm_ctx* ctx, uint32_t method, uint32_t origin, uint32_t des
     // error order of what_if_move, suggest.hpp:89-96
     if (origin >= ctx->C || destination >= ctx->C) return fail(ctx, MM_E_RANGE, "what_if_move: unknown class id");
     if (origin == destination) return fail(ctx, MM_E_ARG, "what_if_move: origin and destination coincide");
-    if (method >= ctx->M || ctx->h_method_owner[method] != origin)
-        return fail(ctx, MM_E_ARG, "what_if_move: method " + std::to_string(method) +
-                                       " is not a member of class " + std::to_string(origin));
+    const std::string not_member = "what_if_move: method " + std::to_string(method) +
+                                   " is not a member of class " + std::to_string(origin);
+    if (method >= ctx->M) return fail(ctx, MM_E_ARG, not_member);
     if (mm_status st = ensure_metrics(ctx)) return st;
     const DevModel dm = ctx->dev();
     mm_status st = run(ctx, "what_if", [&] {
@@ -558,6 +553,10 @@ mm_status mm_what_if(mm_ctx* ctx, uint32_t method, uint32_t origin, uint32_t des
     if (st) return st;
     MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->whatif.p, sizeof *out, cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (out->pad[0]) {  // the kernel found method_owner[method] != origin (suggest.hpp:93-96)
+        std::memset(out, 0, sizeof *out);
+        return fail(ctx, MM_E_ARG, not_member);
+    }
     return MM_OK;
 }
 
