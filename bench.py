@@ -245,21 +245,10 @@ def run_ours(args) -> None:
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
 
     def gather(n_local: int):
-        """All-gather the shard lists: counts, then records padded to the max count."""
-        import torch.distributed as dist
-        cnt = torch.tensor([n_local], dtype=torch.int64, device=dev)
-        cnts = torch.empty(world, dtype=torch.int64, device=dev)
-        dist.all_gather_into_tensor(cnts, cnt)
-        counts = cnts.tolist()
-        mx = max(counts)
+        """All-gather the shard lists (counts, then count-padded records) over NCCL."""
+        from paper_1308_4011_b200.shard import allgather_records, device_records_tensor
         ptr, _ = eng.device_result()
-        send = torch.zeros(mx * 64, dtype=torch.uint8, device=dev)
-        if n_local:  # the records live in the engine's device buffer, same stream
-            _copy_device_bytes(send, ptr, n_local * 64)
-        recv = torch.empty(world * mx * 64, dtype=torch.uint8, device=dev)
-        dist.all_gather_into_tensor(recv, send)
-        parts = [recv[r * mx * 64:(r * mx + counts[r]) * 64] for r in range(world)]
-        return torch.cat(parts), sum(counts)
+        return allgather_records(device_records_tensor(ptr, n_local, dev), n_local)
 
     def step():
         eng.compute_metrics()
@@ -361,19 +350,6 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-def _copy_device_bytes(dst_tensor, src_ptr: int, nbytes: int) -> None:
-    """D2D copy from a raw device pointer into a torch tensor on the current stream."""
-    import ctypes
-    import torch
-    cudart = torch.cuda.cudart()
-    stream = torch.cuda.current_stream().cuda_stream
-    res = cudart.cudaMemcpyAsync(ctypes.c_void_p(dst_tensor.data_ptr()), ctypes.c_void_p(src_ptr), nbytes, 3, stream)
-    if isinstance(res, tuple):
-        res = res[0]
-    if int(res) != 0:
-        raise RuntimeError(f"cudaMemcpyAsync D2D failed: {res}")
-
-
 def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
     import torch
     from paper_1308_4011_b200 import System
@@ -399,7 +375,7 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
         else:
             eng.sweep(thresholds=None, class_range=shard, want_count=False)
             n_local = eng.sweep_stats()["suggestions"]
-            allrec, n = gather(n_local)
+            allrec, counts = gather(n_local)
             recs = allrec.cpu().numpy()
         d2h[0] = lcom.nbytes + ck.nbytes + cbo.nbytes + (recs.nbytes if hasattr(recs, "nbytes") else 0)
 

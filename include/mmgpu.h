@@ -227,6 +227,12 @@ mm_status mm_what_if(mm_ctx* ctx, uint32_t method, uint32_t origin, uint32_t des
                      mm_whatif* out);
 
 /* ---- candidate sweep (suggest_by_cohesion/coupling, suggest_all) ------- */
+/* Class gates from the caller's MetricsReport (report.lcom / report.cbo,
+ * n_classes entries each, host memory, copied): the reference gates on the
+ * report it is given (suggest.hpp:246, :273), which need not be this
+ * engine's own metrics. Both NULL: gate on the device-computed metrics
+ * (the default). */
+mm_status mm_set_gates(mm_ctx* ctx, const double* lcom, const uint32_t* cbo);
 /* Runs the sweep on the device; the ordered result stays resident.
  * n_out (may be NULL) receives the record count (a D2H of 8 bytes). */
 mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out);

@@ -1,0 +1,326 @@
+// modmetrics/gpu.hpp — drop-in B200 engine for the reference library's metric
+// and move-method suggestion path.
+//
+// Include this next to the reference headers (proj/include/modmetrics/) and
+// link libmmgpu.so. The functions below have the reference's names,
+// signatures, argument meaning, result types and exceptions; results are
+// bit-identical (every double, every integer, and the ORDER of the returned
+// vectors). Everything computes on the GPU through the C ABI in mmgpu.h;
+// there is no CPU fallback (no device -> std::runtime_error).
+//
+//   reference (namespace modmetrics)          here (namespace modmetrics::gpu)
+//   parallel_class_metrics  parallel.hpp:149  parallel_class_metrics / Engine::
+//   parallel_lcom_ck        parallel.hpp:164  parallel_lcom_ck / Engine::
+//   lcom_normalized/lcom_ck/cbo metrics.hpp:128,159,187   Engine::
+//   compute_thresholds      suggest.hpp:46    (use the reference's own: host arithmetic on the report)
+//   what_if_move            suggest.hpp:87    what_if_move / Engine::
+//   suggest_by_cohesion     suggest.hpp:239   suggest_by_cohesion / Engine::
+//   suggest_by_coupling     suggest.hpp:266   suggest_by_coupling / Engine::
+//   suggest_all             suggest.hpp:303   suggest_all / Engine:: (criteria ⊆ {Cohesion, Coupling})
+//
+// A persistent Engine keeps the system resident in HBM across calls; the
+// free functions upload per call (like the reference, which takes the model
+// by const& every time).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <modmetrics/metrics.hpp>
+#include <modmetrics/model.hpp>
+#include <modmetrics/parallel.hpp>
+#include <modmetrics/suggest.hpp>
+
+#include "../mmgpu.h"
+
+namespace modmetrics::gpu {
+
+namespace detail {
+
+// status -> the reference's exception types (no exception crosses the C ABI)
+inline void check(mm_status st, const mm_ctx* ctx, const char* what) {
+    if (st == MM_OK) return;
+    const std::string msg = std::string(what) + ": " + (ctx ? mm_last_error(ctx) : "");
+    switch (st) {
+        case MM_E_RANGE: throw std::out_of_range(msg);
+        case MM_E_ARG: throw std::invalid_argument(msg);
+        case MM_E_OOM: throw std::bad_alloc();
+        default: throw std::runtime_error(msg);
+    }
+}
+
+// SystemModel + DependencyTable -> CSR (mm_system points into this object)
+struct Csr {
+    std::vector<uint32_t> cmo, cm, cao, ca, co, ct, ao, at;
+    mm_system sys{};
+
+    Csr(const SystemModel& model, const DependencyTable& deps) {
+        cmo.reserve(model.classes.size() + 1);
+        cao.reserve(model.classes.size() + 1);
+        cmo.push_back(0);
+        cao.push_back(0);
+        for (const ClassRecord& c : model.classes) {
+            cm.insert(cm.end(), c.method_ids.begin(), c.method_ids.end());
+            ca.insert(ca.end(), c.attribute_ids.begin(), c.attribute_ids.end());
+            cmo.push_back(static_cast<uint32_t>(cm.size()));
+            cao.push_back(static_cast<uint32_t>(ca.size()));
+        }
+        const size_t m = model.method_count();
+        if (deps.calls.size() != m || deps.accesses.size() != m)
+            throw std::invalid_argument("gpu: dependency table rows != method count");
+        co.reserve(m + 1);
+        ao.reserve(m + 1);
+        co.push_back(0);
+        ao.push_back(0);
+        for (size_t p = 0; p < m; ++p) {
+            ct.insert(ct.end(), deps.calls[p].begin(), deps.calls[p].end());
+            at.insert(at.end(), deps.accesses[p].begin(), deps.accesses[p].end());
+            co.push_back(static_cast<uint32_t>(ct.size()));
+            ao.push_back(static_cast<uint32_t>(at.size()));
+        }
+        sys.n_classes = static_cast<uint32_t>(model.classes.size());
+        sys.n_methods = static_cast<uint32_t>(m);
+        sys.n_attributes = static_cast<uint32_t>(model.attribute_count());
+        sys.method_owner = model.method_owner.data();
+        sys.attribute_owner = model.attribute_owner.data();
+        sys.class_method_off = cmo.data();
+        sys.class_methods = cm.data();
+        sys.class_attr_off = cao.data();
+        sys.class_attrs = ca.data();
+        sys.call_off = co.data();
+        sys.call_tgt = ct.data();
+        sys.acc_off = ao.data();
+        sys.acc_tgt = at.data();
+    }
+};
+
+inline WhatIfMetrics to_whatif(const mm_suggestion& r) {
+    WhatIfMetrics w;
+    w.lcom_origin_before = r.lcom_origin_before;
+    w.lcom_origin_after = r.lcom_origin_after;
+    w.lcom_dest_before = r.lcom_dest_before;
+    w.lcom_dest_after = r.lcom_dest_after;
+    w.cbo_origin_before = r.cbo_origin_before;
+    w.cbo_origin_after = r.cbo_origin_after;
+    w.cbo_dest_before = r.cbo_dest_before;
+    w.cbo_dest_after = r.cbo_dest_after;
+    w.origin_degenerate_after = r.origin_degenerate_after != 0;
+    w.dest_degenerate_after = r.dest_degenerate_after != 0;
+    return w;
+}
+
+inline MoveSuggestion to_suggestion(const mm_suggestion& r) {
+    MoveSuggestion s;
+    s.method = r.method;
+    s.origin = r.origin;
+    s.destination = r.destination;
+    for (Criterion c : {Criterion::Similarity, Criterion::Cohesion, Criterion::Coupling})
+        if (r.criteria & (1u << static_cast<unsigned>(c))) s.criteria.push_back(c);
+    s.impact = to_whatif(r);
+    return s;
+}
+
+}  // namespace detail
+
+class Engine {
+public:
+    explicit Engine(int device = 0) {
+        mm_ctx* c = nullptr;
+        detail::check(mm_ctx_create(device, &c), nullptr, "mm_ctx_create");
+        ctx_.reset(c);
+    }
+
+    // Uploads (copies) the system into HBM; the model may be destroyed afterwards.
+    void upload(const SystemModel& model, const DependencyTable& deps) {
+        const detail::Csr csr(model, deps);
+        detail::check(mm_upload(ctx_.get(), &csr.sys), ctx_.get(), "mm_upload");
+        n_classes_ = csr.sys.n_classes;
+    }
+
+    ClassMetrics parallel_class_metrics(unsigned n_workers = 1) {
+        if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");  // parallel.hpp:29
+        ClassMetrics out;
+        out.lcom.resize(n_classes_);
+        out.cbo.resize(n_classes_);
+        detail::check(mm_class_metrics(ctx_.get(), out.lcom.data(), nullptr, out.cbo.data()), ctx_.get(),
+                      "parallel_class_metrics");
+        return out;
+    }
+
+    std::vector<std::uint64_t> parallel_lcom_ck(unsigned n_workers = 1) {
+        if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");
+        std::vector<std::uint64_t> out(n_classes_);
+        detail::check(mm_class_metrics(ctx_.get(), nullptr, out.data(), nullptr), ctx_.get(), "parallel_lcom_ck");
+        return out;
+    }
+
+    double lcom_normalized(ClassId c) {
+        double v = 0;
+        detail::check(mm_lcom_normalized(ctx_.get(), c, &v), ctx_.get(), "lcom_normalized");
+        return v;
+    }
+    std::uint64_t lcom_ck(ClassId c) {
+        std::uint64_t v = 0;
+        detail::check(mm_lcom_ck(ctx_.get(), c, &v), ctx_.get(), "lcom_ck");
+        return v;
+    }
+    std::uint32_t cbo(ClassId c) {
+        std::uint32_t v = 0;
+        detail::check(mm_cbo(ctx_.get(), c, &v), ctx_.get(), "cbo");
+        return v;
+    }
+
+    WhatIfMetrics what_if_move(MethodId method, ClassId origin, ClassId destination) {
+        mm_whatif w;
+        detail::check(mm_what_if(ctx_.get(), method, origin, destination, &w), ctx_.get(), "what_if_move");
+        mm_suggestion r{};
+        r.lcom_origin_before = w.lcom_origin_before;
+        r.lcom_origin_after = w.lcom_origin_after;
+        r.lcom_dest_before = w.lcom_dest_before;
+        r.lcom_dest_after = w.lcom_dest_after;
+        r.cbo_origin_before = w.cbo_origin_before;
+        r.cbo_origin_after = w.cbo_origin_after;
+        r.cbo_dest_before = w.cbo_dest_before;
+        r.cbo_dest_after = w.cbo_dest_after;
+        r.origin_degenerate_after = w.origin_degenerate_after;
+        r.dest_degenerate_after = w.dest_degenerate_after;
+        return detail::to_whatif(r);
+    }
+
+    // suggest_all, suggest.hpp:303. Gates use report.lcom / report.cbo (the
+    // caller's report, exactly as the reference does).
+    std::vector<MoveSuggestion> suggest_all(const MetricsReport& report, const Thresholds& thresholds,
+                                            const std::vector<Criterion>& criteria, Combine combine,
+                                            const SuggestOptions& opts = {}) {
+        std::vector<Criterion> sel = criteria;
+        std::sort(sel.begin(), sel.end());
+        sel.erase(std::unique(sel.begin(), sel.end()), sel.end());
+        if (sel.empty()) throw std::invalid_argument("suggest_all: no criteria selected");  // suggest.hpp:313
+        uint32_t mask = 0;
+        for (Criterion c : sel) mask |= 1u << static_cast<unsigned>(c);
+        return run(report, thresholds, mask, combine == Combine::Intersection, opts);
+    }
+
+    // suggest_by_cohesion (suggest.hpp:239): same records, in the reference's
+    // emission order (classes by id; methods by fan_out desc, then id).
+    std::vector<MoveSuggestion> suggest_by_cohesion(const MetricsReport& report, const Thresholds& thresholds,
+                                                    const SuggestOptions& opts = {}) {
+        auto v = run(report, thresholds, MM_CRIT_COHESION, false, opts);
+        order_like_reference(v, [&](MethodId m) { return std::uint64_t(report.fan_out[m]); });
+        return v;
+    }
+
+    // suggest_by_coupling (suggest.hpp:266): methods by fan_in + fan_out desc, then id.
+    std::vector<MoveSuggestion> suggest_by_coupling(const MetricsReport& report, const Thresholds& thresholds,
+                                                    const SuggestOptions& opts = {}) {
+        auto v = run(report, thresholds, MM_CRIT_COUPLING, false, opts);
+        order_like_reference(v, [&](MethodId m) {
+            return std::uint64_t(report.fan_in[m]) + std::uint64_t(report.fan_out[m]);
+        });
+        return v;
+    }
+
+    mm_ctx* handle() { return ctx_.get(); }
+
+private:
+    struct Del {
+        void operator()(mm_ctx* c) const { mm_ctx_destroy(c); }
+    };
+    std::unique_ptr<mm_ctx, Del> ctx_;
+    uint32_t n_classes_ = 0;
+
+    std::vector<MoveSuggestion> run(const MetricsReport& report, const Thresholds& t, uint32_t mask, bool inter,
+                                    const SuggestOptions& opts) {
+        if (mask & MM_CRIT_SIMILARITY)
+            throw std::invalid_argument("gpu: Criterion::Similarity is outside this engine");
+        if (report.lcom.size() != n_classes_ || report.cbo.size() != n_classes_)
+            throw std::invalid_argument("gpu: report does not match the uploaded system");
+        detail::check(mm_set_gates(ctx_.get(), report.lcom.data(), report.cbo.data()), ctx_.get(), "mm_set_gates");
+        mm_sweep_params p{};
+        p.criteria = mask;
+        p.combine = inter ? MM_COMBINE_INTERSECTION : MM_COMBINE_UNION;
+        p.all_candidates = opts.all_candidates ? 1u : 0u;
+        p.top_k = 1;
+        p.thr_lcom = t.lcom;
+        p.thr_cbo = t.cbo;
+        p.threshold_source = MM_THR_EXPLICIT;
+        uint64_t n = 0;
+        detail::check(mm_sweep(ctx_.get(), &p, &n), ctx_.get(), "mm_sweep");
+        std::vector<mm_suggestion> raw(n);
+        if (n) detail::check(mm_copy_suggestions(ctx_.get(), raw.data(), n, &n), ctx_.get(), "mm_copy_suggestions");
+        detail::check(mm_set_gates(ctx_.get(), nullptr, nullptr), ctx_.get(), "mm_set_gates");
+        std::vector<MoveSuggestion> out;
+        out.reserve(raw.size());
+        for (const mm_suggestion& r : raw) out.push_back(detail::to_suggestion(r));
+        return out;
+    }
+
+    // Within one origin class the GPU list is (method, destination) ordered;
+    // the per-criterion reference vectors list methods by a busyness key,
+    // descending, id ascending (destinations of one method stay ascending).
+    template <class Key>
+    static void order_like_reference(std::vector<MoveSuggestion>& v, Key key) {
+        std::stable_sort(v.begin(), v.end(), [&](const MoveSuggestion& a, const MoveSuggestion& b) {
+            if (a.origin != b.origin) return a.origin < b.origin;
+            const auto ka = key(a.method), kb = key(b.method);
+            if (ka != kb) return ka > kb;
+            return a.method < b.method;
+        });
+    }
+};
+
+// ---- free functions with the reference signatures ------------------------
+
+inline ClassMetrics parallel_class_metrics(const SystemModel& model, const DependencyTable& deps,
+                                           unsigned n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");
+    Engine e;
+    e.upload(model, deps);
+    return e.parallel_class_metrics(n_workers);
+}
+
+inline std::vector<std::uint64_t> parallel_lcom_ck(const SystemModel& model, const DependencyTable& deps,
+                                                   unsigned n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");
+    Engine e;
+    e.upload(model, deps);
+    return e.parallel_lcom_ck(n_workers);
+}
+
+inline WhatIfMetrics what_if_move(MethodId method, ClassId origin, ClassId destination, const SystemModel& model,
+                                  const DependencyTable& deps) {
+    Engine e;
+    e.upload(model, deps);
+    return e.what_if_move(method, origin, destination);
+}
+
+inline std::vector<MoveSuggestion> suggest_by_cohesion(const SystemModel& model, const DependencyTable& deps,
+                                                       const MetricsReport& report, const Thresholds& thresholds,
+                                                       const SuggestOptions& opts = {}) {
+    Engine e;
+    e.upload(model, deps);
+    return e.suggest_by_cohesion(report, thresholds, opts);
+}
+
+inline std::vector<MoveSuggestion> suggest_by_coupling(const SystemModel& model, const DependencyTable& deps,
+                                                       const MetricsReport& report, const Thresholds& thresholds,
+                                                       const SuggestOptions& opts = {}) {
+    Engine e;
+    e.upload(model, deps);
+    return e.suggest_by_coupling(report, thresholds, opts);
+}
+
+inline std::vector<MoveSuggestion> suggest_all(const SystemModel& model, const DependencyTable& deps,
+                                               const MetricsReport& report, const Thresholds& thresholds,
+                                               const std::vector<Criterion>& criteria, Combine combine,
+                                               const SuggestOptions& opts = {}) {
+    Engine e;
+    e.upload(model, deps);
+    return e.suggest_all(report, thresholds, criteria, combine, opts);
+}
+
+}  // namespace modmetrics::gpu

@@ -97,6 +97,9 @@ struct mm_ctx {
     DBuf<uint64_t> own_mask;
     DBuf<uint32_t> pos_owner;
     DBuf<uint4> res;
+    DBuf<double> gate_lcom;
+    DBuf<uint32_t> gate_cbo;
+    bool gates_set = false;
     DBuf<ClassRec> rec;
     DBuf<double> lcom;
     DBuf<uint64_t> ck;
@@ -272,6 +275,8 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     ctx->tile_state.release();
     ctx->out.release();
     ctx->res.release();
+    ctx->gate_lcom.release();
+    ctx->gate_cbo.release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->ev_metrics) cudaEventDestroy(ctx->ev_metrics);
@@ -337,6 +342,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     // device buffers are reused across uploads (grown on demand, never shrunk)
     ctx->have_model = ctx->metrics_valid = ctx->sweep_valid = false;
+    ctx->gates_set = false;
     if (!s->call_off || !s->acc_off || !s->class_method_off || !s->class_attr_off)
         return fail(ctx, MM_E_ARG, "mm_upload: NULL offsets");
     const uint32_t C = s->n_classes, M = s->n_methods, A = s->n_attributes;
@@ -560,6 +566,27 @@ mm_status mm_what_if(mm_ctx* ctx, uint32_t method, uint32_t origin, uint32_t des
     return MM_OK;
 }
 
+mm_status mm_set_gates(mm_ctx* ctx, const double* lcom, const uint32_t* cbo) {
+    if (!ctx) return MM_E_ARG;
+    if (!lcom && !cbo) {
+        ctx->gates_set = false;
+        return MM_OK;
+    }
+    if (!lcom || !cbo) return fail(ctx, MM_E_ARG, "mm_set_gates: give both vectors or neither");
+    if (!ctx->have_model) return fail(ctx, MM_E_STATE, "mm_set_gates: no model uploaded");
+    if (mm_status st = set_device(ctx)) return st;
+    const size_t C = ctx->C;
+    MM_CUDA(ctx, ctx->gate_lcom.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->gate_cbo.ensure(C ? C : 1));
+    if (C) {
+        MM_CUDA(ctx, cudaMemcpyAsync(ctx->gate_lcom.p, lcom, 8 * C, cudaMemcpyHostToDevice, ctx->stream));
+        MM_CUDA(ctx, cudaMemcpyAsync(ctx->gate_cbo.p, cbo, 4 * C, cudaMemcpyHostToDevice, ctx->stream));
+        MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // caller buffers may be pageable/temporary
+    }
+    ctx->gates_set = true;
+    return MM_OK;
+}
+
 mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     if (!ctx || !p) return MM_E_ARG;
     const uint32_t sel = p->criteria & (MM_CRIT_SIMILARITY | MM_CRIT_COHESION | MM_CRIT_COUPLING);
@@ -591,8 +618,8 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     a.rec = ctx->rec.p;
     a.recs = ctx->recs.p;
     a.pos_owner = ctx->pos_owner.p;
-    a.lcom = ctx->lcom.p;
-    a.cbo = ctx->cbo.p;
+    a.lcom = ctx->gates_set ? ctx->gate_lcom.p : ctx->lcom.p;
+    a.cbo = ctx->gates_set ? ctx->gate_cbo.p : ctx->cbo.p;
     a.res = ctx->res.p - pb;  // indexed by absolute position
     a.ux = ctx->ux.p;
     a.un = ctx->un.p;

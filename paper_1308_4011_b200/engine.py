@@ -220,6 +220,15 @@ class Engine:
         self._check(lib().mm_sweep(self._ctx, C.byref(p), C.byref(n) if want_count else None), "mm_sweep")
         return n.value if want_count else None
 
+    def set_gates(self, lcom=None, cbo=None) -> None:
+        """Gate on the caller's report vectors (None, None: the device metrics)."""
+        if lcom is None and cbo is None:
+            self._check(lib().mm_set_gates(self._ctx, None, None), "mm_set_gates")
+            return
+        self._gl = np.ascontiguousarray(lcom, dtype=np.float64)
+        self._gc = np.ascontiguousarray(cbo, dtype=np.uint32)
+        self._check(lib().mm_set_gates(self._ctx, self._gl.ctypes.data, self._gc.ctypes.data), "mm_set_gates")
+
     def sweep_stats(self) -> dict:
         s = abi.mm_sweep_stats()
         self._check(lib().mm_sweep_stats_get(self._ctx, C.byref(s)), "mm_sweep_stats_get")
