@@ -79,12 +79,12 @@ def algorithmic_bytes(sys_, nnz_u: int, n_sugg: int, rank_share: float = 1.0) ->
     E = sys_.n_calls + sys_.n_accesses
     ms = int(m * rank_share)
     k = {
-        "layout": 8 * m + 12 * a + 4 * c,
-        "method": 60 * m + 8 * a + 4 * E,
+        "method": 64 * m + 8 * a + 4 * E + 4 * c,
         "class_small": 44 * m + 61 * c + 8 * nnz_u,
         "thresholds": 12 * c,
         "score": 56 * ms + 32 * c + 4 * nnz_u,
-        "emit": 20 * ms + 12 * c + 96 * n_sugg,
+        "offsets": 36 * ms + 12 * c,
+        "write": 20 * ms + 96 * n_sugg,
     }
     # SURVEY.md §8d layout-independent totals, for reference
     b_in = 4 * (2 * (m + 1) + E + m + a)
@@ -311,7 +311,7 @@ def run_ours(args) -> None:
                 "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s"}
-    recompute_us = sum(kern.get(k, {}).get("avg_us", 0.0) for k in ("layout", "method", "class_small",
+    recompute_us = sum(kern.get(k, {}).get("avg_us", 0.0) for k in ("method", "class_small",
                                                                      "class_large", "thresholds"))
 
     # e2e through the public API: pinned host CSR -> H2D upload -> pass -> sweep -> D2H results
@@ -338,7 +338,7 @@ def run_ours(args) -> None:
             "gpu_launches": gpu_launches,
             "clocks": clocks.summary(),
             "recompute_ms": recompute_us / 1e3,
-            "sweep_ms": sum(kern.get(k, {}).get("avg_us", 0.0) for k in ("score", "emit")) / 1e3,
+            "sweep_ms": sum(kern.get(k, {}).get("avg_us", 0.0) for k in ("score", "offsets", "write")) / 1e3,
             "suggestions": int(n_sugg_local) if world == 1 else None,
             "kernels": kern,
             "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),

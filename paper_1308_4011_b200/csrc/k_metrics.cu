@@ -72,56 +72,85 @@ __global__ void k_plan_classes(DevModel s, uint8_t* __restrict__ kind, uint32_t*
         }
     }
     foreign[c] = fr;
-    const bool small = (me - mb) <= kSmallMaxMembers && A <= kSmallMaxAttrs && mdeg <= kSmallMaxDeg;
+    const bool small = (me - mb) <= kSmallMaxMembers && A <= kSmallMaxAttrs && mdeg <= kSmallMaxDeg &&
+                       s.C < (1u << 27);  // warp path packs X << 5 | member into 32 bits
     kind[c] = small ? 0 : 1;
     if (!small) large_list[atomicAdd(n_large, 1u)] = c;
     atomicMax(max_deg, mdeg);
 }
 
-// Layout pass: inv[p] = class-order position of method p (inverse of the
-// concatenated ClassRecord::method_ids) and attr_local[t] = index of
-// attribute t inside its class's sorted attribute list.
-__global__ void k_layout(DevModel s, uint32_t* __restrict__ inv, uint32_t* __restrict__ attr_local) {
-    const uint32_t n = max(s.M, s.A);
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        if (j < s.M) inv[s.cls_methods[j]] = j;
-        if (j < s.A) {
-            const uint32_t t = s.cls_attrs[j];
-            attr_local[t] = j - s.cls_aoff[s.attribute_owner[t]];
+// Position of attribute t inside class c's sorted attribute list
+// (ClassRecord::attribute_ids, model.hpp:22): short lists are scanned with
+// independent loads (one round trip per 8 entries), long ones bisected.
+__device__ __forceinline__ uint32_t attr_pos(const DevModel& s, uint32_t ab, uint32_t ae, uint32_t t) {
+    const uint32_t len = ae - ab;
+    if (len <= 64) {
+        for (uint32_t k0 = 0; k0 < len; k0 += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = (k0 + j < len) ? __ldg(s.cls_attrs + ab + k0 + j) : kNone;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (v[j] == t) return k0 + j;
         }
+        return kNone;
     }
+    uint32_t lo = 0, hi = len;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(s.cls_attrs + ab + mid) < t) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
 }
 
-// Method pass, method-id order (coalesced CSR reads, owner gathers hit L2):
-// each method's sorted used list with per-class access counts, packed into a
-// 32-byte MethRec at its class-order position, plus its own-attribute bit
-// mask (attr_local bits, meaningful for classes with ≤ 64 attributes).
+// Method pass in class order: thread i handles the method at class-order
+// position i. CSR rows are gathered (sector-sized random reads); every write
+// — the 32-byte MethRec, the own-attribute mask, the owner — is coalesced
+// (random partial-sector writes would cost a DRAM read-modify-write each).
+// Each method's sorted used list with per-class access counts is packed into
+// its MethRec; the own-attribute mask has bit k for the k-th attribute of the
+// own class (classes with ≤ 64 attributes).
 template <int K>
 __global__ void __launch_bounds__(256)
-k_method(DevModel s, const uint32_t* __restrict__ inv, const uint32_t* __restrict__ attr_local,
-         MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask, uint32_t* __restrict__ pos_owner) {
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= s.M) return;
+k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask, uint32_t* __restrict__ pos_owner) {
+    const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= s.M) return;
+    const uint32_t p = __ldg(s.cls_methods + pos);
     const uint32_t own = __ldg(s.method_owner + p);
     const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
     const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+    const uint32_t oab = __ldg(s.cls_aoff + own), oae = __ldg(s.cls_aoff + own + 1);
     uint32_t hdr = kRecOverflow;
     uint32_t ent[kRecMaxEnt];
 #pragma unroll
     for (int k = 0; k < kRecMaxEnt; ++k) ent[k] = 0;
     uint64_t mask = 0;
-    if ((ce - cb) + (ae - ab) <= (uint32_t)K) {
+    const uint32_t nc = ce - cb, na = ae - ab;
+    if (nc + na <= (uint32_t)K) {
+        // all targets first, then all owner gathers: two memory round trips
+        // per method instead of two per edge
+        uint32_t tg[K], ow[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const bool isc = (uint32_t)k < nc, isa = !isc && (uint32_t)k < nc + na;
+            tg[k] = isc ? __ldg(s.call_tgt + cb + k) : (isa ? __ldg(s.acc_tgt + ab + (k - nc)) : 0u);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const bool isc = (uint32_t)k < nc, isa = !isc && (uint32_t)k < nc + na;
+            ow[k] = isc ? __ldg(s.method_owner + tg[k]) : (isa ? __ldg(s.attribute_owner + tg[k]) : kNone);
+        }
         UsedList<K> L;
         L.clear();
         uint32_t hown = 0;
-        for (uint32_t e = cb; e < ce; ++e) L.insert(__ldg(s.method_owner + __ldg(s.call_tgt + e)), 0);
-        for (uint32_t e = ab; e < ae; ++e) {
-            const uint32_t t = __ldg(s.acc_tgt + e);
-            const uint32_t o = __ldg(s.attribute_owner + t);
-            L.insert(o, 1);
-            if (o == own) {
-                const uint32_t loc = __ldg(attr_local + t);
-                if (loc < 64) mask |= 1ull << loc;
+        const bool small_attrs = oae - oab <= 64;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const bool isa = (uint32_t)k >= nc && (uint32_t)k < nc + na;
+            if ((uint32_t)k < nc + na) L.insert(ow[k], isa ? 1u : 0u);
+            if (isa && ow[k] == own) {
+                if (small_attrs) mask |= 1ull << attr_pos(s, oab, oae, tg[k]);
                 ++hown;
             }
         }
@@ -134,7 +163,6 @@ k_method(DevModel s, const uint32_t* __restrict__ inv, const uint32_t* __restric
             }
         if (fits) hdr = (uint32_t)L.n | (hown << kRecHownShift);
     }
-    const uint32_t pos = __ldg(inv + p);
     uint4* dst = reinterpret_cast<uint4*>(recs + pos);
     dst[0] = make_uint4(hdr, ent[0], ent[1], ent[2]);
     dst[1] = make_uint4(ent[3], ent[4], ent[5], ent[6]);
@@ -177,26 +205,18 @@ __device__ __forceinline__ void warp_bitonic_u32(uint32_t* buf, int N, int lane)
         }
 }
 
-__device__ __forceinline__ int smem_find(const uint32_t* row, int n, uint32_t x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (row[mid] < x) lo = mid + 1;
-        else hi = mid;
-    }
-    return (lo < n && row[lo] == x) ? lo : -1;
-}
-
 // One warp per class, one lane per member. Members' used lists come from the
 // method pass records (coalesced: a class's members are contiguous in class
 // order); a member whose list overflowed its record is rebuilt from the CSR.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_class_small(DevModel s, const uint8_t* __restrict__ kind, const uint32_t* __restrict__ attr_local,
+k_class_small(DevModel s, const uint8_t* __restrict__ kind,
               MethRec* __restrict__ recs, const uint64_t* __restrict__ own_mask, ClassRec* __restrict__ rec,
               double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
               uint32_t* __restrict__ ux, uint32_t* __restrict__ un, uint32_t* __restrict__ ucursor) {
     __shared__ uint32_t sbuf[kWarpsPerBlock][kSmallEntries];
     __shared__ uint32_t scnt[kWarpsPerBlock][kSmallEntries];
+    __shared__ uint32_t srem[kWarpsPerBlock][32];
+    __shared__ uint32_t ssig[kWarpsPerBlock][kSigWords];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t c = blockIdx.x * kWarpsPerBlock + warp;
     if (c >= s.C || kind[c] != 0) return;  // warp-uniform exit
@@ -226,13 +246,14 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind, const uint32_t* __re
         const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
         for (uint32_t e = cb; e < ce; ++e) L.insert(__ldg(s.method_owner + __ldg(s.call_tgt + e)), 0);
         const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+        const uint32_t cab = s.cls_aoff[c], cae = s.cls_aoff[c + 1];
         mask = 0;
         for (uint32_t e = ab; e < ae; ++e) {
             const uint32_t t = __ldg(s.acc_tgt + e);
             const uint32_t o = __ldg(s.attribute_owner + t);
             L.insert(o, 1);
             if (o == c) {
-                mask |= 1ull << __ldg(attr_local + t);
+                mask |= 1ull << attr_pos(s, cab, cae, t);
                 ++hown;
             }
         }
@@ -247,7 +268,9 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind, const uint32_t* __re
     }
     const uint32_t Q = warp_sum(q);
 
-    // U row: multiset union of the members' used classes other than c
+    // U row: multiset union of the members' used classes other than c, as
+    // keys X << 5 | member so that a run of length 1 names the one member that
+    // alone uses X (that member's cbo_origin_after drops by one, App. A)
     uint32_t cnt = 0;
     if (ovf) cnt = (uint32_t)L.n - (L.has(c) ? 1u : 0u);
     else
@@ -256,23 +279,26 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind, const uint32_t* __re
     const uint32_t off = warp_excl_scan(cnt, lane);
     const uint32_t T = __shfl_sync(0xffffffffu, off + cnt, 31);
     uint32_t* buf = sbuf[warp];
+    uint32_t* rcnt = scnt[warp];
     {
         uint32_t w = off;
         if (ovf) {
 #pragma unroll
             for (int k = 0; k < kSmallMaxDeg; ++k)
-                if (k < L.n && L.X[k] != c) buf[w++] = L.X[k];
+                if (k < L.n && L.X[k] != c) buf[w++] = (L.X[k] << 5) | lane;
         } else {
 #pragma unroll
             for (int k = 0; k < kRecMaxEnt; ++k)
-                if (k < (int)nent && (ent[k] >> 8) != c) buf[w++] = ent[k] >> 8;
+                if (k < (int)nent && (ent[k] >> 8) != c) buf[w++] = ((ent[k] >> 8) << 5) | lane;
         }
     }
+    uint32_t* rem = srem[warp];  // per-member removed counters (smem path)
+    uint32_t* sig = ssig[warp];   // Bloom signature of the U row
+    if (lane < kSigWords) sig[lane] = 0;
+    rem[lane] = 0;
     __syncwarp();
-    uint32_t* row = sbuf[warp];
-    uint32_t* rcnt = scnt[warp];
     uint32_t cbo = 0;
-    uint64_t sig = 0;
+    uint32_t removed_me = 0;
     if (T <= 32) {
         // register bitonic sort across the warp, run-length encode with ballots
         uint32_t v = lane < (int)T ? buf[lane] : kNone;
@@ -287,16 +313,21 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind, const uint32_t* __re
                 v = (lower == up) ? min(v, o) : max(v, o);
             }
         const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
-        const bool head = lane < (int)T && (lane == 0 || v != prev);
+        const bool head = lane < (int)T && (lane == 0 || (v >> 5) != (prev >> 5));
         const uint32_t hb = __ballot_sync(0xffffffffu, head);
         cbo = __popc(hb);
+        // single-user entries: the member named by the key loses X on leaving
+        const uint32_t above = hb & ~((2u << lane) - 1);
+        const uint32_t next = above ? __ffs(above) - 1 : T;
+        const bool single = head && next == (uint32_t)lane + 1;
+        if (single) atomicAdd(rem + (v & 31u), 1u);  // the member named by the key loses X
         if (head) {
             const uint32_t idx = __popc(hb & ((1u << lane) - 1));
-            const uint32_t above = hb & ~((2u << lane) - 1);  // heads after this lane
-            const uint32_t next = above ? __ffs(above) - 1 : T;
-            row[idx] = v;
+            buf[idx] = v >> 5;
             rcnt[idx] = next - lane;
-            sig |= 1ull << uhash(v);
+            const uint32_t b1 = bloom_h1(v >> 5), b2 = bloom_h2(v >> 5);
+            atomicOr(sig + (b1 >> 5), 1u << (b1 & 31));
+            atomicOr(sig + (b2 >> 5), 1u << (b2 & 31));
         }
     } else {
         int N = 64;
@@ -307,57 +338,56 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind, const uint32_t* __re
         uint32_t nh = 0;
         for (uint32_t base = 0; base < T; base += 32) {  // heads compacted into rcnt (positions)
             const uint32_t i = base + lane;
-            const bool head = i < T && (i == 0 || buf[i] != buf[i - 1]);
+            const bool head = i < T && (i == 0 || (buf[i] >> 5) != (buf[i - 1] >> 5));
             const uint32_t b = __ballot_sync(0xffffffffu, head);
             if (head) {
                 rcnt[nh + __popc(b & ((1u << lane) - 1))] = i;
-                sig |= 1ull << uhash(buf[i]);
+                const uint32_t b1 = bloom_h1(buf[i] >> 5), b2 = bloom_h2(buf[i] >> 5);
+                atomicOr(sig + (b1 >> 5), 1u << (b1 & 31));
+                atomicOr(sig + (b2 >> 5), 1u << (b2 & 31));
             }
             nh += __popc(b);
         }
         __syncwarp();
         cbo = nh;
-        // (X, count) into row/rcnt in place: heads are increasing, so slot k ≤ head k
+        // (X, count) into buf/rcnt in place: head k sits at position ≥ k
         for (uint32_t k0 = 0; k0 < cbo; k0 += 32) {
             const uint32_t k = k0 + lane;
-            uint32_t x = 0, cn = 0;
+            uint32_t x = 0, cn = 0, key = 0;
             if (k < cbo) {
                 const uint32_t h0 = rcnt[k];
                 const uint32_t h1 = k + 1 < cbo ? rcnt[k + 1] : T;
-                x = buf[h0];
+                key = buf[h0];
+                x = key >> 5;
                 cn = h1 - h0;
             }
             __syncwarp();
-            if (k < cbo) { row[k] = x; rcnt[k] = cn; }
+            if (k < cbo) {
+                buf[k] = x;
+                rcnt[k] = cn;
+                if (cn == 1) atomicAdd(rem + (key & 31u), 1u);
+            }
             __syncwarp();
         }
     }
     __syncwarp();
-    sig = __reduce_or_sync(0xffffffffu, (uint32_t)sig) | ((uint64_t)__reduce_or_sync(0xffffffffu, (uint32_t)(sig >> 32)) << 32);
+    removed_me = rem[lane];
     uint32_t ubase = 0;
     if (lane == 0 && cbo) ubase = atomicAdd(ucursor, cbo);  // slot reservation
     ubase = __shfl_sync(0xffffffffu, ubase, 0);
     for (uint32_t k = lane; k < cbo; k += 32) {
-        ux[ubase + k] = row[k];
+        ux[ubase + k] = buf[k];
         un[ubase + k] = rcnt[k];
     }
     // per member: #{X ≠ c : U[c][X] == 1} — the sweep's cbo_origin_after
-    if (active && !ovf) {
-        uint32_t removed = 0;
-#pragma unroll
-        for (int k = 0; k < kRecMaxEnt; ++k)
-            if (k < (int)nent && (ent[k] >> 8) != c) {
-                const int at = smem_find(row, (int)cbo, ent[k] >> 8);
-                removed += (at >= 0 && rcnt[at] == 1u);
-            }
-        recs[pos].hdr = r0.x | (removed << kRecRemovedShift) | kRecRemovedValid;
-    }
+    if (active && !ovf) recs[pos].hdr = r0.x | (removed_me << kRecRemovedShift) | kRecRemovedValid;
     if (lane == 0) {
         const double l = lcom_of(A, M, H);
         const uint64_t pairs = (uint64_t)M * (M - 1) / 2;
         const uint64_t P = pairs - Q;
         ClassRec r;
-        r.A = A; r.M = M; r.H = H; r.cbo = cbo; r.ubase = ubase; r.pad = 0; r.sig = sig;
+        r.A = A; r.M = M; r.H = H; r.cbo = cbo; r.ubase = ubase; r.pad = 0;
+        for (int w = 0; w < kSigWords; ++w) r.sig[w] = sig[w];
         rec[c] = r;
         lcom_out[c] = l;
         ck_out[c] = P > Q ? P - Q : 0;
@@ -418,7 +448,7 @@ __device__ void block_bitonic_u64(uint64_t* buf, uint32_t N) {
 
 __global__ void __launch_bounds__(kLargeThreads)
 k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* __restrict__ plan,
-              const uint32_t* __restrict__ attr_local, MethRec* __restrict__ recs, ClassRec* __restrict__ rec,
+              MethRec* __restrict__ recs, ClassRec* __restrict__ rec,
               double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
               uint32_t* __restrict__ ux, uint32_t* __restrict__ un, uint32_t* __restrict__ ucursor,
               uint64_t* __restrict__ gkeys, uint32_t* __restrict__ grows) {
@@ -426,7 +456,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     __shared__ uint64_t red64[kLargeThreads / 32];
     __shared__ uint32_t red32[kLargeThreads / 32];
     __shared__ uint32_t s_nk, s_ubase;
-    __shared__ unsigned long long s_sig;
+    __shared__ uint32_t s_sig[kSigWords];
     const uint32_t c = large_list[blockIdx.x];
     const LargePlan pl = plan[blockIdx.x];
     uint64_t* keys = pl.keys_in_smem ? reinterpret_cast<uint64_t*>(dsm) : gkeys + pl.keys_off;
@@ -438,7 +468,8 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     const uint32_t A = s.cls_aoff[c + 1] - s.cls_aoff[c];
     const uint32_t W = (M + 31) / 32;
     const uint64_t nrow_words = (uint64_t)A * W;
-    if (threadIdx.x == 0) { s_nk = 0; s_sig = 0; }
+    if (threadIdx.x == 0) s_nk = 0;
+    if (threadIdx.x < kSigWords) s_sig[threadIdx.x] = 0;
     for (uint64_t i = threadIdx.x; i < nrow_words; i += blockDim.x) rows[i] = 0;
     __syncthreads();
 
@@ -458,7 +489,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
             if (o != c) {
                 keys[atomicAdd(&s_nk, 1u)] = ((uint64_t)o << 32) | i;
             } else {
-                const uint32_t a = __ldg(attr_local + t);
+                const uint32_t a = attr_pos(s, s.cls_aoff[c], s.cls_aoff[c + 1], t);
                 atomicOr(rows + (uint64_t)a * W + (i >> 5), 1u << (i & 31));
                 ++hown;
             }
@@ -493,7 +524,9 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         if (xh) {
             ux[ubase + xcarry + ex] = (uint32_t)(keys[k] >> 32);
             un[ubase + xcarry + ex] = 0;
-            atomicOr(&s_sig, 1ull << uhash((uint32_t)(keys[k] >> 32)));
+            const uint32_t b1 = bloom_h1((uint32_t)(keys[k] >> 32)), b2 = bloom_h2((uint32_t)(keys[k] >> 32));
+            atomicOr(s_sig + (b1 >> 5), 1u << (b1 & 31));
+            atomicOr(s_sig + (b2 >> 5), 1u << (b2 & 31));
         }
         xcarry += tot;
     }
@@ -538,7 +571,8 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
             if (w < W && w >= (i >> 5)) {
                 for (uint32_t e = ab; e < ae; ++e) {
                     const uint32_t t = __ldg(s.acc_tgt + e);
-                    if (__ldg(s.attribute_owner + t) == c) acc |= rows[(uint64_t)__ldg(attr_local + t) * W + w];
+                    if (__ldg(s.attribute_owner + t) == c)
+                        acc |= rows[(uint64_t)attr_pos(s, s.cls_aoff[c], s.cls_aoff[c + 1], t) * W + w];
                 }
                 if (w == (i >> 5)) acc &= ((i & 31) == 31) ? 0u : (~0u << ((i & 31) + 1));
             }
@@ -551,7 +585,8 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         const uint64_t pairs = (uint64_t)M * (M - 1) / 2;
         const uint64_t P = pairs - Q;
         ClassRec r;
-        r.A = A; r.M = M; r.H = (uint32_t)H; r.cbo = nx; r.ubase = ubase; r.pad = 0; r.sig = s_sig;
+        r.A = A; r.M = M; r.H = (uint32_t)H; r.cbo = nx; r.ubase = ubase; r.pad = 0;
+        for (int w = 0; w < kSigWords; ++w) r.sig[w] = s_sig[w];
         rec[c] = r;
         lcom_out[c] = l;
         ck_out[c] = P > Q ? P - Q : 0;
@@ -577,32 +612,26 @@ void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list,
     if (!s.C) return;
     k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, kind, large_list, n_large, max_deg, foreign);
 }
-void launch_layout(const DevModel& s, uint32_t* inv, uint32_t* attr_local, cudaStream_t st) {
-    const uint32_t n = std::max(s.M, s.A);
-    if (!n) return;
-    const uint32_t blocks = std::min<uint32_t>((n + 255) / 256, 148 * 16);
-    k_layout<<<blocks, 256, 0, st>>>(s, inv, attr_local);
-}
-void launch_method(const DevModel& s, uint32_t maxdeg, const uint32_t* inv, const uint32_t* attr_local,
-                   MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner, cudaStream_t st) {
+void launch_method(const DevModel& s, uint32_t maxdeg, MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner,
+                   cudaStream_t st) {
     if (!s.M) return;
     const uint32_t blocks = (s.M + 255) / 256;
-    if (maxdeg <= 8) k_method<8><<<blocks, 256, 0, st>>>(s, inv, attr_local, recs, own_mask, pos_owner);
-    else k_method<16><<<blocks, 256, 0, st>>>(s, inv, attr_local, recs, own_mask, pos_owner);
+    if (maxdeg <= 8) k_method<8><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
+    else k_method<16><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
 }
-void launch_class_small(const DevModel& s, const uint8_t* kind, const uint32_t* attr_local, MethRec* recs,
-                        const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo,
-                        uint32_t* ux, uint32_t* un, uint32_t* ucursor, cudaStream_t st) {
+void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, const uint64_t* own_mask,
+                        ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,
+                        uint32_t* ucursor, cudaStream_t st) {
     if (!s.C) return;
     k_class_small<<<(s.C + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(
-        s, kind, attr_local, recs, own_mask, rec, lcom, ck, cbo, ux, un, ucursor);
+        s, kind, recs, own_mask, rec, lcom, ck, cbo, ux, un, ucursor);
 }
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
-                        uint32_t smem_bytes, const uint32_t* attr_local, MethRec* recs, ClassRec* rec, double* lcom,
+                        uint32_t smem_bytes, MethRec* recs, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
                         uint64_t* gkeys, uint32_t* grows, cudaStream_t st) {
     if (!n_large) return;
-    k_class_large<<<n_large, kLargeThreads, smem_bytes, st>>>(s, large_list, plan, attr_local, recs, rec, lcom, ck,
+    k_class_large<<<n_large, kLargeThreads, smem_bytes, st>>>(s, large_list, plan, recs, rec, lcom, ck,
                                                               cbo, ux, un, ucursor, gkeys, grows);
 }
 cudaError_t set_class_large_smem(uint32_t bytes) {

@@ -132,19 +132,20 @@ __device__ __forceinline__ bool coh_dest(const ClassRec& rd, uint32_t h, double&
 }
 
 // X ∈ U[d]? Bloom signature first (a clear bit proves absence), then the row.
-__device__ __forceinline__ bool in_urow(const ClassRec& rd, const uint32_t* __restrict__ ux, uint32_t X) {
-    if (!((rd.sig >> uhash(X)) & 1ull)) return false;
+__device__ __forceinline__ bool in_urow(const ClassRec* __restrict__ rec, uint32_t d, const ClassRec& rd,
+                                        const uint32_t* __restrict__ ux, uint32_t X) {
+    if (!sig_maybe(rec, d, X)) return false;
     return urow_find(ux, rd.ubase, rd.cbo, X) >= 0;
 }
 
 // coupling predicate for destination d given co_a < co_b: cd_after <= cd_before
 // ⟺ every X ∈ used(u) \ {d} is already in U[d] (miss == 0).
 template <class E>
-__device__ __forceinline__ bool coup_dest(const ClassRec& rd, const uint32_t* __restrict__ ux, const E& en,
-                                          uint32_t d) {
+__device__ __forceinline__ bool coup_dest(const ClassRec* __restrict__ rec, const ClassRec& rd,
+                                          const uint32_t* __restrict__ ux, const E& en, uint32_t d) {
     bool ok = true;
     en.each([&](int, uint32_t X, uint32_t) {
-        if (ok && X != d && !in_urow(rd, ux, X)) ok = false;
+        if (ok && X != d && !in_urow(rec, d, rd, ux, X)) ok = false;
     });
     return ok;
 }
@@ -158,7 +159,7 @@ __device__ __forceinline__ Dest eval_dest(const ClassRec* __restrict__ rec, cons
     r.ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
     uint32_t miss = 0;
     en.each([&](int, uint32_t X, uint32_t) {
-        if (X != d && !in_urow(rd, ux, X)) ++miss;
+        if (X != d && !in_urow(rec, d, rd, ux, X)) ++miss;
     });
     r.cd_b = rd.cbo;
     r.cd_a = rd.cbo + miss;
@@ -193,7 +194,7 @@ __device__ __forceinline__ void score(const SweepArgs& a, const E& en, const Ori
         pcoh = true;
         kcoh = __dadd_rn(org.lo_a, ld_a);  // lcom_key, suggest.hpp:194-196
     }
-    if (org.co_a < org.co_b && coup_dest(rd, a.ux, en, d)) {
+    if (org.co_a < org.co_b && coup_dest(a.rec, rd, a.ux, en, d)) {
         pcoup = true;
         kcoup = rd.cbo;  // cbo_dest_after == cbo_dest_before when it passes
     }
@@ -393,22 +394,175 @@ __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, ui
 }
 
 // Pass 1: score every candidate of every method (ungated, both criteria) and
-// keep the per-method best / top-k / all-passing destinations. One thread per
-// method, no block barriers, independent of the thresholds (so it overlaps
-// the threshold kernel on another stream).
+// keep the per-method best / top-k / all-passing destinations. Independent
+// of the thresholds, so it overlaps the threshold kernel on another stream.
+//
+// Warp-flattened: a warp takes 32 consecutive methods, stages their packed
+// used lists and origin values in shared memory, then scores the warp's
+// candidates (≈2 per method for C4) 32 at a time, one candidate per lane —
+// every lane issues its destination's 32-byte ClassRec load at once and the
+// per-method loop lengths no longer diverge. Each lane then reduces its own
+// method's candidates in destination order. Methods whose list did not fit
+// the record take the per-thread path (shared-memory list or streaming).
+constexpr int kCandPerWarp = 32 * kRecMaxEnt;
+
 template <int K>
-__global__ void __launch_bounds__(kSweepTile, 2) k_score(SweepArgs a) {
-    __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];  // K >= kRecMaxEnt
+struct ScoreSmem {
+    uint32_t X[K * kSweepTile];   // SmemEnum columns
+    uint32_t H[K * kSweepTile];
+    double lo_a[kSweepTile];
+    uint32_t org_bits[kSweepTile];  // bit0 coh_ok, bit1 co_a < co_b; bits 8-15 list length
+    uint32_t cd[kSweepTile / 32][kCandPerWarp];
+    double ckey[kSweepTile / 32][kCandPerWarp];
+    uint32_t ckp[kSweepTile / 32][kCandPerWarp];
+    uint8_t ch[kSweepTile / 32][kCandPerWarp];
+    uint8_t cl[kSweepTile / 32][kCandPerWarp];
+    uint8_t ck[kSweepTile / 32][kCandPerWarp];
+    uint8_t cres[kSweepTile / 32][kCandPerWarp];
+};
+
+template <int K>
+size_t score_smem_bytes() { return sizeof(ScoreSmem<K>); }
+
+template <int K>
+__global__ void __launch_bounds__(kSweepTile, 4) k_score(SweepArgs a) {
+    extern __shared__ __align__(16) unsigned char score_smem[];
+    ScoreSmem<K>& sm = *reinterpret_cast<ScoreSmem<K>*>(score_smem);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
     const bool valid = pos < a.pos_end;
-    uint32_t cands = 0;
+    uint32_t* myX = sm.X + threadIdx.x;
+    uint32_t* myH = sm.H + threadIdx.x;
+
+    uint32_t o = 0, n = 0, ncand = 0;
+    bool ovf = false;
+    sm.org_bits[threadIdx.x] = 0;
     if (valid) {
+        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
+        const uint4 r0 = rp[0], r1 = rp[1];
+        o = __ldg(a.pos_owner + pos);
+        const ClassRec ro = load_rec(a.rec, o);
+        ovf = (r0.x & kRecOverflow) != 0;
+        if (!ovf) {
+            const uint32_t ent[kRecMaxEnt] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+            n = rec_n(r0.x);
+#pragma unroll
+            for (int k = 0; k < kRecMaxEnt; ++k)
+                if (k < (int)n) {
+                    myX[k * kSweepTile] = ent[k] >> 8;
+                    myH[k * kSweepTile] = ent[k] & 0xffu;
+                    ncand += (ent[k] >> 8) != o;
+                }
+            const SmemEnum en{myX, myH, (int)n};
+            const uint32_t removed = (r0.x & kRecRemovedValid) ? rec_removed(r0.x)
+                                                                : removed_count(ro, a.ux, a.un, en, o);
+            const Origin org = make_origin(ro, rec_hown(r0.x), removed);
+            sm.lo_a[threadIdx.x] = org.lo_a;
+            sm.org_bits[threadIdx.x] = (org.coh_ok ? 1u : 0u) | (org.co_a < org.co_b ? 2u : 0u) | (n << 8);
+        }
+    }
+    // flatten the warp's candidates: (destination, accesses owned by it, owner lane, list index)
+    uint32_t excl = ncand;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, excl, d);
+        if (lane >= d) excl += y;
+    }
+    const uint32_t T = __shfl_sync(0xffffffffu, excl, 31);
+    excl -= ncand;
+    {
+        uint32_t w = excl;
+        for (uint32_t k = 0; k < n; ++k) {
+            const uint32_t X = myX[k * kSweepTile];
+            if (X == o) continue;
+            sm.cd[warp][w] = X;
+            sm.ch[warp][w] = (uint8_t)myH[k * kSweepTile];
+            sm.cl[warp][w] = (uint8_t)lane;
+            sm.ck[warp][w] = (uint8_t)k;
+            ++w;
+        }
+    }
+    __syncwarp();
+    for (uint32_t r = 0; r < T; r += 32) {
+        const uint32_t idx = r + lane;
+        if (idx < T) {
+            const uint32_t d = sm.cd[warp][idx];
+            const int ot = warp * 32 + sm.cl[warp][idx];
+            const uint32_t bits = sm.org_bits[ot];
+            uint8_t res = 0;
+            double key = 0.0;
+            uint32_t kp = 0;
+            if (bits & 3u) {  // otherwise neither criterion can pass: scored without a load
+                const ClassRec rd = load_rec(a.rec, d);
+                double ld_a;
+                if ((bits & 1u) && coh_dest(rd, sm.ch[warp][idx], ld_a)) {
+                    res |= 1u;
+                    key = __dadd_rn(sm.lo_a[ot], ld_a);  // lcom_key, suggest.hpp:194-196
+                }
+                if (bits & 2u) {  // passes iff every other used class is already in U[d]
+                    const uint32_t on = (bits >> 8) & 0xffu;
+                    bool ok = true;
+                    for (uint32_t k = 0; k < on && ok; ++k) {
+                        const uint32_t X = sm.X[ot + k * kSweepTile];
+                        if (X != d && !in_urow(a.rec, d, rd, a.ux, X)) ok = false;
+                    }
+                    if (ok) res |= 2u;
+                }
+                kp = rd.cbo;  // cbo_dest_after when coupling passes
+            }
+            sm.cres[warp][idx] = res;
+            sm.ckey[warp][idx] = key;
+            sm.ckp[warp][idx] = kp;
+        }
+    }
+    __syncwarp();
+
+    // each lane reduces its own method's candidates, destinations ascending
+    uint32_t cands = 0;
+    if (valid && !ovf) {
+        cands = ncand;
+        uint32_t bd_coh = kNone, bd_coup = kNone, best_coup = 0;
+        double best_coh = 0.0;
+        uint32_t m_coh = 0, m_coup = 0;
+        for (uint32_t j = excl; j < excl + ncand; ++j) {
+            const uint32_t res = sm.cres[warp][j];
+            const uint32_t d = sm.cd[warp][j];
+            // argmin over (key, d) with strict < : lowest d wins ties (suggest.hpp:180-184)
+            if ((res & 1u) && (bd_coh == kNone || sm.ckey[warp][j] < best_coh)) { bd_coh = d; best_coh = sm.ckey[warp][j]; }
+            if ((res & 2u) && (bd_coup == kNone || sm.ckp[warp][j] < best_coup)) { bd_coup = d; best_coup = sm.ckp[warp][j]; }
+            if (res & 1u) m_coh |= 1u << sm.ck[warp][j];
+            if (res & 2u) m_coup |= 1u << sm.ck[warp][j];
+        }
+        uint4 out;
+        if (a.mode == 0) {
+            out = make_uint4(bd_coh, bd_coup, ncand, 0);
+        } else {
+            if (a.mode == 1) {  // keep the top-k of each criterion by (key, d)
+                for (int c = 0; c < 2; ++c) {
+                    const uint32_t all = c == 0 ? m_coh : m_coup;
+                    uint32_t keep = 0;
+                    for (uint32_t t = 0; t < a.topk; ++t) {
+                        int best = -1;
+                        double bk = 0.0;
+                        for (uint32_t j = excl; j < excl + ncand; ++j) {
+                            const uint32_t bit = 1u << sm.ck[warp][j];
+                            if (!(all & bit) || (keep & bit)) continue;
+                            const double key = c == 0 ? sm.ckey[warp][j] : (double)sm.ckp[warp][j];
+                            if (best < 0 || key < bk) { best = (int)sm.ck[warp][j]; bk = key; }
+                        }
+                        if (best < 0) break;
+                        keep |= 1u << best;
+                    }
+                    (c == 0 ? m_coh : m_coup) = keep;
+                }
+            }
+            out = make_uint4(m_coh, m_coup, ncand, 0);
+        }
+        a.res[pos] = out;
+    } else if (valid) {
+        // per-thread path for lists the record could not hold
         const uint32_t p = __ldg(a.s.cls_methods + pos);
-        const uint32_t o = __ldg(a.pos_owner + pos);
-        SmemEnum ren;
-        ren.X = s_X + threadIdx.x;
-        ren.H = s_H + threadIdx.x;
-        ren.n = 0;
+        SmemEnum ren{myX, myH, 0};
         StreamEnum sen;
         Origin org;
         MethodResult r;
@@ -424,15 +578,15 @@ __global__ void __launch_bounds__(kSweepTile, 2) k_score(SweepArgs a) {
         a.res[pos] = out;
     }
     const uint32_t wc = __reduce_add_sync(0xffffffffu, cands);
-    if ((threadIdx.x & 31) == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
+    if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
 }
 
-// Pass 2: apply the class gates (suggest.hpp:246, :273), merge the criteria
-// (union / intersection, :315-341), and write the records in (origin,
-// method, destination) order at offsets from a decoupled look-back scan.
-template <int K>
-__global__ void __launch_bounds__(kSweepTile) k_emit(SweepArgs a) {
-    __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
+// Pass 2: apply the class gates (suggest.hpp:246, :273) and the criteria
+// merge (union / intersection, :315-341) to each method's pass-1 result,
+// then a tile scan + decoupled look-back gives every method the global offset
+// of its first record. Light per-thread work, so the look-back chain is short;
+// the result (gated selection, count, offset) replaces res[pos] in place.
+__global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_warp[kSweepTile / 32];
     __shared__ unsigned long long s_excl;
@@ -446,31 +600,29 @@ __global__ void __launch_bounds__(kSweepTile) k_emit(SweepArgs a) {
 
     double thr_l = a.thr_lcom, thr_c = a.thr_cbo;
     if (a.thr_device) { thr_l = a.dthr->lcom; thr_c = a.dthr->cbo; }
-
     const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
     const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
-    uint32_t o = 0, count = 0, gated = 0;
-    MethodResult res{};
+
+    uint32_t count = 0, gated = 0;
+    uint4 r = make_uint4(0, 0, 0, 0);
     if (valid) {
-        const uint4 r = a.res[pos];
-        o = __ldg(a.pos_owner + pos);
+        r = a.res[pos];
+        const uint32_t o = __ldg(a.pos_owner + pos);
         const bool gcoh = (a.crit & MM_CRIT_COHESION) && __ldg(a.lcom + o) > thr_l;
         const bool gcoup = (a.crit & MM_CRIT_COUPLING) && (double)__ldg(a.cbo + o) > thr_c;
         gated = r.z * ((gcoh ? 1u : 0u) + (gcoup ? 1u : 0u));
         if (a.mode == 0) {
-            res.bd_coh = gcoh ? r.x : kNone;
-            res.bd_coup = gcoup ? r.y : kNone;
-            const bool same = res.bd_coh != kNone && res.bd_coh == res.bd_coup;
-            count = inter ? (same ? 1u : 0u)
-                          : (uint32_t)(res.bd_coh != kNone) + (uint32_t)(res.bd_coup != kNone) - (same ? 1u : 0u);
+            const uint32_t bc = gcoh ? r.x : kNone, bp = gcoup ? r.y : kNone;
+            const bool same = bc != kNone && bc == bp;
+            count = inter ? (same ? 1u : 0u) : (uint32_t)(bc != kNone) + (uint32_t)(bp != kNone) - (same ? 1u : 0u);
+            r.x = bc;
+            r.y = bp;
         } else {
-            res.m_coh = gcoh ? r.x : 0u;
-            res.m_coup = gcoup ? r.y : 0u;
-            count = __popcll(inter ? (res.m_coh & res.m_coup) : (res.m_coh | res.m_coup));
+            r.x = gcoh ? r.x : 0u;
+            r.y = gcoup ? r.y : 0u;
+            count = __popc(inter ? (r.x & r.y) : (r.x | r.y));
         }
     }
-
-    // tile-wide exclusive scan of record counts
     const uint32_t inc = warp_incl_scan(count, lane);
     if (lane == 31) s_warp[warp] = inc;
     {
@@ -490,7 +642,6 @@ __global__ void __launch_bounds__(kSweepTile) k_emit(SweepArgs a) {
         agg += s_warp[w];
     }
     const uint32_t texcl = before + inc - count;
-
     // decoupled look-back: warp 0 inspects 32 predecessor tiles per step
     // (relaxed gpu-scope loads; flag and value share one 64-bit word)
     if (warp == 0) {
@@ -528,18 +679,32 @@ __global__ void __launch_bounds__(kSweepTile) k_emit(SweepArgs a) {
         }
     }
     __syncthreads();
-    if (valid && count) {
-        const uint32_t p = __ldg(a.s.cls_methods + pos);
-        SmemEnum ren;
-        ren.X = s_X + threadIdx.x;
-        ren.H = s_H + threadIdx.x;
-        ren.n = 0;
-        StreamEnum sen;
-        Origin org;
-        const uint64_t at = s_excl + texcl;
-        if (load_method<K>(a, (uint32_t)pos, p, o, ren, sen, org)) emit(a, ren, p, o, org, res, at);
-        else emit(a, sen, p, o, org, res, at);
+    if (valid) {
+        r.z = count;
+        r.w = (uint32_t)(s_excl + texcl);
+        a.res[pos] = r;
     }
+}
+
+// Pass 3: each emitting method writes its records (exact what-if values)
+// at its offset. One thread per method, no barriers.
+template <int K>
+__global__ void __launch_bounds__(kSweepTile) k_write(SweepArgs a) {
+    __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
+    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
+    if (pos >= a.pos_end) return;
+    const uint4 r = a.res[pos];
+    if (!r.z) return;
+    const uint32_t o = __ldg(a.pos_owner + pos);
+    const uint32_t p = __ldg(a.s.cls_methods + pos);
+    MethodResult res{};
+    if (a.mode == 0) { res.bd_coh = r.x; res.bd_coup = r.y; }
+    else { res.m_coh = r.x; res.m_coup = r.y; }
+    SmemEnum ren{s_X + threadIdx.x, s_H + threadIdx.x, 0};
+    StreamEnum sen;
+    Origin org;
+    if (load_method<K>(a, (uint32_t)pos, p, o, ren, sen, org)) emit(a, ren, p, o, org, res, r.w);
+    else emit(a, sen, p, o, org, res, r.w);
 }
 
 __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const uint32_t* __restrict__ ux,
@@ -576,14 +741,25 @@ __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const ui
 
 void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     if (!n_tiles) return;
-    if (a.maxdeg_fast <= 8) k_score<8><<<n_tiles, kSweepTile, 0, st>>>(a);
-    else k_score<16><<<n_tiles, kSweepTile, 0, st>>>(a);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_score<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes<8>());
+        cudaFuncSetAttribute(k_score<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes<16>());
+        attr = true;
+    }
+    if (a.maxdeg_fast <= 8) k_score<8><<<n_tiles, kSweepTile, score_smem_bytes<8>(), st>>>(a);
+    else k_score<16><<<n_tiles, kSweepTile, score_smem_bytes<16>(), st>>>(a);
 }
 
-void launch_emit(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
+void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     if (!n_tiles) return;
-    if (a.maxdeg_fast <= 8) k_emit<8><<<n_tiles, kSweepTile, 0, st>>>(a);
-    else k_emit<16><<<n_tiles, kSweepTile, 0, st>>>(a);
+    k_offsets<<<n_tiles, kSweepTile, 0, st>>>(a);
+}
+
+void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
+    if (!n_tiles) return;
+    if (a.maxdeg_fast <= 8) k_write<8><<<n_tiles, kSweepTile, 0, st>>>(a);
+    else k_write<16><<<n_tiles, kSweepTile, 0, st>>>(a);
 }
 
 void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un, uint32_t u,

@@ -92,7 +92,7 @@ struct mm_ctx {
     DBuf<uint64_t> gkeys;
     DBuf<uint32_t> grows;
     // derived
-    DBuf<uint32_t> attr_local, inv, cbo, ux, un;
+    DBuf<uint32_t> cbo, ux, un;
     DBuf<MethRec> recs;
     DBuf<uint64_t> own_mask;
     DBuf<uint32_t> pos_owner;
@@ -189,7 +189,7 @@ void resolve_pending(mm_ctx* ctx) {
 void free_model(mm_ctx* c) {
     for (DBuf<uint32_t>* b : {&c->method_owner, &c->attribute_owner, &c->cls_moff, &c->cls_methods, &c->cls_aoff,
                               &c->cls_attrs, &c->call_off, &c->call_tgt, &c->acc_off, &c->acc_tgt,
-                              &c->large_list, &c->foreign, &c->grows, &c->attr_local, &c->inv, &c->cbo, &c->ux,
+                              &c->large_list, &c->foreign, &c->grows, &c->cbo, &c->ux,
                               &c->un})
         b->release();
     c->recs.release();
@@ -432,8 +432,6 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         MM_CUDA(ctx, set_class_large_smem(ctx->large_smem));
     }
     // derived tables
-    MM_CUDA(ctx, ctx->attr_local.ensure(A ? A : 1));
-    MM_CUDA(ctx, ctx->inv.ensure(M ? M : 1));
     MM_CUDA(ctx, ctx->recs.ensure(M ? M : 1));
     MM_CUDA(ctx, ctx->own_mask.ensure(M ? M : 1));
     MM_CUDA(ctx, ctx->pos_owner.ensure(M ? M : 1));
@@ -457,22 +455,19 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
     Ctl* ctl = ctx->ctl.p;
     MM_CUDA(ctx, cudaMemsetAsync(&ctl->ucursor, 0, sizeof(uint32_t), ctx->stream));
     const DevModel dm = ctx->dev();
-    mm_status st = run(ctx, "layout", [&] { launch_layout(dm, ctx->inv.p, ctx->attr_local.p, ctx->stream); });
-    if (st) return st;
-    st = run(ctx, "method", [&] {
-        launch_method(dm, ctx->max_deg, ctx->inv.p, ctx->attr_local.p, ctx->recs.p, ctx->own_mask.p,
-                      ctx->pos_owner.p, ctx->stream);
+    mm_status st = run(ctx, "method", [&] {
+        launch_method(dm, ctx->max_deg, ctx->recs.p, ctx->own_mask.p, ctx->pos_owner.p, ctx->stream);
     });
     if (st) return st;
     st = run(ctx, "class_small", [&] {
-        launch_class_small(dm, ctx->kind.p, ctx->attr_local.p, ctx->recs.p, ctx->own_mask.p, ctx->rec.p, ctx->lcom.p,
-                           ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p, &ctl->ucursor, ctx->stream);
+        launch_class_small(dm, ctx->kind.p, ctx->recs.p, ctx->own_mask.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p,
+                           ctx->cbo.p, ctx->ux.p, ctx->un.p, &ctl->ucursor, ctx->stream);
     });
     if (st) return st;
     if (ctx->n_large) {
         st = run(ctx, "class_large", [&] {
             launch_class_large(dm, ctx->n_large, ctx->large_list.p, ctx->plans.p, ctx->large_smem,
-                               ctx->attr_local.p, ctx->recs.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
+                               ctx->recs.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
                                ctx->un.p, &ctl->ucursor, ctx->gkeys.p, ctx->grows.p, ctx->stream);
         });
         if (st) return st;
@@ -643,7 +638,9 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     if (st) return st;
     if (a.thr_device)
         if (mm_status s2 = join_thresholds(ctx)) return s2;
-    st = run(ctx, "emit", [&] { launch_emit(a, n_tiles, ctx->stream); });
+    st = run(ctx, "offsets", [&] { launch_offsets(a, n_tiles, ctx->stream); });
+    if (st) return st;
+    st = run(ctx, "write", [&] { launch_write(a, n_tiles, ctx->stream); });
     if (st) return st;
     ctx->sweep_valid = true;
     if (n_out) {

@@ -48,14 +48,13 @@ void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st);
 void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list, uint32_t* n_large,
                          uint32_t* max_deg, uint32_t* foreign, cudaStream_t st);
-void launch_layout(const DevModel& s, uint32_t* inv, uint32_t* attr_local, cudaStream_t st);
-void launch_method(const DevModel& s, uint32_t maxdeg, const uint32_t* inv, const uint32_t* attr_local,
-                   MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner, cudaStream_t st);
-void launch_class_small(const DevModel& s, const uint8_t* kind, const uint32_t* attr_local, MethRec* recs,
-                        const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo,
-                        uint32_t* ux, uint32_t* un, uint32_t* ucursor, cudaStream_t st);
+void launch_method(const DevModel& s, uint32_t maxdeg, MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner,
+                   cudaStream_t st);
+void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, const uint64_t* own_mask,
+                        ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,
+                        uint32_t* ucursor, cudaStream_t st);
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
-                        uint32_t smem_bytes, const uint32_t* attr_local, MethRec* recs, ClassRec* rec, double* lcom,
+                        uint32_t smem_bytes, MethRec* recs, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
                         uint64_t* gkeys, uint32_t* grows, cudaStream_t st);
 cudaError_t set_class_large_smem(uint32_t bytes);
@@ -64,7 +63,8 @@ size_t thresholds_scratch_bytes(uint32_t n);
 cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
                               void* scratch, size_t scratch_bytes, cudaStream_t st);
 void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
-void launch_emit(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
+void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
+void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 constexpr uint32_t kSweepTile = 256;
 void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un,
                     uint32_t u, uint32_t o, uint32_t d, mm_whatif* out, cudaStream_t st);
