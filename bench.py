@@ -96,23 +96,30 @@ def algorithmic_bytes(sys_, nnz_u: int, n_sugg: int, rank_share: float = 1.0) ->
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi clocks + throttle reasons around the timed region (B200_PROFILING.md).
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Sampling starts before the warm-up (nvidia-smi needs ~0.1-0.3 s to emit its
+    first row); `wait_for_samples` lets the caller extend the warm-up until it
+    is live, and `summary` keeps the rows stamped inside the timed window
+    (widened by one sampling interval on each side)."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    PERIOD_MS = 20
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -126,23 +133,55 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self) -> dict:
+    def _rows(self):
         rows = []
         try:
             for line in Path(self.path).read_text().splitlines():
                 f = [x.strip() for x in line.split(",")]
-                if len(f) >= 9:
+                if len(f) >= 10:
                     rows.append(f)
         except OSError:
             pass
-        if not rows:
+        return rows
+
+    def wait_for_samples(self, n: int = 2, timeout_s: float = 3.0) -> bool:
+        t = time.time()
+        while self.proc and time.time() - t < timeout_s:
+            if len(self._rows()) >= n:
+                return True
+            time.sleep(0.02)
+        return False
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+        self.wait_for_samples(len(self._rows()) + 1, 1.0)
+
+    def summary(self) -> dict:
+        import datetime
+        rows = self._rows()
+        sel = []
+        slack = 2 * self.PERIOD_MS / 1e3
+        for r in rows:
+            try:
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                continue
+            if self.t0 is not None and self.t0 - slack <= ts <= (self.t1 or ts) + slack:
+                sel.append(r)
+        window = "timed region"
+        if not sel and rows:
+            sel, window = rows[-5:], "adjacent (timed region shorter than the sampling period)"
+        if not sel:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[2]) for r in sel if r[2].replace(".", "").isdigit()]
+        mx = [float(r[3]) for r in sel if r[3].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        reasons = sorted({n for r in sel for n, v in zip(names, r[6:10]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(sel), "window": window}
 
 
 # ---------------------------------------------------------------------------
@@ -258,9 +297,15 @@ def run_ours(args) -> None:
         n_local = eng.sweep(thresholds=None, class_range=shard, want_count=True)
         return gather(n_local)
 
+    clocks = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
+    # keep warming up (bounded) until the clock sampler is emitting rows
+    t_w = time.time()
+    while not clocks.wait_for_samples(2, 0.0) and time.time() - t_w < 3.0:
+        step()
+        torch.cuda.synchronize(dev)
     st = eng.sweep_stats()
     n_sugg_local = st["suggestions"]
     eng.set_profiling(True)
@@ -270,13 +315,15 @@ def run_ours(args) -> None:
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clocks:
-        for i in range(args.steps):
-            flush.fill_(i)  # evict L2 (256 MiB write) outside the timed interval
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
-        torch.cuda.synchronize(dev)
+    clocks.mark_start()
+    for i in range(args.steps):
+        flush.fill_(i)  # evict L2 (256 MiB write) outside the timed interval
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.mark_end()
+    clocks.__exit__(None, None, None)
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
@@ -401,7 +448,7 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")

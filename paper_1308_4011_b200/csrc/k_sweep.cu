@@ -21,6 +21,7 @@
 // 256-method tiles: no atomics on the data, deterministic placement.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "mm_device.cuh"
@@ -584,49 +585,70 @@ __global__ void __launch_bounds__(kSweepTile, 4) k_score(SweepArgs a) {
 // Pass 2: apply the class gates (suggest.hpp:246, :273) and the criteria
 // merge (union / intersection, :315-341) to each method's pass-1 result,
 // then a tile scan + decoupled look-back gives every method the global offset
-// of its first record. Light per-thread work, so the look-back chain is short;
-// the result (gated selection, count, offset) replaces res[pos] in place.
+// of its first record and every EMITTING method a slot in a compact emitter
+// list (both counts travel packed in one 64-bit look-back word). 1024
+// methods per tile (4 per thread) keep the look-back chain short; the result
+// (gated selection, count, offset) replaces res[pos] in place.
+constexpr int kOffItems = 4;
+constexpr uint32_t kOffTile = kSweepTile * kOffItems;
+
 __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
     __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_warp[kSweepTile / 32];
+    __shared__ unsigned long long s_warp[kSweepTile / 32];
     __shared__ unsigned long long s_excl;
     __shared__ unsigned long long s_red[2][kSweepTile / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
-    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)tile * kSweepTile + threadIdx.x;
-    const bool valid = pos < a.pos_end;
+    const uint64_t pos0 = (uint64_t)a.pos_begin + (uint64_t)tile * kOffTile + (uint64_t)threadIdx.x * kOffItems;
 
     double thr_l = a.thr_lcom, thr_c = a.thr_cbo;
     if (a.thr_device) { thr_l = a.dthr->lcom; thr_c = a.dthr->cbo; }
     const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
     const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
 
-    uint32_t count = 0, gated = 0;
-    uint4 r = make_uint4(0, 0, 0, 0);
-    if (valid) {
-        r = a.res[pos];
+    uint4 r[kOffItems];
+    uint32_t cnt[kOffItems];
+    unsigned long long mine = 0, gated = 0, nvalid = 0;  // packed (emitters << 32) | records
+#pragma unroll
+    for (int it = 0; it < kOffItems; ++it) {
+        const uint64_t pos = pos0 + it;
+        cnt[it] = 0;
+        r[it] = make_uint4(0, 0, 0, 0);
+        if (pos >= a.pos_end) continue;
+        ++nvalid;
+        uint4 v = a.res[pos];
         const uint32_t o = __ldg(a.pos_owner + pos);
         const bool gcoh = (a.crit & MM_CRIT_COHESION) && __ldg(a.lcom + o) > thr_l;
         const bool gcoup = (a.crit & MM_CRIT_COUPLING) && (double)__ldg(a.cbo + o) > thr_c;
-        gated = r.z * ((gcoh ? 1u : 0u) + (gcoup ? 1u : 0u));
+        gated += v.z * ((gcoh ? 1u : 0u) + (gcoup ? 1u : 0u));
+        uint32_t count;
         if (a.mode == 0) {
-            const uint32_t bc = gcoh ? r.x : kNone, bp = gcoup ? r.y : kNone;
+            const uint32_t bc = gcoh ? v.x : kNone, bp = gcoup ? v.y : kNone;
             const bool same = bc != kNone && bc == bp;
             count = inter ? (same ? 1u : 0u) : (uint32_t)(bc != kNone) + (uint32_t)(bp != kNone) - (same ? 1u : 0u);
-            r.x = bc;
-            r.y = bp;
+            v.x = bc;
+            v.y = bp;
         } else {
-            r.x = gcoh ? r.x : 0u;
-            r.y = gcoup ? r.y : 0u;
-            count = __popc(inter ? (r.x & r.y) : (r.x | r.y));
+            v.x = gcoh ? v.x : 0u;
+            v.y = gcoup ? v.y : 0u;
+            count = __popc(inter ? (v.x & v.y) : (v.x | v.y));
         }
+        r[it] = v;
+        cnt[it] = count;
+        mine += count + (count ? (1ull << 32) : 0ull);
     }
-    const uint32_t inc = warp_incl_scan(count, lane);
+    // block scan of the packed pair
+    unsigned long long inc = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+    }
     if (lane == 31) s_warp[warp] = inc;
     {
-        unsigned long long g0 = gated, g1 = valid ? 1ull : 0ull;
+        unsigned long long g0 = gated, g1 = nvalid;
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             g0 += __shfl_down_sync(0xffffffffu, g0, d);
@@ -635,13 +657,13 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
         if (lane == 0) { s_red[0][warp] = g0; s_red[1][warp] = g1; }
     }
     __syncthreads();
-    uint32_t before = 0, agg = 0;
+    unsigned long long before = 0, agg = 0;
 #pragma unroll
     for (int w = 0; w < kSweepTile / 32; ++w) {
         if (w < warp) before += s_warp[w];
         agg += s_warp[w];
     }
-    const uint32_t texcl = before + inc - count;
+    const unsigned long long texcl = before + inc - mine;
     // decoupled look-back: warp 0 inspects 32 predecessor tiles per step
     // (relaxed gpu-scope loads; flag and value share one 64-bit word)
     if (warp == 0) {
@@ -674,37 +696,46 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
             unsigned long long t0 = 0, t1 = 0;
             for (int w = 0; w < kSweepTile / 32; ++w) { t0 += s_red[0][w]; t1 += s_red[1][w]; }
             atomicAdd(a.stats + 1, t0);
-            atomicAdd(a.stats + 2, (unsigned long long)agg);
+            atomicAdd(a.stats + 2, agg & 0xffffffffull);
             atomicAdd(a.stats + 3, t1);
+            atomicAdd(a.n_emit, (uint32_t)(agg >> 32));
         }
     }
     __syncthreads();
-    if (valid) {
-        r.z = count;
-        r.w = (uint32_t)(s_excl + texcl);
-        a.res[pos] = r;
+    unsigned long long at = s_excl + texcl;
+#pragma unroll
+    for (int it = 0; it < kOffItems; ++it) {
+        const uint64_t pos = pos0 + it;
+        if (pos >= a.pos_end) continue;
+        uint4 v = r[it];
+        v.z = cnt[it];
+        v.w = (uint32_t)(at & 0xffffffffull);
+        a.res[pos] = v;
+        if (cnt[it]) a.emit_list[at >> 32] = (uint32_t)pos;
+        at += cnt[it] + (cnt[it] ? (1ull << 32) : 0ull);
     }
 }
 
-// Pass 3: each emitting method writes its records (exact what-if values)
-// at its offset. One thread per method, no barriers.
+// Pass 3: the emitting methods (compact list from pass 2) write their
+// records — exact what-if values — at their offsets. One thread per emitter.
 template <int K>
 __global__ void __launch_bounds__(kSweepTile) k_write(SweepArgs a) {
     __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
-    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
-    if (pos >= a.pos_end) return;
-    const uint4 r = a.res[pos];
-    if (!r.z) return;
-    const uint32_t o = __ldg(a.pos_owner + pos);
-    const uint32_t p = __ldg(a.s.cls_methods + pos);
-    MethodResult res{};
-    if (a.mode == 0) { res.bd_coh = r.x; res.bd_coup = r.y; }
-    else { res.m_coh = r.x; res.m_coup = r.y; }
-    SmemEnum ren{s_X + threadIdx.x, s_H + threadIdx.x, 0};
-    StreamEnum sen;
-    Origin org;
-    if (load_method<K>(a, (uint32_t)pos, p, o, ren, sen, org)) emit(a, ren, p, o, org, res, r.w);
-    else emit(a, sen, p, o, org, res, r.w);
+    const uint32_t n = *a.n_emit;
+    for (uint32_t i = blockIdx.x * kSweepTile + threadIdx.x; i < n; i += gridDim.x * kSweepTile) {
+        const uint32_t pos = a.emit_list[i];
+        const uint4 r = a.res[pos];
+        const uint32_t o = __ldg(a.pos_owner + pos);
+        const uint32_t p = __ldg(a.s.cls_methods + pos);
+        MethodResult res{};
+        if (a.mode == 0) { res.bd_coh = r.x; res.bd_coup = r.y; }
+        else { res.m_coh = r.x; res.m_coup = r.y; }
+        SmemEnum ren{s_X + threadIdx.x, s_H + threadIdx.x, 0};
+        StreamEnum sen;
+        Origin org;
+        if (load_method<K>(a, pos, p, o, ren, sen, org)) emit(a, ren, p, o, org, res, r.w);
+        else emit(a, sen, p, o, org, res, r.w);
+    }
 }
 
 __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const uint32_t* __restrict__ ux,
@@ -751,6 +782,8 @@ void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     else k_score<16><<<n_tiles, kSweepTile, score_smem_bytes<16>(), st>>>(a);
 }
 
+uint32_t offsets_tiles(uint64_t npos) { return (uint32_t)((npos + kOffTile - 1) / kOffTile); }
+
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     if (!n_tiles) return;
     k_offsets<<<n_tiles, kSweepTile, 0, st>>>(a);
@@ -758,8 +791,9 @@ void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
 
 void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     if (!n_tiles) return;
-    if (a.maxdeg_fast <= 8) k_write<8><<<n_tiles, kSweepTile, 0, st>>>(a);
-    else k_write<16><<<n_tiles, kSweepTile, 0, st>>>(a);
+    const uint32_t grid = std::min<uint32_t>(n_tiles, 148 * 8);  // grid-stride over the emitter list
+    if (a.maxdeg_fast <= 8) k_write<8><<<grid, kSweepTile, 0, st>>>(a);
+    else k_write<16><<<grid, kSweepTile, 0, st>>>(a);
 }
 
 void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un, uint32_t u,

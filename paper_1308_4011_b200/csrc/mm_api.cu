@@ -29,7 +29,8 @@ struct Ctl {  // small device-resident control block
     uint32_t ucursor;
     uint32_t tile_counter;
     uint32_t err;
-    uint32_t pad[2];
+    uint32_t n_emit;
+    uint32_t pad;
     unsigned long long stats[4];
     DevThresholds thr;
 };
@@ -97,6 +98,7 @@ struct mm_ctx {
     DBuf<uint64_t> own_mask;
     DBuf<uint32_t> pos_owner;
     DBuf<uint4> res;
+    DBuf<uint32_t> emit_list;
     DBuf<double> gate_lcom;
     DBuf<uint32_t> gate_cbo;
     bool gates_set = false;
@@ -275,6 +277,7 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     ctx->tile_state.release();
     ctx->out.release();
     ctx->res.release();
+    ctx->emit_list.release();
     ctx->gate_lcom.release();
     ctx->gate_cbo.release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -601,10 +604,12 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     const uint64_t cap = std::max<uint64_t>(1, mode == 2 ? Etot : std::min(per * npos, Etot));
     MM_CUDA(ctx, ctx->out.ensure(cap));
     const uint32_t n_tiles = (uint32_t)((npos + kSweepTile - 1) / kSweepTile);
-    MM_CUDA(ctx, ctx->tile_state.ensure(n_tiles ? n_tiles : 1));
+    const uint32_t n_off = offsets_tiles(npos);
+    MM_CUDA(ctx, ctx->tile_state.ensure(n_off ? n_off : 1));
     MM_CUDA(ctx, ctx->res.ensure(npos ? npos : 1));
+    MM_CUDA(ctx, ctx->emit_list.ensure(npos ? npos : 1));
     Ctl* ctl = ctx->ctl.p;
-    if (n_tiles) MM_CUDA(ctx, cudaMemsetAsync(ctx->tile_state.p, 0, 8ull * n_tiles, ctx->stream));
+    if (n_off) MM_CUDA(ctx, cudaMemsetAsync(ctx->tile_state.p, 0, 8ull * n_off, ctx->stream));
     // tile_counter, err, pad, stats
     MM_CUDA(ctx, cudaMemsetAsync(&ctl->tile_counter, 0, offsetof(Ctl, thr) - offsetof(Ctl, tile_counter),
                                  ctx->stream));
@@ -616,6 +621,8 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     a.lcom = ctx->gates_set ? ctx->gate_lcom.p : ctx->lcom.p;
     a.cbo = ctx->gates_set ? ctx->gate_cbo.p : ctx->cbo.p;
     a.res = ctx->res.p - pb;  // indexed by absolute position
+    a.emit_list = ctx->emit_list.p;
+    a.n_emit = &ctl->n_emit;
     a.ux = ctx->ux.p;
     a.un = ctx->un.p;
     a.dthr = &ctl->thr;
@@ -638,7 +645,7 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     if (st) return st;
     if (a.thr_device)
         if (mm_status s2 = join_thresholds(ctx)) return s2;
-    st = run(ctx, "offsets", [&] { launch_offsets(a, n_tiles, ctx->stream); });
+    st = run(ctx, "offsets", [&] { launch_offsets(a, n_off, ctx->stream); });
     if (st) return st;
     st = run(ctx, "write", [&] { launch_write(a, n_tiles, ctx->stream); });
     if (st) return st;

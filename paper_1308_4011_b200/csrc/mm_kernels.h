@@ -26,6 +26,8 @@ struct SweepArgs {
     const double* lcom;         // per-class lcom (gates)
     const uint32_t* cbo;        // per-class cbo (gates)
     uint4* res;                 // per-position pass-1 result
+    uint32_t* emit_list;        // positions of emitting methods (pass 2)
+    uint32_t* n_emit;           // their count
     const uint32_t* ux;
     const uint32_t* un;
     const DevThresholds* dthr;  // used when thr_device != 0
@@ -63,6 +65,7 @@ size_t thresholds_scratch_bytes(uint32_t n);
 cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
                               void* scratch, size_t scratch_bytes, cudaStream_t st);
 void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
+uint32_t offsets_tiles(uint64_t npos);
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 constexpr uint32_t kSweepTile = 256;
