@@ -80,9 +80,9 @@ def algorithmic_bytes(sys_, nnz_u: int, n_sugg: int, rank_share: float = 1.0) ->
     ms = int(m * rank_share)
     k = {
         "method": 64 * m + 8 * a + 4 * E + 4 * c,
-        "class_small": 44 * m + 61 * c + 8 * nnz_u,
+        "class_small": 44 * m + 93 * c + 8 * nnz_u,
         "thresholds": 12 * c,
-        "score": 56 * ms + 32 * c + 4 * nnz_u,
+        "score": 56 * ms + 64 * c + 4 * nnz_u,
         "offsets": 36 * ms + 12 * c,
         "write": 20 * ms + 96 * n_sugg,
     }
