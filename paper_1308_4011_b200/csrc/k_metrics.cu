@@ -83,19 +83,9 @@ __global__ void k_plan_classes(DevModel s, uint8_t* __restrict__ kind, uint32_t*
 // (ClassRecord::attribute_ids, model.hpp:22): short lists are scanned with
 // independent loads (one round trip per 8 entries), long ones bisected.
 __device__ __forceinline__ uint32_t attr_pos(const DevModel& s, uint32_t ab, uint32_t ae, uint32_t t) {
-    const uint32_t len = ae - ab;
-    if (len <= 64) {
-        for (uint32_t k0 = 0; k0 < len; k0 += 8) {
-            uint32_t v[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = (k0 + j < len) ? __ldg(s.cls_attrs + ab + k0 + j) : kNone;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (v[j] == t) return k0 + j;
-        }
-        return kNone;
-    }
-    uint32_t lo = 0, hi = len;
+    // binary search of the sorted list: few instructions; the probes of
+    // neighbouring lanes (same class in class order) hit L1
+    uint32_t lo = 0, hi = ae - ab;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         if (__ldg(s.cls_attrs + ab + mid) < t) lo = mid + 1;
