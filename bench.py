@@ -416,9 +416,9 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
     def e2e_step():
         eng.upload(hs)                                   # H2D from pinned host + device validation + plan
         eng.compute_metrics()
-        lcom, ck, cbo = eng.class_metrics_all()          # D2H per-class metrics
+        lcom, ck, cbo = eng.class_metrics_all(copy=False)  # D2H per-class metrics (pinned)
         if world == 1:
-            recs = eng.suggest_all(eng.compute_thresholds())  # sweep + D2H of the ordered list
+            recs = eng.suggest_all(eng.compute_thresholds(), copy=False)  # sweep + D2H of the ordered list
         else:
             eng.sweep(thresholds=None, class_range=shard, want_count=False)
             n_local = eng.sweep_stats()["suggestions"]

@@ -248,6 +248,12 @@ mm_status mm_copy_suggestions(mm_ctx* ctx, mm_suggestion* out, uint64_t cap, uin
 mm_status mm_suggest(mm_ctx* ctx, const mm_sweep_params* p, mm_suggestion* out, uint64_t cap,
                      uint64_t* n_out);
 
+/* Page-locked host buffers for the caller's inputs/outputs: copies from/to
+ * pinned memory run at full DMA rate (pageable memory is staged by the
+ * driver). */
+mm_status mm_pinned_alloc(uint64_t bytes, void** out);
+void mm_pinned_free(void* p);
+
 /* ---- host-side helpers (no GPU needed) --------------------------------- */
 /* Contiguous class ranges balanced by sweep cost (Σ over members of
  * 1 + |calls| + |accesses|), the GPU analogue of plan_partition

@@ -6,7 +6,10 @@ from pathlib import Path
 
 from . import abi
 
-_LIB_PATH = Path(__file__).resolve().parent / "libmmgpu.so"
+import os
+
+# MMGPU_LIB: an alternative build of the same library (A/B experiments); default in-tree
+_LIB_PATH = Path(os.environ.get("MMGPU_LIB") or (Path(__file__).resolve().parent / "libmmgpu.so"))
 _lib = None
 
 
@@ -58,6 +61,8 @@ _SIGS = {
     "mm_copy_suggestions": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
     "mm_suggest": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_params), C.c_void_p, C.c_uint64,
                              C.POINTER(C.c_uint64)]),
+    "mm_pinned_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
+    "mm_pinned_free": (None, [C.c_void_p]),
     "mm_plan_shards": (C.c_int, [C.POINTER(abi.mm_system), C.c_uint32, C.POINTER(C.c_uint32)]),
     "mm_generate": (C.c_int, [C.POINTER(abi.mm_gen_config), C.POINTER(C.c_void_p)]),
     "mm_host_system_view": (C.POINTER(abi.mm_system), [C.c_void_p]),

@@ -362,9 +362,11 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind,
     }
     __syncwarp();
     removed_me = rem[lane];
-    uint32_t ubase = 0;
-    if (lane == 0 && cbo) ubase = atomicAdd(ucursor, cbo);  // slot reservation
-    ubase = __shfl_sync(0xffffffffu, ubase, 0);
+    // static row slot: a small class has at most kSmallRowCap foreign classes per
+    // member, so rows placed at kSmallRowCap · (first member position) never
+    // overlap — no contended global atomic per class
+    const uint32_t ubase = kSmallRowCap * mb;
+    (void)ucursor;
     for (uint32_t k = lane; k < cbo; k += 32) {
         ux[ubase + k] = buf[k];
         un[ubase + k] = rcnt[k];
@@ -502,7 +504,9 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         block_excl_scan(xh ? 1u : 0u, red32, &tot);
         nx += tot;
     }
-    if (threadIdx.x == 0) s_ubase = nx ? atomicAdd(ucursor, nx) : 0u;
+    // large classes reserve their rows past the small-class region (few, so the
+    // atomic is uncontended): the paper's atomicAdd slot reservation
+    if (threadIdx.x == 0) s_ubase = kSmallRowCap * s.M + (nx ? atomicAdd(ucursor, nx) : 0u);
     __syncthreads();
     const uint32_t ubase = s_ubase;
     uint32_t xcarry = 0;

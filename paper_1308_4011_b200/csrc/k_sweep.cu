@@ -22,11 +22,15 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "mm_device.cuh"
 #include "mm_kernels.h"
 
+#ifndef MMGPU_SCORE_MINB
+#define MMGPU_SCORE_MINB 6
+#endif
 namespace mmg {
 
 namespace {
@@ -494,7 +498,8 @@ __global__ void __launch_bounds__(kSweepTile, 4) k_score(SweepArgs a) {
             double key = 0.0;
             uint32_t kp = 0;
             if (bits & 3u) {  // otherwise neither criterion can pass: scored without a load
-                const ClassRec rd = load_rec(a.rec, d);
+                const ClassRecFull rf = load_rec_full(a.rec, d);  // counts + Bloom words, one round trip
+                const ClassRec& rd = rf.r;
                 double ld_a;
                 if ((bits & 1u) && coh_dest(rd, sm.ch[warp][idx], ld_a)) {
                     res |= 1u;
@@ -505,7 +510,7 @@ __global__ void __launch_bounds__(kSweepTile, 4) k_score(SweepArgs a) {
                     bool ok = true;
                     for (uint32_t k = 0; k < on && ok; ++k) {
                         const uint32_t X = sm.X[ot + k * kSweepTile];
-                        if (X != d && !in_urow(a.rec, d, rd, a.ux, X)) ok = false;
+                        if (X != d && (!rf.maybe(X) || urow_find(a.ux, rd.ubase, rd.cbo, X) < 0)) ok = false;
                     }
                     if (ok) res |= 2u;
                 }
@@ -580,6 +585,35 @@ __global__ void __launch_bounds__(kSweepTile, 4) k_score(SweepArgs a) {
     }
     const uint32_t wc = __reduce_add_sync(0xffffffffu, cands);
     if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
+}
+
+// Per-thread variant of pass 1 (one method per thread, list in shared
+// memory): small state, high occupancy — the default.
+template <int K>
+__global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(SweepArgs a) {
+    __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
+    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
+    uint32_t cands = 0;
+    if (pos < a.pos_end) {
+        const uint32_t p = __ldg(a.s.cls_methods + pos);
+        const uint32_t o = __ldg(a.pos_owner + pos);
+        SmemEnum ren{s_X + threadIdx.x, s_H + threadIdx.x, 0};
+        StreamEnum sen;
+        Origin org;
+        MethodResult r;
+        if (load_method<K>(a, (uint32_t)pos, p, o, ren, sen, org)) r = evaluate(a, ren, o, org, true, true);
+        else r = evaluate(a, sen, o, org, true, true);
+        cands = r.cands;
+        uint4 out;
+        if (a.mode == 0) out = make_uint4(r.bd_coh, r.bd_coup, r.cands, 0);
+        else {
+            if ((r.m_coh | r.m_coup) >> 32) atomicOr(a.err, 2u);
+            out = make_uint4((uint32_t)r.m_coh, (uint32_t)r.m_coup, r.cands, 0);
+        }
+        a.res[pos] = out;
+    }
+    const uint32_t wc = __reduce_add_sync(0xffffffffu, cands);
+    if ((threadIdx.x & 31) == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
 }
 
 // Pass 2: apply the class gates (suggest.hpp:246, :273) and the criteria
@@ -777,6 +811,17 @@ void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
         cudaFuncSetAttribute(k_score<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes<8>());
         cudaFuncSetAttribute(k_score<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes<16>());
         attr = true;
+    }
+    // default: the per-thread kernel (higher occupancy measured faster on C4,
+    // profiles/); MMGPU_SCORE=warp selects the warp-flattened variant
+    static const bool per_thread = [] {
+        const char* e = getenv("MMGPU_SCORE");
+        return !(e && e[0] == 'w');
+    }();
+    if (per_thread) {
+        if (a.maxdeg_fast <= 8) k_score_thread<8><<<n_tiles, kSweepTile, 0, st>>>(a);
+        else k_score_thread<16><<<n_tiles, kSweepTile, 0, st>>>(a);
+        return;
     }
     if (a.maxdeg_fast <= 8) k_score<8><<<n_tiles, kSweepTile, score_smem_bytes<8>(), st>>>(a);
     else k_score<16><<<n_tiles, kSweepTile, score_smem_bytes<16>(), st>>>(a);

@@ -443,8 +443,12 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, ctx->ck.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->cbo.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->thr_scratch.ensure(thresholds_scratch_bytes(C)));
-    MM_CUDA(ctx, ctx->ux.ensure(Ec + Ea + 1));
-    MM_CUDA(ctx, ctx->un.ensure(Ec + Ea + 1));
+    // U rows: kSmallRowCap slots per member for the warp-path classes (static
+    // placement), then the CTA-path classes (bounded by their foreign edges)
+    if ((uint64_t)kSmallRowCap * M + Ec + Ea + 1 >= (1ull << 32))
+        return fail(ctx, MM_E_RANGE, "mm_upload: system too large for 32-bit U-row offsets");
+    MM_CUDA(ctx, ctx->ux.ensure((size_t)kSmallRowCap * M + Ec + Ea + 1));
+    MM_CUDA(ctx, ctx->un.ensure((size_t)kSmallRowCap * M + Ec + Ea + 1));
     ctx->have_model = true;
     ctx->metrics_valid = false;
     ctx->sweep_valid = false;
@@ -725,6 +729,19 @@ mm_status mm_sequential_mean(mm_ctx* ctx, const double* values, uint64_t n, doub
     *out = h.lcom;
     if (fast_path) *fast_path = (int)h.fast_path_ok;
     return MM_OK;
+}
+
+mm_status mm_pinned_alloc(uint64_t bytes, void** out) {
+    if (!out) return MM_E_ARG;
+    *out = nullptr;
+    if (!bytes) return MM_OK;
+    const cudaError_t e = cudaMallocHost(out, bytes);
+    if (e == cudaErrorMemoryAllocation) return MM_E_OOM;
+    return e == cudaSuccess ? MM_OK : MM_E_CUDA;
+}
+
+void mm_pinned_free(void* p) {
+    if (p) cudaFreeHost(p);
 }
 
 mm_status mm_suggest(mm_ctx* ctx, const mm_sweep_params* p, mm_suggestion* out, uint64_t cap, uint64_t* n_out) {

@@ -23,6 +23,7 @@ constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kSmallMaxMembers = 32;  // warp path: one lane per member
 constexpr int kSmallMaxAttrs = 64;    // own-attribute set fits a u64 mask
 constexpr int kSmallMaxDeg = 16;      // per-member used list fits registers
+constexpr uint32_t kSmallRowCap = kSmallMaxDeg;  // U-row slots reserved per member of a small class
 
 struct DevModel {
     uint32_t C, M, A;
@@ -231,6 +232,36 @@ __device__ __forceinline__ ClassRec load_rec(const ClassRec* __restrict__ rec, u
     r.A = a.x; r.M = a.y; r.H = a.z; r.cbo = a.w;
     r.ubase = b.x; r.pad = b.y;  // sig words stay in memory: read on demand (same cache line)
     return r;
+}
+
+// Whole 64-byte record in one round trip (4 independent 16-byte loads), the
+// signature kept in registers.
+struct ClassRecFull {
+    ClassRec r;
+    uint32_t sig[kSigWords];
+    __device__ __forceinline__ uint32_t word(uint32_t i) const {  // unrolled select: no local memory
+        uint32_t w = 0;
+#pragma unroll
+        for (int k = 0; k < kSigWords; ++k)
+            if ((uint32_t)k == i) w = sig[k];
+        return w;
+    }
+    __device__ __forceinline__ bool maybe(uint32_t x) const {
+        const uint32_t b1 = bloom_h1(x), b2 = bloom_h2(x);
+        return ((word(b1 >> 5) >> (b1 & 31)) & (word(b2 >> 5) >> (b2 & 31)) & 1u) != 0;
+    }
+};
+
+__device__ __forceinline__ ClassRecFull load_rec_full(const ClassRec* __restrict__ rec, uint32_t c) {
+    const uint4* p = reinterpret_cast<const uint4*>(rec + c);
+    const uint4 a = __ldg(p), b = __ldg(p + 1), q = __ldg(p + 2), t = __ldg(p + 3);
+    ClassRecFull f;
+    f.r.A = a.x; f.r.M = a.y; f.r.H = a.z; f.r.cbo = a.w;
+    f.r.ubase = b.x; f.r.pad = b.y;
+    f.sig[0] = b.z; f.sig[1] = b.w;
+    f.sig[2] = q.x; f.sig[3] = q.y; f.sig[4] = q.z; f.sig[5] = q.w;
+    f.sig[6] = t.x; f.sig[7] = t.y; f.sig[8] = t.z; f.sig[9] = t.w;
+    return f;
 }
 
 // Bloom test against class c's U-row signature (L1 hits once c's record line is loaded)

@@ -76,10 +76,41 @@ def criteria_of_mask(mask: int) -> list:
     return [c for c in Criterion if mask & (1 << int(c))]
 
 
+class PinnedBuffer:
+    """A reusable page-locked host buffer (mm_pinned_alloc), viewed as numpy."""
+
+    def __init__(self):
+        self.ptr = C.c_void_p()
+        self.nbytes = 0
+
+    def view(self, dtype, count: int) -> np.ndarray:
+        need = max(1, np.dtype(dtype).itemsize * count)
+        if need > self.nbytes:
+            self.free()
+            cap = max(need, 2 * self.nbytes)
+            check(lib().mm_pinned_alloc(cap, C.byref(self.ptr)), None, "mm_pinned_alloc")
+            self.nbytes = cap
+        buf = (C.c_char * self.nbytes).from_address(self.ptr.value)
+        return np.frombuffer(buf, dtype=dtype, count=count)
+
+    def free(self):
+        if self.ptr:
+            lib().mm_pinned_free(self.ptr)
+            self.ptr = C.c_void_p()
+            self.nbytes = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class Engine:
     """One GPU context (`mm_ctx`) holding one uploaded system."""
 
     def __init__(self, device: int = 0, stream: Optional[int] = None):
+        self._pinned = {}
         self._ctx = C.c_void_p()
         check(lib().mm_ctx_create(device, C.byref(self._ctx)), None, f"mm_ctx_create(device={device})")
         if stream is not None:
@@ -88,6 +119,8 @@ class Engine:
 
     # ---- context ------------------------------------------------------
     def close(self) -> None:
+        for b in getattr(self, "_pinned", {}).values():
+            b.free()
         if self._ctx:
             lib().mm_ctx_destroy(self._ctx)
             self._ctx = C.c_void_p()
@@ -137,14 +170,24 @@ class Engine:
     def compute_metrics(self) -> None:
         self._check(lib().mm_compute_metrics(self._ctx), "mm_compute_metrics")
 
-    def class_metrics_all(self):
-        """(lcom f64[c], lcom_ck u64[c], cbo u32[c]) — full_report's class fields."""
+    def _staging(self, name: str, dtype, count: int) -> np.ndarray:
+        b = self._pinned.get(name)
+        if b is None:
+            b = self._pinned[name] = PinnedBuffer()
+        return b.view(dtype, count)
+
+    def class_metrics_all(self, copy: bool = True):
+        """(lcom f64[c], lcom_ck u64[c], cbo u32[c]) — full_report's class fields.
+        D2H lands in reusable pinned buffers; copy=False returns views of them
+        (valid until the next call)."""
         n = self.system.n_classes
-        lcom = np.empty(n, np.float64)
-        ck = np.empty(n, np.uint64)
-        cbo = np.empty(n, np.uint32)
+        lcom = self._staging("lcom", np.float64, n)
+        ck = self._staging("ck", np.uint64, n)
+        cbo = self._staging("cbo", np.uint32, n)
         self._check(lib().mm_class_metrics(self._ctx, lcom.ctypes.data, ck.ctypes.data, cbo.ctypes.data),
                     "mm_class_metrics")
+        if copy:
+            return lcom.copy(), ck.copy(), cbo.copy()
         return lcom, ck, cbo
 
     def parallel_class_metrics(self, n_workers: int = 1) -> ClassMetrics:
@@ -242,21 +285,23 @@ class Engine:
         self._check(lib().mm_sweep_device_result(self._ctx, C.byref(ptr), C.byref(n)), "mm_sweep_device_result")
         return ptr.value, n.value
 
-    def suggestions(self) -> np.ndarray:
+    def suggestions(self, copy: bool = True) -> np.ndarray:
+        """The last sweep's ordered records (D2H into a reusable pinned buffer;
+        copy=False returns a view of it, valid until the next call)."""
         n = C.c_uint64()
         lib().mm_copy_suggestions(self._ctx, None, 0, C.byref(n))
-        out = np.zeros(n.value, dtype=abi.SUGGESTION_DTYPE)
+        out = self._staging("sugg", abi.SUGGESTION_DTYPE, n.value)
         if n.value:
             self._check(lib().mm_copy_suggestions(self._ctx, out.ctypes.data, n.value, C.byref(n)),
                         "mm_copy_suggestions")
-        return out
+        return out.copy() if copy else out
 
     def suggest_all(self, thresholds: Thresholds, criteria: Sequence = (Criterion.Cohesion, Criterion.Coupling),
                     combine: Combine = Combine.Union, all_candidates: bool = False, top_k: int = 1,
-                    class_range: Optional[tuple] = None) -> np.ndarray:
+                    class_range: Optional[tuple] = None, copy: bool = True) -> np.ndarray:
         """suggest_all (suggest.hpp:303): ordered by (origin, method, destination)."""
         self.sweep(criteria, combine, thresholds, all_candidates, top_k, class_range, want_count=False)
-        return self.suggestions()
+        return self.suggestions(copy=copy)
 
     def suggest_by_cohesion(self, thresholds: Thresholds, all_candidates: bool = False) -> np.ndarray:
         """suggest_by_cohesion (suggest.hpp:239) — as a set; ordered (origin, method, dest)."""
