@@ -103,7 +103,8 @@ __device__ __forceinline__ uint32_t attr_pos(const DevModel& s, uint32_t ab, uin
 // own class (classes with ≤ 64 attributes).
 template <int K>
 __global__ void __launch_bounds__(256)
-k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask, uint32_t* __restrict__ pos_owner) {
+k_method(DevModel s, const uint8_t* __restrict__ kind, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask,
+         uint32_t* __restrict__ pos_owner) {
     const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
     if (pos >= s.M) return;
     const uint32_t p = __ldg(s.cls_methods + pos);
@@ -116,43 +117,52 @@ k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask
 #pragma unroll
     for (int k = 0; k < kRecMaxEnt; ++k) ent[k] = 0;
     uint64_t mask = 0;
-    const uint32_t nc = ce - cb, na = ae - ab;
-    if (nc + na <= (uint32_t)K) {
-        // all targets first, then all owner gathers: two memory round trips
-        // per method instead of two per edge
+    const uint32_t nc = ce - cb, na = ae - ab, deg = nc + na;
+    // edges in chunks of K: all targets of a chunk, then all their owner
+    // gathers — two memory round trips per chunk instead of two per edge.
+    // The list keeps kRecMaxEnt + 1 slots: an 8th distinct class means the
+    // record cannot hold the list (consumers then read the CSR).
+    UsedList<kRecMaxEnt + 1> L;
+    L.clear();
+    uint32_t hown = 0;
+    // masks only feed the warp path's LCOM-CK (CTA-path classes rebuild their own)
+    const bool small_attrs = oae - oab <= 64 && __ldg(kind + own) == 0;
+    auto chunk = [&](uint32_t e0) {
         uint32_t tg[K], ow[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const bool isc = (uint32_t)k < nc, isa = !isc && (uint32_t)k < nc + na;
-            tg[k] = isc ? __ldg(s.call_tgt + cb + k) : (isa ? __ldg(s.acc_tgt + ab + (k - nc)) : 0u);
+            const uint32_t e = e0 + k;
+            const bool isc = e < nc, isa = !isc && e < deg;
+            tg[k] = isc ? __ldg(s.call_tgt + cb + e) : (isa ? __ldg(s.acc_tgt + ab + (e - nc)) : 0u);
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const bool isc = (uint32_t)k < nc, isa = !isc && (uint32_t)k < nc + na;
+            const uint32_t e = e0 + k;
+            const bool isc = e < nc, isa = !isc && e < deg;
             ow[k] = isc ? __ldg(s.method_owner + tg[k]) : (isa ? __ldg(s.attribute_owner + tg[k]) : kNone);
         }
-        UsedList<K> L;
-        L.clear();
-        uint32_t hown = 0;
-        const bool small_attrs = oae - oab <= 64;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const bool isa = (uint32_t)k >= nc && (uint32_t)k < nc + na;
-            if ((uint32_t)k < nc + na) L.insert(ow[k], isa ? 1u : 0u);
+            const uint32_t e = e0 + k;
+            const bool isa = e >= nc && e < deg;
+            if (e < deg) L.insert(ow[k], isa ? 1u : 0u);
             if (isa && ow[k] == own) {
                 if (small_attrs) mask |= 1ull << attr_pos(s, oab, oae, tg[k]);
                 ++hown;
             }
         }
-        bool fits = L.n <= kRecMaxEnt && hown < 256;
+    };
+    if (deg <= (uint32_t)K) chunk(0);  // the common case: one straight-line chunk
+    else
+        for (uint32_t e0 = 0; e0 < deg; e0 += K) chunk(e0);
+    bool fits = L.n <= kRecMaxEnt && hown < 256;
 #pragma unroll
-        for (int k = 0; k < K; ++k)
-            if (k < L.n) {
-                fits = fits && L.X[k] < (1u << 24) && L.h[k] < 256;
-                if (k < kRecMaxEnt) ent[k] = (L.X[k] << 8) | L.h[k];
-            }
-        if (fits) hdr = (uint32_t)L.n | (hown << kRecHownShift);
-    }
+    for (int k = 0; k < kRecMaxEnt; ++k)
+        if (k < L.n) {
+            fits = fits && L.X[k] < (1u << 24) && L.h[k] < 256;
+            ent[k] = (L.X[k] << 8) | L.h[k];
+        }
+    if (fits) hdr = (uint32_t)L.n | (hown << kRecHownShift);
     uint4* dst = reinterpret_cast<uint4*>(recs + pos);
     dst[0] = make_uint4(hdr, ent[0], ent[1], ent[2]);
     dst[1] = make_uint4(ent[3], ent[4], ent[5], ent[6]);
@@ -378,7 +388,7 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind,
         const uint64_t pairs = (uint64_t)M * (M - 1) / 2;
         const uint64_t P = pairs - Q;
         ClassRec r;
-        r.A = A; r.M = M; r.H = H; r.cbo = cbo; r.ubase = ubase; r.pad = 0;
+        r.A = A; r.M = M; r.H = H; r.cbo = cbo; r.ubase = ubase; r.dense = kNone;
         for (int w = 0; w < kSigWords; ++w) r.sig[w] = sig[w];
         rec[c] = r;
         lcom_out[c] = l;
@@ -423,13 +433,13 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* red, u
     return before + inc - v;
 }
 
-__device__ void block_bitonic_u64(uint64_t* buf, uint32_t N) {
+__device__ void block_bitonic_u32(uint32_t* buf, uint32_t N) {
     for (uint32_t k = 2; k <= N; k <<= 1)
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
             for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) {
                 const uint32_t ixj = i ^ j;
                 if (ixj > i) {
-                    const uint64_t a = buf[i], b = buf[ixj];
+                    const uint32_t a = buf[i], b = buf[ixj];
                     const bool up = (i & k) == 0;
                     if ((a > b) == up) { buf[i] = b; buf[ixj] = a; }
                 }
@@ -438,68 +448,116 @@ __device__ void block_bitonic_u64(uint64_t* buf, uint32_t N) {
         }
 }
 
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Member i's distinct used classes, ascending (record entries, or a streaming
+// enumeration of the CSR row when the record overflowed); f(X, h).
+template <class F>
+__device__ __forceinline__ void member_used(const DevModel& s, const MethRec* recs, uint32_t pos, uint32_t p, F f) {
+    const uint32_t hdr = recs[pos].hdr;
+    if (!(hdr & kRecOverflow)) {
+        for (uint32_t k = 0; k < rec_n(hdr); ++k) {
+            const uint32_t e = recs[pos].ent[k];
+            f(e >> 8, e & 0xffu);
+        }
+        return;
+    }
+    StreamUsed S;
+    S.init(s, p);
+    uint32_t prev = kNone, h = 0;
+    for (;;) {
+        const uint32_t x = S.next(prev, h);
+        if (x == kNone) break;
+        f(x, h);
+        prev = x;
+    }
+}
+
+// One CTA per class outside the warp path (Zipf giants, C5's 500-method
+// classes). Dynamic shared memory holds, when they fit (host plan): the
+// class's sorted attribute list (own-attribute positions by binary search),
+// the foreign-class keys (one per member and used class — members' lists are
+// already distinct, so a run length IS the member count U[c][X]), and the
+// LCOM-CK structure: per-member own-attribute masks (A ≤ 256: pairs tested by
+// word ANDs) or per-attribute member bitmaps (sparse giants).
 __global__ void __launch_bounds__(kLargeThreads)
 k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* __restrict__ plan,
               MethRec* __restrict__ recs, ClassRec* __restrict__ rec,
               double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
               uint32_t* __restrict__ ux, uint32_t* __restrict__ un, uint32_t* __restrict__ ucursor,
-              uint64_t* __restrict__ gkeys, uint32_t* __restrict__ grows) {
+              uint32_t* __restrict__ gkeys, uint32_t* __restrict__ grows, uint32_t* __restrict__ dense,
+              uint32_t dense_cap, uint32_t* __restrict__ dense_cursor) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ uint64_t red64[kLargeThreads / 32];
     __shared__ uint32_t red32[kLargeThreads / 32];
-    __shared__ uint32_t s_nk, s_ubase;
+    __shared__ uint32_t s_nk, s_ubase, s_dense;
     __shared__ uint32_t s_sig[kSigWords];
     const uint32_t c = large_list[blockIdx.x];
     const LargePlan pl = plan[blockIdx.x];
-    uint64_t* keys = pl.keys_in_smem ? reinterpret_cast<uint64_t*>(dsm) : gkeys + pl.keys_off;
-    uint32_t* rows = pl.rows_in_smem
-                         ? reinterpret_cast<uint32_t*>(dsm + (pl.keys_in_smem ? 8ull * pl.keys_cap : 0))
-                         : grows + pl.rows_off;
     const uint32_t mb = s.cls_moff[c];
     const uint32_t M = s.cls_moff[c + 1] - mb;
-    const uint32_t A = s.cls_aoff[c + 1] - s.cls_aoff[c];
-    const uint32_t W = (M + 31) / 32;
-    const uint64_t nrow_words = (uint64_t)A * W;
+    const uint32_t ab0 = s.cls_aoff[c];
+    const uint32_t A = s.cls_aoff[c + 1] - ab0;
+    const uint32_t W = (M + 31) / 32;        // rows mode: words per attribute bitmap
+    const uint32_t WA = (A + 63) / 64;       // masks mode: u64 words per member
+    unsigned char* cur = dsm;
+    const uint32_t* attrs = s.cls_attrs + ab0;
+    if (pl.attrs_in_smem) {
+        uint32_t* sa = reinterpret_cast<uint32_t*>(cur);
+        for (uint32_t i = threadIdx.x; i < A; i += blockDim.x) sa[i] = s.cls_attrs[ab0 + i];
+        attrs = sa;
+        cur += ((4ull * A + 15) & ~15ull);
+    }
+    uint32_t* keys = pl.keys_in_smem ? reinterpret_cast<uint32_t*>(cur) : gkeys + pl.keys_off;
+    if (pl.keys_in_smem) cur += (4ull * pl.keys_cap + 15) & ~15ull;  // keep the u64 masks aligned
+    uint64_t* masks = reinterpret_cast<uint64_t*>(cur);  // masks mode (always in smem)
+    uint32_t* rows = pl.ck_masks ? nullptr : (pl.rows_in_smem ? reinterpret_cast<uint32_t*>(cur) : grows + pl.rows_off);
+    const uint64_t ck_words = pl.ck_masks ? (uint64_t)M * WA * 2 : (uint64_t)A * W;
+    uint32_t* ckz = pl.ck_masks ? reinterpret_cast<uint32_t*>(masks) : rows;
     if (threadIdx.x == 0) s_nk = 0;
     if (threadIdx.x < kSigWords) s_sig[threadIdx.x] = 0;
-    for (uint64_t i = threadIdx.x; i < nrow_words; i += blockDim.x) rows[i] = 0;
+    for (uint64_t i = threadIdx.x; i < ck_words; i += blockDim.x) ckz[i] = 0;
     __syncthreads();
 
-    // phase 1: foreign (X, member) keys, own-attribute bits, H
+    // phase 1: members' foreign used classes -> keys; H; own-attribute sets
     uint64_t hown = 0;
     for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) {
-        const uint32_t p = s.cls_methods[mb + i];
-        const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
-        for (uint32_t e = cb; e < ce; ++e) {
-            const uint32_t o = __ldg(s.method_owner + __ldg(s.call_tgt + e));
-            if (o != c) keys[atomicAdd(&s_nk, 1u)] = ((uint64_t)o << 32) | i;
-        }
+        const uint32_t pos = mb + i;
+        const uint32_t p = s.cls_methods[pos];
+        member_used(s, recs, pos, p, [&](uint32_t X, uint32_t h) {
+            if (X != c) keys[atomicAdd(&s_nk, 1u)] = X;
+        });
         const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
         for (uint32_t e = ab; e < ae; ++e) {
             const uint32_t t = __ldg(s.acc_tgt + e);
-            const uint32_t o = __ldg(s.attribute_owner + t);
-            if (o != c) {
-                keys[atomicAdd(&s_nk, 1u)] = ((uint64_t)o << 32) | i;
-            } else {
-                const uint32_t a = attr_pos(s, s.cls_aoff[c], s.cls_aoff[c + 1], t);
-                atomicOr(rows + (uint64_t)a * W + (i >> 5), 1u << (i & 31));
-                ++hown;
-            }
+            if (__ldg(s.attribute_owner + t) != c) continue;
+            ++hown;
+            const uint32_t a = lower_bound_u32(attrs, A, t);
+            if (pl.ck_masks) masks[(uint64_t)i * WA + (a >> 6)] |= 1ull << (a & 63);  // member i: this thread only
+            else atomicOr(rows + (uint64_t)a * W + (i >> 5), 1u << (i & 31));
         }
     }
     const uint64_t H = block_sum_u64(hown, red64);  // includes a __syncthreads
     const uint32_t nk = s_nk;
     uint32_t N = 1;
     while (N < nk) N <<= 1;
-    for (uint32_t i = nk + threadIdx.x; i < N; i += blockDim.x) keys[i] = ~0ull;
+    for (uint32_t i = nk + threadIdx.x; i < N; i += blockDim.x) keys[i] = kNone;
     __syncthreads();
-    if (N > 1) block_bitonic_u64(keys, N);
+    if (N > 1) block_bitonic_u32(keys, N);
 
-    // phase 2: distinct X (cbo) and per-X distinct members (U counts)
+    // phase 2: runs of equal X = one U row entry with count = run length
     uint32_t nx = 0;
     for (uint32_t b = 0; b < nk; b += blockDim.x) {
         const uint32_t k = b + threadIdx.x;
-        const bool xh = k < nk && (k == 0 || (keys[k] >> 32) != (keys[k - 1] >> 32));
+        const bool xh = k < nk && (k == 0 || keys[k] != keys[k - 1]);
         uint32_t tot;
         block_excl_scan(xh ? 1u : 0u, red32, &tot);
         nx += tot;
@@ -512,33 +570,41 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     uint32_t xcarry = 0;
     for (uint32_t b = 0; b < nk; b += blockDim.x) {
         const uint32_t k = b + threadIdx.x;
-        const bool xh = k < nk && (k == 0 || (keys[k] >> 32) != (keys[k - 1] >> 32));
+        const bool xh = k < nk && (k == 0 || keys[k] != keys[k - 1]);
         uint32_t tot;
         const uint32_t ex = block_excl_scan(xh ? 1u : 0u, red32, &tot);
         if (xh) {
-            ux[ubase + xcarry + ex] = (uint32_t)(keys[k] >> 32);
-            un[ubase + xcarry + ex] = 0;
-            const uint32_t b1 = bloom_h1((uint32_t)(keys[k] >> 32)), b2 = bloom_h2((uint32_t)(keys[k] >> 32));
+            const uint32_t X = keys[k];
+            ux[ubase + xcarry + ex] = X;
+            un[ubase + xcarry + ex] = lower_bound_u32(keys, nk, X + 1) - k;  // run length
+            const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
             atomicOr(s_sig + (b1 >> 5), 1u << (b1 & 31));
             atomicOr(s_sig + (b2 >> 5), 1u << (b2 & 31));
         }
         xcarry += tot;
     }
+
+    // dense rows also get an exact bitmap over all classes (O(1) membership
+    // in the sweep where a Bloom signature of a long row says "maybe" to all)
+    const uint32_t dwords = (s.C + 31) / 32;
+    if (threadIdx.x == 0) {
+        s_dense = kNone;
+        if (nx > kDenseRowMin && dense) {
+            const uint32_t off = atomicAdd(dense_cursor, dwords);
+            if ((uint64_t)off + dwords <= dense_cap) s_dense = off;
+        }
+    }
     __syncthreads();
-    xcarry = 0;
-    for (uint32_t b = 0; b < nk; b += blockDim.x) {
-        const uint32_t k = b + threadIdx.x;
-        const bool xh = k < nk && (k == 0 || (keys[k] >> 32) != (keys[k - 1] >> 32));
-        const bool ph = k < nk && (k == 0 || keys[k] != keys[k - 1]);
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan(xh ? 1u : 0u, red32, &tot);
-        // run index of position k = (#X heads at or before k) - 1
-        if (ph) atomicAdd(un + ubase + xcarry + ex + (xh ? 1u : 0u) - 1u, 1u);
-        xcarry += tot;
+    if (s_dense != kNone) {
+        for (uint32_t w = threadIdx.x; w < dwords; w += blockDim.x) dense[s_dense + w] = 0;
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < nx; k += blockDim.x) {
+            const uint32_t X = ux[ubase + k];
+            atomicOr(dense + s_dense + (X >> 5), 1u << (X & 31));
+        }
     }
 
-    __syncthreads();
-    // per member: #{X ≠ c : U[c][X] == 1} into its method record (the sweep's cbo_origin_after)
+    // phase 3: per member, #{X ≠ c : U[c][X] == 1} into its method record
     for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) {
         MethRec* r = recs + mb + i;
         const uint32_t hdr = r->hdr;
@@ -547,30 +613,39 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         for (uint32_t k = 0; k < rec_n(hdr); ++k) {
             const uint32_t X = r->ent[k] >> 8;
             if (X == c) continue;
-            const int at = urow_find(ux, ubase, nx, X);
-            removed += (at >= 0 && un[ubase + at] == 1u);
+            const uint32_t lo = lower_bound_u32(keys, nk, X);
+            removed += (lower_bound_u32(keys, nk, X + 1) - lo) == 1u;
         }
         r->hdr = hdr | (removed << kRecRemovedShift) | kRecRemovedValid;
     }
 
-    // phase 3: LCOM-CK via per-attribute member bitmaps (rows[a] = methods using a)
+    // phase 4: LCOM-CK, Q = #pairs (i<j) sharing an own attribute
     uint64_t q = 0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t i = warp; i < M; i += kLargeThreads / 32) {
-        const uint32_t p = s.cls_methods[mb + i];
-        const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
-        for (uint32_t wb = 0; wb < W; wb += 32) {
-            const uint32_t w = wb + lane;
-            uint32_t acc = 0;
-            if (w < W && w >= (i >> 5)) {
-                for (uint32_t e = ab; e < ae; ++e) {
-                    const uint32_t t = __ldg(s.acc_tgt + e);
-                    if (__ldg(s.attribute_owner + t) == c)
-                        acc |= rows[(uint64_t)attr_pos(s, s.cls_aoff[c], s.cls_aoff[c + 1], t) * W + w];
-                }
-                if (w == (i >> 5)) acc &= ((i & 31) == 31) ? 0u : (~0u << ((i & 31) + 1));
+    if (pl.ck_masks) {
+        for (uint32_t i = threadIdx.x; i < M; i += blockDim.x)
+            for (uint32_t j = i + 1; j < M; ++j) {
+                uint64_t any = 0;
+                for (uint32_t w = 0; w < WA; ++w) any |= masks[(uint64_t)i * WA + w] & masks[(uint64_t)j * WA + w];
+                q += any != 0;
             }
-            q += __popc(acc);
+    } else {
+        // rows[a] = members using a; member i's sharers = OR of its rows, above i
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (uint32_t i = warp; i < M; i += kLargeThreads / 32) {
+            const uint32_t p = s.cls_methods[mb + i];
+            const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+            for (uint32_t wb = 0; wb < W; wb += 32) {
+                const uint32_t w = wb + lane;
+                uint32_t acc = 0;
+                if (w < W && w >= (i >> 5)) {
+                    for (uint32_t e = ab; e < ae; ++e) {
+                        const uint32_t t = __ldg(s.acc_tgt + e);
+                        if (__ldg(s.attribute_owner + t) == c) acc |= rows[(uint64_t)lower_bound_u32(attrs, A, t) * W + w];
+                    }
+                    if (w == (i >> 5)) acc &= ((i & 31) == 31) ? 0u : (~0u << ((i & 31) + 1));
+                }
+                q += __popc(acc);
+            }
         }
     }
     const uint64_t Q = block_sum_u64(q, red64);
@@ -579,7 +654,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         const uint64_t pairs = (uint64_t)M * (M - 1) / 2;
         const uint64_t P = pairs - Q;
         ClassRec r;
-        r.A = A; r.M = M; r.H = (uint32_t)H; r.cbo = nx; r.ubase = ubase; r.pad = 0;
+        r.A = A; r.M = M; r.H = (uint32_t)H; r.cbo = nx; r.ubase = ubase; r.dense = s_dense;
         for (int w = 0; w < kSigWords; ++w) r.sig[w] = s_sig[w];
         rec[c] = r;
         lcom_out[c] = l;
@@ -606,12 +681,11 @@ void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list,
     if (!s.C) return;
     k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, kind, large_list, n_large, max_deg, foreign);
 }
-void launch_method(const DevModel& s, uint32_t maxdeg, MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner,
+void launch_method(const DevModel& s, const uint8_t* kind, MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner,
                    cudaStream_t st) {
     if (!s.M) return;
     const uint32_t blocks = (s.M + 255) / 256;
-    if (maxdeg <= 8) k_method<8><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
-    else k_method<16><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
+    k_method<8><<<blocks, 256, 0, st>>>(s, kind, recs, own_mask, pos_owner);
 }
 void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, const uint64_t* own_mask,
                         ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,
@@ -623,10 +697,12 @@ void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, c
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
                         uint32_t smem_bytes, MethRec* recs, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
-                        uint64_t* gkeys, uint32_t* grows, cudaStream_t st) {
+                        uint32_t* gkeys, uint32_t* grows, uint32_t* dense, uint32_t dense_cap,
+                        uint32_t* dense_cursor, cudaStream_t st) {
     if (!n_large) return;
-    k_class_large<<<n_large, kLargeThreads, smem_bytes, st>>>(s, large_list, plan, recs, rec, lcom, ck,
-                                                              cbo, ux, un, ucursor, gkeys, grows);
+    k_class_large<<<n_large, kLargeThreads, smem_bytes, st>>>(s, large_list, plan, recs, rec, lcom, ck, cbo, ux,
+                                                              un, ucursor, gkeys, grows, dense, dense_cap,
+                                                              dense_cursor);
 }
 cudaError_t set_class_large_smem(uint32_t bytes) {
     return cudaFuncSetAttribute(k_class_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);

@@ -56,13 +56,15 @@ struct SmemEnum {
             if (X[k * kSweepTile] == v) return H[k * kSweepTile];
         return 0;
     }
-    __device__ __forceinline__ void insert(uint32_t v, uint32_t acc) {
+    // returns false when a new class would exceed `cap` distinct entries
+    __device__ __forceinline__ bool insert(uint32_t v, uint32_t acc, int cap) {
         int k = 0;
         while (k < n && X[k * kSweepTile] < v) ++k;
         if (k < n && X[k * kSweepTile] == v) {
             H[k * kSweepTile] += acc;
-            return;
+            return true;
         }
+        if (n >= cap) return false;
         for (int j = n; j > k; --j) {
             X[j * kSweepTile] = X[(j - 1) * kSweepTile];
             H[j * kSweepTile] = H[(j - 1) * kSweepTile];
@@ -70,13 +72,18 @@ struct SmemEnum {
         X[k * kSweepTile] = v;
         H[k * kSweepTile] = acc;
         ++n;
+        return true;
     }
-    __device__ __forceinline__ void build(const DevModel& s, uint32_t p) {
+    // distinct used classes of p from the CSR (any degree); false if more than cap
+    __device__ __forceinline__ bool build(const DevModel& s, uint32_t p, int cap) {
         n = 0;
         const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
-        for (uint32_t e = cb; e < ce; ++e) insert(__ldg(s.method_owner + __ldg(s.call_tgt + e)), 0);
+        for (uint32_t e = cb; e < ce; ++e)
+            if (!insert(__ldg(s.method_owner + __ldg(s.call_tgt + e)), 0, cap)) return false;
         const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
-        for (uint32_t e = ab; e < ae; ++e) insert(__ldg(s.attribute_owner + __ldg(s.acc_tgt + e)), 1);
+        for (uint32_t e = ab; e < ae; ++e)
+            if (!insert(__ldg(s.attribute_owner + __ldg(s.acc_tgt + e)), 1, cap)) return false;
+        return true;
     }
 };
 
@@ -136,9 +143,12 @@ __device__ __forceinline__ bool coh_dest(const ClassRec& rd, uint32_t h, double&
     return ld_a < lcom_of(rd.A, rd.M, rd.H);
 }
 
-// X ∈ U[d]? Bloom signature first (a clear bit proves absence), then the row.
+// X ∈ U[d]? Exact bitmap for dense rows; else the Bloom signature (a clear
+// bit proves absence), then the row.
 __device__ __forceinline__ bool in_urow(const ClassRec* __restrict__ rec, uint32_t d, const ClassRec& rd,
-                                        const uint32_t* __restrict__ ux, uint32_t X) {
+                                        const uint32_t* __restrict__ ux, const uint32_t* __restrict__ dense,
+                                        uint32_t X) {
+    if (rd.dense != kNone) return (__ldg(dense + rd.dense + (X >> 5)) >> (X & 31)) & 1u;
     if (!sig_maybe(rec, d, X)) return false;
     return urow_find(ux, rd.ubase, rd.cbo, X) >= 0;
 }
@@ -147,24 +157,25 @@ __device__ __forceinline__ bool in_urow(const ClassRec* __restrict__ rec, uint32
 // ⟺ every X ∈ used(u) \ {d} is already in U[d] (miss == 0).
 template <class E>
 __device__ __forceinline__ bool coup_dest(const ClassRec* __restrict__ rec, const ClassRec& rd,
-                                          const uint32_t* __restrict__ ux, const E& en, uint32_t d) {
+                                          const uint32_t* __restrict__ ux, const uint32_t* __restrict__ dense,
+                                          const E& en, uint32_t d) {
     bool ok = true;
     en.each([&](int, uint32_t X, uint32_t) {
-        if (ok && X != d && !in_urow(rec, d, rd, ux, X)) ok = false;
+        if (ok && X != d && !in_urow(rec, d, rd, ux, dense, X)) ok = false;
     });
     return ok;
 }
 
 template <class E>
 __device__ __forceinline__ Dest eval_dest(const ClassRec* __restrict__ rec, const uint32_t* __restrict__ ux,
-                                          const E& en, uint32_t d, uint32_t hd) {
+                                          const uint32_t* __restrict__ dense, const E& en, uint32_t d, uint32_t hd) {
     const ClassRec rd = load_rec(rec, d);
     Dest r;
     r.ld_b = lcom_of(rd.A, rd.M, rd.H);
     r.ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
     uint32_t miss = 0;
     en.each([&](int, uint32_t X, uint32_t) {
-        if (X != d && !in_urow(rec, d, rd, ux, X)) ++miss;
+        if (X != d && !in_urow(rec, d, rd, ux, dense, X)) ++miss;
     });
     r.cd_b = rd.cbo;
     r.cd_a = rd.cbo + miss;
@@ -199,7 +210,7 @@ __device__ __forceinline__ void score(const SweepArgs& a, const E& en, const Ori
         pcoh = true;
         kcoh = __dadd_rn(org.lo_a, ld_a);  // lcom_key, suggest.hpp:194-196
     }
-    if (org.co_a < org.co_b && coup_dest(a.rec, rd, a.ux, en, d)) {
+    if (org.co_a < org.co_b && coup_dest(a.rec, rd, a.ux, a.dense, en, d)) {
         pcoup = true;
         kcoup = rd.cbo;  // cbo_dest_after == cbo_dest_before when it passes
     }
@@ -324,7 +335,7 @@ __device__ __forceinline__ void emit(const SweepArgs& a, const E& en, uint32_t p
             tcoup = k < 64 && ((r.m_coup >> k) & 1ull);
         }
         if (inter ? !(tcoh && tcoup) : !(tcoh || tcoup)) return;
-        const Dest dv = eval_dest(a.rec, a.ux, en, d, hd);
+        const Dest dv = eval_dest(a.rec, a.ux, a.dense, en, d, hd);
         mm_suggestion s;
         s.lcom_origin_before = org.lo_b;
         s.lcom_origin_after = org.lo_a;
@@ -386,10 +397,7 @@ __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, ui
         org = make_origin(ro, rec_hown(r0.x), removed);
         return true;
     }
-    const uint32_t deg = (__ldg(a.s.call_off + p + 1) - __ldg(a.s.call_off + p)) +
-                         (__ldg(a.s.acc_off + p + 1) - __ldg(a.s.acc_off + p));
-    if (deg <= (uint32_t)K) {
-        ren.build(a.s, p);
+    if (ren.build(a.s, p, K)) {  // ≤ K distinct classes (any degree): shared-memory list
         org = make_origin(ro, ren.hits(o), removed_count(ro, a.ux, a.un, ren, o));
         return true;
     }
@@ -510,7 +518,10 @@ __global__ void __launch_bounds__(kSweepTile, 4) k_score(SweepArgs a) {
                     bool ok = true;
                     for (uint32_t k = 0; k < on && ok; ++k) {
                         const uint32_t X = sm.X[ot + k * kSweepTile];
-                        if (X != d && (!rf.maybe(X) || urow_find(a.ux, rd.ubase, rd.cbo, X) < 0)) ok = false;
+                        const bool in = rd.dense != kNone
+                                            ? ((__ldg(a.dense + rd.dense + (X >> 5)) >> (X & 31)) & 1u) != 0
+                                            : (rf.maybe(X) && urow_find(a.ux, rd.ubase, rd.cbo, X) >= 0);
+                        if (X != d && !in) ok = false;
                     }
                     if (ok) res |= 2u;
                 }
@@ -773,8 +784,8 @@ __global__ void __launch_bounds__(kSweepTile) k_write(SweepArgs a) {
 }
 
 __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const uint32_t* __restrict__ ux,
-                          const uint32_t* __restrict__ un, uint32_t u, uint32_t o, uint32_t d,
-                          mm_whatif* __restrict__ out) {
+                          const uint32_t* __restrict__ un, const uint32_t* __restrict__ dense, uint32_t u,
+                          uint32_t o, uint32_t d, mm_whatif* __restrict__ out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (s.method_owner[u] != o) {  // not a member of the origin: invalid_argument (suggest.hpp:93-96)
         mm_whatif w{};
@@ -786,7 +797,7 @@ __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const ui
     en.S.init(s, u);
     const ClassRec ro = load_rec(rec, o);
     const Origin org = make_origin(ro, en.hits(o), removed_count(ro, ux, un, en, o));
-    const Dest dv = eval_dest(rec, ux, en, d, en.hits(d));
+    const Dest dv = eval_dest(rec, ux, dense, en, d, en.hits(d));
     mm_whatif w;
     w.lcom_origin_before = org.lo_b;
     w.lcom_origin_after = org.lo_a;
@@ -841,9 +852,9 @@ void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     else k_write<16><<<grid, kSweepTile, 0, st>>>(a);
 }
 
-void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un, uint32_t u,
-                    uint32_t o, uint32_t d, mm_whatif* out, cudaStream_t st) {
-    k_what_if<<<1, 32, 0, st>>>(s, rec, ux, un, u, o, d, out);
+void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un,
+                    const uint32_t* dense, uint32_t u, uint32_t o, uint32_t d, mm_whatif* out, cudaStream_t st) {
+    k_what_if<<<1, 32, 0, st>>>(s, rec, ux, un, dense, u, o, d, out);
 }
 
 }  // namespace mmg

@@ -27,6 +27,8 @@ struct Ctl {  // small device-resident control block
     uint32_t n_large;
     uint32_t max_deg;
     uint32_t ucursor;
+    uint32_t dense_cursor;
+    uint32_t pad0;
     uint32_t tile_counter;
     uint32_t err;
     uint32_t n_emit;
@@ -86,11 +88,18 @@ struct mm_ctx {
     DBuf<uint32_t> method_owner, attribute_owner, cls_moff, cls_methods, cls_aoff, cls_attrs, call_off, call_tgt,
         acc_off, acc_tgt;
     // plan
-    uint32_t n_large = 0, max_deg = 0, large_smem = 0;
+    uint32_t n_large = 0, max_deg = 0;
+    struct LargeGroup {
+        uint32_t first, count, smem;
+        int tier;
+    };
+    std::vector<LargeGroup> large_groups;  // CTA-path launches, grouped by shared-memory need
+    DBuf<uint32_t> dense;                  // exact U-row bitmaps of dense classes
+    uint32_t dense_cap = 0;
     DBuf<uint8_t> kind;
     DBuf<uint32_t> large_list, foreign;
     DBuf<LargePlan> plans;
-    DBuf<uint64_t> gkeys;
+    DBuf<uint32_t> gkeys;
     DBuf<uint32_t> grows;
     // derived
     DBuf<uint32_t> cbo, ux, un;
@@ -200,6 +209,7 @@ void free_model(mm_ctx* c) {
     c->kind.release();
     c->plans.release();
     c->gkeys.release();
+    c->dense.release();
     c->rec.release();
     c->lcom.release();
     c->ck.release();
@@ -406,33 +416,79 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         std::sort(list.begin(), list.end());
         int dev_smem = 0;
         cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-        const uint64_t budget = std::min<uint64_t>(dev_smem > 0 ? (uint64_t)dev_smem - 4096 : 48 * 1024, 160 * 1024);
+        const uint64_t budget = dev_smem > 8192 ? (uint64_t)dev_smem - 8192 : 40 * 1024;
         std::vector<LargePlan> plans(ctx->n_large);
-        uint64_t koff = 0, roff = 0, smem_need = 0;
+        std::vector<uint64_t> need(ctx->n_large);
+        uint64_t n_dense = 0;
         for (uint32_t i = 0; i < ctx->n_large; ++i) {
             const uint32_t c = list[i];
-            const uint32_t Mc = s->class_method_off[c + 1] - s->class_method_off[c];
-            const uint32_t Ac = s->class_attr_off[c + 1] - s->class_attr_off[c];
+            const uint64_t Mc = s->class_method_off[c + 1] - s->class_method_off[c];
+            const uint64_t Ac = s->class_attr_off[c + 1] - s->class_attr_off[c];
             LargePlan& pl = plans[i];
             std::memset(&pl, 0, sizeof pl);
             pl.keys_cap = next_pow2(std::max<uint32_t>(fr[c], 1));
-            const uint64_t kbytes = 8ull * pl.keys_cap;
-            const uint64_t rbytes = 4ull * Ac * ((Mc + 31) / 32);
+            n_dense += fr[c] > kDenseRowMin;
+            // shared memory, in order of benefit: keys (sorted in place), the
+            // attribute list, the LCOM-CK structure
             uint64_t used = 0;
-            if (kbytes <= budget) { pl.keys_in_smem = 1; used = kbytes; }
-            else { pl.keys_off = koff; koff += pl.keys_cap; }
-            if (used + rbytes <= budget) { pl.rows_in_smem = 1; used += rbytes; }
-            else { pl.rows_off = roff; roff += Ac * ((Mc + 31) / 32); }
-            smem_need = std::max(smem_need, used);
+            const uint64_t kbytes = (4ull * pl.keys_cap + 15) & ~15ull;
+            if (kbytes <= budget) { pl.keys_in_smem = 1; used += kbytes; }
+            const uint64_t abytes = (4 * Ac + 15) & ~15ull;
+            if (used + abytes <= budget) { pl.attrs_in_smem = 1; used += abytes; }
+            const uint64_t WA = (Ac + 63) / 64;
+            const uint64_t mbytes = 8 * Mc * WA;
+            if (WA <= 4 && used + mbytes <= budget) { pl.ck_masks = 1; used += mbytes; }
+            else {
+                const uint64_t rbytes = 4 * Ac * ((Mc + 31) / 32);
+                if (used + rbytes <= budget) { pl.rows_in_smem = 1; used += rbytes; }
+            }
+            need[i] = used;
         }
-        MM_CUDA(ctx, cudaMemcpy(ctx->large_list.p, list.data(), 4ull * ctx->n_large, cudaMemcpyHostToDevice));
+        // launch groups by shared-memory need, so small CTAs are not held to one per SM by a giant
+        std::vector<uint32_t> order(ctx->n_large);
+        for (uint32_t i = 0; i < ctx->n_large; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return need[x] < need[y]; });
+        std::vector<uint32_t> list2(ctx->n_large);
+        std::vector<LargePlan> plans2(ctx->n_large);
+        uint64_t koff = 0, roff = 0;
+        ctx->large_groups.clear();
+        static const uint64_t tiers[] = {16 * 1024, 48 * 1024, 100 * 1024, ~0ull};
+        for (uint32_t j = 0; j < ctx->n_large; ++j) {
+            const uint32_t i = order[j];
+            list2[j] = list[i];
+            plans2[j] = plans[i];
+            LargePlan& pl = plans2[j];
+            if (!pl.keys_in_smem) { pl.keys_off = koff; koff += pl.keys_cap; }
+            const uint32_t c = list[i];
+            const uint64_t Mc = s->class_method_off[c + 1] - s->class_method_off[c];
+            const uint64_t Ac = s->class_attr_off[c + 1] - s->class_attr_off[c];
+            if (!pl.ck_masks && !pl.rows_in_smem) { pl.rows_off = roff; roff += Ac * ((Mc + 31) / 32); }
+            int tier = 0;
+            while (need[i] > tiers[tier]) ++tier;
+            const uint32_t smem = (uint32_t)std::max<uint64_t>(16, (need[i] + 15) & ~15ull);
+            if (ctx->large_groups.empty() || ctx->large_groups.back().tier != tier)
+                ctx->large_groups.push_back({j, 0, smem, tier});
+            auto& g = ctx->large_groups.back();
+            ++g.count;
+            g.smem = std::max(g.smem, smem);
+        }
+        MM_CUDA(ctx, cudaMemcpy(ctx->large_list.p, list2.data(), 4ull * ctx->n_large, cudaMemcpyHostToDevice));
         MM_CUDA(ctx, ctx->plans.ensure(ctx->n_large));
-        MM_CUDA(ctx, cudaMemcpy(ctx->plans.p, plans.data(), sizeof(LargePlan) * ctx->n_large,
+        MM_CUDA(ctx, cudaMemcpy(ctx->plans.p, plans2.data(), sizeof(LargePlan) * ctx->n_large,
                                 cudaMemcpyHostToDevice));
         MM_CUDA(ctx, ctx->gkeys.ensure(koff ? koff : 1));
         MM_CUDA(ctx, ctx->grows.ensure(roff ? roff : 1));
-        ctx->large_smem = (uint32_t)((smem_need + 15) & ~15ull);
-        MM_CUDA(ctx, set_class_large_smem(ctx->large_smem));
+        uint32_t max_smem = 0;
+        for (const auto& g : ctx->large_groups) max_smem = std::max(max_smem, g.smem);
+        MM_CUDA(ctx, set_class_large_smem(max_smem));
+        // exact bitmaps for dense U rows: ≤ one per CTA-path class with > kDenseRowMin
+        // foreign keys, capped at 256 MB (classes past the cap keep Bloom + scan)
+        const uint64_t words = (uint64_t)((C + 31) / 32) * n_dense;
+        ctx->dense_cap = (uint32_t)std::min<uint64_t>(words, 64ull << 20);
+        MM_CUDA(ctx, ctx->dense.ensure(ctx->dense_cap ? ctx->dense_cap : 1));
+    } else {
+        ctx->large_groups.clear();
+        ctx->dense_cap = 0;
     }
     // derived tables
     MM_CUDA(ctx, ctx->recs.ensure(M ? M : 1));
@@ -460,10 +516,10 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
     if (!ctx->have_model) return fail(ctx, MM_E_STATE, "mm_compute_metrics: no model uploaded");
     if (mm_status st = set_device(ctx)) return st;
     Ctl* ctl = ctx->ctl.p;
-    MM_CUDA(ctx, cudaMemsetAsync(&ctl->ucursor, 0, sizeof(uint32_t), ctx->stream));
+    MM_CUDA(ctx, cudaMemsetAsync(&ctl->ucursor, 0, 2 * sizeof(uint32_t), ctx->stream));  // ucursor, dense_cursor
     const DevModel dm = ctx->dev();
     mm_status st = run(ctx, "method", [&] {
-        launch_method(dm, ctx->max_deg, ctx->recs.p, ctx->own_mask.p, ctx->pos_owner.p, ctx->stream);
+        launch_method(dm, ctx->kind.p, ctx->recs.p, ctx->own_mask.p, ctx->pos_owner.p, ctx->stream);
     });
     if (st) return st;
     st = run(ctx, "class_small", [&] {
@@ -473,9 +529,12 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
     if (st) return st;
     if (ctx->n_large) {
         st = run(ctx, "class_large", [&] {
-            launch_class_large(dm, ctx->n_large, ctx->large_list.p, ctx->plans.p, ctx->large_smem,
-                               ctx->recs.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
-                               ctx->un.p, &ctl->ucursor, ctx->gkeys.p, ctx->grows.p, ctx->stream);
+            for (const auto& g : ctx->large_groups)
+                launch_class_large(dm, g.count, ctx->large_list.p + g.first, ctx->plans.p + g.first, g.smem,
+                                   ctx->recs.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
+                                   ctx->un.p, &ctl->ucursor, ctx->gkeys.p, ctx->grows.p,
+                                   ctx->dense_cap ? ctx->dense.p : nullptr, ctx->dense_cap, &ctl->dense_cursor,
+                                   ctx->stream);
         });
         if (st) return st;
     }
@@ -555,8 +614,8 @@ mm_status mm_what_if(mm_ctx* ctx, uint32_t method, uint32_t origin, uint32_t des
     if (mm_status st = ensure_metrics(ctx)) return st;
     const DevModel dm = ctx->dev();
     mm_status st = run(ctx, "what_if", [&] {
-        launch_what_if(dm, ctx->rec.p, ctx->ux.p, ctx->un.p, method, origin, destination, ctx->whatif.p,
-                       ctx->stream);
+        launch_what_if(dm, ctx->rec.p, ctx->ux.p, ctx->un.p, ctx->dense.p, method, origin, destination,
+                       ctx->whatif.p, ctx->stream);
     });
     if (st) return st;
     MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->whatif.p, sizeof *out, cudaMemcpyDeviceToHost, ctx->stream));
@@ -629,6 +688,7 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     a.n_emit = &ctl->n_emit;
     a.ux = ctx->ux.p;
     a.un = ctx->un.p;
+    a.dense = ctx->dense.p;
     a.dthr = &ctl->thr;
     a.thr_lcom = p->thr_lcom;
     a.thr_cbo = p->thr_cbo;

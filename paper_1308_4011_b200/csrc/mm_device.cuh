@@ -51,9 +51,10 @@ struct __align__(64) ClassRec {
     uint32_t H;      // Σ_{p∈c} |acc(p) ∩ attrs(c)|
     uint32_t cbo;    // |U row|
     uint32_t ubase;  // U row start in ux/un
-    uint32_t pad;
+    uint32_t dense;  // word offset of an exact class bitmap of the U row (dense rows), or kNone
     uint32_t sig[kSigWords];
 };
+constexpr uint32_t kDenseRowMin = 64;  // rows longer than this get an exact bitmap (CTA path)
 
 __device__ __forceinline__ uint32_t bloom_h1(uint32_t x) {
     return (uint32_t)(((uint64_t)(x * 0x9E3779B1u) * kSigBits) >> 32);
@@ -230,7 +231,7 @@ __device__ __forceinline__ ClassRec load_rec(const ClassRec* __restrict__ rec, u
     const uint4 a = __ldg(p), b = __ldg(p + 1);
     ClassRec r;
     r.A = a.x; r.M = a.y; r.H = a.z; r.cbo = a.w;
-    r.ubase = b.x; r.pad = b.y;  // sig words stay in memory: read on demand (same cache line)
+    r.ubase = b.x; r.dense = b.y;  // sig words stay in memory: read on demand (same cache line)
     return r;
 }
 
@@ -257,7 +258,7 @@ __device__ __forceinline__ ClassRecFull load_rec_full(const ClassRec* __restrict
     const uint4 a = __ldg(p), b = __ldg(p + 1), q = __ldg(p + 2), t = __ldg(p + 3);
     ClassRecFull f;
     f.r.A = a.x; f.r.M = a.y; f.r.H = a.z; f.r.cbo = a.w;
-    f.r.ubase = b.x; f.r.pad = b.y;
+    f.r.ubase = b.x; f.r.dense = b.y;
     f.sig[0] = b.z; f.sig[1] = b.w;
     f.sig[2] = q.x; f.sig[3] = q.y; f.sig[4] = q.z; f.sig[5] = q.w;
     f.sig[6] = t.x; f.sig[7] = t.y; f.sig[8] = t.z; f.sig[9] = t.w;

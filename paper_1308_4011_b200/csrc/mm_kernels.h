@@ -10,12 +10,13 @@ namespace mmg {
 
 // Per large class (CTA path) scratch placement, planned on the host at upload.
 struct LargePlan {
-    uint64_t keys_off;   // u64 element offset into the global key scratch
-    uint64_t rows_off;   // u32 element offset into the global row scratch
-    uint32_t keys_cap;   // power of two ≥ foreign edge count
+    uint64_t keys_off;     // u32 element offset into the global key scratch
+    uint64_t rows_off;     // u32 element offset into the global row scratch
+    uint32_t keys_cap;     // power of two ≥ foreign edge count (≥ foreign keys)
     uint8_t keys_in_smem;
     uint8_t rows_in_smem;
-    uint8_t pad[2];
+    uint8_t attrs_in_smem;
+    uint8_t ck_masks;      // 1: per-member own-attribute masks (A ≤ 256) in smem; 0: attribute bitmaps
 };
 
 struct SweepArgs {
@@ -30,6 +31,7 @@ struct SweepArgs {
     uint32_t* n_emit;           // their count
     const uint32_t* ux;
     const uint32_t* un;
+    const uint32_t* dense;      // exact U-row bitmaps of dense classes (ClassRec::dense)
     const DevThresholds* dthr;  // used when thr_device != 0
     double thr_lcom, thr_cbo;
     uint32_t thr_device;
@@ -50,7 +52,7 @@ void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st);
 void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list, uint32_t* n_large,
                          uint32_t* max_deg, uint32_t* foreign, cudaStream_t st);
-void launch_method(const DevModel& s, uint32_t maxdeg, MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner,
+void launch_method(const DevModel& s, const uint8_t* kind, MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner,
                    cudaStream_t st);
 void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, const uint64_t* own_mask,
                         ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,
@@ -58,7 +60,8 @@ void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, c
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
                         uint32_t smem_bytes, MethRec* recs, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
-                        uint64_t* gkeys, uint32_t* grows, cudaStream_t st);
+                        uint32_t* gkeys, uint32_t* grows, uint32_t* dense, uint32_t dense_cap,
+                        uint32_t* dense_cursor, cudaStream_t st);
 cudaError_t set_class_large_smem(uint32_t bytes);
 // means with sequential-sum semantics; cbo may be NULL (treated as zeros)
 size_t thresholds_scratch_bytes(uint32_t n);
@@ -70,6 +73,6 @@ void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 constexpr uint32_t kSweepTile = 256;
 void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un,
-                    uint32_t u, uint32_t o, uint32_t d, mm_whatif* out, cudaStream_t st);
+                    const uint32_t* dense, uint32_t u, uint32_t o, uint32_t d, mm_whatif* out, cudaStream_t st);
 
 }  // namespace mmg
