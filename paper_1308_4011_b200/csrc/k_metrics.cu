@@ -102,7 +102,7 @@ __device__ __forceinline__ uint32_t attr_pos(const DevModel& s, uint32_t ab, uin
 // its MethRec; the own-attribute mask has bit k for the k-th attribute of the
 // own class (classes with ≤ 64 attributes).
 template <int K>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 5)
 k_method(DevModel s, const uint8_t* __restrict__ kind, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask,
          uint32_t* __restrict__ pos_owner) {
     const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
@@ -401,7 +401,8 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind,
 // CTA path: one CTA per large class (any M, A, degree)
 // ---------------------------------------------------------------------------
 
-constexpr int kLargeThreads = 256;
+constexpr int kLargeThreads = 256;     // default CTA size; the largest classes launch with 1024
+constexpr int kMaxWarps = 32;
 
 __device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -411,7 +412,7 @@ __device__ __forceinline__ uint64_t block_sum_u64(uint64_t v, uint64_t* red) {
     if (lane == 0) red[warp] = v;
     __syncthreads();
     uint64_t t = 0;
-    for (int w = 0; w < kLargeThreads / 32; ++w) t += red[w];
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += red[w];
     __syncthreads();
     return t;
 }
@@ -424,7 +425,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* red, u
     if (lane == 31) red[warp] = inc;
     __syncthreads();
     uint32_t before = 0, all = 0;
-    for (int w = 0; w < kLargeThreads / 32; ++w) {
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
         if (w < warp) before += red[w];
         all += red[w];
     }
@@ -488,7 +489,7 @@ __device__ __forceinline__ void member_used(const DevModel& s, const MethRec* re
 // already distinct, so a run length IS the member count U[c][X]), and the
 // LCOM-CK structure: per-member own-attribute masks (A ≤ 256: pairs tested by
 // word ANDs) or per-attribute member bitmaps (sparse giants).
-__global__ void __launch_bounds__(kLargeThreads)
+__global__ void __launch_bounds__(1024)
 k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* __restrict__ plan,
               MethRec* __restrict__ recs, ClassRec* __restrict__ rec,
               double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
@@ -496,8 +497,8 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
               uint32_t* __restrict__ gkeys, uint32_t* __restrict__ grows, uint32_t* __restrict__ dense,
               uint32_t dense_cap, uint32_t* __restrict__ dense_cursor) {
     extern __shared__ __align__(16) unsigned char dsm[];
-    __shared__ uint64_t red64[kLargeThreads / 32];
-    __shared__ uint32_t red32[kLargeThreads / 32];
+    __shared__ uint64_t red64[kMaxWarps];
+    __shared__ uint32_t red32[kMaxWarps];
     __shared__ uint32_t s_nk, s_ubase, s_dense;
     __shared__ uint32_t s_sig[kSigWords];
     const uint32_t c = large_list[blockIdx.x];
@@ -524,7 +525,9 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     uint32_t* ckz = pl.ck_masks ? reinterpret_cast<uint32_t*>(masks) : rows;
     if (threadIdx.x == 0) s_nk = 0;
     if (threadIdx.x < kSigWords) s_sig[threadIdx.x] = 0;
-    for (uint64_t i = threadIdx.x; i < ck_words; i += blockDim.x) ckz[i] = 0;
+    // (global-scratch bitmaps are cleared by one cudaMemsetAsync before the launch)
+    if (pl.ck_masks || pl.rows_in_smem)
+        for (uint64_t i = threadIdx.x; i < ck_words; i += blockDim.x) ckz[i] = 0;
     __syncthreads();
 
     // phase 1: members' foreign used classes -> keys; H; own-attribute sets
@@ -619,9 +622,13 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         r->hdr = hdr | (removed << kRecRemovedShift) | kRecRemovedValid;
     }
 
-    // phase 4: LCOM-CK, Q = #pairs (i<j) sharing an own attribute
+    // phase 4: LCOM-CK, Q = #pairs (i<j) sharing an own attribute. Classes
+    // whose attribute bitmaps live in global scratch (Zipf giants) are split
+    // over many CTAs by k_ck_rows instead (ck_out[c] accumulates Q there).
+    const bool split = !pl.ck_masks && !pl.rows_in_smem;
     uint64_t q = 0;
-    if (pl.ck_masks) {
+    if (split) {
+    } else if (pl.ck_masks) {
         for (uint32_t i = threadIdx.x; i < M; i += blockDim.x)
             for (uint32_t j = i + 1; j < M; ++j) {
                 uint64_t any = 0;
@@ -631,7 +638,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     } else {
         // rows[a] = members using a; member i's sharers = OR of its rows, above i
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        for (uint32_t i = warp; i < M; i += kLargeThreads / 32) {
+        for (uint32_t i = warp; i < M; i += blockDim.x / 32) {
             const uint32_t p = s.cls_methods[mb + i];
             const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
             for (uint32_t wb = 0; wb < W; wb += 32) {
@@ -658,9 +665,85 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         for (int w = 0; w < kSigWords; ++w) r.sig[w] = s_sig[w];
         rec[c] = r;
         lcom_out[c] = l;
-        ck_out[c] = P > Q ? P - Q : 0;
+        ck_out[c] = split ? 0ull : (P > Q ? P - Q : 0);
         cbo_out[c] = nx;
     }
+}
+
+// LCOM-CK of a split class, one CTA per (class, 256-member chunk): member i's
+// sharers above it = OR of the bitmaps rows[a] of its own attributes a.
+__global__ void __launch_bounds__(kLargeThreads)
+k_ck_rows(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* __restrict__ plan,
+          const uint2* __restrict__ items, const uint32_t* __restrict__ grows, uint64_t* __restrict__ ck_out) {
+    __shared__ uint64_t red64[kLargeThreads / 32];
+    const uint2 it = items[blockIdx.x];  // (index into the large list, first member)
+    const uint32_t c = large_list[it.x];
+    const LargePlan pl = plan[it.x];
+    const uint32_t mb = s.cls_moff[c];
+    const uint32_t M = s.cls_moff[c + 1] - mb;
+    const uint32_t ab0 = s.cls_aoff[c];
+    const uint32_t A = s.cls_aoff[c + 1] - ab0;
+    const uint32_t W = (M + 31) / 32;
+    const uint32_t* rows = grows + pl.rows_off;
+    const uint32_t* attrs = s.cls_attrs + ab0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t iend = min(M, it.y + kLargeThreads);
+    uint64_t q = 0;
+    for (uint32_t i = it.y + warp; i < iend; i += kLargeThreads / 32) {
+        const uint32_t p = s.cls_methods[mb + i];
+        const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+        // the member's own-attribute positions, gathered once (lane-parallel)
+        uint32_t mypos = kNone;
+        uint32_t nown = 0;
+        __shared__ uint32_t spos[kLargeThreads / 32][64];
+        for (uint32_t e0 = ab; e0 < ae; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            bool own = false;
+            if (e < ae) {
+                const uint32_t t = __ldg(s.acc_tgt + e);
+                own = __ldg(s.attribute_owner + t) == c;
+                if (own) mypos = lower_bound_u32(attrs, A, t);
+            }
+            const uint32_t b = __ballot_sync(0xffffffffu, own);
+            if (own) {
+                const uint32_t at = nown + __popc(b & ((1u << lane) - 1));
+                if (at < 64) spos[warp][at] = mypos;
+            }
+            nown += __popc(b);
+        }
+        __syncwarp();
+        const uint32_t nk = min(nown, 64u);
+        for (uint32_t wb = (i >> 5) & ~31u; wb < W; wb += 32) {
+            const uint32_t w = wb + lane;
+            uint32_t acc = 0;
+            if (w < W && w >= (i >> 5)) {
+                for (uint32_t k = 0; k < nk; ++k) acc |= __ldg(rows + (uint64_t)spos[warp][k] * W + w);
+                if (nown > 64) {  // rare: more own attributes than the staging list
+                    for (uint32_t e = ab; e < ae; ++e) {
+                        const uint32_t t = __ldg(s.acc_tgt + e);
+                        if (__ldg(s.attribute_owner + t) == c) acc |= __ldg(rows + (uint64_t)lower_bound_u32(attrs, A, t) * W + w);
+                    }
+                }
+                if (w == (i >> 5)) acc &= ((i & 31) == 31) ? 0u : (~0u << ((i & 31) + 1));
+            }
+            q += __popc(acc);
+        }
+        __syncwarp();
+    }
+    const uint64_t Q = block_sum_u64(q, red64);
+    if (threadIdx.x == 0 && Q) atomicAdd(reinterpret_cast<unsigned long long*>(ck_out + c), (unsigned long long)Q);
+}
+
+// P = C(M,2) - Q; lcom_ck = P > Q ? P - Q : 0 (metrics.hpp:147-156) for the split classes
+__global__ void k_ck_finalize(DevModel s, const uint32_t* __restrict__ split_list, uint32_t n,
+                              uint64_t* __restrict__ ck_out) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t c = split_list[k];
+    const uint64_t M = s.cls_moff[c + 1] - s.cls_moff[c];
+    const uint64_t Q = ck_out[c];
+    const uint64_t P = M * (M - 1) / 2 - Q;
+    ck_out[c] = P > Q ? P - Q : 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -698,11 +781,18 @@ void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* lar
                         uint32_t smem_bytes, MethRec* recs, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
                         uint32_t* gkeys, uint32_t* grows, uint32_t* dense, uint32_t dense_cap,
-                        uint32_t* dense_cursor, cudaStream_t st) {
+                        uint32_t* dense_cursor, uint32_t threads, cudaStream_t st) {
     if (!n_large) return;
-    k_class_large<<<n_large, kLargeThreads, smem_bytes, st>>>(s, large_list, plan, recs, rec, lcom, ck, cbo, ux,
+    k_class_large<<<n_large, threads, smem_bytes, st>>>(s, large_list, plan, recs, rec, lcom, ck, cbo, ux,
                                                               un, ucursor, gkeys, grows, dense, dense_cap,
                                                               dense_cursor);
+}
+void launch_ck_rows(const DevModel& s, const uint32_t* large_list, const LargePlan* plan, const uint2* items,
+                    uint32_t n_items, const uint32_t* grows, const uint32_t* split_list, uint32_t n_split,
+                    uint64_t* ck, cudaStream_t st) {
+    if (!n_items) return;
+    k_ck_rows<<<n_items, kLargeThreads, 0, st>>>(s, large_list, plan, items, grows, ck);
+    k_ck_finalize<<<(n_split + 127) / 128, 128, 0, st>>>(s, split_list, n_split, ck);
 }
 cudaError_t set_class_large_smem(uint32_t bytes) {
     return cudaFuncSetAttribute(k_class_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);

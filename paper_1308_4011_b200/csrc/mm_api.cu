@@ -96,6 +96,10 @@ struct mm_ctx {
     std::vector<LargeGroup> large_groups;  // CTA-path launches, grouped by shared-memory need
     DBuf<uint32_t> dense;                  // exact U-row bitmaps of dense classes
     uint32_t dense_cap = 0;
+    DBuf<uint2> ck_items;                  // (large index, first member) chunks of split LCOM-CK classes
+    DBuf<uint32_t> split_list;             // the split classes
+    uint32_t n_ck_items = 0, n_split = 0;
+    uint64_t grows_words = 0;              // global attribute-bitmap scratch in use
     DBuf<uint8_t> kind;
     DBuf<uint32_t> large_list, foreign;
     DBuf<LargePlan> plans;
@@ -210,6 +214,8 @@ void free_model(mm_ctx* c) {
     c->plans.release();
     c->gkeys.release();
     c->dense.release();
+    c->ck_items.release();
+    c->split_list.release();
     c->rec.release();
     c->lcom.release();
     c->ck.release();
@@ -472,12 +478,32 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             ++g.count;
             g.smem = std::max(g.smem, smem);
         }
+        // classes whose attribute bitmaps live in global scratch: LCOM-CK split over 256-member chunks
+        std::vector<uint2> items;
+        std::vector<uint32_t> split;
+        for (uint32_t j = 0; j < ctx->n_large; ++j) {
+            const LargePlan& pl = plans2[j];
+            if (pl.ck_masks || pl.rows_in_smem) continue;
+            const uint32_t c = list2[j];
+            const uint32_t Mc = s->class_method_off[c + 1] - s->class_method_off[c];
+            split.push_back(c);
+            for (uint32_t b = 0; b < Mc; b += 256) items.push_back(make_uint2(j, b));
+        }
+        ctx->n_ck_items = (uint32_t)items.size();
+        ctx->n_split = (uint32_t)split.size();
+        MM_CUDA(ctx, ctx->ck_items.ensure(items.size() ? items.size() : 1));
+        MM_CUDA(ctx, ctx->split_list.ensure(split.size() ? split.size() : 1));
+        if (!items.empty()) {
+            MM_CUDA(ctx, cudaMemcpy(ctx->ck_items.p, items.data(), sizeof(uint2) * items.size(), cudaMemcpyHostToDevice));
+            MM_CUDA(ctx, cudaMemcpy(ctx->split_list.p, split.data(), 4 * split.size(), cudaMemcpyHostToDevice));
+        }
         MM_CUDA(ctx, cudaMemcpy(ctx->large_list.p, list2.data(), 4ull * ctx->n_large, cudaMemcpyHostToDevice));
         MM_CUDA(ctx, ctx->plans.ensure(ctx->n_large));
         MM_CUDA(ctx, cudaMemcpy(ctx->plans.p, plans2.data(), sizeof(LargePlan) * ctx->n_large,
                                 cudaMemcpyHostToDevice));
         MM_CUDA(ctx, ctx->gkeys.ensure(koff ? koff : 1));
         MM_CUDA(ctx, ctx->grows.ensure(roff ? roff : 1));
+        ctx->grows_words = roff;
         uint32_t max_smem = 0;
         for (const auto& g : ctx->large_groups) max_smem = std::max(max_smem, g.smem);
         MM_CUDA(ctx, set_class_large_smem(max_smem));
@@ -489,6 +515,8 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     } else {
         ctx->large_groups.clear();
         ctx->dense_cap = 0;
+        ctx->n_ck_items = ctx->n_split = 0;
+        ctx->grows_words = 0;
     }
     // derived tables
     MM_CUDA(ctx, ctx->recs.ensure(M ? M : 1));
@@ -528,13 +556,16 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
     });
     if (st) return st;
     if (ctx->n_large) {
+        if (ctx->grows_words) MM_CUDA(ctx, cudaMemsetAsync(ctx->grows.p, 0, 4ull * ctx->grows_words, ctx->stream));
         st = run(ctx, "class_large", [&] {
             for (const auto& g : ctx->large_groups)
                 launch_class_large(dm, g.count, ctx->large_list.p + g.first, ctx->plans.p + g.first, g.smem,
                                    ctx->recs.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
                                    ctx->un.p, &ctl->ucursor, ctx->gkeys.p, ctx->grows.p,
                                    ctx->dense_cap ? ctx->dense.p : nullptr, ctx->dense_cap, &ctl->dense_cursor,
-                                   ctx->stream);
+                                   g.tier >= 3 ? 1024u : 256u, ctx->stream);  // giants: 4x the threads
+            launch_ck_rows(dm, ctx->large_list.p, ctx->plans.p, ctx->ck_items.p, ctx->n_ck_items, ctx->grows.p,
+                           ctx->split_list.p, ctx->n_split, ctx->ck.p, ctx->stream);
         });
         if (st) return st;
     }

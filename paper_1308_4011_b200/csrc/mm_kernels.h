@@ -61,8 +61,11 @@ void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* lar
                         uint32_t smem_bytes, MethRec* recs, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
                         uint32_t* gkeys, uint32_t* grows, uint32_t* dense, uint32_t dense_cap,
-                        uint32_t* dense_cursor, cudaStream_t st);
+                        uint32_t* dense_cursor, uint32_t threads, cudaStream_t st);
 cudaError_t set_class_large_smem(uint32_t bytes);
+void launch_ck_rows(const DevModel& s, const uint32_t* large_list, const LargePlan* plan, const uint2* items,
+                    uint32_t n_items, const uint32_t* grows, const uint32_t* split_list, uint32_t n_split,
+                    uint64_t* ck, cudaStream_t st);
 // means with sequential-sum semantics; cbo may be NULL (treated as zeros)
 size_t thresholds_scratch_bytes(uint32_t n);
 cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,

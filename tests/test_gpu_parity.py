@@ -134,6 +134,10 @@ def test_gpu_large_class_paths(gpu_engine):
              intra_class_bias=0.5, zipf_s=1.0),  # C3-like Zipf skew
         dict(seed=12, n_classes=1, n_methods=300, n_attributes=40, k_max_calls=20, k_max_accesses=20,
              intra_class_bias=0.7),   # single class
+        dict(seed=13, n_classes=150, n_methods=9000, n_attributes=3000, k_max_calls=6, k_max_accesses=6,
+             intra_class_bias=0.1),   # dense coupling: U rows > 64 -> exact class bitmaps
+        dict(seed=14, n_classes=40, n_methods=4000, n_attributes=30000, k_max_calls=3, k_max_accesses=24,
+             intra_class_bias=0.6),   # A > 256 per class: attribute-bitmap LCOM-CK, degree > 16
     ]
     for cfg in cfgs:
         s = System.generate(**cfg)
