@@ -78,7 +78,18 @@ def algorithmic_bytes(sys_, nnz_u: int, n_sugg: int, rank_share: float = 1.0) ->
     m, c, a = sys_.n_methods, sys_.n_classes, sys_.n_attributes
     E = sys_.n_calls + sys_.n_accesses
     ms = int(m * rank_share)
+    # classes on the CTA path (M > 32, A > 64 or a member of degree > 16), as mm_upload plans them
+    msz = np.diff(sys_.class_method_off).astype(np.int64)
+    asz = np.diff(sys_.class_attr_off).astype(np.int64)
+    deg = (np.diff(sys_.call_off) + np.diff(sys_.acc_off)).astype(np.int64)
+    owner_of_pos = np.repeat(np.arange(c), msz)
+    maxdeg = np.zeros(c, np.int64)
+    np.maximum.at(maxdeg, owner_of_pos, deg[sys_.class_methods])
+    large = (msz > 32) | (asz > 64) | (maxdeg > 16)
+    m_l, c_l, a_l = int(msz[large].sum()), int(large.sum()), int(asz[large].sum())
+    e_l = int(deg[sys_.class_methods][np.repeat(large, msz)].sum())
     k = {
+        "class_large": 36 * m_l + 8 * e_l + 8 * a_l + 93 * c_l + 8 * nnz_u,
         "method": 64 * m + 8 * a + 4 * E + 4 * c,
         "class_small": 44 * m + 93 * c + 8 * nnz_u,
         "thresholds": 12 * c,

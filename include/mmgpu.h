@@ -217,8 +217,9 @@ mm_status mm_cbo(mm_ctx* ctx, uint32_t cls, uint32_t* out);
 mm_status mm_compute_thresholds(mm_ctx* ctx, const mm_overrides* ov, mm_thresholds* out);
 /* Mean of caller-supplied doubles with compute_thresholds' sequential
  * left-to-right double-sum semantics (suggest.hpp:48-53), bit-identical,
- * computed on the device (parallel exact emulation; serial device fallback
- * outside its preconditions). *fast_path (may be NULL) reports which ran.
+ * computed on the device (always the parallel exact emulation when its
+ * preconditions hold; serial device loop otherwise). *fast_path (may be NULL)
+ * reports which ran.
  * Used for caller-built report vectors and to test the threshold kernel. */
 mm_status mm_sequential_mean(mm_ctx* ctx, const double* values, uint64_t n, double* out, int* fast_path);
 

@@ -46,32 +46,47 @@ __global__ void k_validate_offsets(const uint32_t* __restrict__ off, uint64_t n_
 
 // Per class: member/attribute counts, Σ degree, max degree, foreign-edge
 // count; classify into the warp path (small) or the CTA path (large).
-__global__ void k_plan_classes(DevModel s, uint8_t* __restrict__ kind, uint32_t* __restrict__ large_list,
-                               uint32_t* __restrict__ n_large, uint32_t* __restrict__ max_deg,
-                               uint32_t* __restrict__ foreign) {
-    // every index is bounds-checked: this runs before the validation result is known
+// Upload-time plan, method-parallel (a class-per-thread loop serialises on
+// Zipf giants): per member, its degree and foreign-edge count, folded into its
+// class with atomics. Every index is bounds-checked: this runs before the
+// validation result is known.
+__global__ void k_plan_methods(DevModel s, uint32_t* __restrict__ foreign, uint32_t* __restrict__ cmaxdeg) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= s.M) return;
+    uint32_t lo = 0, hi = s.C;  // class of position i: last c with cls_moff[c] <= i
+    while (lo + 1 < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s.cls_moff[mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    const uint32_t c = lo;
+    const uint32_t p = s.cls_methods[i];
+    if (p >= s.M || c >= s.C) return;
+    const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
+    const uint32_t cb = min(s.call_off[p], Ec), ce = min(max(s.call_off[p + 1], cb), Ec);
+    const uint32_t ab = min(s.acc_off[p], Ea), ae = min(max(s.acc_off[p + 1], ab), Ea);
+    uint32_t fr = 0;
+    for (uint32_t e = cb; e < ce; ++e) {
+        const uint32_t t = s.call_tgt[e];
+        fr += t >= s.M || s.method_owner[t] != c;
+    }
+    for (uint32_t e = ab; e < ae; ++e) {
+        const uint32_t t = s.acc_tgt[e];
+        fr += t >= s.A || s.attribute_owner[t] != c;
+    }
+    if (fr) atomicAdd(foreign + c, fr);
+    atomicMax(cmaxdeg + c, (ce - cb) + (ae - ab));
+}
+
+// classify into the warp path (small) or the CTA path (large)
+__global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg, uint8_t* __restrict__ kind,
+                               uint32_t* __restrict__ large_list, uint32_t* __restrict__ n_large,
+                               uint32_t* __restrict__ max_deg) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= s.C) return;
     const uint32_t mb = min(s.cls_moff[c], s.M), me = min(max(s.cls_moff[c + 1], mb), s.M);
     const uint32_t A = s.cls_aoff[c + 1] - s.cls_aoff[c];
-    const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
-    uint32_t mdeg = 0, fr = 0;
-    for (uint32_t i = mb; i < me; ++i) {
-        const uint32_t p = s.cls_methods[i];
-        if (p >= s.M) continue;
-        const uint32_t cb = min(s.call_off[p], Ec), ce = min(max(s.call_off[p + 1], cb), Ec);
-        const uint32_t ab = min(s.acc_off[p], Ea), ae = min(max(s.acc_off[p + 1], ab), Ea);
-        mdeg = max(mdeg, (ce - cb) + (ae - ab));
-        for (uint32_t e = cb; e < ce; ++e) {
-            const uint32_t t = s.call_tgt[e];
-            fr += t >= s.M || s.method_owner[t] != c;
-        }
-        for (uint32_t e = ab; e < ae; ++e) {
-            const uint32_t t = s.acc_tgt[e];
-            fr += t >= s.A || s.attribute_owner[t] != c;
-        }
-    }
-    foreign[c] = fr;
+    const uint32_t mdeg = cmaxdeg[c];
     const bool small = (me - mb) <= kSmallMaxMembers && A <= kSmallMaxAttrs && mdeg <= kSmallMaxDeg &&
                        s.C < (1u << 27);  // warp path packs X << 5 | member into 32 bits
     kind[c] = small ? 0 : 1;
@@ -760,9 +775,12 @@ void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, u
     k_validate_offsets<<<blocks, 256, 0, st>>>(off, n1, total, bad);
 }
 void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list, uint32_t* n_large,
-                         uint32_t* max_deg, uint32_t* foreign, cudaStream_t st) {
+                         uint32_t* max_deg, uint32_t* foreign, uint32_t* cmaxdeg, cudaStream_t st) {
     if (!s.C) return;
-    k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, kind, large_list, n_large, max_deg, foreign);
+    cudaMemsetAsync(foreign, 0, 4ull * s.C, st);
+    cudaMemsetAsync(cmaxdeg, 0, 4ull * s.C, st);
+    if (s.M) k_plan_methods<<<(s.M + 255) / 256, 256, 0, st>>>(s, foreign, cmaxdeg);
+    k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, cmaxdeg, kind, large_list, n_large, max_deg);
 }
 void launch_method(const DevModel& s, const uint8_t* kind, MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner,
                    cudaStream_t st) {

@@ -438,20 +438,37 @@ k_thresholds_coop(const double* __restrict__ lcom, const uint32_t* __restrict__ 
 }
 
 // Serial fallback kernel (n too large for one co-resident tile per CTA).
+// The sequential sums literally, by one warp: each 32-element chunk is loaded
+// coalesced, then every lane runs the same left-to-right chain over the
+// shuffled values (loads and shuffles stay off the dependent add chain).
+// Exact for any input; used for small n (faster than the cooperative kernel's
+// grid syncs below ~16k classes) and as the fallback.
 __global__ void k_thresholds_serial(const double* __restrict__ lcom, const uint32_t* __restrict__ cbo, uint32_t n,
                                     DevThresholds* __restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (blockIdx.x != 0) return;
+    const int lane = threadIdx.x & 31;
     double sl = 0.0, sc = 0.0;
-    for (uint32_t i = 0; i < n; ++i) {
-        sl = __dadd_rn(sl, lcom[i]);
-        sc = __dadd_rn(sc, cbo ? (double)cbo[i] : 0.0);
+    for (uint32_t b = 0; b < n; b += 32) {
+        const uint32_t i = b + lane;
+        const double v = i < n ? lcom[i] : 0.0;
+        const double w = (i < n && cbo) ? (double)cbo[i] : 0.0;
+        const uint32_t m = min(32u, n - b);
+#pragma unroll 8
+        for (uint32_t k = 0; k < m; ++k) {
+            sl = __dadd_rn(sl, __shfl_sync(0xffffffffu, v, k));
+            sc = __dadd_rn(sc, __shfl_sync(0xffffffffu, w, k));
+        }
     }
-    out->lcom = n ? __ddiv_rn(sl, (double)n) : 0.0;
-    out->cbo = n ? __ddiv_rn(sc, (double)n) : 0.0;
-    out->fast_path_ok = 0;
+    if (lane == 0) {
+        out->lcom = n ? __ddiv_rn(sl, (double)n) : 0.0;
+        out->cbo = n ? __ddiv_rn(sc, (double)n) : 0.0;
+        out->fast_path_ok = 0;
+    }
 }
 
 }  // namespace
+
+constexpr uint32_t kSerialMax = 12288;  // below this one warp's serial chain beats three grid syncs
 
 size_t thresholds_scratch_bytes(uint32_t n) {
     const size_t tiles = (n + kTile - 1) / kTile;
@@ -459,7 +476,7 @@ size_t thresholds_scratch_bytes(uint32_t n) {
 }
 
 cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
-                              void* scratch, size_t scratch_bytes, cudaStream_t st) {
+                              void* scratch, size_t scratch_bytes, cudaStream_t st, bool allow_serial) {
     const uint32_t tiles = (n + kTile - 1) / kTile;
     static int max_coresident = -1;
     if (max_coresident < 0) {
@@ -469,7 +486,8 @@ cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_thresholds_coop, kTT, 0);
         max_coresident = sms * per_sm;
     }
-    if (n == 0 || tiles > (uint32_t)max_coresident || scratch_bytes < thresholds_scratch_bytes(n)) {
+    if (n == 0 || (allow_serial && n <= kSerialMax) || tiles > (uint32_t)max_coresident ||
+        scratch_bytes < thresholds_scratch_bytes(n)) {
         k_thresholds_serial<<<1, 32, 0, st>>>(lcom, cbo, n, out);
         return cudaGetLastError();
     }

@@ -101,7 +101,7 @@ struct mm_ctx {
     uint32_t n_ck_items = 0, n_split = 0;
     uint64_t grows_words = 0;              // global attribute-bitmap scratch in use
     DBuf<uint8_t> kind;
-    DBuf<uint32_t> large_list, foreign;
+    DBuf<uint32_t> large_list, foreign, cmaxdeg;
     DBuf<LargePlan> plans;
     DBuf<uint32_t> gkeys;
     DBuf<uint32_t> grows;
@@ -204,7 +204,7 @@ void resolve_pending(mm_ctx* ctx) {
 void free_model(mm_ctx* c) {
     for (DBuf<uint32_t>* b : {&c->method_owner, &c->attribute_owner, &c->cls_moff, &c->cls_methods, &c->cls_aoff,
                               &c->cls_attrs, &c->call_off, &c->call_tgt, &c->acc_off, &c->acc_tgt,
-                              &c->large_list, &c->foreign, &c->grows, &c->cbo, &c->ux,
+                              &c->large_list, &c->foreign, &c->cmaxdeg, &c->grows, &c->cbo, &c->ux,
                               &c->un})
         b->release();
     c->recs.release();
@@ -403,10 +403,11 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, ctx->kind.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->large_list.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->foreign.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->cmaxdeg.ensure(C ? C : 1));
     const DevModel dm = ctx->dev();
     st = run(ctx, "plan", [&] {
         launch_plan_classes(dm, ctx->kind.p, ctx->large_list.p, &ctl->n_large, &ctl->max_deg, ctx->foreign.p,
-                            ctx->stream);
+                            ctx->cmaxdeg.p, ctx->stream);
     });
     if (st) return st;
     Ctl h{};
@@ -806,7 +807,7 @@ mm_status mm_sequential_mean(mm_ctx* ctx, const double* values, uint64_t n, doub
     MM_CUDA(ctx, scratch.alloc(thresholds_scratch_bytes((uint32_t)n)));
     cudaError_t te = cudaSuccess;
     mm_status st = run(ctx, "thresholds", [&] {
-        te = launch_thresholds(d.p, nullptr, (uint32_t)n, dt, scratch.p, scratch.n, ctx->stream);
+        te = launch_thresholds(d.p, nullptr, (uint32_t)n, dt, scratch.p, scratch.n, ctx->stream, false);
     });
     if (st) return st;
     if (te != cudaSuccess) return cuda_fail(ctx, te, "thresholds");

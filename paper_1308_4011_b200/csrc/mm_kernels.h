@@ -51,7 +51,7 @@ struct SweepArgs {
 void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t* bad, cudaStream_t st);
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st);
 void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list, uint32_t* n_large,
-                         uint32_t* max_deg, uint32_t* foreign, cudaStream_t st);
+                         uint32_t* max_deg, uint32_t* foreign, uint32_t* cmaxdeg, cudaStream_t st);
 void launch_method(const DevModel& s, const uint8_t* kind, MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner,
                    cudaStream_t st);
 void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, const uint64_t* own_mask,
@@ -68,8 +68,9 @@ void launch_ck_rows(const DevModel& s, const uint32_t* large_list, const LargePl
                     uint64_t* ck, cudaStream_t st);
 // means with sequential-sum semantics; cbo may be NULL (treated as zeros)
 size_t thresholds_scratch_bytes(uint32_t n);
+// allow_serial: small n may take the one-warp serial kernel (faster there)
 cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
-                              void* scratch, size_t scratch_bytes, cudaStream_t st);
+                              void* scratch, size_t scratch_bytes, cudaStream_t st, bool allow_serial = true);
 void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 uint32_t offsets_tiles(uint64_t npos);
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
