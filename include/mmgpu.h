@@ -237,6 +237,14 @@ mm_status mm_set_gates(mm_ctx* ctx, const double* lcom, const uint32_t* cbo);
 /* Runs the sweep on the device; the ordered result stays resident.
  * n_out (may be NULL) receives the record count (a D2H of 8 bytes). */
 mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out);
+/* One full step — mm_compute_metrics + mm_sweep(p) — replayed from a CUDA
+ * graph captured on the first call (re-captured when the parameters, the
+ * model, the gates, the stream or profiling change). No host
+ * synchronisation. MMGPU_NO_GRAPH=1 runs it eagerly. */
+mm_status mm_run(mm_ctx* ctx, const mm_sweep_params* p);
+/* With profiling on and a graph replay, accumulates the kernel times of the
+ * LAST replay into mm_kernel_stats (synchronises the context's streams). */
+mm_status mm_collect_timings(mm_ctx* ctx);
 /* Device pointer to the last sweep's records (mm_suggestion[n]), for
  * device-side exchange (NCCL all-gather) without a host round trip. */
 mm_status mm_sweep_device_result(mm_ctx* ctx, const void** dev_records, uint64_t* n);

@@ -56,6 +56,8 @@ _SIGS = {
     "mm_what_if": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(abi.mm_whatif)]),
     "mm_set_gates": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "mm_sweep": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_params), C.POINTER(C.c_uint64)]),
+    "mm_run": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_params)]),
+    "mm_collect_timings": (C.c_int, [C.c_void_p]),
     "mm_sweep_device_result": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
     "mm_sweep_stats_get": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_stats)]),
     "mm_copy_suggestions": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),

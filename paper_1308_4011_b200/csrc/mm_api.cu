@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstddef>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -125,6 +126,13 @@ struct mm_ctx {
     DBuf<mm_whatif> whatif;
     DBuf<char> thr_scratch;
     bool sweep_valid = false;
+    // CUDA graph of one full step (mm_run)
+    bool capturing = false;
+    bool graph_disabled = false;
+    cudaGraphExec_t graph_exec = nullptr;
+    std::vector<uint8_t> graph_key;
+    std::vector<Pending> graph_events;  // event pairs recorded by graph nodes (profiling)
+    uint64_t layout_gen = 0;            // bumped whenever a device buffer the graph uses moves
 
     DevModel dev() const {
         DevModel s;
@@ -159,17 +167,20 @@ mm_status cuda_fail(mm_ctx* ctx, cudaError_t e, const char* where) {
 template <class F>
 mm_status run_on(mm_ctx* ctx, cudaStream_t st, const char* name, F&& launch) {
     Pending pe;
+    // during graph capture the timing events must become external event-record
+    // nodes, readable after each replay
+    const unsigned rec_flags = ctx->capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (ctx->profiling) {
         cudaEventCreate(&pe.a);
         cudaEventCreate(&pe.b);
-        cudaEventRecord(pe.a, st);
+        cudaEventRecordWithFlags(pe.a, st, rec_flags);
     }
     launch();
     const cudaError_t e = cudaGetLastError();
     if (ctx->profiling) {
-        cudaEventRecord(pe.b, st);
+        cudaEventRecordWithFlags(pe.b, st, rec_flags);
         pe.name = name;
-        ctx->pending.push_back(pe);
+        (ctx->capturing ? ctx->graph_events : ctx->pending).push_back(pe);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, name);
     return MM_OK;
@@ -286,6 +297,11 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->side);
     resolve_pending(ctx);
+    if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+    for (Pending& p : ctx->graph_events) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
     free_model(ctx);
     ctx->ctl.release();
     ctx->whatif.release();
@@ -362,6 +378,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     // device buffers are reused across uploads (grown on demand, never shrunk)
     ctx->have_model = ctx->metrics_valid = ctx->sweep_valid = false;
     ctx->gates_set = false;
+    ++ctx->layout_gen;
     if (!s->call_off || !s->acc_off || !s->class_method_off || !s->class_attr_off)
         return fail(ctx, MM_E_ARG, "mm_upload: NULL offsets");
     const uint32_t C = s->n_classes, M = s->n_methods, A = s->n_attributes;
@@ -663,6 +680,7 @@ mm_status mm_set_gates(mm_ctx* ctx, const double* lcom, const uint32_t* cbo) {
     if (!ctx) return MM_E_ARG;
     if (!lcom && !cbo) {
         ctx->gates_set = false;
+        ++ctx->layout_gen;
         return MM_OK;
     }
     if (!lcom || !cbo) return fail(ctx, MM_E_ARG, "mm_set_gates: give both vectors or neither");
@@ -677,6 +695,7 @@ mm_status mm_set_gates(mm_ctx* ctx, const double* lcom, const uint32_t* cbo) {
         MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // caller buffers may be pageable/temporary
     }
     ctx->gates_set = true;
+    ++ctx->layout_gen;
     return MM_OK;
 }
 
@@ -697,12 +716,16 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     const uint64_t per = mode == 0 ? 2ull : (mode == 1 ? 2ull * p->top_k : ~0ull);
     const uint64_t Etot = ctx->Ec + ctx->Ea;
     const uint64_t cap = std::max<uint64_t>(1, mode == 2 ? Etot : std::min(per * npos, Etot));
+    const void* before[4] = {ctx->out.p, ctx->tile_state.p, ctx->res.p, ctx->emit_list.p};
     MM_CUDA(ctx, ctx->out.ensure(cap));
     const uint32_t n_tiles = (uint32_t)((npos + kSweepTile - 1) / kSweepTile);
     const uint32_t n_off = offsets_tiles(npos);
     MM_CUDA(ctx, ctx->tile_state.ensure(n_off ? n_off : 1));
     MM_CUDA(ctx, ctx->res.ensure(npos ? npos : 1));
     MM_CUDA(ctx, ctx->emit_list.ensure(npos ? npos : 1));
+    if (before[0] != ctx->out.p || before[1] != ctx->tile_state.p || before[2] != ctx->res.p ||
+        before[3] != ctx->emit_list.p)
+        ++ctx->layout_gen;
     Ctl* ctl = ctx->ctl.p;
     if (n_off) MM_CUDA(ctx, cudaMemsetAsync(ctx->tile_state.p, 0, 8ull * n_off, ctx->stream));
     // tile_counter, err, pad, stats
@@ -751,6 +774,87 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
         if (mm_status s2 = mm_sweep_stats_get(ctx, &ss)) return s2;
         *n_out = ss.suggestions;
     }
+    return MM_OK;
+}
+
+static void drop_graph(mm_ctx* ctx) {
+    if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+    ctx->graph_exec = nullptr;
+    for (Pending& p : ctx->graph_events) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    ctx->graph_events.clear();
+    ctx->graph_key.clear();
+}
+
+mm_status mm_run(mm_ctx* ctx, const mm_sweep_params* p) {
+    if (!ctx || !p) return MM_E_ARG;
+    if (!ctx->have_model) return fail(ctx, MM_E_STATE, "mm_run: no model uploaded");
+    if (mm_status st = set_device(ctx)) return st;
+    static const bool env_off = [] {
+        const char* e = getenv("MMGPU_NO_GRAPH");
+        return e && e[0] == '1';
+    }();
+    std::vector<uint8_t> key(sizeof *p + 3 * sizeof(uint64_t));
+    std::memcpy(key.data(), p, sizeof *p);
+    const uint64_t extra[3] = {ctx->layout_gen, (uint64_t)ctx->profiling, (uint64_t)(uintptr_t)ctx->stream};
+    std::memcpy(key.data() + sizeof *p, extra, sizeof extra);
+    if (!env_off && !ctx->graph_disabled && ctx->graph_exec && key == ctx->graph_key) {
+        MM_CUDA(ctx, cudaGraphLaunch(ctx->graph_exec, ctx->stream));
+        ctx->metrics_valid = ctx->sweep_valid = true;
+        return MM_OK;
+    }
+    // eager step (this call's result), which also sizes every buffer the
+    // graph will use: allocations cannot be captured
+    if (mm_status st = mm_compute_metrics(ctx)) return st;
+    if (mm_status st = mm_sweep(ctx, p, nullptr)) return st;
+    if (env_off || ctx->graph_disabled) return MM_OK;
+    key.resize(sizeof *p);
+    key.insert(key.end(), reinterpret_cast<const uint8_t*>(&ctx->layout_gen),
+               reinterpret_cast<const uint8_t*>(&ctx->layout_gen) + sizeof(uint64_t));
+    const uint64_t more[2] = {(uint64_t)ctx->profiling, (uint64_t)(uintptr_t)ctx->stream};
+    key.insert(key.end(), reinterpret_cast<const uint8_t*>(more), reinterpret_cast<const uint8_t*>(more) + sizeof more);
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    resolve_pending(ctx);
+    drop_graph(ctx);
+    // capture the same step
+    if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        ctx->graph_disabled = true;
+        cudaGetLastError();
+        return MM_OK;
+    }
+    ctx->capturing = true;
+    const mm_status s1 = mm_compute_metrics(ctx);
+    const mm_status s2 = s1 ? s1 : mm_sweep(ctx, p, nullptr);
+    ctx->capturing = false;
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    if (s2 || e != cudaSuccess || !g || cudaGraphInstantiate(&ctx->graph_exec, g, 0) != cudaSuccess) {
+        ctx->graph_disabled = true;  // keep running eagerly (the result above stands)
+        ctx->graph_exec = nullptr;
+        cudaGetLastError();
+    } else {
+        ctx->graph_key = key;
+    }
+    if (g) cudaGraphDestroy(g);
+    ctx->metrics_valid = ctx->sweep_valid = true;
+    return MM_OK;
+}
+
+mm_status mm_collect_timings(mm_ctx* ctx) {
+    if (!ctx) return MM_E_ARG;
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->side));
+    for (Pending& p : ctx->graph_events) {  // the last replay's kernel times
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            KStat& k = ctx->kstats[p.name];
+            ++k.launches;
+            k.total_ms += ms;
+        }
+    }
+    cudaGetLastError();
     return MM_OK;
 }
 

@@ -245,10 +245,8 @@ class Engine:
                 for f in abi.WHATIF_FIELDS}
 
     # ---- sweep --------------------------------------------------------
-    def sweep(self, criteria=(Criterion.Cohesion, Criterion.Coupling), combine=Combine.Union,
-              thresholds: Optional[Thresholds] = None, all_candidates: bool = False, top_k: int = 1,
-              class_range: Optional[tuple] = None, want_count: bool = True) -> Optional[int]:
-        """Device-resident sweep. thresholds=None uses the device-computed means."""
+    @staticmethod
+    def _params(criteria, combine, thresholds, all_candidates, top_k, class_range) -> abi.mm_sweep_params:
         p = abi.mm_sweep_params(criteria=criteria_mask(criteria), combine=int(combine),
                                 all_candidates=int(bool(all_candidates)), top_k=int(top_k))
         if thresholds is None:
@@ -259,6 +257,13 @@ class Engine:
             p.thr_cbo = float(thresholds.cbo)
         if class_range is not None:
             p.class_begin, p.class_end = int(class_range[0]), int(class_range[1])
+        return p
+
+    def sweep(self, criteria=(Criterion.Cohesion, Criterion.Coupling), combine=Combine.Union,
+              thresholds: Optional[Thresholds] = None, all_candidates: bool = False, top_k: int = 1,
+              class_range: Optional[tuple] = None, want_count: bool = True) -> Optional[int]:
+        """Device-resident sweep. thresholds=None uses the device-computed means."""
+        p = self._params(criteria, combine, thresholds, all_candidates, top_k, class_range)
         n = C.c_uint64()
         self._check(lib().mm_sweep(self._ctx, C.byref(p), C.byref(n) if want_count else None), "mm_sweep")
         return n.value if want_count else None
@@ -271,6 +276,16 @@ class Engine:
         self._gl = np.ascontiguousarray(lcom, dtype=np.float64)
         self._gc = np.ascontiguousarray(cbo, dtype=np.uint32)
         self._check(lib().mm_set_gates(self._ctx, self._gl.ctypes.data, self._gc.ctypes.data), "mm_set_gates")
+
+    def run(self, criteria=(Criterion.Cohesion, Criterion.Coupling), combine=Combine.Union,
+            thresholds: Optional[Thresholds] = None, all_candidates: bool = False, top_k: int = 1,
+            class_range: Optional[tuple] = None) -> None:
+        """One full step (metric pass + sweep), replayed from a CUDA graph; no host sync."""
+        p = self._params(criteria, combine, thresholds, all_candidates, top_k, class_range)
+        self._check(lib().mm_run(self._ctx, C.byref(p)), "mm_run")
+
+    def collect_timings(self) -> None:
+        self._check(lib().mm_collect_timings(self._ctx), "mm_collect_timings")
 
     def sweep_stats(self) -> dict:
         s = abi.mm_sweep_stats()
