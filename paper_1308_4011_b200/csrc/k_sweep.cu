@@ -22,7 +22,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <cstdint>
 
 #include "mm_device.cuh"
@@ -409,197 +408,10 @@ __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, ui
 // Pass 1: score every candidate of every method (ungated, both criteria) and
 // keep the per-method best / top-k / all-passing destinations. Independent
 // of the thresholds, so it overlaps the threshold kernel on another stream.
-//
-// Warp-flattened: a warp takes 32 consecutive methods, stages their packed
-// used lists and origin values in shared memory, then scores the warp's
-// candidates (≈2 per method for C4) 32 at a time, one candidate per lane —
-// every lane issues its destination's 32-byte ClassRec load at once and the
-// per-method loop lengths no longer diverge. Each lane then reduces its own
-// method's candidates in destination order. Methods whose list did not fit
-// the record take the per-thread path (shared-memory list or streaming).
-constexpr int kCandPerWarp = 32 * kRecMaxEnt;
-
-template <int K>
-struct ScoreSmem {
-    uint32_t X[K * kSweepTile];   // SmemEnum columns
-    uint32_t H[K * kSweepTile];
-    double lo_a[kSweepTile];
-    uint32_t org_bits[kSweepTile];  // bit0 coh_ok, bit1 co_a < co_b; bits 8-15 list length
-    uint32_t cd[kSweepTile / 32][kCandPerWarp];
-    double ckey[kSweepTile / 32][kCandPerWarp];
-    uint32_t ckp[kSweepTile / 32][kCandPerWarp];
-    uint8_t ch[kSweepTile / 32][kCandPerWarp];
-    uint8_t cl[kSweepTile / 32][kCandPerWarp];
-    uint8_t ck[kSweepTile / 32][kCandPerWarp];
-    uint8_t cres[kSweepTile / 32][kCandPerWarp];
-};
-
-template <int K>
-size_t score_smem_bytes() { return sizeof(ScoreSmem<K>); }
-
-template <int K>
-__global__ void __launch_bounds__(kSweepTile, 4) k_score(SweepArgs a) {
-    extern __shared__ __align__(16) unsigned char score_smem[];
-    ScoreSmem<K>& sm = *reinterpret_cast<ScoreSmem<K>*>(score_smem);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
-    const bool valid = pos < a.pos_end;
-    uint32_t* myX = sm.X + threadIdx.x;
-    uint32_t* myH = sm.H + threadIdx.x;
-
-    uint32_t o = 0, n = 0, ncand = 0;
-    bool ovf = false;
-    sm.org_bits[threadIdx.x] = 0;
-    if (valid) {
-        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
-        const uint4 r0 = rp[0], r1 = rp[1];
-        o = __ldg(a.pos_owner + pos);
-        const ClassRec ro = load_rec(a.rec, o);
-        ovf = (r0.x & kRecOverflow) != 0;
-        if (!ovf) {
-            const uint32_t ent[kRecMaxEnt] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-            n = rec_n(r0.x);
-#pragma unroll
-            for (int k = 0; k < kRecMaxEnt; ++k)
-                if (k < (int)n) {
-                    myX[k * kSweepTile] = ent[k] >> 8;
-                    myH[k * kSweepTile] = ent[k] & 0xffu;
-                    ncand += (ent[k] >> 8) != o;
-                }
-            const SmemEnum en{myX, myH, (int)n};
-            const uint32_t removed = (r0.x & kRecRemovedValid) ? rec_removed(r0.x)
-                                                                : removed_count(ro, a.ux, a.un, en, o);
-            const Origin org = make_origin(ro, rec_hown(r0.x), removed);
-            sm.lo_a[threadIdx.x] = org.lo_a;
-            sm.org_bits[threadIdx.x] = (org.coh_ok ? 1u : 0u) | (org.co_a < org.co_b ? 2u : 0u) | (n << 8);
-        }
-    }
-    // flatten the warp's candidates: (destination, accesses owned by it, owner lane, list index)
-    uint32_t excl = ncand;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, excl, d);
-        if (lane >= d) excl += y;
-    }
-    const uint32_t T = __shfl_sync(0xffffffffu, excl, 31);
-    excl -= ncand;
-    {
-        uint32_t w = excl;
-        for (uint32_t k = 0; k < n; ++k) {
-            const uint32_t X = myX[k * kSweepTile];
-            if (X == o) continue;
-            sm.cd[warp][w] = X;
-            sm.ch[warp][w] = (uint8_t)myH[k * kSweepTile];
-            sm.cl[warp][w] = (uint8_t)lane;
-            sm.ck[warp][w] = (uint8_t)k;
-            ++w;
-        }
-    }
-    __syncwarp();
-    for (uint32_t r = 0; r < T; r += 32) {
-        const uint32_t idx = r + lane;
-        if (idx < T) {
-            const uint32_t d = sm.cd[warp][idx];
-            const int ot = warp * 32 + sm.cl[warp][idx];
-            const uint32_t bits = sm.org_bits[ot];
-            uint8_t res = 0;
-            double key = 0.0;
-            uint32_t kp = 0;
-            if (bits & 3u) {  // otherwise neither criterion can pass: scored without a load
-                const ClassRecFull rf = load_rec_full(a.rec, d);  // counts + Bloom words, one round trip
-                const ClassRec& rd = rf.r;
-                double ld_a;
-                if ((bits & 1u) && coh_dest(rd, sm.ch[warp][idx], ld_a)) {
-                    res |= 1u;
-                    key = __dadd_rn(sm.lo_a[ot], ld_a);  // lcom_key, suggest.hpp:194-196
-                }
-                if (bits & 2u) {  // passes iff every other used class is already in U[d]
-                    const uint32_t on = (bits >> 8) & 0xffu;
-                    bool ok = true;
-                    for (uint32_t k = 0; k < on && ok; ++k) {
-                        const uint32_t X = sm.X[ot + k * kSweepTile];
-                        const bool in = rd.dense != kNone
-                                            ? ((__ldg(a.dense + rd.dense + (X >> 5)) >> (X & 31)) & 1u) != 0
-                                            : (rf.maybe(X) && urow_find(a.ux, rd.ubase, rd.cbo, X) >= 0);
-                        if (X != d && !in) ok = false;
-                    }
-                    if (ok) res |= 2u;
-                }
-                kp = rd.cbo;  // cbo_dest_after when coupling passes
-            }
-            sm.cres[warp][idx] = res;
-            sm.ckey[warp][idx] = key;
-            sm.ckp[warp][idx] = kp;
-        }
-    }
-    __syncwarp();
-
-    // each lane reduces its own method's candidates, destinations ascending
-    uint32_t cands = 0;
-    if (valid && !ovf) {
-        cands = ncand;
-        uint32_t bd_coh = kNone, bd_coup = kNone, best_coup = 0;
-        double best_coh = 0.0;
-        uint32_t m_coh = 0, m_coup = 0;
-        for (uint32_t j = excl; j < excl + ncand; ++j) {
-            const uint32_t res = sm.cres[warp][j];
-            const uint32_t d = sm.cd[warp][j];
-            // argmin over (key, d) with strict < : lowest d wins ties (suggest.hpp:180-184)
-            if ((res & 1u) && (bd_coh == kNone || sm.ckey[warp][j] < best_coh)) { bd_coh = d; best_coh = sm.ckey[warp][j]; }
-            if ((res & 2u) && (bd_coup == kNone || sm.ckp[warp][j] < best_coup)) { bd_coup = d; best_coup = sm.ckp[warp][j]; }
-            if (res & 1u) m_coh |= 1u << sm.ck[warp][j];
-            if (res & 2u) m_coup |= 1u << sm.ck[warp][j];
-        }
-        uint4 out;
-        if (a.mode == 0) {
-            out = make_uint4(bd_coh, bd_coup, ncand, 0);
-        } else {
-            if (a.mode == 1) {  // keep the top-k of each criterion by (key, d)
-                for (int c = 0; c < 2; ++c) {
-                    const uint32_t all = c == 0 ? m_coh : m_coup;
-                    uint32_t keep = 0;
-                    for (uint32_t t = 0; t < a.topk; ++t) {
-                        int best = -1;
-                        double bk = 0.0;
-                        for (uint32_t j = excl; j < excl + ncand; ++j) {
-                            const uint32_t bit = 1u << sm.ck[warp][j];
-                            if (!(all & bit) || (keep & bit)) continue;
-                            const double key = c == 0 ? sm.ckey[warp][j] : (double)sm.ckp[warp][j];
-                            if (best < 0 || key < bk) { best = (int)sm.ck[warp][j]; bk = key; }
-                        }
-                        if (best < 0) break;
-                        keep |= 1u << best;
-                    }
-                    (c == 0 ? m_coh : m_coup) = keep;
-                }
-            }
-            out = make_uint4(m_coh, m_coup, ncand, 0);
-        }
-        a.res[pos] = out;
-    } else if (valid) {
-        // per-thread path for lists the record could not hold
-        const uint32_t p = __ldg(a.s.cls_methods + pos);
-        SmemEnum ren{myX, myH, 0};
-        StreamEnum sen;
-        Origin org;
-        MethodResult r;
-        if (load_method<K>(a, (uint32_t)pos, p, o, ren, sen, org)) r = evaluate(a, ren, o, org, true, true);
-        else r = evaluate(a, sen, o, org, true, true);
-        cands = r.cands;
-        uint4 out;
-        if (a.mode == 0) out = make_uint4(r.bd_coh, r.bd_coup, r.cands, 0);
-        else {
-            if ((r.m_coh | r.m_coup) >> 32) atomicOr(a.err, 2u);
-            out = make_uint4((uint32_t)r.m_coh, (uint32_t)r.m_coup, r.cands, 0);
-        }
-        a.res[pos] = out;
-    }
-    const uint32_t wc = __reduce_add_sync(0xffffffffu, cands);
-    if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
-}
-
-// Per-thread variant of pass 1 (one method per thread, list in shared
-// memory): small state, high occupancy — the default.
+// One method per thread, its used list in shared memory: small per-thread
+// state and high occupancy measured faster on C4 than a warp-flattened
+// variant (one candidate per lane), the round-1 profiles show why — every
+// kernel here is latency-bound, so resident warps matter most.
 template <int K>
 __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(SweepArgs a) {
     __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
@@ -817,25 +629,8 @@ __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const ui
 
 void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     if (!n_tiles) return;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_score<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes<8>());
-        cudaFuncSetAttribute(k_score<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)score_smem_bytes<16>());
-        attr = true;
-    }
-    // default: the per-thread kernel (higher occupancy measured faster on C4,
-    // profiles/); MMGPU_SCORE=warp selects the warp-flattened variant
-    static const bool per_thread = [] {
-        const char* e = getenv("MMGPU_SCORE");
-        return !(e && e[0] == 'w');
-    }();
-    if (per_thread) {
-        if (a.maxdeg_fast <= 8) k_score_thread<8><<<n_tiles, kSweepTile, 0, st>>>(a);
-        else k_score_thread<16><<<n_tiles, kSweepTile, 0, st>>>(a);
-        return;
-    }
-    if (a.maxdeg_fast <= 8) k_score<8><<<n_tiles, kSweepTile, score_smem_bytes<8>(), st>>>(a);
-    else k_score<16><<<n_tiles, kSweepTile, score_smem_bytes<16>(), st>>>(a);
+    if (a.maxdeg_fast <= 8) k_score_thread<8><<<n_tiles, kSweepTile, 0, st>>>(a);
+    else k_score_thread<16><<<n_tiles, kSweepTile, 0, st>>>(a);
 }
 
 uint32_t offsets_tiles(uint64_t npos) { return (uint32_t)((npos + kOffTile - 1) / kOffTile); }

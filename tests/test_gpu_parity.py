@@ -268,3 +268,26 @@ def test_gpu_threshold_fast_path_on_systems(gpu_engine):
         t = gpu_engine.compute_thresholds()
         assert t.lcom == _seq_mean(lcom) and t.cbo == _seq_mean(cbo.astype(np.float64))
         assert gpu_engine.sequential_mean(lcom) == (t.lcom, True)
+
+
+def test_gpu_graph_step_equals_eager(gpu_engine):
+    # mm_run replays a captured CUDA graph of metric pass + sweep: same bits as the eager calls
+    s = System.generate(seed=21, n_classes=2000, n_methods=30000, n_attributes=40000, k_max_calls=5,
+                        k_max_accesses=5, intra_class_bias=0.45)
+    gpu_engine.upload(s)
+    t = gpu_engine.compute_thresholds()
+    eager = gpu_engine.suggest_all(t)
+    for _ in range(3):
+        gpu_engine.run(thresholds=None)  # capture, then replays
+        assert records_equal(gpu_engine.suggestions(), eager)
+    lcom, ck, cbo = gpu_engine.class_metrics_all()
+    want = oracle.class_metrics(s)
+    assert_metrics_equal((lcom, ck, cbo), want, "graph")
+    # a new model invalidates the graph
+    s2 = System.generate(seed=22, n_classes=2000, n_methods=30000, n_attributes=40000)
+    gpu_engine.upload(s2)
+    gpu_engine.run(thresholds=None)
+    l2, k2, c2 = oracle.class_metrics(s2)
+    t2 = oracle.thresholds(l2, c2)
+    o2 = oracle.suggest(s2, l2, c2, COH | COUP, 0, False, 1, t2.lcom, t2.cbo)
+    assert records_equal(gpu_engine.suggestions(), o2)
