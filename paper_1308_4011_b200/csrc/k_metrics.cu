@@ -644,12 +644,23 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     uint64_t q = 0;
     if (split) {
     } else if (pl.ck_masks) {
-        for (uint32_t i = threadIdx.x; i < M; i += blockDim.x)
-            for (uint32_t j = i + 1; j < M; ++j) {
-                uint64_t any = 0;
-                for (uint32_t w = 0; w < WA; ++w) any |= masks[(uint64_t)i * WA + w] & masks[(uint64_t)j * WA + w];
-                q += any != 0;
+        // warp per row i, lanes over j > i: conflict-free consecutive mask
+        // loads, no per-thread trip-count imbalance
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        if (WA == 1) {
+            for (uint32_t i = warp; i < M; i += nw) {
+                const uint64_t mi = masks[i];
+                if (!mi) continue;  // no own attribute: shares with nobody
+                for (uint32_t j = i + 1 + lane; j < M; j += 32) q += (mi & masks[j]) != 0;
             }
+        } else {
+            for (uint32_t i = warp; i < M; i += nw)
+                for (uint32_t j = i + 1 + lane; j < M; j += 32) {
+                    uint64_t any = 0;
+                    for (uint32_t w = 0; w < WA; ++w) any |= masks[(uint64_t)i * WA + w] & masks[(uint64_t)j * WA + w];
+                    q += any != 0;
+                }
+        }
     } else {
         // rows[a] = members using a; member i's sharers = OR of its rows, above i
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

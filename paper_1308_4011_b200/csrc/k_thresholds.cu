@@ -468,7 +468,7 @@ __global__ void k_thresholds_serial(const double* __restrict__ lcom, const uint3
 
 }  // namespace
 
-constexpr uint32_t kSerialMax = 12288;  // below this one warp's serial chain beats three grid syncs
+constexpr uint32_t kSerialMax = 2048;  // below this one warp's serial chain beats three grid syncs (measured)
 
 size_t thresholds_scratch_bytes(uint32_t n) {
     const size_t tiles = (n + kTile - 1) / kTile;
