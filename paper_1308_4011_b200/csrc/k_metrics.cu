@@ -602,23 +602,25 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         xcarry += tot;
     }
 
-    // dense rows also get an exact bitmap over all classes (O(1) membership
+    // dense rows also get exact bitmaps over all classes: membership (O(1)
     // in the sweep where a Bloom signature of a long row says "maybe" to all)
+    // then the U[c][X] == 1 singletons (the origin's removed count)
     const uint32_t dwords = (s.C + 31) / 32;
     if (threadIdx.x == 0) {
         s_dense = kNone;
         if (nx > kDenseRowMin && dense) {
-            const uint32_t off = atomicAdd(dense_cursor, dwords);
-            if ((uint64_t)off + dwords <= dense_cap) s_dense = off;
+            const uint32_t off = atomicAdd(dense_cursor, 2 * dwords);
+            if ((uint64_t)off + 2 * dwords <= dense_cap) s_dense = off;
         }
     }
     __syncthreads();
     if (s_dense != kNone) {
-        for (uint32_t w = threadIdx.x; w < dwords; w += blockDim.x) dense[s_dense + w] = 0;
+        for (uint32_t w = threadIdx.x; w < 2 * dwords; w += blockDim.x) dense[s_dense + w] = 0;
         __syncthreads();
         for (uint32_t k = threadIdx.x; k < nx; k += blockDim.x) {
             const uint32_t X = ux[ubase + k];
             atomicOr(dense + s_dense + (X >> 5), 1u << (X & 31));
+            if (un[ubase + k] == 1u) atomicOr(dense + s_dense + dwords + (X >> 5), 1u << (X & 31));
         }
     }
 

@@ -183,11 +183,20 @@ __device__ __forceinline__ Dest eval_dest(const ClassRec* __restrict__ rec, cons
 }
 
 // #{X ∈ used(u) \ {o} : U[o][X] == 1} from the rows (methods whose record
-// could not carry it)
+// could not carry it); a dense origin row answers from its singleton bitmap
 template <class E>
 __device__ __forceinline__ uint32_t removed_count(const ClassRec& ro, const uint32_t* __restrict__ ux,
-                                                  const uint32_t* __restrict__ un, const E& en, uint32_t o) {
+                                                  const uint32_t* __restrict__ un,
+                                                  const uint32_t* __restrict__ dense, uint32_t C, const E& en,
+                                                  uint32_t o) {
     uint32_t removed = 0;
+    if (ro.dense != kNone) {
+        const uint32_t* single = dense + ro.dense + (C + 31) / 32;
+        en.each([&](int, uint32_t X, uint32_t) {
+            if (X != o) removed += (__ldg(single + (X >> 5)) >> (X & 31)) & 1u;
+        });
+        return removed;
+    }
     en.each([&](int, uint32_t X, uint32_t) {
         if (X != o) {
             const int pos = urow_find(ux, ro.ubase, ro.cbo, X);
@@ -392,16 +401,16 @@ __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, ui
             if (k < (int)n) { ren.X[k * kSweepTile] = ent[k] >> 8; ren.H[k * kSweepTile] = ent[k] & 0xffu; }
         ren.n = (int)n;
         const uint32_t removed = (r0.x & kRecRemovedValid) ? rec_removed(r0.x)
-                                                            : removed_count(ro, a.ux, a.un, ren, o);
+                                                            : removed_count(ro, a.ux, a.un, a.dense, a.s.C, ren, o);
         org = make_origin(ro, rec_hown(r0.x), removed);
         return true;
     }
     if (ren.build(a.s, p, K)) {  // ≤ K distinct classes (any degree): shared-memory list
-        org = make_origin(ro, ren.hits(o), removed_count(ro, a.ux, a.un, ren, o));
+        org = make_origin(ro, ren.hits(o), removed_count(ro, a.ux, a.un, a.dense, a.s.C, ren, o));
         return true;
     }
     sen.S.init(a.s, p);
-    org = make_origin(ro, sen.hits(o), removed_count(ro, a.ux, a.un, sen, o));
+    org = make_origin(ro, sen.hits(o), removed_count(ro, a.ux, a.un, a.dense, a.s.C, sen, o));
     return false;
 }
 
@@ -608,7 +617,7 @@ __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const ui
     StreamEnum en;
     en.S.init(s, u);
     const ClassRec ro = load_rec(rec, o);
-    const Origin org = make_origin(ro, en.hits(o), removed_count(ro, ux, un, en, o));
+    const Origin org = make_origin(ro, en.hits(o), removed_count(ro, ux, un, dense, s.C, en, o));
     const Dest dv = eval_dest(rec, ux, dense, en, d, en.hits(d));
     mm_whatif w;
     w.lcom_origin_before = org.lo_b;

@@ -527,7 +527,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         MM_CUDA(ctx, set_class_large_smem(max_smem));
         // exact bitmaps for dense U rows: ≤ one per CTA-path class with > kDenseRowMin
         // foreign keys, capped at 256 MB (classes past the cap keep Bloom + scan)
-        const uint64_t words = (uint64_t)((C + 31) / 32) * n_dense;
+        const uint64_t words = 2ull * ((C + 31) / 32) * n_dense;  // membership + singletons
         ctx->dense_cap = (uint32_t)std::min<uint64_t>(words, 64ull << 20);
         MM_CUDA(ctx, ctx->dense.ensure(ctx->dense_cap ? ctx->dense_cap : 1));
     } else {
