@@ -78,6 +78,23 @@ __global__ void k_plan_methods(DevModel s, uint32_t* __restrict__ foreign, uint3
     atomicMax(cmaxdeg + c, (ce - cb) + (ae - ab));
 }
 
+// attr_info[t] = (owner(t), position of t in its owner's attribute list): one
+// 8-byte gather gives the method pass both the owner and the LCOM-CK mask bit
+// (the list is the class's attribute order, so the bit is the same one the
+// reference's sorted-list intersection test would find). Bounds-checked.
+__global__ void k_attr_info(DevModel s, uint2* __restrict__ info) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;  // position in cls_attrs
+    if (i >= s.A) return;
+    uint32_t lo = 0, hi = s.C;  // class of list position i
+    while (lo + 1 < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s.cls_aoff[mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    const uint32_t t = s.cls_attrs[i];
+    if (t < s.A) info[t] = make_uint2(s.attribute_owner[t], i - min(s.cls_aoff[lo], i));
+}
+
 // classify into the warp path (small) or the CTA path (large)
 __global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg, uint8_t* __restrict__ kind,
                                uint32_t* __restrict__ large_list, uint32_t* __restrict__ n_large,
@@ -140,10 +157,10 @@ k_method(DevModel s, const uint8_t* __restrict__ kind, MethRec* __restrict__ rec
     UsedList<kRecMaxEnt + 1> L;
     L.clear();
     uint32_t hown = 0;
-    // masks only feed the warp path's LCOM-CK (CTA-path classes rebuild their own)
-    const bool small_attrs = oae - oab <= 64 && __ldg(kind + own) == 0;
+    // masks feed LCOM-CK of every class with ≤ 64 attributes (both class paths)
+    const bool small_attrs = oae - oab <= 64;
     auto chunk = [&](uint32_t e0) {
-        uint32_t tg[K], ow[K];
+        uint32_t tg[K], ow[K], rk[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const uint32_t e = e0 + k;
@@ -154,7 +171,15 @@ k_method(DevModel s, const uint8_t* __restrict__ kind, MethRec* __restrict__ rec
         for (int k = 0; k < K; ++k) {
             const uint32_t e = e0 + k;
             const bool isc = e < nc, isa = !isc && e < deg;
-            ow[k] = isc ? __ldg(s.method_owner + tg[k]) : (isa ? __ldg(s.attribute_owner + tg[k]) : kNone);
+            if (isc) {
+                ow[k] = __ldg(s.method_owner + tg[k]);
+            } else if (isa) {
+                const uint2 ai = __ldg(s.attr_info + tg[k]);
+                ow[k] = ai.x;
+                rk[k] = ai.y;
+            } else {
+                ow[k] = kNone;
+            }
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -162,7 +187,7 @@ k_method(DevModel s, const uint8_t* __restrict__ kind, MethRec* __restrict__ rec
             const bool isa = e >= nc && e < deg;
             if (e < deg) L.insert(ow[k], isa ? 1u : 0u);
             if (isa && ow[k] == own) {
-                if (small_attrs) mask |= 1ull << attr_pos(s, oab, oae, tg[k]);
+                if (small_attrs) mask |= 1ull << rk[k];
                 ++hown;
             }
         }
@@ -506,7 +531,7 @@ __device__ __forceinline__ void member_used(const DevModel& s, const MethRec* re
 // word ANDs) or per-attribute member bitmaps (sparse giants).
 __global__ void __launch_bounds__(1024)
 k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* __restrict__ plan,
-              MethRec* __restrict__ recs, ClassRec* __restrict__ rec,
+              MethRec* __restrict__ recs, const uint64_t* __restrict__ own_mask, ClassRec* __restrict__ rec,
               double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
               uint32_t* __restrict__ ux, uint32_t* __restrict__ un, uint32_t* __restrict__ ucursor,
               uint32_t* __restrict__ gkeys, uint32_t* __restrict__ grows, uint32_t* __restrict__ dense,
@@ -532,6 +557,11 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         attrs = sa;
         cur += ((4ull * A + 15) & ~15ull);
     }
+    // foreign classes: a per-class histogram cnt[X] = U[c][X] over all C
+    // classes when it fits (few classes, many keys: no sort, no searches),
+    // else the keys sorted in place
+    uint32_t* cnt = pl.hist ? reinterpret_cast<uint32_t*>(cur) : nullptr;
+    if (pl.hist) cur += (4ull * s.C + 15) & ~15ull;
     uint32_t* keys = pl.keys_in_smem ? reinterpret_cast<uint32_t*>(cur) : gkeys + pl.keys_off;
     if (pl.keys_in_smem) cur += (4ull * pl.keys_cap + 15) & ~15ull;  // keep the u64 masks aligned
     uint64_t* masks = reinterpret_cast<uint64_t*>(cur);  // masks mode (always in smem)
@@ -543,6 +573,8 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     // (global-scratch bitmaps are cleared by one cudaMemsetAsync before the launch)
     if (pl.ck_masks || pl.rows_in_smem)
         for (uint64_t i = threadIdx.x; i < ck_words; i += blockDim.x) ckz[i] = 0;
+    if (pl.hist)
+        for (uint32_t i = threadIdx.x; i < s.C; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
 
     // phase 1: members' foreign used classes -> keys; H; own-attribute sets
@@ -550,9 +582,20 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) {
         const uint32_t pos = mb + i;
         const uint32_t p = s.cls_methods[pos];
-        member_used(s, recs, pos, p, [&](uint32_t X, uint32_t h) {
-            if (X != c) keys[atomicAdd(&s_nk, 1u)] = X;
-        });
+        if (pl.hist)
+            member_used(s, recs, pos, p, [&](uint32_t X, uint32_t) {
+                if (X != c) atomicAdd(cnt + X, 1u);
+            });
+        else
+            member_used(s, recs, pos, p, [&](uint32_t X, uint32_t) {
+                if (X != c) keys[atomicAdd(&s_nk, 1u)] = X;
+            });
+        if (A <= 64 && pl.ck_masks && !(recs[pos].hdr & kRecOverflow)) {
+            // the method pass already built this member's mask and own-hit count
+            masks[i] = own_mask[pos];
+            hown += rec_hown(recs[pos].hdr);
+            continue;
+        }
         const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
         for (uint32_t e = ab; e < ae; ++e) {
             const uint32_t t = __ldg(s.acc_tgt + e);
@@ -564,63 +607,105 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         }
     }
     const uint64_t H = block_sum_u64(hown, red64);  // includes a __syncthreads
-    const uint32_t nk = s_nk;
-    uint32_t N = 1;
-    while (N < nk) N <<= 1;
-    for (uint32_t i = nk + threadIdx.x; i < N; i += blockDim.x) keys[i] = kNone;
-    __syncthreads();
-    if (N > 1) block_bitonic_u32(keys, N);
-
-    // phase 2: runs of equal X = one U row entry with count = run length
-    uint32_t nx = 0;
-    for (uint32_t b = 0; b < nk; b += blockDim.x) {
-        const uint32_t k = b + threadIdx.x;
-        const bool xh = k < nk && (k == 0 || keys[k] != keys[k - 1]);
-        uint32_t tot;
-        block_excl_scan(xh ? 1u : 0u, red32, &tot);
-        nx += tot;
-    }
-    // large classes reserve their rows past the small-class region (few, so the
-    // atomic is uncontended): the paper's atomicAdd slot reservation
-    if (threadIdx.x == 0) s_ubase = kSmallRowCap * s.M + (nx ? atomicAdd(ucursor, nx) : 0u);
-    __syncthreads();
-    const uint32_t ubase = s_ubase;
-    uint32_t xcarry = 0;
-    for (uint32_t b = 0; b < nk; b += blockDim.x) {
-        const uint32_t k = b + threadIdx.x;
-        const bool xh = k < nk && (k == 0 || keys[k] != keys[k - 1]);
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan(xh ? 1u : 0u, red32, &tot);
-        if (xh) {
-            const uint32_t X = keys[k];
-            ux[ubase + xcarry + ex] = X;
-            un[ubase + xcarry + ex] = lower_bound_u32(keys, nk, X + 1) - k;  // run length
-            const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
-            atomicOr(s_sig + (b1 >> 5), 1u << (b1 & 31));
-            atomicOr(s_sig + (b2 >> 5), 1u << (b2 & 31));
-        }
-        xcarry += tot;
-    }
-
-    // dense rows also get exact bitmaps over all classes: membership (O(1)
-    // in the sweep where a Bloom signature of a long row says "maybe" to all)
-    // then the U[c][X] == 1 singletons (the origin's removed count)
     const uint32_t dwords = (s.C + 31) / 32;
-    if (threadIdx.x == 0) {
-        s_dense = kNone;
-        if (nx > kDenseRowMin && dense) {
-            const uint32_t off = atomicAdd(dense_cursor, 2 * dwords);
-            if ((uint64_t)off + 2 * dwords <= dense_cap) s_dense = off;
+    uint32_t nx = 0, ubase = 0, nk = 0;
+    if (pl.hist) {
+        // phase 2 (histogram): the nonzero counts, in class order, are the U row
+        uint32_t mine = 0;
+        for (uint32_t k = threadIdx.x; k < s.C; k += blockDim.x) mine += cnt[k] != 0u;
+        nx = (uint32_t)block_sum_u64(mine, red64);
+        if (threadIdx.x == 0) {
+            s_ubase = kSmallRowCap * s.M + (nx ? atomicAdd(ucursor, nx) : 0u);
+            s_dense = kNone;
+            if (nx > kDenseRowMin && dense) {
+                const uint32_t off = atomicAdd(dense_cursor, 2 * dwords);
+                if ((uint64_t)off + 2 * dwords <= dense_cap) s_dense = off;
+            }
         }
-    }
-    __syncthreads();
-    if (s_dense != kNone) {
-        for (uint32_t w = threadIdx.x; w < 2 * dwords; w += blockDim.x) dense[s_dense + w] = 0;
         __syncthreads();
-        for (uint32_t k = threadIdx.x; k < nx; k += blockDim.x) {
-            const uint32_t X = ux[ubase + k];
-            atomicOr(dense + s_dense + (X >> 5), 1u << (X & 31));
-            if (un[ubase + k] == 1u) atomicOr(dense + s_dense + dwords + (X >> 5), 1u << (X & 31));
+        ubase = s_ubase;
+        const uint32_t dn = s_dense;
+        const int lane = threadIdx.x & 31;
+        uint32_t xcarry = 0;
+        for (uint32_t b = 0; b < s.C; b += blockDim.x) {
+            const uint32_t k = b + threadIdx.x;
+            const uint32_t v = k < s.C ? cnt[k] : 0u;
+            uint32_t tot;
+            const uint32_t ex = block_excl_scan(v != 0u ? 1u : 0u, red32, &tot);
+            if (v) {
+                ux[ubase + xcarry + ex] = k;
+                un[ubase + xcarry + ex] = v;
+                const uint32_t b1 = bloom_h1(k), b2 = bloom_h2(k);
+                atomicOr(s_sig + (b1 >> 5), 1u << (b1 & 31));
+                atomicOr(s_sig + (b2 >> 5), 1u << (b2 & 31));
+            }
+            if (dn != kNone) {  // warps cover whole 32-class words: membership, singletons
+                const uint32_t m = __ballot_sync(0xffffffffu, v != 0u);
+                const uint32_t one = __ballot_sync(0xffffffffu, v == 1u);
+                if (lane == 0 && (k >> 5) < dwords) {
+                    dense[dn + (k >> 5)] = m;
+                    dense[dn + dwords + (k >> 5)] = one;
+                }
+            }
+            xcarry += tot;
+        }
+    } else {
+        nk = s_nk;
+        uint32_t N = 1;
+        while (N < nk) N <<= 1;
+        for (uint32_t i = nk + threadIdx.x; i < N; i += blockDim.x) keys[i] = kNone;
+        __syncthreads();
+        if (N > 1) block_bitonic_u32(keys, N);
+
+        // phase 2: runs of equal X = one U row entry with count = run length
+        for (uint32_t b = 0; b < nk; b += blockDim.x) {
+            const uint32_t k = b + threadIdx.x;
+            const bool xh = k < nk && (k == 0 || keys[k] != keys[k - 1]);
+            uint32_t tot;
+            block_excl_scan(xh ? 1u : 0u, red32, &tot);
+            nx += tot;
+        }
+        // large classes reserve their rows past the small-class region (few, so the
+        // atomic is uncontended): the paper's atomicAdd slot reservation
+        if (threadIdx.x == 0) s_ubase = kSmallRowCap * s.M + (nx ? atomicAdd(ucursor, nx) : 0u);
+        __syncthreads();
+        ubase = s_ubase;
+        uint32_t xcarry = 0;
+        for (uint32_t b = 0; b < nk; b += blockDim.x) {
+            const uint32_t k = b + threadIdx.x;
+            const bool xh = k < nk && (k == 0 || keys[k] != keys[k - 1]);
+            uint32_t tot;
+            const uint32_t ex = block_excl_scan(xh ? 1u : 0u, red32, &tot);
+            if (xh) {
+                const uint32_t X = keys[k];
+                ux[ubase + xcarry + ex] = X;
+                un[ubase + xcarry + ex] = lower_bound_u32(keys, nk, X + 1) - k;  // run length
+                const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
+                atomicOr(s_sig + (b1 >> 5), 1u << (b1 & 31));
+                atomicOr(s_sig + (b2 >> 5), 1u << (b2 & 31));
+            }
+            xcarry += tot;
+        }
+
+        // dense rows also get exact bitmaps over all classes: membership (O(1)
+        // in the sweep where a Bloom signature of a long row says "maybe" to all)
+        // then the U[c][X] == 1 singletons (the origin's removed count)
+        if (threadIdx.x == 0) {
+            s_dense = kNone;
+            if (nx > kDenseRowMin && dense) {
+                const uint32_t off = atomicAdd(dense_cursor, 2 * dwords);
+                if ((uint64_t)off + 2 * dwords <= dense_cap) s_dense = off;
+            }
+        }
+        __syncthreads();
+        if (s_dense != kNone) {
+            for (uint32_t w = threadIdx.x; w < 2 * dwords; w += blockDim.x) dense[s_dense + w] = 0;
+            __syncthreads();
+            for (uint32_t k = threadIdx.x; k < nx; k += blockDim.x) {
+                const uint32_t X = ux[ubase + k];
+                atomicOr(dense + s_dense + (X >> 5), 1u << (X & 31));
+                if (un[ubase + k] == 1u) atomicOr(dense + s_dense + dwords + (X >> 5), 1u << (X & 31));
+            }
         }
     }
 
@@ -633,8 +718,12 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         for (uint32_t k = 0; k < rec_n(hdr); ++k) {
             const uint32_t X = r->ent[k] >> 8;
             if (X == c) continue;
-            const uint32_t lo = lower_bound_u32(keys, nk, X);
-            removed += (lower_bound_u32(keys, nk, X + 1) - lo) == 1u;
+            if (pl.hist) {
+                removed += cnt[X] == 1u;
+            } else {
+                const uint32_t lo = lower_bound_u32(keys, nk, X);
+                removed += (lower_bound_u32(keys, nk, X + 1) - lo) == 1u;
+            }
         }
         r->hdr = hdr | (removed << kRecRemovedShift) | kRecRemovedValid;
     }
@@ -792,6 +881,7 @@ void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list,
     if (!s.C) return;
     cudaMemsetAsync(foreign, 0, 4ull * s.C, st);
     cudaMemsetAsync(cmaxdeg, 0, 4ull * s.C, st);
+    if (s.A) k_attr_info<<<(s.A + 255) / 256, 256, 0, st>>>(s, const_cast<uint2*>(s.attr_info));
     if (s.M) k_plan_methods<<<(s.M + 255) / 256, 256, 0, st>>>(s, foreign, cmaxdeg);
     k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, cmaxdeg, kind, large_list, n_large, max_deg);
 }
@@ -809,12 +899,12 @@ void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, c
         s, kind, recs, own_mask, rec, lcom, ck, cbo, ux, un, ucursor);
 }
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
-                        uint32_t smem_bytes, MethRec* recs, ClassRec* rec, double* lcom,
+                        uint32_t smem_bytes, MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
                         uint32_t* gkeys, uint32_t* grows, uint32_t* dense, uint32_t dense_cap,
                         uint32_t* dense_cursor, uint32_t threads, cudaStream_t st) {
     if (!n_large) return;
-    k_class_large<<<n_large, threads, smem_bytes, st>>>(s, large_list, plan, recs, rec, lcom, ck, cbo, ux,
+    k_class_large<<<n_large, threads, smem_bytes, st>>>(s, large_list, plan, recs, own_mask, rec, lcom, ck, cbo, ux,
                                                               un, ucursor, gkeys, grows, dense, dense_cap,
                                                               dense_cursor);
 }

@@ -23,6 +23,9 @@ using namespace mmg;
 
 namespace {
 
+// CTA-path classes count foreign classes in an smem histogram when 4·C fits this
+constexpr uint64_t kHistMaxBytes = 64 * 1024;
+
 struct Ctl {  // small device-resident control block
     uint32_t bad;
     uint32_t n_large;
@@ -97,6 +100,7 @@ struct mm_ctx {
     std::vector<LargeGroup> large_groups;  // CTA-path launches, grouped by shared-memory need
     DBuf<uint32_t> dense;                  // exact U-row bitmaps of dense classes
     uint32_t dense_cap = 0;
+    uint64_t hist_max_bytes = kHistMaxBytes;  // env MMGPU_HIST_MAX_BYTES (tuning / tests)
     DBuf<uint2> ck_items;                  // (large index, first member) chunks of split LCOM-CK classes
     DBuf<uint32_t> split_list;             // the split classes
     uint32_t n_ck_items = 0, n_split = 0;
@@ -110,6 +114,7 @@ struct mm_ctx {
     DBuf<uint32_t> cbo, ux, un;
     DBuf<MethRec> recs;
     DBuf<uint64_t> own_mask;
+    DBuf<uint2> attr_info;
     DBuf<uint32_t> pos_owner;
     DBuf<uint4> res;
     DBuf<uint32_t> emit_list;
@@ -142,6 +147,7 @@ struct mm_ctx {
         s.cls_aoff = cls_aoff.p; s.cls_attrs = cls_attrs.p;
         s.call_off = call_off.p; s.call_tgt = call_tgt.p;
         s.acc_off = acc_off.p; s.acc_tgt = acc_tgt.p;
+        s.attr_info = attr_info.p;
         return s;
     }
 };
@@ -220,6 +226,7 @@ void free_model(mm_ctx* c) {
         b->release();
     c->recs.release();
     c->own_mask.release();
+    c->attr_info.release();
     c->pos_owner.release();
     c->kind.release();
     c->plans.release();
@@ -287,6 +294,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
         return MM_E_CUDA;
     }
     ctx->stream = ctx->own;
+    if (const char* v = std::getenv("MMGPU_HIST_MAX_BYTES")) ctx->hist_max_bytes = std::strtoull(v, nullptr, 10);
     *out = ctx;
     return MM_OK;
 }
@@ -421,6 +429,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, ctx->large_list.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->foreign.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->cmaxdeg.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->attr_info.ensure(A ? A : 1));
     const DevModel dm = ctx->dev();
     st = run(ctx, "plan", [&] {
         launch_plan_classes(dm, ctx->kind.p, ctx->large_list.p, &ctl->n_large, &ctl->max_deg, ctx->foreign.p,
@@ -456,7 +465,16 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             // attribute list, the LCOM-CK structure
             uint64_t used = 0;
             const uint64_t kbytes = (4ull * pl.keys_cap + 15) & ~15ull;
-            if (kbytes <= budget) { pl.keys_in_smem = 1; used += kbytes; }
+            const uint64_t hbytes = (4ull * C + 15) & ~15ull;
+            if (hbytes <= ctx->hist_max_bytes && C <= 16ull * pl.keys_cap) {
+                // few classes, many keys: an smem histogram over all C replaces sorting
+                pl.hist = 1;
+                pl.keys_cap = 0;
+                used += hbytes;
+            } else if (kbytes <= budget) {
+                pl.keys_in_smem = 1;
+                used += kbytes;
+            }
             const uint64_t abytes = (4 * Ac + 15) & ~15ull;
             if (used + abytes <= budget) { pl.attrs_in_smem = 1; used += abytes; }
             const uint64_t WA = (Ac + 63) / 64;
@@ -578,7 +596,7 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
         st = run(ctx, "class_large", [&] {
             for (const auto& g : ctx->large_groups)
                 launch_class_large(dm, g.count, ctx->large_list.p + g.first, ctx->plans.p + g.first, g.smem,
-                                   ctx->recs.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
+                                   ctx->recs.p, ctx->own_mask.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
                                    ctx->un.p, &ctl->ucursor, ctx->gkeys.p, ctx->grows.p,
                                    ctx->dense_cap ? ctx->dense.p : nullptr, ctx->dense_cap, &ctl->dense_cursor,
                                    g.tier >= 3 ? 1024u : 256u, ctx->stream);  // giants: 4x the threads

@@ -37,6 +37,7 @@ struct DevModel {
     const uint32_t* __restrict__ call_tgt;
     const uint32_t* __restrict__ acc_off;
     const uint32_t* __restrict__ acc_tgt;
+    const uint2* __restrict__ attr_info;  // derived at upload: (owner, position in the owner's attribute list)
 };
 
 constexpr int kSigWords = 10;               // 320-bit Bloom signature

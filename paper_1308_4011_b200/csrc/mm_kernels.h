@@ -17,6 +17,7 @@ struct LargePlan {
     uint8_t rows_in_smem;
     uint8_t attrs_in_smem;
     uint8_t ck_masks;      // 1: per-member own-attribute masks (A ≤ 256) in smem; 0: attribute bitmaps
+    uint8_t hist;          // 1: foreign classes counted in an smem histogram over all C (no keys)
 };
 
 struct SweepArgs {
@@ -58,7 +59,7 @@ void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, c
                         ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,
                         uint32_t* ucursor, cudaStream_t st);
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
-                        uint32_t smem_bytes, MethRec* recs, ClassRec* rec, double* lcom,
+                        uint32_t smem_bytes, MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
                         uint32_t* gkeys, uint32_t* grows, uint32_t* dense, uint32_t dense_cap,
                         uint32_t* dense_cursor, uint32_t threads, cudaStream_t st);

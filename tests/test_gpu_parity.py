@@ -122,7 +122,7 @@ def test_gpu_what_if_every_pair_random(gpu_engine):
                     assert g[f] == getattr(w, f), (seed, u, o, d, f)
 
 
-def test_gpu_large_class_paths(gpu_engine):
+def test_gpu_large_class_paths(gpu_engine, monkeypatch):
     # classes with > 32 members, > 64 attributes and methods of degree > 16
     # exercise the CTA path of the metric pass and the streaming sweep path
     cfgs = [
@@ -139,10 +139,16 @@ def test_gpu_large_class_paths(gpu_engine):
         dict(seed=14, n_classes=40, n_methods=4000, n_attributes=30000, k_max_calls=3, k_max_accesses=24,
              intra_class_bias=0.6),   # A > 256 per class: attribute-bitmap LCOM-CK, degree > 16
     ]
-    for cfg in cfgs:
-        s = System.generate(**cfg)
-        check_against_oracle(gpu_engine, s, str(cfg), modes=((COH | COUP, 0, False), (COH | COUP, 0, True),
-                                                             (COH | COUP, 1, False)), top_ks=(1, 4))
+    # CTA-path U rows come from an smem class histogram (4·C ≤ 64 KB, as here)
+    # or from sorted keys (many classes); MMGPU_HIST_MAX_BYTES=0 forces the latter
+    monkeypatch.setenv("MMGPU_HIST_MAX_BYTES", "0")
+    from paper_1308_4011_b200 import Engine
+    with Engine(0) as keys_engine:
+        for e, tag in ((gpu_engine, "hist"), (keys_engine, "keys")):
+            for cfg in cfgs:
+                s = System.generate(**cfg)
+                check_against_oracle(e, s, f"{tag} {cfg}", modes=((COH | COUP, 0, False), (COH | COUP, 0, True),
+                                                                   (COH | COUP, 1, False)), top_ks=(1, 4))
 
 
 def test_gpu_explicit_thresholds_and_degenerate(gpu_engine):
