@@ -111,21 +111,6 @@ __global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg,
     atomicMax(max_deg, mdeg);
 }
 
-// Position of attribute t inside class c's sorted attribute list
-// (ClassRecord::attribute_ids, model.hpp:22): short lists are scanned with
-// independent loads (one round trip per 8 entries), long ones bisected.
-__device__ __forceinline__ uint32_t attr_pos(const DevModel& s, uint32_t ab, uint32_t ae, uint32_t t) {
-    // binary search of the sorted list: few instructions; the probes of
-    // neighbouring lanes (same class in class order) hit L1
-    uint32_t lo = 0, hi = ae - ab;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(s.cls_attrs + ab + mid) < t) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
 // Method pass in class order: thread i handles the method at class-order
 // position i. CSR rows are gathered (sector-sized random reads); every write
 // — the 32-byte MethRec, the own-attribute mask, the owner — is coalesced
@@ -286,14 +271,12 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind,
         const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
         for (uint32_t e = cb; e < ce; ++e) L.insert(__ldg(s.method_owner + __ldg(s.call_tgt + e)), 0);
         const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
-        const uint32_t cab = s.cls_aoff[c], cae = s.cls_aoff[c + 1];
         mask = 0;
         for (uint32_t e = ab; e < ae; ++e) {
-            const uint32_t t = __ldg(s.acc_tgt + e);
-            const uint32_t o = __ldg(s.attribute_owner + t);
-            L.insert(o, 1);
-            if (o == c) {
-                mask |= 1ull << attr_pos(s, cab, cae, t);
+            const uint2 ai = __ldg(s.attr_info + __ldg(s.acc_tgt + e));
+            L.insert(ai.x, 1);
+            if (ai.x == c) {
+                mask |= 1ull << ai.y;
                 ++hown;
             }
         }
@@ -523,11 +506,11 @@ __device__ __forceinline__ void member_used(const DevModel& s, const MethRec* re
 }
 
 // One CTA per class outside the warp path (Zipf giants, C5's 500-method
-// classes). Dynamic shared memory holds, when they fit (host plan): the
-// class's sorted attribute list (own-attribute positions by binary search),
-// the foreign-class keys (one per member and used class — members' lists are
-// already distinct, so a run length IS the member count U[c][X]), and the
-// LCOM-CK structure: per-member own-attribute masks (A ≤ 256: pairs tested by
+// classes). Dynamic shared memory holds, when they fit (host plan): a
+// histogram over all C classes (cnt[X] = U[c][X]) or the foreign-class keys
+// (one per member and used class — members' lists are already distinct, so a
+// run length IS the member count U[c][X]), and the LCOM-CK structure
+// (own-attribute positions come from attr_info, no searches): per-member own-attribute masks (A ≤ 256: pairs tested by
 // word ANDs) or per-attribute member bitmaps (sparse giants).
 __global__ void __launch_bounds__(1024)
 k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* __restrict__ plan,
@@ -550,13 +533,6 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     const uint32_t W = (M + 31) / 32;        // rows mode: words per attribute bitmap
     const uint32_t WA = (A + 63) / 64;       // masks mode: u64 words per member
     unsigned char* cur = dsm;
-    const uint32_t* attrs = s.cls_attrs + ab0;
-    if (pl.attrs_in_smem) {
-        uint32_t* sa = reinterpret_cast<uint32_t*>(cur);
-        for (uint32_t i = threadIdx.x; i < A; i += blockDim.x) sa[i] = s.cls_attrs[ab0 + i];
-        attrs = sa;
-        cur += ((4ull * A + 15) & ~15ull);
-    }
     // foreign classes: a per-class histogram cnt[X] = U[c][X] over all C
     // classes when it fits (few classes, many keys: no sort, no searches),
     // else the keys sorted in place
@@ -598,10 +574,10 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         }
         const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
         for (uint32_t e = ab; e < ae; ++e) {
-            const uint32_t t = __ldg(s.acc_tgt + e);
-            if (__ldg(s.attribute_owner + t) != c) continue;
+            const uint2 ai = __ldg(s.attr_info + __ldg(s.acc_tgt + e));
+            if (ai.x != c) continue;
             ++hown;
-            const uint32_t a = lower_bound_u32(attrs, A, t);
+            const uint32_t a = ai.y;
             if (pl.ck_masks) masks[(uint64_t)i * WA + (a >> 6)] |= 1ull << (a & 63);  // member i: this thread only
             else atomicOr(rows + (uint64_t)a * W + (i >> 5), 1u << (i & 31));
         }
@@ -763,8 +739,8 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
                 uint32_t acc = 0;
                 if (w < W && w >= (i >> 5)) {
                     for (uint32_t e = ab; e < ae; ++e) {
-                        const uint32_t t = __ldg(s.acc_tgt + e);
-                        if (__ldg(s.attribute_owner + t) == c) acc |= rows[(uint64_t)lower_bound_u32(attrs, A, t) * W + w];
+                        const uint2 ai = __ldg(s.attr_info + __ldg(s.acc_tgt + e));
+                        if (ai.x == c) acc |= rows[(uint64_t)ai.y * W + w];
                     }
                     if (w == (i >> 5)) acc &= ((i & 31) == 31) ? 0u : (~0u << ((i & 31) + 1));
                 }
@@ -787,7 +763,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     }
 }
 
-// LCOM-CK of a split class, one CTA per (class, 256-member chunk): member i's
+// LCOM-CK of a split class, one CTA per (class, kCkChunk-member chunk): member i's
 // sharers above it = OR of the bitmaps rows[a] of its own attributes a.
 __global__ void __launch_bounds__(kLargeThreads)
 k_ck_rows(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* __restrict__ plan,
@@ -802,9 +778,8 @@ k_ck_rows(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* 
     const uint32_t A = s.cls_aoff[c + 1] - ab0;
     const uint32_t W = (M + 31) / 32;
     const uint32_t* rows = grows + pl.rows_off;
-    const uint32_t* attrs = s.cls_attrs + ab0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t iend = min(M, it.y + kLargeThreads);
+    const uint32_t iend = min(M, it.y + kCkChunk);
     uint64_t q = 0;
     for (uint32_t i = it.y + warp; i < iend; i += kLargeThreads / 32) {
         const uint32_t p = s.cls_methods[mb + i];
@@ -817,9 +792,9 @@ k_ck_rows(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* 
             const uint32_t e = e0 + lane;
             bool own = false;
             if (e < ae) {
-                const uint32_t t = __ldg(s.acc_tgt + e);
-                own = __ldg(s.attribute_owner + t) == c;
-                if (own) mypos = lower_bound_u32(attrs, A, t);
+                const uint2 ai = __ldg(s.attr_info + __ldg(s.acc_tgt + e));
+                own = ai.x == c;
+                if (own) mypos = ai.y;
             }
             const uint32_t b = __ballot_sync(0xffffffffu, own);
             if (own) {
@@ -837,8 +812,8 @@ k_ck_rows(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* 
                 for (uint32_t k = 0; k < nk; ++k) acc |= __ldg(rows + (uint64_t)spos[warp][k] * W + w);
                 if (nown > 64) {  // rare: more own attributes than the staging list
                     for (uint32_t e = ab; e < ae; ++e) {
-                        const uint32_t t = __ldg(s.acc_tgt + e);
-                        if (__ldg(s.attribute_owner + t) == c) acc |= __ldg(rows + (uint64_t)lower_bound_u32(attrs, A, t) * W + w);
+                        const uint2 ai = __ldg(s.attr_info + __ldg(s.acc_tgt + e));
+                        if (ai.x == c) acc |= __ldg(rows + (uint64_t)ai.y * W + w);
                     }
                 }
                 if (w == (i >> 5)) acc &= ((i & 31) == 31) ? 0u : (~0u << ((i & 31) + 1));

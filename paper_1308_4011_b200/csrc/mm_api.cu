@@ -13,6 +13,7 @@
 #include <map>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/mmgpu.h"
@@ -25,6 +26,8 @@ namespace {
 
 // CTA-path classes count foreign classes in an smem histogram when 4·C fits this
 constexpr uint64_t kHistMaxBytes = 64 * 1024;
+constexpr int kMaxTiers = 8;  // CTA-path launch groups (shared-memory tier x CTA size)
+constexpr uint64_t kBigCtaMembers = 2048;  // classes this large launch 1024-thread CTAs
 
 struct Ctl {  // small device-resident control block
     uint32_t bad;
@@ -77,6 +80,10 @@ struct mm_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;       // threshold means run here, overlapping the candidate scoring
     cudaEvent_t ev_metrics = nullptr;  // class tables ready (main -> side)
+    // CTA-path tiers run on their own streams, concurrently with the warp path
+    cudaStream_t aux[kMaxTiers] = {};
+    cudaEvent_t ev_fork = nullptr;
+    cudaEvent_t ev_join[kMaxTiers] = {};
     cudaEvent_t ev_thr = nullptr;      // threshold means ready (side -> main)
     std::string err;
     bool profiling = false;
@@ -95,7 +102,9 @@ struct mm_ctx {
     uint32_t n_large = 0, max_deg = 0;
     struct LargeGroup {
         uint32_t first, count, smem;
-        int tier;
+        int key;           // 2 * shared-memory tier + (1024-thread CTAs)
+        uint32_t threads;
+        uint32_t item_first, n_items, split_first, n_split;  // split LCOM-CK work of this group
     };
     std::vector<LargeGroup> large_groups;  // CTA-path launches, grouped by shared-memory need
     DBuf<uint32_t> dense;                  // exact U-row bitmaps of dense classes
@@ -181,13 +190,16 @@ mm_status run_on(mm_ctx* ctx, cudaStream_t st, const char* name, F&& launch) {
         cudaEventCreate(&pe.b);
         cudaEventRecordWithFlags(pe.a, st, rec_flags);
     }
-    launch();
+    mm_status inner = MM_OK;
+    if constexpr (std::is_same_v<decltype(launch()), mm_status>) inner = launch();
+    else launch();
     const cudaError_t e = cudaGetLastError();
     if (ctx->profiling) {
         cudaEventRecordWithFlags(pe.b, st, rec_flags);
         pe.name = name;
         (ctx->capturing ? ctx->graph_events : ctx->pending).push_back(pe);
     }
+    if (inner != MM_OK) return inner;
     if (e != cudaSuccess) return cuda_fail(ctx, e, name);
     return MM_OK;
 }
@@ -289,10 +301,17 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
         cudaEventCreateWithFlags(&ctx->ev_metrics, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_thr, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventRecord(ctx->ev_thr, ctx->side) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         ctx->ctl.alloc(1) != cudaSuccess || ctx->whatif.alloc(1) != cudaSuccess) {
-        delete ctx;
+        mm_ctx_destroy(ctx);
         return MM_E_CUDA;
     }
+    for (int k = 0; k < kMaxTiers; ++k)
+        if (cudaStreamCreateWithFlags(&ctx->aux[k], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_join[k], cudaEventDisableTiming) != cudaSuccess) {
+            mm_ctx_destroy(ctx);
+            return MM_E_CUDA;
+        }
     ctx->stream = ctx->own;
     if (const char* v = std::getenv("MMGPU_HIST_MAX_BYTES")) ctx->hist_max_bytes = std::strtoull(v, nullptr, 10);
     *out = ctx;
@@ -324,6 +343,11 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->ev_metrics) cudaEventDestroy(ctx->ev_metrics);
     if (ctx->ev_thr) cudaEventDestroy(ctx->ev_thr);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    for (int k = 0; k < kMaxTiers; ++k) {
+        if (ctx->aux[k]) cudaStreamDestroy(ctx->aux[k]);
+        if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
+    }
     delete ctx;
 }
 
@@ -461,8 +485,8 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             std::memset(&pl, 0, sizeof pl);
             pl.keys_cap = next_pow2(std::max<uint32_t>(fr[c], 1));
             n_dense += fr[c] > kDenseRowMin;
-            // shared memory, in order of benefit: keys (sorted in place), the
-            // attribute list, the LCOM-CK structure
+            // shared memory, in order of benefit: the class histogram or the keys
+            // (sorted in place), then the LCOM-CK structure
             uint64_t used = 0;
             const uint64_t kbytes = (4ull * pl.keys_cap + 15) & ~15ull;
             const uint64_t hbytes = (4ull * C + 15) & ~15ull;
@@ -475,8 +499,6 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
                 pl.keys_in_smem = 1;
                 used += kbytes;
             }
-            const uint64_t abytes = (4 * Ac + 15) & ~15ull;
-            if (used + abytes <= budget) { pl.attrs_in_smem = 1; used += abytes; }
             const uint64_t WA = (Ac + 63) / 64;
             const uint64_t mbytes = 8 * Mc * WA;
             if (WA <= 4 && used + mbytes <= budget) { pl.ck_masks = 1; used += mbytes; }
@@ -486,15 +508,26 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             }
             need[i] = used;
         }
-        // launch groups by shared-memory need, so small CTAs are not held to one per SM by a giant
+        // launch groups by shared-memory tier and CTA size, so small CTAs are not
+        // held to one per SM by a giant and giants get 1024 threads
+        static const uint64_t tiers[] = {16 * 1024, 48 * 1024, 100 * 1024, ~0ull};
+        std::vector<int> gkey(ctx->n_large);
+        for (uint32_t i = 0; i < ctx->n_large; ++i) {
+            const uint32_t c = list[i];
+            const uint64_t Mc = s->class_method_off[c + 1] - s->class_method_off[c];
+            int tier = 0;
+            while (need[i] > tiers[tier]) ++tier;
+            gkey[i] = 2 * tier + ((tier >= 3 || Mc >= kBigCtaMembers) ? 1 : 0);
+        }
         std::vector<uint32_t> order(ctx->n_large);
         for (uint32_t i = 0; i < ctx->n_large; ++i) order[i] = i;
-        std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return need[x] < need[y]; });
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
+            return gkey[x] != gkey[y] ? gkey[x] < gkey[y] : need[x] < need[y];
+        });
         std::vector<uint32_t> list2(ctx->n_large);
         std::vector<LargePlan> plans2(ctx->n_large);
         uint64_t koff = 0, roff = 0;
         ctx->large_groups.clear();
-        static const uint64_t tiers[] = {16 * 1024, 48 * 1024, 100 * 1024, ~0ull};
         for (uint32_t j = 0; j < ctx->n_large; ++j) {
             const uint32_t i = order[j];
             list2[j] = list[i];
@@ -505,25 +538,29 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             const uint64_t Mc = s->class_method_off[c + 1] - s->class_method_off[c];
             const uint64_t Ac = s->class_attr_off[c + 1] - s->class_attr_off[c];
             if (!pl.ck_masks && !pl.rows_in_smem) { pl.rows_off = roff; roff += Ac * ((Mc + 31) / 32); }
-            int tier = 0;
-            while (need[i] > tiers[tier]) ++tier;
             const uint32_t smem = (uint32_t)std::max<uint64_t>(16, (need[i] + 15) & ~15ull);
-            if (ctx->large_groups.empty() || ctx->large_groups.back().tier != tier)
-                ctx->large_groups.push_back({j, 0, smem, tier});
+            if (ctx->large_groups.empty() || ctx->large_groups.back().key != gkey[i])
+                ctx->large_groups.push_back({j, 0, smem, gkey[i], (gkey[i] & 1) ? 1024u : 256u, 0, 0, 0, 0});
             auto& g = ctx->large_groups.back();
             ++g.count;
             g.smem = std::max(g.smem, smem);
         }
-        // classes whose attribute bitmaps live in global scratch: LCOM-CK split over 256-member chunks
+        // classes whose attribute bitmaps live in global scratch: LCOM-CK split over kCkChunk-member chunks
         std::vector<uint2> items;
         std::vector<uint32_t> split;
-        for (uint32_t j = 0; j < ctx->n_large; ++j) {
-            const LargePlan& pl = plans2[j];
-            if (pl.ck_masks || pl.rows_in_smem) continue;
-            const uint32_t c = list2[j];
-            const uint32_t Mc = s->class_method_off[c + 1] - s->class_method_off[c];
-            split.push_back(c);
-            for (uint32_t b = 0; b < Mc; b += 256) items.push_back(make_uint2(j, b));
+        for (auto& g : ctx->large_groups) {  // per group: its split classes' work follows it on its stream
+            g.item_first = (uint32_t)items.size();
+            g.split_first = (uint32_t)split.size();
+            for (uint32_t j = g.first; j < g.first + g.count; ++j) {
+                const LargePlan& pl = plans2[j];
+                if (pl.ck_masks || pl.rows_in_smem) continue;
+                const uint32_t c = list2[j];
+                const uint32_t Mc = s->class_method_off[c + 1] - s->class_method_off[c];
+                split.push_back(c);
+                for (uint32_t b = 0; b < Mc; b += kCkChunk) items.push_back(make_uint2(j, b));
+            }
+            g.n_items = (uint32_t)items.size() - g.item_first;
+            g.n_split = (uint32_t)split.size() - g.split_first;
         }
         ctx->n_ck_items = (uint32_t)items.size();
         ctx->n_split = (uint32_t)split.size();
@@ -586,25 +623,42 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
         launch_method(dm, ctx->kind.p, ctx->recs.p, ctx->own_mask.p, ctx->pos_owner.p, ctx->stream);
     });
     if (st) return st;
-    st = run(ctx, "class_small", [&] {
-        launch_class_small(dm, ctx->kind.p, ctx->recs.p, ctx->own_mask.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p,
-                           ctx->cbo.p, ctx->ux.p, ctx->un.p, &ctl->ucursor, ctx->stream);
+    // class pass: the CTA-path tiers fork onto their own streams (longest
+    // tier first) and overlap each other and the warp path on the main stream
+    st = run(ctx, "class_pass", [&] {
+        if (ctx->grows_words) MM_CUDA(ctx, cudaMemsetAsync(ctx->grows.p, 0, 4ull * ctx->grows_words, ctx->stream));
+        const size_t ng = ctx->large_groups.size();
+        if (ng) MM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
+        for (size_t k = 0; k < ng; ++k) {
+            const auto& g = ctx->large_groups[ng - 1 - k];
+            cudaStream_t as = ctx->aux[k];
+            MM_CUDA(ctx, cudaStreamWaitEvent(as, ctx->ev_fork, 0));
+            if (mm_status e = run_on(ctx, as, "class_large", [&] {
+                    launch_class_large(dm, g.count, ctx->large_list.p + g.first, ctx->plans.p + g.first, g.smem,
+                                       ctx->recs.p, ctx->own_mask.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p,
+                                       ctx->ux.p, ctx->un.p, &ctl->ucursor, ctx->gkeys.p, ctx->grows.p,
+                                       ctx->dense_cap ? ctx->dense.p : nullptr, ctx->dense_cap, &ctl->dense_cursor,
+                                       g.threads, as);
+                }))
+                return e;
+            if (g.n_items)
+                if (mm_status e = run_on(ctx, as, "ck_rows", [&] {
+                        launch_ck_rows(dm, ctx->large_list.p, ctx->plans.p, ctx->ck_items.p + g.item_first,
+                                       g.n_items, ctx->grows.p, ctx->split_list.p + g.split_first, g.n_split,
+                                       ctx->ck.p, as);
+                    }))
+                    return e;
+            MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[k], as));
+        }
+        if (mm_status e = run(ctx, "class_small", [&] {
+                launch_class_small(dm, ctx->kind.p, ctx->recs.p, ctx->own_mask.p, ctx->rec.p, ctx->lcom.p,
+                                   ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p, &ctl->ucursor, ctx->stream);
+            }))
+            return e;
+        for (size_t k = 0; k < ng; ++k) MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[k], 0));
+        return MM_OK;
     });
     if (st) return st;
-    if (ctx->n_large) {
-        if (ctx->grows_words) MM_CUDA(ctx, cudaMemsetAsync(ctx->grows.p, 0, 4ull * ctx->grows_words, ctx->stream));
-        st = run(ctx, "class_large", [&] {
-            for (const auto& g : ctx->large_groups)
-                launch_class_large(dm, g.count, ctx->large_list.p + g.first, ctx->plans.p + g.first, g.smem,
-                                   ctx->recs.p, ctx->own_mask.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p,
-                                   ctx->un.p, &ctl->ucursor, ctx->gkeys.p, ctx->grows.p,
-                                   ctx->dense_cap ? ctx->dense.p : nullptr, ctx->dense_cap, &ctl->dense_cursor,
-                                   g.tier >= 3 ? 1024u : 256u, ctx->stream);  // giants: 4x the threads
-            launch_ck_rows(dm, ctx->large_list.p, ctx->plans.p, ctx->ck_items.p, ctx->n_ck_items, ctx->grows.p,
-                           ctx->split_list.p, ctx->n_split, ctx->ck.p, ctx->stream);
-        });
-        if (st) return st;
-    }
     // threshold means on the side stream: they overlap the candidate scoring,
     // only the emission pass of the sweep waits for them
     MM_CUDA(ctx, cudaEventRecord(ctx->ev_metrics, ctx->stream));

@@ -9,13 +9,14 @@
 namespace mmg {
 
 // Per large class (CTA path) scratch placement, planned on the host at upload.
+constexpr uint32_t kCkChunk = 64;  // members per k_ck_rows CTA (2 per warp: latency-bound chains)
+
 struct LargePlan {
     uint64_t keys_off;     // u32 element offset into the global key scratch
     uint64_t rows_off;     // u32 element offset into the global row scratch
     uint32_t keys_cap;     // power of two ≥ foreign edge count (≥ foreign keys)
     uint8_t keys_in_smem;
     uint8_t rows_in_smem;
-    uint8_t attrs_in_smem;
     uint8_t ck_masks;      // 1: per-member own-attribute masks (A ≤ 256) in smem; 0: attribute bitmaps
     uint8_t hist;          // 1: foreign classes counted in an smem histogram over all C (no keys)
 };
