@@ -428,16 +428,20 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
         pinned[f] = t
     hs = System(s.n_classes, s.n_methods, s.n_attributes,
                 **{f: t.numpy().view(np.uint32) for f, t in pinned.items()})
-    h2d = s.nbytes()
+    # owner tables stay on the host: the device derives them from the
+    # membership lists (mm_system contract), so they are not in the H2D bytes
+    h2d = s.nbytes() - s.method_owner.nbytes - s.attribute_owner.nbytes
     d2h = [0]
 
     def e2e_step():
-        eng.upload(hs)                                   # H2D from pinned host + device validation + plan
+        eng.upload(hs, owner_tables=False)               # H2D from pinned host + device validation + plan
         eng.compute_metrics()
-        lcom, ck, cbo = eng.class_metrics_all(copy=False)  # D2H per-class metrics (pinned)
         if world == 1:
-            recs = eng.suggest_all(eng.compute_thresholds(), copy=False)  # sweep + D2H of the ordered list
+            eng.sweep(thresholds=None, want_count=False)   # thresholds = device means of this pass
+            lcom, ck, cbo = eng.class_metrics_all(copy=False)  # D2H per-class metrics (pinned)
+            recs = eng.suggestions(copy=False)             # D2H of the ordered list
         else:
+            lcom, ck, cbo = eng.class_metrics_all(copy=False)
             eng.sweep(thresholds=None, class_range=shard, want_count=False)
             n_local = eng.sweep_stats()["suggestions"]
             allrec, counts = gather(n_local)
@@ -460,7 +464,8 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
         dt = float(t.item())
     return {"value": n_cand / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h[0]),
             "ms_per_step": dt * 1e3, "steps": n,
-            "path": "Engine.upload(pinned host CSR) -> compute_metrics -> class_metrics_all (D2H) -> suggest_all (D2H)"}
+            "path": "Engine.upload(pinned host CSR, owners derived on device) -> compute_metrics -> sweep "
+                    "(device thresholds) -> class_metrics_all (D2H) -> suggestions (D2H)"}
 
 
 def main():

@@ -50,16 +50,11 @@ __global__ void k_validate_offsets(const uint32_t* __restrict__ off, uint64_t n_
 // Zipf giants): per member, its degree and foreign-edge count, folded into its
 // class with atomics. Every index is bounds-checked: this runs before the
 // validation result is known.
-__global__ void k_plan_methods(DevModel s, uint32_t* __restrict__ foreign, uint32_t* __restrict__ cmaxdeg) {
+__global__ void k_plan_methods(DevModel s, const uint32_t* __restrict__ pos_owner, uint32_t* __restrict__ foreign,
+                               uint32_t* __restrict__ cmaxdeg) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= s.M) return;
-    uint32_t lo = 0, hi = s.C;  // class of position i: last c with cls_moff[c] <= i
-    while (lo + 1 < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s.cls_moff[mid] <= i) lo = mid;
-        else hi = mid;
-    }
-    const uint32_t c = lo;
+    const uint32_t c = pos_owner[i];
     const uint32_t p = s.cls_methods[i];
     if (p >= s.M || c >= s.C) return;
     const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
@@ -78,21 +73,37 @@ __global__ void k_plan_methods(DevModel s, uint32_t* __restrict__ foreign, uint3
     atomicMax(cmaxdeg + c, (ce - cb) + (ae - ab));
 }
 
-// attr_info[t] = (owner(t), position of t in its owner's attribute list): one
-// 8-byte gather gives the method pass both the owner and the LCOM-CK mask bit
-// (the list is the class's attribute order, so the bit is the same one the
-// reference's sorted-list intersection test would find). Bounds-checked.
-__global__ void k_attr_info(DevModel s, uint2* __restrict__ info) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;  // position in cls_attrs
-    if (i >= s.A) return;
-    uint32_t lo = 0, hi = s.C;  // class of list position i
-    while (lo + 1 < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s.cls_aoff[mid] <= i) lo = mid;
-        else hi = mid;
+// Upload-time expansion of the membership lists, one warp per class (lanes
+// over the class's list positions, coalesced; no per-position searches):
+//   pos_owner[k]  = class of method position k (the class-order owner table
+//                   every pass reads instead of gathering method_owner)
+//   attr_info[t]  = (owner(t), position of t in its owner's attribute list):
+//                   one 8-byte gather gives the method pass the owner and the
+//                   LCOM-CK mask bit
+//   method_owner / attribute_owner, when the caller omitted them
+// Every index is clamped or bounds-checked: this runs before validation's
+// verdict is known.
+__global__ void k_expand(DevModel s, uint32_t* __restrict__ mo_out, uint32_t* __restrict__ ao_out,
+                         uint32_t* __restrict__ pos_owner, uint2* __restrict__ info) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < s.C; c += nw) {
+        const uint32_t mb = min(s.cls_moff[c], s.M), me = min(max(s.cls_moff[c + 1], mb), s.M);
+        for (uint32_t k = mb + lane; k < me; k += 32) {
+            pos_owner[k] = c;
+            if (mo_out) {
+                const uint32_t p = s.cls_methods[k];
+                if (p < s.M) mo_out[p] = c;
+            }
+        }
+        const uint32_t ab = min(s.cls_aoff[c], s.A), ae = min(max(s.cls_aoff[c + 1], ab), s.A);
+        for (uint32_t k = ab + lane; k < ae; k += 32) {
+            const uint32_t t = s.cls_attrs[k];
+            if (t >= s.A) continue;
+            if (ao_out) ao_out[t] = c;
+            info[t] = make_uint2(ao_out ? c : s.attribute_owner[t], k - ab);
+        }
     }
-    const uint32_t t = s.cls_attrs[i];
-    if (t < s.A) info[t] = make_uint2(s.attribute_owner[t], i - min(s.cls_aoff[lo], i));
 }
 
 // classify into the warp path (small) or the CTA path (large)
@@ -120,12 +131,12 @@ __global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg,
 // own class (classes with ≤ 64 attributes).
 template <int K>
 __global__ void __launch_bounds__(256, 5)
-k_method(DevModel s, const uint8_t* __restrict__ kind, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask,
-         uint32_t* __restrict__ pos_owner) {
+k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask,
+         const uint32_t* __restrict__ pos_owner) {
     const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
     if (pos >= s.M) return;
     const uint32_t p = __ldg(s.cls_methods + pos);
-    const uint32_t own = __ldg(s.method_owner + p);
+    const uint32_t own = __ldg(pos_owner + pos);
     const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
     const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
     const uint32_t oab = __ldg(s.cls_aoff + own), oae = __ldg(s.cls_aoff + own + 1);
@@ -192,7 +203,6 @@ k_method(DevModel s, const uint8_t* __restrict__ kind, MethRec* __restrict__ rec
     dst[0] = make_uint4(hdr, ent[0], ent[1], ent[2]);
     dst[1] = make_uint4(ent[3], ent[4], ent[5], ent[6]);
     own_mask[pos] = mask;
-    pos_owner[pos] = own;
 }
 
 // ---------------------------------------------------------------------------
@@ -847,24 +857,31 @@ void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
     k_validate_ids<<<blocks, 256, 0, st>>>(v, n, bound, bad);
 }
+void launch_expand(const DevModel& s, uint32_t* mo_out, uint32_t* ao_out, uint32_t* pos_owner, uint2* info,
+                   cudaStream_t st) {
+    if (!s.C) return;
+    if (mo_out && s.M) cudaMemsetAsync(mo_out, 0xff, 4ull * s.M, st);  // unowned ids fail validation
+    if (ao_out && s.A) cudaMemsetAsync(ao_out, 0xff, 4ull * s.A, st);
+    const uint32_t blocks = std::min<uint32_t>((s.C + 7) / 8, 148 * 8);
+    k_expand<<<blocks, 256, 0, st>>>(s, mo_out, ao_out, pos_owner, info);
+}
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st) {
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((n1 + 255) / 256, 148 * 16);
     k_validate_offsets<<<blocks, 256, 0, st>>>(off, n1, total, bad);
 }
-void launch_plan_classes(const DevModel& s, uint8_t* kind, uint32_t* large_list, uint32_t* n_large,
-                         uint32_t* max_deg, uint32_t* foreign, uint32_t* cmaxdeg, cudaStream_t st) {
+void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint8_t* kind, uint32_t* large_list,
+                         uint32_t* n_large, uint32_t* max_deg, uint32_t* foreign, uint32_t* cmaxdeg, cudaStream_t st) {
     if (!s.C) return;
     cudaMemsetAsync(foreign, 0, 4ull * s.C, st);
     cudaMemsetAsync(cmaxdeg, 0, 4ull * s.C, st);
-    if (s.A) k_attr_info<<<(s.A + 255) / 256, 256, 0, st>>>(s, const_cast<uint2*>(s.attr_info));
-    if (s.M) k_plan_methods<<<(s.M + 255) / 256, 256, 0, st>>>(s, foreign, cmaxdeg);
+    if (s.M) k_plan_methods<<<(s.M + 255) / 256, 256, 0, st>>>(s, pos_owner, foreign, cmaxdeg);
     k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, cmaxdeg, kind, large_list, n_large, max_deg);
 }
-void launch_method(const DevModel& s, const uint8_t* kind, MethRec* recs, uint64_t* own_mask, uint32_t* pos_owner,
+void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
                    cudaStream_t st) {
     if (!s.M) return;
     const uint32_t blocks = (s.M + 255) / 256;
-    k_method<8><<<blocks, 256, 0, st>>>(s, kind, recs, own_mask, pos_owner);
+    k_method<8><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
 }
 void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, const uint64_t* own_mask,
                         ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,

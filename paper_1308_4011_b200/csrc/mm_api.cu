@@ -28,6 +28,7 @@ namespace {
 constexpr uint64_t kHistMaxBytes = 64 * 1024;
 constexpr int kMaxTiers = 8;  // CTA-path launch groups (shared-memory tier x CTA size)
 constexpr uint64_t kBigCtaMembers = 2048;  // classes this large launch 1024-thread CTAs
+constexpr int kUploadArrays = 10;
 
 struct Ctl {  // small device-resident control block
     uint32_t bad;
@@ -84,6 +85,7 @@ struct mm_ctx {
     cudaStream_t aux[kMaxTiers] = {};
     cudaEvent_t ev_fork = nullptr;
     cudaEvent_t ev_join[kMaxTiers] = {};
+    cudaEvent_t ev_up[kUploadArrays] = {};  // per-array copy done (upload validation overlaps the copies)
     cudaEvent_t ev_thr = nullptr;      // threshold means ready (side -> main)
     std::string err;
     bool profiling = false;
@@ -312,6 +314,11 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
             mm_ctx_destroy(ctx);
             return MM_E_CUDA;
         }
+    for (int k = 0; k < kUploadArrays; ++k)
+        if (cudaEventCreateWithFlags(&ctx->ev_up[k], cudaEventDisableTiming) != cudaSuccess) {
+            mm_ctx_destroy(ctx);
+            return MM_E_CUDA;
+        }
     ctx->stream = ctx->own;
     if (const char* v = std::getenv("MMGPU_HIST_MAX_BYTES")) ctx->hist_max_bytes = std::strtoull(v, nullptr, 10);
     *out = ctx;
@@ -348,6 +355,8 @@ void mm_ctx_destroy(mm_ctx* ctx) {
         if (ctx->aux[k]) cudaStreamDestroy(ctx->aux[k]);
         if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
     }
+    for (int k = 0; k < kUploadArrays; ++k)
+        if (ctx->ev_up[k]) cudaEventDestroy(ctx->ev_up[k]);
     delete ctx;
 }
 
@@ -398,8 +407,8 @@ uint64_t mm_system_bytes(const mm_system* s) {
     if (!s) return 0;
     const uint64_t Ec = s->call_off ? s->call_off[s->n_methods] : 0;
     const uint64_t Ea = s->acc_off ? s->acc_off[s->n_methods] : 0;
-    return 4ull * (2ull * s->n_methods + 2ull * s->n_attributes + 2ull * (s->n_classes + 1) +
-                   2ull * (s->n_methods + 1) + Ec + Ea);
+    return 4ull * ((s->method_owner ? 2ull : 1ull) * s->n_methods + (s->attribute_owner ? 2ull : 1ull) * s->n_attributes +
+                   2ull * (s->n_classes + 1) + 2ull * (s->n_methods + 1) + Ec + Ea);
 }
 
 mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
@@ -416,34 +425,57 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     const uint32_t C = s->n_classes, M = s->n_methods, A = s->n_attributes;
     const uint64_t Ec = s->call_off[M], Ea = s->acc_off[M];
     ctx->C = C; ctx->M = M; ctx->A = A; ctx->Ec = Ec; ctx->Ea = Ea;
-    if (mm_status st = upload_array(ctx, ctx->method_owner, s->method_owner, M, "method_owner")) return st;
-    if (mm_status st = upload_array(ctx, ctx->attribute_owner, s->attribute_owner, A, "attribute_owner")) return st;
-    if (mm_status st = upload_array(ctx, ctx->cls_moff, s->class_method_off, C + 1ull, "class_method_off")) return st;
-    if (mm_status st = upload_array(ctx, ctx->cls_methods, s->class_methods, M, "class_methods")) return st;
-    if (mm_status st = upload_array(ctx, ctx->cls_aoff, s->class_attr_off, C + 1ull, "class_attr_off")) return st;
-    if (mm_status st = upload_array(ctx, ctx->cls_attrs, s->class_attrs, A, "class_attrs")) return st;
-    if (mm_status st = upload_array(ctx, ctx->call_off, s->call_off, M + 1ull, "call_off")) return st;
-    if (mm_status st = upload_array(ctx, ctx->call_tgt, s->call_tgt, Ec, "call_tgt")) return st;
-    if (mm_status st = upload_array(ctx, ctx->acc_off, s->acc_off, M + 1ull, "acc_off")) return st;
-    if (mm_status st = upload_array(ctx, ctx->acc_tgt, s->acc_tgt, Ea, "acc_tgt")) return st;
     ctx->h_cls_moff.assign(s->class_method_off, s->class_method_off + C + 1);
 
-    // device-side range validation: offsets first (totals come from the
-    // host arrays), then every id against its id space
+    // H2D copies on the main stream; each array's range validation runs on an
+    // aux stream as soon as its copy lands, overlapping the next copies.
+    // Offsets are checked against the host totals, ids against their id space.
     Ctl* ctl = ctx->ctl.p;
-    MM_CUDA(ctx, cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx->stream));
     uint32_t* bad = &ctl->bad;
-    mm_status st = run(ctx, "validate", [&] {
-        launch_validate_offsets(ctx->cls_moff.p, C + 1ull, M, bad, ctx->stream);
-        launch_validate_offsets(ctx->cls_aoff.p, C + 1ull, A, bad, ctx->stream);
-        launch_validate_offsets(ctx->call_off.p, M + 1ull, (uint32_t)Ec, bad, ctx->stream);
-        launch_validate_offsets(ctx->acc_off.p, M + 1ull, (uint32_t)Ea, bad, ctx->stream);
-        launch_validate_ids(ctx->method_owner.p, M, C, bad, ctx->stream);
-        launch_validate_ids(ctx->attribute_owner.p, A, C, bad, ctx->stream);
-        launch_validate_ids(ctx->cls_methods.p, M, M, bad, ctx->stream);
-        launch_validate_ids(ctx->cls_attrs.p, A, A, bad, ctx->stream);
-        launch_validate_ids(ctx->call_tgt.p, Ec, M, bad, ctx->stream);
-        launch_validate_ids(ctx->acc_tgt.p, Ea, A, bad, ctx->stream);
+    MM_CUDA(ctx, cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx->stream));
+    cudaStream_t vs = ctx->aux[0];
+    int n_up = 0;
+    auto up = [&](DBuf<uint32_t>& d, const uint32_t* h, size_t n, const char* what, auto&& validate) -> mm_status {
+        if (mm_status st = upload_array(ctx, d, h, n, what)) return st;
+        MM_CUDA(ctx, cudaEventRecord(ctx->ev_up[n_up], ctx->stream));
+        MM_CUDA(ctx, cudaStreamWaitEvent(vs, ctx->ev_up[n_up], 0));
+        ++n_up;
+        validate(d.p);
+        MM_CUDA(ctx, cudaGetLastError());
+        return MM_OK;
+    };
+    auto ids = [&](size_t n, uint32_t bound) { return [=](const uint32_t* p) { launch_validate_ids(p, n, bound, bad, vs); }; };
+    auto offs = [&](size_t n1, uint32_t total) {
+        return [=](const uint32_t* p) { launch_validate_offsets(p, n1, total, bad, vs); };
+    };
+    const bool derive_mo = !s->method_owner, derive_ao = !s->attribute_owner;
+    mm_status st = MM_OK;
+    if ((st = up(ctx->cls_moff, s->class_method_off, C + 1ull, "class_method_off", offs(C + 1ull, M))) ||
+        (st = up(ctx->cls_methods, s->class_methods, M, "class_methods", ids(M, M))) ||
+        (st = up(ctx->cls_aoff, s->class_attr_off, C + 1ull, "class_attr_off", offs(C + 1ull, A))) ||
+        (st = up(ctx->cls_attrs, s->class_attrs, A, "class_attrs", ids(A, A))) ||
+        (!derive_mo && (st = up(ctx->method_owner, s->method_owner, M, "method_owner", ids(M, C)))) ||
+        (!derive_ao && (st = up(ctx->attribute_owner, s->attribute_owner, A, "attribute_owner", ids(A, C)))) ||
+        (st = up(ctx->call_off, s->call_off, M + 1ull, "call_off", offs(M + 1ull, (uint32_t)Ec))) ||
+        (st = up(ctx->call_tgt, s->call_tgt, Ec, "call_tgt", ids(Ec, M))) ||
+        (st = up(ctx->acc_off, s->acc_off, M + 1ull, "acc_off", offs(M + 1ull, (uint32_t)Ea))) ||
+        (st = up(ctx->acc_tgt, s->acc_tgt, Ea, "acc_tgt", ids(Ea, A))))
+        return st;
+    MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[0], vs));
+    MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[0], 0));
+    // expansion of the membership lists: the class-order owner table, the
+    // attribute (owner, rank) table and — when the caller left them out — the
+    // owner tables (the validate() precondition makes them equal; unowned ids
+    // stay kNone and fail the range check)
+    MM_CUDA(ctx, ctx->pos_owner.ensure(M ? M : 1));
+    MM_CUDA(ctx, ctx->attr_info.ensure(A ? A : 1));
+    if (derive_mo) MM_CUDA(ctx, ctx->method_owner.ensure(M ? M : 1));
+    if (derive_ao) MM_CUDA(ctx, ctx->attribute_owner.ensure(A ? A : 1));
+    st = run(ctx, "expand", [&] {
+        launch_expand(ctx->dev(), derive_mo ? ctx->method_owner.p : nullptr, derive_ao ? ctx->attribute_owner.p : nullptr,
+                      ctx->pos_owner.p, ctx->attr_info.p, ctx->stream);
+        if (derive_mo) launch_validate_ids(ctx->method_owner.p, M, C, bad, ctx->stream);
+        if (derive_ao) launch_validate_ids(ctx->attribute_owner.p, A, C, bad, ctx->stream);
     });
     if (st) return st;
 
@@ -453,10 +485,9 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, ctx->large_list.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->foreign.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->cmaxdeg.ensure(C ? C : 1));
-    MM_CUDA(ctx, ctx->attr_info.ensure(A ? A : 1));
     const DevModel dm = ctx->dev();
     st = run(ctx, "plan", [&] {
-        launch_plan_classes(dm, ctx->kind.p, ctx->large_list.p, &ctl->n_large, &ctl->max_deg, ctx->foreign.p,
+        launch_plan_classes(dm, ctx->pos_owner.p, ctx->kind.p, ctx->large_list.p, &ctl->n_large, &ctl->max_deg, ctx->foreign.p,
                             ctx->cmaxdeg.p, ctx->stream);
     });
     if (st) return st;
@@ -594,7 +625,6 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     // derived tables
     MM_CUDA(ctx, ctx->recs.ensure(M ? M : 1));
     MM_CUDA(ctx, ctx->own_mask.ensure(M ? M : 1));
-    MM_CUDA(ctx, ctx->pos_owner.ensure(M ? M : 1));
     MM_CUDA(ctx, ctx->rec.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->lcom.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->ck.ensure(C ? C : 1));
@@ -620,7 +650,7 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
     MM_CUDA(ctx, cudaMemsetAsync(&ctl->ucursor, 0, 2 * sizeof(uint32_t), ctx->stream));  // ucursor, dense_cursor
     const DevModel dm = ctx->dev();
     mm_status st = run(ctx, "method", [&] {
-        launch_method(dm, ctx->kind.p, ctx->recs.p, ctx->own_mask.p, ctx->pos_owner.p, ctx->stream);
+        launch_method(dm, ctx->recs.p, ctx->own_mask.p, ctx->pos_owner.p, ctx->stream);
     });
     if (st) return st;
     // class pass: the CTA-path tiers fork onto their own streams (longest

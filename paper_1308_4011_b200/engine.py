@@ -160,8 +160,14 @@ class Engine:
         self._check(lib().mm_reset_kernel_stats(self._ctx), "mm_reset_kernel_stats")
 
     # ---- model --------------------------------------------------------
-    def upload(self, system: System) -> "Engine":
+    def upload(self, system: System, owner_tables: bool = True) -> "Engine":
+        """H2D of the system. owner_tables=False leaves method_owner /
+        attribute_owner out of the copy: the device derives them from the
+        membership lists (equal for any model that passes validate())."""
         s = system.as_c()
+        if not owner_tables:
+            s.method_owner = abi.U32P()
+            s.attribute_owner = abi.U32P()
         self._check(lib().mm_upload(self._ctx, C.byref(s)), "mm_upload")
         self.system = system
         return self

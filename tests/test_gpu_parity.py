@@ -297,3 +297,33 @@ def test_gpu_graph_step_equals_eager(gpu_engine):
     t2 = oracle.thresholds(l2, c2)
     o2 = oracle.suggest(s2, l2, c2, COH | COUP, 0, False, 1, t2.lcom, t2.cbo)
     assert records_equal(gpu_engine.suggestions(), o2)
+
+
+def test_gpu_upload_without_owner_tables(gpu_engine):
+    # mm_system with NULL owner tables: the device derives them from the
+    # membership lists; every result equals the full upload's
+    for cfg in (dict(seed=31, n_classes=300, n_methods=4000, n_attributes=6000, k_max_calls=5, k_max_accesses=5,
+                     intra_class_bias=0.5),
+                dict(seed=32, n_classes=40, n_methods=6000, n_attributes=3000, k_max_calls=4, k_max_accesses=12,
+                     intra_class_bias=0.6, zipf_s=1.0)):
+        s = System.generate(**cfg)
+        gpu_engine.upload(s)
+        want_m = gpu_metrics(gpu_engine, s)
+        t = gpu_engine.compute_thresholds()
+        want = gpu_engine.suggest_all(t, all_candidates=True)
+        gpu_engine.upload(s, owner_tables=False)
+        got_m = gpu_metrics(gpu_engine, s)
+        assert_metrics_equal(got_m, want_m, str(cfg))
+        assert records_equal(gpu_engine.suggest_all(t, all_candidates=True), want)
+        for u in range(0, s.n_methods, 97):
+            o = int(s.method_owner[u])
+            d = int((o + 1 + u % (s.n_classes - 1)) % s.n_classes)
+            g = gpu_engine.what_if_move(u, o, d)
+            w = oracle.what_if(s, u, o, d)[1]
+            assert all(g[f] == getattr(w, f) for f in abi.WHATIF_FIELDS)
+    # a method no class lists has no derivable owner: rejected like a bad id
+    bad = System.build([([0, 1], [0, 1]), ([2, 3], [2])], [[2], [], []], [[2, 3], [0, 1], [2]])
+    bad.class_methods = bad.class_methods.copy()
+    bad.class_methods[-1] = 0  # method 2 unlisted, method 0 listed twice
+    with pytest.raises(MMArgError):
+        gpu_engine.upload(bad, owner_tables=False)
