@@ -107,9 +107,10 @@ __global__ void k_expand(DevModel s, uint32_t* __restrict__ mo_out, uint32_t* __
 }
 
 // classify into the warp path (small) or the CTA path (large)
-__global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg, uint8_t* __restrict__ kind,
-                               uint32_t* __restrict__ large_list, uint32_t* __restrict__ n_large,
-                               uint32_t* __restrict__ max_deg) {
+__global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg, const uint32_t* __restrict__ foreign,
+                               uint4* __restrict__ cplan, uint32_t* __restrict__ large_list,
+                               uint32_t* __restrict__ n_large, uint32_t* __restrict__ big_list,
+                               uint32_t* __restrict__ n_big, uint32_t* __restrict__ max_deg) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= s.C) return;
     const uint32_t mb = min(s.cls_moff[c], s.M), me = min(max(s.cls_moff[c + 1], mb), s.M);
@@ -117,8 +118,12 @@ __global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg,
     const uint32_t mdeg = cmaxdeg[c];
     const bool small = (me - mb) <= kSmallMaxMembers && A <= kSmallMaxAttrs && mdeg <= kSmallMaxDeg &&
                        s.C < (1u << 27);  // warp path packs X << 5 | member into 32 bits
-    kind[c] = small ? 0 : 1;
-    if (!small) large_list[atomicAdd(n_large, 1u)] = c;
+    // warp path: ≤ 32 foreign edges (so ≤ 32 U-row keys) take the lean
+    // register-sort variant, the rest the shared-memory one (listed)
+    const uint32_t kind = !small ? kKindCta : (foreign[c] <= 32 ? kKindLean : kKindWarpBig);
+    cplan[c] = make_uint4(mb, me - mb, A, kind);
+    if (kind == kKindCta) large_list[atomicAdd(n_large, 1u)] = c;
+    if (kind == kKindWarpBig) big_list[atomicAdd(n_big, 1u)] = c;
     atomicMax(max_deg, mdeg);
 }
 
@@ -243,21 +248,30 @@ __device__ __forceinline__ void warp_bitonic_u32(uint32_t* buf, int N, int lane)
 // One warp per class, one lane per member. Members' used lists come from the
 // method pass records (coalesced: a class's members are contiguous in class
 // order); a member whose list overflowed its record is rebuilt from the CSR.
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-k_class_small(DevModel s, const uint8_t* __restrict__ kind,
+template <bool BIG>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BIG ? 1 : 6)
+k_class_small(DevModel s, const uint4* __restrict__ cplan, const uint32_t* __restrict__ list, uint32_t n_list,
               MethRec* __restrict__ recs, const uint64_t* __restrict__ own_mask, ClassRec* __restrict__ rec,
               double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
-              uint32_t* __restrict__ ux, uint32_t* __restrict__ un, uint32_t* __restrict__ ucursor) {
-    __shared__ uint32_t sbuf[kWarpsPerBlock][kSmallEntries];
-    __shared__ uint32_t scnt[kWarpsPerBlock][kSmallEntries];
+              uint32_t* __restrict__ ux, uint32_t* __restrict__ un) {
+    constexpr int kBuf = BIG ? kSmallEntries : 32;
+    __shared__ uint32_t sbuf[kWarpsPerBlock][kBuf];
+    __shared__ uint32_t scnt[kWarpsPerBlock][BIG ? kSmallEntries : 1];
     __shared__ uint32_t srem[kWarpsPerBlock][32];
     __shared__ uint32_t ssig[kWarpsPerBlock][kSigWords];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t c = blockIdx.x * kWarpsPerBlock + warp;
-    if (c >= s.C || kind[c] != 0) return;  // warp-uniform exit
-    const uint32_t mb = s.cls_moff[c];
-    const uint32_t M = s.cls_moff[c + 1] - mb;
-    const uint32_t A = s.cls_aoff[c + 1] - s.cls_aoff[c];
+    const uint32_t wid = blockIdx.x * kWarpsPerBlock + warp;
+    uint32_t c;
+    if (BIG) {
+        if (wid >= n_list) return;
+        c = list[wid];
+    } else {
+        c = wid;
+        if (c >= s.C) return;
+    }
+    const uint4 cp = cplan[c];  // (first member position, M, A, kind): one load
+    if (!BIG && cp.w != kKindLean) return;  // warp-uniform exit
+    const uint32_t mb = cp.x, M = cp.y, A = cp.z;
     const bool active = lane < (int)M;
     const uint32_t pos = mb + lane;
 
@@ -313,6 +327,7 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind,
     const uint32_t T = __shfl_sync(0xffffffffu, off + cnt, 31);
     uint32_t* buf = sbuf[warp];
     uint32_t* rcnt = scnt[warp];
+    const uint32_t ubase = kSmallRowCap * mb;
     {
         uint32_t w = off;
         if (ovf) {
@@ -333,36 +348,27 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind,
     uint32_t cbo = 0;
     uint32_t removed_me = 0;
     if (T <= 32) {
-        // register bitonic sort across the warp, run-length encode with ballots
-        uint32_t v = lane < (int)T ? buf[lane] : kNone;
-        __syncwarp();
-#pragma unroll
-        for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                const uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
-                const bool up = (lane & k) == 0;
-                const bool lower = (lane & j) == 0;
-                v = (lower == up) ? min(v, o) : max(v, o);
-            }
-        const uint32_t prev = __shfl_up_sync(0xffffffffu, v, 1);
-        const bool head = lane < (int)T && (lane == 0 || (v >> 5) != (prev >> 5));
+        // one key per lane; lanes holding the same class X form a match group:
+        // its size is U[c][X], a group of one names the member that alone uses
+        // X. Rows this short are scanned linearly by every consumer, so they
+        // stay in lane order — no sort.
+        const uint32_t v = lane < (int)T ? buf[lane] : kNone;
+        const uint32_t X = v >> 5;  // X < 2^27 - 1 < kNone >> 5: padding lanes never join a real group
+        const uint32_t grp = __match_any_sync(0xffffffffu, X);
+        const bool head = lane < (int)T && (uint32_t)(__ffs(grp) - 1) == (uint32_t)lane;
         const uint32_t hb = __ballot_sync(0xffffffffu, head);
         cbo = __popc(hb);
-        // single-user entries: the member named by the key loses X on leaving
-        const uint32_t above = hb & ~((2u << lane) - 1);
-        const uint32_t next = above ? __ffs(above) - 1 : T;
-        const bool single = head && next == (uint32_t)lane + 1;
-        if (single) atomicAdd(rem + (v & 31u), 1u);  // the member named by the key loses X
         if (head) {
+            const uint32_t n = __popc(grp);
+            if (n == 1) atomicAdd(rem + (v & 31u), 1u);  // the member named by the key loses X
             const uint32_t idx = __popc(hb & ((1u << lane) - 1));
-            buf[idx] = v >> 5;
-            rcnt[idx] = next - lane;
-            const uint32_t b1 = bloom_h1(v >> 5), b2 = bloom_h2(v >> 5);
+            ux[ubase + idx] = X;
+            un[ubase + idx] = n;
+            const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
             atomicOr(sig + (b1 >> 5), 1u << (b1 & 31));
             atomicOr(sig + (b2 >> 5), 1u << (b2 & 31));
         }
-    } else {
+    } else if (BIG) {
         int N = 64;
         while (N < (int)T) N <<= 1;
         for (int i = (int)T + lane; i < N; i += 32) buf[i] = kNone;
@@ -402,18 +408,16 @@ k_class_small(DevModel s, const uint8_t* __restrict__ kind,
             }
             __syncwarp();
         }
+        // static row slot: a small class has at most kSmallRowCap foreign classes
+        // per member, so rows placed at kSmallRowCap · (first member position)
+        // never overlap — no contended global atomic per class
+        for (uint32_t k = lane; k < cbo; k += 32) {
+            ux[ubase + k] = buf[k];
+            un[ubase + k] = rcnt[k];
+        }
     }
     __syncwarp();
     removed_me = rem[lane];
-    // static row slot: a small class has at most kSmallRowCap foreign classes per
-    // member, so rows placed at kSmallRowCap · (first member position) never
-    // overlap — no contended global atomic per class
-    const uint32_t ubase = kSmallRowCap * mb;
-    (void)ucursor;
-    for (uint32_t k = lane; k < cbo; k += 32) {
-        ux[ubase + k] = buf[k];
-        un[ubase + k] = rcnt[k];
-    }
     // per member: #{X ≠ c : U[c][X] == 1} — the sweep's cbo_origin_after
     if (active && !ovf) recs[pos].hdr = r0.x | (removed_me << kRecRemovedShift) | kRecRemovedValid;
     if (lane == 0) {
@@ -869,13 +873,15 @@ void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, u
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((n1 + 255) / 256, 148 * 16);
     k_validate_offsets<<<blocks, 256, 0, st>>>(off, n1, total, bad);
 }
-void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint8_t* kind, uint32_t* large_list,
-                         uint32_t* n_large, uint32_t* max_deg, uint32_t* foreign, uint32_t* cmaxdeg, cudaStream_t st) {
+void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint32_t* large_list,
+                         uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,
+                         uint32_t* cmaxdeg, cudaStream_t st) {
     if (!s.C) return;
     cudaMemsetAsync(foreign, 0, 4ull * s.C, st);
     cudaMemsetAsync(cmaxdeg, 0, 4ull * s.C, st);
     if (s.M) k_plan_methods<<<(s.M + 255) / 256, 256, 0, st>>>(s, pos_owner, foreign, cmaxdeg);
-    k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, cmaxdeg, kind, large_list, n_large, max_deg);
+    k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, cmaxdeg, foreign, cplan, large_list, n_large, big_list,
+                                                       n_big, max_deg);
 }
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
                    cudaStream_t st) {
@@ -883,12 +889,15 @@ void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const u
     const uint32_t blocks = (s.M + 255) / 256;
     k_method<8><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
 }
-void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, const uint64_t* own_mask,
-                        ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,
-                        uint32_t* ucursor, cudaStream_t st) {
+void launch_class_small(const DevModel& s, const uint4* cplan, const uint32_t* big_list, uint32_t n_big,
+                        MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck,
+                        uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st) {
     if (!s.C) return;
-    k_class_small<<<(s.C + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(
-        s, kind, recs, own_mask, rec, lcom, ck, cbo, ux, un, ucursor);
+    k_class_small<false><<<(s.C + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(
+        s, cplan, nullptr, 0, recs, own_mask, rec, lcom, ck, cbo, ux, un);
+    if (n_big)
+        k_class_small<true><<<(n_big + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(
+            s, cplan, big_list, n_big, recs, own_mask, rec, lcom, ck, cbo, ux, un);
 }
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
                         uint32_t smem_bytes, MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom,

@@ -36,7 +36,7 @@ struct Ctl {  // small device-resident control block
     uint32_t max_deg;
     uint32_t ucursor;
     uint32_t dense_cursor;
-    uint32_t pad0;
+    uint32_t n_big;     // warp-path classes with > 32 U-row keys
     uint32_t tile_counter;
     uint32_t err;
     uint32_t n_emit;
@@ -116,7 +116,9 @@ struct mm_ctx {
     DBuf<uint32_t> split_list;             // the split classes
     uint32_t n_ck_items = 0, n_split = 0;
     uint64_t grows_words = 0;              // global attribute-bitmap scratch in use
-    DBuf<uint8_t> kind;
+    DBuf<uint4> cplan;         // per class (first member position, M, A, kind)
+    DBuf<uint32_t> big_list;   // kKindWarpBig classes
+    uint32_t n_big = 0;
     DBuf<uint32_t> large_list, foreign, cmaxdeg;
     DBuf<LargePlan> plans;
     DBuf<uint32_t> gkeys;
@@ -242,7 +244,8 @@ void free_model(mm_ctx* c) {
     c->own_mask.release();
     c->attr_info.release();
     c->pos_owner.release();
-    c->kind.release();
+    c->cplan.release();
+    c->big_list.release();
     c->plans.release();
     c->gkeys.release();
     c->dense.release();
@@ -481,14 +484,15 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
 
     // class plan (bounds-checked, so it is safe on a model validation rejects):
     // warp path vs CTA path, scratch for the CTA path. One sync for both.
-    MM_CUDA(ctx, ctx->kind.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->cplan.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->big_list.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->large_list.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->foreign.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->cmaxdeg.ensure(C ? C : 1));
     const DevModel dm = ctx->dev();
     st = run(ctx, "plan", [&] {
-        launch_plan_classes(dm, ctx->pos_owner.p, ctx->kind.p, ctx->large_list.p, &ctl->n_large, &ctl->max_deg, ctx->foreign.p,
-                            ctx->cmaxdeg.p, ctx->stream);
+        launch_plan_classes(dm, ctx->pos_owner.p, ctx->cplan.p, ctx->large_list.p, &ctl->n_large, ctx->big_list.p,
+                            &ctl->n_big, &ctl->max_deg, ctx->foreign.p, ctx->cmaxdeg.p, ctx->stream);
     });
     if (st) return st;
     Ctl h{};
@@ -496,6 +500,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     if (h.bad) return fail(ctx, MM_E_ARG, (h.bad & 2u) ? "mm_upload: malformed offsets" : "mm_upload: id out of range");
     ctx->n_large = h.n_large;
+    ctx->n_big = h.n_big;
     ctx->max_deg = h.max_deg;
     if (ctx->n_large) {
         std::vector<uint32_t> list(ctx->n_large), fr(C);
@@ -681,8 +686,8 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
             MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[k], as));
         }
         if (mm_status e = run(ctx, "class_small", [&] {
-                launch_class_small(dm, ctx->kind.p, ctx->recs.p, ctx->own_mask.p, ctx->rec.p, ctx->lcom.p,
-                                   ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p, &ctl->ucursor, ctx->stream);
+                launch_class_small(dm, ctx->cplan.p, ctx->big_list.p, ctx->n_big, ctx->recs.p, ctx->own_mask.p,
+                                   ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p, ctx->stream);
             }))
             return e;
         for (size_t k = 0; k < ng; ++k) MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[k], 0));

@@ -24,6 +24,9 @@ constexpr int kSmallMaxMembers = 32;  // warp path: one lane per member
 constexpr int kSmallMaxAttrs = 64;    // own-attribute set fits a u64 mask
 constexpr int kSmallMaxDeg = 16;      // per-member used list fits registers
 constexpr uint32_t kSmallRowCap = kSmallMaxDeg;  // U-row slots reserved per member of a small class
+// class kinds (upload plan): warp path with ≤ 32 U-row keys, CTA path, warp
+// path with more keys (shared-memory sort)
+constexpr uint32_t kKindLean = 0, kKindCta = 1, kKindWarpBig = 2;
 
 struct DevModel {
     uint32_t C, M, A;
@@ -200,9 +203,10 @@ struct StreamUsed {
     }
 };
 
-// Position of X in U row [base, base+len) (sorted), or -1. Short rows are
-// scanned with independent loads (one memory round trip per 8 entries instead
-// of one per binary-search probe); long rows are binary searched.
+// Position of X in U row [base, base+len), or -1. Short rows (any order: the
+// warp path leaves rows of ≤ 32 entries unsorted) are scanned with independent
+// loads, one memory round trip per 8 entries instead of one per binary-search
+// probe; long rows (always sorted) are binary searched.
 __device__ __forceinline__ int urow_find(const uint32_t* __restrict__ ux, uint32_t base, uint32_t len,
                                          uint32_t X) {
     if (len <= 48) {
@@ -213,7 +217,6 @@ __device__ __forceinline__ int urow_find(const uint32_t* __restrict__ ux, uint32
 #pragma unroll
             for (int j = 0; j < 8; ++j)
                 if (v[j] == X) return (int)(k0 + j);
-            if (v[7] > X) return -1;  // sorted: passed the slot
         }
         return -1;
     }

@@ -54,13 +54,14 @@ void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t
 void launch_expand(const DevModel& s, uint32_t* mo_out, uint32_t* ao_out, uint32_t* pos_owner, uint2* info,
                    cudaStream_t st);
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st);
-void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint8_t* kind, uint32_t* large_list,
-                         uint32_t* n_large, uint32_t* max_deg, uint32_t* foreign, uint32_t* cmaxdeg, cudaStream_t st);
+void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint32_t* large_list,
+                         uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,
+                         uint32_t* cmaxdeg, cudaStream_t st);
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
                    cudaStream_t st);
-void launch_class_small(const DevModel& s, const uint8_t* kind, MethRec* recs, const uint64_t* own_mask,
-                        ClassRec* rec, double* lcom, uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un,
-                        uint32_t* ucursor, cudaStream_t st);
+void launch_class_small(const DevModel& s, const uint4* cplan, const uint32_t* big_list, uint32_t n_big,
+                        MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck,
+                        uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st);
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
                         uint32_t smem_bytes, MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
