@@ -891,12 +891,12 @@ void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const u
 }
 void launch_class_small(const DevModel& s, const uint4* cplan, const uint32_t* big_list, uint32_t n_big,
                         MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck,
-                        uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st) {
+                        uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st, cudaStream_t st_big) {
     if (!s.C) return;
     k_class_small<false><<<(s.C + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(
         s, cplan, nullptr, 0, recs, own_mask, rec, lcom, ck, cbo, ux, un);
     if (n_big)
-        k_class_small<true><<<(n_big + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(
+        k_class_small<true><<<(n_big + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st_big>>>(
             s, cplan, big_list, n_big, recs, own_mask, rec, lcom, ck, cbo, ux, un);
 }
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,

@@ -82,9 +82,9 @@ struct mm_ctx {
     cudaStream_t side = nullptr;       // threshold means run here, overlapping the candidate scoring
     cudaEvent_t ev_metrics = nullptr;  // class tables ready (main -> side)
     // CTA-path tiers run on their own streams, concurrently with the warp path
-    cudaStream_t aux[kMaxTiers] = {};
+    cudaStream_t aux[kMaxTiers + 1] = {};  // + the listed warp-path classes
     cudaEvent_t ev_fork = nullptr;
-    cudaEvent_t ev_join[kMaxTiers] = {};
+    cudaEvent_t ev_join[kMaxTiers + 1] = {};
     cudaEvent_t ev_up[kUploadArrays] = {};  // per-array copy done (upload validation overlaps the copies)
     cudaEvent_t ev_thr = nullptr;      // threshold means ready (side -> main)
     std::string err;
@@ -311,7 +311,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
         mm_ctx_destroy(ctx);
         return MM_E_CUDA;
     }
-    for (int k = 0; k < kMaxTiers; ++k)
+    for (int k = 0; k <= kMaxTiers; ++k)
         if (cudaStreamCreateWithFlags(&ctx->aux[k], cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&ctx->ev_join[k], cudaEventDisableTiming) != cudaSuccess) {
             mm_ctx_destroy(ctx);
@@ -354,7 +354,7 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     if (ctx->ev_metrics) cudaEventDestroy(ctx->ev_metrics);
     if (ctx->ev_thr) cudaEventDestroy(ctx->ev_thr);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    for (int k = 0; k < kMaxTiers; ++k) {
+    for (int k = 0; k <= kMaxTiers; ++k) {
         if (ctx->aux[k]) cudaStreamDestroy(ctx->aux[k]);
         if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
     }
@@ -685,11 +685,22 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
                     return e;
             MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[k], as));
         }
+        // warp-path classes with > 32 U-row keys: their own stream too
+        cudaStream_t bs = ctx->aux[kMaxTiers];
+        if (ctx->n_big) {
+            if (!ng) MM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
+            MM_CUDA(ctx, cudaStreamWaitEvent(bs, ctx->ev_fork, 0));
+        }
         if (mm_status e = run(ctx, "class_small", [&] {
                 launch_class_small(dm, ctx->cplan.p, ctx->big_list.p, ctx->n_big, ctx->recs.p, ctx->own_mask.p,
-                                   ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p, ctx->stream);
+                                   ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p, ctx->stream,
+                                   bs);
             }))
             return e;
+        if (ctx->n_big) {
+            MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[kMaxTiers], bs));
+            MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[kMaxTiers], 0));
+        }
         for (size_t k = 0; k < ng; ++k) MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[k], 0));
         return MM_OK;
     });

@@ -61,7 +61,7 @@ void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const u
                    cudaStream_t st);
 void launch_class_small(const DevModel& s, const uint4* cplan, const uint32_t* big_list, uint32_t n_big,
                         MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck,
-                        uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st);
+                        uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st, cudaStream_t st_big);
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
                         uint32_t smem_bytes, MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
