@@ -457,9 +457,10 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
         eng.upload(hs, owner_tables=False)               # H2D from pinned host + device validation + plan
         eng.compute_metrics()
         if world == 1:
+            lcom, ck, cbo = eng.class_metrics_async()      # D2H per-class metrics (pinned), under the sweep
             eng.sweep(thresholds=None, want_count=False)   # thresholds = device means of this pass
-            lcom, ck, cbo = eng.class_metrics_all(copy=False)  # D2H per-class metrics (pinned)
             recs = eng.suggestions(copy=False)             # D2H of the ordered list
+            eng.synchronize()
         else:
             lcom, ck, cbo = eng.class_metrics_all(copy=False)
             eng.sweep(thresholds=None, class_range=shard, want_count=False)
@@ -484,8 +485,8 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
         dt = float(t.item())
     return {"value": n_cand / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h[0]),
             "ms_per_step": dt * 1e3, "steps": n,
-            "path": "Engine.upload(pinned host CSR, owners derived on device) -> compute_metrics -> sweep "
-                    "(device thresholds) -> class_metrics_all (D2H) -> suggestions (D2H)"}
+            "path": "Engine.upload(pinned host CSR, owners derived on device) -> compute_metrics -> "
+                    "class_metrics_async (D2H under the sweep) -> sweep (device thresholds) -> suggestions (D2H)"}
 
 
 def main():

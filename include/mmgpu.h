@@ -205,6 +205,11 @@ mm_status mm_compute_metrics(mm_ctx* ctx);
  *   lcom_ck == lcom_ck per class         (metrics.hpp:159)
  *   cbo     == cbo per class             (metrics.hpp:187) */
 mm_status mm_class_metrics(mm_ctx* ctx, double* lcom, uint64_t* lcom_ck, uint32_t* cbo);
+/* The same copies, only enqueued: they run on a copy stream behind the work
+ * already launched and overlap what is launched next (e.g. mm_sweep). The
+ * buffers (pinned, for a truly asynchronous copy) hold the results after
+ * mm_ctx_synchronize; the next metric pass waits for the copies. */
+mm_status mm_class_metrics_async(mm_ctx* ctx, double* lcom, uint64_t* lcom_ck, uint32_t* cbo);
 /* Single-class accessors with the reference's error behaviour
  * (out_of_range on a bad id, metrics.hpp:97-100). */
 mm_status mm_lcom_normalized(mm_ctx* ctx, uint32_t cls, double* out);

@@ -86,6 +86,8 @@ struct mm_ctx {
     cudaEvent_t ev_fork = nullptr;
     cudaEvent_t ev_join[kMaxTiers + 1] = {};
     cudaEvent_t ev_up[kUploadArrays] = {};  // per-array copy done (upload validation overlaps the copies)
+    cudaStream_t d2h = nullptr;             // mm_class_metrics_async copies
+    cudaEvent_t ev_d2h_go = nullptr, ev_d2h_done = nullptr;
     cudaEvent_t ev_thr = nullptr;      // threshold means ready (side -> main)
     std::string err;
     bool profiling = false;
@@ -322,6 +324,13 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
             mm_ctx_destroy(ctx);
             return MM_E_CUDA;
         }
+    if (cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_d2h_go, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_d2h_done, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ctx->ev_d2h_done, ctx->d2h) != cudaSuccess) {
+        mm_ctx_destroy(ctx);
+        return MM_E_CUDA;
+    }
     ctx->stream = ctx->own;
     if (const char* v = std::getenv("MMGPU_HIST_MAX_BYTES")) ctx->hist_max_bytes = std::strtoull(v, nullptr, 10);
     *out = ctx;
@@ -333,6 +342,7 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->side);
+    if (ctx->d2h) cudaStreamSynchronize(ctx->d2h);
     resolve_pending(ctx);
     if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
     for (Pending& p : ctx->graph_events) {
@@ -360,6 +370,9 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     }
     for (int k = 0; k < kUploadArrays; ++k)
         if (ctx->ev_up[k]) cudaEventDestroy(ctx->ev_up[k]);
+    if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
+    if (ctx->ev_d2h_go) cudaEventDestroy(ctx->ev_d2h_go);
+    if (ctx->ev_d2h_done) cudaEventDestroy(ctx->ev_d2h_done);
     delete ctx;
 }
 
@@ -371,6 +384,7 @@ mm_status mm_ctx_set_stream(mm_ctx* ctx, void* s) {
 
 mm_status mm_ctx_synchronize(mm_ctx* ctx) {
     if (!ctx) return MM_E_ARG;
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->d2h));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->side));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return MM_OK;
@@ -452,6 +466,30 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         return [=](const uint32_t* p) { launch_validate_offsets(p, n1, total, bad, vs); };
     };
     const bool derive_mo = !s->method_owner, derive_ao = !s->attribute_owner;
+    // every buffer first: the expansion below captures pointers while later
+    // arrays are still being copied
+    MM_CUDA(ctx, ctx->method_owner.ensure(M ? M : 1));
+    MM_CUDA(ctx, ctx->attribute_owner.ensure(A ? A : 1));
+    MM_CUDA(ctx, ctx->call_off.ensure(M + 1ull));
+    MM_CUDA(ctx, ctx->call_tgt.ensure(Ec ? Ec : 1));
+    MM_CUDA(ctx, ctx->acc_off.ensure(M + 1ull));
+    MM_CUDA(ctx, ctx->acc_tgt.ensure(Ea ? Ea : 1));
+    MM_CUDA(ctx, ctx->pos_owner.ensure(M ? M : 1));
+    MM_CUDA(ctx, ctx->attr_info.ensure(A ? A : 1));
+    // expansion of the membership lists, on the validation stream as soon as
+    // the lists (and any owner tables) are in, under the remaining copies: the
+    // class-order owner table, the attribute (owner, rank) table and — when
+    // the caller left them out — the owner tables (the validate()
+    // precondition makes them equal; unowned ids stay kNone and fail the
+    // range check)
+    auto expand = [&]() -> mm_status {
+        return run_on(ctx, vs, "expand", [&] {
+            launch_expand(ctx->dev(), derive_mo ? ctx->method_owner.p : nullptr,
+                          derive_ao ? ctx->attribute_owner.p : nullptr, ctx->pos_owner.p, ctx->attr_info.p, vs);
+            if (derive_mo) launch_validate_ids(ctx->method_owner.p, M, C, bad, vs);
+            if (derive_ao) launch_validate_ids(ctx->attribute_owner.p, A, C, bad, vs);
+        });
+    };
     mm_status st = MM_OK;
     if ((st = up(ctx->cls_moff, s->class_method_off, C + 1ull, "class_method_off", offs(C + 1ull, M))) ||
         (st = up(ctx->cls_methods, s->class_methods, M, "class_methods", ids(M, M))) ||
@@ -459,6 +497,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         (st = up(ctx->cls_attrs, s->class_attrs, A, "class_attrs", ids(A, A))) ||
         (!derive_mo && (st = up(ctx->method_owner, s->method_owner, M, "method_owner", ids(M, C)))) ||
         (!derive_ao && (st = up(ctx->attribute_owner, s->attribute_owner, A, "attribute_owner", ids(A, C)))) ||
+        (st = expand()) ||
         (st = up(ctx->call_off, s->call_off, M + 1ull, "call_off", offs(M + 1ull, (uint32_t)Ec))) ||
         (st = up(ctx->call_tgt, s->call_tgt, Ec, "call_tgt", ids(Ec, M))) ||
         (st = up(ctx->acc_off, s->acc_off, M + 1ull, "acc_off", offs(M + 1ull, (uint32_t)Ea))) ||
@@ -466,21 +505,6 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         return st;
     MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[0], vs));
     MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[0], 0));
-    // expansion of the membership lists: the class-order owner table, the
-    // attribute (owner, rank) table and — when the caller left them out — the
-    // owner tables (the validate() precondition makes them equal; unowned ids
-    // stay kNone and fail the range check)
-    MM_CUDA(ctx, ctx->pos_owner.ensure(M ? M : 1));
-    MM_CUDA(ctx, ctx->attr_info.ensure(A ? A : 1));
-    if (derive_mo) MM_CUDA(ctx, ctx->method_owner.ensure(M ? M : 1));
-    if (derive_ao) MM_CUDA(ctx, ctx->attribute_owner.ensure(A ? A : 1));
-    st = run(ctx, "expand", [&] {
-        launch_expand(ctx->dev(), derive_mo ? ctx->method_owner.p : nullptr, derive_ao ? ctx->attribute_owner.p : nullptr,
-                      ctx->pos_owner.p, ctx->attr_info.p, ctx->stream);
-        if (derive_mo) launch_validate_ids(ctx->method_owner.p, M, C, bad, ctx->stream);
-        if (derive_ao) launch_validate_ids(ctx->attribute_owner.p, A, C, bad, ctx->stream);
-    });
-    if (st) return st;
 
     // class plan (bounds-checked, so it is safe on a model validation rejects):
     // warp path vs CTA path, scratch for the CTA path. One sync for both.
@@ -652,6 +676,7 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
     if (!ctx->have_model) return fail(ctx, MM_E_STATE, "mm_compute_metrics: no model uploaded");
     if (mm_status st = set_device(ctx)) return st;
     Ctl* ctl = ctx->ctl.p;
+    MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_d2h_done, 0));  // async copies of the last results
     MM_CUDA(ctx, cudaMemsetAsync(&ctl->ucursor, 0, 2 * sizeof(uint32_t), ctx->stream));  // ucursor, dense_cursor
     const DevModel dm = ctx->dev();
     mm_status st = run(ctx, "method", [&] {
@@ -731,6 +756,19 @@ mm_status mm_class_metrics(mm_ctx* ctx, double* lcom, uint64_t* lcom_ck, uint32_
     if (C && lcom_ck) MM_CUDA(ctx, cudaMemcpyAsync(lcom_ck, ctx->ck.p, 8 * C, cudaMemcpyDeviceToHost, ctx->stream));
     if (C && cbo) MM_CUDA(ctx, cudaMemcpyAsync(cbo, ctx->cbo.p, 4 * C, cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+mm_status mm_class_metrics_async(mm_ctx* ctx, double* lcom, uint64_t* lcom_ck, uint32_t* cbo) {
+    if (!ctx) return MM_E_ARG;
+    if (mm_status st = ensure_metrics(ctx)) return st;
+    const size_t C = ctx->C;
+    MM_CUDA(ctx, cudaEventRecord(ctx->ev_d2h_go, ctx->stream));
+    MM_CUDA(ctx, cudaStreamWaitEvent(ctx->d2h, ctx->ev_d2h_go, 0));
+    if (C && lcom) MM_CUDA(ctx, cudaMemcpyAsync(lcom, ctx->lcom.p, 8 * C, cudaMemcpyDeviceToHost, ctx->d2h));
+    if (C && lcom_ck) MM_CUDA(ctx, cudaMemcpyAsync(lcom_ck, ctx->ck.p, 8 * C, cudaMemcpyDeviceToHost, ctx->d2h));
+    if (C && cbo) MM_CUDA(ctx, cudaMemcpyAsync(cbo, ctx->cbo.p, 4 * C, cudaMemcpyDeviceToHost, ctx->d2h));
+    MM_CUDA(ctx, cudaEventRecord(ctx->ev_d2h_done, ctx->d2h));
     return MM_OK;
 }
 

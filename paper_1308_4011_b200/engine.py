@@ -196,6 +196,18 @@ class Engine:
             return lcom.copy(), ck.copy(), cbo.copy()
         return lcom, ck, cbo
 
+    def class_metrics_async(self):
+        """Enqueue the D2H of (lcom, lcom_ck, cbo) into the pinned staging
+        buffers behind the work already launched; it overlaps what is launched
+        next. The returned views hold the results after synchronize()."""
+        n = self.system.n_classes
+        lcom = self._staging("lcom", np.float64, n)
+        ck = self._staging("ck", np.uint64, n)
+        cbo = self._staging("cbo", np.uint32, n)
+        self._check(lib().mm_class_metrics_async(self._ctx, lcom.ctypes.data, ck.ctypes.data, cbo.ctypes.data),
+                    "mm_class_metrics_async")
+        return lcom, ck, cbo
+
     def parallel_class_metrics(self, n_workers: int = 1) -> ClassMetrics:
         if n_workers == 0:
             raise MMArgError(abi.MM_E_ARG, "plan_partition: zero workers")  # parallel.hpp:29

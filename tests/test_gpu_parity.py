@@ -327,3 +327,17 @@ def test_gpu_upload_without_owner_tables(gpu_engine):
     bad.class_methods[-1] = 0  # method 2 unlisted, method 0 listed twice
     with pytest.raises(MMArgError):
         gpu_engine.upload(bad, owner_tables=False)
+
+
+def test_gpu_class_metrics_async(gpu_engine):
+    # enqueued D2H under the sweep: same values once synchronized; the next
+    # metric pass waits for the copies
+    s = System.generate(seed=41, n_classes=2000, n_methods=25000, n_attributes=30000)
+    gpu_engine.upload(s, owner_tables=False)
+    gpu_engine.compute_metrics()
+    lcom, ck, cbo = gpu_engine.class_metrics_async()
+    gpu_engine.sweep(thresholds=None, want_count=False)
+    gpu_engine.compute_metrics()
+    gpu_engine.synchronize()
+    got = (lcom.copy(), ck.copy(), cbo.copy())
+    assert_metrics_equal(got, oracle.class_metrics(s), "async")
