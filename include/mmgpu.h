@@ -210,6 +210,11 @@ mm_status mm_class_metrics(mm_ctx* ctx, double* lcom, uint64_t* lcom_ck, uint32_
  * buffers (pinned, for a truly asynchronous copy) hold the results after
  * mm_ctx_synchronize; the next metric pass waits for the copies. */
 mm_status mm_class_metrics_async(mm_ctx* ctx, double* lcom, uint64_t* lcom_ck, uint32_t* cbo);
+/* Per-method fan metrics (either pointer may be NULL), MetricsReport::fan_in
+ * / fan_out: fan_in[p] = number of call lists containing p (metrics.hpp:79-85,
+ * = parallel_fan_metrics' fan_in for a validated model, parallel.hpp:186-206),
+ * fan_out[p] = |calls(p)| (metrics.hpp:87-93). */
+mm_status mm_fan_metrics(mm_ctx* ctx, uint32_t* fan_in, uint32_t* fan_out);
 /* Single-class accessors with the reference's error behaviour
  * (out_of_range on a bad id, metrics.hpp:97-100). */
 mm_status mm_lcom_normalized(mm_ctx* ctx, uint32_t cls, double* out);

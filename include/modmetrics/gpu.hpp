@@ -11,6 +11,8 @@
 //   reference (namespace modmetrics)          here (namespace modmetrics::gpu)
 //   parallel_class_metrics  parallel.hpp:149  parallel_class_metrics / Engine::
 //   parallel_lcom_ck        parallel.hpp:164  parallel_lcom_ck / Engine::
+//   fan_in / fan_out        metrics.hpp:79-93 fan_in / fan_out
+//   parallel_fan_metrics    parallel.hpp:186  parallel_fan_metrics / Engine::
 //   lcom_normalized/lcom_ck/cbo metrics.hpp:128,159,187   Engine::
 //   compute_thresholds      suggest.hpp:46    (use the reference's own: host arithmetic on the report)
 //   what_if_move            suggest.hpp:87    what_if_move / Engine::
@@ -139,6 +141,17 @@ public:
         const detail::Csr csr(model, deps);
         detail::check(mm_upload(ctx_.get(), &csr.sys), ctx_.get(), "mm_upload");
         n_classes_ = csr.sys.n_classes;
+        n_methods_ = csr.sys.n_methods;
+    }
+
+    FanMetrics parallel_fan_metrics(unsigned n_workers = 1) {
+        if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");  // parallel.hpp:29
+        FanMetrics out;
+        out.fan_in.resize(n_methods_);
+        out.fan_out.resize(n_methods_);
+        detail::check(mm_fan_metrics(ctx_.get(), out.fan_in.data(), out.fan_out.data()), ctx_.get(),
+                      "parallel_fan_metrics");
+        return out;
     }
 
     ClassMetrics parallel_class_metrics(unsigned n_workers = 1) {
@@ -232,6 +245,7 @@ private:
     };
     std::unique_ptr<mm_ctx, Del> ctx_;
     uint32_t n_classes_ = 0;
+    uint32_t n_methods_ = 0;
 
     std::vector<MoveSuggestion> run(const MetricsReport& report, const Thresholds& t, uint32_t mask, bool inter,
                                     const SuggestOptions& opts) {
@@ -281,6 +295,21 @@ inline ClassMetrics parallel_class_metrics(const SystemModel& model, const Depen
     Engine e;
     e.upload(model, deps);
     return e.parallel_class_metrics(n_workers);
+}
+
+inline FanMetrics parallel_fan_metrics(const SystemModel& model, const DependencyTable& deps, unsigned n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");
+    Engine e;
+    e.upload(model, deps);
+    return e.parallel_fan_metrics(n_workers);
+}
+
+inline std::vector<std::uint32_t> fan_in(const SystemModel& model, const DependencyTable& deps) {
+    return gpu::parallel_fan_metrics(model, deps, 1u).fan_in;
+}
+
+inline std::vector<std::uint32_t> fan_out(const SystemModel& model, const DependencyTable& deps) {
+    return gpu::parallel_fan_metrics(model, deps, 1u).fan_out;
 }
 
 inline std::vector<std::uint64_t> parallel_lcom_ck(const SystemModel& model, const DependencyTable& deps,

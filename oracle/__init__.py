@@ -27,6 +27,7 @@ def oracle_lib():
         l = C.CDLL(str(ORACLE_SO))
         S = C.POINTER(abi.mm_system)
         l.or_class_metrics.argtypes = [S, C.c_void_p, C.c_void_p, C.c_void_p]
+        l.or_fan_metrics.argtypes = [S, C.c_void_p, C.c_void_p]
         l.or_thresholds.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
                                     C.POINTER(abi.mm_overrides), C.POINTER(abi.mm_thresholds)]
         l.or_what_if.argtypes = [S, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(abi.mm_whatif)]
@@ -54,6 +55,7 @@ def ref_lib():
         l.ref_model_view.argtypes = [C.c_void_p]
         l.ref_model_view.restype = S
         l.ref_class_metrics.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p, C.c_void_p]
+        l.ref_fan_metrics.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p]
         l.ref_single_metric.argtypes = [C.c_void_p, C.c_int, C.c_uint32, C.POINTER(C.c_double),
                                         C.POINTER(C.c_uint64)]
         l.ref_thresholds.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
@@ -90,6 +92,13 @@ def _params(criteria_mask, combine=0, all_candidates=False, top_k=1, thr_lcom=0.
 
 
 # ---- oracle (C restatement) ----------------------------------------------
+
+def fan_metrics(sys_: System):
+    s = sys_.as_c()
+    fi, fo = np.empty(sys_.n_methods, np.uint32), np.empty(sys_.n_methods, np.uint32)
+    oracle_lib().or_fan_metrics(C.byref(s), fi.ctypes.data, fo.ctypes.data)
+    return fi, fo
+
 
 def class_metrics(sys_: System):
     s = sys_.as_c()
@@ -140,7 +149,9 @@ class RefModel:
     def __init__(self, sys_: System = None, handle=None):
         self._keep = sys_
         self.h = handle if handle is not None else ref_lib().ref_model_create(C.byref(sys_.as_c()))
-        self.n_classes = ref_lib().ref_model_view(self.h).contents.n_classes if handle is not None else sys_.n_classes
+        view = ref_lib().ref_model_view(self.h).contents if handle is not None else None
+        self.n_classes = view.n_classes if view is not None else sys_.n_classes
+        self.n_methods = view.n_methods if view is not None else sys_.n_methods
 
     def close(self):
         if self.h:
@@ -155,6 +166,14 @@ class RefModel:
 
     def validate(self) -> int:
         return ref_lib().ref_validate(self.h)
+
+    def fan_metrics(self, n_workers=0):
+        m = self.n_methods
+        fi, fo = np.empty(m, np.uint32), np.empty(m, np.uint32)
+        st = ref_lib().ref_fan_metrics(self.h, n_workers, fi.ctypes.data, fo.ctypes.data)
+        if st:
+            raise RuntimeError(f"ref_fan_metrics status {st}")
+        return fi, fo
 
     def class_metrics(self, n_workers=0):
         n = self.n_classes

@@ -129,6 +129,19 @@ uint32_t or_cbo_over(const mm_system* s, uint32_t cls, const uint32_t* methods, 
     return (uint32_t)u;
 }
 
+/* fan_in, metrics.hpp:79-85: for every call list, ++in[t] per target;
+ * fan_out, metrics.hpp:87-93: the call list's length */
+int or_fan_metrics(const mm_system* s, uint32_t* fan_in, uint32_t* fan_out) {
+    if (fan_in) {
+        for (uint32_t p = 0; p < s->n_methods; ++p) fan_in[p] = 0;
+        for (uint32_t q = 0; q < s->n_methods; ++q)
+            for (uint32_t e = s->call_off[q]; e < s->call_off[q + 1]; ++e) ++fan_in[s->call_tgt[e]];
+    }
+    if (fan_out)
+        for (uint32_t p = 0; p < s->n_methods; ++p) fan_out[p] = s->call_off[p + 1] - s->call_off[p];
+    return MM_OK;
+}
+
 /* full_report class loop, metrics.hpp:253-261 */
 int or_class_metrics(const mm_system* s, double* lcom, uint64_t* lcom_ck, uint32_t* cbo) {
     for (uint32_t c = 0; c < s->n_classes; ++c) {

@@ -171,6 +171,28 @@ void* ref_generate(const mm_gen_config* cfg) {
 
 const mm_system* ref_model_view(void* h) { return &static_cast<RefModel*>(h)->view; }
 
+// n_workers == 0: fan_in / fan_out (metrics.hpp:79-93); otherwise
+// parallel_fan_metrics (parallel.hpp:186-206).
+int ref_fan_metrics(void* h, unsigned n_workers, uint32_t* fan_in_out, uint32_t* fan_out_out) {
+    const RefModel* r = static_cast<RefModel*>(h);
+    try {
+        FanMetrics f;
+        if (n_workers == 0) {
+            f.fan_in = fan_in(r->model, r->deps);
+            f.fan_out = fan_out(r->model, r->deps);
+        } else {
+            f = parallel_fan_metrics(r->model, r->deps, n_workers);
+        }
+        for (size_t p = 0; p < f.fan_in.size(); ++p) {
+            if (fan_in_out) fan_in_out[p] = f.fan_in[p];
+            if (fan_out_out) fan_out_out[p] = f.fan_out[p];
+        }
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+    return MM_OK;
+}
+
 // n_workers == 0: sequential full_report class loop (metrics.hpp:253-261);
 // otherwise parallel_class_metrics + parallel_lcom_ck (parallel.hpp:149,164).
 int ref_class_metrics(void* h, unsigned n_workers, double* lcom, uint64_t* ck, uint32_t* cbo) {

@@ -69,6 +69,12 @@ static void check_system(const std::string& name, const SystemModel& model, cons
     }
     expect(gpu::parallel_class_metrics(model, deps, 2) == parallel_class_metrics(model, deps, 2),
            name + " free parallel_class_metrics");
+    for (unsigned w : {1u, 4u})
+        expect(e.parallel_fan_metrics(w) == parallel_fan_metrics(model, deps, w), name + " fan metrics");
+    expect(gpu::fan_in(model, deps) == fan_in(model, deps), name + " fan_in");
+    expect(gpu::fan_out(model, deps) == fan_out(model, deps), name + " fan_out");
+    same_outcome([&] { return parallel_fan_metrics(model, deps, 0); },
+                 [&] { return gpu::parallel_fan_metrics(model, deps, 0); }, name + " fan zero workers");
     const ClassId C = static_cast<ClassId>(model.class_count());
     for (ClassId c = 0; c < C + 2; ++c) {
         same_outcome([&] { return lcom_normalized(c, model, deps); }, [&] { return e.lcom_normalized(c); },

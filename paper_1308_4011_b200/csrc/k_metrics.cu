@@ -73,6 +73,18 @@ __global__ void k_plan_methods(DevModel s, const uint32_t* __restrict__ pos_owne
     atomicMax(cmaxdeg + c, (ce - cb) + (ae - ab));
 }
 
+// fan_out[p] = |calls(p)| (metrics.hpp:87-93); fan_in[t] += 1 per call-list
+// occurrence of t (metrics.hpp:79-85) — integer atomics, so the counts are
+// exact and order-free. Thread per method: its own row, then its targets.
+__global__ void k_fan(DevModel s, uint32_t* __restrict__ fan_in, uint32_t* __restrict__ fan_out) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= s.M) return;
+    const uint32_t cb = s.call_off[p], ce = s.call_off[p + 1];
+    if (fan_out) fan_out[p] = ce - cb;
+    if (fan_in)
+        for (uint32_t e = cb; e < ce; ++e) atomicAdd(fan_in + __ldg(s.call_tgt + e), 1u);
+}
+
 // Upload-time expansion of the membership lists, one warp per class (lanes
 // over the class's list positions, coalesced; no per-position searches):
 //   pos_owner[k]  = class of method position k (the class-order owner table
@@ -868,6 +880,11 @@ void launch_expand(const DevModel& s, uint32_t* mo_out, uint32_t* ao_out, uint32
     if (ao_out && s.A) cudaMemsetAsync(ao_out, 0xff, 4ull * s.A, st);
     const uint32_t blocks = std::min<uint32_t>((s.C + 7) / 8, 148 * 8);
     k_expand<<<blocks, 256, 0, st>>>(s, mo_out, ao_out, pos_owner, info);
+}
+void launch_fan(const DevModel& s, uint32_t* fan_in, uint32_t* fan_out, cudaStream_t st) {
+    if (!s.M) return;
+    if (fan_in) cudaMemsetAsync(fan_in, 0, 4ull * s.M, st);
+    k_fan<<<(s.M + 255) / 256, 256, 0, st>>>(s, fan_in, fan_out);
 }
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st) {
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((n1 + 255) / 256, 148 * 16);

@@ -130,6 +130,7 @@ struct mm_ctx {
     DBuf<MethRec> recs;
     DBuf<uint64_t> own_mask;
     DBuf<uint2> attr_info;
+    DBuf<uint32_t> fan;  // mm_fan_metrics: fan_in[m] then fan_out[m]
     DBuf<uint32_t> pos_owner;
     DBuf<uint4> res;
     DBuf<uint32_t> emit_list;
@@ -245,6 +246,7 @@ void free_model(mm_ctx* c) {
     c->recs.release();
     c->own_mask.release();
     c->attr_info.release();
+    c->fan.release();
     c->pos_owner.release();
     c->cplan.release();
     c->big_list.release();
@@ -755,6 +757,23 @@ mm_status mm_class_metrics(mm_ctx* ctx, double* lcom, uint64_t* lcom_ck, uint32_
     if (C && lcom) MM_CUDA(ctx, cudaMemcpyAsync(lcom, ctx->lcom.p, 8 * C, cudaMemcpyDeviceToHost, ctx->stream));
     if (C && lcom_ck) MM_CUDA(ctx, cudaMemcpyAsync(lcom_ck, ctx->ck.p, 8 * C, cudaMemcpyDeviceToHost, ctx->stream));
     if (C && cbo) MM_CUDA(ctx, cudaMemcpyAsync(cbo, ctx->cbo.p, 4 * C, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+mm_status mm_fan_metrics(mm_ctx* ctx, uint32_t* fan_in, uint32_t* fan_out) {
+    if (!ctx) return MM_E_ARG;
+    if (!ctx->have_model) return fail(ctx, MM_E_STATE, "mm_fan_metrics: no model uploaded");
+    if (mm_status st = set_device(ctx)) return st;
+    const size_t M = ctx->M;
+    if (!M) return MM_OK;
+    MM_CUDA(ctx, ctx->fan.ensure(2 * M));
+    mm_status st = run(ctx, "fan", [&] {
+        launch_fan(ctx->dev(), fan_in ? ctx->fan.p : nullptr, fan_out ? ctx->fan.p + M : nullptr, ctx->stream);
+    });
+    if (st) return st;
+    if (fan_in) MM_CUDA(ctx, cudaMemcpyAsync(fan_in, ctx->fan.p, 4 * M, cudaMemcpyDeviceToHost, ctx->stream));
+    if (fan_out) MM_CUDA(ctx, cudaMemcpyAsync(fan_out, ctx->fan.p + M, 4 * M, cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return MM_OK;
 }

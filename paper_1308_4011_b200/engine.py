@@ -196,6 +196,14 @@ class Engine:
             return lcom.copy(), ck.copy(), cbo.copy()
         return lcom, ck, cbo
 
+    def fan_metrics(self):
+        """(fan_in u32[m], fan_out u32[m]) — MetricsReport's fan fields
+        (metrics.hpp:79-93, parallel_fan_metrics parallel.hpp:186)."""
+        m = self.system.n_methods
+        fi, fo = np.empty(m, np.uint32), np.empty(m, np.uint32)
+        self._check(lib().mm_fan_metrics(self._ctx, fi.ctypes.data, fo.ctypes.data), "mm_fan_metrics")
+        return fi, fo
+
     def class_metrics_async(self):
         """Enqueue the D2H of (lcom, lcom_ck, cbo) into the pinned staging
         buffers behind the work already launched; it overlaps what is launched

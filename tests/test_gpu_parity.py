@@ -341,3 +341,16 @@ def test_gpu_class_metrics_async(gpu_engine):
     gpu_engine.synchronize()
     got = (lcom.copy(), ck.copy(), cbo.copy())
     assert_metrics_equal(got, oracle.class_metrics(s), "async")
+
+
+def test_gpu_fan_metrics(gpu_engine):
+    # MetricsReport::fan_in / fan_out (metrics.hpp:79-93) against the oracle,
+    # the golden systems through C4
+    systems = [golden_system(load_golden(n)) for n in golden_names()[:4]]
+    systems += [System.generate(**random_cfg(np.random.default_rng(900 + k), k)) for k in range(10)]
+    systems.append(System.generate(seed=1, n_classes=100000, n_methods=1000000, n_attributes=2000000))
+    for s in systems:
+        gpu_engine.upload(s)
+        fi, fo = gpu_engine.fan_metrics()
+        wi, wo = oracle.fan_metrics(s)
+        assert (fi == wi).all() and (fo == wo).all()

@@ -145,6 +145,10 @@ def test_oracle_matches_compiled_reference_random():
         l, k, c = oracle.class_metrics(s)
         l2, k2, c2 = R.class_metrics()
         assert l.tobytes() == l2.tobytes() and (k == k2).all() and (c == c2).all()
+        fi, fo = oracle.fan_metrics(s)
+        for w in (0, 3):  # fan_in/fan_out and parallel_fan_metrics
+            fi2, fo2 = R.fan_metrics(w)
+            assert (fi == fi2).all() and (fo == fo2).all()
         t = oracle.thresholds(l, c)
         for mask, comb, allc in ((COH | COUP, 0, False), (COH | COUP, 1, True), (COH, 0, False), (COUP, 0, True)):
             a = oracle.suggest(s, l, c, mask, comb, allc, 1, t.lcom, t.cbo)
