@@ -215,6 +215,13 @@ mm_status mm_class_metrics_async(mm_ctx* ctx, double* lcom, uint64_t* lcom_ck, u
  * = parallel_fan_metrics' fan_in for a validated model, parallel.hpp:186-206),
  * fan_out[p] = |calls(p)| (metrics.hpp:87-93). */
 mm_status mm_fan_metrics(mm_ctx* ctx, uint32_t* fan_in, uint32_t* fan_out);
+/* WorkloadEstimate, metrics.hpp:195-233 (same fields and order): the largest
+ * call / access set from a device max-reduce, the closed forms of
+ * estimate_workload_counts on top. */
+typedef struct mm_workload {
+    uint64_t m, c, k_m, k_a, n_fan, n_sim, n_lcom, n_cbo, n_total;
+} mm_workload;
+mm_status mm_estimate_workload(mm_ctx* ctx, mm_workload* out);
 /* Single-class accessors with the reference's error behaviour
  * (out_of_range on a bad id, metrics.hpp:97-100). */
 mm_status mm_lcom_normalized(mm_ctx* ctx, uint32_t cls, double* out);

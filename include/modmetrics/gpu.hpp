@@ -13,6 +13,8 @@
 //   parallel_lcom_ck        parallel.hpp:164  parallel_lcom_ck / Engine::
 //   fan_in / fan_out        metrics.hpp:79-93 fan_in / fan_out
 //   parallel_fan_metrics    parallel.hpp:186  parallel_fan_metrics / Engine::
+//   estimate_workload       metrics.hpp:228   estimate_workload / Engine::
+//   full_report minus similarity              Engine::report_without_similarity
 //   lcom_normalized/lcom_ck/cbo metrics.hpp:128,159,187   Engine::
 //   compute_thresholds      suggest.hpp:46    (use the reference's own: host arithmetic on the report)
 //   what_if_move            suggest.hpp:87    what_if_move / Engine::
@@ -142,6 +144,31 @@ public:
         detail::check(mm_upload(ctx_.get(), &csr.sys), ctx_.get(), "mm_upload");
         n_classes_ = csr.sys.n_classes;
         n_methods_ = csr.sys.n_methods;
+    }
+
+    WorkloadEstimate estimate_workload() {
+        mm_workload w{};
+        detail::check(mm_estimate_workload(ctx_.get(), &w), ctx_.get(), "estimate_workload");
+        WorkloadEstimate e;
+        e.m = w.m; e.c = w.c; e.k_m = w.k_m; e.k_a = w.k_a;
+        e.n_fan = w.n_fan; e.n_sim = w.n_sim; e.n_lcom = w.n_lcom; e.n_cbo = w.n_cbo; e.n_total = w.n_total;
+        return e;
+    }
+
+    // full_report (metrics.hpp:249-264) with every field but `similarity`
+    // (left empty: the all-pairs table is outside this engine)
+    MetricsReport report_without_similarity() {
+        MetricsReport r;
+        FanMetrics f = parallel_fan_metrics();
+        r.fan_in = std::move(f.fan_in);
+        r.fan_out = std::move(f.fan_out);
+        r.lcom.resize(n_classes_);
+        r.lcom_ck.resize(n_classes_);
+        r.cbo.resize(n_classes_);
+        detail::check(mm_class_metrics(ctx_.get(), r.lcom.data(), r.lcom_ck.data(), r.cbo.data()), ctx_.get(),
+                      "report_without_similarity");
+        r.workload = estimate_workload();
+        return r;
     }
 
     FanMetrics parallel_fan_metrics(unsigned n_workers = 1) {
@@ -302,6 +329,12 @@ inline FanMetrics parallel_fan_metrics(const SystemModel& model, const Dependenc
     Engine e;
     e.upload(model, deps);
     return e.parallel_fan_metrics(n_workers);
+}
+
+inline WorkloadEstimate estimate_workload(const SystemModel& model, const DependencyTable& deps) {
+    Engine e;
+    e.upload(model, deps);
+    return e.estimate_workload();
 }
 
 inline std::vector<std::uint32_t> fan_in(const SystemModel& model, const DependencyTable& deps) {

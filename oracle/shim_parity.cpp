@@ -72,6 +72,9 @@ static void check_system(const std::string& name, const SystemModel& model, cons
     for (unsigned w : {1u, 4u})
         expect(e.parallel_fan_metrics(w) == parallel_fan_metrics(model, deps, w), name + " fan metrics");
     expect(gpu::fan_in(model, deps) == fan_in(model, deps), name + " fan_in");
+    expect(gpu::estimate_workload(model, deps) == estimate_workload(model, deps), name + " estimate_workload");
+    expect(e.report_without_similarity() == report_without_similarity(model, deps),
+           name + " report without similarity");
     expect(gpu::fan_out(model, deps) == fan_out(model, deps), name + " fan_out");
     same_outcome([&] { return parallel_fan_metrics(model, deps, 0); },
                  [&] { return gpu::parallel_fan_metrics(model, deps, 0); }, name + " fan zero workers");

@@ -42,6 +42,11 @@ class mm_system(C.Structure):
     ]
 
 
+class mm_workload(C.Structure):
+    """WorkloadEstimate, metrics.hpp:195-207."""
+    _fields_ = [(f, C.c_uint64) for f in ("m", "c", "k_m", "k_a", "n_fan", "n_sim", "n_lcom", "n_cbo", "n_total")]
+
+
 class mm_whatif(C.Structure):
     _fields_ = [
         ("lcom_origin_before", C.c_double), ("lcom_origin_after", C.c_double),

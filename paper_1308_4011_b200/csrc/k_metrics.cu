@@ -76,13 +76,26 @@ __global__ void k_plan_methods(DevModel s, const uint32_t* __restrict__ pos_owne
 // fan_out[p] = |calls(p)| (metrics.hpp:87-93); fan_in[t] += 1 per call-list
 // occurrence of t (metrics.hpp:79-85) — integer atomics, so the counts are
 // exact and order-free. Thread per method: its own row, then its targets.
-__global__ void k_fan(DevModel s, uint32_t* __restrict__ fan_in, uint32_t* __restrict__ fan_out) {
+// Also the largest call and access sets (estimate_workload's k_m / k_a,
+// metrics.hpp:228-233): a warp max, then one atomic per warp.
+__global__ void k_fan(DevModel s, uint32_t* __restrict__ fan_in, uint32_t* __restrict__ fan_out,
+                      uint32_t* __restrict__ kmax) {
     const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= s.M) return;
-    const uint32_t cb = s.call_off[p], ce = s.call_off[p + 1];
-    if (fan_out) fan_out[p] = ce - cb;
-    if (fan_in)
-        for (uint32_t e = cb; e < ce; ++e) atomicAdd(fan_in + __ldg(s.call_tgt + e), 1u);
+    uint32_t nc = 0, na = 0;
+    if (p < s.M) {
+        const uint32_t cb = s.call_off[p], ce = s.call_off[p + 1];
+        nc = ce - cb;
+        na = s.acc_off[p + 1] - s.acc_off[p];
+        if (fan_out) fan_out[p] = nc;
+        if (fan_in)
+            for (uint32_t e = cb; e < ce; ++e) atomicAdd(fan_in + __ldg(s.call_tgt + e), 1u);
+    }
+    nc = __reduce_max_sync(0xffffffffu, nc);
+    na = __reduce_max_sync(0xffffffffu, na);
+    if ((threadIdx.x & 31) == 0 && kmax) {
+        atomicMax(kmax, nc);
+        atomicMax(kmax + 1, na);
+    }
 }
 
 // Upload-time expansion of the membership lists, one warp per class (lanes
@@ -881,10 +894,11 @@ void launch_expand(const DevModel& s, uint32_t* mo_out, uint32_t* ao_out, uint32
     const uint32_t blocks = std::min<uint32_t>((s.C + 7) / 8, 148 * 8);
     k_expand<<<blocks, 256, 0, st>>>(s, mo_out, ao_out, pos_owner, info);
 }
-void launch_fan(const DevModel& s, uint32_t* fan_in, uint32_t* fan_out, cudaStream_t st) {
+void launch_fan(const DevModel& s, uint32_t* fan_in, uint32_t* fan_out, uint32_t* kmax, cudaStream_t st) {
+    if (kmax) cudaMemsetAsync(kmax, 0, 8, st);
     if (!s.M) return;
     if (fan_in) cudaMemsetAsync(fan_in, 0, 4ull * s.M, st);
-    k_fan<<<(s.M + 255) / 256, 256, 0, st>>>(s, fan_in, fan_out);
+    k_fan<<<(s.M + 255) / 256, 256, 0, st>>>(s, fan_in, fan_out, kmax);
 }
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st) {
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((n1 + 255) / 256, 148 * 16);

@@ -769,12 +769,38 @@ mm_status mm_fan_metrics(mm_ctx* ctx, uint32_t* fan_in, uint32_t* fan_out) {
     if (!M) return MM_OK;
     MM_CUDA(ctx, ctx->fan.ensure(2 * M));
     mm_status st = run(ctx, "fan", [&] {
-        launch_fan(ctx->dev(), fan_in ? ctx->fan.p : nullptr, fan_out ? ctx->fan.p + M : nullptr, ctx->stream);
+        launch_fan(ctx->dev(), fan_in ? ctx->fan.p : nullptr, fan_out ? ctx->fan.p + M : nullptr, nullptr,
+                   ctx->stream);
     });
     if (st) return st;
     if (fan_in) MM_CUDA(ctx, cudaMemcpyAsync(fan_in, ctx->fan.p, 4 * M, cudaMemcpyDeviceToHost, ctx->stream));
     if (fan_out) MM_CUDA(ctx, cudaMemcpyAsync(fan_out, ctx->fan.p + M, 4 * M, cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+mm_status mm_estimate_workload(mm_ctx* ctx, mm_workload* out) {
+    if (!ctx || !out) return MM_E_ARG;
+    if (!ctx->have_model) return fail(ctx, MM_E_STATE, "mm_estimate_workload: no model uploaded");
+    if (mm_status st = set_device(ctx)) return st;
+    MM_CUDA(ctx, ctx->fan.ensure(2 * (size_t)ctx->M + 2));
+    uint32_t* kmax = ctx->fan.p + 2 * (size_t)ctx->M;
+    mm_status st = run(ctx, "fan", [&] { launch_fan(ctx->dev(), nullptr, nullptr, kmax, ctx->stream); });
+    if (st) return st;
+    uint32_t k[2] = {0, 0};
+    MM_CUDA(ctx, cudaMemcpyAsync(k, kmax, sizeof k, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    // estimate_workload_counts, metrics.hpp:211-226 (closed forms, exact in 64 bits)
+    const uint64_t m = ctx->M, c = ctx->C;
+    out->m = m;
+    out->c = c;
+    out->k_m = k[0];
+    out->k_a = k[1];
+    out->n_fan = 2 * m;
+    out->n_sim = m == 0 ? 0 : m * (m - 1) / 2;
+    out->n_lcom = c * (m + 1);
+    out->n_cbo = c * (m + 1);
+    out->n_total = out->n_fan + out->n_sim + out->n_lcom + out->n_cbo;
     return MM_OK;
 }
 

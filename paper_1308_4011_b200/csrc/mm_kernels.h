@@ -53,7 +53,7 @@ struct SweepArgs {
 void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t* bad, cudaStream_t st);
 void launch_expand(const DevModel& s, uint32_t* mo_out, uint32_t* ao_out, uint32_t* pos_owner, uint2* info,
                    cudaStream_t st);
-void launch_fan(const DevModel& s, uint32_t* fan_in, uint32_t* fan_out, cudaStream_t st);
+void launch_fan(const DevModel& s, uint32_t* fan_in, uint32_t* fan_out, uint32_t* kmax, cudaStream_t st);
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st);
 void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint32_t* large_list,
                          uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,

@@ -204,6 +204,12 @@ class Engine:
         self._check(lib().mm_fan_metrics(self._ctx, fi.ctypes.data, fo.ctypes.data), "mm_fan_metrics")
         return fi, fo
 
+    def estimate_workload(self) -> dict:
+        """WorkloadEstimate (metrics.hpp:195-233): k_m / k_a by a device max-reduce."""
+        w = abi.mm_workload()
+        self._check(lib().mm_estimate_workload(self._ctx, C.byref(w)), "mm_estimate_workload")
+        return {f: getattr(w, f) for f, _ in abi.mm_workload._fields_}
+
     def class_metrics_async(self):
         """Enqueue the D2H of (lcom, lcom_ck, cbo) into the pinned staging
         buffers behind the work already launched; it overlaps what is launched

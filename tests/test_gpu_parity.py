@@ -354,3 +354,20 @@ def test_gpu_fan_metrics(gpu_engine):
         fi, fo = gpu_engine.fan_metrics()
         wi, wo = oracle.fan_metrics(s)
         assert (fi == wi).all() and (fo == wo).all()
+
+
+def test_gpu_estimate_workload(gpu_engine):
+    # WorkloadEstimate (metrics.hpp:195-233): device max-reduce + closed forms
+    for s in (System.generate(seed=51, n_classes=300, n_methods=5000, n_attributes=7000, k_max_calls=7,
+                              k_max_accesses=3),
+              System.build([([], [])], [], []),
+              System.generate(seed=1, n_classes=100000, n_methods=1000000, n_attributes=2000000)):
+        gpu_engine.upload(s)
+        w = gpu_engine.estimate_workload()
+        m, c = s.n_methods, s.n_classes
+        k_m = int(np.diff(s.call_off).max()) if m else 0
+        k_a = int(np.diff(s.acc_off).max()) if m else 0
+        n_sim = m * (m - 1) // 2 if m else 0
+        want = dict(m=m, c=c, k_m=k_m, k_a=k_a, n_fan=2 * m, n_sim=n_sim, n_lcom=c * (m + 1), n_cbo=c * (m + 1),
+                    n_total=2 * m + n_sim + 2 * c * (m + 1))
+        assert w == want
