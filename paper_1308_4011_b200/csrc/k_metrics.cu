@@ -544,6 +544,44 @@ __device__ __forceinline__ void member_used(const DevModel& s, const MethRec* re
     }
 }
 
+// Phase 1 of a giant CTA-path class (≥ kGiantMembers members, histogram U
+// row, attribute bitmaps in global scratch) spread over many CTAs, one
+// member per thread: foreign used classes counted into the giant's global
+// histogram, own accesses into H and the attribute bitmaps. k_class_large
+// then starts from the histogram instead of walking 10k members itself.
+__global__ void __launch_bounds__(kGiantChunk)
+k_giant_p1(DevModel s, const uint32_t* __restrict__ large_list, const LargePlan* __restrict__ plan,
+           const uint2* __restrict__ items, const MethRec* __restrict__ recs, uint32_t* __restrict__ gcnt,
+           unsigned long long* __restrict__ gH, uint32_t* __restrict__ grows) {
+    __shared__ uint64_t red64[kGiantChunk / 32];
+    const uint2 it = items[blockIdx.x];  // (index into the large list, first member)
+    const uint32_t c = large_list[it.x];
+    const LargePlan pl = plan[it.x];
+    const uint32_t mb = s.cls_moff[c];
+    const uint32_t M = s.cls_moff[c + 1] - mb;
+    const uint32_t W = (M + 31) / 32;
+    uint32_t* hist = gcnt + (uint64_t)pl.pre_slot * s.C;
+    uint32_t* rows = grows + pl.rows_off;
+    const uint32_t i = it.y + threadIdx.x;
+    uint64_t hown = 0;
+    if (i < M) {
+        const uint32_t pos = mb + i;
+        const uint32_t p = s.cls_methods[pos];
+        member_used(s, recs, pos, p, [&](uint32_t X, uint32_t) {
+            if (X != c) atomicAdd(hist + X, 1u);
+        });
+        const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+        for (uint32_t e = ab; e < ae; ++e) {
+            const uint2 ai = __ldg(s.attr_info + __ldg(s.acc_tgt + e));
+            if (ai.x != c) continue;
+            ++hown;
+            atomicOr(rows + (uint64_t)ai.y * W + (i >> 5), 1u << (i & 31));
+        }
+    }
+    const uint64_t h = block_sum_u64(hown, red64);
+    if (threadIdx.x == 0 && h) atomicAdd(gH + pl.pre_slot, (unsigned long long)h);
+}
+
 // One CTA per class outside the warp path (Zipf giants, C5's 500-method
 // classes). Dynamic shared memory holds, when they fit (host plan): a
 // histogram over all C classes (cnt[X] = U[c][X]) or the foreign-class keys
@@ -557,7 +595,8 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
               double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
               uint32_t* __restrict__ ux, uint32_t* __restrict__ un, uint32_t* __restrict__ ucursor,
               uint32_t* __restrict__ gkeys, uint32_t* __restrict__ grows, uint32_t* __restrict__ dense,
-              uint32_t dense_cap, uint32_t* __restrict__ dense_cursor) {
+              uint32_t dense_cap, uint32_t* __restrict__ dense_cursor, const uint32_t* __restrict__ gcnt,
+              const unsigned long long* __restrict__ gH) {
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ uint64_t red64[kMaxWarps];
     __shared__ uint32_t red32[kMaxWarps];
@@ -588,13 +627,17 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     // (global-scratch bitmaps are cleared by one cudaMemsetAsync before the launch)
     if (pl.ck_masks || pl.rows_in_smem)
         for (uint64_t i = threadIdx.x; i < ck_words; i += blockDim.x) ckz[i] = 0;
-    if (pl.hist)
+    if (pl.hist && pl.pre_slot == kNone)
         for (uint32_t i = threadIdx.x; i < s.C; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
 
-    // phase 1: members' foreign used classes -> keys; H; own-attribute sets
+    // phase 1: members' foreign used classes -> keys; H; own-attribute sets.
+    // Giants had it done by k_giant_p1 over many CTAs: load their histogram.
+    const bool pre = pl.pre_slot != kNone;
+    if (pre)
+        for (uint32_t k = threadIdx.x; k < s.C; k += blockDim.x) cnt[k] = gcnt[(uint64_t)pl.pre_slot * s.C + k];
     uint64_t hown = 0;
-    for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) {
+    for (uint32_t i = pre ? M : threadIdx.x; i < M; i += blockDim.x) {
         const uint32_t pos = mb + i;
         const uint32_t p = s.cls_methods[pos];
         if (pl.hist)
@@ -621,7 +664,8 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
             else atomicOr(rows + (uint64_t)a * W + (i >> 5), 1u << (i & 31));
         }
     }
-    const uint64_t H = block_sum_u64(hown, red64);  // includes a __syncthreads
+    const uint64_t H = pre ? gH[pl.pre_slot] : block_sum_u64(hown, red64);  // (includes a __syncthreads)
+    if (pre) __syncthreads();
     const uint32_t dwords = (s.C + 31) / 32;
     uint32_t nx = 0, ubase = 0, nk = 0;
     if (pl.hist) {
@@ -934,11 +978,12 @@ void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* lar
                         uint32_t smem_bytes, MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
                         uint32_t* gkeys, uint32_t* grows, uint32_t* dense, uint32_t dense_cap,
-                        uint32_t* dense_cursor, uint32_t threads, cudaStream_t st) {
+                        uint32_t* dense_cursor, const uint32_t* gcnt, const unsigned long long* gH,
+                        uint32_t threads, cudaStream_t st) {
     if (!n_large) return;
     k_class_large<<<n_large, threads, smem_bytes, st>>>(s, large_list, plan, recs, own_mask, rec, lcom, ck, cbo, ux,
                                                               un, ucursor, gkeys, grows, dense, dense_cap,
-                                                              dense_cursor);
+                                                              dense_cursor, gcnt, gH);
 }
 void launch_ck_rows(const DevModel& s, const uint32_t* large_list, const LargePlan* plan, const uint2* items,
                     uint32_t n_items, const uint32_t* grows, const uint32_t* split_list, uint32_t n_split,
@@ -946,6 +991,12 @@ void launch_ck_rows(const DevModel& s, const uint32_t* large_list, const LargePl
     if (!n_items) return;
     k_ck_rows<<<n_items, kLargeThreads, 0, st>>>(s, large_list, plan, items, grows, ck);
     k_ck_finalize<<<(n_split + 127) / 128, 128, 0, st>>>(s, split_list, n_split, ck);
+}
+void launch_giant_p1(const DevModel& s, const uint32_t* large_list, const LargePlan* plan, const uint2* items,
+                     uint32_t n_items, const MethRec* recs, uint32_t* gcnt, unsigned long long* gH, uint32_t* grows,
+                     cudaStream_t st) {
+    if (!n_items) return;
+    k_giant_p1<<<n_items, kGiantChunk, 0, st>>>(s, large_list, plan, items, recs, gcnt, gH, grows);
 }
 cudaError_t set_class_large_smem(uint32_t bytes) {
     return cudaFuncSetAttribute(k_class_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);

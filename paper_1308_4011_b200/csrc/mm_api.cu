@@ -29,6 +29,7 @@ constexpr uint64_t kHistMaxBytes = 64 * 1024;
 constexpr int kMaxTiers = 8;  // CTA-path launch groups (shared-memory tier x CTA size)
 constexpr uint64_t kBigCtaMembers = 2048;  // classes this large launch 1024-thread CTAs
 constexpr int kUploadArrays = 10;
+constexpr uint32_t kNoSlot = 0xffffffffu;
 
 struct Ctl {  // small device-resident control block
     uint32_t bad;
@@ -109,14 +110,20 @@ struct mm_ctx {
         int key;           // 2 * shared-memory tier + (1024-thread CTAs)
         uint32_t threads;
         uint32_t item_first, n_items, split_first, n_split;  // split LCOM-CK work of this group
+        uint32_t giant_first, n_giant_items;                  // k_giant_p1 work of this group
     };
     std::vector<LargeGroup> large_groups;  // CTA-path launches, grouped by shared-memory need
     DBuf<uint32_t> dense;                  // exact U-row bitmaps of dense classes
     uint32_t dense_cap = 0;
     uint64_t hist_max_bytes = kHistMaxBytes;  // env MMGPU_HIST_MAX_BYTES (tuning / tests)
+    uint64_t giant_min = kGiantMembers;       // env MMGPU_GIANT_MIN (tuning / tests)
     DBuf<uint2> ck_items;                  // (large index, first member) chunks of split LCOM-CK classes
     DBuf<uint32_t> split_list;             // the split classes
     uint32_t n_ck_items = 0, n_split = 0;
+    DBuf<uint2> giant_items;           // k_giant_p1 CTAs
+    DBuf<uint32_t> gcnt;               // giants' foreign-class histograms (C words each)
+    DBuf<unsigned long long> gH;       // giants' H
+    uint32_t n_giant = 0;
     uint64_t grows_words = 0;              // global attribute-bitmap scratch in use
     DBuf<uint4> cplan;         // per class (first member position, M, A, kind)
     DBuf<uint32_t> big_list;   // kKindWarpBig classes
@@ -246,6 +253,9 @@ void free_model(mm_ctx* c) {
     c->recs.release();
     c->own_mask.release();
     c->attr_info.release();
+    c->giant_items.release();
+    c->gcnt.release();
+    c->gH.release();
     c->fan.release();
     c->pos_owner.release();
     c->cplan.release();
@@ -335,6 +345,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     }
     ctx->stream = ctx->own;
     if (const char* v = std::getenv("MMGPU_HIST_MAX_BYTES")) ctx->hist_max_bytes = std::strtoull(v, nullptr, 10);
+    if (const char* v = std::getenv("MMGPU_GIANT_MIN")) ctx->giant_min = std::strtoull(v, nullptr, 10);
     *out = ctx;
     return MM_OK;
 }
@@ -563,8 +574,13 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             }
             const uint64_t WA = (Ac + 63) / 64;
             const uint64_t mbytes = 8 * Mc * WA;
+            pl.pre_slot = kNoSlot;
             if (WA <= 4 && used + mbytes <= budget) { pl.ck_masks = 1; used += mbytes; }
-            else {
+            else if (pl.hist && Mc >= ctx->giant_min) {
+                // giant: phase 1 over many CTAs (k_giant_p1) into a global histogram;
+                // its attribute bitmaps live in global scratch (split LCOM-CK)
+                pl.pre_slot = 0;
+            } else {
                 const uint64_t rbytes = 4 * Ac * ((Mc + 31) / 32);
                 if (used + rbytes <= budget) { pl.rows_in_smem = 1; used += rbytes; }
             }
@@ -602,7 +618,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             if (!pl.ck_masks && !pl.rows_in_smem) { pl.rows_off = roff; roff += Ac * ((Mc + 31) / 32); }
             const uint32_t smem = (uint32_t)std::max<uint64_t>(16, (need[i] + 15) & ~15ull);
             if (ctx->large_groups.empty() || ctx->large_groups.back().key != gkey[i])
-                ctx->large_groups.push_back({j, 0, smem, gkey[i], (gkey[i] & 1) ? 1024u : 256u, 0, 0, 0, 0});
+                ctx->large_groups.push_back({j, 0, smem, gkey[i], (gkey[i] & 1) ? 1024u : 256u, 0, 0, 0, 0, 0, 0});
             auto& g = ctx->large_groups.back();
             ++g.count;
             g.smem = std::max(g.smem, smem);
@@ -610,9 +626,21 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         // classes whose attribute bitmaps live in global scratch: LCOM-CK split over kCkChunk-member chunks
         std::vector<uint2> items;
         std::vector<uint32_t> split;
+        std::vector<uint2> gitems;  // giants: (index into the large list, first member) per k_giant_p1 CTA
+        uint32_t n_giant = 0;
         for (auto& g : ctx->large_groups) {  // per group: its split classes' work follows it on its stream
             g.item_first = (uint32_t)items.size();
             g.split_first = (uint32_t)split.size();
+            g.giant_first = (uint32_t)gitems.size();
+            for (uint32_t j = g.first; j < g.first + g.count; ++j) {
+                LargePlan& pl = plans2[j];
+                if (pl.pre_slot == kNoSlot) continue;
+                pl.pre_slot = n_giant++;
+                const uint32_t c = list2[j];
+                const uint32_t Mc = s->class_method_off[c + 1] - s->class_method_off[c];
+                for (uint32_t b = 0; b < Mc; b += kGiantChunk) gitems.push_back(make_uint2(j, b));
+            }
+            g.n_giant_items = (uint32_t)gitems.size() - g.giant_first;
             for (uint32_t j = g.first; j < g.first + g.count; ++j) {
                 const LargePlan& pl = plans2[j];
                 if (pl.ck_masks || pl.rows_in_smem) continue;
@@ -626,6 +654,13 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         }
         ctx->n_ck_items = (uint32_t)items.size();
         ctx->n_split = (uint32_t)split.size();
+        ctx->n_giant = n_giant;
+        MM_CUDA(ctx, ctx->giant_items.ensure(gitems.size() ? gitems.size() : 1));
+        MM_CUDA(ctx, ctx->gcnt.ensure(n_giant ? (size_t)n_giant * C : 1));
+        MM_CUDA(ctx, ctx->gH.ensure(n_giant ? n_giant : 1));
+        if (!gitems.empty())
+            MM_CUDA(ctx, cudaMemcpy(ctx->giant_items.p, gitems.data(), sizeof(uint2) * gitems.size(),
+                                    cudaMemcpyHostToDevice));
         MM_CUDA(ctx, ctx->ck_items.ensure(items.size() ? items.size() : 1));
         MM_CUDA(ctx, ctx->split_list.ensure(split.size() ? split.size() : 1));
         if (!items.empty()) {
@@ -651,6 +686,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         ctx->large_groups.clear();
         ctx->dense_cap = 0;
         ctx->n_ck_items = ctx->n_split = 0;
+        ctx->n_giant = 0;
         ctx->grows_words = 0;
     }
     // derived tables
@@ -689,18 +725,28 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
     // tier first) and overlap each other and the warp path on the main stream
     st = run(ctx, "class_pass", [&] {
         if (ctx->grows_words) MM_CUDA(ctx, cudaMemsetAsync(ctx->grows.p, 0, 4ull * ctx->grows_words, ctx->stream));
+        if (ctx->n_giant) {
+            MM_CUDA(ctx, cudaMemsetAsync(ctx->gcnt.p, 0, 4ull * ctx->n_giant * ctx->C, ctx->stream));
+            MM_CUDA(ctx, cudaMemsetAsync(ctx->gH.p, 0, 8ull * ctx->n_giant, ctx->stream));
+        }
         const size_t ng = ctx->large_groups.size();
         if (ng) MM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
         for (size_t k = 0; k < ng; ++k) {
             const auto& g = ctx->large_groups[ng - 1 - k];
             cudaStream_t as = ctx->aux[k];
             MM_CUDA(ctx, cudaStreamWaitEvent(as, ctx->ev_fork, 0));
+            if (g.n_giant_items)
+                if (mm_status e = run_on(ctx, as, "giant_p1", [&] {
+                        launch_giant_p1(dm, ctx->large_list.p, ctx->plans.p, ctx->giant_items.p + g.giant_first,
+                                        g.n_giant_items, ctx->recs.p, ctx->gcnt.p, ctx->gH.p, ctx->grows.p, as);
+                    }))
+                    return e;
             if (mm_status e = run_on(ctx, as, "class_large", [&] {
                     launch_class_large(dm, g.count, ctx->large_list.p + g.first, ctx->plans.p + g.first, g.smem,
                                        ctx->recs.p, ctx->own_mask.p, ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p,
                                        ctx->ux.p, ctx->un.p, &ctl->ucursor, ctx->gkeys.p, ctx->grows.p,
                                        ctx->dense_cap ? ctx->dense.p : nullptr, ctx->dense_cap, &ctl->dense_cursor,
-                                       g.threads, as);
+                                       ctx->gcnt.p, ctx->gH.p, g.threads, as);
                 }))
                 return e;
             if (g.n_items)

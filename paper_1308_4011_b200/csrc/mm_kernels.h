@@ -10,6 +10,8 @@ namespace mmg {
 
 // Per large class (CTA path) scratch placement, planned on the host at upload.
 constexpr uint32_t kCkChunk = 64;  // members per k_ck_rows CTA (2 per warp: latency-bound chains)
+constexpr uint32_t kGiantMembers = 2048;  // histogram classes this large: phase 1 over many CTAs
+constexpr uint32_t kGiantChunk = 256;     // members (= threads) per k_giant_p1 CTA
 
 struct LargePlan {
     uint64_t keys_off;     // u32 element offset into the global key scratch
@@ -19,6 +21,7 @@ struct LargePlan {
     uint8_t rows_in_smem;
     uint8_t ck_masks;      // 1: per-member own-attribute masks (A ≤ 256) in smem; 0: attribute bitmaps
     uint8_t hist;          // 1: foreign classes counted in an smem histogram over all C (no keys)
+    uint32_t pre_slot;     // giants: slot of the global histogram / H that k_giant_p1 fills; else kNone
 };
 
 struct SweepArgs {
@@ -67,7 +70,11 @@ void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* lar
                         uint32_t smem_bytes, MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
                         uint32_t* gkeys, uint32_t* grows, uint32_t* dense, uint32_t dense_cap,
-                        uint32_t* dense_cursor, uint32_t threads, cudaStream_t st);
+                        uint32_t* dense_cursor, const uint32_t* gcnt, const unsigned long long* gH,
+                        uint32_t threads, cudaStream_t st);
+void launch_giant_p1(const DevModel& s, const uint32_t* large_list, const LargePlan* plan, const uint2* items,
+                     uint32_t n_items, const MethRec* recs, uint32_t* gcnt, unsigned long long* gH, uint32_t* grows,
+                     cudaStream_t st);
 cudaError_t set_class_large_smem(uint32_t bytes);
 void launch_ck_rows(const DevModel& s, const uint32_t* large_list, const LargePlan* plan, const uint2* items,
                     uint32_t n_items, const uint32_t* grows, const uint32_t* split_list, uint32_t n_split,

@@ -141,10 +141,15 @@ def test_gpu_large_class_paths(gpu_engine, monkeypatch):
     ]
     # CTA-path U rows come from an smem class histogram (4·C ≤ 64 KB, as here)
     # or from sorted keys (many classes); MMGPU_HIST_MAX_BYTES=0 forces the latter
-    monkeypatch.setenv("MMGPU_HIST_MAX_BYTES", "0")
+    # MMGPU_GIANT_MIN=64 sends every histogram class of ≥ 64 members with
+    # global attribute bitmaps through the multi-CTA giant phase 1
     from paper_1308_4011_b200 import Engine
-    with Engine(0) as keys_engine:
-        for e, tag in ((gpu_engine, "hist"), (keys_engine, "keys")):
+    monkeypatch.setenv("MMGPU_GIANT_MIN", "64")
+    giant_engine = Engine(0)
+    monkeypatch.delenv("MMGPU_GIANT_MIN")
+    monkeypatch.setenv("MMGPU_HIST_MAX_BYTES", "0")
+    with Engine(0) as keys_engine, giant_engine:
+        for e, tag in ((gpu_engine, "hist"), (keys_engine, "keys"), (giant_engine, "giant")):
             for cfg in cfgs:
                 s = System.generate(**cfg)
                 check_against_oracle(e, s, f"{tag} {cfg}", modes=((COH | COUP, 0, False), (COH | COUP, 0, True),
@@ -371,3 +376,29 @@ def test_gpu_estimate_workload(gpu_engine):
         want = dict(m=m, c=c, k_m=k_m, k_a=k_a, n_fan=2 * m, n_sim=n_sim, n_lcom=c * (m + 1), n_cbo=c * (m + 1),
                     n_total=2 * m + n_sim + 2 * c * (m + 1))
         assert w == want
+
+
+def test_gpu_giant_phase1_equals_single_cta(gpu_engine, monkeypatch):
+    # a Zipf system whose largest class (> 2048 members) takes the multi-CTA
+    # giant path by default: metrics against the oracle, every sweep mode
+    # against the single-CTA path (the oracle's recompute-based sweep needs
+    # minutes per mode on a 2k-member class)
+    from paper_1308_4011_b200 import Engine
+    s = System.generate(seed=16, n_classes=150, n_methods=12000, n_attributes=20000, k_max_calls=4,
+                        k_max_accesses=4, intra_class_bias=0.5, zipf_s=1.0)
+    assert np.diff(s.class_method_off).max() > 2048
+    monkeypatch.setenv("MMGPU_GIANT_MIN", str(1 << 30))
+    with Engine(0) as single:
+        single.upload(s)
+        gpu_engine.upload(s)
+        assert_metrics_equal(gpu_metrics(gpu_engine, s), oracle.class_metrics(s), "giant")
+        assert_metrics_equal(gpu_metrics(single, s), oracle.class_metrics(s), "single")
+        t = gpu_engine.compute_thresholds()
+        for crit in ([Criterion.Cohesion, Criterion.Coupling], [Criterion.Coupling]):
+            for comb in (Combine.Union, Combine.Intersection):
+                for allc in (False, True):
+                    a = gpu_engine.suggest_all(t, crit, comb, allc)
+                    b = single.suggest_all(t, crit, comb, allc)
+                    assert records_equal(a, b), (crit, comb, allc, first_diff(a, b))
+        for k in (2, 5):
+            assert records_equal(gpu_engine.suggest_all(t, top_k=k), single.suggest_all(t, top_k=k))
