@@ -9,8 +9,8 @@
 namespace mmg {
 
 // Per large class (CTA path) scratch placement, planned on the host at upload.
-constexpr uint32_t kCkChunk = 64;  // members per k_ck_rows CTA (2 per warp: latency-bound chains)
-constexpr uint32_t kGiantMembers = 2048;  // histogram classes this large: phase 1 over many CTAs
+constexpr uint32_t kCkChunk = 16;  // members per k_ck_rows CTA (2 per warp: latency-bound chains)
+constexpr uint32_t kGiantMembers = 512;  // histogram classes this large: phase 1 over many CTAs
 constexpr uint32_t kGiantChunk = 256;     // members (= threads) per k_giant_p1 CTA
 
 struct LargePlan {
