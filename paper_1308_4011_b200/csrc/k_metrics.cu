@@ -159,11 +159,52 @@ __global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg,
 // Each method's sorted used list with per-class access counts is packed into
 // its MethRec; the own-attribute mask has bit k for the k-th attribute of the
 // own class (classes with ≤ 64 attributes).
-template <int K>
+constexpr int kChunkBuckets = 8;  // k_method regrouping: 0..6 chunks, 7 = more or past the end
+
+template <int K, bool REGROUP>
 __global__ void __launch_bounds__(256, 5)
 k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask,
          const uint32_t* __restrict__ pos_owner) {
-    const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+    // Blocks holding methods of more than one chunk (dense shapes like C5)
+    // first regroup their positions by chunk count (a counting sort in shared
+    // memory), so a warp's threads loop the same number of chunks instead of
+    // all waiting for the warp's longest row. Writes stay inside the block's
+    // own position range (whole 32-byte records; L2 merges the masks).
+    __shared__ uint32_t s_cnt[kChunkBuckets], s_perm[256];
+    uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (REGROUP) {
+        const bool live = pos < s.M;
+        uint32_t nch = 0;
+        if (live) {
+            const uint32_t q = __ldg(s.cls_methods + pos);
+            const uint32_t d = (__ldg(s.call_off + q + 1) - __ldg(s.call_off + q)) +
+                               (__ldg(s.acc_off + q + 1) - __ldg(s.acc_off + q));
+            nch = (d + K - 1) / K;
+        }
+        if (threadIdx.x < kChunkBuckets) s_cnt[threadIdx.x] = 0;
+        if (__syncthreads_or(nch > 1)) {
+            const uint32_t b = live ? min(nch, (uint32_t)kChunkBuckets - 1) : kChunkBuckets - 1;
+            const int lane = threadIdx.x & 31;
+            const uint32_t grp = __match_any_sync(0xffffffffu, b);
+            const int lead = __ffs(grp) - 1;
+            uint32_t base = 0;
+            if (lane == lead) base = atomicAdd(&s_cnt[b], __popc(grp));
+            base = __shfl_sync(0xffffffffu, base, lead) + __popc(grp & ((1u << lane) - 1));
+            __syncthreads();
+            if (threadIdx.x == 0) {  // bucket starts (exclusive prefix)
+                uint32_t acc = 0;
+                for (int k = 0; k < kChunkBuckets; ++k) {
+                    const uint32_t c = s_cnt[k];
+                    s_cnt[k] = acc;
+                    acc += c;
+                }
+            }
+            __syncthreads();
+            s_perm[s_cnt[b] + base] = live ? pos : kNone;
+            __syncthreads();
+            pos = s_perm[threadIdx.x];
+        }
+    }
     if (pos >= s.M) return;
     const uint32_t p = __ldg(s.cls_methods + pos);
     const uint32_t own = __ldg(pos_owner + pos);
@@ -183,6 +224,7 @@ k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask
     UsedList<kRecMaxEnt + 1> L;
     L.clear();
     uint32_t hown = 0;
+    bool own_used = false;
     // masks feed LCOM-CK of every class with ≤ 64 attributes (both class paths)
     const bool small_attrs = oae - oab <= 64;
     auto chunk = [&](uint32_t e0) {
@@ -211,16 +253,22 @@ k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask
         for (int k = 0; k < K; ++k) {
             const uint32_t e = e0 + k;
             const bool isa = e >= nc && e < deg;
-            if (e < deg) L.insert(ow[k], isa ? 1u : 0u);
-            if (isa && ow[k] == own) {
-                if (small_attrs) mask |= 1ull << rk[k];
-                ++hown;
+            if (e >= deg) continue;
+            if (ow[k] == own) {  // own class: counted here, inserted once below (cheap for intra-class edges)
+                own_used = true;
+                if (isa) {
+                    if (small_attrs) mask |= 1ull << rk[k];
+                    ++hown;
+                }
+            } else {
+                L.insert(ow[k], isa ? 1u : 0u);
             }
         }
     };
     if (deg <= (uint32_t)K) chunk(0);  // the common case: one straight-line chunk
     else
         for (uint32_t e0 = 0; e0 < deg; e0 += K) chunk(e0);
+    if (own_used) L.insert(own, hown);
     bool fits = L.n <= kRecMaxEnt && hown < 256;
 #pragma unroll
     for (int k = 0; k < kRecMaxEnt; ++k)
@@ -959,10 +1007,13 @@ void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cp
                                                        n_big, max_deg);
 }
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
-                   cudaStream_t st) {
+                   uint32_t max_deg, cudaStream_t st) {
     if (!s.M) return;
     const uint32_t blocks = (s.M + 255) / 256;
-    k_method<8><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
+    if (max_deg > 8)  // some method needs several chunks: regroup by chunk count
+        k_method<8, true><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
+    else
+        k_method<8, false><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
 }
 void launch_class_small(const DevModel& s, const uint4* cplan, const uint32_t* big_list, uint32_t n_big,
                         MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck,

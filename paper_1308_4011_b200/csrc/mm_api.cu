@@ -718,7 +718,7 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
     MM_CUDA(ctx, cudaMemsetAsync(&ctl->ucursor, 0, 2 * sizeof(uint32_t), ctx->stream));  // ucursor, dense_cursor
     const DevModel dm = ctx->dev();
     mm_status st = run(ctx, "method", [&] {
-        launch_method(dm, ctx->recs.p, ctx->own_mask.p, ctx->pos_owner.p, ctx->stream);
+        launch_method(dm, ctx->recs.p, ctx->own_mask.p, ctx->pos_owner.p, ctx->max_deg, ctx->stream);
     });
     if (st) return st;
     // class pass: the CTA-path tiers fork onto their own streams (longest

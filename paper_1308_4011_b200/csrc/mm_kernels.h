@@ -62,7 +62,7 @@ void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cp
                          uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,
                          uint32_t* cmaxdeg, cudaStream_t st);
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
-                   cudaStream_t st);
+                   uint32_t max_deg, cudaStream_t st);
 void launch_class_small(const DevModel& s, const uint4* cplan, const uint32_t* big_list, uint32_t n_big,
                         MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck,
                         uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st, cudaStream_t st_big);
