@@ -840,7 +840,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     // over many CTAs by k_ck_rows instead (ck_out[c] accumulates Q there).
     const bool split = !pl.ck_masks && !pl.rows_in_smem;
     uint64_t q = 0;
-    if (split) {
+    if (split || pl.ck_mma) {  // another kernel owns this class's LCOM-CK
     } else if (pl.ck_masks) {
         // warp per row i, lanes over j > i: conflict-free consecutive mask
         // loads, no per-thread trip-count imbalance
@@ -889,7 +889,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         for (int w = 0; w < kSigWords; ++w) r.sig[w] = s_sig[w];
         rec[c] = r;
         lcom_out[c] = l;
-        ck_out[c] = split ? 0ull : (P > Q ? P - Q : 0);
+        if (!pl.ck_mma) ck_out[c] = split ? 0ull : (P > Q ? P - Q : 0);
         cbo_out[c] = nx;
     }
 }

@@ -30,6 +30,8 @@ constexpr int kMaxTiers = 8;  // CTA-path launch groups (shared-memory tier x CT
 constexpr uint64_t kBigCtaMembers = 2048;  // classes this large launch 1024-thread CTAs
 constexpr int kUploadArrays = 10;
 constexpr uint32_t kNoSlot = 0xffffffffu;
+constexpr uint64_t kCkMmaMin = 128;      // dense classes this large count LCOM-CK pairs with tcgen05 MMA
+constexpr uint64_t kCkMmaMaxMembers = 3328;  // operand rows × 64 B must fit shared memory
 
 struct Ctl {  // small device-resident control block
     uint32_t bad;
@@ -83,9 +85,9 @@ struct mm_ctx {
     cudaStream_t side = nullptr;       // threshold means run here, overlapping the candidate scoring
     cudaEvent_t ev_metrics = nullptr;  // class tables ready (main -> side)
     // CTA-path tiers run on their own streams, concurrently with the warp path
-    cudaStream_t aux[kMaxTiers + 1] = {};  // + the listed warp-path classes
+    cudaStream_t aux[kMaxTiers + 2] = {};  // + the listed warp-path classes, + tensor-core LCOM-CK
     cudaEvent_t ev_fork = nullptr;
-    cudaEvent_t ev_join[kMaxTiers + 1] = {};
+    cudaEvent_t ev_join[kMaxTiers + 2] = {};
     cudaEvent_t ev_up[kUploadArrays] = {};  // per-array copy done (upload validation overlaps the copies)
     cudaStream_t d2h = nullptr;             // mm_class_metrics_async copies
     cudaEvent_t ev_d2h_go = nullptr, ev_d2h_done = nullptr;
@@ -117,6 +119,9 @@ struct mm_ctx {
     uint32_t dense_cap = 0;
     uint64_t hist_max_bytes = kHistMaxBytes;  // env MMGPU_HIST_MAX_BYTES (tuning / tests)
     uint64_t giant_min = kGiantMembers;       // env MMGPU_GIANT_MIN (tuning / tests)
+    uint64_t ck_mma_min = kCkMmaMin;          // env MMGPU_CK_MMA_MIN: tensor-core LCOM-CK from this many members
+    DBuf<uint32_t> mma_list;                  // classes whose LCOM-CK runs on the tensor cores
+    uint32_t n_mma = 0, mma_smem = 0;
     DBuf<uint2> ck_items;                  // (large index, first member) chunks of split LCOM-CK classes
     DBuf<uint32_t> split_list;             // the split classes
     uint32_t n_ck_items = 0, n_split = 0;
@@ -254,6 +259,7 @@ void free_model(mm_ctx* c) {
     c->own_mask.release();
     c->attr_info.release();
     c->giant_items.release();
+    c->mma_list.release();
     c->gcnt.release();
     c->gH.release();
     c->fan.release();
@@ -325,7 +331,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
         mm_ctx_destroy(ctx);
         return MM_E_CUDA;
     }
-    for (int k = 0; k <= kMaxTiers; ++k)
+    for (int k = 0; k <= kMaxTiers + 1; ++k)
         if (cudaStreamCreateWithFlags(&ctx->aux[k], cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&ctx->ev_join[k], cudaEventDisableTiming) != cudaSuccess) {
             mm_ctx_destroy(ctx);
@@ -346,6 +352,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     ctx->stream = ctx->own;
     if (const char* v = std::getenv("MMGPU_HIST_MAX_BYTES")) ctx->hist_max_bytes = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_GIANT_MIN")) ctx->giant_min = std::strtoull(v, nullptr, 10);
+    if (const char* v = std::getenv("MMGPU_CK_MMA_MIN")) ctx->ck_mma_min = std::strtoull(v, nullptr, 10);
     *out = ctx;
     return MM_OK;
 }
@@ -377,7 +384,7 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     if (ctx->ev_metrics) cudaEventDestroy(ctx->ev_metrics);
     if (ctx->ev_thr) cudaEventDestroy(ctx->ev_thr);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    for (int k = 0; k <= kMaxTiers; ++k) {
+    for (int k = 0; k <= kMaxTiers + 1; ++k) {
         if (ctx->aux[k]) cudaStreamDestroy(ctx->aux[k]);
         if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
     }
@@ -575,7 +582,12 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             const uint64_t WA = (Ac + 63) / 64;
             const uint64_t mbytes = 8 * Mc * WA;
             pl.pre_slot = kNoSlot;
-            if (WA <= 4 && used + mbytes <= budget) { pl.ck_masks = 1; used += mbytes; }
+            if (WA <= 4 && used + mbytes <= budget) {
+                pl.ck_masks = 1;
+                used += mbytes;
+                // A ≤ 64: the method pass's masks are complete, B·Bᵀ on the tensor cores
+                pl.ck_mma = WA == 1 && Mc >= ctx->ck_mma_min && Mc <= kCkMmaMaxMembers;
+            }
             else if (pl.hist && Mc >= ctx->giant_min) {
                 // giant: phase 1 over many CTAs (k_giant_p1) into a global histogram;
                 // its attribute bitmaps live in global scratch (split LCOM-CK)
@@ -668,6 +680,20 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             MM_CUDA(ctx, cudaMemcpy(ctx->split_list.p, split.data(), 4 * split.size(), cudaMemcpyHostToDevice));
         }
         MM_CUDA(ctx, cudaMemcpy(ctx->large_list.p, list2.data(), 4ull * ctx->n_large, cudaMemcpyHostToDevice));
+        std::vector<uint32_t> mma;
+        uint32_t mma_max = 0;
+        for (uint32_t j = 0; j < ctx->n_large; ++j)
+            if (plans2[j].ck_mma) {
+                mma.push_back(list2[j]);
+                mma_max = std::max<uint32_t>(mma_max, s->class_method_off[list2[j] + 1] - s->class_method_off[list2[j]]);
+            }
+        ctx->n_mma = (uint32_t)mma.size();
+        MM_CUDA(ctx, ctx->mma_list.ensure(mma.size() ? mma.size() : 1));
+        if (!mma.empty()) {
+            MM_CUDA(ctx, cudaMemcpy(ctx->mma_list.p, mma.data(), 4 * mma.size(), cudaMemcpyHostToDevice));
+            ctx->mma_smem = ck_mma_smem_bytes(mma_max);
+            MM_CUDA(ctx, set_ck_mma_smem(ctx->mma_smem));
+        }
         MM_CUDA(ctx, ctx->plans.ensure(ctx->n_large));
         MM_CUDA(ctx, cudaMemcpy(ctx->plans.p, plans2.data(), sizeof(LargePlan) * ctx->n_large,
                                 cudaMemcpyHostToDevice));
@@ -687,6 +713,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         ctx->dense_cap = 0;
         ctx->n_ck_items = ctx->n_split = 0;
         ctx->n_giant = 0;
+        ctx->n_mma = 0;
         ctx->grows_words = 0;
     }
     // derived tables
@@ -760,9 +787,17 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
         }
         // warp-path classes with > 32 U-row keys: their own stream too
         cudaStream_t bs = ctx->aux[kMaxTiers];
-        if (ctx->n_big) {
-            if (!ng) MM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
-            MM_CUDA(ctx, cudaStreamWaitEvent(bs, ctx->ev_fork, 0));
+        if ((ctx->n_big || ctx->n_mma) && !ng) MM_CUDA(ctx, cudaEventRecord(ctx->ev_fork, ctx->stream));
+        if (ctx->n_big) MM_CUDA(ctx, cudaStreamWaitEvent(bs, ctx->ev_fork, 0));
+        // tensor-core LCOM-CK of the dense classes: needs only the method pass
+        cudaStream_t ms = ctx->aux[kMaxTiers + 1];
+        if (ctx->n_mma) {
+            MM_CUDA(ctx, cudaStreamWaitEvent(ms, ctx->ev_fork, 0));
+            if (mm_status e = run_on(ctx, ms, "ck_mma", [&] {
+                    launch_ck_mma(dm, ctx->mma_list.p, ctx->n_mma, ctx->mma_smem, ctx->own_mask.p, ctx->ck.p, ms);
+                }))
+                return e;
+            MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[kMaxTiers + 1], ms));
         }
         if (mm_status e = run(ctx, "class_small", [&] {
                 launch_class_small(dm, ctx->cplan.p, ctx->big_list.p, ctx->n_big, ctx->recs.p, ctx->own_mask.p,
@@ -774,6 +809,7 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
             MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[kMaxTiers], bs));
             MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[kMaxTiers], 0));
         }
+        if (ctx->n_mma) MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[kMaxTiers + 1], 0));
         for (size_t k = 0; k < ng; ++k) MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[k], 0));
         return MM_OK;
     });

@@ -22,6 +22,7 @@ struct LargePlan {
     uint8_t ck_masks;      // 1: per-member own-attribute masks (A ≤ 256) in smem; 0: attribute bitmaps
     uint8_t hist;          // 1: foreign classes counted in an smem histogram over all C (no keys)
     uint32_t pre_slot;     // giants: slot of the global histogram / H that k_giant_p1 fills; else kNone
+    uint32_t ck_mma;       // 1: LCOM-CK by k_ck_mma on the tensor cores (this kernel skips phase 4)
 };
 
 struct SweepArgs {
@@ -75,6 +76,11 @@ void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* lar
 void launch_giant_p1(const DevModel& s, const uint32_t* large_list, const LargePlan* plan, const uint2* items,
                      uint32_t n_items, const MethRec* recs, uint32_t* gcnt, unsigned long long* gH, uint32_t* grows,
                      cudaStream_t st);
+// LCOM-CK of listed dense classes (A ≤ 64) on the tensor cores (k_ck_mma.cu)
+uint32_t ck_mma_smem_bytes(uint32_t max_members);
+cudaError_t set_ck_mma_smem(uint32_t bytes);
+void launch_ck_mma(const DevModel& s, const uint32_t* list, uint32_t n, uint32_t smem_bytes,
+                   const uint64_t* own_mask, uint64_t* ck, cudaStream_t st);
 cudaError_t set_class_large_smem(uint32_t bytes);
 void launch_ck_rows(const DevModel& s, const uint32_t* large_list, const LargePlan* plan, const uint2* items,
                     uint32_t n_items, const uint32_t* grows, const uint32_t* split_list, uint32_t n_split,

@@ -147,9 +147,14 @@ def test_gpu_large_class_paths(gpu_engine, monkeypatch):
     monkeypatch.setenv("MMGPU_GIANT_MIN", "64")
     giant_engine = Engine(0)
     monkeypatch.delenv("MMGPU_GIANT_MIN")
+    # dense classes (A ≤ 64, ≥ 128 members) count LCOM-CK pairs with tcgen05
+    # MMA by default; MMGPU_CK_MMA_MIN past every class keeps the popc path
+    monkeypatch.setenv("MMGPU_CK_MMA_MIN", str(1 << 30))
+    popc_engine = Engine(0)
+    monkeypatch.delenv("MMGPU_CK_MMA_MIN")
     monkeypatch.setenv("MMGPU_HIST_MAX_BYTES", "0")
-    with Engine(0) as keys_engine, giant_engine:
-        for e, tag in ((gpu_engine, "hist"), (keys_engine, "keys"), (giant_engine, "giant")):
+    with Engine(0) as keys_engine, giant_engine, popc_engine:
+        for e, tag in ((gpu_engine, "hist"), (keys_engine, "keys"), (giant_engine, "giant"), (popc_engine, "popc")):
             for cfg in cfgs:
                 s = System.generate(**cfg)
                 check_against_oracle(e, s, f"{tag} {cfg}", modes=((COH | COUP, 0, False), (COH | COUP, 0, True),
