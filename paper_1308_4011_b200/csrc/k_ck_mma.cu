@@ -168,6 +168,9 @@ __global__ void __launch_bounds__(256) k_ck_mma(DevModel s, const uint32_t* __re
             const uint32_t jlim = min(kTile, M - J * kTile);  // valid columns of this tile
             uint32_t qt = 0;
             for (uint32_t c0 = half * (kTile / 2); c0 < (half + 1) * (kTile / 2); c0 += 32) {
+                // diagonal tile: columns left of this warp's rows lie below the diagonal
+                // (warp-uniform: the chunk is 32 columns, the rows 32 lanes)
+                if (I == J && c0 + 32 <= 32 * quarter) continue;
                 uint32_t v[32];
                 tmem_ld32(tmem + ((32u * quarter) << 16) + c0, v);
                 if (I != J && c0 + 32 <= jlim) {
