@@ -407,3 +407,66 @@ def test_gpu_giant_phase1_equals_single_cta(gpu_engine, monkeypatch):
                     assert records_equal(a, b), (crit, comb, allc, first_diff(a, b))
         for k in (2, 5):
             assert records_equal(gpu_engine.suggest_all(t, top_k=k), single.suggest_all(t, top_k=k))
+
+
+def boundary_system(rng, sizes, attrs, max_calls, max_accs, intra=0.7, shuffle=True):
+    """Classes of the given member / attribute counts (ids shuffled across
+    classes), dependencies drawn like the reference generator: each edge stays
+    in the own class with probability `intra`."""
+    n_m, n_a = int(sum(sizes)), int(sum(attrs))
+    mids = rng.permutation(n_m) if shuffle else np.arange(n_m)
+    aids = rng.permutation(n_a) if shuffle else np.arange(n_a)
+    classes, mo, ao = [], np.zeros(n_m, np.int64), np.zeros(n_a, np.int64)
+    mo_off = ao_off = 0
+    for c, (m, a) in enumerate(zip(sizes, attrs)):
+        ms, as_ = mids[mo_off:mo_off + m], aids[ao_off:ao_off + a]
+        mo[ms], ao[as_] = c, c
+        classes.append((as_.tolist(), ms.tolist()))
+        mo_off += m
+        ao_off += a
+    members = [np.array(cl[1]) for cl in classes]
+    owned = [np.array(cl[0]) for cl in classes]
+    calls, accs = [], []
+    for p in range(n_m):
+        c = mo[p]
+        cl, al = set(), set()
+        for _ in range(int(rng.integers(0, max_calls + 1))):
+            pool = members[c] if rng.random() < intra else members[int(rng.integers(0, len(sizes)))]
+            t = int(pool[rng.integers(0, len(pool))])
+            if t != p:
+                cl.add(t)
+        for _ in range(int(rng.integers(0, max_accs + 1))):
+            pool = owned[c] if (rng.random() < intra and len(owned[c])) else owned[int(rng.integers(0, len(sizes)))]
+            if len(pool):
+                al.add(int(pool[rng.integers(0, len(pool))]))
+        calls.append(sorted(cl))
+        accs.append(sorted(al))
+    return System.build(classes, calls, accs)
+
+
+def test_gpu_path_boundaries(gpu_engine):
+    # classes on both sides of every planning threshold: warp path limits
+    # (32 members, 64 attributes, degree 16, 32 foreign edges), the popc /
+    # tensor-core LCOM-CK cut (128 members), the giant cut (512), mask width
+    # (64 / 65 / 256 / 257 attributes) — metrics and the sweep against the oracle
+    rng = np.random.default_rng(2024)
+    cases = [
+        ([31, 32, 33, 1, 2, 40], [63, 64, 65, 1, 0, 10], 4, 12),
+        ([127, 128, 129, 5, 6], [64, 64, 64, 3, 3], 3, 16),
+        ([20, 20, 20, 20], [257, 256, 255, 8], 2, 18),
+        ([511, 512, 513, 3], [40, 300, 70, 2], 3, 6),
+        ([32] * 12, [64] * 12, 6, 10),
+    ]
+    for sizes, attrs, mc, ma in cases:
+        s = boundary_system(rng, sizes, attrs, mc, ma)
+        check_against_oracle(gpu_engine, s, f"sizes {sizes} attrs {attrs}",
+                             modes=((COH | COUP, 0, False), (COH | COUP, 0, True), (COH | COUP, 1, False)),
+                             top_ks=(1, 3))
+        for u in range(0, s.n_methods, 53):
+            o = int(s.method_owner[u])
+            for d in range(s.n_classes):
+                if d == o:
+                    continue
+                g = gpu_engine.what_if_move(u, o, d)
+                w = oracle.what_if(s, u, o, d)[1]
+                assert all(g[f] == getattr(w, f) for f in abi.WHATIF_FIELDS), (sizes, u, o, d)
