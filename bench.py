@@ -46,12 +46,16 @@ CONFIGS = {
                k_max_accesses=4, intra_class_bias=0.5),
     "c5": dict(seed=3, n_classes=5000, n_methods=2500000, n_attributes=320000, k_max_calls=4, k_max_accesses=32,
                intra_class_bias=0.9),
+    # C4 shape at 8x the size (size scaling of one GPU; not a SURVEY config)
+    "c4x8": dict(seed=1, n_classes=800000, n_methods=8000000, n_attributes=16000000, k_max_calls=4,
+                 k_max_accesses=4, intra_class_bias=0.5),
 }
 WORKLOAD_NAMES = {
     "c2": "C2 synthetic 1k classes / 10k methods / 20k attributes",
     "c3": "C3 synthetic Zipf(s=1) 10k classes / 100k methods / 200k attributes",
     "c4": "C4 synthetic 100k classes / 1M methods / 2M attributes (metric pass + cohesion/coupling sweep)",
     "c5": "C5 dense-coupling 5k classes x 500 methods / 320k attributes",
+    "c4x8": "C4 shape x8: 800k classes / 8M methods / 16M attributes",
 }
 METRIC = "move-method candidates scored/sec (full LCOM+CBO recompute + cohesion/coupling sweep per step)"
 UNIT = "candidates/s"

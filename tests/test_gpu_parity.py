@@ -470,3 +470,20 @@ def test_gpu_path_boundaries(gpu_engine):
                 g = gpu_engine.what_if_move(u, o, d)
                 w = oracle.what_if(s, u, o, d)[1]
                 assert all(g[f] == getattr(w, f) for f in abi.WHATIF_FIELDS), (sizes, u, o, d)
+
+
+def test_gpu_c4x8_metrics_and_sampled_sweep(gpu_engine):
+    # 800k classes / 8M methods: every class metric and both threshold means
+    # (the cooperative sequential-sum emulation over 391 tiles) against the
+    # oracle, the sweep on a 20k-class range of the full-system pass
+    s = System.generate(seed=1, n_classes=800000, n_methods=8000000, n_attributes=16000000)
+    gpu_engine.upload(s, owner_tables=False)
+    got = gpu_metrics(gpu_engine, s)
+    want = oracle.class_metrics(s)
+    assert_metrics_equal(got, want, "c4x8")
+    t_or = oracle.thresholds(want[0], want[2])
+    t = gpu_engine.compute_thresholds()
+    assert (t.lcom, t.cbo) == (t_or.lcom, t_or.cbo)
+    g = gpu_engine.suggest_all(t, class_range=(0, 20000))
+    o = oracle.suggest(s, want[0], want[2], COH | COUP, 0, False, 1, t.lcom, t.cbo, class_range=(0, 20000))
+    assert records_equal(g, o), first_diff(g, o)
