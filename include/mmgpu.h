@@ -243,6 +243,22 @@ mm_status mm_compute_thresholds(mm_ctx* ctx, const mm_overrides* ov, mm_threshol
  * Used for caller-built report vectors and to test the threshold kernel. */
 mm_status mm_sequential_mean(mm_ctx* ctx, const double* values, uint64_t n, double* out, int* fast_path);
 
+/* ---- similarity table (all_similarities, metrics.hpp:39-77) ----------- */
+/* SimilarityEntry, metrics.hpp:31-37 (same field order and types). */
+typedef struct mm_similarity {
+    uint32_t first;   /* first < second */
+    uint32_t second;
+    double value;     /* |shared properties| / |union|, the reference's single division */
+} mm_similarity;      /* 16 bytes */
+/* Every unordered method pair with a nonzero Jaccard similarity of their
+ * property sets (calls and accesses, the two id spaces kept apart), ordered
+ * by (first, second) — all_similarities / parallel_similarities
+ * (parallel.hpp:71-121). Two-call size query: out may be NULL; *n_out gets
+ * the count; MM_E_CAPACITY when cap is smaller. MM_E_UNSUPPORTED when one
+ * method's candidate list (Σ over its properties of their users) exceeds
+ * 4096 entries or it has more than 1024 properties. */
+mm_status mm_similarities(mm_ctx* ctx, mm_similarity* out, uint64_t cap, uint64_t* n_out);
+
 /* ---- what-if (what_if_move, suggest.hpp:87-122) ----------------------- */
 mm_status mm_what_if(mm_ctx* ctx, uint32_t method, uint32_t origin, uint32_t destination,
                      mm_whatif* out);

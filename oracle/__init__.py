@@ -28,6 +28,7 @@ def oracle_lib():
         S = C.POINTER(abi.mm_system)
         l.or_class_metrics.argtypes = [S, C.c_void_p, C.c_void_p, C.c_void_p]
         l.or_fan_metrics.argtypes = [S, C.c_void_p, C.c_void_p]
+        l.or_similarities.argtypes = [S, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
         l.or_thresholds.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
                                     C.POINTER(abi.mm_overrides), C.POINTER(abi.mm_thresholds)]
         l.or_what_if.argtypes = [S, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(abi.mm_whatif)]
@@ -56,6 +57,7 @@ def ref_lib():
         l.ref_model_view.restype = S
         l.ref_class_metrics.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p, C.c_void_p]
         l.ref_fan_metrics.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p]
+        l.ref_similarities.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
         l.ref_single_metric.argtypes = [C.c_void_p, C.c_int, C.c_uint32, C.POINTER(C.c_double),
                                         C.POINTER(C.c_uint64)]
         l.ref_thresholds.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
@@ -98,6 +100,16 @@ def fan_metrics(sys_: System):
     fi, fo = np.empty(sys_.n_methods, np.uint32), np.empty(sys_.n_methods, np.uint32)
     oracle_lib().or_fan_metrics(C.byref(s), fi.ctypes.data, fo.ctypes.data)
     return fi, fo
+
+
+def similarities(sys_: System):
+    s = sys_.as_c()
+    n = C.c_uint64()
+    oracle_lib().or_similarities(C.byref(s), None, 0, C.byref(n))
+    out = np.zeros(n.value, dtype=abi.SIMILARITY_DTYPE)
+    if n.value:
+        oracle_lib().or_similarities(C.byref(s), out.ctypes.data, n.value, C.byref(n))
+    return out
 
 
 def class_metrics(sys_: System):
@@ -166,6 +178,18 @@ class RefModel:
 
     def validate(self) -> int:
         return ref_lib().ref_validate(self.h)
+
+    def similarities(self, n_workers=0):
+        n = C.c_uint64()
+        st = ref_lib().ref_similarities(self.h, n_workers, None, 0, C.byref(n))
+        if st:
+            raise RuntimeError(f"ref_similarities status {st}")
+        out = np.zeros(n.value, dtype=abi.SIMILARITY_DTYPE)
+        if n.value:
+            st = ref_lib().ref_similarities(self.h, n_workers, out.ctypes.data, n.value, C.byref(n))
+        if st:
+            raise RuntimeError(f"ref_similarities status {st}")
+        return out
 
     def fan_metrics(self, n_workers=0):
         m = self.n_methods

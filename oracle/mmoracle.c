@@ -142,6 +142,45 @@ int or_fan_metrics(const mm_system* s, uint32_t* fan_in, uint32_t* fan_out) {
     return MM_OK;
 }
 
+/* |a ∩ b| of two sorted unique lists, detail::intersection_count (metrics.hpp:15-25) */
+static uint64_t isect(const uint32_t* a, uint32_t na, const uint32_t* b, uint32_t nb) {
+    uint64_t n = 0;
+    uint32_t i = 0, j = 0;
+    while (i < na && j < nb) {
+        if (a[i] < b[j]) ++i;
+        else if (b[j] < a[i]) ++j;
+        else { ++n; ++i; ++j; }
+    }
+    return n;
+}
+
+/* all_similarities, metrics.hpp:67-77 with similarity_if_nonzero (:47-55):
+ * inter = shared calls + shared accesses, uni = |P_i| + |P_j| - inter,
+ * value = (double)inter / (double)uni; pairs with inter == 0 not stored */
+int or_similarities(const mm_system* s, mm_similarity* out, uint64_t cap, uint64_t* n_out) {
+    uint64_t n = 0;
+    for (uint32_t i = 0; i < s->n_methods; ++i) {
+        const uint32_t ci = s->call_off[i], nci = s->call_off[i + 1] - ci;
+        const uint32_t ai = s->acc_off[i], nai = s->acc_off[i + 1] - ai;
+        for (uint32_t j = i + 1; j < s->n_methods; ++j) {
+            const uint32_t cj = s->call_off[j], ncj = s->call_off[j + 1] - cj;
+            const uint32_t aj = s->acc_off[j], naj = s->acc_off[j + 1] - aj;
+            const uint64_t inter = isect(s->call_tgt + ci, nci, s->call_tgt + cj, ncj) +
+                                   isect(s->acc_tgt + ai, nai, s->acc_tgt + aj, naj);
+            if (inter == 0) continue;
+            const uint64_t uni = (uint64_t)nci + nai + ncj + naj - inter;
+            if (out && n < cap) {
+                out[n].first = i;
+                out[n].second = j;
+                out[n].value = (double)inter / (double)uni;
+            }
+            ++n;
+        }
+    }
+    *n_out = n;
+    return (out && n > cap) ? MM_E_CAPACITY : MM_OK;
+}
+
 /* full_report class loop, metrics.hpp:253-261 */
 int or_class_metrics(const mm_system* s, double* lcom, uint64_t* lcom_ck, uint32_t* cbo) {
     for (uint32_t c = 0; c < s->n_classes; ++c) {

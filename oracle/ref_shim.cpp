@@ -171,6 +171,27 @@ void* ref_generate(const mm_gen_config* cfg) {
 
 const mm_system* ref_model_view(void* h) { return &static_cast<RefModel*>(h)->view; }
 
+// n_workers == 0: all_similarities (metrics.hpp:67-77); otherwise
+// parallel_similarities (parallel.hpp:71-121). Two-call size query.
+int ref_similarities(void* h, unsigned n_workers, mm_similarity* out, uint64_t cap, uint64_t* n_out) {
+    const RefModel* r = static_cast<RefModel*>(h);
+    try {
+        const std::vector<SimilarityEntry> v =
+            n_workers == 0 ? all_similarities(r->model, r->deps) : parallel_similarities(r->model, r->deps, n_workers);
+        *n_out = v.size();
+        if (!out) return MM_OK;
+        if (cap < v.size()) return MM_E_CAPACITY;
+        for (size_t k = 0; k < v.size(); ++k) {
+            out[k].first = v[k].first;
+            out[k].second = v[k].second;
+            out[k].value = v[k].value;
+        }
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+    return MM_OK;
+}
+
 // n_workers == 0: fan_in / fan_out (metrics.hpp:79-93); otherwise
 // parallel_fan_metrics (parallel.hpp:186-206).
 int ref_fan_metrics(void* h, unsigned n_workers, uint32_t* fan_in_out, uint32_t* fan_out_out) {

@@ -42,6 +42,14 @@ class mm_system(C.Structure):
     ]
 
 
+class mm_similarity(C.Structure):
+    """SimilarityEntry, metrics.hpp:31-37."""
+    _fields_ = [("first", C.c_uint32), ("second", C.c_uint32), ("value", C.c_double)]
+
+
+SIMILARITY_DTYPE = np.dtype([("first", np.uint32), ("second", np.uint32), ("value", np.float64)])
+
+
 class mm_workload(C.Structure):
     """WorkloadEstimate, metrics.hpp:195-207."""
     _fields_ = [(f, C.c_uint64) for f in ("m", "c", "k_m", "k_a", "n_fan", "n_sim", "n_lcom", "n_cbo", "n_total")]

@@ -143,6 +143,12 @@ struct mm_ctx {
     DBuf<uint64_t> own_mask;
     DBuf<uint2> attr_info;
     DBuf<uint32_t> fan;  // mm_fan_metrics: fan_in[m] then fan_out[m]
+    // similarity table: inverted indices, per-row counts / offsets, the pairs
+    DBuf<uint32_t> sim_u32;               // uc_off | uc | ua_off | ua | cursors | totals | row_cnt | row_off | wide
+    DBuf<unsigned long long> sim_ctl;     // [0] Σ pairs, [1] (n_wide, err, grand)
+    DBuf<mm_similarity> sim_out;
+    uint64_t sim_n = 0;
+    bool sim_valid = false;
     DBuf<uint32_t> pos_owner;
     DBuf<uint4> res;
     DBuf<uint32_t> emit_list;
@@ -263,6 +269,9 @@ void free_model(mm_ctx* c) {
     c->gcnt.release();
     c->gH.release();
     c->fan.release();
+    c->sim_u32.release();
+    c->sim_ctl.release();
+    c->sim_out.release();
     c->pos_owner.release();
     c->cplan.release();
     c->big_list.release();
@@ -455,6 +464,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     // device buffers are reused across uploads (grown on demand, never shrunk)
     ctx->have_model = ctx->metrics_valid = ctx->sweep_valid = false;
+    ctx->sim_valid = false;
     ctx->gates_set = false;
     ++ctx->layout_gen;
     if (!s->call_off || !s->acc_off || !s->class_method_off || !s->class_attr_off)
@@ -857,6 +867,63 @@ mm_status mm_fan_metrics(mm_ctx* ctx, uint32_t* fan_in, uint32_t* fan_out) {
     if (st) return st;
     if (fan_in) MM_CUDA(ctx, cudaMemcpyAsync(fan_in, ctx->fan.p, 4 * M, cudaMemcpyDeviceToHost, ctx->stream));
     if (fan_out) MM_CUDA(ctx, cudaMemcpyAsync(fan_out, ctx->fan.p + M, 4 * M, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+static mm_status compute_similarities(mm_ctx* ctx) {
+    const uint64_t M = ctx->M, A = ctx->A, Ec = ctx->Ec, Ea = ctx->Ea;
+    const uint64_t mx = std::max(M, A) + 1;
+    const uint64_t nb = (mx + 1023) / 1024 + 1;
+    // layout of the u32 scratch
+    const uint64_t o_ucoff = 0, o_uc = o_ucoff + M + 1, o_uaoff = o_uc + (Ec ? Ec : 1), o_ua = o_uaoff + A + 1,
+                   o_cur = o_ua + (Ea ? Ea : 1), o_tot = o_cur + mx, o_cnt = o_tot + nb, o_off = o_cnt + M + 1,
+                   o_wide = o_off + M + 1, o_end = o_wide + M + 1;
+    MM_CUDA(ctx, ctx->sim_u32.ensure(o_end));
+    MM_CUDA(ctx, ctx->sim_ctl.ensure(4));
+    uint32_t* u = ctx->sim_u32.p;
+    unsigned long long* ctl = ctx->sim_ctl.p;
+    uint32_t* small = reinterpret_cast<uint32_t*>(ctl + 1);  // n_wide, err, grand
+    MM_CUDA(ctx, cudaMemsetAsync(ctl, 0, 4 * sizeof(unsigned long long), ctx->stream));
+    const DevModel dm = ctx->dev();
+    mm_status st = run(ctx, "similarity", [&] {
+        launch_similarity_index(dm, Ec, Ea, u + o_ucoff, u + o_uc, u + o_uaoff, u + o_ua, u + o_cur, u + o_tot,
+                                small + 2, ctx->stream);
+        launch_similarity_rows(dm, 0, u + o_ucoff, u + o_uc, u + o_uaoff, u + o_ua, u + o_cnt, nullptr, nullptr,
+                               u + o_wide, small, small + 1, ctl, ctx->stream);
+    });
+    if (st) return st;
+    unsigned long long h[3] = {0, 0, 0};
+    MM_CUDA(ctx, cudaMemcpyAsync(h, ctl, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const uint32_t err = static_cast<uint32_t>(h[1] >> 32);
+    if (err & 2u)
+        return fail(ctx, MM_E_UNSUPPORTED, "mm_similarities: a method's candidate list exceeds 4096 entries");
+    if (h[0] >= (1ull << 32)) return fail(ctx, MM_E_UNSUPPORTED, "mm_similarities: more than 2^32 - 1 pairs");
+    ctx->sim_n = h[0];
+    MM_CUDA(ctx, ctx->sim_out.ensure(ctx->sim_n ? ctx->sim_n : 1));
+    st = run(ctx, "similarity", [&] {
+        launch_scan(u + o_cnt, u + o_off, static_cast<uint32_t>(M), u + o_tot, small + 2, ctx->stream);
+        launch_similarity_rows(dm, 1, u + o_ucoff, u + o_uc, u + o_uaoff, u + o_ua, u + o_cnt, u + o_off,
+                               ctx->sim_out.p, u + o_wide, small, small + 1, ctl, ctx->stream);
+    });
+    if (st) return st;
+    ctx->sim_valid = true;
+    return MM_OK;
+}
+
+mm_status mm_similarities(mm_ctx* ctx, mm_similarity* out, uint64_t cap, uint64_t* n_out) {
+    if (!ctx || !n_out) return MM_E_ARG;
+    if (!ctx->have_model) return fail(ctx, MM_E_STATE, "mm_similarities: no model uploaded");
+    if (mm_status st = set_device(ctx)) return st;
+    if (!ctx->sim_valid)
+        if (mm_status st = compute_similarities(ctx)) return st;
+    *n_out = ctx->sim_n;
+    if (!out) return MM_OK;
+    if (cap < ctx->sim_n) return fail(ctx, MM_E_CAPACITY, "mm_similarities: buffer too small");
+    if (ctx->sim_n)
+        MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->sim_out.p, sizeof(mm_similarity) * ctx->sim_n, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return MM_OK;
 }

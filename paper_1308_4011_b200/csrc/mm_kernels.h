@@ -81,6 +81,16 @@ uint32_t ck_mma_smem_bytes(uint32_t max_members);
 cudaError_t set_ck_mma_smem(uint32_t bytes);
 void launch_ck_mma(const DevModel& s, const uint32_t* list, uint32_t n, uint32_t smem_bytes,
                    const uint64_t* own_mask, uint64_t* ck, cudaStream_t st);
+// similarity table (k_similarity.cu)
+cudaError_t launch_similarity_index(const DevModel& s, uint64_t Ec, uint64_t Ea, uint32_t* uc_off, uint32_t* uc,
+                                    uint32_t* ua_off, uint32_t* ua, uint32_t* cur, uint32_t* totals,
+                                    uint32_t* grand, cudaStream_t st);
+cudaError_t launch_similarity_rows(const DevModel& s, int pass, const uint32_t* uc_off, const uint32_t* uc,
+                                   const uint32_t* ua_off, const uint32_t* ua, uint32_t* row_cnt,
+                                   const uint32_t* row_off, mm_similarity* out, uint32_t* wide_list, uint32_t* n_wide,
+                                   uint32_t* err, unsigned long long* total, cudaStream_t st);
+cudaError_t launch_scan(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* totals, uint32_t* grand,
+                        cudaStream_t st);
 cudaError_t set_class_large_smem(uint32_t bytes);
 void launch_ck_rows(const DevModel& s, const uint32_t* large_list, const LargePlan* plan, const uint2* items,
                     uint32_t n_items, const uint32_t* grows, const uint32_t* split_list, uint32_t n_split,

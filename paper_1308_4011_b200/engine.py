@@ -204,6 +204,16 @@ class Engine:
         self._check(lib().mm_fan_metrics(self._ctx, fi.ctypes.data, fo.ctypes.data), "mm_fan_metrics")
         return fi, fo
 
+    def similarities(self) -> np.ndarray:
+        """all_similarities (metrics.hpp:67-77): every pair with a nonzero
+        Jaccard similarity, ordered by (first, second), as SIMILARITY_DTYPE."""
+        n = C.c_uint64()
+        self._check(lib().mm_similarities(self._ctx, None, 0, C.byref(n)), "mm_similarities")
+        out = np.zeros(n.value, dtype=abi.SIMILARITY_DTYPE)
+        if n.value:
+            self._check(lib().mm_similarities(self._ctx, out.ctypes.data, n.value, C.byref(n)), "mm_similarities")
+        return out
+
     def estimate_workload(self) -> dict:
         """WorkloadEstimate (metrics.hpp:195-233): k_m / k_a by a device max-reduce."""
         w = abi.mm_workload()

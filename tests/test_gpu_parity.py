@@ -487,3 +487,28 @@ def test_gpu_c4x8_metrics_and_sampled_sweep(gpu_engine):
     g = gpu_engine.suggest_all(t, class_range=(0, 20000))
     o = oracle.suggest(s, want[0], want[2], COH | COUP, 0, False, 1, t.lcom, t.cbo, class_range=(0, 20000))
     assert records_equal(g, o), first_diff(g, o)
+
+
+def test_gpu_similarities(gpu_engine):
+    # all_similarities (metrics.hpp:39-77): pairs, order and every double
+    # against the oracle; the golden systems, random ones, a dense one whose
+    # rows take the wide kernel, and an empty system
+    systems = [golden_system(load_golden(n)) for n in golden_names()[:4]]
+    systems += [System.generate(**random_cfg(np.random.default_rng(500 + k), k)) for k in range(12)]
+    systems.append(System.generate(seed=9, n_classes=8, n_methods=1200, n_attributes=90, k_max_calls=6,
+                                   k_max_accesses=20, intra_class_bias=0.9))
+    systems.append(System.build([([], [])], [], []))
+    for s in systems:
+        gpu_engine.upload(s)
+        g = gpu_engine.similarities()
+        o = oracle.similarities(s)
+        assert g.tobytes() == o.tobytes(), (len(g), len(o))
+    # a 20k-method system against the compiled reference's parallel engine
+    s = System.generate(seed=1, n_classes=2000, n_methods=20000, n_attributes=40000)
+    gpu_engine.upload(s, owner_tables=False)
+    g = gpu_engine.similarities()
+    if oracle.ref_available():
+        o = oracle.RefModel(s).similarities(8)
+    else:
+        o = oracle.similarities(s)
+    assert g.tobytes() == o.tobytes()
