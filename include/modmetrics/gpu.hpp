@@ -14,7 +14,10 @@
 //   fan_in / fan_out        metrics.hpp:79-93 fan_in / fan_out
 //   parallel_fan_metrics    parallel.hpp:186  parallel_fan_metrics / Engine::
 //   estimate_workload       metrics.hpp:228   estimate_workload / Engine::
-//   full_report minus similarity              Engine::report_without_similarity
+//   all_similarities        metrics.hpp:67    all_similarities / Engine::similarities
+//   parallel_similarities   parallel.hpp:71   parallel_similarities
+//   full_report             metrics.hpp:249   full_report / Engine:: (every field on the GPU)
+//   parallel_full_report    parallel.hpp:210  parallel_full_report
 //   lcom_normalized/lcom_ck/cbo metrics.hpp:128,159,187   Engine::
 //   compute_thresholds      suggest.hpp:46    (use the reference's own: host arithmetic on the report)
 //   what_if_move            suggest.hpp:87    what_if_move / Engine::
@@ -168,6 +171,23 @@ public:
         detail::check(mm_class_metrics(ctx_.get(), r.lcom.data(), r.lcom_ck.data(), r.cbo.data()), ctx_.get(),
                       "report_without_similarity");
         r.workload = estimate_workload();
+        return r;
+    }
+
+    std::vector<SimilarityEntry> similarities() {
+        uint64_t n = 0;
+        detail::check(mm_similarities(ctx_.get(), nullptr, 0, &n), ctx_.get(), "all_similarities");
+        std::vector<mm_similarity> raw(n);
+        if (n) detail::check(mm_similarities(ctx_.get(), raw.data(), n, &n), ctx_.get(), "all_similarities");
+        std::vector<SimilarityEntry> out(n);
+        for (uint64_t k = 0; k < n; ++k) out[k] = SimilarityEntry{raw[k].first, raw[k].second, raw[k].value};
+        return out;
+    }
+
+    // full_report (metrics.hpp:249-264), every field computed on the device
+    MetricsReport full_report() {
+        MetricsReport r = report_without_similarity();
+        r.similarity = similarities();
         return r;
     }
 
@@ -329,6 +349,29 @@ inline FanMetrics parallel_fan_metrics(const SystemModel& model, const Dependenc
     Engine e;
     e.upload(model, deps);
     return e.parallel_fan_metrics(n_workers);
+}
+
+inline std::vector<SimilarityEntry> all_similarities(const SystemModel& model, const DependencyTable& deps) {
+    Engine e;
+    e.upload(model, deps);
+    return e.similarities();
+}
+
+inline std::vector<SimilarityEntry> parallel_similarities(const SystemModel& model, const DependencyTable& deps,
+                                                          unsigned n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");  // parallel.hpp:29
+    return gpu::all_similarities(model, deps);
+}
+
+inline MetricsReport full_report(const SystemModel& model, const DependencyTable& deps) {
+    Engine e;
+    e.upload(model, deps);
+    return e.full_report();
+}
+
+inline MetricsReport parallel_full_report(const SystemModel& model, const DependencyTable& deps, unsigned n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");
+    return gpu::full_report(model, deps);
 }
 
 inline WorkloadEstimate estimate_workload(const SystemModel& model, const DependencyTable& deps) {

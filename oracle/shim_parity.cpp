@@ -75,6 +75,12 @@ static void check_system(const std::string& name, const SystemModel& model, cons
     expect(gpu::estimate_workload(model, deps) == estimate_workload(model, deps), name + " estimate_workload");
     expect(e.report_without_similarity() == report_without_similarity(model, deps),
            name + " report without similarity");
+    if (model.method_count() <= 3000) {  // the reference's tables are O(m^2)
+        expect(e.full_report() == full_report(model, deps), name + " full_report");
+        expect(gpu::parallel_full_report(model, deps, 3) == parallel_full_report(model, deps, 3),
+               name + " parallel_full_report");
+        expect(gpu::all_similarities(model, deps) == all_similarities(model, deps), name + " all_similarities");
+    }
     expect(gpu::fan_out(model, deps) == fan_out(model, deps), name + " fan_out");
     same_outcome([&] { return parallel_fan_metrics(model, deps, 0); },
                  [&] { return gpu::parallel_fan_metrics(model, deps, 0); }, name + " fan zero workers");
