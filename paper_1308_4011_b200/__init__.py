@@ -4,14 +4,14 @@ The product is `libmmgpu.so` (hand-written sm_100a CUDA behind the C ABI in
 include/mmgpu.h). This package is its thin Python host layer: `System` (CSR
 snapshots), `Engine` (the reference API mirror) and the shard planner.
 """
-from .abi import SUGGESTION_DTYPE
+from .abi import SIMILARITY_DTYPE, SUGGESTION_DTYPE
 from ._lib import MMArgError, MMError, MMRangeError, lib, lib_path
-from .engine import (ClassMetrics, Combine, Criterion, Engine, ThresholdOverrides, Thresholds, parallel_class_metrics,
-                     parallel_lcom_ck, plan_shards, suggest_all, what_if_move)
+from .engine import (ClassMetrics, Combine, Criterion, Engine, ThresholdOverrides, Thresholds, all_similarities,
+                     full_report, parallel_class_metrics, parallel_lcom_ck, plan_shards, suggest_all, what_if_move)
 from .system import System
 
 __all__ = [
     "System", "Engine", "Criterion", "Combine", "Thresholds", "ThresholdOverrides", "ClassMetrics",
-    "MMError", "MMRangeError", "MMArgError", "SUGGESTION_DTYPE", "lib", "lib_path", "plan_shards",
-    "parallel_class_metrics", "parallel_lcom_ck", "suggest_all", "what_if_move",
+    "MMError", "MMRangeError", "MMArgError", "SUGGESTION_DTYPE", "SIMILARITY_DTYPE", "lib", "lib_path", "plan_shards",
+    "parallel_class_metrics", "parallel_lcom_ck", "suggest_all", "what_if_move", "all_similarities", "full_report",
 ]

@@ -214,6 +214,14 @@ class Engine:
             self._check(lib().mm_similarities(self._ctx, out.ctypes.data, n.value, C.byref(n)), "mm_similarities")
         return out
 
+    def full_report(self) -> dict:
+        """full_report (metrics.hpp:249-264), every field from the device:
+        fan_in, fan_out, similarity, lcom, lcom_ck, cbo, workload."""
+        fi, fo = self.fan_metrics()
+        lcom, ck, cbo = self.class_metrics_all()
+        return {"fan_in": fi, "fan_out": fo, "similarity": self.similarities(), "lcom": lcom, "lcom_ck": ck,
+                "cbo": cbo, "workload": self.estimate_workload()}
+
     def estimate_workload(self) -> dict:
         """WorkloadEstimate (metrics.hpp:195-233): k_m / k_a by a device max-reduce."""
         w = abi.mm_workload()
@@ -391,6 +399,18 @@ def parallel_lcom_ck(system: System, n_workers: int = 1, device: int = 0) -> np.
 def what_if_move(method: int, origin: int, destination: int, system: System, device: int = 0) -> dict:
     with Engine(device) as e:
         return e.upload(system).what_if_move(method, origin, destination)
+
+
+def all_similarities(system: System, device: int = 0) -> np.ndarray:
+    """all_similarities (metrics.hpp:67-77) as SIMILARITY_DTYPE records."""
+    with Engine(device) as e:
+        return e.upload(system).similarities()
+
+
+def full_report(system: System, device: int = 0) -> dict:
+    """full_report (metrics.hpp:249-264), every field from the device."""
+    with Engine(device) as e:
+        return e.upload(system).full_report()
 
 
 def suggest_all(system: System, thresholds: Thresholds, criteria: Sequence, combine: Combine = Combine.Union,

@@ -512,3 +512,21 @@ def test_gpu_similarities(gpu_engine):
     else:
         o = oracle.similarities(s)
     assert g.tobytes() == o.tobytes()
+
+
+def test_gpu_similarity_limits_and_full_report(gpu_engine):
+    # a method whose candidate list passes 4096 entries: MM_E_UNSUPPORTED, not
+    # a wrong table; the full report's fields agree with their own calls
+    n = 5000
+    s = System.build([(list(range(2)), list(range(n)))], [], [[0, 1]] * n)
+    gpu_engine.upload(s)
+    with pytest.raises(MMError) as ei:
+        gpu_engine.similarities()
+    assert ei.value.status == abi.MM_E_UNSUPPORTED
+    s = System.generate(seed=61, n_classes=50, n_methods=800, n_attributes=600, k_max_calls=5, k_max_accesses=5)
+    gpu_engine.upload(s)
+    r = gpu_engine.full_report()
+    assert r["similarity"].tobytes() == oracle.similarities(s).tobytes()
+    fi, fo = oracle.fan_metrics(s)
+    assert (r["fan_in"] == fi).all() and (r["fan_out"] == fo).all()
+    assert_metrics_equal((r["lcom"], r["lcom_ck"], r["cbo"]), oracle.class_metrics(s), "full_report")
