@@ -1237,14 +1237,27 @@ mm_status mm_sweep_device_result(mm_ctx* ctx, const void** dev_records, uint64_t
 
 mm_status mm_copy_suggestions(mm_ctx* ctx, mm_suggestion* out, uint64_t cap, uint64_t* n_out) {
     if (!ctx || !n_out) return MM_E_ARG;
-    mm_sweep_stats ss;
-    if (mm_status st = mm_sweep_stats_get(ctx, &ss)) return st;
-    *n_out = ss.suggestions;
-    if (!ss.suggestions) return MM_OK;
-    if (!out || cap < ss.suggestions) return fail(ctx, MM_E_CAPACITY, "output buffer too small");
-    MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->out.p, sizeof(mm_suggestion) * ss.suggestions, cudaMemcpyDeviceToHost,
-                                 ctx->stream));
+    if (!out || !cap) {  // size query
+        mm_sweep_stats ss;
+        if (mm_status st = mm_sweep_stats_get(ctx, &ss)) return st;
+        *n_out = ss.suggestions;
+        return (!out && !ss.suggestions) || !ss.suggestions ? MM_OK
+                                                            : fail(ctx, MM_E_CAPACITY, "output buffer too small");
+    }
+    if (!ctx->sweep_valid) return fail(ctx, MM_E_STATE, "no sweep has run");
+    // one round trip: the count and up to `cap` records travel together (a
+    // caller that sized `cap` from the previous sweep of the same system
+    // gets exactly its records); a larger count reports MM_E_CAPACITY
+    Ctl h{};
+    const uint64_t k = std::min<uint64_t>(cap, ctx->out.n);
+    MM_CUDA(ctx, cudaMemcpyAsync(&h, ctx->ctl.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    if (k) MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->out.p, sizeof(mm_suggestion) * k, cudaMemcpyDeviceToHost,
+                                        ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (h.err & 2u)
+        return fail(ctx, MM_E_UNSUPPORTED, "a method uses more than 32 classes (all/top-k mode limit)");
+    *n_out = h.stats[2];
+    if (h.stats[2] > cap) return fail(ctx, MM_E_CAPACITY, "output buffer too small");
     return MM_OK;
 }
 

@@ -353,12 +353,27 @@ class Engine:
     def suggestions(self, copy: bool = True) -> np.ndarray:
         """The last sweep's ordered records (D2H into a reusable pinned buffer;
         copy=False returns a view of it, valid until the next call)."""
+        # one round trip when the staging buffer already fits the list (the
+        # previous sweep's count), else size query + copy
         n = C.c_uint64()
-        lib().mm_copy_suggestions(self._ctx, None, 0, C.byref(n))
+        cap = getattr(self, "_sugg_cap", 0)
+        if cap:
+            buf = self._staging("sugg", abi.SUGGESTION_DTYPE, cap)
+            st = lib().mm_copy_suggestions(self._ctx, buf.ctypes.data, cap, C.byref(n))
+            if st == abi.MM_OK:
+                self._sugg_cap = max(int(n.value), 1)
+                out = buf[: n.value]
+                return out.copy() if copy else out
+            if st != abi.MM_E_CAPACITY:
+                self._check(st, "mm_copy_suggestions")
+        st = lib().mm_copy_suggestions(self._ctx, None, 0, C.byref(n))
+        if st not in (abi.MM_OK, abi.MM_E_CAPACITY):
+            self._check(st, "mm_copy_suggestions")
         out = self._staging("sugg", abi.SUGGESTION_DTYPE, n.value)
         if n.value:
             self._check(lib().mm_copy_suggestions(self._ctx, out.ctypes.data, n.value, C.byref(n)),
                         "mm_copy_suggestions")
+        self._sugg_cap = max(int(n.value), 1)
         return out.copy() if copy else out
 
     def suggest_all(self, thresholds: Thresholds, criteria: Sequence = (Criterion.Cohesion, Criterion.Coupling),
