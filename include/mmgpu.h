@@ -259,6 +259,17 @@ typedef struct mm_similarity {
  * 4096 entries or it has more than 1024 properties. */
 mm_status mm_similarities(mm_ctx* ctx, mm_similarity* out, uint64_t cap, uint64_t* n_out);
 
+/* suggest_by_similarity (suggest.hpp:200-232): pairs of `table` (the
+ * caller's report.similarity; NULL = the device table of mm_similarities)
+ * with value > thr and methods in different classes make both methods
+ * candidates, destinations = the partner's class + the owners of what the
+ * method calls; a move passes when both lcoms strictly drop, best by
+ * lcom_key (lowest destination on ties) or every passing one
+ * (all_candidates). Records carry MM_CRIT_SIMILARITY, ordered by method
+ * then destination (the reference's order). Two-call size query. */
+mm_status mm_suggest_similarity(mm_ctx* ctx, const mm_similarity* table, uint64_t n_table, double thr,
+                                uint32_t all_candidates, mm_suggestion* out, uint64_t cap, uint64_t* n_out);
+
 /* ---- what-if (what_if_move, suggest.hpp:87-122) ----------------------- */
 mm_status mm_what_if(mm_ctx* ctx, uint32_t method, uint32_t origin, uint32_t destination,
                      mm_whatif* out);

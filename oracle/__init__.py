@@ -58,6 +58,8 @@ def ref_lib():
         l.ref_class_metrics.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p, C.c_void_p]
         l.ref_fan_metrics.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p]
         l.ref_similarities.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        l.ref_suggest_full.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(abi.mm_sweep_params),
+                                       C.c_double, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
         l.ref_single_metric.argtypes = [C.c_void_p, C.c_int, C.c_uint32, C.POINTER(C.c_double),
                                         C.POINTER(C.c_uint64)]
         l.ref_thresholds.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
@@ -189,6 +191,23 @@ class RefModel:
             st = ref_lib().ref_similarities(self.h, n_workers, out.ctypes.data, n.value, C.byref(n))
         if st:
             raise RuntimeError(f"ref_similarities status {st}")
+        return out
+
+    def suggest_full(self, lcom_gate, cbo_gate, criteria_mask, combine=0, all_candidates=False, thr_sim=0.0,
+                     thr_lcom=0.0, thr_cbo=0.0):
+        """suggest_all with every criterion, the report's similarity = all_similarities."""
+        lg = np.ascontiguousarray(lcom_gate, np.float64)
+        cg = np.ascontiguousarray(cbo_gate, np.uint32)
+        p = _params(criteria_mask, combine, all_candidates, 1, thr_lcom, thr_cbo, None)
+        n = C.c_uint64()
+        st = ref_lib().ref_suggest_full(self.h, lg.ctypes.data, cg.ctypes.data, C.byref(p), thr_sim, None, 0,
+                                        C.byref(n))
+        out = np.zeros(n.value, dtype=abi.SUGGESTION_DTYPE)
+        if n.value:
+            st = ref_lib().ref_suggest_full(self.h, lg.ctypes.data, cg.ctypes.data, C.byref(p), thr_sim,
+                                            out.ctypes.data, n.value, C.byref(n))
+        if st:
+            raise RuntimeError(f"ref_suggest_full status {st}")
         return out
 
     def fan_metrics(self, n_workers=0):

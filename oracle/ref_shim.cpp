@@ -324,6 +324,37 @@ int ref_suggest(void* h, const double* lcom_gate, const uint32_t* cbo_gate,
     return MM_OK;
 }
 
+// suggest_all with the similarity criterion available: the report's
+// similarity table is the reference's all_similarities (O(m^2): small systems),
+// thresholds.similarity = thr_sim.
+int ref_suggest_full(void* h, const double* lcom_gate, const uint32_t* cbo_gate, const mm_sweep_params* p,
+                     double thr_sim, mm_suggestion* out, uint64_t cap, uint64_t* n_out) {
+    const RefModel* r = static_cast<RefModel*>(h);
+    MetricsReport rep;
+    rep.fan_in = fan_in(r->model, r->deps);
+    rep.fan_out = fan_out(r->model, r->deps);
+    rep.similarity = all_similarities(r->model, r->deps);
+    rep.lcom.assign(lcom_gate, lcom_gate + r->model.class_count());
+    rep.cbo.assign(cbo_gate, cbo_gate + r->model.class_count());
+    Thresholds t;
+    t.similarity = thr_sim;
+    t.lcom = p->thr_lcom;
+    t.cbo = p->thr_cbo;
+    SuggestOptions opts;
+    opts.all_candidates = p->all_candidates != 0;
+    std::vector<MoveSuggestion> s;
+    try {
+        s = suggest_all(r->model, r->deps, rep, t, criteria_of(p->criteria),
+                        p->combine == MM_COMBINE_INTERSECTION ? Combine::Intersection : Combine::Union, opts);
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+    *n_out = s.size();
+    if (!out || cap < s.size()) return s.empty() ? MM_OK : MM_E_CAPACITY;
+    for (size_t i = 0; i < s.size(); ++i) fill(out[i], s[i]);
+    return MM_OK;
+}
+
 // One criterion alone, in the reference's own emission order
 // (suggest_by_cohesion :239 / suggest_by_coupling :266).
 int ref_suggest_by(void* h, uint32_t crit, const double* lcom_gate, const uint32_t* cbo_gate,

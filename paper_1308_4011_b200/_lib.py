@@ -50,6 +50,8 @@ _SIGS = {
     "mm_class_metrics_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mm_fan_metrics": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "mm_similarities": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "mm_suggest_similarity": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_double, C.c_uint32, C.c_void_p,
+                                        C.c_uint64, C.c_void_p]),
     "mm_estimate_workload": (C.c_int, [C.c_void_p, C.c_void_p]),
     "mm_lcom_normalized": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_double)]),
     "mm_lcom_ck": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]),

@@ -634,6 +634,115 @@ __global__ void k_what_if(DevModel s, const ClassRec* __restrict__ rec, const ui
     *out = w;
 }
 
+// ---- the similarity criterion (suggest_by_similarity, suggest.hpp:200-232) ----
+// A stored pair above the threshold whose methods live in different classes
+// makes both methods candidates; each candidate's destinations are the other
+// method's class plus the owners of what it calls, and a move passes when it
+// strictly lowers both lcoms (lcom_improves, key lcom_key — the cohesion
+// test). lcom_dest_after < lcom_dest_before needs h_u(d)·M_d > H_d, so only
+// destinations that own an attribute u accesses can pass: the candidates are
+// the used-list entries with h > 0 that are a partner's class or a callee's.
+
+// partners: per method, the classes of its above-threshold partners
+__global__ void k_sim_partner_count(const mm_similarity* __restrict__ tab, uint64_t n, double thr,
+                                    const uint32_t* __restrict__ owner, uint32_t* __restrict__ cnt) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const mm_similarity e = tab[k];
+        if (!(e.value > thr) || owner[e.first] == owner[e.second]) continue;  // suggest.hpp:217-218
+        atomicAdd(cnt + e.first, 1u);
+        atomicAdd(cnt + e.second, 1u);
+    }
+}
+
+__global__ void k_sim_partner_fill(const mm_similarity* __restrict__ tab, uint64_t n, double thr,
+                                   const uint32_t* __restrict__ owner, uint32_t* __restrict__ cur,
+                                   uint32_t* __restrict__ part) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const mm_similarity e = tab[k];
+        const uint32_t of = owner[e.first], os = owner[e.second];
+        if (!(e.value > thr) || of == os) continue;
+        part[atomicAdd(cur + e.first, 1u)] = os;
+        part[atomicAdd(cur + e.second, 1u)] = of;
+    }
+}
+
+struct SimCrit {
+    const uint32_t* part_off;  // by method id
+    const uint32_t* part;
+    uint32_t* rec_cnt;         // pass 0: records per method id
+    const uint32_t* rec_off;   // pass 1: first record of each method id
+    uint32_t all_candidates;
+};
+
+// pass 0 counts each candidate method's records, pass 1 writes them (the
+// reference's order: methods ascending, destinations ascending)
+template <int K, int PASS>
+__global__ void __launch_bounds__(kSweepTile) k_sim_emit(SweepArgs a, SimCrit sc) {
+    __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
+    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
+    if (pos >= a.pos_end) return;
+    const uint32_t p = __ldg(a.s.cls_methods + pos);
+    const uint32_t pb = sc.part_off[p], pe = sc.part_off[p + 1];
+    if (pb == pe) return;  // no partner above the threshold
+    const uint32_t o = __ldg(a.pos_owner + pos);
+    SmemEnum ren{s_X + threadIdx.x, s_H + threadIdx.x, 0};
+    StreamEnum sen;
+    Origin org;
+    const bool smem = load_method<K>(a, (uint32_t)pos, p, o, ren, sen, org);
+    const uint32_t cb = __ldg(a.s.call_off + p), ce = __ldg(a.s.call_off + p + 1);
+    auto run = [&](const auto& en) {
+        uint32_t n = 0, best = kNone, best_h = 0;
+        double best_key = 0.0;
+        uint64_t at = PASS ? sc.rec_off[p] : 0;
+        auto emit_one = [&](uint32_t d, uint32_t hd) {
+            const Dest dv = eval_dest(a.rec, a.ux, a.dense, en, d, hd);
+            mm_suggestion r;
+            r.lcom_origin_before = org.lo_b;
+            r.lcom_origin_after = org.lo_a;
+            r.lcom_dest_before = dv.ld_b;
+            r.lcom_dest_after = dv.ld_a;
+            r.method = p;
+            r.origin = o;
+            r.destination = d;
+            r.cbo_origin_before = org.co_b;
+            r.cbo_origin_after = org.co_a;
+            r.cbo_dest_before = dv.cd_b;
+            r.cbo_dest_after = dv.cd_a;
+            r.criteria = (uint8_t)MM_CRIT_SIMILARITY;
+            r.origin_degenerate_after = org.odeg;
+            r.dest_degenerate_after = dv.ddeg;
+            r.pad = 0;
+            store_record(a.out + at, r);
+            ++at;
+        };
+        if (org.coh_ok)
+            en.each([&](int, uint32_t d, uint32_t hd) {
+                if (d == o || hd == 0) return;
+                bool cand = false;
+                for (uint32_t k = pb; k < pe && !cand; ++k) cand = __ldg(sc.part + k) == d;
+                for (uint32_t e = cb; e < ce && !cand; ++e) cand = __ldg(a.s.method_owner + __ldg(a.s.call_tgt + e)) == d;
+                if (!cand) return;
+                const ClassRec rd = load_rec(a.rec, d);
+                double ld_a;
+                if (!coh_dest(rd, hd, ld_a)) return;  // lcom_improves (suggest.hpp:189-192)
+                if (sc.all_candidates) {
+                    ++n;
+                    if (PASS) emit_one(d, hd);
+                    return;
+                }
+                const double key = __dadd_rn(org.lo_a, ld_a);  // lcom_key; d ascending, strict <
+                if (best == kNone || key < best_key) { best = d; best_h = hd; best_key = key; }
+            });
+        if (!sc.all_candidates && best != kNone) {
+            n = 1;
+            if (PASS) emit_one(best, best_h);
+        }
+        if (!PASS) sc.rec_cnt[p] = n;
+    };
+    if (smem) run(ren);
+    else run(sen);
+}
+
 }  // namespace
 
 void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
@@ -654,6 +763,32 @@ void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     const uint32_t grid = std::min<uint32_t>(n_tiles, 148 * 8);  // grid-stride over the emitter list
     if (a.maxdeg_fast <= 8) k_write<8><<<grid, kSweepTile, 0, st>>>(a);
     else k_write<16><<<grid, kSweepTile, 0, st>>>(a);
+}
+
+void launch_sim_partners(const mm_similarity* tab, uint64_t n, double thr, const uint32_t* owner, uint32_t M,
+                         uint32_t* cnt, uint32_t* off, uint32_t* cur, uint32_t* part, uint32_t* totals, uint32_t* grand,
+                         cudaStream_t st) {
+    cudaMemsetAsync(cnt, 0, 4ull * (M + 1), st);
+    const uint32_t grid = 148 * 8;
+    if (n) k_sim_partner_count<<<grid, 256, 0, st>>>(tab, n, thr, owner, cnt);
+    launch_scan(cnt, off, M + 1, totals, grand, st);
+    cudaMemcpyAsync(cur, off, 4ull * (M + 1), cudaMemcpyDeviceToDevice, st);
+    if (n) k_sim_partner_fill<<<grid, 256, 0, st>>>(tab, n, thr, owner, cur, part);
+}
+
+void launch_sim_emit(const SweepArgs& a, int pass, const uint32_t* part_off, const uint32_t* part, uint32_t* rec_cnt,
+                     const uint32_t* rec_off, uint32_t all_candidates, cudaStream_t st) {
+    const uint64_t npos = a.pos_end - a.pos_begin;
+    if (!npos) return;
+    const uint32_t n_tiles = (uint32_t)((npos + kSweepTile - 1) / kSweepTile);
+    const SimCrit sc{part_off, part, rec_cnt, rec_off, all_candidates};
+    if (a.maxdeg_fast <= 8) {
+        if (pass == 0) k_sim_emit<8, 0><<<n_tiles, kSweepTile, 0, st>>>(a, sc);
+        else k_sim_emit<8, 1><<<n_tiles, kSweepTile, 0, st>>>(a, sc);
+    } else {
+        if (pass == 0) k_sim_emit<16, 0><<<n_tiles, kSweepTile, 0, st>>>(a, sc);
+        else k_sim_emit<16, 1><<<n_tiles, kSweepTile, 0, st>>>(a, sc);
+    }
 }
 
 void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un,

@@ -147,6 +147,9 @@ struct mm_ctx {
     DBuf<uint32_t> sim_u32;               // uc_off | uc | ua_off | ua | cursors | totals | row_cnt | row_off | wide
     DBuf<unsigned long long> sim_ctl;     // [0] Σ pairs, [1] (n_wide, err, grand)
     DBuf<mm_similarity> sim_out;
+    DBuf<mm_similarity> sim_caller;       // a caller's table (mm_suggest_similarity)
+    DBuf<uint32_t> simc_u32;              // partner counts / offsets / cursors / classes, record counts / offsets
+    DBuf<mm_suggestion> simc_out;
     uint64_t sim_n = 0;
     bool sim_valid = false;
     DBuf<uint32_t> pos_owner;
@@ -272,6 +275,9 @@ void free_model(mm_ctx* c) {
     c->sim_u32.release();
     c->sim_ctl.release();
     c->sim_out.release();
+    c->sim_caller.release();
+    c->simc_u32.release();
+    c->simc_out.release();
     c->pos_owner.release();
     c->cplan.release();
     c->big_list.release();
@@ -924,6 +930,73 @@ mm_status mm_similarities(mm_ctx* ctx, mm_similarity* out, uint64_t cap, uint64_
     if (ctx->sim_n)
         MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->sim_out.p, sizeof(mm_similarity) * ctx->sim_n, cudaMemcpyDeviceToHost,
                                      ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return MM_OK;
+}
+
+mm_status mm_suggest_similarity(mm_ctx* ctx, const mm_similarity* table, uint64_t n_table, double thr,
+                                uint32_t all_candidates, mm_suggestion* out, uint64_t cap, uint64_t* n_out) {
+    if (!ctx || !n_out || (n_table && !table)) return MM_E_ARG;
+    if (mm_status st = ensure_metrics(ctx)) return st;
+    const uint64_t M = ctx->M;
+    // the pairs: the caller's report.similarity, else the device table
+    const mm_similarity* tab = nullptr;
+    uint64_t ntab = 0;
+    if (table) {
+        MM_CUDA(ctx, ctx->sim_caller.ensure(n_table ? n_table : 1));
+        if (n_table)
+            MM_CUDA(ctx, cudaMemcpyAsync(ctx->sim_caller.p, table, sizeof(mm_similarity) * n_table,
+                                         cudaMemcpyHostToDevice, ctx->stream));
+        tab = ctx->sim_caller.p;
+        ntab = n_table;
+    } else {
+        if (!ctx->sim_valid)
+            if (mm_status st = compute_similarities(ctx)) return st;
+        tab = ctx->sim_out.p;
+        ntab = ctx->sim_n;
+    }
+    for (uint64_t k = 0; table && k < n_table; ++k)
+        if (table[k].first >= M || table[k].second >= M)
+            return fail(ctx, MM_E_RANGE, "mm_suggest_similarity: unknown method id in the table");
+    const uint64_t nb = (M + 1 + 1023) / 1024 + 1;
+    const uint64_t o_cnt = 0, o_off = M + 1, o_cur = 2 * (M + 1), o_rc = 3 * (M + 1), o_ro = 4 * (M + 1),
+                   o_tot = 5 * (M + 1), o_grand = o_tot + nb, o_part = o_grand + 1, o_end = o_part + 2 * ntab + 1;
+    MM_CUDA(ctx, ctx->simc_u32.ensure(o_end));
+    uint32_t* u = ctx->simc_u32.p;
+    SweepArgs a{};
+    a.s = ctx->dev();
+    a.rec = ctx->rec.p;
+    a.recs = ctx->recs.p;
+    a.pos_owner = ctx->pos_owner.p;
+    a.ux = ctx->ux.p;
+    a.un = ctx->un.p;
+    a.dense = ctx->dense.p;
+    a.pos_begin = 0;
+    a.pos_end = M;
+    a.maxdeg_fast = ctx->max_deg <= 8 ? 8u : 16u;
+    mm_status st = run(ctx, "sim_criterion", [&] {
+        launch_sim_partners(tab, ntab, thr, ctx->method_owner.p, static_cast<uint32_t>(M), u + o_cnt, u + o_off,
+                            u + o_cur, u + o_part, u + o_tot, u + o_grand, ctx->stream);
+        cudaMemsetAsync(u + o_rc, 0, 4ull * (M + 1), ctx->stream);
+        launch_sim_emit(a, 0, u + o_off, u + o_part, u + o_rc, nullptr, all_candidates, ctx->stream);
+        launch_scan(u + o_rc, u + o_ro, static_cast<uint32_t>(M + 1), u + o_tot, u + o_grand, ctx->stream);
+    });
+    if (st) return st;
+    uint32_t n = 0;
+    MM_CUDA(ctx, cudaMemcpyAsync(&n, u + o_ro + M, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    *n_out = n;
+    if (!out) return n ? fail(ctx, MM_E_CAPACITY, "output buffer too small") : MM_OK;
+    if (cap < n) return fail(ctx, MM_E_CAPACITY, "output buffer too small");
+    if (!n) return MM_OK;
+    MM_CUDA(ctx, ctx->simc_out.ensure(n));
+    a.out = ctx->simc_out.p;
+    st = run(ctx, "sim_criterion", [&] {
+        launch_sim_emit(a, 1, u + o_off, u + o_part, u + o_rc, u + o_ro, all_candidates, ctx->stream);
+    });
+    if (st) return st;
+    MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->simc_out.p, sizeof(mm_suggestion) * n, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return MM_OK;
 }

@@ -91,6 +91,12 @@ cudaError_t launch_similarity_rows(const DevModel& s, int pass, const uint32_t* 
                                    uint32_t* err, unsigned long long* total, cudaStream_t st);
 cudaError_t launch_scan(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* totals, uint32_t* grand,
                         cudaStream_t st);
+// similarity criterion (k_sweep.cu)
+void launch_sim_partners(const mm_similarity* tab, uint64_t n, double thr, const uint32_t* owner, uint32_t M,
+                         uint32_t* cnt, uint32_t* off, uint32_t* cur, uint32_t* part, uint32_t* totals, uint32_t* grand,
+                         cudaStream_t st);
+void launch_sim_emit(const SweepArgs& a, int pass, const uint32_t* part_off, const uint32_t* part, uint32_t* rec_cnt,
+                     const uint32_t* rec_off, uint32_t all_candidates, cudaStream_t st);
 cudaError_t set_class_large_smem(uint32_t bytes);
 void launch_ck_rows(const DevModel& s, const uint32_t* large_list, const LargePlan* plan, const uint2* items,
                     uint32_t n_items, const uint32_t* grows, const uint32_t* split_list, uint32_t n_split,

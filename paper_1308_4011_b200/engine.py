@@ -29,7 +29,7 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 from . import abi
-from ._lib import MMArgError, check, lib
+from ._lib import MMArgError, MMError, check, lib
 from .system import System
 
 
@@ -380,8 +380,52 @@ class Engine:
                     combine: Combine = Combine.Union, all_candidates: bool = False, top_k: int = 1,
                     class_range: Optional[tuple] = None, copy: bool = True) -> np.ndarray:
         """suggest_all (suggest.hpp:303): ordered by (origin, method, destination)."""
-        self.sweep(criteria, combine, thresholds, all_candidates, top_k, class_range, want_count=False)
-        return self.suggestions(copy=copy)
+        crit = set(Criterion(c) for c in criteria)
+        if Criterion.Similarity not in crit:
+            self.sweep(criteria, combine, thresholds, all_candidates, top_k, class_range, want_count=False)
+            return self.suggestions(copy=copy)
+        if top_k != 1 or class_range is not None:
+            raise MMError(abi.MM_E_UNSUPPORTED, "suggest_all: top-k / class ranges with the similarity criterion")
+        # the sweep for the other criteria, the similarity criterion on its own,
+        # merged by (method, destination) as suggest.hpp:315-341 does
+        parts = [self.suggest_by_similarity(thresholds.similarity, all_candidates)]
+        rest = crit - {Criterion.Similarity}
+        if rest:
+            parts.append(self.suggest_all(thresholds, sorted(rest), combine, all_candidates))
+        recs = np.concatenate(parts) if len(parts) > 1 else parts[0]
+        if not len(recs):
+            return recs
+        order = np.lexsort((recs["destination"], recs["method"]))
+        recs = recs[order]
+        key = recs["method"].astype(np.uint64) << np.uint64(32) | recs["destination"].astype(np.uint64)
+        first = np.ones(len(recs), dtype=bool)
+        first[1:] = key[1:] != key[:-1]
+        groups = np.cumsum(first) - 1
+        tags = np.zeros(int(groups[-1]) + 1, dtype=np.uint8)
+        np.bitwise_or.at(tags, groups, recs["criteria"])
+        out = recs[first].copy()
+        out["criteria"] = tags
+        if combine == Combine.Intersection:
+            out = out[out["criteria"] == criteria_mask(crit)]
+        return out[np.lexsort((out["destination"], out["method"], out["origin"]))]
+
+    def suggest_by_similarity(self, thr: float, all_candidates: bool = False, table: np.ndarray = None) -> np.ndarray:
+        """suggest_by_similarity (suggest.hpp:200-232), ordered by method then
+        destination; `table` = the caller's report.similarity (default: the
+        device table, as all_similarities)."""
+        ptr, n_tab = None, 0
+        if table is not None:
+            table = np.ascontiguousarray(table, dtype=abi.SIMILARITY_DTYPE)
+            ptr, n_tab = table.ctypes.data, len(table)
+        n = C.c_uint64()
+        st = lib().mm_suggest_similarity(self._ctx, ptr, n_tab, float(thr), int(all_candidates), None, 0, C.byref(n))
+        if st not in (abi.MM_OK, abi.MM_E_CAPACITY):
+            self._check(st, "mm_suggest_similarity")
+        out = np.zeros(n.value, dtype=abi.SUGGESTION_DTYPE)
+        if n.value:
+            self._check(lib().mm_suggest_similarity(self._ctx, ptr, n_tab, float(thr), int(all_candidates),
+                                                    out.ctypes.data, n.value, C.byref(n)), "mm_suggest_similarity")
+        return out
 
     def suggest_by_cohesion(self, thresholds: Thresholds, all_candidates: bool = False) -> np.ndarray:
         """suggest_by_cohesion (suggest.hpp:239) — as a set; ordered (origin, method, dest)."""

@@ -10,6 +10,7 @@ import pytest
 import oracle
 from conftest import first_diff, golden_names, golden_records, golden_system, load_golden, records_equal, unhex
 from paper_1308_4011_b200 import Combine, Criterion, Engine, MMArgError, MMError, MMRangeError, System, Thresholds, abi
+from paper_1308_4011_b200.engine import criteria_mask
 
 pytestmark = pytest.mark.gpu
 
@@ -197,8 +198,8 @@ def test_gpu_errors(gpu_engine):
         gpu_engine.lcom_normalized(5)
     with pytest.raises(MMArgError):
         gpu_engine.suggest_all(Thresholds(), [])
-    with pytest.raises(MMError) as ei:
-        gpu_engine.suggest_all(Thresholds(), [Criterion.Similarity])
+    with pytest.raises(MMError) as ei:  # the similarity criterion has no top-k extension
+        gpu_engine.suggest_all(Thresholds(), [Criterion.Similarity], top_k=3)
     assert ei.value.status == abi.MM_E_UNSUPPORTED
     with pytest.raises(MMRangeError):
         gpu_engine.suggest_all(Thresholds(), class_range=(0, 9))
@@ -530,3 +531,33 @@ def test_gpu_similarity_limits_and_full_report(gpu_engine):
     fi, fo = oracle.fan_metrics(s)
     assert (r["fan_in"] == fi).all() and (r["fan_out"] == fo).all()
     assert_metrics_equal((r["lcom"], r["lcom_ck"], r["cbo"]), oracle.class_metrics(s), "full_report")
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+def test_gpu_similarity_criterion_vs_reference(gpu_engine):
+    # suggest_all with every criterion combination that includes Similarity,
+    # union / intersection, best / all candidates, mean and explicit
+    # thresholds — against the compiled reference (report.similarity =
+    # all_similarities)
+    combos = [[Criterion.Similarity], [Criterion.Similarity, Criterion.Cohesion],
+              [Criterion.Similarity, Criterion.Coupling],
+              [Criterion.Similarity, Criterion.Cohesion, Criterion.Coupling]]
+    systems = [golden_system(load_golden(n)) for n in golden_names()[:3]]
+    systems += [System.generate(**random_cfg(np.random.default_rng(700 + k), k)) for k in range(10)]
+    for s in systems:
+        gpu_engine.upload(s)
+        lcom, ck, cbo = gpu_metrics(gpu_engine, s)
+        table = gpu_engine.similarities()
+        R = oracle.RefModel(s)
+        sim_mean = float(np.sum(table["value"]) / len(table)) if len(table) else 0.0
+        t_mean = oracle.thresholds(lcom, cbo, table["value"])
+        for thr in (Thresholds(t_mean.similarity, t_mean.lcom, t_mean.cbo), Thresholds(0.3, 0.2, 1.0),
+                    Thresholds(0.0, -1.0, -1.0)):
+            for crit in combos:
+                for comb in (Combine.Union, Combine.Intersection):
+                    for allc in (False, True):
+                        g = gpu_engine.suggest_all(thr, crit, comb, allc)
+                        o = R.suggest_full(lcom, cbo, criteria_mask(crit), int(comb), allc, thr.similarity,
+                                           thr.lcom, thr.cbo)
+                        assert records_equal(g, o), (crit, comb, allc, thr, first_diff(g, o))
+        del sim_mean
