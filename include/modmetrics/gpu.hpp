@@ -23,7 +23,8 @@
 //   what_if_move            suggest.hpp:87    what_if_move / Engine::
 //   suggest_by_cohesion     suggest.hpp:239   suggest_by_cohesion / Engine::
 //   suggest_by_coupling     suggest.hpp:266   suggest_by_coupling / Engine::
-//   suggest_all             suggest.hpp:303   suggest_all / Engine:: (criteria ⊆ {Cohesion, Coupling})
+//   suggest_by_similarity   suggest.hpp:206   suggest_by_similarity / Engine::
+//   suggest_all             suggest.hpp:303   suggest_all / Engine:: (every criterion)
 //
 // A persistent Engine keeps the system resident in HBM across calls; the
 // free functions upload per call (like the reference, which takes the model
@@ -32,6 +33,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -262,7 +264,56 @@ public:
         if (sel.empty()) throw std::invalid_argument("suggest_all: no criteria selected");  // suggest.hpp:313
         uint32_t mask = 0;
         for (Criterion c : sel) mask |= 1u << static_cast<unsigned>(c);
-        return run(report, thresholds, mask, combine == Combine::Intersection, opts);
+        if (!(mask & MM_CRIT_SIMILARITY)) return run(report, thresholds, mask, combine == Combine::Intersection, opts);
+        // similarity runs on its own; merged by (method, destination) with the
+        // other criteria's records, tags unioned (suggest.hpp:315-341)
+        const bool inter = combine == Combine::Intersection;
+        std::vector<MoveSuggestion> parts = suggest_by_similarity(report, thresholds, opts);
+        if (mask & ~MM_CRIT_SIMILARITY) {
+            std::vector<MoveSuggestion> rest = run(report, thresholds, mask & ~MM_CRIT_SIMILARITY, inter, opts);
+            parts.insert(parts.end(), rest.begin(), rest.end());
+        }
+        std::map<std::pair<MethodId, ClassId>, MoveSuggestion> merged;
+        for (MoveSuggestion& m : parts) {
+            auto [it, fresh] = merged.try_emplace(std::make_pair(m.method, m.destination), m);
+            if (!fresh) it->second.criteria.insert(it->second.criteria.end(), m.criteria.begin(), m.criteria.end());
+        }
+        std::vector<MoveSuggestion> out;
+        for (auto& [key, m] : merged) {
+            std::sort(m.criteria.begin(), m.criteria.end());
+            m.criteria.erase(std::unique(m.criteria.begin(), m.criteria.end()), m.criteria.end());
+            if (inter && m.criteria.size() != sel.size()) continue;
+            out.push_back(std::move(m));
+        }
+        std::sort(out.begin(), out.end(), [](const MoveSuggestion& a, const MoveSuggestion& b) {
+            if (a.origin != b.origin) return a.origin < b.origin;
+            if (a.method != b.method) return a.method < b.method;
+            return a.destination < b.destination;
+        });
+        return out;
+    }
+
+    // suggest_by_similarity (suggest.hpp:206): pairs from report.similarity
+    // (the caller's table, as the reference reads it), ordered by method,
+    // then destination — the reference's map order.
+    std::vector<MoveSuggestion> suggest_by_similarity(const MetricsReport& report, const Thresholds& thresholds,
+                                                      const SuggestOptions& opts = {}) {
+        std::vector<mm_similarity> tab(report.similarity.size());
+        for (size_t k = 0; k < tab.size(); ++k)
+            tab[k] = mm_similarity{report.similarity[k].first, report.similarity[k].second, report.similarity[k].value};
+        uint64_t n = 0;
+        const mm_status st = mm_suggest_similarity(ctx_.get(), tab.data(), tab.size(), thresholds.similarity,
+                                                   opts.all_candidates ? 1u : 0u, nullptr, 0, &n);
+        if (st != MM_OK && st != MM_E_CAPACITY) detail::check(st, ctx_.get(), "suggest_by_similarity");
+        std::vector<mm_suggestion> raw(n);
+        if (n)
+            detail::check(mm_suggest_similarity(ctx_.get(), tab.data(), tab.size(), thresholds.similarity,
+                                                opts.all_candidates ? 1u : 0u, raw.data(), n, &n),
+                          ctx_.get(), "suggest_by_similarity");
+        std::vector<MoveSuggestion> out;
+        out.reserve(raw.size());
+        for (const mm_suggestion& r : raw) out.push_back(detail::to_suggestion(r));
+        return out;
     }
 
     // suggest_by_cohesion (suggest.hpp:239): same records, in the reference's
@@ -296,8 +347,6 @@ private:
 
     std::vector<MoveSuggestion> run(const MetricsReport& report, const Thresholds& t, uint32_t mask, bool inter,
                                     const SuggestOptions& opts) {
-        if (mask & MM_CRIT_SIMILARITY)
-            throw std::invalid_argument("gpu: Criterion::Similarity is outside this engine");
         if (report.lcom.size() != n_classes_ || report.cbo.size() != n_classes_)
             throw std::invalid_argument("gpu: report does not match the uploaded system");
         detail::check(mm_set_gates(ctx_.get(), report.lcom.data(), report.cbo.data()), ctx_.get(), "mm_set_gates");
@@ -417,6 +466,14 @@ inline std::vector<MoveSuggestion> suggest_by_coupling(const SystemModel& model,
     Engine e;
     e.upload(model, deps);
     return e.suggest_by_coupling(report, thresholds, opts);
+}
+
+inline std::vector<MoveSuggestion> suggest_by_similarity(const SystemModel& model, const DependencyTable& deps,
+                                                         const MetricsReport& report, const Thresholds& thresholds,
+                                                         const SuggestOptions& opts = {}) {
+    Engine e;
+    e.upload(model, deps);
+    return e.suggest_by_similarity(report, thresholds, opts);
 }
 
 inline std::vector<MoveSuggestion> suggest_all(const SystemModel& model, const DependencyTable& deps,

@@ -76,6 +76,23 @@ static void check_system(const std::string& name, const SystemModel& model, cons
     expect(e.report_without_similarity() == report_without_similarity(model, deps),
            name + " report without similarity");
     if (model.method_count() <= 3000) {  // the reference's tables are O(m^2)
+        // every criterion, with the report's similarity table
+        MetricsReport full = report_without_similarity(model, deps);
+        full.similarity = all_similarities(model, deps);
+        Thresholds ts = compute_thresholds(full);
+        for (bool allc : {false, true}) {
+            SuggestOptions o;
+            o.all_candidates = allc;
+            expect(e.suggest_by_similarity(full, ts, o) == suggest_by_similarity(model, deps, full, ts, o),
+                   name + " suggest_by_similarity");
+            for (Combine cb : {Combine::Union, Combine::Intersection})
+                expect(e.suggest_all(full, ts, {Criterion::Similarity, Criterion::Cohesion, Criterion::Coupling}, cb,
+                                     o) == suggest_all(model, deps, full, ts,
+                                                       {Criterion::Similarity, Criterion::Cohesion,
+                                                        Criterion::Coupling},
+                                                       cb, o),
+                       name + " suggest_all every criterion");
+        }
         expect(e.full_report() == full_report(model, deps), name + " full_report");
         expect(gpu::parallel_full_report(model, deps, 3) == parallel_full_report(model, deps, 3),
                name + " parallel_full_report");
