@@ -152,15 +152,6 @@ struct UsedList {
     }
 };
 
-template <int K>
-__device__ __forceinline__ void build_used(const DevModel& s, uint32_t p, UsedList<K>& L) {
-    L.clear();
-    const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
-    for (uint32_t e = cb; e < ce; ++e) L.insert(__ldg(s.method_owner + __ldg(s.call_tgt + e)), 0);
-    const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
-    for (uint32_t e = ab; e < ae; ++e) L.insert(__ldg(s.attribute_owner + __ldg(s.acc_tgt + e)), 1);
-}
-
 // Streaming used list for methods whose degree exceeds the register list:
 // distinct owners are enumerated in ascending order by repeated min-scans of
 // the method's edges. O(deg) per step; correct for any degree.
@@ -237,36 +228,6 @@ __device__ __forceinline__ ClassRec load_rec(const ClassRec* __restrict__ rec, u
     r.A = a.x; r.M = a.y; r.H = a.z; r.cbo = a.w;
     r.ubase = b.x; r.dense = b.y;  // sig words stay in memory: read on demand (same cache line)
     return r;
-}
-
-// Whole 64-byte record in one round trip (4 independent 16-byte loads), the
-// signature kept in registers.
-struct ClassRecFull {
-    ClassRec r;
-    uint32_t sig[kSigWords];
-    __device__ __forceinline__ uint32_t word(uint32_t i) const {  // unrolled select: no local memory
-        uint32_t w = 0;
-#pragma unroll
-        for (int k = 0; k < kSigWords; ++k)
-            if ((uint32_t)k == i) w = sig[k];
-        return w;
-    }
-    __device__ __forceinline__ bool maybe(uint32_t x) const {
-        const uint32_t b1 = bloom_h1(x), b2 = bloom_h2(x);
-        return ((word(b1 >> 5) >> (b1 & 31)) & (word(b2 >> 5) >> (b2 & 31)) & 1u) != 0;
-    }
-};
-
-__device__ __forceinline__ ClassRecFull load_rec_full(const ClassRec* __restrict__ rec, uint32_t c) {
-    const uint4* p = reinterpret_cast<const uint4*>(rec + c);
-    const uint4 a = __ldg(p), b = __ldg(p + 1), q = __ldg(p + 2), t = __ldg(p + 3);
-    ClassRecFull f;
-    f.r.A = a.x; f.r.M = a.y; f.r.H = a.z; f.r.cbo = a.w;
-    f.r.ubase = b.x; f.r.dense = b.y;
-    f.sig[0] = b.z; f.sig[1] = b.w;
-    f.sig[2] = q.x; f.sig[3] = q.y; f.sig[4] = q.z; f.sig[5] = q.w;
-    f.sig[6] = t.x; f.sig[7] = t.y; f.sig[8] = t.z; f.sig[9] = t.w;
-    return f;
 }
 
 // Bloom test against class c's U-row signature (L1 hits once c's record line is loaded)
