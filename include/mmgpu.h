@@ -36,7 +36,10 @@ typedef enum mm_status {
     MM_E_OOM = 4,         /* device allocation failed */
     MM_E_STATE = 5,       /* call order violated (e.g. sweep before upload) */
     MM_E_UNSUPPORTED = 6, /* outside this engine's scope (e.g. Criterion::Similarity) */
-    MM_E_CAPACITY = 7     /* caller buffer too small; *n_out holds the needed count */
+    MM_E_CAPACITY = 7,    /* caller buffer too small; *n_out holds the needed count */
+    MM_E_PARSE = 8,       /* modmetrics::ParseError      (facts.hpp:22-24), see mmfacts.h */
+    MM_E_VALIDATION = 9,  /* modmetrics::ValidationError (facts.hpp:28-37) */
+    MM_E_IO = 10          /* modmetrics::IoError         (facts.hpp:39-41) */
 } mm_status;
 
 /* Criterion bits: bit (1 << Criterion) with Criterion as in suggest.hpp:17

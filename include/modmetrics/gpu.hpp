@@ -151,6 +151,13 @@ public:
         n_methods_ = csr.sys.n_methods;
     }
 
+    // Uploads a CSR system as-is (e.g. the direct view of gpu::Facts, gpu_facts.hpp).
+    void upload(const mm_system& sys) {
+        detail::check(mm_upload(ctx_.get(), &sys), ctx_.get(), "mm_upload");
+        n_classes_ = sys.n_classes;
+        n_methods_ = sys.n_methods;
+    }
+
     WorkloadEstimate estimate_workload() {
         mm_workload w{};
         detail::check(mm_estimate_workload(ctx_.get(), &w), ctx_.get(), "estimate_workload");

@@ -79,6 +79,26 @@ _SIGS = {
 
 EXPORTED = tuple(_SIGS)
 
+# include/mmfacts.h (facts ingest, host-only)
+_FACTS_SIGS = {
+    "mm_facts_parse": (C.c_int, [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "mm_facts_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "mm_facts_free": (None, [C.c_void_p]),
+    "mm_facts_status": (C.c_int, [C.c_void_p]),
+    "mm_facts_error": (C.c_char_p, [C.c_void_p]),
+    "mm_facts_system": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_system)]),
+    "mm_facts_violation_count": (C.c_uint32, [C.c_void_p]),
+    "mm_facts_violation": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_int), C.POINTER(C.c_char_p)]),
+    "mm_facts_warning_count": (C.c_uint32, [C.c_void_p]),
+    "mm_facts_warning": (C.c_char_p, [C.c_void_p, C.c_uint32]),
+    "mm_facts_class_name": (C.c_void_p, [C.c_void_p, C.c_uint32, C.POINTER(C.c_size_t)]),
+    "mm_facts_method_name": (C.c_void_p, [C.c_void_p, C.c_uint32, C.POINTER(C.c_size_t)]),
+    "mm_facts_attribute_name": (C.c_void_p, [C.c_void_p, C.c_uint32, C.POINTER(C.c_size_t)]),
+    "mm_facts_to_json": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+}
+
+FACTS_EXPORTED = tuple(_FACTS_SIGS)
+
 
 def lib_path() -> Path:
     return _LIB_PATH
@@ -93,7 +113,7 @@ def lib() -> C.CDLL:
                 f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
                 "(this engine has no CPU fallback)")
         l = C.CDLL(str(_LIB_PATH))
-        for name, (res, args) in _SIGS.items():
+        for name, (res, args) in {**_SIGS, **_FACTS_SIGS}.items():
             fn = getattr(l, name)
             fn.restype = res
             fn.argtypes = args

@@ -13,10 +13,13 @@ MM_E_OOM = 4
 MM_E_STATE = 5
 MM_E_UNSUPPORTED = 6
 MM_E_CAPACITY = 7
+MM_E_PARSE = 8
+MM_E_VALIDATION = 9
+MM_E_IO = 10
 
 STATUS_NAMES = {
     0: "MM_OK", 1: "MM_E_RANGE", 2: "MM_E_ARG", 3: "MM_E_CUDA", 4: "MM_E_OOM",
-    5: "MM_E_STATE", 6: "MM_E_UNSUPPORTED", 7: "MM_E_CAPACITY",
+    5: "MM_E_STATE", 6: "MM_E_UNSUPPORTED", 7: "MM_E_CAPACITY", 8: "MM_E_PARSE", 9: "MM_E_VALIDATION", 10: "MM_E_IO",
 }
 
 MM_CRIT_SIMILARITY = 1 << 0

@@ -41,7 +41,7 @@ def _stale(target: Path, deps) -> bool:
 
 
 def build_lib(force: bool = False, verbose: bool = False) -> Path:
-    deps = _sources() + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "mmgpu.h"]
+    deps = _sources() + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "mmgpu.h", ROOT / "include" / "mmfacts.h"]
     if not force and not _stale(LIB, deps):
         return LIB
     cmd = [NVCC, *NVCC_FLAGS, "-shared", "-o", str(LIB), *map(str, _sources())]

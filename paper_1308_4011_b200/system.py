@@ -85,28 +85,16 @@ class System:
 
     @classmethod
     def from_facts(cls, obj) -> "System":
-        """Facts JSON (schema of SPEC.md / facts.hpp): dict, JSON text or path."""
-        if isinstance(obj, (str, Path)) and Path(obj).exists():
-            obj = json.loads(Path(obj).read_text())
-        elif isinstance(obj, str):
-            obj = json.loads(obj)
-        classes = obj["classes"]
-        n_m = 1 + max((m["id"] for c in classes for m in c["methods"]), default=-1)
-        n_a = 1 + max((a["id"] for c in classes for a in c["attributes"]), default=-1)
-        calls = [[] for _ in range(n_m)]
-        accs = [[] for _ in range(n_m)]
-        specs = []
-        for ci, c in enumerate(classes):
-            if c["id"] != ci:
-                raise ValueError(f"classes[{ci}] has id {c['id']}, expected dense ids")
-            specs.append(([a["id"] for a in c["attributes"]], [m["id"] for m in c["methods"]]))
-            for m in c["methods"]:
-                calls[m["id"]] = [t for t in m["calls"] if t != m["id"]]  # self-call dropped
-                accs[m["id"]] = list(m["accesses"])
-        sys_ = cls.build(specs, calls, accs)
-        if sys_.n_methods != n_m or sys_.n_attributes != n_a:
-            raise ValueError("facts: ids are not dense")
-        return sys_
+        """Facts JSON (facts.hpp schema): dict, JSON text/bytes or a path. Parsed
+        natively (mmfacts.h) with the reference's parse_facts semantics; errors
+        raise facts.FactsParseError / FactsValidationError (ValueError) or
+        FactsIoError."""
+        from .facts import load_facts, parse_facts
+        if isinstance(obj, dict):
+            return parse_facts(json.dumps(obj)).system
+        if isinstance(obj, Path) or (isinstance(obj, str) and not obj.lstrip().startswith(("{", "[")) and Path(obj).exists()):
+            return load_facts(obj).system
+        return parse_facts(obj).system
 
     @classmethod
     def generate(cls, seed: int, n_classes: int, n_methods: int, n_attributes: int,
