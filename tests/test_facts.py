@@ -1,7 +1,7 @@
 """Facts ingest (include/mmfacts.h, paper_1308_4011_b200.facts) against the
 reference's parse_facts / load_facts / facts_to_json (facts.hpp:91-320).
 
-* golden outcomes: tests/golden/facts_outcomes.json holds the reference's own
+* golden outcomes: tests/golden/facts/outcomes.json holds the reference's own
   outcome (exception type, what(), violations, warnings, canonical bytes) for
   86 documents — test_facts.cpp's cases, shape/violation/syntax errors at
   every level; made by `oracle/_ref/facts_parity --golden` (the reference
@@ -26,7 +26,7 @@ from paper_1308_4011_b200._lib import FACTS_EXPORTED, lib
 from paper_1308_4011_b200.facts import VIOLATION_KINDS
 
 ROOT = Path(__file__).resolve().parents[1]
-GOLDEN = ROOT / "tests" / "golden" / "facts_outcomes.json"
+GOLDEN = ROOT / "tests" / "golden" / "facts" / "outcomes.json"
 HARNESS = ROOT / "oracle" / "_ref" / "facts_parity"
 
 _TYPE = {FactsParseError: "ParseError", FactsValidationError: "ValidationError", FactsIoError: "IoError",
