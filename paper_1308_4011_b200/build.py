@@ -60,9 +60,15 @@ def build_oracle() -> None:
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
 
 
+def build_tools() -> None:
+    """tools/_build/mmgpu (the CLI with --engine gpu; needs the reference headers)."""
+    subprocess.run(["make", "-s", "-C", str(ROOT / "tools")], check=True)
+
+
 def build_all(force: bool = False) -> None:
     build_lib(force=force)
     build_oracle()
+    build_tools()
 
 
 if __name__ == "__main__":
