@@ -20,6 +20,7 @@
 //
 // Build: tools/Makefile (needs the reference headers, like every user of the
 // drop-in headers: the north star keeps proj/include as the API surface).
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -39,6 +40,19 @@ namespace {
 using namespace modmetrics;
 
 constexpr int kExitOk = 0, kExitParse = 2, kExitValidation = 3, kExitIo = 4, kExitUsage = 64;
+
+// MMGPU_CLI_TIMING=1: phase times on stderr (wall clock, host side)
+struct Phase {
+    const char* name;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit Phase(const char* n) : name(n) {}
+    ~Phase() {
+        static const bool on = std::getenv("MMGPU_CLI_TIMING") != nullptr;
+        if (on)
+            std::fprintf(stderr, "timing %-14s %9.3f ms\n", name,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
 
 struct Usage : std::runtime_error {
     using std::runtime_error::runtime_error;
@@ -100,12 +114,13 @@ struct Analysis {
 Analysis analyze_facts(const RunConfig& cfg) {
     Analysis a;
     if (cfg.engine == "gpu") {
-        const gpu::Facts facts = gpu::Facts::load(cfg.facts_path);
-        a.engine.emplace(cfg.device);
-        a.engine->upload(facts.system());  // CSR straight from the parse
-        a.loaded = facts.to_load_result();  // names and records for the renderers
+        std::optional<gpu::Facts> facts;
+        { Phase p("load_facts"); facts.emplace(gpu::Facts::load(cfg.facts_path)); }
+        { Phase p("ctx_create"); a.engine.emplace(cfg.device); }
+        { Phase p("upload"); a.engine->upload(facts->system()); }  // CSR straight from the parse
+        { Phase p("load_result"); a.loaded = facts->to_load_result(); }  // names and records for the renderers
         print_warnings(a.loaded.warnings);
-        a.report = a.engine->full_report();
+        { Phase p("full_report"); a.report = a.engine->full_report(); }
         return a;
     }
     a.loaded = load_facts(cfg.facts_path);
@@ -117,6 +132,7 @@ Analysis analyze_facts(const RunConfig& cfg) {
 
 int cmd_analyze(const RunConfig& cfg) {  // modmetrics.cpp:88-95
     const Analysis a = analyze_facts(cfg);
+    Phase p("render+write");
     write_output(cfg.out_path, cfg.format == "text" ? render_report_text(a.loaded.model, a.report)
                                                     : render_report_json(a.loaded.model, a.report));
     return kExitOk;
@@ -133,9 +149,13 @@ int cmd_suggest(const RunConfig& cfg) {  // modmetrics.cpp:109-131
     SuggestOptions opts;
     opts.all_candidates = cfg.all_candidates;
     const std::vector<Criterion> criteria = parse_criteria(cfg.criteria);
-    const std::vector<MoveSuggestion> suggestions =
-        a.engine ? a.engine->suggest_all(a.report, thresholds, criteria, combine, opts)
-                 : suggest_all(a.loaded.model, a.loaded.deps, a.report, thresholds, criteria, combine, opts);
+    std::vector<MoveSuggestion> suggestions;
+    {
+        Phase p("suggest_all");
+        suggestions = a.engine ? a.engine->suggest_all(a.report, thresholds, criteria, combine, opts)
+                               : suggest_all(a.loaded.model, a.loaded.deps, a.report, thresholds, criteria, combine, opts);
+    }
+    Phase p("render+write");
     write_output(cfg.out_path, cfg.format == "text" ? render_suggestions_text(a.loaded.model, suggestions, thresholds)
                                                     : render_suggestions_json(a.loaded.model, suggestions, thresholds));
     return kExitOk;
