@@ -406,8 +406,11 @@ def run_ours(args) -> None:
         e2e = run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather if world > 1 else None)
 
     cb = None
+    ingest = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cb = cpu_baseline(s, n_cand, args.cpu_frac)
+        if args.config == "c4":
+            ingest = ingest_bench(cfg)
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -432,11 +435,54 @@ def run_ours(args) -> None:
             "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
             "ms_per_step_instrumented": float(np.mean(step_ms_prof)),
             "algorithmic_bytes": ab,
+            "ingest": ingest,
         }
         print(json.dumps(out), flush=True)
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def ingest_bench(cfg):
+    """Facts file -> device-ready CSR, host side, on this
+    box: the config's canonical facts document (written by the product CLI's
+    generator) parsed by mm_facts_load (C ABI, best of 3) against the
+    reference's own parse_facts compiled in place (oracle/_ref/facts_parity
+    --bench, the same C4 document, one thread each). Never fails the line."""
+    import ctypes as C
+    cli, harness = ROOT / "tools" / "_build" / "mmgpu", ROOT / "oracle" / "_ref" / "facts_parity"
+    try:
+        if not cli.exists():
+            return {"unavailable": "tools/_build/mmgpu not built"}
+        from paper_1308_4011_b200._lib import lib
+        with tempfile.TemporaryDirectory() as d:
+            path = Path(d) / "facts.json"
+            subprocess.run([str(cli), "generate", "--classes", str(cfg["n_classes"]), "--methods", str(cfg["n_methods"]),
+                            "--attributes", str(cfg["n_attributes"]), "--kmax-calls", str(cfg["k_max_calls"]),
+                            "--kmax-accesses", str(cfg["k_max_accesses"]), "--intra-bias", str(cfg["intra_class_bias"]),
+                            "--seed", str(cfg["seed"]), "--out", str(path)], check=True, timeout=300)
+            size = path.stat().st_size
+            best = float("inf")
+            for _ in range(3):
+                h = C.c_void_p()
+                t0 = time.perf_counter()
+                st = lib().mm_facts_load(str(path).encode(), C.byref(h))
+                dt = time.perf_counter() - t0
+                lib().mm_facts_free(h)
+                if st != 0:
+                    return {"error": f"mm_facts_load status {st}"}
+                best = min(best, dt)
+        out = {"doc_mb": size / 1e6, "csr_load_s": best, "csr_mb_per_s": size / 1e6 / best, "threads": 1,
+               "path": "mm_facts_load (file read + streaming parse + semantic checks + CSR)"}
+        if harness.exists():
+            r = subprocess.run([str(harness), "--bench"], capture_output=True, text=True, timeout=300)
+            ref = json.loads(r.stdout.strip().splitlines()[-1])
+            out["reference_parse_facts_s"] = ref["reference_parse_facts_s"]
+            out["reference_kind"] = "reference parse_facts (nlohmann DOM + model walk), compiled in place, 1 thread"
+            out["speedup_vs_reference"] = ref["reference_parse_facts_s"] / best
+        return out
+    except Exception as e:  # reported, never fatal
+        return {"error": f"{type(e).__name__}: {e}"}
 
 
 def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
