@@ -26,13 +26,16 @@
 // enforced), so it is not repeated.
 
 #include <algorithm>
+#include <chrono>
 #include <cerrno>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -547,35 +550,132 @@ private:
         if (peek() != '[') { skip_value(); classes_kind = F_OTHER; return; }
         classes_kind = F_ARRAY;
         cls_begin = classes.size();
-        array([&](size_t) {
+        ++p_;
+        ws();
+        if (peek() == ']') { ++p_; cls_end = classes.size(); return; }
+        for (;;) {
             ws();
-            RawClass rc;
-            if (peek() != '{') { skip_value(); classes.push_back(rc); return; }
-            rc.is_object = 1;
-            object([&](int k) {
-                if (k == K_ID) id_value(rc.id);
-                else if (k == K_NAME) name_value(rc.name);
-                else if (k == K_ATTRIBUTES) {
-                    ws();
-                    if (peek() != '[') { skip_value(); rc.attrs_kind = F_OTHER; return; }
-                    rc.attrs_kind = F_ARRAY;
-                    rc.attr_begin = attrs.size();
-                    array([&](size_t) { attr_value(); });
-                    rc.attr_end = attrs.size();
-                } else if (k == K_METHODS) {
-                    ws();
-                    if (peek() != '[') { skip_value(); rc.methods_kind = F_OTHER; return; }
-                    rc.methods_kind = F_ARRAY;
-                    rc.meth_begin = methods.size();
-                    array([&](size_t) { method_value(); });
-                    rc.meth_end = methods.size();
-                } else skip_value();
-            });
-            classes.push_back(rc);
-        });
+            if (splice_ && p_ == splice_->first_start()) {
+                const size_t q = splice_->apply(*this);
+                if (q == p_) class_element();  // nothing verified: parse it here
+                else p_ = q;
+            } else class_element();
+            ws();
+            if (p_ >= n_) fail_eof();
+            if (s_[p_] == ',') { ++p_; continue; }
+            if (s_[p_] == ']') { ++p_; break; }
+            fail_token();
+        }
         cls_end = classes.size();
     }
 
+    void class_element() {
+        RawClass rc;
+        if (peek() != '{') { skip_value(); classes.push_back(rc); return; }
+        rc.is_object = 1;
+        object([&](int k) {
+            if (k == K_ID) id_value(rc.id);
+            else if (k == K_NAME) name_value(rc.name);
+            else if (k == K_ATTRIBUTES) {
+                ws();
+                if (peek() != '[') { skip_value(); rc.attrs_kind = F_OTHER; return; }
+                rc.attrs_kind = F_ARRAY;
+                rc.attr_begin = attrs.size();
+                array([&](size_t) { attr_value(); });
+                rc.attr_end = attrs.size();
+            } else if (k == K_METHODS) {
+                ws();
+                if (peek() != '[') { skip_value(); rc.methods_kind = F_OTHER; return; }
+                rc.methods_kind = F_ARRAY;
+                rc.meth_begin = methods.size();
+                array([&](size_t) { method_value(); });
+                rc.meth_end = methods.size();
+            } else skip_value();
+        });
+        classes.push_back(rc);
+    }
+
+public:
+    // Speculative chunk of the classes array (parallel ingest): starting at a
+    // guessed element start, parse class elements until the next element
+    // start at or past `limit`, or the closing ']'. Any failure just means the
+    // main reader parses this stretch itself.
+    struct Chunk {
+        size_t start = 0, next = 0, end_pos = 0;  // next: first element start >= limit; end_pos: after the last element
+        bool ok = false, closed = false;          // closed: stopped at the array's ']'
+    };
+    void run_chunk(Chunk& c, size_t limit) {
+        try {
+            const size_t span = limit > c.start ? limit - c.start : 0;
+            classes.reserve(span / 48 + 16); methods.reserve(span / 44 + 16);
+            attrs.reserve(span / 20 + 16); deps.reserve(span / 2 + 16); blob_.reserve(span + 16);
+            p_ = c.start;
+            for (;;) {
+                class_element();
+                c.end_pos = p_;
+                ws();
+                if (p_ >= n_) return;
+                if (s_[p_] == ']') { c.closed = true; c.ok = true; return; }
+                if (s_[p_] != ',') return;
+                ++p_;
+                ws();
+                if (p_ >= limit) { c.next = p_; c.ok = true; return; }
+            }
+        } catch (...) {
+            c.ok = false;
+        }
+    }
+
+    // Verified chain of chunks the main reader splices in when it reaches the
+    // first chunk's start exactly (which proves that start is a real element
+    // start; each verified chunk then proves the next one's).
+    struct Splice {
+        std::vector<Chunk>* chunks;
+        std::vector<Reader*>* readers;
+        std::vector<std::thread>* threads;
+        size_t first_start() const { return (*chunks)[0].start; }
+        size_t apply(Reader& main) {
+            for (std::thread& t : *threads) if (t.joinable()) t.join();
+            size_t pos = main.p_;
+            for (size_t k = 0; k < chunks->size(); ++k) {
+                const Chunk& c = (*chunks)[k];
+                if (!c.ok || c.start != pos) break;
+                main.absorb(*(*readers)[k]);
+                pos = c.end_pos;
+                if (c.closed || k + 1 == chunks->size() || c.next != (*chunks)[k + 1].start) break;
+                pos = c.next;
+                // the main loop consumes the ',' between chunks: hand back the
+                // end of this chunk unless the next one is verified too
+                if (!(*chunks)[k + 1].ok) { pos = c.end_pos; break; }
+            }
+            main.splice_ = nullptr;
+            if (std::getenv("MMGPU_FACTS_DEBUG")) {
+                size_t okc = 0;
+                for (const Chunk& c : *chunks) okc += c.ok;
+                std::fprintf(stderr, "facts splice: %zu chunks, %zu ok, resume at %zu\n", chunks->size(), okc, pos);
+            }
+            return pos;
+        }
+    };
+    Splice* splice_ = nullptr;
+
+    void absorb(const Reader& w) {
+        const uint64_t ab = attrs.size(), mb = methods.size(), db = deps.size(), bb = blob_.size();
+        for (RawClass rc : w.classes) {
+            rc.attr_begin += ab; rc.attr_end += ab; rc.meth_begin += mb; rc.meth_end += mb; rc.name.s.off += bb;
+            classes.push_back(rc);
+        }
+        for (RawAttr ra : w.attrs) { ra.name.s.off += bb; attrs.push_back(ra); }
+        for (RawMethod rm : w.methods) {
+            rm.name.s.off += bb;
+            rm.calls.begin += db; rm.calls.end += db; rm.accesses.begin += db; rm.accesses.end += db;
+            methods.push_back(rm);
+        }
+        deps.insert(deps.end(), w.deps.begin(), w.deps.end());
+        blob_.append(w.blob_);
+    }
+
+private:
     void attr_value() {
         ws();
         RawAttr ra;
@@ -691,8 +791,10 @@ void build(Reader& r, mm_facts& f) {
                     if (valid_id(r.methods[i].id)) mm = std::max(mm, r.methods[i].id.value + 1);
         }
         if (ma < id_cap && mm < id_cap) {
-            aown.reserve(ma); f.attribute_name.reserve(ma);
-            mown.reserve(mm); f.method_name.reserve(mm);
+            // the final sizes are exactly these (max visited id + 1), so
+            // growing to them up front is the same as growing id by id
+            aown.assign(ma, kNone); f.attribute_name.resize(ma);
+            mown.assign(mm, kNone); f.method_name.resize(mm);
         }
     }
     for (uint64_t ci = 0; ci < nc; ++ci) {
@@ -731,7 +833,7 @@ void build(Reader& r, mm_facts& f) {
                 f.cattr.push_back(id);
             }
         }
-        std::sort(f.cattr.begin() + abeg, f.cattr.end());
+        if (!std::is_sorted(f.cattr.begin() + abeg, f.cattr.end())) std::sort(f.cattr.begin() + abeg, f.cattr.end());
         f.caoff[ci + 1] = uint32_t(f.cattr.size());
 
         if (rc.methods_kind == F_MISSING) parse_error(cw + ": missing \"methods\"");
@@ -760,7 +862,7 @@ void build(Reader& r, mm_facts& f) {
                 pending.push_back({id, rc.meth_begin + mi, uint32_t(ci), uint32_t(mi)});
             }
         }
-        std::sort(f.cmeth.begin() + mbeg, f.cmeth.end());
+        if (!std::is_sorted(f.cmeth.begin() + mbeg, f.cmeth.end())) std::sort(f.cmeth.begin() + mbeg, f.cmeth.end());
         f.cmoff[ci + 1] = uint32_t(f.cmeth.size());
     }
 
@@ -847,11 +949,142 @@ void build(Reader& r, mm_facts& f) {
     scatter(acount, f.acc_off, f.acc_tgt, false);
 }
 
+// ---------------------------------------------------------------------------
+// Parallel ingest: the classes array is cut into chunks parsed speculatively
+// on worker threads while the main reader parses the head. Chunk starts are
+// guessed from a parallel bracket-depth scan (the first '{' at depth 2 after
+// each split point); the main reader only splices a chunk in when it reaches
+// that chunk's start exactly at an element boundary, and each spliced chunk
+// must end exactly where the next one starts. Anything else — a wrong guess,
+// an error inside a chunk — is simply parsed by the main reader, so results
+// and errors are the sequential reader's by construction.
+// ---------------------------------------------------------------------------
+struct Parallel {
+    std::vector<Reader::Chunk> chunks;
+    std::vector<std::string> blobs;
+    std::vector<std::unique_ptr<Reader>> owned;
+    std::vector<Reader*> readers;
+    std::vector<std::thread> threads;
+    Reader::Splice splice{};
+    ~Parallel() {
+        for (std::thread& t : threads) if (t.joinable()) t.join();
+    }
+};
+
+size_t env_size(const char* name, size_t dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? size_t(std::strtoull(v, nullptr, 10)) : dflt;
+}
+
+// depth change over [b, e), assuming the segment starts outside a string
+int64_t depth_delta(const unsigned char* s, size_t b, size_t e) {
+    int64_t d = 0;
+    bool in_str = false;
+    for (size_t i = b; i < e; ++i) {
+        const unsigned char c = s[i];
+        if (in_str) {
+            if (c == '\\') ++i;
+            else if (c == '"') in_str = false;
+        } else if (c == '"') in_str = true;
+        else if (c == '{' || c == '[') ++d;
+        else if (c == '}' || c == ']') --d;
+    }
+    return d;
+}
+
+// first '{' opened at depth 2 at or after b (a class element of the top-level classes array)
+size_t element_start(const unsigned char* s, size_t n, size_t b, int64_t depth) {
+    bool in_str = false;
+    for (size_t i = b; i < n; ++i) {
+        const unsigned char c = s[i];
+        if (in_str) {
+            if (c == '\\') ++i;
+            else if (c == '"') in_str = false;
+        } else if (c == '"') in_str = true;
+        else if (c == '{') { if (depth == 2) return i; ++depth; }
+        else if (c == '[') ++depth;
+        else if (c == '}' || c == ']') --depth;
+    }
+    return n;
+}
+
+// next "}" ws "," ws "{" at or after b: the '{' (a likely object-element
+// start, outside any string in any sane document)
+size_t resync(const unsigned char* s, size_t n, size_t b) {
+    auto ws = [](unsigned char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r'; };
+    for (size_t i = b; i < n; ++i) {
+        if (s[i] != '}') continue;
+        size_t j = i + 1;
+        while (j < n && ws(s[j])) ++j;
+        if (j >= n || s[j] != ',') continue;
+        ++j;
+        while (j < n && ws(s[j])) ++j;
+        if (j < n && s[j] == '{') return j;
+    }
+    return n;
+}
+
+void plan_parallel(Parallel& P, Reader& main, const char* text, size_t len) {
+    const size_t min_len = env_size("MMGPU_FACTS_PAR_MIN", size_t(8) << 20);
+    size_t T = env_size("MMGPU_FACTS_THREADS", std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency())));
+    if (len < min_len || T < 2) return;
+    T = std::min<size_t>(T, std::max<size_t>(2, len / std::max<size_t>(min_len / 8, 1)));
+    const unsigned char* s = reinterpret_cast<const unsigned char*>(text);
+    // segment boundaries at likely element starts (outside strings), so each
+    // segment's depth change can be counted independently
+    std::vector<size_t> bound{0};
+    for (size_t k = 1; k < T; ++k) {
+        const size_t b = resync(s, len, std::max(len * k / T, bound.back() + 1));
+        if (b >= len) break;
+        bound.push_back(b);
+    }
+    bound.push_back(len);
+    const size_t S = bound.size() - 1;
+    std::vector<int64_t> delta(S, 0);
+    {
+        std::vector<std::thread> th;
+        for (size_t k = 0; k < S; ++k) th.emplace_back([&, k] { delta[k] = depth_delta(s, bound[k], bound[k + 1]); });
+        for (std::thread& t : th) t.join();
+    }
+    int64_t depth = 0;
+    std::vector<size_t> starts;
+    for (size_t k = 1; k < S; ++k) {
+        depth += delta[k - 1];
+        const size_t st = element_start(s, len, bound[k], depth);
+        if (st < len && (starts.empty() || st > starts.back())) starts.push_back(st);
+    }
+    if (starts.empty()) return;
+    const size_t C = starts.size();
+    P.chunks.resize(C);
+    P.blobs.resize(C);
+    for (size_t k = 0; k < C; ++k) {
+        P.chunks[k].start = starts[k];
+        P.owned.emplace_back(new Reader(text, len, P.blobs[k]));
+        P.readers.push_back(P.owned.back().get());
+    }
+    for (size_t k = 0; k < C; ++k) {
+        const size_t limit = k + 1 < C ? starts[k + 1] : len;
+        P.threads.emplace_back([&P, k, limit] { P.readers[k]->run_chunk(P.chunks[k], limit); });
+    }
+    P.splice = Reader::Splice{&P.chunks, &P.readers, &P.threads};
+    main.splice_ = &P.splice;
+}
+
 mm_status finish(mm_facts* f, const char* text, size_t len) {
     try {
         Reader rd(text, len, f->blob);
+        Parallel par;
         try {
+            try {
+                plan_parallel(par, rd, text, len);
+            } catch (...) {  // no threads: the sequential reader alone
+                rd.splice_ = nullptr;
+            }
+            const auto t0 = std::chrono::steady_clock::now();
             rd.run();
+            if (std::getenv("MMGPU_FACTS_DEBUG"))
+                std::fprintf(stderr, "facts read %.1f ms\n",
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         } catch (const ParseFail& pf) {
             // facts.hpp:51-58 applied to nlohmann's byte count
             size_t line = 1, col = 1;
@@ -864,7 +1097,11 @@ mm_status finish(mm_facts* f, const char* text, size_t len) {
             // json::out_of_range 406, escapes parse_facts unwrapped
             throw FactsError{MM_E_RANGE, "number overflow parsing '" + no.token + "'"};
         }
+        const auto t1 = std::chrono::steady_clock::now();
         build(rd, *f);
+        if (std::getenv("MMGPU_FACTS_DEBUG"))
+            std::fprintf(stderr, "facts build %.1f ms\n",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
         f->status = MM_OK;
     } catch (const FactsError& e) {
         f->status = e.status;

@@ -147,6 +147,30 @@ def test_cpp_harness_reference_vs_dropin():
     assert "PASS" in res.stdout
 
 
+@pytest.mark.skipif(not HARNESS.exists(), reason="oracle/_ref/facts_parity not built (needs /root/reference)")
+def test_cpp_harness_parallel_reader():
+    # every document through the speculative parallel reader (chunks guessed,
+    # verified by the sequential walk), against the reference
+    import os
+    env = dict(os.environ, MMGPU_FACTS_PAR_MIN="1", MMGPU_FACTS_THREADS="5")
+    res = subprocess.run([str(HARNESS), "10000"], capture_output=True, text=True, timeout=600,
+                         preexec_fn=_limit_memory, env=env)
+    assert res.returncode == 0, res.stdout[-3000:]
+    assert "PASS" in res.stdout
+
+
+@pytest.mark.parametrize("threads", ["2", "7"])
+def test_parallel_reader_equals_sequential(monkeypatch, threads):
+    s = System.generate(3, 400, 6000, 3000, 5, 7, 0.3)
+    text = _canonical(s)
+    spaced = text.replace(",", ", ").replace("{", "{\n ")
+    monkeypatch.setenv("MMGPU_FACTS_PAR_MIN", "1")
+    monkeypatch.setenv("MMGPU_FACTS_THREADS", threads)
+    for doc in (text, spaced):
+        f = parse_facts(doc)
+        assert f.system.equals(s) and f.to_json() == text.encode()
+
+
 @pytest.mark.gpu
 def test_parsed_system_uploads():
     s = System.generate(1, 1000, 10000, 20000, 4, 4, 0.5)
