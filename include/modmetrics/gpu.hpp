@@ -53,7 +53,10 @@ namespace detail {
 // status -> the reference's exception types (no exception crosses the C ABI)
 inline void check(mm_status st, const mm_ctx* ctx, const char* what) {
     if (st == MM_OK) return;
-    const std::string msg = std::string(what) + ": " + (ctx ? mm_last_error(ctx) : "");
+    const char* detail = ctx ? mm_last_error(ctx)
+                       : st == MM_E_CUDA ? "no usable CUDA device (this engine has no CPU fallback)"
+                       : st == MM_E_RANGE ? "device index out of range" : "failed";
+    const std::string msg = std::string(what) + ": " + detail;
     switch (st) {
         case MM_E_RANGE: throw std::out_of_range(msg);
         case MM_E_ARG: throw std::invalid_argument(msg);

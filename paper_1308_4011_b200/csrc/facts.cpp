@@ -1170,6 +1170,13 @@ mm_status mm_facts_load(const char* path, mm_facts** out) {
     FILE* fp = std::fopen(path, "rb");
     if (!fp) { f->status = MM_E_IO; f->error = std::string("cannot open ") + path; return f->status; }
     std::string text;
+    // one read of the whole file when its size is known, chunks otherwise (pipes)
+    long sz = -1;
+    if (std::fseek(fp, 0, SEEK_END) == 0) { sz = std::ftell(fp); std::fseek(fp, 0, SEEK_SET); }
+    if (sz > 0) {
+        text.resize(size_t(sz));
+        text.resize(std::fread(&text[0], 1, size_t(sz), fp));
+    }
     char buf[1 << 16];
     size_t got;
     while ((got = std::fread(buf, 1, sizeof buf, fp)) > 0) text.append(buf, got);

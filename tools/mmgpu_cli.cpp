@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <fstream>
 #include <iostream>
 #include <optional>
@@ -114,9 +115,30 @@ struct Analysis {
 Analysis analyze_facts(const RunConfig& cfg) {
     Analysis a;
     if (cfg.engine == "gpu") {
+        // CUDA context creation (≈ 1-2 s on a fresh process) overlaps the
+        // facts load; a facts error still wins, as in the reference's order
+        std::exception_ptr ctx_err;
+        std::thread init([&] {
+            try {
+                Phase p("ctx_create");
+                a.engine.emplace(cfg.device);
+            } catch (...) {
+                ctx_err = std::current_exception();
+            }
+        });
         std::optional<gpu::Facts> facts;
-        { Phase p("load_facts"); facts.emplace(gpu::Facts::load(cfg.facts_path)); }
-        { Phase p("ctx_create"); a.engine.emplace(cfg.device); }
+        try {
+            Phase p("load_facts");
+            facts.emplace(gpu::Facts::load(cfg.facts_path));
+        } catch (...) {
+            init.join();
+            throw;
+        }
+        {
+            Phase p("ctx_wait");
+            init.join();
+        }
+        if (ctx_err) std::rethrow_exception(ctx_err);
         { Phase p("upload"); a.engine->upload(facts->system()); }  // CSR straight from the parse
         { Phase p("load_result"); a.loaded = facts->to_load_result(); }  // names and records for the renderers
         print_warnings(a.loaded.warnings);
