@@ -448,7 +448,8 @@ def ingest_bench(cfg):
     box: the config's canonical facts document (written by the product CLI's
     generator) parsed by mm_facts_load (C ABI, best of 3) against the
     reference's own parse_facts compiled in place (oracle/_ref/facts_parity
-    --bench, the same C4 document, one thread each). Never fails the line."""
+    --bench, the same C4 document; the reference single-threaded, ours with
+    its parallel reader on min(16, cores) threads). Never fails the line."""
     import ctypes as C
     cli, harness = ROOT / "tools" / "_build" / "mmgpu", ROOT / "oracle" / "_ref" / "facts_parity"
     try:
@@ -472,7 +473,8 @@ def ingest_bench(cfg):
                 if st != 0:
                     return {"error": f"mm_facts_load status {st}"}
                 best = min(best, dt)
-        out = {"doc_mb": size / 1e6, "csr_load_s": best, "csr_mb_per_s": size / 1e6 / best, "threads": 1,
+        threads = int(os.environ.get("MMGPU_FACTS_THREADS", min(16, os.cpu_count() or 1)))
+        out = {"doc_mb": size / 1e6, "csr_load_s": best, "csr_mb_per_s": size / 1e6 / best, "threads": threads,
                "path": "mm_facts_load (file read + streaming parse + semantic checks + CSR)"}
         if harness.exists():
             r = subprocess.run([str(harness), "--bench"], capture_output=True, text=True, timeout=300)
