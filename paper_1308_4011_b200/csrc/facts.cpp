@@ -743,8 +743,22 @@ void name_check(const NameField& f, const std::string& where, const std::string&
     if (f.kind != F_STRING) parse_error(field_where + ": expected a string name");
 }
 
+size_t env_size(const char* name, size_t dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? size_t(std::strtoull(v, nullptr, 10)) : dflt;
+}
+
+void dbg_mark(const char* what) {
+    static const bool on = std::getenv("MMGPU_FACTS_DEBUG") != nullptr;
+    if (!on) return;
+    static std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  build mark %-12s +%.1f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
 // Phase 2: the reference's semantic walk (facts.hpp:100-254) over the arrays.
-void build(Reader& r, mm_facts& f) {
+void build(Reader& r, mm_facts& f, bool parallel_ok) {
     if (r.top_kind != F_OBJECT) parse_error("top level must be an object");
     auto& V = f.violations;
     enum { NonDenseClassIds = MM_VK_NON_DENSE_CLASS_IDS, DupMethod = MM_VK_DUPLICATE_METHOD_MEMBERSHIP,
@@ -777,6 +791,7 @@ void build(Reader& r, mm_facts& f) {
     std::vector<Pending> pending;
     pending.reserve(r.methods.size());
 
+    dbg_mark("start");
     {   // size the id spaces once: max valid id + 1 over the declarations the
         // walk below will visit (it grows them the same way, facts.hpp:146-149)
         uint64_t ma = 0, mm = 0;
@@ -866,6 +881,7 @@ void build(Reader& r, mm_facts& f) {
         f.cmoff[ci + 1] = uint32_t(f.cmeth.size());
     }
 
+    dbg_mark("class_walk");
     for (uint64_t p = 0; p < mown.size(); ++p)
         if (mown[p] == kNone) {
             V.push_back({UnownedMethod, "method id " + std::to_string(p) + " is never declared"});
@@ -880,6 +896,7 @@ void build(Reader& r, mm_facts& f) {
     f.A = uint32_t(aown.size());
     const uint64_t M = f.M, A = f.A;
 
+    dbg_mark("unowned");
     // Second pass (facts.hpp:200-241): shape checks, self-call repair,
     // dangling targets; rows gathered into CSR by method id.
     std::vector<uint32_t> ccount(M + 1, 0), acount(M + 1, 0);
@@ -912,41 +929,66 @@ void build(Reader& r, mm_facts& f) {
         }
     }
 
+    dbg_mark("pass2_loop");
     if (!V.empty()) {
         throw FactsError{MM_E_VALIDATION, "facts validation failed with " + std::to_string(V.size()) +
                                               " violation(s): " + V.front().second};
     }
 
     // CSR rows: scatter, then sort-unique each row in place and compact.
+    // Rows land where their method id says; each pending method owns its
+    // row, so threads over ranges of `pending` never touch the same words.
+    const size_t T = parallel_ok ? std::max<size_t>(1, std::min<size_t>(
+        env_size("MMGPU_FACTS_THREADS", std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency()))), 16)) : 1;
+    auto parallel_pending = [&](auto&& body) {
+        const size_t n = pending.size();
+        if (T <= 1 || n < 2 * T) { body(size_t(0), n); return; }
+        std::vector<std::thread> th;
+        for (size_t k = 0; k < T; ++k) th.emplace_back([&, k] { body(n * k / T, n * (k + 1) / T); });
+        for (std::thread& t : th) t.join();
+    };
     auto scatter = [&](std::vector<uint32_t>& cnt, std::vector<uint32_t>& off, std::vector<uint32_t>& tgt, bool calls) {
         off.assign(M + 1, 0);
         for (uint64_t p = 0; p < M; ++p) off[p + 1] = off[p] + cnt[p];
         tgt.resize(off[M]);
-        std::vector<uint32_t> fill(off.begin(), off.end() - 1);
-        for (const Pending& pm : pending) {
-            const RawMethod& rm = r.methods[pm.raw];
-            const DepList& d = calls ? rm.calls : rm.accesses;
-            for (uint64_t i = d.begin; i < d.end; ++i) {
-                const uint64_t t = r.deps[i];
-                if (calls && t == pm.id) continue;
-                tgt[fill[pm.id]++] = uint32_t(t);
+        // fill each row, sort-unique it in place, keep its final length
+        std::vector<uint32_t> len(M, 0);
+        parallel_pending([&](size_t b, size_t e) {
+            for (size_t k = b; k < e; ++k) {
+                const Pending& pm = pending[k];
+                const RawMethod& rm = r.methods[pm.raw];
+                const DepList& d = calls ? rm.calls : rm.accesses;
+                uint32_t* row = tgt.data() + off[pm.id];
+                uint32_t* w = row;
+                for (uint64_t i = d.begin; i < d.end; ++i) {
+                    const uint64_t t = r.deps[i];
+                    if (calls && t == pm.id) continue;
+                    *w++ = uint32_t(t);
+                }
+                bool sorted = true;
+                for (uint32_t* q = row + 1; q < w; ++q) if (q[-1] >= q[0]) { sorted = false; break; }
+                if (!sorted) { std::sort(row, w); w = std::unique(row, w); }
+                len[pm.id] = uint32_t(w - row);
             }
+        });
+        std::vector<uint32_t> noff(M + 1, 0);
+        for (uint64_t p = 0; p < M; ++p) noff[p + 1] = noff[p] + len[p];
+        if (noff[M] != off[M]) {  // duplicates collapsed: compact into a fresh array
+            std::vector<uint32_t> packed(noff[M]);
+            parallel_pending([&](size_t b, size_t e) {
+                for (size_t k = b; k < e; ++k) {
+                    const uint32_t p = pending[k].id;
+                    std::copy(tgt.begin() + off[p], tgt.begin() + off[p] + len[p], packed.begin() + noff[p]);
+                }
+            });
+            tgt.swap(packed);
         }
-        uint32_t w = 0;
-        for (uint64_t p = 0; p < M; ++p) {
-            uint32_t* b = tgt.data() + off[p];
-            uint32_t* e = tgt.data() + off[p + 1];
-            bool sorted = true;
-            for (uint32_t* q = b + 1; q < e; ++q) if (q[-1] >= q[0]) { sorted = false; break; }
-            if (!sorted) { std::sort(b, e); e = std::unique(b, e); }
-            off[p] = w;
-            for (uint32_t* q = b; q < e; ++q) tgt[w++] = *q;
-        }
-        off[M] = w;
-        tgt.resize(w);
+        off.swap(noff);
     };
+    dbg_mark("pass2");
     scatter(ccount, f.call_off, f.call_tgt, true);
     scatter(acount, f.acc_off, f.acc_tgt, false);
+    dbg_mark("scatter_acc");
 }
 
 // ---------------------------------------------------------------------------
@@ -971,10 +1013,6 @@ struct Parallel {
     }
 };
 
-size_t env_size(const char* name, size_t dflt) {
-    const char* v = std::getenv(name);
-    return v && *v ? size_t(std::strtoull(v, nullptr, 10)) : dflt;
-}
 
 // depth change over [b, e), assuming the segment starts outside a string
 int64_t depth_delta(const unsigned char* s, size_t b, size_t e) {
@@ -1098,7 +1136,7 @@ mm_status finish(mm_facts* f, const char* text, size_t len) {
             throw FactsError{MM_E_RANGE, "number overflow parsing '" + no.token + "'"};
         }
         const auto t1 = std::chrono::steady_clock::now();
-        build(rd, *f);
+        build(rd, *f, len >= env_size("MMGPU_FACTS_PAR_MIN", size_t(8) << 20));
         if (std::getenv("MMGPU_FACTS_DEBUG"))
             std::fprintf(stderr, "facts build %.1f ms\n",
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
