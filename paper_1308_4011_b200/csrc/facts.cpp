@@ -792,27 +792,120 @@ void build(Reader& r, mm_facts& f, bool parallel_ok) {
     pending.reserve(r.methods.size());
 
     dbg_mark("start");
+    bool presized = false;
     {   // size the id spaces once: max valid id + 1 over the declarations the
         // walk below will visit (it grows them the same way, facts.hpp:146-149)
+        // per class range: (max attr id + 1, max method id + 1, stopped at a non-object class?)
+        auto scan = [&](uint64_t c0, uint64_t c1, uint64_t& ma, uint64_t& mm) {
+            for (uint64_t ci = c0; ci < c1; ++ci) {
+                const RawClass& rc = r.classes[r.cls_begin + ci];
+                if (!rc.is_object) return true;
+                if (rc.attrs_kind == F_ARRAY)
+                    for (uint64_t i = rc.attr_begin; i < rc.attr_end; ++i)
+                        if (valid_id(r.attrs[i].id)) ma = std::max(ma, r.attrs[i].id.value + 1);
+                if (rc.methods_kind == F_ARRAY)
+                    for (uint64_t i = rc.meth_begin; i < rc.meth_end; ++i)
+                        if (valid_id(r.methods[i].id)) mm = std::max(mm, r.methods[i].id.value + 1);
+            }
+            return false;
+        };
+        const size_t TS = parallel_ok && nc >= 2 ? size_t(16) : size_t(1);
+        std::vector<uint64_t> pa(TS, 0), pm(TS, 0);
+        std::vector<char> stop(TS, 0);
+        {
+            std::vector<std::thread> th;
+            for (size_t k = 1; k < TS; ++k)
+                th.emplace_back([&, k] { stop[k] = scan(nc * k / TS, nc * (k + 1) / TS, pa[k], pm[k]); });
+            stop[0] = scan(0, nc / TS, pa[0], pm[0]);
+            for (std::thread& t : th) t.join();
+        }
         uint64_t ma = 0, mm = 0;
-        for (uint64_t ci = 0; ci < nc; ++ci) {
-            const RawClass& rc = r.classes[r.cls_begin + ci];
-            if (!rc.is_object) break;
-            if (rc.attrs_kind == F_ARRAY)
-                for (uint64_t i = rc.attr_begin; i < rc.attr_end; ++i)
-                    if (valid_id(r.attrs[i].id)) ma = std::max(ma, r.attrs[i].id.value + 1);
-            if (rc.methods_kind == F_ARRAY)
-                for (uint64_t i = rc.meth_begin; i < rc.meth_end; ++i)
-                    if (valid_id(r.methods[i].id)) mm = std::max(mm, r.methods[i].id.value + 1);
+        for (size_t k = 0; k < TS; ++k) {  // ranges in order, up to the first non-object class
+            ma = std::max(ma, pa[k]);
+            mm = std::max(mm, pm[k]);
+            if (stop[k]) break;
         }
         if (ma < id_cap && mm < id_cap) {
             // the final sizes are exactly these (max visited id + 1), so
             // growing to them up front is the same as growing id by id
             aown.assign(ma, kNone); f.attribute_name.resize(ma);
             mown.assign(mm, kNone); f.method_name.resize(mm);
+            presized = true;
         }
     }
-    for (uint64_t ci = 0; ci < nc; ++ci) {
+    // Optimistic parallel walk for the common case — every field well-formed,
+    // class ids dense, no id declared twice — over class ranges (ownership
+    // claimed with compare-and-swap). Its result is then exactly the
+    // sequential walk's. Any deviation anywhere: undo and walk sequentially,
+    // which produces the reference's errors in the reference's order.
+    dbg_mark("presize");
+    bool walked = false;
+    const size_t TW = parallel_ok && presized && nc >= 2
+        ? std::min<size_t>(env_size("MMGPU_FACTS_THREADS", std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency()))), 16)
+        : 1;
+    if (TW > 1) {
+        std::vector<uint32_t> apre(nc + 1, 0), mpre(nc + 1, 0);
+        for (uint64_t ci = 0; ci < nc; ++ci) {
+            const RawClass& rc = r.classes[r.cls_begin + ci];
+            apre[ci + 1] = apre[ci] + uint32_t(rc.attrs_kind == F_ARRAY ? rc.attr_end - rc.attr_begin : 0);
+            mpre[ci + 1] = mpre[ci] + uint32_t(rc.methods_kind == F_ARRAY ? rc.meth_end - rc.meth_begin : 0);
+        }
+        f.cattr.assign(apre[nc], 0);
+        f.cmeth.assign(mpre[nc], 0);
+        pending.assign(mpre[nc], Pending{});
+        int bad = 0;
+        auto claim = [](uint32_t* slot, uint32_t v) {
+            uint32_t want = kNone;
+            return __atomic_compare_exchange_n(slot, &want, v, false, __ATOMIC_RELAXED, __ATOMIC_RELAXED);
+        };
+        auto walk = [&](uint64_t c0, uint64_t c1) {
+            for (uint64_t ci = c0; ci < c1; ++ci) {
+                if (__atomic_load_n(&bad, __ATOMIC_RELAXED)) return;
+                const RawClass& rc = r.classes[r.cls_begin + ci];
+                if (!rc.is_object || !valid_id(rc.id) || rc.id.value != ci || rc.name.kind != F_STRING ||
+                    rc.attrs_kind != F_ARRAY || rc.methods_kind != F_ARRAY) { __atomic_store_n(&bad, 1, __ATOMIC_RELAXED); return; }
+                f.class_ids[ci] = uint32_t(ci);
+                f.class_name[ci] = rc.name.s;
+                uint32_t* ca = f.cattr.data() + apre[ci];
+                for (uint64_t ai = 0; ai < rc.attr_end - rc.attr_begin; ++ai) {
+                    const RawAttr& ra = r.attrs[rc.attr_begin + ai];
+                    if (!ra.is_object || !valid_id(ra.id) || ra.name.kind != F_STRING ||
+                        !claim(&aown[ra.id.value], uint32_t(ci))) { __atomic_store_n(&bad, 1, __ATOMIC_RELAXED); return; }
+                    f.attribute_name[ra.id.value] = ra.name.s;
+                    ca[ai] = uint32_t(ra.id.value);
+                }
+                if (!std::is_sorted(ca, f.cattr.data() + apre[ci + 1])) std::sort(ca, f.cattr.data() + apre[ci + 1]);
+                uint32_t* cm = f.cmeth.data() + mpre[ci];
+                for (uint64_t mi = 0; mi < rc.meth_end - rc.meth_begin; ++mi) {
+                    const RawMethod& rm = r.methods[rc.meth_begin + mi];
+                    if (!rm.is_object || !valid_id(rm.id) || rm.name.kind != F_STRING ||
+                        !claim(&mown[rm.id.value], uint32_t(ci))) { __atomic_store_n(&bad, 1, __ATOMIC_RELAXED); return; }
+                    f.method_name[rm.id.value] = rm.name.s;
+                    cm[mi] = uint32_t(rm.id.value);
+                    pending[mpre[ci] + mi] = Pending{uint32_t(rm.id.value), rc.meth_begin + mi, uint32_t(ci), uint32_t(mi)};
+                }
+                if (!std::is_sorted(cm, f.cmeth.data() + mpre[ci + 1])) std::sort(cm, f.cmeth.data() + mpre[ci + 1]);
+            }
+        };
+        {
+            std::vector<std::thread> th;
+            for (size_t k = 0; k < TW; ++k) th.emplace_back([&, k] { walk(nc * k / TW, nc * (k + 1) / TW); });
+            for (std::thread& t : th) t.join();
+        }
+        dbg_mark(bad ? "pwalk_bad" : "pwalk_ok");
+        if (!bad) {
+            f.caoff.swap(apre);
+            f.cmoff.swap(mpre);
+            walked = true;
+        } else {  // undo: the sequential walk starts from the presized, unowned tables
+            std::fill(aown.begin(), aown.end(), kNone);
+            std::fill(mown.begin(), mown.end(), kNone);
+            f.cattr.clear();
+            f.cmeth.clear();
+            pending.clear();
+        }
+    }
+    for (uint64_t ci = 0; ci < nc && !walked; ++ci) {
         const RawClass& rc = r.classes[r.cls_begin + ci];
         const std::string cw = "classes[" + std::to_string(ci) + "]";
         if (!rc.is_object) parse_error(cw + ": expected an object");
@@ -900,7 +993,38 @@ void build(Reader& r, mm_facts& f, bool parallel_ok) {
     // Second pass (facts.hpp:200-241): shape checks, self-call repair,
     // dangling targets; rows gathered into CSR by method id.
     std::vector<uint32_t> ccount(M + 1, 0), acount(M + 1, 0);
+    bool counted = false;
+    if (parallel_ok && pending.size() >= 2) {
+        // optimistic: no shape error, self-call or dangling target anywhere
+        // (each pending method owns its counters); otherwise recount below
+        int bad = 0;
+        const size_t TP = 16, n = pending.size();
+        std::vector<std::thread> th;
+        for (size_t k = 0; k < TP; ++k)
+            th.emplace_back([&, k] {
+                for (size_t j = n * k / TP; j < n * (k + 1) / TP; ++j) {
+                    const Pending& pm = pending[j];
+                    const RawMethod& rm = r.methods[pm.raw];
+                    if (rm.calls.kind != F_ARRAY || rm.accesses.kind != F_ARRAY) { __atomic_store_n(&bad, 1, __ATOMIC_RELAXED); return; }
+                    for (uint64_t i = rm.calls.begin; i < rm.calls.end; ++i) {
+                        const uint64_t t = r.deps[i];
+                        if (t >= M || t == pm.id) { __atomic_store_n(&bad, 1, __ATOMIC_RELAXED); return; }
+                    }
+                    for (uint64_t i = rm.accesses.begin; i < rm.accesses.end; ++i)
+                        if (r.deps[i] >= A) { __atomic_store_n(&bad, 1, __ATOMIC_RELAXED); return; }
+                    ccount[pm.id] = uint32_t(rm.calls.end - rm.calls.begin);
+                    acount[pm.id] = uint32_t(rm.accesses.end - rm.accesses.begin);
+                }
+            });
+        for (std::thread& t : th) t.join();
+        if (!bad) counted = true;
+        else {
+            std::fill(ccount.begin(), ccount.end(), 0u);
+            std::fill(acount.begin(), acount.end(), 0u);
+        }
+    }
     for (const Pending& pm : pending) {
+        if (counted) break;
         const RawMethod& rm = r.methods[pm.raw];
         auto where = [&] { return "classes[" + std::to_string(pm.ci) + "].methods[" + std::to_string(pm.mi) + "]"; };
         auto shape = [&](const DepList& d, const char* nm) {
