@@ -1333,40 +1333,40 @@ mm_status mm_facts_load(const char* path, mm_facts** out) {
     if (!f) return MM_E_OOM;
     *out = f;
     // facts.hpp:258-265. A regular file is mapped, not copied: the reader
-    // threads fault its pages in in parallel.
-    {
-        const int fd = ::open(path, O_RDONLY);
-        struct stat st;
-        if (fd >= 0 && ::fstat(fd, &st) == 0 && S_ISREG(st.st_mode) && st.st_size > 0) {
-            const size_t n = size_t(st.st_size);
-            void* m = ::mmap(nullptr, n, PROT_READ, MAP_PRIVATE, fd, 0);
+    // threads fault its pages in in parallel. Other files are read to EOF.
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) { f->status = MM_E_IO; f->error = std::string("cannot open ") + path; return f->status; }
+    struct stat st;
+    if (::fstat(fd, &st) == 0 && S_ISDIR(st.st_mode)) {
+        // std::ifstream opens a directory and then reads nothing (no badbit):
+        // the reference parses "" -> JSON parse error at line 1, column 1
+        ::close(fd);
+        return finish(f, "", 0);
+    }
+    if (S_ISREG(st.st_mode) && st.st_size > 0) {
+        const size_t n = size_t(st.st_size);
+        void* m = ::mmap(nullptr, n, PROT_READ, MAP_PRIVATE, fd, 0);
+        if (m != MAP_FAILED) {
             ::close(fd);
-            if (m != MAP_FAILED) {
-                ::madvise(m, n, MADV_SEQUENTIAL);
-                const mm_status r = finish(f, static_cast<const char*>(m), n);
-                ::munmap(m, n);
-                return r;
-            }
-        } else if (fd >= 0) {
-            ::close(fd);
+            ::madvise(m, n, MADV_SEQUENTIAL);
+            const mm_status r = finish(f, static_cast<const char*>(m), n);
+            ::munmap(m, n);
+            return r;
         }
     }
-    FILE* fp = std::fopen(path, "rb");
-    if (!fp) { f->status = MM_E_IO; f->error = std::string("cannot open ") + path; return f->status; }
     std::string text;
-    // one read of the whole file when its size is known, chunks otherwise (pipes)
-    long sz = -1;
-    if (std::fseek(fp, 0, SEEK_END) == 0) { sz = std::ftell(fp); std::fseek(fp, 0, SEEK_SET); }
-    if (sz > 0) {
-        text.resize(size_t(sz));
-        text.resize(std::fread(&text[0], 1, size_t(sz), fp));
-    }
     char buf[1 << 16];
-    size_t got;
-    while ((got = std::fread(buf, 1, sizeof buf, fp)) > 0) text.append(buf, got);
-    const bool bad = std::ferror(fp) != 0;
-    std::fclose(fp);
-    if (bad) { f->status = MM_E_IO; f->error = std::string("read error on ") + path; return f->status; }
+    for (;;) {
+        const ssize_t got = ::read(fd, buf, sizeof buf);
+        if (got > 0) { text.append(buf, size_t(got)); continue; }
+        if (got == 0) break;
+        if (errno == EINTR) continue;
+        ::close(fd);
+        f->status = MM_E_IO;
+        f->error = std::string("read error on ") + path;
+        return f->status;
+    }
+    ::close(fd);
     return finish(f, text.data(), text.size());
 }
 

@@ -95,6 +95,13 @@ def test_load_facts_io(tmp_path):
     p.write_text('{"classes": [], "schema_version": "1"}')
     f = load_facts(p)
     assert f.system.n_classes == 0 and f.to_json() == b'{"classes":[],"schema_version":"1"}\n'
+    # a directory opens and reads as nothing under std::ifstream, and so does an
+    # empty file: the reference then fails to parse "" (checked against it by hand)
+    empty = tmp_path / "empty.json"
+    empty.write_bytes(b"")
+    for q in (tmp_path, empty):
+        with pytest.raises(FactsParseError, match=r"facts: JSON parse error at line 1, column 1$"):
+            load_facts(q)
 
 
 def _canonical(s: System) -> str:
