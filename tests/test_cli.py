@@ -67,6 +67,16 @@ def test_exit_codes(tmp_path):
     assert cli(check=False).returncode == 64
 
 
+def test_gpu_engine_never_falls_back(tmp_path):
+    # no device here: the gpu engine (the default) must fail loudly, not compute on the CPU
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    p = gen(tmp_path, "g", 4, 20, 10)
+    r = cli("analyze", "--facts", p, check=False)
+    assert r.returncode == 1 and b"no usable CUDA device" in r.stderr and not r.stdout
+
+
 SUGGEST_VARIANTS = [
     (),
     ("--format", "text"),
