@@ -15,6 +15,7 @@
 #include <memory>
 #include <string>
 #include <string_view>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -66,23 +67,26 @@ public:
         m.method_owner.assign(s.method_owner, s.method_owner + s.n_methods);
         m.attribute_owner.assign(s.attribute_owner, s.attribute_owner + s.n_attributes);
         m.method_names.resize(s.n_methods);
-        for (uint32_t p = 0; p < s.n_methods; ++p) {
-            size_t len = 0;
-            const char* nm = mm_facts_method_name(f_.get(), p, &len);
-            m.method_names[p].assign(nm, len);
-        }
         m.attribute_names.resize(s.n_attributes);
-        for (uint32_t a = 0; a < s.n_attributes; ++a) {
-            size_t len = 0;
-            const char* nm = mm_facts_attribute_name(f_.get(), a, &len);
-            m.attribute_names[a].assign(nm, len);
-        }
         r.deps.calls.resize(s.n_methods);
         r.deps.accesses.resize(s.n_methods);
-        for (uint32_t p = 0; p < s.n_methods; ++p) {
-            r.deps.calls[p].assign(s.call_tgt + s.call_off[p], s.call_tgt + s.call_off[p + 1]);
-            r.deps.accesses[p].assign(s.acc_tgt + s.acc_off[p], s.acc_tgt + s.acc_off[p + 1]);
-        }
+        // every index is written by one thread only
+        for_ranges(s.n_methods, [&](uint32_t b, uint32_t e) {
+            for (uint32_t p = b; p < e; ++p) {
+                size_t len = 0;
+                const char* nm = mm_facts_method_name(f_.get(), p, &len);
+                m.method_names[p].assign(nm, len);
+                r.deps.calls[p].assign(s.call_tgt + s.call_off[p], s.call_tgt + s.call_off[p + 1]);
+                r.deps.accesses[p].assign(s.acc_tgt + s.acc_off[p], s.acc_tgt + s.acc_off[p + 1]);
+            }
+        });
+        for_ranges(s.n_attributes, [&](uint32_t b, uint32_t e) {
+            for (uint32_t a = b; a < e; ++a) {
+                size_t len = 0;
+                const char* nm = mm_facts_attribute_name(f_.get(), a, &len);
+                m.attribute_names[a].assign(nm, len);
+            }
+        });
         r.warnings = warnings();
         return r;
     }
@@ -97,6 +101,17 @@ public:
     }
 
 private:
+    template <class Fn>
+    static void for_ranges(uint32_t n, Fn&& fn) {
+        const unsigned hw = std::thread::hardware_concurrency();
+        const uint32_t T = n >= (1u << 16) ? std::min(8u, hw ? hw : 1u) : 1u;
+        if (T <= 1) { fn(0u, n); return; }
+        std::vector<std::thread> th;
+        for (uint32_t k = 0; k < T; ++k)
+            th.emplace_back([&, k] { fn(uint32_t(uint64_t(n) * k / T), uint32_t(uint64_t(n) * (k + 1) / T)); });
+        for (std::thread& t : th) t.join();
+    }
+
     struct Del {
         void operator()(mm_facts* f) const { mm_facts_free(f); }
     };
