@@ -57,6 +57,7 @@ WORKLOAD_NAMES = {
     "c5": "C5 dense-coupling 5k classes x 500 methods / 320k attributes",
     "c4x8": "C4 shape x8: 800k classes / 8M methods / 16M attributes",
 }
+DATA = "synthetic (the reference generate(), SURVEY.md §8d seeds; C3 Zipf ownership + the reference's draws)"
 METRIC = "move-method candidates scored/sec (full LCOM+CBO recompute + cohesion/coupling sweep per step)"
 UNIT = "candidates/s"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
@@ -202,74 +203,128 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference (oracle/_ref) or the oracle port, bounded sample
+# CPU baseline / reference arm: the reference compiled in place (oracle/_ref)
 # ---------------------------------------------------------------------------
 
-def cpu_baseline(sys_, n_cand_total: int, frac: float = 0.25) -> dict:
-    import oracle  # CPU baseline leg: the reference compiled from its own headers
-    threads = os.cpu_count() or 1
-    C = sys_.n_classes
-    c_hi = max(1, int(C * frac))
-    used = sys_.used_classes()
-    cand_sample = int(used[sys_.class_methods[:sys_.class_method_off[c_hi]]].sum())
-    if oracle.ref_available():
-        R = oracle.RefModel(sys_)
+def host_cpu() -> dict:
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"nproc": os.cpu_count(), "lscpu_model": model}
+
+
+class RefJob:
+    """One step of the reference's own CPU path on the host cores, on the same
+    workload: parallel_class_metrics + parallel_lcom_ck (parallel.hpp:149,164)
+    with n_workers = all host threads, compute_thresholds (suggest.hpp:46),
+    then the cohesion+coupling sweep — the reference's suggest_all is
+    single-threaded, so its per-method body (detail::used_classes +
+    detail::emit_for_method + what_if_move) runs on all host threads over the
+    reference's detail::run_partitioned ranges and suggest_all's merge/sort
+    follows ("reference logic, harness threads", SURVEY.md §8d item 4;
+    oracle/ref_shim.cpp ref_sweep). The input comes from the reference's own
+    generate() (no product library is loaded). `frac` < 1 sweeps every
+    k-th method only (bounded sample) and is extrapolated by candidate
+    count; the measured sample time is reported beside it."""
+
+    def __init__(self, config: str):
+        import oracle  # CPU baseline / reference arm only
+        self.oracle = oracle
+        if not oracle.ref_available():
+            raise RuntimeError("oracle/_ref/libmmref.so missing (build() compiles it where /root/reference exists)")
+        self.cfg = CONFIGS[config]
         t0 = time.perf_counter()
-        lcom, ck, cbo = R.class_metrics(threads)          # parallel_class_metrics + parallel_lcom_ck
-        t1 = time.perf_counter()
-        thr = oracle.ref_thresholds(lcom, cbo)            # compute_thresholds
-        t2 = time.perf_counter()
-        n_s, n_c = R.sweep_sample(lcom, cbo, thr.lcom, thr.cbo, 0, c_hi, threads)
-        t3 = time.perf_counter()
-        assert n_c == cand_sample
-        kind, cores = "reference", threads
-        sample = (f"reference headers compiled in place (oracle/_ref): parallel_class_metrics+parallel_lcom_ck over "
-                  f"all {C} classes on {threads} threads; compute_thresholds; cohesion+coupling sweep "
-                  f"(detail::used_classes/emit_for_method/what_if_move, 'reference logic, harness threads' via "
-                  f"detail::run_partitioned) over classes [0,{c_hi}) = {cand_sample} candidates, extrapolated "
-                  f"by candidate count to {n_cand_total}")
-    else:
+        self.R = oracle.ref_generate_model(**self.cfg)
+        self.n_cand = self.R.candidates()
+        self.gen_s = time.perf_counter() - t0
+        self.threads = os.cpu_count() or 1
+        self.n_methods = self.R.n_methods
+
+    def step(self, frac: float = 1.0) -> dict:
+        o = self.oracle
         t0 = time.perf_counter()
-        lcom, ck, cbo = oracle.class_metrics(sys_)
+        lcom, ck, cbo = self.R.class_metrics(self.threads)
         t1 = time.perf_counter()
-        thr = oracle.thresholds(lcom, cbo)
+        thr = o.ref_thresholds(lcom, cbo)
         t2 = time.perf_counter()
-        oracle.suggest(sys_, lcom, cbo, 6, 0, False, 1, thr.lcom, thr.cbo, class_range=(0, c_hi))
+        methods = None
+        if frac < 1.0:
+            k = max(1, int(round(1.0 / frac)))
+            methods = np.arange(0, self.n_methods, k, dtype=np.uint32)
+        recs, cand = self.R.sweep(lcom, cbo, abi_mask(), thr.lcom, thr.cbo, 0, False, methods=methods,
+                                  n_workers=self.threads, dynamic=False)
         t3 = time.perf_counter()
-        kind, cores = "port", 1
-        sample = (f"oracle/liboracle.so C restatement, single thread: metrics over all classes, sweep over classes "
-                  f"[0,{c_hi}) = {cand_sample} candidates, extrapolated by candidate count")
-    t_full = (t1 - t0) + (t2 - t1) + (t3 - t2) * (n_cand_total / max(1, cand_sample))
-    return {"value": n_cand_total / t_full, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
-            "metric_pass_s": t1 - t0, "sweep_sample_s": t3 - t2, "full_job_s_extrapolated": t_full}
+        sweep_s = t3 - t2
+        full_s = (t1 - t0) + (t2 - t1) + sweep_s * (self.n_cand / max(1, cand))
+        return {"metric_pass_s": t1 - t0, "thresholds_s": t2 - t1, "sweep_s": sweep_s, "sweep_candidates": cand,
+                "suggestions": len(recs), "full_job_s": full_s, "measured_s": t3 - t0,
+                "extrapolated": methods is not None}
+
+    def describe(self, r: dict) -> str:
+        what = ("the full job" if not r["extrapolated"] else
+                f"a sample (every {int(round(self.n_cand / max(1, r['sweep_candidates'])))}-th method's sweep, "
+                f"{r['sweep_candidates']} of {self.n_cand} candidates, {r['measured_s']:.2f} s measured, "
+                f"extrapolated by candidate count)")
+        return (f"reference headers compiled in place (oracle/_ref, g++ -O3 -DNDEBUG): parallel_class_metrics + "
+                f"parallel_lcom_ck on {self.threads} threads, compute_thresholds, cohesion+coupling sweep with the "
+                f"reference's per-method code on {self.threads} threads (detail::run_partitioned) + suggest_all's "
+                f"merge; input from the reference's generate(); {what}")
+
+
+def abi_mask() -> int:
+    return (1 << 1) | (1 << 2)  # MM_CRIT_COHESION | MM_CRIT_COUPLING (include/mmgpu.h)
+
+
+def cpu_baseline(config: str, budget_s: float = 30.0) -> dict:
+    """Bounded CPU baseline for our arm's line (rank 0, N=1): one full
+    reference job when it fits the budget, else a method sample."""
+    job = RefJob(config)
+    frac = 1.0
+    r = job.step(0.02)  # probe: 2 % of the sweep
+    est = r["metric_pass_s"] + r["sweep_s"] * 50
+    if est > budget_s:
+        frac = max(0.001, min(1.0, (budget_s - r["metric_pass_s"]) / max(1e-9, r["sweep_s"] * 50)))
+    r = job.step(frac)
+    return {"value": job.n_cand / r["full_job_s"], "unit": UNIT, "cores": job.threads, "kind": "reference",
+            "sample": job.describe(r), "host": host_cpu(), **r}
 
 
 def run_reference(args) -> None:
     rank, world, _ = dist_env()
     if rank != 0:
-        return
-    from paper_1308_4011_b200 import System
-    cfg = CONFIGS[args.config]
-    s = System.generate(**cfg)
-    n_cand = s.n_candidates()
-    frac = args.cpu_frac
+        return  # the reference CPU path runs once, on rank 0
+    job = RefJob(args.config)
+    # size each step so the whole --steps K --warmup W run ends in a few minutes
+    probe = job.step(0.02)
+    full_est = probe["metric_pass_s"] + probe["sweep_s"] * 50
+    budget = 180.0 / max(1, args.steps + args.warmup)
+    frac = 1.0 if full_est <= budget else max(0.001, (budget - probe["metric_pass_s"]) / max(1e-9, probe["sweep_s"] * 50))
     for _ in range(args.warmup):
-        cpu_baseline(s, n_cand, frac)
-    vals, last = [], None
-    for _ in range(args.steps):
-        last = cpu_baseline(s, n_cand, frac)
-        vals.append(last["full_job_s_extrapolated"])
-    t = float(np.mean(vals))
-    v = n_cand / t
-    cb = {k: last[k] for k in ("kind", "cores", "sample")}
-    cb.update({"value": v, "unit": UNIT})
+        job.step(frac)
+    rs = [job.step(frac) for _ in range(args.steps)]
+    t = float(np.mean([r["full_job_s"] for r in rs]))
+    v = job.n_cand / t
+    last = rs[-1]
+    cb = {"value": v, "unit": UNIT, "kind": "reference", "cores": job.threads, "sample": job.describe(last),
+          "host": host_cpu(), "measured_s_per_step": float(np.mean([r["measured_s"] for r in rs])),
+          "extrapolated": last["extrapolated"], "suggestions": last["suggestions"]}
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u32+f64", "data": "synthetic (reference generate(), SURVEY.md §8d)",
-        "config": {"workload": WORKLOAD_NAMES[args.config], **cfg, "candidates": n_cand},
+        "vs_baseline": None, "dtype": "u32+f64", "data": DATA, "config": bench_config(args.config, job.n_cand),
         "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "metric_pass_ms": float(np.mean([r["metric_pass_s"] for r in rs])) * 1e3,
     }), flush=True)
+
+
+def bench_config(config: str, n_cand: int) -> dict:
+    """The workload, identical on both arms (the driver compares them)."""
+    return {"workload": WORKLOAD_NAMES[config], **CONFIGS[config], "candidates": n_cand,
+            "l2": "inputs resident; L2 flushed between timed steps by a 256 MiB device write outside the events"}
 
 
 # ---------------------------------------------------------------------------
@@ -408,21 +463,23 @@ def run_ours(args) -> None:
     cb = None
     ingest = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cb = cpu_baseline(s, n_cand, args.cpu_frac)
+        cb = cpu_baseline(args.config)
+        if cb.get("suggestions") is not None and not cb.get("extrapolated") and world == 1:
+            cb["same_list_length_as_gpu"] = int(cb["suggestions"]) == int(n_sugg_local)
         if args.config == "c4":
             ingest = ingest_bench(cfg)
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u32+f64",
-            "data": "synthetic (reference generate() port, SURVEY.md §8d seeds)",
-            "config": {"workload": WORKLOAD_NAMES[args.config], **cfg, "candidates": n_cand,
-                       "parallelism": f"dp{world} (class-range shards of the sweep, metric pass replicated)",
-                       "l2": "flushed between timed steps (256 MiB device write outside the events)",
-                       "timing": "ms_per_step: K uninstrumented graph replays; kernels: a second K-step pass "
-                                 "with CUDA events around each kernel (ms_per_step_instrumented)",
-                       "criteria": "cohesion+coupling, union, best-only, device mean thresholds"},
+            "vs_baseline": None, "dtype": "u32+f64", "data": DATA,
+            "config": bench_config(args.config, n_cand),
+            "parallelism": f"dp{world} (class-range shards of the sweep, metric pass replicated, exact-count "
+                           f"record exchange over NCCL)",
+            "timing": "ms_per_step: K uninstrumented graph replays between CUDA events on the engine stream, max "
+                      "over ranks; kernels: a second K-step pass with CUDA events around each kernel "
+                      "(ms_per_step_instrumented)",
+            "criteria": "cohesion+coupling, union, best-only, device mean thresholds",
             "roofline": roofline,
             "cpu_baseline": cb,
             "e2e": e2e,
@@ -541,6 +598,32 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
                     "class_metrics_async (D2H under the sweep) -> sweep (device thresholds) -> suggestions (D2H)"}
 
 
+def ensure_world(args) -> None:
+    """--gpus N means N ranks, one per GPU: under torchrun WORLD_SIZE must be
+    N; run directly with N > 1 this process re-launches itself under
+    torch.distributed.run (127.0.0.1) — or fails loudly when fewer than N GPUs
+    are visible. Never a silent 1-GPU measurement."""
+    _, world, _ = dist_env()
+    if "WORLD_SIZE" in os.environ:
+        if world != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+        return
+    if args.gpus <= 1:
+        return
+    if args.impl == "ours":
+        import torch
+        n_dev = torch.cuda.device_count()
+        if n_dev < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} requested but only {n_dev} CUDA device(s) are visible")
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -548,13 +631,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")
-    ap.add_argument("--cpu-frac", type=float, default=0.25, help="class fraction swept by the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--traffic-bytes", type=float, default=None,
                     help="dram bytes per launch of the dominant kernel from an ncu --set full capture")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus < 1:
+        sys.exit("bench.py: --gpus must be >= 1")
+    ensure_world(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -39,7 +39,8 @@ typedef enum mm_status {
     MM_E_CAPACITY = 7,    /* caller buffer too small; *n_out holds the needed count */
     MM_E_PARSE = 8,       /* modmetrics::ParseError      (facts.hpp:22-24), see mmfacts.h */
     MM_E_VALIDATION = 9,  /* modmetrics::ValidationError (facts.hpp:28-37) */
-    MM_E_IO = 10          /* modmetrics::IoError         (facts.hpp:39-41) */
+    MM_E_IO = 10,         /* modmetrics::IoError         (facts.hpp:39-41) */
+    MM_E_NCCL = 11        /* NCCL missing or failing (multi-GPU groups, mm_group_*) */
 } mm_status;
 
 /* Criterion bits: bit (1 << Criterion) with Criterion as in suggest.hpp:17
@@ -152,16 +153,18 @@ typedef struct mm_sweep_params {
     double thr_lcom;         /* Thresholds::lcom  (gate: lcom[c] > thr_lcom, suggest.hpp:246) */
     double thr_cbo;          /* Thresholds::cbo   (gate: (double)cbo[c] > thr_cbo, suggest.hpp:273) */
     uint32_t class_begin;
-    uint32_t class_end;      /* 0 == n_classes */
+    uint32_t class_end;      /* 0 == n_classes, unless flags has MM_SWEEP_EXACT_RANGE */
     uint32_t threshold_source; /* MM_THR_EXPLICIT: thr_lcom/thr_cbo above;
                                   MM_THR_DEVICE_MEANS: the means computed on the device by the
                                   last mm_compute_metrics (compute_thresholds with no overrides),
                                   read without a host round trip */
-    uint32_t pad;
+    uint32_t flags;          /* MM_SWEEP_* */
 } mm_sweep_params;
 
 #define MM_THR_EXPLICIT 0
 #define MM_THR_DEVICE_MEANS 1
+/* class_end is taken literally (an empty range [b, b) sweeps nothing) */
+#define MM_SWEEP_EXACT_RANGE 1u
 
 typedef struct mm_sweep_stats {
     uint64_t candidates;     /* (method, destination) pairs scored, ungated: Σ|used_classes(u)| */
@@ -186,6 +189,8 @@ int mm_abi_version(void);
 /* Run all work on this cudaStream_t (e.g. torch's current stream). NULL = the ctx's own stream. */
 mm_status mm_ctx_set_stream(mm_ctx* ctx, void* cuda_stream);
 mm_status mm_ctx_synchronize(mm_ctx* ctx);
+/* The stream the context's work runs on (its own, or the one set above). */
+mm_status mm_ctx_stream(mm_ctx* ctx, void** cuda_stream);
 /* Per-kernel CUDA-event timing (adds two event records per launch). */
 mm_status mm_ctx_set_profiling(mm_ctx* ctx, int on);
 mm_status mm_kernel_stats(mm_ctx* ctx, mm_kernel_stat* out, int cap, int* n_out);
@@ -298,6 +303,10 @@ mm_status mm_collect_timings(mm_ctx* ctx);
 /* Device pointer to the last sweep's records (mm_suggestion[n]), for
  * device-side exchange (NCCL all-gather) without a host round trip. */
 mm_status mm_sweep_device_result(mm_ctx* ctx, const void** dev_records, uint64_t* n);
+/* Device address of the last sweep's record count (uint64, written by the
+ * sweep's kernels on the context's stream): device-side exchanges read it
+ * without a host round trip (mm_group_run all-gathers it over NCCL). */
+mm_status mm_sweep_device_count(mm_ctx* ctx, const uint64_t** dev_count);
 mm_status mm_sweep_stats_get(mm_ctx* ctx, mm_sweep_stats* out);
 /* Copies the last sweep's records to host memory; MM_E_CAPACITY (with
  * *n_out = needed) when cap is too small. */
@@ -312,6 +321,45 @@ mm_status mm_suggest(mm_ctx* ctx, const mm_sweep_params* p, mm_suggestion* out, 
  * driver). */
 mm_status mm_pinned_alloc(uint64_t bytes, void** out);
 void mm_pinned_free(void* p);
+
+/* ---- multi-GPU groups (SURVEY.md §8b mm_comm_init, §8e) ---------------- */
+/* One process, n GPUs: the reference's n_workers (parallel.hpp:149, :164,
+ * plan_partition :20-41) mapped to GPUs. Each GPU holds the whole system and
+ * recomputes the metric pass (replicas); the candidate sweep runs on
+ * cost-balanced contiguous class ranges (mm_plan_shards), and the shard
+ * lists are exchanged over NCCL with exact counts — an all-gather of the
+ * per-GPU record counts, then one broadcast per non-empty shard of exactly
+ * its records into every GPU's assembled list — which in rank order is
+ * suggest_all's ordered list (suggest.hpp:344-348). NCCL is dlopen'ed
+ * (libnccl.so.2); a one-GPU group needs none. devices == NULL: 0..n-1.
+ * n == 0 -> MM_E_ARG (plan_partition's zero-worker check, parallel.hpp:29);
+ * a bad or repeated device -> MM_E_RANGE; NCCL unusable for n > 1 ->
+ * MM_E_NCCL. mm_group_ctx gives each GPU's context (metrics, what-if, ...). */
+typedef struct mm_group mm_group;
+mm_status mm_group_create(const int* devices, int n, mm_group** out);
+void mm_group_destroy(mm_group* g);
+const char* mm_group_last_error(const mm_group* g);
+int mm_group_size(const mm_group* g);
+int mm_group_uses_nccl(const mm_group* g);
+mm_ctx* mm_group_ctx(mm_group* g, int i);
+/* Upload to every GPU (one host thread each) and plan the shards. */
+mm_status mm_group_upload(mm_group* g, const mm_system* sys);
+/* Shard i's class range [*class_begin, *class_end). */
+mm_status mm_group_shard(const mm_group* g, int i, uint32_t* class_begin, uint32_t* class_end);
+/* mm_set_gates on every GPU. */
+mm_status mm_group_set_gates(mm_group* g, const double* lcom, const uint32_t* cbo);
+/* One step on every GPU — metric pass + the sweep of its shard (mm_run with
+ * p's criteria/modes/thresholds; p's class range is replaced by the shard)
+ * — then the exact-count exchange. n_out (may be NULL: no host sync)
+ * receives the assembled list's length. */
+mm_status mm_group_run(mm_group* g, const mm_sweep_params* p, uint64_t* n_out);
+mm_status mm_group_synchronize(mm_group* g);
+/* Per-shard record counts (n entries, may be NULL) and their total. */
+mm_status mm_group_counts(const mm_group* g, uint64_t* counts, uint64_t* total);
+/* GPU i's copy of the assembled list (device memory). */
+mm_status mm_group_device_result(mm_group* g, int i, const void** dev_records, uint64_t* n);
+/* The assembled list to host memory (from GPU 0); MM_E_CAPACITY when small. */
+mm_status mm_group_copy_suggestions(mm_group* g, mm_suggestion* out, uint64_t cap, uint64_t* n_out);
 
 /* ---- host-side helpers (no GPU needed) --------------------------------- */
 /* Contiguous class ranges balanced by sweep cost (Σ over members of

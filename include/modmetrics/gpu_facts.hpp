@@ -15,6 +15,7 @@
 #include <memory>
 #include <string>
 #include <string_view>
+#include <exception>
 #include <thread>
 #include <utility>
 #include <vector>
@@ -106,10 +107,30 @@ private:
         const unsigned hw = std::thread::hardware_concurrency();
         const uint32_t T = n >= (1u << 16) ? std::min(8u, hw ? hw : 1u) : 1u;
         if (T <= 1) { fn(0u, n); return; }
+        // exceptions (e.g. bad_alloc from a worker's assign) are carried back
+        // and rethrown after every started thread joined, as the reference's
+        // single-threaded walk would throw them to the caller
+        std::vector<std::exception_ptr> errs(T);
         std::vector<std::thread> th;
-        for (uint32_t k = 0; k < T; ++k)
-            th.emplace_back([&, k] { fn(uint32_t(uint64_t(n) * k / T), uint32_t(uint64_t(n) * (k + 1) / T)); });
+        th.reserve(T);
+        std::exception_ptr spawn_err;
+        for (uint32_t k = 0; k < T && !spawn_err; ++k) {
+            try {
+                th.emplace_back([&, k] {
+                    try {
+                        fn(uint32_t(uint64_t(n) * k / T), uint32_t(uint64_t(n) * (k + 1) / T));
+                    } catch (...) {
+                        errs[k] = std::current_exception();
+                    }
+                });
+            } catch (...) {
+                spawn_err = std::current_exception();
+            }
+        }
         for (std::thread& t : th) t.join();
+        if (spawn_err) std::rethrow_exception(spawn_err);
+        for (const std::exception_ptr& e : errs)
+            if (e) std::rethrow_exception(e);
     }
 
     struct Del {

@@ -7,14 +7,77 @@ timed CPU baseline, never as the product path.
 from __future__ import annotations
 
 import ctypes as C
+import importlib.util
+import sys
 from pathlib import Path
 
 import numpy as np
 
-from paper_1308_4011_b200 import abi
-from paper_1308_4011_b200.system import System
-
 HERE = Path(__file__).resolve().parent
+
+
+def _load_abi():
+    """The ctypes mirror of include/mmgpu.h (plain struct layouts), loaded by
+    path: the oracle never imports the product package, so bench.py's
+    reference arm loads no product library."""
+    name = "_mm_abi_for_oracle"
+    if name not in sys.modules:
+        spec = importlib.util.spec_from_file_location(name, HERE.parent / "paper_1308_4011_b200" / "abi.py")
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules[name] = mod
+        spec.loader.exec_module(mod)
+    return sys.modules[name]
+
+
+abi = _load_abi()
+_FIELDS = ("method_owner", "attribute_owner", "class_method_off", "class_methods", "class_attr_off",
+           "class_attrs", "call_off", "call_tgt", "acc_off", "acc_tgt")
+
+
+class CsrSystem:
+    """A system in the mm_system CSR layout (the same fields as the product's
+    System, which the oracle functions also accept: any object with these
+    arrays and n_classes / n_methods / n_attributes)."""
+
+    def __init__(self, n_classes, n_methods, n_attributes, **arrays):
+        self.n_classes, self.n_methods, self.n_attributes = n_classes, n_methods, n_attributes
+        for f in _FIELDS:
+            setattr(self, f, np.ascontiguousarray(arrays[f], dtype=np.uint32))
+
+    @classmethod
+    def from_view(cls, v):
+        nc, nm, na = v.n_classes, v.n_methods, v.n_attributes
+
+        def take(ptr, n):
+            return np.ctypeslib.as_array(ptr, shape=(n,)).copy() if n else np.zeros(0, np.uint32)
+
+        co, ao = take(v.call_off, nm + 1), take(v.acc_off, nm + 1)
+        return cls(nc, nm, na, method_owner=take(v.method_owner, nm), attribute_owner=take(v.attribute_owner, na),
+                   class_method_off=take(v.class_method_off, nc + 1), class_methods=take(v.class_methods, nm),
+                   class_attr_off=take(v.class_attr_off, nc + 1), class_attrs=take(v.class_attrs, na),
+                   call_off=co, call_tgt=take(v.call_tgt, int(co[-1])), acc_off=ao,
+                   acc_tgt=take(v.acc_tgt, int(ao[-1])))
+
+    @property
+    def n_calls(self):
+        return int(self.call_off[-1])
+
+    @property
+    def n_accesses(self):
+        return int(self.acc_off[-1])
+
+    def equals(self, other) -> bool:
+        return (self.n_classes, self.n_methods, self.n_attributes) == (
+            other.n_classes, other.n_methods, other.n_attributes) and all(
+            np.array_equal(getattr(self, f), getattr(other, f)) for f in _FIELDS)
+
+
+def _csys(sys_):
+    """(keep-alive, address) of an mm_system over sys_'s arrays."""
+    s = abi.mm_system(n_classes=sys_.n_classes, n_methods=sys_.n_methods, n_attributes=sys_.n_attributes)
+    for f in _FIELDS:
+        setattr(s, f, np.ascontiguousarray(getattr(sys_, f), np.uint32).ctypes.data_as(abi.U32P))
+    return s, C.addressof(s)
 ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libmmref.so"
 _or = None
@@ -25,7 +88,7 @@ def oracle_lib():
     global _or
     if _or is None:
         l = C.CDLL(str(ORACLE_SO))
-        S = C.POINTER(abi.mm_system)
+        S = C.c_void_p
         l.or_class_metrics.argtypes = [S, C.c_void_p, C.c_void_p, C.c_void_p]
         l.or_fan_metrics.argtypes = [S, C.c_void_p, C.c_void_p]
         l.or_similarities.argtypes = [S, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
@@ -46,7 +109,7 @@ def ref_lib():
     global _ref
     if _ref is None:
         l = C.CDLL(str(REF_SO))
-        S = C.POINTER(abi.mm_system)
+        S = C.c_void_p
         l.ref_model_create.argtypes = [S]
         l.ref_model_create.restype = C.c_void_p
         l.ref_model_free.argtypes = [C.c_void_p]
@@ -54,7 +117,7 @@ def ref_lib():
         l.ref_generate.argtypes = [C.POINTER(abi.mm_gen_config)]
         l.ref_generate.restype = C.c_void_p
         l.ref_model_view.argtypes = [C.c_void_p]
-        l.ref_model_view.restype = S
+        l.ref_model_view.restype = C.POINTER(abi.mm_system)
         l.ref_class_metrics.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p, C.c_void_p]
         l.ref_fan_metrics.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_void_p]
         l.ref_similarities.argtypes = [C.c_void_p, C.c_uint, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
@@ -72,6 +135,11 @@ def ref_lib():
                                      C.POINTER(C.c_uint64)]
         l.ref_sweep_sample.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_uint32,
                                        C.c_uint32, C.c_uint, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        l.ref_sweep.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(abi.mm_sweep_params), C.c_void_p,
+                                C.c_uint64, C.c_uint, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        l.ref_sweep_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64]
+        l.ref_candidates.argtypes = [C.c_void_p]
+        l.ref_candidates.restype = C.c_uint64
         _ref = l
     return _ref
 
@@ -97,28 +165,28 @@ def _params(criteria_mask, combine=0, all_candidates=False, top_k=1, thr_lcom=0.
 
 # ---- oracle (C restatement) ----------------------------------------------
 
-def fan_metrics(sys_: System):
-    s = sys_.as_c()
+def fan_metrics(sys_):
+    s, sp = _csys(sys_)
     fi, fo = np.empty(sys_.n_methods, np.uint32), np.empty(sys_.n_methods, np.uint32)
-    oracle_lib().or_fan_metrics(C.byref(s), fi.ctypes.data, fo.ctypes.data)
+    oracle_lib().or_fan_metrics(sp, fi.ctypes.data, fo.ctypes.data)
     return fi, fo
 
 
-def similarities(sys_: System):
-    s = sys_.as_c()
+def similarities(sys_):
+    s, sp = _csys(sys_)
     n = C.c_uint64()
-    oracle_lib().or_similarities(C.byref(s), None, 0, C.byref(n))
+    oracle_lib().or_similarities(sp, None, 0, C.byref(n))
     out = np.zeros(n.value, dtype=abi.SIMILARITY_DTYPE)
     if n.value:
-        oracle_lib().or_similarities(C.byref(s), out.ctypes.data, n.value, C.byref(n))
+        oracle_lib().or_similarities(sp, out.ctypes.data, n.value, C.byref(n))
     return out
 
 
-def class_metrics(sys_: System):
-    s = sys_.as_c()
+def class_metrics(sys_):
+    s, sp = _csys(sys_)
     n = sys_.n_classes
     lcom, ck, cbo = np.empty(n, np.float64), np.empty(n, np.uint64), np.empty(n, np.uint32)
-    oracle_lib().or_class_metrics(C.byref(s), lcom.ctypes.data, ck.ctypes.data, cbo.ctypes.data)
+    oracle_lib().or_class_metrics(sp, lcom.ctypes.data, ck.ctypes.data, cbo.ctypes.data)
     return lcom, ck, cbo
 
 
@@ -133,24 +201,24 @@ def thresholds(lcom, cbo, similarity=None, overrides=None):
     return t
 
 
-def what_if(sys_: System, u, o, d):
-    s = sys_.as_c()
+def what_if(sys_, u, o, d):
+    s, sp = _csys(sys_)
     w = abi.mm_whatif()
-    st = oracle_lib().or_what_if(C.byref(s), u, o, d, C.byref(w))
+    st = oracle_lib().or_what_if(sp, u, o, d, C.byref(w))
     return st, w
 
 
-def suggest(sys_: System, lcom_gate, cbo_gate, criteria_mask, combine=0, all_candidates=False, top_k=1,
+def suggest(sys_, lcom_gate, cbo_gate, criteria_mask, combine=0, all_candidates=False, top_k=1,
             thr_lcom=0.0, thr_cbo=0.0, class_range=None):
-    s = sys_.as_c()
+    s, sp = _csys(sys_)
     lg = np.ascontiguousarray(lcom_gate, np.float64)
     cg = np.ascontiguousarray(cbo_gate, np.uint32)
     p = _params(criteria_mask, combine, all_candidates, top_k, thr_lcom, thr_cbo, class_range)
     n = C.c_uint64()
-    st = oracle_lib().or_suggest(C.byref(s), lg.ctypes.data, cg.ctypes.data, C.byref(p), None, 0, C.byref(n))
+    st = oracle_lib().or_suggest(sp, lg.ctypes.data, cg.ctypes.data, C.byref(p), None, 0, C.byref(n))
     out = np.zeros(n.value, dtype=abi.SUGGESTION_DTYPE)
     if n.value:
-        st = oracle_lib().or_suggest(C.byref(s), lg.ctypes.data, cg.ctypes.data, C.byref(p), out.ctypes.data,
+        st = oracle_lib().or_suggest(sp, lg.ctypes.data, cg.ctypes.data, C.byref(p), out.ctypes.data,
                                      n.value, C.byref(n))
     if st:
         raise RuntimeError(f"or_suggest status {st}")
@@ -160,9 +228,11 @@ def suggest(sys_: System, lcom_gate, cbo_gate, criteria_mask, combine=0, all_can
 # ---- the reference itself (compiled headers) -----------------------------
 
 class RefModel:
-    def __init__(self, sys_: System = None, handle=None):
+    def __init__(self, sys_=None, handle=None):
         self._keep = sys_
-        self.h = handle if handle is not None else ref_lib().ref_model_create(C.byref(sys_.as_c()))
+        if handle is None:
+            cs, sp = _csys(sys_)
+        self.h = handle if handle is not None else ref_lib().ref_model_create(sp)
         view = ref_lib().ref_model_view(self.h).contents if handle is not None else None
         self.n_classes = view.n_classes if view is not None else sys_.n_classes
         self.n_methods = view.n_methods if view is not None else sys_.n_methods
@@ -252,6 +322,31 @@ class RefModel:
             st = call(out.ctypes.data, n.value)
         return st, out
 
+    def sweep(self, lcom_gate, cbo_gate, criteria_mask, thr_lcom, thr_cbo, combine=0, all_candidates=False,
+              methods=None, n_workers=1, dynamic=True):
+        """suggest_all's cohesion/coupling list restricted to `methods` (None =
+        all), evaluated by the reference's own per-method code on n_workers
+        threads (ref_sweep in ref_shim.cpp). Returns (records, candidates)."""
+        lg = np.ascontiguousarray(lcom_gate, np.float64)
+        cg = np.ascontiguousarray(cbo_gate, np.uint32)
+        p = _params(criteria_mask, combine, all_candidates, 1, thr_lcom, thr_cbo)
+        ml = None if methods is None else np.ascontiguousarray(methods, np.uint32)
+        nr, nc = C.c_uint64(), C.c_uint64()
+        st = ref_lib().ref_sweep(self.h, lg.ctypes.data, cg.ctypes.data, C.byref(p),
+                                 None if ml is None else ml.ctypes.data, 0 if ml is None else len(ml), n_workers,
+                                 int(dynamic), C.byref(nr), C.byref(nc))
+        if st:
+            raise RuntimeError(f"ref_sweep status {st}")
+        out = np.zeros(nr.value, dtype=abi.SUGGESTION_DTYPE)
+        if nr.value:
+            st = ref_lib().ref_sweep_copy(self.h, out.ctypes.data, nr.value)
+            if st:
+                raise RuntimeError(f"ref_sweep_copy status {st}")
+        return out, nc.value
+
+    def candidates(self) -> int:
+        return int(ref_lib().ref_candidates(self.h))
+
     def sweep_sample(self, lcom_gate, cbo_gate, thr_lcom, thr_cbo, class_begin, class_end, n_workers):
         lg = np.ascontiguousarray(lcom_gate, np.float64)
         cg = np.ascontiguousarray(cbo_gate, np.uint32)
@@ -263,13 +358,21 @@ class RefModel:
         return ns.value, nc.value
 
 
-def ref_generate(**cfg) -> System:
+def ref_generate(**cfg) -> CsrSystem:
+    """The reference's generate() (generate.hpp:94); zipf_s > 0: config C3's
+    skewed ownership with the reference's dependency draws (ref_shim.cpp)."""
     c = abi.mm_gen_config(**cfg)
     h = ref_lib().ref_generate(C.byref(c))
     try:
-        return System.from_view(ref_lib().ref_model_view(h).contents)
+        return CsrSystem.from_view(ref_lib().ref_model_view(h).contents)
     finally:
         ref_lib().ref_model_free(h)
+
+
+def ref_generate_model(**cfg) -> "RefModel":
+    """generate() straight into a reference model handle (no CSR round trip)."""
+    c = abi.mm_gen_config(**cfg)
+    return RefModel(handle=ref_lib().ref_generate(C.byref(c)))
 
 
 def ref_thresholds(lcom, cbo, similarity=None, overrides=None):

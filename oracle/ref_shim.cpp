@@ -6,10 +6,14 @@
 // the native generator here, (b) generate tests/golden fixtures, and (c) time
 // the reference CPU path for bench.py's cpu_baseline / --impl reference arm.
 // The product never links it.
+#include <atomic>
 #include <chrono>
+#include <cmath>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <map>
 #include <stdexcept>
 #include <vector>
 
@@ -30,6 +34,7 @@ struct RefModel {
     // CSR view for generate() round trips
     std::vector<uint32_t> mo, ao, cmo, cm, cao, ca, co, ct, ao2, at;
     mm_system view{};
+    std::vector<mm_suggestion> last;  // ref_sweep's result (ref_sweep_copy)
 };
 
 void to_csr(RefModel& r) {
@@ -134,6 +139,95 @@ std::vector<Criterion> criteria_of(uint32_t mask) {
     return v;
 }
 
+
+// ---- config C3: Zipf class sizes -----------------------
+// The reference has no skewed generator. Ownership is restated here from the
+// C3 recipe (sizes ∝ 1/rank^s, min 1, ids shuffled by SplitMix64 seeded
+// seed ^ 0x5a17f00dd15ea5e5); the dependencies are drawn by the reference's
+// own SplitMix64 / detail::pick_excluding / detail::pick_foreign in
+// generate()'s exact loop (generate.hpp:124-161). tests/test_abi_cpu.py pins
+// the product's mm_generate(zipf_s) against this.
+std::vector<uint32_t> zipf_sizes(uint32_t n, uint32_t c, double s) {
+    std::vector<double> w(c);
+    double W = 0.0;
+    for (uint32_t r = 0; r < c; ++r) W += (w[r] = 1.0 / std::pow(double(r) + 1.0, s));
+    std::vector<uint32_t> sz(c);
+    uint64_t total = 0;
+    const uint32_t lo = n >= c ? 1u : 0u;
+    for (uint32_t r = 0; r < c; ++r) {
+        sz[r] = std::max<uint32_t>(lo, static_cast<uint32_t>(std::floor(double(n) * w[r] / W)));
+        total += sz[r];
+    }
+    for (uint32_t r = 0; total > n; r = (r + 1) % c)
+        if (sz[r] > lo) { --sz[r]; --total; }
+    for (uint32_t r = 0; total < n; r = (r + 1) % c) { ++sz[r]; ++total; }
+    return sz;
+}
+
+std::vector<ClassId> zipf_owner(uint32_t n, uint32_t c, double s, SplitMix64& shuffle) {
+    std::vector<uint32_t> perm(n);
+    for (uint32_t i = 0; i < n; ++i) perm[i] = i;
+    for (uint32_t i = n; i > 1; --i) std::swap(perm[i - 1], perm[shuffle.below(i)]);
+    const std::vector<uint32_t> sz = zipf_sizes(n, c, s);
+    std::vector<ClassId> owner(n);
+    uint32_t at = 0;
+    for (uint32_t r = 0; r < c; ++r)
+        for (uint32_t k = 0; k < sz[r]; ++k) owner[perm[at++]] = r;
+    return owner;
+}
+
+void generate_zipf(RefModel& r, const GeneratorConfig& cfg, double zs) {
+    if (cfg.n_classes == 0) throw std::invalid_argument("generate: n_classes must be positive");
+    SystemModel& model = r.model;
+    model.classes.resize(cfg.n_classes);
+    for (ClassId c = 0; c < cfg.n_classes; ++c) {
+        model.classes[c].id = c;
+        model.classes[c].name = "C" + std::to_string(c);
+    }
+    SplitMix64 shuffle(cfg.seed ^ 0x5a17f00dd15ea5e5ULL);
+    model.method_owner = zipf_owner(cfg.n_methods, cfg.n_classes, zs, shuffle);
+    model.attribute_owner = zipf_owner(cfg.n_attributes, cfg.n_classes, zs, shuffle);
+    model.method_names.resize(cfg.n_methods);
+    model.attribute_names.resize(cfg.n_attributes);
+    for (MethodId p = 0; p < cfg.n_methods; ++p) model.classes[model.method_owner[p]].method_ids.push_back(p);
+    for (AttributeId a = 0; a < cfg.n_attributes; ++a)
+        model.classes[model.attribute_owner[a]].attribute_ids.push_back(a);
+    SplitMix64 rng(cfg.seed);
+    DependencyTable& deps = r.deps;
+    deps.calls.assign(cfg.n_methods, {});
+    deps.accesses.assign(cfg.n_methods, {});
+    for (MethodId p = 0; p < cfg.n_methods; ++p) {
+        const ClassId home = model.method_owner[p];
+        const std::uint64_t n_calls = cfg.k_max_calls ? rng.below(cfg.k_max_calls + 1ULL) : 0;
+        for (std::uint64_t i = 0; i < n_calls; ++i) {
+            const bool stay = rng.unit() < cfg.intra_class_bias;
+            std::uint32_t target;
+            if (stay ? detail::pick_excluding(rng, model.classes[home].method_ids, p, target)
+                     : detail::pick_foreign(rng, model.method_owner, home, target))
+                deps.calls[p].push_back(target);
+        }
+        const std::uint64_t n_acc = cfg.k_max_accesses ? rng.below(cfg.k_max_accesses + 1ULL) : 0;
+        for (std::uint64_t i = 0; i < n_acc; ++i) {
+            const bool stay = rng.unit() < cfg.intra_class_bias;
+            std::uint32_t target;
+            if (stay) {
+                const auto& pool = model.classes[home].attribute_ids;
+                if (pool.empty()) continue;
+                target = pool[rng.below(pool.size())];
+            } else if (!detail::pick_foreign(rng, model.attribute_owner, home, target)) {
+                continue;
+            }
+            deps.accesses[p].push_back(target);
+        }
+        auto& cs = deps.calls[p];
+        std::sort(cs.begin(), cs.end());
+        cs.erase(std::unique(cs.begin(), cs.end()), cs.end());
+        auto& as = deps.accesses[p];
+        std::sort(as.begin(), as.end());
+        as.erase(std::unique(as.begin(), as.end()), as.end());
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -162,9 +256,13 @@ void* ref_generate(const mm_gen_config* cfg) {
     g.k_max_accesses = cfg->k_max_accesses;
     g.intra_class_bias = cfg->intra_class_bias;
     RefModel* r = new RefModel();
-    GeneratedSystem gs = generate(g);
-    r->model = std::move(gs.model);
-    r->deps = std::move(gs.deps);
+    if (cfg->zipf_s > 0.0) {
+        generate_zipf(*r, g, cfg->zipf_s);
+    } else {
+        GeneratedSystem gs = generate(g);
+        r->model = std::move(gs.model);
+        r->deps = std::move(gs.deps);
+    }
     to_csr(*r);
     return r;
 }
@@ -433,6 +531,129 @@ int ref_sweep_sample(void* h, const double* lcom_gate, const uint32_t* cbo_gate,
         *n_candidates += cand[i];
     }
     return MM_OK;
+}
+
+// The reference's cohesion/coupling sweep restricted to a method subset,
+// records in suggest_all's order — "reference logic, harness threads"
+// (SURVEY.md §8d item 4), for the parity tests at the BASELINE sizes and the
+// CPU arm. Per method, exactly suggest_by_cohesion / suggest_by_coupling's
+// body (suggest.hpp:239-294): class gate, detail::used_classes,
+// detail::emit_for_method with detail::lcom_improves / lcom_key or the
+// coupling pass/key, which run the reference's what_if_move. Then
+// suggest_all's merge (suggest.hpp:315-348): keyed by (method, destination),
+// the first criterion's record kept and later criteria appended, sort-unique
+// of the tags, intersection filter, sort by (origin, method, destination).
+// Per-method work is independent given the report and thresholds, so any
+// subset and any thread split give suggest_all's list restricted to that
+// subset. methods == NULL: every method. dynamic != 0: methods handed out in
+// chunks of 64 from an atomic counter (Zipf giants); else the reference's
+// detail::run_partitioned contiguous ranges. *n_candidates = Σ
+// |used_classes(u)| over the swept methods (ungated). Result kept in the
+// model handle (ref_sweep_copy).
+int ref_sweep(void* h, const double* lcom_gate, const uint32_t* cbo_gate, const mm_sweep_params* p,
+              const uint32_t* methods, uint64_t n_methods, unsigned n_workers, int dynamic, uint64_t* n_records,
+              uint64_t* n_candidates) {
+    RefModel* r = static_cast<RefModel*>(h);
+    const SystemModel& model = r->model;
+    const DependencyTable& deps = r->deps;
+    const uint64_t n = methods ? n_methods : model.method_owner.size();
+    const unsigned W = n_workers ? n_workers : 1;
+    const bool want_coh = p->criteria & MM_CRIT_COHESION, want_coup = p->criteria & MM_CRIT_COUPLING;
+    if (!want_coh && !want_coup) return MM_E_ARG;
+    if (p->criteria & MM_CRIT_SIMILARITY) return MM_E_UNSUPPORTED;
+    SuggestOptions opts;
+    opts.all_candidates = p->all_candidates != 0;
+    struct Part {
+        std::vector<MoveSuggestion> coh, coup;
+        uint64_t cand = 0;
+    };
+    std::vector<Part> parts(W);
+    auto one = [&](Part& pt, MethodId u) {
+        const ClassId c = model.method_owner[u];
+        const std::vector<ClassId> dests = detail::used_classes(u, c, model, deps);
+        pt.cand += dests.size();
+        if (want_coh && lcom_gate[c] > p->thr_lcom)
+            detail::emit_for_method(u, c, dests, Criterion::Cohesion, detail::lcom_improves, detail::lcom_key, opts,
+                                    model, deps, pt.coh);
+        if (want_coup && static_cast<double>(cbo_gate[c]) > p->thr_cbo)
+            detail::emit_for_method(
+                u, c, dests, Criterion::Coupling,
+                [](const WhatIfMetrics& wm) {
+                    return wm.cbo_origin_after < wm.cbo_origin_before && wm.cbo_dest_after <= wm.cbo_dest_before;
+                },
+                [](const WhatIfMetrics& wm) { return static_cast<double>(wm.cbo_dest_after); }, opts, model, deps,
+                pt.coup);
+    };
+    auto mid = [&](uint64_t i) -> MethodId { return methods ? methods[i] : static_cast<MethodId>(i); };
+    try {
+        if (dynamic) {
+            std::atomic<uint64_t> next{0};
+            std::vector<std::thread> th;
+            for (unsigned w = 0; w < W; ++w)
+                th.emplace_back([&, w] {
+                    for (;;) {
+                        const uint64_t b = next.fetch_add(64);
+                        if (b >= n) break;
+                        for (uint64_t i = b; i < std::min<uint64_t>(n, b + 64); ++i) one(parts[w], mid(i));
+                    }
+                });
+            for (std::thread& t : th) t.join();
+        } else {
+            detail::run_partitioned(n, W, [&](unsigned w, size_t b, size_t e) {
+                for (size_t i = b; i < e; ++i) one(parts[w], mid(i));
+            });
+        }
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+    // suggest_all's merge, criteria in ascending order (Cohesion < Coupling)
+    std::map<std::pair<MethodId, ClassId>, MoveSuggestion> merged;
+    uint64_t cand = 0;
+    for (Part& pt : parts) cand += pt.cand;
+    for (int pass = 0; pass < 2; ++pass)
+        for (Part& pt : parts)
+            for (MoveSuggestion& s : pass == 0 ? pt.coh : pt.coup) {
+                const Criterion crit = s.criteria.front();
+                const auto key = std::make_pair(s.method, s.destination);
+                auto [it, inserted] = merged.try_emplace(key, std::move(s));
+                if (!inserted) it->second.criteria.push_back(crit);
+            }
+    const size_t n_sel = (want_coh ? 1 : 0) + (want_coup ? 1 : 0);
+    std::vector<MoveSuggestion> out;
+    out.reserve(merged.size());
+    for (auto& [key, s] : merged) {
+        std::sort(s.criteria.begin(), s.criteria.end());
+        s.criteria.erase(std::unique(s.criteria.begin(), s.criteria.end()), s.criteria.end());
+        if (p->combine == MM_COMBINE_INTERSECTION && s.criteria.size() != n_sel) continue;
+        out.push_back(std::move(s));
+    }
+    std::sort(out.begin(), out.end(), [](const MoveSuggestion& a, const MoveSuggestion& b) {
+        if (a.origin != b.origin) return a.origin < b.origin;
+        if (a.method != b.method) return a.method < b.method;
+        return a.destination < b.destination;
+    });
+    r->last.resize(out.size());
+    for (size_t i = 0; i < out.size(); ++i) fill(r->last[i], out[i]);
+    *n_records = out.size();
+    *n_candidates = cand;
+    return MM_OK;
+}
+
+int ref_sweep_copy(void* h, mm_suggestion* out, uint64_t cap) {
+    RefModel* r = static_cast<RefModel*>(h);
+    if (cap < r->last.size()) return MM_E_CAPACITY;
+    std::memcpy(out, r->last.data(), r->last.size() * sizeof(mm_suggestion));
+    return MM_OK;
+}
+
+// N_cand = Σ_u |used_classes(u)| with the reference's own
+// detail::used_classes.
+uint64_t ref_candidates(void* h) {
+    const RefModel* r = static_cast<RefModel*>(h);
+    uint64_t n = 0;
+    for (MethodId u = 0; u < r->model.method_owner.size(); ++u)
+        n += detail::used_classes(u, r->model.method_owner[u], r->model, r->deps).size();
+    return n;
 }
 
 }  // extern "C"

@@ -65,6 +65,22 @@ _SIGS = {
     "mm_run": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_params)]),
     "mm_collect_timings": (C.c_int, [C.c_void_p]),
     "mm_sweep_device_result": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
+    "mm_sweep_device_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "mm_ctx_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "mm_group_create": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]),
+    "mm_group_destroy": (None, [C.c_void_p]),
+    "mm_group_last_error": (C.c_char_p, [C.c_void_p]),
+    "mm_group_size": (C.c_int, [C.c_void_p]),
+    "mm_group_uses_nccl": (C.c_int, [C.c_void_p]),
+    "mm_group_ctx": (C.c_void_p, [C.c_void_p, C.c_int]),
+    "mm_group_upload": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_system)]),
+    "mm_group_shard": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "mm_group_set_gates": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "mm_group_run": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_params), C.POINTER(C.c_uint64)]),
+    "mm_group_synchronize": (C.c_int, [C.c_void_p]),
+    "mm_group_counts": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]),
+    "mm_group_device_result": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
+    "mm_group_copy_suggestions": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
     "mm_sweep_stats_get": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_stats)]),
     "mm_copy_suggestions": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
     "mm_suggest": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_sweep_params), C.c_void_p, C.c_uint64,

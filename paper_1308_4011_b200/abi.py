@@ -16,10 +16,12 @@ MM_E_CAPACITY = 7
 MM_E_PARSE = 8
 MM_E_VALIDATION = 9
 MM_E_IO = 10
+MM_E_NCCL = 11
 
 STATUS_NAMES = {
     0: "MM_OK", 1: "MM_E_RANGE", 2: "MM_E_ARG", 3: "MM_E_CUDA", 4: "MM_E_OOM",
     5: "MM_E_STATE", 6: "MM_E_UNSUPPORTED", 7: "MM_E_CAPACITY", 8: "MM_E_PARSE", 9: "MM_E_VALIDATION", 10: "MM_E_IO",
+    11: "MM_E_NCCL",
 }
 
 MM_CRIT_SIMILARITY = 1 << 0
@@ -29,6 +31,7 @@ MM_COMBINE_UNION = 0
 MM_COMBINE_INTERSECTION = 1
 MM_THR_EXPLICIT = 0
 MM_THR_DEVICE_MEANS = 1
+MM_SWEEP_EXACT_RANGE = 1
 
 U32P = C.POINTER(C.c_uint32)
 
@@ -100,7 +103,7 @@ class mm_sweep_params(C.Structure):
         ("criteria", C.c_uint32), ("combine", C.c_uint32), ("all_candidates", C.c_uint32),
         ("top_k", C.c_uint32), ("thr_lcom", C.c_double), ("thr_cbo", C.c_double),
         ("class_begin", C.c_uint32), ("class_end", C.c_uint32),
-        ("threshold_source", C.c_uint32), ("pad", C.c_uint32),
+        ("threshold_source", C.c_uint32), ("flags", C.c_uint32),
     ]
 
 

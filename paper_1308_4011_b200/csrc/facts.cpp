@@ -824,11 +824,16 @@ void build(Reader& r, mm_facts& f, bool parallel_ok) {
             for (std::thread& t : th) t.join();
         }
         uint64_t ma = 0, mm = 0;
+        bool any_stop = false;
         for (size_t k = 0; k < TS; ++k) {  // ranges in order, up to the first non-object class
             ma = std::max(ma, pa[k]);
             mm = std::max(mm, pm[k]);
-            if (stop[k]) break;
+            if (stop[k]) { any_stop = true; break; }
         }
+        // a non-object class element ends the reference's walk there (a
+        // ParseError): the tables are sized only up to it, so the optimistic
+        // parallel walk — which visits every range — must not run
+        if (any_stop) parallel_ok = false;
         if (ma < id_cap && mm < id_cap) {
             // the final sizes are exactly these (max visited id + 1), so
             // growing to them up front is the same as growing id by id
@@ -873,7 +878,7 @@ void build(Reader& r, mm_facts& f, bool parallel_ok) {
                 uint32_t* ca = f.cattr.data() + apre[ci];
                 for (uint64_t ai = 0; ai < rc.attr_end - rc.attr_begin; ++ai) {
                     const RawAttr& ra = r.attrs[rc.attr_begin + ai];
-                    if (!ra.is_object || !valid_id(ra.id) || ra.name.kind != F_STRING ||
+                    if (!ra.is_object || !valid_id(ra.id) || ra.name.kind != F_STRING || ra.id.value >= aown.size() ||
                         !claim(&aown[ra.id.value], uint32_t(ci))) { __atomic_store_n(&bad, 1, __ATOMIC_RELAXED); return; }
                     f.attribute_name[ra.id.value] = ra.name.s;
                     ca[ai] = uint32_t(ra.id.value);
@@ -882,7 +887,7 @@ void build(Reader& r, mm_facts& f, bool parallel_ok) {
                 uint32_t* cm = f.cmeth.data() + mpre[ci];
                 for (uint64_t mi = 0; mi < rc.meth_end - rc.meth_begin; ++mi) {
                     const RawMethod& rm = r.methods[rc.meth_begin + mi];
-                    if (!rm.is_object || !valid_id(rm.id) || rm.name.kind != F_STRING ||
+                    if (!rm.is_object || !valid_id(rm.id) || rm.name.kind != F_STRING || rm.id.value >= mown.size() ||
                         !claim(&mown[rm.id.value], uint32_t(ci))) { __atomic_store_n(&bad, 1, __ATOMIC_RELAXED); return; }
                     f.method_name[rm.id.value] = rm.name.s;
                     cm[mi] = uint32_t(rm.id.value);

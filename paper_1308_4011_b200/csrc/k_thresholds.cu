@@ -29,6 +29,8 @@
 // reference's running double sum while Σ < 2^53 (checked; else serial).
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cooperative_groups.h>
 
 #include <cstdint>
@@ -468,6 +470,7 @@ __global__ void k_thresholds_serial(const double* __restrict__ lcom, const uint3
 
 }  // namespace
 
+constexpr int kMaxDevices = 64;
 constexpr uint32_t kSerialMax = 2048;  // below this one warp's serial chain beats three grid syncs (measured)
 
 size_t thresholds_scratch_bytes(uint32_t n) {
@@ -478,13 +481,18 @@ size_t thresholds_scratch_bytes(uint32_t n) {
 cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
                               void* scratch, size_t scratch_bytes, cudaStream_t st, bool allow_serial) {
     const uint32_t tiles = (n + kTile - 1) / kTile;
-    static int max_coresident = -1;
-    if (max_coresident < 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+    // co-resident CTA bound of the current device (per device: contexts on
+    // several GPUs may be driven from several host threads)
+    static std::atomic<int> coresident[kMaxDevices];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int max_coresident = dev < kMaxDevices ? coresident[dev].load(std::memory_order_relaxed) : 0;
+    if (max_coresident <= 0) {
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_thresholds_coop, kTT, 0);
         max_coresident = sms * per_sm;
+        if (dev < kMaxDevices) coresident[dev].store(max_coresident, std::memory_order_relaxed);
     }
     if (n == 0 || (allow_serial && n <= kSerialMax) || tiles > (uint32_t)max_coresident ||
         scratch_bytes < thresholds_scratch_bytes(n)) {

@@ -425,6 +425,12 @@ mm_status mm_ctx_synchronize(mm_ctx* ctx) {
     return MM_OK;
 }
 
+mm_status mm_ctx_stream(mm_ctx* ctx, void** s) {
+    if (!ctx || !s) return MM_E_ARG;
+    *s = ctx->stream;
+    return MM_OK;
+}
+
 mm_status mm_ctx_set_profiling(mm_ctx* ctx, int on) {
     if (!ctx) return MM_E_ARG;
     ctx->profiling = on != 0;
@@ -1131,7 +1137,8 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     if (p->combine > MM_COMBINE_INTERSECTION) return fail(ctx, MM_E_ARG, "mm_sweep: bad combine");
     if (!p->all_candidates && p->top_k > 8) return fail(ctx, MM_E_UNSUPPORTED, "mm_sweep: top_k > 8");
     if (mm_status st = ensure_metrics(ctx)) return st;
-    const uint32_t cb = p->class_begin, ce = p->class_end ? p->class_end : ctx->C;
+    const uint32_t cb = p->class_begin,
+                   ce = (p->class_end || (p->flags & MM_SWEEP_EXACT_RANGE)) ? p->class_end : ctx->C;
     if (cb > ce || ce > ctx->C) return fail(ctx, MM_E_RANGE, "mm_sweep: class range outside the model");
     const uint32_t pb = ctx->h_cls_moff[cb], pe = ctx->h_cls_moff[ce];
     const uint64_t npos = pe - pb;
@@ -1305,6 +1312,13 @@ mm_status mm_sweep_device_result(mm_ctx* ctx, const void** dev_records, uint64_t
         if (mm_status st = mm_sweep_stats_get(ctx, &ss)) return st;
         *n = ss.suggestions;
     }
+    return MM_OK;
+}
+
+mm_status mm_sweep_device_count(mm_ctx* ctx, const uint64_t** dev_count) {
+    if (!ctx || !dev_count) return MM_E_ARG;
+    if (!ctx->sweep_valid) return fail(ctx, MM_E_STATE, "no sweep has run");
+    *dev_count = reinterpret_cast<const uint64_t*>(&ctx->ctl.p->stats[2]);
     return MM_OK;
 }
 

@@ -435,6 +435,92 @@ class Engine:
         return self.suggest_all(thresholds, [Criterion.Coupling], Combine.Union, all_candidates)
 
 
+class Group:
+    """Several GPUs in one process (`mm_group`, include/mmgpu.h): the
+    reference's n_workers mapped to GPUs. Metric pass replicated, sweep on
+    cost-balanced class-range shards, exact-count NCCL exchange into every
+    GPU's assembled list (= suggest_all's ordered list)."""
+
+    def __init__(self, devices: Optional[Sequence[int]] = None, n: Optional[int] = None):
+        if devices is None:
+            devices = list(range(n if n is not None else 1))
+        arr = (C.c_int * max(1, len(devices)))(*devices)
+        self._g = C.c_void_p()
+        st = lib().mm_group_create(arr, len(devices), C.byref(self._g))
+        if st:
+            check(st, None, f"mm_group_create(devices={list(devices)})")
+        self.n = len(devices)
+        self.system: Optional[System] = None
+
+    def close(self) -> None:
+        if self._g:
+            lib().mm_group_destroy(self._g)
+            self._g = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int, what: str) -> None:
+        if st:
+            from ._lib import _exc_for
+            raise _exc_for(st)(st, f"{what}: {lib().mm_group_last_error(self._g).decode(errors='replace')}")
+
+    @property
+    def uses_nccl(self) -> bool:
+        return bool(lib().mm_group_uses_nccl(self._g))
+
+    def upload(self, system: System) -> "Group":
+        self._s = system.as_c()
+        self._check(lib().mm_group_upload(self._g, C.byref(self._s)), "mm_group_upload")
+        self.system = system
+        return self
+
+    def shards(self) -> list:
+        out = []
+        for i in range(self.n):
+            b, e = C.c_uint32(), C.c_uint32()
+            self._check(lib().mm_group_shard(self._g, i, C.byref(b), C.byref(e)), "mm_group_shard")
+            out.append((b.value, e.value))
+        return out
+
+    def run(self, criteria=(Criterion.Cohesion, Criterion.Coupling), combine=Combine.Union,
+            thresholds: Optional[Thresholds] = None, all_candidates: bool = False, top_k: int = 1,
+            want_count: bool = True) -> Optional[int]:
+        p = Engine._params(criteria, combine, thresholds, all_candidates, top_k, None)
+        n = C.c_uint64()
+        self._check(lib().mm_group_run(self._g, C.byref(p), C.byref(n) if want_count else None), "mm_group_run")
+        return n.value if want_count else None
+
+    def counts(self) -> list:
+        c = np.zeros(self.n, np.uint64)
+        t = C.c_uint64()
+        self._check(lib().mm_group_counts(self._g, c.ctypes.data, C.byref(t)), "mm_group_counts")
+        return [int(x) for x in c]
+
+    def suggestions(self) -> np.ndarray:
+        n = C.c_uint64()
+        st = lib().mm_group_copy_suggestions(self._g, None, 0, C.byref(n))
+        if st not in (abi.MM_OK, abi.MM_E_CAPACITY):
+            self._check(st, "mm_group_copy_suggestions")
+        out = np.zeros(n.value, dtype=abi.SUGGESTION_DTYPE)
+        if n.value:
+            self._check(lib().mm_group_copy_suggestions(self._g, out.ctypes.data, n.value, C.byref(n)),
+                        "mm_group_copy_suggestions")
+        return out
+
+    def synchronize(self) -> None:
+        self._check(lib().mm_group_synchronize(self._g), "mm_group_synchronize")
+
+
 # ---- free functions with the reference's call shapes ---------------------
 
 def plan_shards(system: System, n_shards: int) -> np.ndarray:

@@ -189,3 +189,25 @@ def test_parsed_system_uploads():
     b.compute_metrics()
     for x, y in zip(a.class_metrics_all(), b.class_metrics_all()):
         assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
+
+
+@pytest.mark.parametrize("bad_at", [40000, 1, 399999])
+def test_large_document_non_object_class(bad_at):
+    # ≥ 8 MB takes the parallel reader + optimistic parallel walk: the id
+    # tables are presized only up to the first non-object class, so that walk
+    # must not run (it once wrote past the tables: ADVICE r1 facts.cpp:877).
+    # The reference stops at that element with a ParseError.
+    n = 400000
+    parts = [f'{{"attributes":[{{"id":{c},"name":"a{c}"}}],"id":{c},'
+             f'"methods":[{{"accesses":[{c}],"calls":[],"id":{c},"name":"m{c}"}}],"name":"C{c}"}}'
+             for c in range(n)]
+    parts[bad_at] = "null"
+    doc = '{"classes":[' + ",".join(parts) + '],"schema_version":"1"}\n'
+    assert len(doc) > 8 << 20
+    with pytest.raises(FactsParseError, match=rf"classes\[{bad_at}\]: expected an object$"):
+        parse_facts(doc)
+    # a well-formed document of the same size parses (parallel walk taken)
+    parts[bad_at] = (f'{{"attributes":[{{"id":{bad_at},"name":"a"}}],"id":{bad_at},'
+                     f'"methods":[{{"accesses":[],"calls":[],"id":{bad_at},"name":"m"}}],"name":"C"}}')
+    f = parse_facts('{"classes":[' + ",".join(parts) + '],"schema_version":"1"}\n')
+    assert f.system.n_classes == n and f.system.n_methods == n

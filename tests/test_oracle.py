@@ -154,3 +154,50 @@ def test_oracle_matches_compiled_reference_random():
             a = oracle.suggest(s, l, c, mask, comb, allc, 1, t.lcom, t.cbo)
             st, b = R.suggest(l, c, mask, comb, allc, t.lcom, t.cbo)
             assert st == 0 and records_equal(a, b), (seed, mask, first_diff(a, b))
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built (no /root/reference)")
+def test_ref_sweep_equals_suggest_all():
+    # ref_sweep (the reference's per-method code on threads + suggest_all's
+    # merge) is suggest_all itself over all methods, and suggest_all
+    # restricted to the methods given otherwise — the basis of the sampled
+    # parity tests at the BASELINE sizes
+    for seed in range(25):
+        rng = np.random.default_rng(4000 + seed)
+        cfg = dict(seed=seed, n_classes=int(rng.integers(2, 60)), n_methods=int(rng.integers(4, 600)),
+                   n_attributes=int(rng.integers(1, 300)), k_max_calls=int(rng.integers(0, 7)),
+                   k_max_accesses=int(rng.integers(0, 7)), intra_class_bias=float(rng.random()),
+                   zipf_s=float(rng.choice([0.0, 1.0])))
+        s = System.generate(**cfg)
+        R = oracle.RefModel(s)
+        l, k, c = R.class_metrics()
+        t = oracle.ref_thresholds(l, c)
+        for mask, comb, allc in ((COH | COUP, 0, False), (COH | COUP, 1, False), (COH | COUP, 0, True),
+                                 (COH | COUP, 1, True), (COH, 0, False), (COUP, 0, True)):
+            st, want = R.suggest(l, c, mask, comb, allc, t.lcom, t.cbo)
+            assert st == 0
+            for workers, dyn in ((1, False), (3, True), (4, False)):
+                got, cand = R.sweep(l, c, mask, t.lcom, t.cbo, comb, allc, n_workers=workers, dynamic=dyn)
+                assert records_equal(got, want), (seed, mask, comb, allc, workers, first_diff(got, want))
+                assert cand == s.n_candidates()
+            sub = np.sort(rng.choice(s.n_methods, size=max(1, s.n_methods // 5), replace=False)).astype(np.uint32)
+            got, _ = R.sweep(l, c, mask, t.lcom, t.cbo, comb, allc, methods=sub[::-1].copy(), n_workers=2)
+            assert records_equal(got, want[np.isin(want["method"], sub)])
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built (no /root/reference)")
+def test_reference_generate_without_product():
+    # bench.py's reference arm builds its input with the reference's own
+    # generate() (no product library); it equals the product generator, Zipf
+    # variant (config C3) included
+    for cfg in (dict(seed=1, n_classes=1000, n_methods=10000, n_attributes=20000, k_max_calls=4, k_max_accesses=4,
+                     intra_class_bias=0.5),
+                dict(seed=1, n_classes=2000, n_methods=20000, n_attributes=40000, k_max_calls=4, k_max_accesses=4,
+                     intra_class_bias=0.5, zipf_s=1.0),
+                dict(seed=7, n_classes=37, n_methods=900, n_attributes=50, k_max_calls=6, k_max_accesses=2,
+                     intra_class_bias=0.2, zipf_s=0.7)):
+        r = oracle.ref_generate(**cfg)
+        assert System.generate(**cfg).equals(r), cfg
+        R = oracle.ref_generate_model(**cfg)
+        assert R.validate() == 0
+        assert R.candidates() == System.generate(**cfg).n_candidates()
