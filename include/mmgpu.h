@@ -186,6 +186,8 @@ mm_status mm_ctx_create(int device, mm_ctx** out);
 void mm_ctx_destroy(mm_ctx* ctx);
 const char* mm_last_error(const mm_ctx* ctx); /* never NULL */
 int mm_abi_version(void);
+/* CUDA devices visible to this process (0 when none or no driver). */
+int mm_device_count(void);
 /* Run all work on this cudaStream_t (e.g. torch's current stream). NULL = the ctx's own stream. */
 mm_status mm_ctx_set_stream(mm_ctx* ctx, void* cuda_stream);
 mm_status mm_ctx_synchronize(mm_ctx* ctx);
@@ -237,12 +239,19 @@ mm_status mm_lcom_ck(mm_ctx* ctx, uint32_t cls, uint64_t* out);
 mm_status mm_cbo(mm_ctx* ctx, uint32_t cls, uint32_t* out);
 
 /* ---- thresholds (compute_thresholds, suggest.hpp:46-61) --------------- */
-/* Means of the device-resident per-class lcom/cbo, bit-identical to the
- * reference's sequential double sums (computed on the device by the metric
- * pass; this call copies 24 bytes back and applies the overrides).
- * similarity is out of scope for this engine (no similarity table): it is
- * the override when given, else 0. */
+/* compute_thresholds(full_report(...), ov): means of the device-resident
+ * per-class lcom / cbo (computed on the device by the metric pass) and of the
+ * device similarity table's values in table order (built here when absent,
+ * like full_report's similarity field), each bit-identical to the reference's
+ * sequential double sum; an override replaces its mean and sets
+ * explicit_mode. */
 mm_status mm_compute_thresholds(mm_ctx* ctx, const mm_overrides* ov, mm_thresholds* out);
+/* compute_thresholds(report, ov) (suggest.hpp:46-61) on a caller's report:
+ * report.lcom, report.cbo and report.similarity's values (host memory,
+ * copied), each mean computed on the device with the reference's sequential
+ * left-to-right double-sum semantics, bit-identical; empty -> 0. */
+mm_status mm_report_thresholds(mm_ctx* ctx, const double* lcom, uint64_t n_lcom, const uint32_t* cbo, uint64_t n_cbo,
+                               const double* similarity, uint64_t n_sim, const mm_overrides* ov, mm_thresholds* out);
 /* Mean of caller-supplied doubles with compute_thresholds' sequential
  * left-to-right double-sum semantics (suggest.hpp:48-53), bit-identical,
  * computed on the device (always the parallel exact emulation when its
@@ -262,9 +271,9 @@ typedef struct mm_similarity {
  * property sets (calls and accesses, the two id spaces kept apart), ordered
  * by (first, second) — all_similarities / parallel_similarities
  * (parallel.hpp:71-121). Two-call size query: out may be NULL; *n_out gets
- * the count; MM_E_CAPACITY when cap is smaller. MM_E_UNSUPPORTED when one
- * method's candidate list (Σ over its properties of their users) exceeds
- * 4096 entries or it has more than 1024 properties. */
+ * the count; MM_E_CAPACITY when cap is smaller. Any row length: rows beyond
+ * a warp's shared-memory buffer go through global scratch in batches.
+ * MM_E_UNSUPPORTED only past 2^32 - 1 pairs in all (u32 row offsets). */
 mm_status mm_similarities(mm_ctx* ctx, mm_similarity* out, uint64_t cap, uint64_t* n_out);
 
 /* suggest_by_similarity (suggest.hpp:200-232): pairs of `table` (the

@@ -19,7 +19,7 @@
 //   full_report             metrics.hpp:249   full_report / Engine:: (every field on the GPU)
 //   parallel_full_report    parallel.hpp:210  parallel_full_report
 //   lcom_normalized/lcom_ck/cbo metrics.hpp:128,159,187   Engine::
-//   compute_thresholds      suggest.hpp:46    (use the reference's own: host arithmetic on the report)
+//   compute_thresholds      suggest.hpp:46    compute_thresholds / Engine:: (device sequential-sum means)
 //   what_if_move            suggest.hpp:87    what_if_move / Engine::
 //   suggest_by_cohesion     suggest.hpp:239   suggest_by_cohesion / Engine::
 //   suggest_by_coupling     suggest.hpp:266   suggest_by_coupling / Engine::
@@ -230,6 +230,27 @@ public:
         return out;
     }
 
+    // compute_thresholds (suggest.hpp:46-61) on the caller's report: the three
+    // means on the device, bit-identical to the reference's sequential sums
+    Thresholds compute_thresholds(const MetricsReport& report, const ThresholdOverrides& ov = {}) {
+        std::vector<double> sim(report.similarity.size());
+        for (size_t k = 0; k < sim.size(); ++k) sim[k] = report.similarity[k].value;
+        mm_overrides o{};
+        if (ov.similarity) { o.has_similarity = 1; o.similarity = *ov.similarity; }
+        if (ov.lcom) { o.has_lcom = 1; o.lcom = *ov.lcom; }
+        if (ov.cbo) { o.has_cbo = 1; o.cbo = *ov.cbo; }
+        mm_thresholds t{};
+        detail::check(mm_report_thresholds(ctx_.get(), report.lcom.data(), report.lcom.size(), report.cbo.data(),
+                                           report.cbo.size(), sim.data(), sim.size(), &o, &t),
+                      ctx_.get(), "compute_thresholds");
+        Thresholds r;
+        r.similarity = t.similarity;
+        r.lcom = t.lcom;
+        r.cbo = t.cbo;
+        r.explicit_mode = t.explicit_mode != 0;
+        return r;
+    }
+
     double lcom_normalized(ClassId c) {
         double v = 0;
         detail::check(mm_lcom_normalized(ctx_.get(), c, &v), ctx_.get(), "lcom_normalized");
@@ -393,25 +414,138 @@ private:
     }
 };
 
+// ---- several GPUs: n_workers -> GPUs (mm_group, include/mmgpu.h) --------
+
+// The sweep on n GPUs of one process: each GPU recomputes the metric pass
+// (replicas) and sweeps a cost-balanced class range; the shard lists are
+// exchanged over NCCL with exact counts and concatenated in rank order, which
+// is suggest_all's ordered list. Criteria ⊆ {Cohesion, Coupling}.
+class Group {
+public:
+    explicit Group(unsigned n_gpus) {
+        if (n_gpus == 0) throw std::invalid_argument("plan_partition: zero workers");  // parallel.hpp:29
+        mm_group* g = nullptr;
+        const mm_status st = mm_group_create(nullptr, static_cast<int>(n_gpus), &g);
+        if (st != MM_OK) detail::check(st, nullptr, "mm_group_create");
+        g_.reset(g);
+    }
+    unsigned size() const { return static_cast<unsigned>(mm_group_size(g_.get())); }
+
+    void upload(const SystemModel& model, const DependencyTable& deps) {
+        const detail::Csr csr(model, deps);
+        check(mm_group_upload(g_.get(), &csr.sys), "mm_group_upload");
+        n_classes_ = csr.sys.n_classes;
+    }
+
+    std::vector<MoveSuggestion> suggest_all(const MetricsReport& report, const Thresholds& thresholds,
+                                            const std::vector<Criterion>& criteria, Combine combine,
+                                            const SuggestOptions& opts = {}) {
+        uint32_t mask = 0;
+        for (Criterion c : criteria) mask |= 1u << static_cast<unsigned>(c);
+        if (!mask) throw std::invalid_argument("suggest_all: no criteria selected");  // suggest.hpp:313
+        if (mask & MM_CRIT_SIMILARITY)
+            throw std::invalid_argument("gpu::Group: the similarity criterion runs on one GPU (gpu::Engine)");
+        if (report.lcom.size() != n_classes_ || report.cbo.size() != n_classes_)
+            throw std::invalid_argument("gpu: report does not match the uploaded system");
+        check(mm_group_set_gates(g_.get(), report.lcom.data(), report.cbo.data()), "mm_group_set_gates");
+        mm_sweep_params p{};
+        p.criteria = mask;
+        p.combine = combine == Combine::Intersection ? MM_COMBINE_INTERSECTION : MM_COMBINE_UNION;
+        p.all_candidates = opts.all_candidates ? 1u : 0u;
+        p.top_k = 1;
+        p.thr_lcom = thresholds.lcom;
+        p.thr_cbo = thresholds.cbo;
+        p.threshold_source = MM_THR_EXPLICIT;
+        uint64_t n = 0;
+        check(mm_group_run(g_.get(), &p, &n), "mm_group_run");
+        std::vector<mm_suggestion> raw(n);
+        if (n) check(mm_group_copy_suggestions(g_.get(), raw.data(), n, &n), "mm_group_copy_suggestions");
+        std::vector<MoveSuggestion> out;
+        out.reserve(raw.size());
+        for (const mm_suggestion& r : raw) out.push_back(detail::to_suggestion(r));
+        return out;
+    }
+
+    mm_group* handle() { return g_.get(); }
+
+private:
+    struct Del {
+        void operator()(mm_group* g) const { mm_group_destroy(g); }
+    };
+    std::unique_ptr<mm_group, Del> g_;
+    uint32_t n_classes_ = 0;
+
+    void check(mm_status st, const char* what) {
+        if (st == MM_OK) return;
+        const std::string msg = std::string(what) + ": " + mm_group_last_error(g_.get());
+        switch (st) {
+            case MM_E_RANGE: throw std::out_of_range(msg);
+            case MM_E_ARG: throw std::invalid_argument(msg);
+            case MM_E_OOM: throw std::bad_alloc();
+            default: throw std::runtime_error(msg);
+        }
+    }
+};
+
+namespace detail {
+// The free functions keep one engine per host thread (a context, its streams
+// and device buffers persist across calls; the system is uploaded per call,
+// as the reference takes the model by const& each time).
+inline Engine& thread_engine() {
+    thread_local Engine e;
+    return e;
+}
+
+inline unsigned visible_gpus() {
+    const int n = mm_device_count();
+    return n > 0 ? static_cast<unsigned>(n) : 0u;
+}
+}  // namespace detail
+
 // ---- free functions with the reference signatures ------------------------
+
+inline Thresholds compute_thresholds(const MetricsReport& report, const ThresholdOverrides& ov = {}) {
+    return detail::thread_engine().compute_thresholds(report, ov);
+}
+
+// suggest_all on min(n_workers, visible GPUs) GPUs (an extension in the
+// reference's parallel_* naming: the reference's suggest_all is sequential).
+// One GPU, or the similarity criterion: the single-GPU engine.
+inline std::vector<MoveSuggestion> parallel_suggest_all(const SystemModel& model, const DependencyTable& deps,
+                                                        const MetricsReport& report, const Thresholds& thresholds,
+                                                        const std::vector<Criterion>& criteria, Combine combine,
+                                                        const SuggestOptions& opts, unsigned n_workers) {
+    if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");
+    const unsigned n = std::min(n_workers, detail::visible_gpus());
+    bool sim = false;
+    for (Criterion c : criteria) sim |= c == Criterion::Similarity;
+    if (n <= 1 || sim) {
+        Engine& e = detail::thread_engine();
+        e.upload(model, deps);
+        return e.suggest_all(report, thresholds, criteria, combine, opts);
+    }
+    Group g(n);
+    g.upload(model, deps);
+    return g.suggest_all(report, thresholds, criteria, combine, opts);
+}
 
 inline ClassMetrics parallel_class_metrics(const SystemModel& model, const DependencyTable& deps,
                                            unsigned n_workers) {
     if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.parallel_class_metrics(n_workers);
 }
 
 inline FanMetrics parallel_fan_metrics(const SystemModel& model, const DependencyTable& deps, unsigned n_workers) {
     if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.parallel_fan_metrics(n_workers);
 }
 
 inline std::vector<SimilarityEntry> all_similarities(const SystemModel& model, const DependencyTable& deps) {
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.similarities();
 }
@@ -423,7 +557,7 @@ inline std::vector<SimilarityEntry> parallel_similarities(const SystemModel& mod
 }
 
 inline MetricsReport full_report(const SystemModel& model, const DependencyTable& deps) {
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.full_report();
 }
@@ -434,7 +568,7 @@ inline MetricsReport parallel_full_report(const SystemModel& model, const Depend
 }
 
 inline WorkloadEstimate estimate_workload(const SystemModel& model, const DependencyTable& deps) {
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.estimate_workload();
 }
@@ -450,14 +584,14 @@ inline std::vector<std::uint32_t> fan_out(const SystemModel& model, const Depend
 inline std::vector<std::uint64_t> parallel_lcom_ck(const SystemModel& model, const DependencyTable& deps,
                                                    unsigned n_workers) {
     if (n_workers == 0) throw std::invalid_argument("plan_partition: zero workers");
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.parallel_lcom_ck(n_workers);
 }
 
 inline WhatIfMetrics what_if_move(MethodId method, ClassId origin, ClassId destination, const SystemModel& model,
                                   const DependencyTable& deps) {
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.what_if_move(method, origin, destination);
 }
@@ -465,7 +599,7 @@ inline WhatIfMetrics what_if_move(MethodId method, ClassId origin, ClassId desti
 inline std::vector<MoveSuggestion> suggest_by_cohesion(const SystemModel& model, const DependencyTable& deps,
                                                        const MetricsReport& report, const Thresholds& thresholds,
                                                        const SuggestOptions& opts = {}) {
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.suggest_by_cohesion(report, thresholds, opts);
 }
@@ -473,7 +607,7 @@ inline std::vector<MoveSuggestion> suggest_by_cohesion(const SystemModel& model,
 inline std::vector<MoveSuggestion> suggest_by_coupling(const SystemModel& model, const DependencyTable& deps,
                                                        const MetricsReport& report, const Thresholds& thresholds,
                                                        const SuggestOptions& opts = {}) {
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.suggest_by_coupling(report, thresholds, opts);
 }
@@ -481,7 +615,7 @@ inline std::vector<MoveSuggestion> suggest_by_coupling(const SystemModel& model,
 inline std::vector<MoveSuggestion> suggest_by_similarity(const SystemModel& model, const DependencyTable& deps,
                                                          const MetricsReport& report, const Thresholds& thresholds,
                                                          const SuggestOptions& opts = {}) {
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.suggest_by_similarity(report, thresholds, opts);
 }
@@ -490,7 +624,7 @@ inline std::vector<MoveSuggestion> suggest_all(const SystemModel& model, const D
                                                const MetricsReport& report, const Thresholds& thresholds,
                                                const std::vector<Criterion>& criteria, Combine combine,
                                                const SuggestOptions& opts = {}) {
-    Engine e;
+    Engine& e = detail::thread_engine();
     e.upload(model, deps);
     return e.suggest_all(report, thresholds, criteria, combine, opts);
 }

@@ -546,7 +546,7 @@ int ref_sweep_sample(void* h, const double* lcom_gate, const uint32_t* cbo_gate,
 // Per-method work is independent given the report and thresholds, so any
 // subset and any thread split give suggest_all's list restricted to that
 // subset. methods == NULL: every method. dynamic != 0: methods handed out in
-// chunks of 64 from an atomic counter (Zipf giants); else the reference's
+// small chunks from an atomic counter (Zipf giants); else the reference's
 // detail::run_partitioned contiguous ranges. *n_candidates = Σ
 // |used_classes(u)| over the swept methods (ungated). Result kept in the
 // model handle (ref_sweep_copy).
@@ -588,13 +588,14 @@ int ref_sweep(void* h, const double* lcom_gate, const uint32_t* cbo_gate, const 
     try {
         if (dynamic) {
             std::atomic<uint64_t> next{0};
+            const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(64, n / (16ull * W)));
             std::vector<std::thread> th;
             for (unsigned w = 0; w < W; ++w)
                 th.emplace_back([&, w] {
                     for (;;) {
-                        const uint64_t b = next.fetch_add(64);
+                        const uint64_t b = next.fetch_add(chunk);
                         if (b >= n) break;
-                        for (uint64_t i = b; i < std::min<uint64_t>(n, b + 64); ++i) one(parts[w], mid(i));
+                        for (uint64_t i = b; i < std::min<uint64_t>(n, b + chunk); ++i) one(parts[w], mid(i));
                     }
                 });
             for (std::thread& t : th) t.join();

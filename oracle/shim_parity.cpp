@@ -125,6 +125,36 @@ static void check_system(const std::string& name, const SystemModel& model, cons
         compute_thresholds(report, ThresholdOverrides{0.2, 0.4, 1.0}),
         compute_thresholds(report, ThresholdOverrides{std::nullopt, 0.0, 0.0}),
     };
+    // compute_thresholds on the device (suggest.hpp:46-61), similarity table included when small
+    {
+        MetricsReport withsim = report;
+        if (model.method_count() <= 3000) withsim.similarity = all_similarities(model, deps);
+        for (const ThresholdOverrides& ov : {ThresholdOverrides{}, ThresholdOverrides{0.2, 0.4, 1.0},
+                                             ThresholdOverrides{std::nullopt, 0.0, std::nullopt}})
+            expect(gpu::compute_thresholds(withsim, ov) == compute_thresholds(withsim, ov),
+                   name + " gpu::compute_thresholds");
+    }
+    // n_workers -> GPUs: the multi-GPU group (one GPU here) and parallel_suggest_all
+    {
+        gpu::Group grp(1);
+        grp.upload(model, deps);
+        const Thresholds t0 = thrs[0];
+        for (Combine cb : {Combine::Union, Combine::Intersection})
+            for (bool allc : {false, true}) {
+                SuggestOptions o;
+                o.all_candidates = allc;
+                const auto want = suggest_all(model, deps, report, t0, {Criterion::Cohesion, Criterion::Coupling}, cb, o);
+                expect(grp.suggest_all(report, t0, {Criterion::Cohesion, Criterion::Coupling}, cb, o) == want,
+                       name + " gpu::Group suggest_all");
+                expect(gpu::parallel_suggest_all(model, deps, report, t0, {Criterion::Cohesion, Criterion::Coupling},
+                                                 cb, o, 4) == want,
+                       name + " gpu::parallel_suggest_all");
+            }
+        same_outcome([&] { return parallel_lcom_ck(model, deps, 0).size(); },
+                     [&] { return gpu::parallel_suggest_all(model, deps, report, t0, {Criterion::Cohesion}, Combine::Union,
+                                                            SuggestOptions{}, 0).size(); },
+                     name + " zero workers");
+    }
     const std::vector<std::vector<Criterion>> crits = {
         {Criterion::Cohesion}, {Criterion::Coupling}, {Criterion::Cohesion, Criterion::Coupling},
         {Criterion::Coupling, Criterion::Cohesion, Criterion::Cohesion}};

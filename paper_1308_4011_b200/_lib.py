@@ -35,6 +35,7 @@ def _exc_for(status: int):
 
 _SIGS = {
     "mm_abi_version": (C.c_int, []),
+    "mm_device_count": (C.c_int, []),
     "mm_last_error": (C.c_char_p, [C.c_void_p]),
     "mm_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "mm_ctx_destroy": (None, [C.c_void_p]),
@@ -57,6 +58,8 @@ _SIGS = {
     "mm_lcom_ck": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64)]),
     "mm_cbo": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32)]),
     "mm_compute_thresholds": (C.c_int, [C.c_void_p, C.POINTER(abi.mm_overrides), C.POINTER(abi.mm_thresholds)]),
+    "mm_report_thresholds": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
+                                       C.c_uint64, C.POINTER(abi.mm_overrides), C.POINTER(abi.mm_thresholds)]),
     "mm_sequential_mean": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_double),
                                      C.POINTER(C.c_int)]),
     "mm_what_if": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(abi.mm_whatif)]),

@@ -247,13 +247,58 @@ __device__ __forceinline__ int select_next(const SweepArgs& a, const E& en, uint
     return best;
 }
 
+// Top-k / all-candidates modes keep the passing destinations as bit masks over
+// the method's used-list index (bits 0..30). A method whose list has 32 or
+// more entries ("wide", e.g. a hub calling into 100+ classes) instead keeps
+// three counts — destinations passing only cohesion, only coupling, both —
+// in a side table; k_offsets turns them into its record count under the
+// class gates and k_write re-scores its candidates to emit them. No cap on
+// the number of classes a method uses.
+constexpr uint32_t kMaskBits = 31;
+constexpr uint32_t kWideMark = 0x80000000u;  // res.x marker of a wide method (never a mask bit)
+constexpr int kTopMax = 8;
+
+// records of a top-k / all-candidates method from its pass counts under the
+// class gates: union = every gated pass, intersection = passes of both
+__device__ __forceinline__ uint32_t wide_count(uint32_t n_co, uint32_t n_cp, uint32_t n_both, bool gcoh, bool gcoup,
+                                               bool inter) {
+    if (inter) return (gcoh && gcoup) ? n_both : 0u;
+    return (gcoh ? n_co + n_both : 0u) + (gcoup ? n_cp + n_both : 0u) - ((gcoh && gcoup) ? n_both : 0u);
+}
+
 struct MethodResult {
     uint32_t count;
     uint32_t cands;
     uint32_t gated;
     uint32_t bd_coh, bd_coup;             // best-only mode
-    unsigned long long m_coh, m_coup;     // top-k / all mode (bits over list index)
+    unsigned long long m_coh, m_coup;     // top-k / all mode (bits over list index, narrow lists)
+    uint32_t n_co, n_cp, n_both;          // top-k / all mode: passing only cohesion / only coupling / both
+    uint32_t n_list;                      // used-list length (own class included)
 };
+
+// the k best passing list indices of one criterion, ascending by (key, index)
+// (top-k extension; k ≤ kTopMax rounds of select_next)
+template <class E>
+__device__ __forceinline__ int select_topk(const SweepArgs& a, const E& en, uint32_t o, const Origin& org, bool coh,
+                                           int* sel) {
+    double pk = 0.0;
+    int pi = -1, n = 0;
+    for (uint32_t t = 0; t < a.topk && t < (uint32_t)kTopMax; ++t) {
+        double key;
+        const int k = select_next(a, en, o, org, coh, pi >= 0, pk, pi, key);
+        if (k < 0) break;
+        sel[n++] = k;
+        pk = key;
+        pi = k;
+    }
+    return n;
+}
+
+__device__ __forceinline__ bool in_sel(const int* sel, int n, int k) {
+    bool f = false;
+    for (int i = 0; i < n; ++i) f |= sel[i] == k;
+    return f;
+}
 
 template <class E>
 __device__ __forceinline__ MethodResult evaluate(const SweepArgs& a, const E& en, uint32_t o,
@@ -261,12 +306,14 @@ __device__ __forceinline__ MethodResult evaluate(const SweepArgs& a, const E& en
     MethodResult r;
     r.bd_coh = r.bd_coup = kNone;
     r.m_coh = r.m_coup = 0;
-    uint32_t cands = 0;
+    r.n_co = r.n_cp = r.n_both = 0;
+    uint32_t cands = 0, n_list = 0;
     double best_coh = 0.0;
     uint32_t best_coup = 0;
     // every candidate is scored for both criteria (ungated); the class gates
     // only decide what is emitted
     en.each([&](int k, uint32_t d, uint32_t hd) {
+        n_list = (uint32_t)k + 1;
         if (d == o) return;
         ++cands;
         bool pcoh, pcoup;
@@ -276,31 +323,30 @@ __device__ __forceinline__ MethodResult evaluate(const SweepArgs& a, const E& en
         // argmin over (key, d), d ascending, strict < : lowest d wins ties (suggest.hpp:180-184)
         if (pcoh && (r.bd_coh == kNone || kc < best_coh)) { r.bd_coh = d; best_coh = kc; }
         if (pcoup && (r.bd_coup == kNone || kp < best_coup)) { r.bd_coup = d; best_coup = kp; }
-        if (a.mode == 2 && k < 64) {
-            if (pcoh) r.m_coh |= 1ull << k;
-            if (pcoup) r.m_coup |= 1ull << k;
-        } else if (a.mode == 2 && (pcoh || pcoup)) {
-            atomicOr(a.err, 2u);
+        if (a.mode == 2) {
+            if (k < (int)kMaskBits) {
+                if (pcoh) r.m_coh |= 1ull << k;
+                if (pcoup) r.m_coup |= 1ull << k;
+            }
+            r.n_both += pcoh && pcoup;
+            r.n_co += pcoh && !pcoup;
+            r.n_cp += pcoup && !pcoh;
         }
     });
+    r.n_list = n_list;
     if (a.mode == 1) {
-        for (int c = 0; c < 2; ++c) {
-            const bool coh = c == 0;
-            if (coh ? !gcoh : !gcoup) continue;
-            double pk = 0.0;
-            int pi = -1;
-            unsigned long long m = 0;
-            for (uint32_t t = 0; t < a.topk; ++t) {
-                double key;
-                const int k = select_next(a, en, o, org, coh, pi >= 0, pk, pi, key);
-                if (k < 0) break;
-                if (k >= 64) { atomicOr(a.err, 2u); break; }
-                m |= 1ull << k;
-                pk = key;
-                pi = k;
-            }
-            (coh ? r.m_coh : r.m_coup) = m;
-        }
+        int sc[kTopMax], sp[kTopMax];
+        const int nc = gcoh ? select_topk(a, en, o, org, true, sc) : 0;
+        const int np = gcoup ? select_topk(a, en, o, org, false, sp) : 0;
+        for (int i = 0; i < nc; ++i)
+            if (sc[i] < (int)kMaskBits) r.m_coh |= 1ull << sc[i];
+        for (int i = 0; i < np; ++i)
+            if (sp[i] < (int)kMaskBits) r.m_coup |= 1ull << sp[i];
+        uint32_t both = 0;
+        for (int i = 0; i < nc; ++i) both += in_sel(sp, np, sc[i]);
+        r.n_both = both;
+        r.n_co = (uint32_t)nc - both;
+        r.n_cp = (uint32_t)np - both;
     }
     if (!gcoh) { r.bd_coh = kNone; r.m_coh = 0; }
     if (!gcoup) { r.bd_coup = kNone; r.m_coup = 0; }
@@ -314,7 +360,7 @@ __device__ __forceinline__ MethodResult evaluate(const SweepArgs& a, const E& en
         count = inter ? (same ? 1u : 0u)
                       : (uint32_t)(r.bd_coh != kNone) + (uint32_t)(r.bd_coup != kNone) - (same ? 1u : 0u);
     } else {
-        count = __popcll(inter ? (r.m_coh & r.m_coup) : (r.m_coh | r.m_coup));
+        count = wide_count(r.n_co, r.n_cp, r.n_both, gcoh, gcoup, inter);
     }
     r.count = count;
     return r;
@@ -327,20 +373,38 @@ __device__ __forceinline__ void store_record(mm_suggestion* dst, const mm_sugges
     for (int i = 0; i < 4; ++i) d[i] = src[i];
 }
 
+// wide == true (top-k / all modes, lists of ≥ 32 entries): the passing
+// destinations are re-derived here; r.m_coh / r.m_coup then hold the class
+// gates (bit 0) instead of masks
 template <class E>
 __device__ __forceinline__ void emit(const SweepArgs& a, const E& en, uint32_t p, uint32_t o,
-                                     const Origin& org, const MethodResult& r, uint64_t at) {
+                                     const Origin& org, const MethodResult& r, uint64_t at, bool wide = false) {
     const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
     const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
+    int sc[kTopMax], sp[kTopMax], nc = 0, np = 0;
+    if (wide && a.mode == 1) {
+        if (r.m_coh) nc = select_topk(a, en, o, org, true, sc);
+        if (r.m_coup) np = select_topk(a, en, o, org, false, sp);
+    }
     en.each([&](int k, uint32_t d, uint32_t hd) {
         if (d == o) return;
         bool tcoh, tcoup;
         if (a.mode == 0) {
             tcoh = d == r.bd_coh;
             tcoup = d == r.bd_coup;
+        } else if (!wide) {
+            tcoh = k < (int)kMaskBits && ((r.m_coh >> k) & 1ull);
+            tcoup = k < (int)kMaskBits && ((r.m_coup >> k) & 1ull);
+        } else if (a.mode == 1) {
+            tcoh = in_sel(sc, nc, k);
+            tcoup = in_sel(sp, np, k);
         } else {
-            tcoh = k < 64 && ((r.m_coh >> k) & 1ull);
-            tcoup = k < 64 && ((r.m_coup >> k) & 1ull);
+            bool pcoh, pcoup;
+            double kc;
+            uint32_t kp;
+            score(a, en, org, d, hd, pcoh, kc, pcoup, kp);
+            tcoh = pcoh && r.m_coh;
+            tcoup = pcoup && r.m_coup;
         }
         if (inter ? !(tcoh && tcoup) : !(tcoh || tcoup)) return;
         const Dest dv = eval_dest(a.rec, a.ux, a.dense, en, d, hd);
@@ -437,9 +501,13 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
         else r = evaluate(a, sen, o, org, true, true);
         cands = r.cands;
         uint4 out;
-        if (a.mode == 0) out = make_uint4(r.bd_coh, r.bd_coup, r.cands, 0);
-        else {
-            if ((r.m_coh | r.m_coup) >> 32) atomicOr(a.err, 2u);
+        if (a.mode == 0) {
+            out = make_uint4(r.bd_coh, r.bd_coup, r.cands, 0);
+        } else if (r.n_list > kMaskBits) {  // wide: counts in the side table
+            const uint32_t slot = atomicAdd(a.n_wide, 1u);
+            a.wide_cnt[slot] = make_uint4(r.n_co, r.n_cp, r.n_both, (uint32_t)pos);
+            out = make_uint4(kWideMark | slot, 0u, r.cands, 0);
+        } else {
             out = make_uint4((uint32_t)r.m_coh, (uint32_t)r.m_coup, r.cands, 0);
         }
         a.res[pos] = out;
@@ -496,6 +564,11 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
             count = inter ? (same ? 1u : 0u) : (uint32_t)(bc != kNone) + (uint32_t)(bp != kNone) - (same ? 1u : 0u);
             v.x = bc;
             v.y = bp;
+        } else if (v.x & kWideMark) {
+            const uint4 wc = a.wide_cnt[v.x & ~kWideMark];
+            count = wide_count(wc.x, wc.y, wc.z, gcoh, gcoup, inter);
+            v.x = kWideMark | (gcoh ? 1u : 0u);  // k_write re-derives the destinations under these gates
+            v.y = gcoup ? 1u : 0u;
         } else {
             v.x = gcoh ? v.x : 0u;
             v.y = gcoup ? v.y : 0u;
@@ -594,13 +667,15 @@ __global__ void __launch_bounds__(kSweepTile) k_write(SweepArgs a) {
         const uint32_t o = __ldg(a.pos_owner + pos);
         const uint32_t p = __ldg(a.s.cls_methods + pos);
         MethodResult res{};
+        const bool wide = a.mode != 0 && (r.x & kWideMark);
         if (a.mode == 0) { res.bd_coh = r.x; res.bd_coup = r.y; }
+        else if (wide) { res.m_coh = r.x & 1u; res.m_coup = r.y & 1u; }
         else { res.m_coh = r.x; res.m_coup = r.y; }
         SmemEnum ren{s_X + threadIdx.x, s_H + threadIdx.x, 0};
         StreamEnum sen;
         Origin org;
-        if (load_method<K>(a, pos, p, o, ren, sen, org)) emit(a, ren, p, o, org, res, r.w);
-        else emit(a, sen, p, o, org, res, r.w);
+        if (load_method<K>(a, pos, p, o, ren, sen, org)) emit(a, ren, p, o, org, res, r.w, wide);
+        else emit(a, sen, p, o, org, res, r.w, wide);
     }
 }
 

@@ -43,9 +43,10 @@ struct Ctl {  // small device-resident control block
     uint32_t tile_counter;
     uint32_t err;
     uint32_t n_emit;
-    uint32_t pad;
+    uint32_t n_wide;    // top-k / all-candidates methods with >= 32 used classes (side table)
     unsigned long long stats[4];
     DevThresholds thr;
+    DevThresholds thr_aux;  // mm_sequential_mean / the similarity mean (never the metric pass's means)
 };
 
 struct KStat {
@@ -59,9 +60,13 @@ struct Pending {
 };
 
 template <class T>
-struct DBuf {
+struct DBuf {  // owning device buffer (freed on release() or destruction)
     T* p = nullptr;
     size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
     cudaError_t alloc(size_t count) {
         release();
         n = count;
@@ -155,6 +160,7 @@ struct mm_ctx {
     DBuf<uint32_t> pos_owner;
     DBuf<uint4> res;
     DBuf<uint32_t> emit_list;
+    DBuf<uint4> wide_cnt;  // top-k / all-candidates: pass counts of methods with >= 32 used classes
     DBuf<double> gate_lcom;
     DBuf<uint32_t> gate_cbo;
     bool gates_set = false;
@@ -324,6 +330,12 @@ extern "C" {
 
 int mm_abi_version(void) { return MMGPU_ABI_VERSION; }
 
+int mm_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
 const char* mm_last_error(const mm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 mm_status mm_ctx_create(int device, mm_ctx** out) {
@@ -392,6 +404,7 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     ctx->out.release();
     ctx->res.release();
     ctx->emit_list.release();
+    ctx->wide_cnt.release();
     ctx->gate_lcom.release();
     ctx->gate_cbo.release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -890,36 +903,95 @@ static mm_status compute_similarities(mm_ctx* ctx) {
     // layout of the u32 scratch
     const uint64_t o_ucoff = 0, o_uc = o_ucoff + M + 1, o_uaoff = o_uc + (Ec ? Ec : 1), o_ua = o_uaoff + A + 1,
                    o_cur = o_ua + (Ea ? Ea : 1), o_tot = o_cur + mx, o_cnt = o_tot + nb, o_off = o_cnt + M + 1,
-                   o_wide = o_off + M + 1, o_end = o_wide + M + 1;
+                   o_wide = o_off + M + 1, o_huge = o_wide + M + 1, o_end = o_huge + M + 1;
     MM_CUDA(ctx, ctx->sim_u32.ensure(o_end));
-    MM_CUDA(ctx, ctx->sim_ctl.ensure(4));
+    MM_CUDA(ctx, ctx->sim_ctl.ensure(4 + M + 1));  // control words, then the huge rows' candidate counts
     uint32_t* u = ctx->sim_u32.p;
     unsigned long long* ctl = ctx->sim_ctl.p;
-    uint32_t* small = reinterpret_cast<uint32_t*>(ctl + 1);  // n_wide, err, grand
+    uint32_t* small = reinterpret_cast<uint32_t*>(ctl + 1);  // n_wide, err, grand, n_huge
+    unsigned long long* huge_tot = ctl + 4;
     MM_CUDA(ctx, cudaMemsetAsync(ctl, 0, 4 * sizeof(unsigned long long), ctx->stream));
     const DevModel dm = ctx->dev();
     mm_status st = run(ctx, "similarity", [&] {
         launch_similarity_index(dm, Ec, Ea, u + o_ucoff, u + o_uc, u + o_uaoff, u + o_ua, u + o_cur, u + o_tot,
                                 small + 2, ctx->stream);
         launch_similarity_rows(dm, 0, u + o_ucoff, u + o_uc, u + o_uaoff, u + o_ua, u + o_cnt, nullptr, nullptr,
-                               u + o_wide, small, small + 1, ctl, ctx->stream);
+                               u + o_wide, small, small + 1, ctl, u + o_huge, huge_tot, small + 3, ctx->stream);
     });
     if (st) return st;
     unsigned long long h[3] = {0, 0, 0};
     MM_CUDA(ctx, cudaMemcpyAsync(h, ctl, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    const uint32_t err = static_cast<uint32_t>(h[1] >> 32);
-    if (err & 2u)
-        return fail(ctx, MM_E_UNSUPPORTED, "mm_similarities: a method's candidate list exceeds 4096 entries");
+    // rows beyond the warp buffers: in batches through global scratch (any length)
+    const uint32_t n_huge = static_cast<uint32_t>(h[2] >> 32);
+    std::vector<uint32_t> hrows(n_huge);
+    std::vector<unsigned long long> htot(n_huge);
+    struct Batch { uint32_t first, count; uint64_t items; };
+    std::vector<Batch> batches;
+    DBuf<uint32_t> hseg, hkeys, hsorted;
+    DBuf<char> htemp;
+    if (n_huge) {
+        MM_CUDA(ctx, cudaMemcpy(hrows.data(), u + o_huge, 4ull * n_huge, cudaMemcpyDeviceToHost));
+        MM_CUDA(ctx, cudaMemcpy(htot.data(), huge_tot, 8ull * n_huge, cudaMemcpyDeviceToHost));
+        const uint64_t kBatchItems = 64ull << 20;  // 256 MB of keys per batch (a longer row gets its own)
+        uint64_t max_items = 0;
+        for (uint32_t k = 0; k < n_huge;) {
+            Batch b{k, 0, 0};
+            while (k < n_huge && (b.count == 0 || b.items + htot[k] <= kBatchItems)) b.items += htot[k++], ++b.count;
+            if (b.items >= (1ull << 31)) return fail(ctx, MM_E_UNSUPPORTED, "mm_similarities: one method's candidate "
+                                                                             "list exceeds 2^31 entries");
+            max_items = std::max(max_items, b.items);
+            batches.push_back(b);
+        }
+        MM_CUDA(ctx, hseg.alloc(n_huge + batches.size()));
+        MM_CUDA(ctx, hkeys.alloc(max_items ? max_items : 1));
+        MM_CUDA(ctx, hsorted.alloc(max_items ? max_items : 1));
+        MM_CUDA(ctx, htemp.alloc(std::max<size_t>(1, similarity_huge_temp_bytes((uint32_t)max_items, n_huge))));
+        std::vector<uint32_t> seg;
+        seg.reserve(n_huge + batches.size());
+        for (const Batch& b : batches) {
+            uint64_t acc = 0;
+            for (uint32_t k = b.first; k < b.first + b.count; ++k) {
+                seg.push_back((uint32_t)acc);
+                acc += htot[k];
+            }
+            seg.push_back((uint32_t)acc);
+        }
+        MM_CUDA(ctx, cudaMemcpyAsync(hseg.p, seg.data(), 4 * seg.size(), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    auto huge_pass = [&](int pass) -> mm_status {
+        uint32_t seg_at = 0;
+        for (const Batch& b : batches) {
+            cudaError_t e = cudaSuccess;
+            mm_status s2 = run(ctx, "similarity", [&] {
+                e = launch_similarity_huge(dm, pass, u + o_ucoff, u + o_uc, u + o_uaoff, u + o_ua, u + o_huge + b.first,
+                                           b.count, hseg.p + seg_at, (uint32_t)b.items, hkeys.p, hsorted.p, htemp.p,
+                                           htemp.n, u + o_cnt, u + o_off, ctx->sim_out.p, ctl, ctx->stream);
+            });
+            if (s2) return s2;
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "similarity (huge rows)");
+            seg_at += b.count + 1;
+        }
+        return MM_OK;
+    };
+    if (n_huge) {
+        if (mm_status s2 = huge_pass(0)) return s2;
+        MM_CUDA(ctx, cudaMemcpyAsync(h, ctl, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+        MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
     if (h[0] >= (1ull << 32)) return fail(ctx, MM_E_UNSUPPORTED, "mm_similarities: more than 2^32 - 1 pairs");
     ctx->sim_n = h[0];
     MM_CUDA(ctx, ctx->sim_out.ensure(ctx->sim_n ? ctx->sim_n : 1));
     st = run(ctx, "similarity", [&] {
         launch_scan(u + o_cnt, u + o_off, static_cast<uint32_t>(M), u + o_tot, small + 2, ctx->stream);
         launch_similarity_rows(dm, 1, u + o_ucoff, u + o_uc, u + o_uaoff, u + o_ua, u + o_cnt, u + o_off,
-                               ctx->sim_out.p, u + o_wide, small, small + 1, ctl, ctx->stream);
+                               ctx->sim_out.p, u + o_wide, small, small + 1, ctl, u + o_huge, huge_tot, small + 3,
+                               ctx->stream);
     });
     if (st) return st;
+    if (n_huge)
+        if (mm_status s2 = huge_pass(1)) return s2;
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // the batch scratch is freed on return
     ctx->sim_valid = true;
     return MM_OK;
 }
@@ -1065,6 +1137,27 @@ mm_status mm_cbo(mm_ctx* ctx, uint32_t cls, uint32_t* out) {
     return single(ctx, cls, out, ctx ? ctx->cbo.p : nullptr, 4);
 }
 
+// mean of n doubles on the device with compute_thresholds' sequential-sum
+// semantics (the threshold kernel), into ctl->thr_aux; `values` is device memory
+static mm_status device_mean(mm_ctx* ctx, const double* values, uint64_t n, double* mean, int* fast) {
+    if (n >= 0xffffffffull) return fail(ctx, MM_E_RANGE, "mean: n too large");
+    DevThresholds* dt = &ctx->ctl.p->thr_aux;
+    DBuf<char> scratch;
+    MM_CUDA(ctx, scratch.alloc(thresholds_scratch_bytes((uint32_t)n)));
+    cudaError_t te = cudaSuccess;
+    mm_status st = run(ctx, "thresholds", [&] {
+        te = launch_thresholds(values, nullptr, (uint32_t)n, dt, scratch.p, scratch.n, ctx->stream, false);
+    });
+    if (st) return st;
+    if (te != cudaSuccess) return cuda_fail(ctx, te, "thresholds");
+    DevThresholds h{};
+    MM_CUDA(ctx, cudaMemcpyAsync(&h, dt, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    *mean = h.lcom;
+    if (fast) *fast = (int)h.fast_path_ok;
+    return MM_OK;
+}
+
 mm_status mm_compute_thresholds(mm_ctx* ctx, const mm_overrides* ov, mm_thresholds* out) {
     if (!ctx || !out) return MM_E_ARG;
     if (mm_status st = ensure_metrics(ctx)) return st;
@@ -1072,10 +1165,81 @@ mm_status mm_compute_thresholds(mm_ctx* ctx, const mm_overrides* ov, mm_threshol
     DevThresholds t{};
     MM_CUDA(ctx, cudaMemcpyAsync(&t, &ctx->ctl.p->thr, sizeof t, cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    // similarity: the mean of full_report's similarity table (suggest.hpp:55-56),
+    // the device table (built here when absent), in table order
+    double sim_mean = 0.0;
+    if (!(ov && ov->has_similarity)) {
+        if (!ctx->sim_valid)
+            if (mm_status st = compute_similarities(ctx)) return st;
+        if (ctx->sim_n) {
+            DBuf<double> vals;
+            MM_CUDA(ctx, vals.alloc(ctx->sim_n));
+            MM_CUDA(ctx, cudaMemcpy2DAsync(vals.p, sizeof(double), &ctx->sim_out.p->value, sizeof(mm_similarity),
+                                           sizeof(double), ctx->sim_n, cudaMemcpyDeviceToDevice, ctx->stream));
+            if (mm_status st = device_mean(ctx, vals.p, ctx->sim_n, &sim_mean, nullptr)) return st;
+        }
+    }
     std::memset(out, 0, sizeof *out);
-    out->similarity = (ov && ov->has_similarity) ? ov->similarity : 0.0;
+    out->similarity = (ov && ov->has_similarity) ? ov->similarity : sim_mean;
     out->lcom = (ov && ov->has_lcom) ? ov->lcom : t.lcom;
     out->cbo = (ov && ov->has_cbo) ? ov->cbo : t.cbo;
+    out->explicit_mode = (uint8_t)(ov && (ov->has_similarity || ov->has_lcom || ov->has_cbo));
+    return MM_OK;
+}
+
+mm_status mm_report_thresholds(mm_ctx* ctx, const double* lcom, uint64_t n_lcom, const uint32_t* cbo, uint64_t n_cbo,
+                               const double* similarity, uint64_t n_sim, const mm_overrides* ov, mm_thresholds* out) {
+    if (!ctx || !out || (n_lcom && !lcom) || (n_cbo && !cbo) || (n_sim && !similarity)) return MM_E_ARG;
+    if (n_lcom >= 0xffffffffull || n_cbo >= 0xffffffffull || n_sim >= 0xffffffffull)
+        return fail(ctx, MM_E_RANGE, "compute_thresholds: too many values");
+    if (mm_status st = set_device(ctx)) return st;
+    const bool need_l = !(ov && ov->has_lcom), need_c = !(ov && ov->has_cbo), need_s = !(ov && ov->has_similarity);
+    double ml = 0.0, mc = 0.0, ms = 0.0;
+    DevThresholds* dt = &ctx->ctl.p->thr_aux;
+    auto means = [&](const double* l, const uint32_t* c, uint64_t n, double* out_l, double* out_c) -> mm_status {
+        if (!n) return MM_OK;
+        DBuf<double> dl;
+        DBuf<uint32_t> dc;
+        MM_CUDA(ctx, dl.alloc(n));
+        if (l) MM_CUDA(ctx, cudaMemcpyAsync(dl.p, l, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+        else MM_CUDA(ctx, cudaMemsetAsync(dl.p, 0, 8 * n, ctx->stream));
+        if (c) {
+            MM_CUDA(ctx, dc.alloc(n));
+            MM_CUDA(ctx, cudaMemcpyAsync(dc.p, c, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        DBuf<char> scratch;
+        MM_CUDA(ctx, scratch.alloc(thresholds_scratch_bytes((uint32_t)n)));
+        cudaError_t te = cudaSuccess;
+        mm_status st = run(ctx, "thresholds", [&] {
+            te = launch_thresholds(dl.p, dc.p, (uint32_t)n, dt, scratch.p, scratch.n, ctx->stream, true);
+        });
+        if (st) return st;
+        if (te != cudaSuccess) return cuda_fail(ctx, te, "thresholds");
+        DevThresholds h{};
+        MM_CUDA(ctx, cudaMemcpyAsync(&h, dt, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+        MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (out_l) *out_l = h.lcom;
+        if (out_c) *out_c = h.cbo;
+        return MM_OK;
+    };
+    if (need_l && need_c && n_lcom == n_cbo) {
+        if (mm_status st = means(lcom, cbo, n_lcom, &ml, &mc)) return st;
+    } else {
+        if (need_l)
+            if (mm_status st = means(lcom, nullptr, n_lcom, &ml, nullptr)) return st;
+        if (need_c)
+            if (mm_status st = means(nullptr, cbo, n_cbo, nullptr, &mc)) return st;
+    }
+    if (need_s && n_sim) {
+        DBuf<double> d;
+        MM_CUDA(ctx, d.alloc(n_sim));
+        MM_CUDA(ctx, cudaMemcpyAsync(d.p, similarity, 8 * n_sim, cudaMemcpyHostToDevice, ctx->stream));
+        if (mm_status st = device_mean(ctx, d.p, n_sim, &ms, nullptr)) return st;
+    }
+    std::memset(out, 0, sizeof *out);
+    out->similarity = need_s ? ms : ov->similarity;
+    out->lcom = need_l ? ml : ov->lcom;
+    out->cbo = need_c ? mc : ov->cbo;
     out->explicit_mode = (uint8_t)(ov && (ov->has_similarity || ov->has_lcom || ov->has_cbo));
     return MM_OK;
 }
@@ -1153,12 +1317,15 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     MM_CUDA(ctx, ctx->tile_state.ensure(n_off ? n_off : 1));
     MM_CUDA(ctx, ctx->res.ensure(npos ? npos : 1));
     MM_CUDA(ctx, ctx->emit_list.ensure(npos ? npos : 1));
+    const void* wide_before = ctx->wide_cnt.p;
+    if (mode != 0) MM_CUDA(ctx, ctx->wide_cnt.ensure(npos ? npos : 1));
+    if (wide_before != ctx->wide_cnt.p) ++ctx->layout_gen;
     if (before[0] != ctx->out.p || before[1] != ctx->tile_state.p || before[2] != ctx->res.p ||
         before[3] != ctx->emit_list.p)
         ++ctx->layout_gen;
     Ctl* ctl = ctx->ctl.p;
     if (n_off) MM_CUDA(ctx, cudaMemsetAsync(ctx->tile_state.p, 0, 8ull * n_off, ctx->stream));
-    // tile_counter, err, pad, stats
+    // tile_counter, err, n_emit, n_wide, stats
     MM_CUDA(ctx, cudaMemsetAsync(&ctl->tile_counter, 0, offsetof(Ctl, thr) - offsetof(Ctl, tile_counter),
                                  ctx->stream));
     SweepArgs a{};
@@ -1190,6 +1357,8 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     a.tile_counter = &ctl->tile_counter;
     a.stats = ctl->stats;
     a.err = &ctl->err;
+    a.wide_cnt = ctx->wide_cnt.p;
+    a.n_wide = &ctl->n_wide;
     mm_status st = run(ctx, "score", [&] { launch_score(a, n_tiles, ctx->stream); });
     if (st) return st;
     if (a.thr_device)
@@ -1294,8 +1463,6 @@ mm_status mm_sweep_stats_get(mm_ctx* ctx, mm_sweep_stats* out) {
     Ctl h{};
     MM_CUDA(ctx, cudaMemcpyAsync(&h, ctx->ctl.p, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    if (h.err & 2u)
-        return fail(ctx, MM_E_UNSUPPORTED, "a method uses more than 32 classes (all/top-k mode limit)");
     out->candidates = h.stats[0];
     out->gated_whatifs = h.stats[1];
     out->suggestions = h.stats[2];
@@ -1341,8 +1508,6 @@ mm_status mm_copy_suggestions(mm_ctx* ctx, mm_suggestion* out, uint64_t cap, uin
     if (k) MM_CUDA(ctx, cudaMemcpyAsync(out, ctx->out.p, sizeof(mm_suggestion) * k, cudaMemcpyDeviceToHost,
                                         ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    if (h.err & 2u)
-        return fail(ctx, MM_E_UNSUPPORTED, "a method uses more than 32 classes (all/top-k mode limit)");
     *n_out = h.stats[2];
     if (h.stats[2] > cap) return fail(ctx, MM_E_CAPACITY, "output buffer too small");
     return MM_OK;
@@ -1355,26 +1520,7 @@ mm_status mm_sequential_mean(mm_ctx* ctx, const double* values, uint64_t n, doub
     DBuf<double> d;
     MM_CUDA(ctx, d.alloc(n ? n : 1));
     if (n) MM_CUDA(ctx, cudaMemcpyAsync(d.p, values, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
-    if (mm_status st2 = join_thresholds(ctx)) return st2;
-    DevThresholds* dt = &ctx->ctl.p->thr;
-    DBuf<char> scratch;
-    MM_CUDA(ctx, scratch.alloc(thresholds_scratch_bytes((uint32_t)n)));
-    cudaError_t te = cudaSuccess;
-    mm_status st = run(ctx, "thresholds", [&] {
-        te = launch_thresholds(d.p, nullptr, (uint32_t)n, dt, scratch.p, scratch.n, ctx->stream, false);
-    });
-    if (st) return st;
-    if (te != cudaSuccess) return cuda_fail(ctx, te, "thresholds");
-    DevThresholds h{};
-    MM_CUDA(ctx, cudaMemcpyAsync(&h, dt, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
-    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    d.release();
-    scratch.release();
-    ctx->metrics_valid = false;  // the control block's thresholds were overwritten
-    *out = h.lcom;
-    if (fast_path) *fast_path = (int)h.fast_path_ok;
-    return MM_OK;
+    return device_mean(ctx, d.p, n, out, fast_path);
 }
 
 mm_status mm_pinned_alloc(uint64_t bytes, void** out) {

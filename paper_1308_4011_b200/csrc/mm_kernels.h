@@ -51,7 +51,9 @@ struct SweepArgs {
     unsigned long long* tile_state;
     uint32_t* tile_counter;
     unsigned long long* stats;  // [candidates, gated, suggestions, methods]
-    uint32_t* err;              // bit 1: distinct-class overflow in all/top-k mode
+    uint32_t* err;              // reserved error bits
+    uint4* wide_cnt;            // top-k / all modes: counts of methods with ≥ 32 used classes
+    uint32_t* n_wide;           // their number
 };
 
 void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t* bad, cudaStream_t st);
@@ -88,7 +90,15 @@ cudaError_t launch_similarity_index(const DevModel& s, uint64_t Ec, uint64_t Ea,
 cudaError_t launch_similarity_rows(const DevModel& s, int pass, const uint32_t* uc_off, const uint32_t* uc,
                                    const uint32_t* ua_off, const uint32_t* ua, uint32_t* row_cnt,
                                    const uint32_t* row_off, mm_similarity* out, uint32_t* wide_list, uint32_t* n_wide,
-                                   uint32_t* err, unsigned long long* total, cudaStream_t st);
+                                   uint32_t* err, unsigned long long* total, uint32_t* huge_list,
+                                   unsigned long long* huge_tot, uint32_t* n_huge, cudaStream_t st);
+// rows beyond the warp buffers: batches of (rows, segment offsets, items) through global scratch
+size_t similarity_huge_temp_bytes(uint32_t max_items, uint32_t max_rows);
+cudaError_t launch_similarity_huge(const DevModel& s, int pass, const uint32_t* uc_off, const uint32_t* uc,
+                                   const uint32_t* ua_off, const uint32_t* ua, const uint32_t* rows, uint32_t n_rows,
+                                   const uint32_t* seg, uint32_t n_items, uint32_t* keys, uint32_t* sorted,
+                                   void* temp, size_t temp_bytes, uint32_t* row_cnt, const uint32_t* row_off,
+                                   mm_similarity* out, unsigned long long* total, cudaStream_t st);
 cudaError_t launch_scan(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* totals, uint32_t* grand,
                         cudaStream_t st);
 // similarity criterion (k_sweep.cu)

@@ -268,6 +268,8 @@ class Engine:
 
     # ---- thresholds ---------------------------------------------------
     def compute_thresholds(self, overrides: Optional[ThresholdOverrides] = None) -> Thresholds:
+        """compute_thresholds(full_report(...), overrides): the means of this
+        engine's lcom / cbo and of its similarity table (built when absent)."""
         ov = abi.mm_overrides()
         if overrides is not None:
             for name in ("similarity", "lcom", "cbo"):
@@ -277,6 +279,33 @@ class Engine:
                     setattr(ov, name, float(v))
         t = abi.mm_thresholds()
         self._check(lib().mm_compute_thresholds(self._ctx, C.byref(ov), C.byref(t)), "compute_thresholds")
+        return Thresholds(t.similarity, t.lcom, t.cbo, bool(t.explicit_mode))
+
+    def report_thresholds(self, lcom, cbo, similarity=None,
+                          overrides: Optional[ThresholdOverrides] = None) -> Thresholds:
+        """compute_thresholds(report, overrides) (suggest.hpp:46-61) on a caller's
+        report vectors: every mean on the device, bit-identical to the
+        reference's sequential double sums. `similarity` = the report's
+        similarity values (or a SIMILARITY_DTYPE table)."""
+        l = np.ascontiguousarray(lcom, dtype=np.float64)
+        c = np.ascontiguousarray(cbo, dtype=np.uint32)
+        if similarity is None:
+            sv = np.zeros(0, np.float64)
+        elif getattr(similarity, "dtype", None) is not None and similarity.dtype.names:
+            sv = np.ascontiguousarray(similarity["value"], dtype=np.float64)
+        else:
+            sv = np.ascontiguousarray(similarity, dtype=np.float64)
+        ov = abi.mm_overrides()
+        if overrides is not None:
+            for name in ("similarity", "lcom", "cbo"):
+                v = getattr(overrides, name)
+                if v is not None:
+                    setattr(ov, "has_" + name, 1)
+                    setattr(ov, name, float(v))
+        t = abi.mm_thresholds()
+        self._check(lib().mm_report_thresholds(self._ctx, l.ctypes.data, len(l), c.ctypes.data, len(c),
+                                               sv.ctypes.data, len(sv), C.byref(ov), C.byref(t)),
+                    "compute_thresholds")
         return Thresholds(t.similarity, t.lcom, t.cbo, bool(t.explicit_mode))
 
     def sequential_mean(self, values) -> tuple:

@@ -4,12 +4,15 @@ Bar: bit-exact — lcom doubles compared as raw bits, every integer equal, the
 ordered suggestion list equal record by record (all 64 bytes but padding).
 All calls go through the C ABI (paper_1308_4011_b200.Engine is a ctypes shim).
 """
+import os
+
 import numpy as np
 import pytest
 
 import oracle
 from conftest import first_diff, golden_names, golden_records, golden_system, load_golden, records_equal, unhex
-from paper_1308_4011_b200 import Combine, Criterion, Engine, MMArgError, MMError, MMRangeError, System, Thresholds, abi
+from paper_1308_4011_b200 import (Combine, Criterion, Engine, MMArgError, MMError, MMRangeError, System, ThresholdOverrides,
+                                  Thresholds, abi)
 from paper_1308_4011_b200.engine import criteria_mask
 
 pytestmark = pytest.mark.gpu
@@ -532,14 +535,14 @@ def test_gpu_similarities(gpu_engine):
 
 
 def test_gpu_similarity_limits_and_full_report(gpu_engine):
-    # a method whose candidate list passes 4096 entries: MM_E_UNSUPPORTED, not
-    # a wrong table; the full report's fields agree with their own calls
+    # rows whose candidate lists pass 4096 entries take the huge-row path (a
+    # table equal to the oracle's, no error); the full report's fields agree
+    # with their own calls
     n = 5000
     s = System.build([(list(range(2)), list(range(n)))], [], [[0, 1]] * n)
     gpu_engine.upload(s)
-    with pytest.raises(MMError) as ei:
-        gpu_engine.similarities()
-    assert ei.value.status == abi.MM_E_UNSUPPORTED
+    g = gpu_engine.similarities()
+    assert len(g) == n * (n - 1) // 2 and g.tobytes() == oracle.similarities(s).tobytes()
     s = System.generate(seed=61, n_classes=50, n_methods=800, n_attributes=600, k_max_calls=5, k_max_accesses=5)
     gpu_engine.upload(s)
     r = gpu_engine.full_report()
@@ -577,3 +580,116 @@ def test_gpu_similarity_criterion_vs_reference(gpu_engine):
                                            thr.lcom, thr.cbo)
                         assert records_equal(g, o), (crit, comb, allc, thr, first_diff(g, o))
         del sim_mean
+
+
+def hub_system(rng, n_classes=220, per=5, hubs=((0, 150, 120), (7, 40, 31), (13, 31, 0), (21, 33, 2))):
+    """Classes of `per` methods / attributes; hub methods (method id, classes
+    called into, classes accessed) use 31..270 classes; the rest draw a few
+    dependencies. Ids are class-major (method p of class p // per)."""
+    n_m = n_a = n_classes * per
+    classes = [(list(range(c * per, (c + 1) * per)), list(range(c * per, (c + 1) * per))) for c in range(n_classes)]
+    calls = [[] for _ in range(n_m)]
+    accs = [[] for _ in range(n_m)]
+    for p in range(n_m):
+        for _ in range(int(rng.integers(0, 4))):
+            t = int(rng.integers(0, n_m))
+            if t != p:
+                calls[p].append(t)
+        for _ in range(int(rng.integers(0, 3))):
+            accs[p].append(int(rng.integers(0, n_a)) if rng.random() < 0.8 else (p // per) * per + int(rng.integers(0, per)))
+    for p, n_call, n_acc in hubs:
+        own = p // per
+        for q in range(own * per, (own + 1) * per):  # a cohesive home class: moving the hub out lowers its lcom
+            if q != p:
+                accs[q].extend(range(own * per, (own + 1) * per))
+        others = [c for c in range(n_classes) if c != own]
+        for c in rng.choice(others, size=n_call, replace=False):
+            calls[p].append(int(c) * per + int(rng.integers(0, per)))
+        for c in rng.choice(others, size=n_acc, replace=False):  # two attributes in each: lcom(dest) can drop
+            accs[p].extend([int(c) * per, int(c) * per + 1])
+        accs[p].append(own * per)  # and one own attribute
+    return System.build(classes, calls, accs)
+
+
+def test_gpu_hub_methods_all_candidates_and_topk(gpu_engine):
+    # top-k / all-candidates modes for methods using 32..271 classes (the
+    # reference's emit_for_method has no bound on |used(u)|, suggest.hpp:165-187)
+    for seed in range(3):
+        s = hub_system(np.random.default_rng(77 + seed))
+        used = s.used_classes()
+        assert used.max() >= 150 and (used >= 32).sum() >= 4
+        check_against_oracle(gpu_engine, s, f"hub {seed}",
+                             modes=((COH | COUP, 0, True), (COH | COUP, 1, True), (COH, 0, True), (COUP, 0, True),
+                                    (COH | COUP, 0, False), (COH | COUP, 1, False)), top_ks=(1, 3, 8))
+        for thr in (Thresholds(0, -1.0, -1.0), Thresholds(0, 0.0, 0.0)):
+            lcom, ck, cbo = oracle.class_metrics(s)
+            for mask, comb, allc, k in ((COH | COUP, 0, True, 1), (COH | COUP, 1, True, 1), (COH | COUP, 0, False, 5)):
+                g = gpu_engine.suggest_all(thr, CRIT[mask], Combine(comb), allc, top_k=k)
+                o = oracle.suggest(s, lcom, cbo, mask, comb, allc, k, thr.lcom, thr.cbo)
+                assert records_equal(g, o), (seed, thr, mask, comb, allc, k, first_diff(g, o))
+        if oracle.ref_available():  # and the reference itself, all-candidates
+            R = oracle.RefModel(s)
+            lcom, ck, cbo = R.class_metrics()
+            gpu_engine.upload(s)
+            for comb in (0, 1):  # every class gated in: the hubs emit up to ~120 records each
+                want, _ = R.sweep(lcom, cbo, COH | COUP, -1.0, -1.0, comb, True, n_workers=4)
+                g = gpu_engine.suggest_all(Thresholds(0, -1.0, -1.0), all_candidates=True, combine=Combine(comb))
+                assert (want["method"] == 0).sum() > 100
+                assert records_equal(g, want), (seed, comb, first_diff(g, want))
+
+
+def test_gpu_similarity_huge_rows_and_mean(gpu_engine):
+    # all_similarities has no row bound (metrics.hpp:67-77): an attribute with
+    # 10,200 users (every user's candidate list is > 4096 entries) and a
+    # method with 1,500 properties take the huge-row path (global scratch +
+    # segmented sort); against the oracle and the compiled reference. The
+    # similarity mean of compute_thresholds (suggest.hpp:55-56) on the device
+    # table bit-equals the reference's sequential mean.
+    rng = np.random.default_rng(5)
+    n_cls, per = 60, 200
+    n_m = n_a = n_cls * per
+    classes = [(list(range(c * per, (c + 1) * per)), list(range(c * per, (c + 1) * per))) for c in range(n_cls)]
+    calls = [[int(t) for t in rng.integers(0, n_m, size=int(rng.integers(0, 3))) if t != p] for p in range(n_m)]
+    accs = [[int(a) for a in rng.integers(0, n_a, size=int(rng.integers(0, 3)))] for p in range(n_m)]
+    for p in range(10200):
+        accs[p].append(7)  # attribute 7: 10,200 users
+    calls[11000] = [t for t in range(1500) if t != 11000]  # 1,499 call properties
+    s = System.build(classes, calls, accs)
+    gpu_engine.upload(s)
+    g = gpu_engine.similarities()
+    assert len(g) > 10200 * 10199 // 2
+    o = oracle.similarities(s)
+    assert g.tobytes() == o.tobytes(), (len(g), len(o))
+    del o
+    lcom, ck, cbo = gpu_engine.class_metrics_all()
+    t = gpu_engine.compute_thresholds()
+    want = oracle.thresholds(lcom, cbo, g["value"])
+    assert (t.similarity, t.lcom, t.cbo) == (want.similarity, want.lcom, want.cbo)
+    if oracle.ref_available():
+        r = oracle.RefModel(s).similarities(os.cpu_count() or 1)
+        assert g.tobytes() == r.tobytes()
+        del r
+        wr = oracle.ref_thresholds(lcom, cbo, g["value"])
+        assert (t.similarity, t.lcom, t.cbo) == (wr.similarity, wr.lcom, wr.cbo)
+        # compute_thresholds on a caller's report, every override combination
+        for ov in (None, ThresholdOverrides(lcom=0.25), ThresholdOverrides(0.1, None, 3.0)):
+            a = gpu_engine.report_thresholds(lcom, cbo, g, ov)
+            b = oracle.ref_thresholds(lcom, cbo, g["value"], None if ov is None else
+                                      {k: getattr(ov, k) for k in ("similarity", "lcom", "cbo")})
+            assert (a.similarity, a.lcom, a.cbo, a.explicit_mode) == (b.similarity, b.lcom, b.cbo,
+                                                                      bool(b.explicit_mode)), ov
+
+
+def test_gpu_report_thresholds_random(gpu_engine):
+    # the device means of arbitrary report vectors (the drop-in's
+    # gpu::compute_thresholds) against the reference's compute_thresholds
+    rng = np.random.default_rng(11)
+    for n in (0, 1, 5, 2047, 2048, 2049, 100000, 333333):
+        lcom = rng.integers(0, 2 ** 53 + 1, n).astype(np.float64) * 2.0 ** -53
+        cbo = rng.integers(0, 200, n).astype(np.uint32)
+        sim = rng.random(n // 3 + 1)
+        a = gpu_engine.report_thresholds(lcom, cbo, sim)
+        b = oracle.thresholds(lcom, cbo, sim)
+        assert (a.similarity, a.lcom, a.cbo) == (b.similarity, b.lcom, b.cbo), n
+    a = gpu_engine.report_thresholds(rng.random(10), rng.integers(0, 9, 7).astype(np.uint32), None)
+    assert a.similarity == 0.0
