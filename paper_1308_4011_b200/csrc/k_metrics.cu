@@ -51,7 +51,7 @@ __global__ void k_validate_offsets(const uint32_t* __restrict__ off, uint64_t n_
 // class with atomics. Every index is bounds-checked: this runs before the
 // validation result is known.
 __global__ void k_plan_methods(DevModel s, const uint32_t* __restrict__ pos_owner, uint32_t* __restrict__ foreign,
-                               uint32_t* __restrict__ cmaxdeg) {
+                               uint32_t* __restrict__ cmaxdeg, uint32_t* __restrict__ n_hideg) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= s.M) return;
     const uint32_t c = pos_owner[i];
@@ -71,6 +71,9 @@ __global__ void k_plan_methods(DevModel s, const uint32_t* __restrict__ pos_owne
     }
     if (fr) atomicAdd(foreign + c, fr);
     atomicMax(cmaxdeg + c, (ce - cb) + (ae - ab));
+    // a used list longer than a method record holds needs more than kRecMaxEnt edges
+    const uint32_t hi = __ballot_sync(__activemask(), (ce - cb) + (ae - ab) > (uint32_t)kRecMaxEnt);
+    if (hi && (threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(n_hideg, __popc(hi));
 }
 
 // fan_out[p] = |calls(p)| (metrics.hpp:87-93); fan_in[t] += 1 per call-list
@@ -998,11 +1001,11 @@ void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, u
 }
 void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint32_t* large_list,
                          uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,
-                         uint32_t* cmaxdeg, cudaStream_t st) {
+                         uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st) {
     if (!s.C) return;
     cudaMemsetAsync(foreign, 0, 4ull * s.C, st);
     cudaMemsetAsync(cmaxdeg, 0, 4ull * s.C, st);
-    if (s.M) k_plan_methods<<<(s.M + 255) / 256, 256, 0, st>>>(s, pos_owner, foreign, cmaxdeg);
+    if (s.M) k_plan_methods<<<(s.M + 255) / 256, 256, 0, st>>>(s, pos_owner, foreign, cmaxdeg, n_hideg);
     k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, cmaxdeg, foreign, cplan, large_list, n_large, big_list,
                                                        n_big, max_deg);
 }

@@ -206,6 +206,26 @@ __device__ __forceinline__ uint32_t removed_count(const ClassRec& ro, const uint
     return removed;
 }
 
+// #{X ∈ list \ {o} : U[o][X] == 1} for a packed used list (records whose
+// removed count the class pass did not fill in)
+__device__ __forceinline__ uint32_t removed_from_list(const ClassRec& ro, const uint32_t* __restrict__ ux,
+                                                      const uint32_t* __restrict__ un,
+                                                      const uint32_t* __restrict__ dense, uint32_t C,
+                                                      const uint32_t* ent, uint32_t n, uint32_t o) {
+    uint32_t removed = 0;
+    for (uint32_t k = 0; k < n; ++k) {
+        const uint32_t X = ent[k] >> 8;
+        if (X == o) continue;
+        if (ro.dense != kNone) {
+            removed += (__ldg(dense + ro.dense + (C + 31) / 32 + (X >> 5)) >> (X & 31)) & 1u;
+        } else {
+            const int p = urow_find(ux, ro.ubase, ro.cbo, X);
+            if (p >= 0 && __ldg(un + ro.ubase + p) == 1u) ++removed;
+        }
+    }
+    return removed;
+}
+
 // Both predicates and keys of one candidate (the shared core of the modes).
 template <class E>
 __device__ __forceinline__ void score(const SweepArgs& a, const E& en, const Origin& org, uint32_t d, uint32_t hd,
@@ -485,12 +505,21 @@ __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, ui
 // state and high occupancy measured faster on C4 than a warp-flattened
 // variant (one candidate per lane), the round-1 profiles show why — every
 // kernel here is latency-bound, so resident warps matter most.
-template <int K>
+template <int K, bool LIST = false>
 __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(SweepArgs a) {
     __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
-    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
+    uint64_t pos;
+    bool live;
+    if (LIST) {  // the methods k_screen handed over (record overflow)
+        const uint32_t i = blockIdx.x * kSweepTile + threadIdx.x;
+        live = i < *a.n_fallback;
+        pos = live ? a.fallback[i] : 0;
+    } else {
+        pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
+        live = pos < a.pos_end;
+    }
     uint32_t cands = 0;
-    if (pos < a.pos_end) {
+    if (live) {
         const uint32_t p = __ldg(a.s.cls_methods + pos);
         const uint32_t o = __ldg(a.pos_owner + pos);
         SmemEnum ren{s_X + threadIdx.x, s_H + threadIdx.x, 0};
@@ -516,13 +545,166 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
     if ((threadIdx.x & 31) == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
 }
 
+// Pass 1, best-only mode (the reference's default and the bench step): a
+// flattened candidate screen. Each warp takes 32 consecutive class-order
+// positions (one method per lane) and then spreads the warp's candidates
+// (u, d) over its lanes, one candidate per lane and iteration, so lanes never
+// idle on a neighbour's longer list. Per method (its own lane): the packed
+// used list from the method pass's record, the origin's counts, and — only
+// when the exact-rational pre-test h·M < H allows lcom(origin) to drop — the
+// two origin doubles. Per candidate lane: d's counts and lcom, the integer
+// pre-test h_u(d)·M_d > H_d (then the one fp64 division of lcom_dest_after),
+// and, if the method can lower the origin's cbo, the membership of every
+// other used class in U[d] (exact bitmap, or Bloom then the row). Per-method
+// argmin over (key, d) in ascending-d order with strict < (lowest d wins
+// ties, suggest.hpp:180-184) reads the candidates' results back from shared
+// memory. Methods whose used list did not fit their record go to the
+// per-thread kernel (k_score_thread<K, true>) through a short list.
+constexpr int kScreenWarps = kSweepTile / 32;
+constexpr int kScreenSlots = 32 * kRecMaxEnt;  // candidates of one warp: ≤ 7 per method
+
+struct ScreenSmem {
+    uint32_t ent[kScreenWarps][32][kRecMaxEnt];   // the methods' used lists (X << 8 | h), own class included
+    uint8_t cm[kScreenWarps][kScreenSlots];       // candidate slot -> method lane
+    uint8_t ck[kScreenWarps][kScreenSlots];       // candidate slot -> list index
+    double kc[kScreenWarps][kScreenSlots];        // cohesion key (passing) or -1
+    uint32_t kp[kScreenWarps][kScreenSlots];      // coupling key cbo_d (passing) or kNone
+};
+
+__global__ void __launch_bounds__(kSweepTile) k_screen(SweepArgs a) {
+    __shared__ ScreenSmem sm;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
+    const bool live = pos < a.pos_end;
+    uint32_t (*ent)[kRecMaxEnt] = sm.ent[warp];
+    uint8_t* cm = sm.cm[warp];
+    uint8_t* ck = sm.ck[warp];
+    double* kc = sm.kc[warp];
+    uint32_t* kp = sm.kp[warp];
+
+    // ---- per method (this lane)
+    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
+    uint32_t o = 0;
+    if (live) {
+        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
+        r0 = rp[0];
+        r1 = rp[1];
+        o = __ldg(a.pos_owner + pos);
+    }
+    const bool ovf = live && (r0.x & kRecOverflow);
+    const uint32_t n = (live && !ovf) ? rec_n(r0.x) : 0u;
+    {
+        const uint32_t e7[kRecMaxEnt] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k) ent[lane][k] = e7[k];
+    }
+    uint32_t nc = 0;  // candidates: list entries other than the own class
+#pragma unroll
+    for (int k = 0; k < kRecMaxEnt; ++k) nc += (k < (int)n && (ent[lane][k] >> 8) != o);
+    // origin
+    bool coh_ok = false, can_coup = false;
+    double lo_a = 0.0;
+    if (n) {
+        const ClassRec ro = load_rec(a.rec, o);
+        const uint32_t h = rec_hown(r0.x);
+        const uint32_t removed = (r0.x & kRecRemovedValid) ? rec_removed(r0.x)
+                                                            : removed_from_list(ro, a.ux, a.un, a.dense, a.s.C,
+                                                                                ent[lane], n, o);
+        can_coup = removed > 0;  // cbo_origin_after < cbo_origin_before
+        // lcom(A, M-1, H-h) < lcom(A, M, H): impossible when A == 0 (both 0.0)
+        // or, with exact denominators and M ≥ 2, when (H-h)·M ≤ H·(M-1)
+        bool maybe = ro.A != 0 && ro.M != 0;
+        if (maybe && ro.M >= 2 && (uint64_t)ro.A * ro.M < kExact53) maybe = (uint64_t)h * ro.M < ro.H;
+        if (maybe) {
+            lo_a = lcom_of(ro.A, (uint64_t)ro.M - 1, (uint64_t)ro.H - h);
+            coh_ok = lo_a < __ldg(a.dlcom + o);
+        }
+    }
+    // candidate slots: this method's at [excl, excl + nc), list order (d ascending)
+    uint32_t incl = nc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+    }
+    const uint32_t excl = incl - nc;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    {
+        uint32_t w = excl;
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k)
+            if (k < (int)n && (ent[lane][k] >> 8) != o) {
+                cm[w] = (uint8_t)lane;
+                ck[w] = (uint8_t)k;
+                ++w;
+            }
+    }
+    const uint32_t flags = (coh_ok ? 1u : 0u) | (can_coup ? 2u : 0u);
+    __syncwarp();
+
+    // ---- per candidate (one per lane and round)
+    for (uint32_t c0 = 0; c0 < total; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        const bool act = c < total;
+        const uint32_t m = act ? cm[c] : 0u;
+        const uint32_t mflags = __shfl_sync(0xffffffffu, flags, m);
+        const double m_lo_a = __shfl_sync(0xffffffffu, lo_a, m);
+        const uint32_t m_n = __shfl_sync(0xffffffffu, n, m);
+        if (!act) continue;
+        const uint32_t e = ent[m][ck[c]];
+        const uint32_t d = e >> 8, hd = e & 0xffu;
+        double key = -1.0;
+        uint32_t kpv = kNone;
+        if (mflags) {
+            const ClassRec rd = load_rec(a.rec, d);
+            if ((mflags & 1u) && rd.A != 0 && rd.M != 0) {
+                const bool exact = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
+                if (!exact || (uint64_t)hd * rd.M > rd.H) {
+                    const double ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
+                    if (ld_a < __ldg(a.dlcom + d)) key = __dadd_rn(m_lo_a, ld_a);  // lcom_key, suggest.hpp:194-196
+                }
+            }
+            if (mflags & 2u) {
+                bool ok = true;
+                for (uint32_t j = 0; j < m_n && ok; ++j) {
+                    const uint32_t X = ent[m][j] >> 8;
+                    if (X != d && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ok = false;
+                }
+                if (ok) kpv = rd.cbo;  // cbo_dest_after == cbo_dest_before when it passes
+            }
+        }
+        kc[c] = key;
+        kp[c] = kpv;
+    }
+    __syncwarp();
+
+    // ---- per method: argmin over its slots (d ascending, strict <)
+    uint32_t bd_coh = kNone, bd_coup = kNone;
+    double bk = 0.0;
+    uint32_t bp = 0;
+    for (uint32_t j = 0; j < nc; ++j) {
+        const uint32_t slot = excl + j;
+        const double kcv = kc[slot];
+        const uint32_t kpv = kp[slot];
+        if (kcv >= 0.0 || kpv != kNone) {
+            const uint32_t d = ent[lane][ck[slot]] >> 8;
+            if (kcv >= 0.0 && (bd_coh == kNone || kcv < bk)) { bd_coh = d; bk = kcv; }
+            if (kpv != kNone && (bd_coup == kNone || kpv < bp)) { bd_coup = d; bp = kpv; }
+        }
+    }
+    if (live && !ovf) a.res[pos] = make_uint4(bd_coh, bd_coup, nc, 0);
+    if (ovf) a.fallback[atomicAdd(a.n_fallback, 1u)] = (uint32_t)pos;
+    const uint32_t wc = __reduce_add_sync(0xffffffffu, nc);
+    if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
+}
+
 // Pass 2: apply the class gates (suggest.hpp:246, :273) and the criteria
 // merge (union / intersection, :315-341) to each method's pass-1 result,
-// then a tile scan + decoupled look-back gives every method the global offset
-// of its first record and every EMITTING method a slot in a compact emitter
-// list (both counts travel packed in one 64-bit look-back word). 1024
-// methods per tile (4 per thread) keep the look-back chain short; the result
-// (gated selection, count, offset) replaces res[pos] in place.
+// then a tile scan + decoupled look-back gives every EMITTING method a slot in
+// a compact emitter list — (position, gated selection, offset of its first
+// record) — both counts travel packed in one 64-bit look-back word. 1024
+// methods per tile (4 per thread) keep the look-back chain short; res is only
+// read.
 constexpr int kOffItems = 4;
 constexpr uint32_t kOffTile = kSweepTile * kOffItems;
 
@@ -646,11 +828,10 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
     for (int it = 0; it < kOffItems; ++it) {
         const uint64_t pos = pos0 + it;
         if (pos >= a.pos_end) continue;
-        uint4 v = r[it];
-        v.z = cnt[it];
-        v.w = (uint32_t)(at & 0xffffffffull);
-        a.res[pos] = v;
-        if (cnt[it]) a.emit_list[at >> 32] = (uint32_t)pos;
+        if (cnt[it]) {  // compact emitter record: (position, gated selection, first record)
+            const uint4 v = r[it];
+            a.emitters[at >> 32] = make_uint4((uint32_t)pos, v.x, v.y, (uint32_t)(at & 0xffffffffull));
+        }
         at += cnt[it] + (cnt[it] ? (1ull << 32) : 0ull);
     }
 }
@@ -662,8 +843,9 @@ __global__ void __launch_bounds__(kSweepTile) k_write(SweepArgs a) {
     __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
     const uint32_t n = *a.n_emit;
     for (uint32_t i = blockIdx.x * kSweepTile + threadIdx.x; i < n; i += gridDim.x * kSweepTile) {
-        const uint32_t pos = a.emit_list[i];
-        const uint4 r = a.res[pos];
+        const uint4 em = a.emitters[i];
+        const uint32_t pos = em.x;
+        const uint4 r = make_uint4(em.y, em.z, 0u, em.w);
         const uint32_t o = __ldg(a.pos_owner + pos);
         const uint32_t p = __ldg(a.s.cls_methods + pos);
         MethodResult res{};
@@ -820,8 +1002,16 @@ __global__ void __launch_bounds__(kSweepTile) k_sim_emit(SweepArgs a, SimCrit sc
 
 }  // namespace
 
-void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
+void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st) {
     if (!n_tiles) return;
+    if (a.mode == 0 && !a.no_screen) {
+        k_screen<<<n_tiles, kSweepTile, 0, st>>>(a);
+        if (fallback_tiles) {  // methods whose used list overflowed its record
+            if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
+            else k_score_thread<16, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
+        }
+        return;
+    }
     if (a.maxdeg_fast <= 8) k_score_thread<8><<<n_tiles, kSweepTile, 0, st>>>(a);
     else k_score_thread<16><<<n_tiles, kSweepTile, 0, st>>>(a);
 }

@@ -439,6 +439,278 @@ k_thresholds_coop(const double* __restrict__ lcom, const uint32_t* __restrict__ 
     }
 }
 
+// ---- one-CTA variant (n ≤ kBlockMax): the same exact emulation without grid
+// syncs, so it runs on a single SM next to the candidate scoring instead of
+// holding every SM through three grid-wide barriers. 1024 threads, each owning
+// a contiguous chunk of ⌈n/1024⌉ values: (1) exact chunk sums (u128 in 2^-53
+// units) and a block scan give each chunk's exact prefix; (2) a chunk whose
+// prefix stays in one binade (all but ≤ ~34 chunks) composes its elements'
+// one-bit-state functions in one straight pass, the few chunks where a binade
+// starts walk element by element and record the segment starts; a segmented
+// block scan of the functions and one thread chaining the segments give every
+// chunk's start state; (3) every chunk is replayed with IEEE double adds from
+// its start state and must end exactly on the next chunk's start (induction
+// from 0): the result is then the sequential sum. Anything else -> serial.
+constexpr int kBT = 1024;
+constexpr uint32_t kBlockMax = kBT * 256;
+
+struct BlockShared {
+    u128 warp_u128[kBT / 32];
+    Fn warp_fn[kBT / 32];
+    unsigned long long warp_c[kBT / 32];
+    double start[kBT];
+    uint32_t seg_pos[kMaxSegs];
+    int seg_e[kMaxSegs];
+    uint64_t seg_x[kMaxSegs];
+    Fn seg_total[kMaxSegs + 1];
+    u128 seg_first[kMaxSegs];
+    u128 seg_end[kMaxSegs + 1];
+    int n_segs;
+    int bad;
+};
+
+__device__ __forceinline__ u128 blk1k_excl_u128(u128 v, BlockShared& sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    u128 inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const u128 y = shfl_up_u128(inc, d);
+        if (lane >= d) inc += y;
+    }
+    if (lane == 31) sh.warp_u128[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {  // scan of the 32 warp totals
+        u128 w = sh.warp_u128[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u128 y = shfl_up_u128(w, d);
+            if (lane >= d) w += y;
+        }
+        sh.warp_u128[lane] = w;
+    }
+    __syncthreads();
+    return (warp ? sh.warp_u128[warp - 1] : (u128)0) + inc - v;
+}
+
+__device__ __forceinline__ Fn blk1k_excl_fn(const Fn& agg, BlockShared& sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Fn x = agg;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const Fn y = shfl_up_fn(x, d);
+        if (lane >= d) x = seg_combine(y, x);
+    }
+    if (lane == 31) sh.warp_fn[warp] = x;
+    const Fn xin = shfl_up_fn(x, 1);
+    __syncthreads();
+    if (warp == 0) {
+        Fn w = sh.warp_fn[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const Fn y = shfl_up_fn(w, d);
+            if (lane >= d) w = seg_combine(y, w);
+        }
+        sh.warp_fn[lane] = w;
+    }
+    __syncthreads();
+    const Fn wp = warp ? sh.warp_fn[warp - 1] : fn_id();
+    return lane == 0 ? wp : seg_combine(wp, xin);
+}
+
+__device__ __forceinline__ double u128_to_double(u128 T) {  // T·2^-53, exact for ≤ 53 significant bits
+    const int bl = bitlen128(T);
+    const int sft = bl > 64 ? bl - 64 : 0;
+    return ldexp((double)(uint64_t)(T >> sft), sft - 53);
+}
+
+__global__ void __launch_bounds__(kBT, 1)
+k_thresholds_block(const double* __restrict__ lcom, const uint32_t* __restrict__ cbo, uint32_t n,
+                   DevThresholds* __restrict__ out) {
+    __shared__ BlockShared sh;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint32_t E = (n + kBT - 1) / kBT;
+    const uint32_t my = (uint32_t)t * E;
+    const uint32_t cnt = my < n ? min(E, n - my) : 0u;
+    if (t == 0) { sh.n_segs = 0; sh.bad = 0; }
+    // (1) preconditions, exact chunk sum, cbo sum
+    u128 S = 0;
+    unsigned long long cs = 0;
+    int bad = 0;
+    for (uint32_t j = 0; j < cnt; ++j) {
+        uint64_t X;
+        bad |= !lcom_units(__ldg(lcom + my + j), X);
+        S += X;
+        if (cbo) cs += __ldg(cbo + my + j);
+    }
+    {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) cs += __shfl_down_sync(0xffffffffu, cs, d);
+        if (lane == 0) sh.warp_c[warp] = cs;
+    }
+    if (__syncthreads_or(bad)) {  // outside the fast path's precondition: serial
+        if (warp == 0) {
+            double sl = 0.0;
+            for (uint32_t b = 0; b < n; b += 32) {
+                const uint32_t i = b + lane;
+                const double v = i < n ? lcom[i] : 0.0;
+                const uint32_t m = min(32u, n - b);
+                for (uint32_t k = 0; k < m; ++k) sl = __dadd_rn(sl, __shfl_sync(0xffffffffu, v, k));
+            }
+            if (lane == 0) sh.seg_first[0] = (u128)0, sh.start[0] = sl;
+        }
+        __syncthreads();
+        if (t == 0) {
+            unsigned long long csum = 0;
+            for (int w = 0; w < kBT / 32; ++w) csum += sh.warp_c[w];
+            out->lcom = n ? __ddiv_rn(sh.start[0], (double)n) : 0.0;
+            double mc;
+            if (csum < (1ull << 53)) {
+                mc = n ? __ddiv_rn((double)csum, (double)n) : 0.0;
+            } else {
+                double sc = 0.0;
+                for (uint32_t i = 0; i < n; ++i) sc = __dadd_rn(sc, cbo ? (double)cbo[i] : 0.0);
+                mc = n ? __ddiv_rn(sc, (double)n) : 0.0;
+            }
+            out->cbo = mc;
+            out->fast_path_ok = 0;
+        }
+        return;
+    }
+    const u128 P_my = blk1k_excl_u128(S, sh);
+    // (2) binade segments and per-chunk functions
+    const int e_prev = my == 0 ? -1 : gran_exp(P_my);
+    const bool has_start = cnt > 0 && gran_exp(P_my + S) != e_prev;
+    Fn agg = fn_id();
+    if (cnt > 0 && !has_start) {
+        for (uint32_t j = 0; j < cnt; ++j) {
+            uint64_t X;
+            lcom_units(__ldg(lcom + my + j), X);
+            agg = compose(agg, fn_elem(X, e_prev));
+        }
+    } else if (has_start) {
+        u128 P = P_my;
+        int ep = e_prev;
+        for (uint32_t j = 0; j < cnt; ++j) {
+            uint64_t X;
+            lcom_units(__ldg(lcom + my + j), X);
+            P += X;
+            const int e = gran_exp(P);
+            if (e != ep) {
+                const int k = atomicAdd(&sh.n_segs, 1);
+                if (k < kMaxSegs) { sh.seg_pos[k] = my + j; sh.seg_e[k] = e; sh.seg_x[k] = X; }
+                agg = fn_id();
+                agg.bits |= 4u;
+            } else {
+                const uint32_t fl = agg.bits & 4u;
+                agg = compose(agg, fn_elem(X, e));
+                agg.bits |= fl;
+            }
+            ep = e;
+        }
+    }
+    const Fn excl = blk1k_excl_fn(agg, sh);
+    if (t == 0) {
+        if (sh.n_segs > kMaxSegs) sh.bad = 1;
+        const int ns = min(sh.n_segs, kMaxSegs);
+        for (int a = 1; a < ns; ++a)
+            for (int b = a; b > 0 && sh.seg_pos[b - 1] > sh.seg_pos[b]; --b) {
+                const uint32_t tp = sh.seg_pos[b]; sh.seg_pos[b] = sh.seg_pos[b - 1]; sh.seg_pos[b - 1] = tp;
+                const int te = sh.seg_e[b]; sh.seg_e[b] = sh.seg_e[b - 1]; sh.seg_e[b - 1] = te;
+                const uint64_t tx = sh.seg_x[b]; sh.seg_x[b] = sh.seg_x[b - 1]; sh.seg_x[b - 1] = tx;
+            }
+    }
+    __syncthreads();
+    const int ns = min(sh.n_segs, kMaxSegs);
+    int kb = -1;  // the segment active just before this chunk
+    for (int k = 0; k < ns; ++k)
+        if (sh.seg_pos[k] < my) kb = k;
+    // segment totals: closed by the chunk holding the next segment's start, or the last chunk
+    if (has_start) {
+        Fn run = excl;
+        int k = kb;
+        u128 P = P_my;
+        int ep = e_prev;
+        for (uint32_t j = 0; j < cnt; ++j) {
+            uint64_t X;
+            lcom_units(__ldg(lcom + my + j), X);
+            P += X;
+            const int e = gran_exp(P);
+            if (e != ep) {
+                if (k + 1 <= kMaxSegs) sh.seg_total[k + 1] = run;
+                ++k;
+                run = fn_id();
+            } else {
+                run = compose(run, fn_elem(X, e));
+            }
+            ep = e;
+        }
+        if (my + cnt == n && k + 1 <= kMaxSegs) sh.seg_total[k + 1] = run;
+    } else if (cnt > 0 && my + cnt == n && kb + 1 <= kMaxSegs) {
+        sh.seg_total[kb + 1] = compose(excl, agg);
+    }
+    __syncthreads();
+    if (t == 0) {  // chain the segments from S_0 = 0
+        u128 T = 0;
+        sh.seg_end[0] = T;
+        for (int k = 0; k < ns; ++k) {
+            const int e = sh.seg_e[k];
+            T = rne53(T + sh.seg_x[k]);
+            sh.seg_first[k] = T;
+            T += (u128)finc(sh.seg_total[k + 1], (int)((T >> e) & 1)) << e;
+            sh.seg_end[k + 1] = T;
+        }
+    }
+    __syncthreads();
+    // start state of this chunk
+    u128 S0 = 0;
+    if (cnt > 0) {
+        if (has_start && sh.seg_pos[kb + 1] == my) {
+            S0 = sh.seg_end[kb + 1];
+        } else if (kb >= 0) {
+            const int e = sh.seg_e[kb];
+            const u128 F = sh.seg_first[kb];
+            S0 = F + ((u128)finc(excl, (int)((F >> e) & 1)) << e);
+        }
+    }
+    const double s0 = u128_to_double(S0);
+    sh.start[t] = s0;
+    __syncthreads();
+    // (3) exact replay in IEEE doubles; every join must hold
+    double sv = s0;
+    for (uint32_t j = 0; j < cnt; ++j) sv = __dadd_rn(sv, __ldg(lcom + my + j));
+    int jb = 0;
+    if (cnt > 0 && my + cnt < n && sh.start[t + 1] != sv) jb = 1;
+    if (my == 0 && cnt > 0 && s0 != 0.0) jb = 1;
+    if (cnt > 0 && my + cnt == n) sh.start[0] = sv;  // the last chunk's end: the sequential sum (t ≥ 1 or n small)
+    const int any_bad = __syncthreads_or(jb | sh.bad);
+    if (t == 0) {
+        unsigned long long csum = 0;
+        for (int w = 0; w < kBT / 32; ++w) csum += sh.warp_c[w];
+        double ml;
+        uint32_t fast = 1;
+        if (any_bad) {
+            fast = 0;
+            double sl = 0.0;
+            for (uint32_t i = 0; i < n; ++i) sl = __dadd_rn(sl, lcom[i]);
+            ml = n ? __ddiv_rn(sl, (double)n) : 0.0;
+        } else {
+            ml = n ? __ddiv_rn(sh.start[0], (double)n) : 0.0;
+        }
+        double mc;
+        if (csum < (1ull << 53)) {
+            mc = n ? __ddiv_rn((double)csum, (double)n) : 0.0;
+        } else {
+            fast = 0;
+            double sc = 0.0;
+            for (uint32_t i = 0; i < n; ++i) sc = __dadd_rn(sc, cbo ? (double)cbo[i] : 0.0);
+            mc = n ? __ddiv_rn(sc, (double)n) : 0.0;
+        }
+        out->lcom = ml;
+        out->cbo = mc;
+        out->fast_path_ok = fast;
+    }
+}
+
 // Serial fallback kernel (n too large for one co-resident tile per CTA).
 // The sequential sums literally, by one warp: each 32-element chunk is loaded
 // coalesced, then every lane runs the same left-to-right chain over the
@@ -494,8 +766,15 @@ cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t 
         max_coresident = sms * per_sm;
         if (dev < kMaxDevices) coresident[dev].store(max_coresident, std::memory_order_relaxed);
     }
-    if (n == 0 || (allow_serial && n <= kSerialMax) || tiles > (uint32_t)max_coresident ||
-        scratch_bytes < thresholds_scratch_bytes(n)) {
+    if (n == 0 || (allow_serial && n <= kSerialMax)) {
+        k_thresholds_serial<<<1, 32, 0, st>>>(lcom, cbo, n, out);
+        return cudaGetLastError();
+    }
+    if (n <= kBlockMax) {  // one CTA, no grid syncs
+        k_thresholds_block<<<1, kBT, 0, st>>>(lcom, cbo, n, out);
+        return cudaGetLastError();
+    }
+    if (tiles > (uint32_t)max_coresident || scratch_bytes < thresholds_scratch_bytes(n)) {
         k_thresholds_serial<<<1, 32, 0, st>>>(lcom, cbo, n, out);
         return cudaGetLastError();
     }

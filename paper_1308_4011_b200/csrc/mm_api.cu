@@ -44,6 +44,8 @@ struct Ctl {  // small device-resident control block
     uint32_t err;
     uint32_t n_emit;
     uint32_t n_wide;    // top-k / all-candidates methods with >= 32 used classes (side table)
+    uint32_t n_fallback;  // best-only screen: methods handed to the per-thread kernel
+    uint32_t n_hideg;     // upload plan: methods with more than kRecMaxEnt edges
     unsigned long long stats[4];
     DevThresholds thr;
     DevThresholds thr_aux;  // mm_sequential_mean / the similarity mean (never the metric pass's means)
@@ -112,6 +114,7 @@ struct mm_ctx {
         acc_off, acc_tgt;
     // plan
     uint32_t n_large = 0, max_deg = 0;
+    uint32_t n_maybe_ovf = 0;  // upper bound of record-overflow methods (upload plan)
     struct LargeGroup {
         uint32_t first, count, smem;
         int key;           // 2 * shared-memory tier + (1024-thread CTAs)
@@ -159,8 +162,10 @@ struct mm_ctx {
     bool sim_valid = false;
     DBuf<uint32_t> pos_owner;
     DBuf<uint4> res;
-    DBuf<uint32_t> emit_list;
+    DBuf<uint4> emit_list;  // compact emitter records (k_offsets -> k_write)
     DBuf<uint4> wide_cnt;  // top-k / all-candidates: pass counts of methods with >= 32 used classes
+    DBuf<uint32_t> fallback;  // best-only screen: record-overflow positions
+    bool no_screen = false;   // env MMGPU_NO_SCREEN=1: best-only mode on the per-thread kernel (A/B)
     DBuf<double> gate_lcom;
     DBuf<uint32_t> gate_cbo;
     bool gates_set = false;
@@ -380,6 +385,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     if (const char* v = std::getenv("MMGPU_HIST_MAX_BYTES")) ctx->hist_max_bytes = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_GIANT_MIN")) ctx->giant_min = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_CK_MMA_MIN")) ctx->ck_mma_min = std::strtoull(v, nullptr, 10);
+    if (const char* v = std::getenv("MMGPU_NO_SCREEN")) ctx->no_screen = v[0] == '1';
     *out = ctx;
     return MM_OK;
 }
@@ -405,6 +411,7 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     ctx->res.release();
     ctx->emit_list.release();
     ctx->wide_cnt.release();
+    ctx->fallback.release();
     ctx->gate_lcom.release();
     ctx->gate_cbo.release();
     if (ctx->own) cudaStreamDestroy(ctx->own);
@@ -571,7 +578,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     const DevModel dm = ctx->dev();
     st = run(ctx, "plan", [&] {
         launch_plan_classes(dm, ctx->pos_owner.p, ctx->cplan.p, ctx->large_list.p, &ctl->n_large, ctx->big_list.p,
-                            &ctl->n_big, &ctl->max_deg, ctx->foreign.p, ctx->cmaxdeg.p, ctx->stream);
+                            &ctl->n_big, &ctl->max_deg, ctx->foreign.p, ctx->cmaxdeg.p, &ctl->n_hideg, ctx->stream);
     });
     if (st) return st;
     Ctl h{};
@@ -581,6 +588,9 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     ctx->n_large = h.n_large;
     ctx->n_big = h.n_big;
     ctx->max_deg = h.max_deg;
+    // methods the best-only screen may hand to the per-thread kernel: more edges
+    // than a record's entries, or (class ids ≥ 2^24) any
+    ctx->n_maybe_ovf = C >= (1u << 24) ? M : h.n_hideg;
     if (ctx->n_large) {
         std::vector<uint32_t> list(ctx->n_large), fr(C);
         MM_CUDA(ctx, cudaMemcpy(list.data(), ctx->large_list.p, 4ull * ctx->n_large, cudaMemcpyDeviceToHost));
@@ -1320,12 +1330,17 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     const void* wide_before = ctx->wide_cnt.p;
     if (mode != 0) MM_CUDA(ctx, ctx->wide_cnt.ensure(npos ? npos : 1));
     if (wide_before != ctx->wide_cnt.p) ++ctx->layout_gen;
+    const uint64_t n_fb = std::min<uint64_t>(npos, ctx->n_maybe_ovf);
+    const void* fb_before = ctx->fallback.p;
+    MM_CUDA(ctx, ctx->fallback.ensure(n_fb ? n_fb : 1));
+    if (fb_before != ctx->fallback.p) ++ctx->layout_gen;
+    const uint32_t fallback_tiles = (uint32_t)((n_fb + kSweepTile - 1) / kSweepTile);
     if (before[0] != ctx->out.p || before[1] != ctx->tile_state.p || before[2] != ctx->res.p ||
         before[3] != ctx->emit_list.p)
         ++ctx->layout_gen;
     Ctl* ctl = ctx->ctl.p;
     if (n_off) MM_CUDA(ctx, cudaMemsetAsync(ctx->tile_state.p, 0, 8ull * n_off, ctx->stream));
-    // tile_counter, err, n_emit, n_wide, stats
+    // tile_counter, err, n_emit, n_wide, n_fallback, n_hideg (rezeroed: unused here), stats
     MM_CUDA(ctx, cudaMemsetAsync(&ctl->tile_counter, 0, offsetof(Ctl, thr) - offsetof(Ctl, tile_counter),
                                  ctx->stream));
     SweepArgs a{};
@@ -1336,7 +1351,7 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     a.lcom = ctx->gates_set ? ctx->gate_lcom.p : ctx->lcom.p;
     a.cbo = ctx->gates_set ? ctx->gate_cbo.p : ctx->cbo.p;
     a.res = ctx->res.p - pb;  // indexed by absolute position
-    a.emit_list = ctx->emit_list.p;
+    a.emitters = ctx->emit_list.p;
     a.n_emit = &ctl->n_emit;
     a.ux = ctx->ux.p;
     a.un = ctx->un.p;
@@ -1359,7 +1374,11 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     a.err = &ctl->err;
     a.wide_cnt = ctx->wide_cnt.p;
     a.n_wide = &ctl->n_wide;
-    mm_status st = run(ctx, "score", [&] { launch_score(a, n_tiles, ctx->stream); });
+    a.dlcom = ctx->lcom.p;
+    a.fallback = ctx->fallback.p;
+    a.n_fallback = &ctl->n_fallback;
+    a.no_screen = ctx->no_screen ? 1u : 0u;
+    mm_status st = run(ctx, "score", [&] { launch_score(a, n_tiles, fallback_tiles, ctx->stream); });
     if (st) return st;
     if (a.thr_device)
         if (mm_status s2 = join_thresholds(ctx)) return s2;

