@@ -6,7 +6,10 @@
 // tests/test_cpp_shim.py. Every comparison uses the reference's own types
 // and their defaulted operator== (bitwise doubles, exact vector order), and
 // exception TYPES must match.
+#include <atomic>
 #include <cstdio>
+#include <mutex>
+#include <thread>
 #include <exception>
 #include <functional>
 #include <stdexcept>
@@ -22,12 +25,14 @@
 
 using namespace modmetrics;
 
-static int g_fail = 0, g_checks = 0;
+static std::atomic<int> g_fail{0}, g_checks{0};
+static std::mutex g_print;
 
 static void expect(bool ok, const std::string& what) {
     ++g_checks;
     if (!ok) {
         ++g_fail;
+        std::lock_guard<std::mutex> lk(g_print);
         std::printf("FAIL %s\n", what.c_str());
     }
 }
@@ -226,7 +231,10 @@ int main() {
         (void)m;
         (void)d;
     }
-    // generated systems: small (every what-if) to acceptance-sized
+    // generated systems: small (every what-if) to acceptance-sized, checked
+    // concurrently (one host thread and one engine per system: the reference
+    // functions are pure and the drop-in's engines are per thread)
+    std::vector<std::thread> pool;
     for (uint64_t seed = 0; seed < 12; ++seed) {
         SplitMix64 draw(seed * 0x9e3779b9ULL + 1);
         GeneratorConfig cfg;
@@ -238,17 +246,23 @@ int main() {
         cfg.k_max_calls = static_cast<uint32_t>(draw.below(6));
         cfg.k_max_accesses = static_cast<uint32_t>(draw.below(6));
         cfg.intra_class_bias = draw.unit();
-        const GeneratedSystem g = generate(cfg);
-        check_system("gen" + std::to_string(seed), g.model, g.deps, small);
+        pool.emplace_back([cfg, seed, small] {
+            const GeneratedSystem g = generate(cfg);
+            check_system("gen" + std::to_string(seed), g.model, g.deps, small);
+        });
     }
-    {  // dense classes (the CTA path) and C2
+    // dense classes (the CTA path) and C2
+    pool.emplace_back([] {
         GeneratorConfig cfg{3, 6, 3000, 384, 4, 32, 0.9};
         const GeneratedSystem g = generate(cfg);
         check_system("dense", g.model, g.deps, false);
+    });
+    pool.emplace_back([] {
         GeneratorConfig c2{1, 1000, 10000, 20000, 4, 4, 0.5};
         const GeneratedSystem g2 = generate(c2);
         check_system("c2", g2.model, g2.deps, false);
-    }
-    std::printf("%s: %d checks, %d failures\n", g_fail ? "FAIL" : "PASS", g_checks, g_fail);
+    });
+    for (std::thread& t : pool) t.join();
+    std::printf("%s: %d checks, %d failures\n", g_fail ? "FAIL" : "PASS", g_checks.load(), g_fail.load());
     return g_fail ? 1 : 0;
 }

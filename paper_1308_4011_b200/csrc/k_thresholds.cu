@@ -34,6 +34,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "mm_device.cuh"
 #include "mm_kernels.h"
@@ -469,7 +470,8 @@ struct BlockShared {
     int bad;
 };
 
-__device__ __forceinline__ u128 blk1k_excl_u128(u128 v, BlockShared& sh) {
+template <class SH>
+__device__ __forceinline__ u128 blk1k_excl_u128(u128 v, SH& sh) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     u128 inc = v;
 #pragma unroll
@@ -492,7 +494,8 @@ __device__ __forceinline__ u128 blk1k_excl_u128(u128 v, BlockShared& sh) {
     return (warp ? sh.warp_u128[warp - 1] : (u128)0) + inc - v;
 }
 
-__device__ __forceinline__ Fn blk1k_excl_fn(const Fn& agg, BlockShared& sh) {
+template <class SH>
+__device__ __forceinline__ Fn blk1k_excl_fn(const Fn& agg, SH& sh) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Fn x = agg;
 #pragma unroll
@@ -711,6 +714,299 @@ k_thresholds_block(const double* __restrict__ lcom, const uint32_t* __restrict__
     }
 }
 
+// ---- cluster variant (n ≤ kClusterMax): the one-CTA algorithm spread over a
+// thread-block cluster of 8 CTAs (8 SMs) whose shared memory holds every value:
+// one coalesced load per value into the owning CTA's shared memory, then the
+// three phases read shared memory only; the block-level scans are combined
+// across the cluster through distributed shared memory, with cluster barriers
+// (hardware) between phases. Segment chaining (≤ kMaxSegs starts, in rank
+// order) is done by one thread of CTA 0, which publishes the chained states.
+constexpr int kCC = 8;                                  // CTAs per cluster (portable)
+constexpr int kCPer = 24;                               // values per thread (max)
+constexpr uint32_t kClusterMax = (uint32_t)kCC * kBT * kCPer;  // 196,608 values
+
+struct ClusterShared {
+    u128 warp_u128[kBT / 32];
+    Fn warp_fn[kBT / 32];
+    unsigned long long warp_c[kBT / 32];
+    double start[kBT];
+    // this CTA's segment starts (local list), each with the function of the
+    // segment it closes (the previous one)
+    uint32_t seg_pos[kMaxSegs];
+    int seg_e[kMaxSegs];
+    uint64_t seg_x[kMaxSegs];
+    Fn seg_close[kMaxSegs];
+    int n_segs;
+    int bad;
+    u128 cta_total;
+    Fn cta_agg;
+    unsigned long long cta_cbo;
+    Fn final_total;   // the last segment's function (written by the CTA owning the last value)
+    int has_final;
+    double final_sum;
+    // cluster-wide chained segment table (filled in CTA 0, copied by every CTA)
+    int g_n;
+    uint32_t g_pos[kMaxSegs];
+    int g_e[kMaxSegs];
+    u128 g_first[kMaxSegs];
+    u128 g_end[kMaxSegs + 1];
+};
+
+__global__ void __cluster_dims__(kCC, 1, 1) __launch_bounds__(kBT, 1)
+k_thresholds_cluster(const double* __restrict__ lcom, const uint32_t* __restrict__ cbo, uint32_t n,
+                     DevThresholds* __restrict__ out) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    __shared__ ClusterShared sh;
+    extern __shared__ double vals[];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int rank = (int)cluster.block_rank();
+    const uint32_t E = (n + kCC * kBT - 1) / (kCC * kBT);
+    const uint32_t base = (uint32_t)rank * kBT * E;
+    const uint32_t len = base < n ? min((uint32_t)kBT * E, n - base) : 0u;
+    const uint32_t lo = (uint32_t)t * E;                  // local chunk start
+    const uint32_t cnt = lo < len ? min(E, len - lo) : 0u;
+    const uint32_t my = base + lo;                        // global chunk start
+    if (t == 0) { sh.n_segs = 0; sh.bad = 0; sh.has_final = 0; }
+    // ---- load this CTA's values (coalesced) and its cbo sum
+    unsigned long long cs = 0;
+    for (uint32_t i = t; i < len; i += kBT) {
+        vals[i] = __ldg(lcom + base + i);
+        if (cbo) cs += __ldg(cbo + base + i);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) cs += __shfl_down_sync(0xffffffffu, cs, d);
+    if (lane == 0) sh.warp_c[warp] = cs;
+    __syncthreads();
+    // ---- (1) preconditions, exact chunk sums, cluster prefix
+    u128 S = 0;
+    int bad = 0;
+    for (uint32_t j = 0; j < cnt; ++j) {
+        uint64_t X;
+        bad |= !lcom_units(vals[lo + j], X);
+        S += X;
+    }
+    bad = __syncthreads_or(bad);
+    const u128 ex_blk = blk1k_excl_u128(S, sh);
+    if (t == kBT - 1) sh.cta_total = ex_blk + S;
+    if (t == 0) {
+        unsigned long long c = 0;
+        for (int w = 0; w < kBT / 32; ++w) c += sh.warp_c[w];
+        sh.cta_cbo = c;
+        sh.bad = bad;
+    }
+    cluster.sync();
+    int any_bad = 0;
+    u128 cta_prefix = 0;
+    for (int r = 0; r < kCC; ++r) {
+        ClusterShared* o = cluster.map_shared_rank(&sh, r);
+        any_bad |= o->bad;
+        if (r < rank) cta_prefix += o->cta_total;
+    }
+    if (any_bad) {  // outside the fast path's precondition: CTA 0 sums serially
+        if (rank == 0 && warp == 0) {
+            double sl = 0.0;
+            for (uint32_t b = 0; b < n; b += 32) {
+                const uint32_t i = b + lane;
+                const double v = i < n ? lcom[i] : 0.0;
+                const uint32_t m = min(32u, n - b);
+                for (uint32_t k = 0; k < m; ++k) sl = __dadd_rn(sl, __shfl_sync(0xffffffffu, v, k));
+            }
+            if (lane == 0) {
+                unsigned long long csum = 0;
+                for (int r = 0; r < kCC; ++r) csum += cluster.map_shared_rank(&sh, r)->cta_cbo;
+                out->lcom = n ? __ddiv_rn(sl, (double)n) : 0.0;
+                double mc;
+                if (csum < (1ull << 53)) {
+                    mc = n ? __ddiv_rn((double)csum, (double)n) : 0.0;
+                } else {
+                    double sc = 0.0;
+                    for (uint32_t i = 0; i < n; ++i) sc = __dadd_rn(sc, cbo ? (double)cbo[i] : 0.0);
+                    mc = n ? __ddiv_rn(sc, (double)n) : 0.0;
+                }
+                out->cbo = mc;
+                out->fast_path_ok = 0;
+            }
+        }
+        cluster.sync();  // no CTA leaves while its shared memory may still be read
+        return;
+    }
+    const u128 P_my = cta_prefix + ex_blk;
+    // ---- (2) binade segments and per-chunk functions
+    const int e_prev = my == 0 ? -1 : gran_exp(P_my);
+    const bool has_start = cnt > 0 && gran_exp(P_my + S) != e_prev;
+    Fn agg = fn_id();
+    if (cnt > 0 && !has_start) {
+        for (uint32_t j = 0; j < cnt; ++j) {
+            uint64_t X;
+            lcom_units(vals[lo + j], X);
+            agg = compose(agg, fn_elem(X, e_prev));
+        }
+    } else if (has_start) {
+        u128 P = P_my;
+        int ep = e_prev;
+        for (uint32_t j = 0; j < cnt; ++j) {
+            uint64_t X;
+            lcom_units(vals[lo + j], X);
+            P += X;
+            const int e = gran_exp(P);
+            if (e != ep) {
+                agg = fn_id();
+                agg.bits |= 4u;
+            } else {
+                const uint32_t fl = agg.bits & 4u;
+                agg = compose(agg, fn_elem(X, e));
+                agg.bits |= fl;
+            }
+            ep = e;
+        }
+    }
+    const Fn ex_fn = blk1k_excl_fn(agg, sh);
+    if (t == kBT - 1) sh.cta_agg = seg_combine(ex_fn, agg);
+    cluster.sync();
+    Fn cta_in = fn_id();
+    for (int r = 0; r < rank; ++r) cta_in = seg_combine(cta_in, cluster.map_shared_rank(&sh, r)->cta_agg);
+    // the function since the last segment start before this chunk
+    const Fn excl = seg_combine(cta_in, ex_fn);
+    if (has_start) {  // record starts with the function of the segment each closes
+        Fn run = excl;
+        u128 P = P_my;
+        int ep = e_prev;
+        for (uint32_t j = 0; j < cnt; ++j) {
+            uint64_t X;
+            lcom_units(vals[lo + j], X);
+            P += X;
+            const int e = gran_exp(P);
+            if (e != ep) {
+                const int k = atomicAdd(&sh.n_segs, 1);
+                if (k < kMaxSegs) {
+                    sh.seg_pos[k] = my + j; sh.seg_e[k] = e; sh.seg_x[k] = X; sh.seg_close[k] = run;
+                } else {
+                    sh.bad = 1;
+                }
+                run = fn_id();
+            } else {
+                run = compose(run, fn_elem(X, e));
+            }
+            ep = e;
+        }
+        if (my + cnt == n) { sh.final_total = run; sh.has_final = 1; }
+    } else if (cnt > 0 && my + cnt == n) {
+        sh.final_total = compose(excl, agg);
+        sh.has_final = 1;
+    }
+    cluster.sync();
+    if (rank == 0 && t == 0) {  // chain every segment, in rank (= position) order, from S_0 = 0
+        int K = 0;
+        u128 T = 0;
+        int bad_seg = 0;
+        Fn fin = fn_id();
+        uint32_t pos[kMaxSegs];
+        int ee[kMaxSegs];
+        uint64_t xx[kMaxSegs];
+        Fn cl[kMaxSegs];
+        for (int r = 0; r < kCC; ++r) {
+            ClusterShared* o = cluster.map_shared_rank(&sh, r);
+            bad_seg |= o->bad;
+            const int ns = min(o->n_segs, kMaxSegs);
+            for (int a = 0; a < ns; ++a) {  // a CTA's list in position order (insertion sort, ≤ 64)
+                const uint32_t p = o->seg_pos[a];
+                int b = K;
+                while (b > 0 && pos[b - 1] > p) {
+                    if (b < kMaxSegs) { pos[b] = pos[b - 1]; ee[b] = ee[b - 1]; xx[b] = xx[b - 1]; cl[b] = cl[b - 1]; }
+                    --b;
+                }
+                if (K < kMaxSegs) {
+                    pos[b] = p; ee[b] = o->seg_e[a]; xx[b] = o->seg_x[a]; cl[b] = o->seg_close[a];
+                    ++K;
+                } else {
+                    bad_seg = 1;
+                }
+            }
+            if (o->has_final) fin = o->final_total;
+        }
+        sh.g_end[0] = T;
+        for (int k = 0; k < K; ++k) {
+            const Fn tot = k + 1 < K ? cl[k + 1] : fin;  // segment k closes at start k+1 (or the end)
+            const int e = ee[k];
+            T = rne53(T + xx[k]);
+            sh.g_pos[k] = pos[k];
+            sh.g_e[k] = e;
+            sh.g_first[k] = T;
+            T += (u128)finc(tot, (int)((T >> e) & 1)) << e;
+            sh.g_end[k + 1] = T;
+        }
+        sh.g_n = K;
+        sh.bad = bad_seg;
+    }
+    cluster.sync();
+    ClusterShared* z = cluster.map_shared_rank(&sh, 0);
+    const int K = z->g_n;
+    int kb = -1;
+    for (int k = 0; k < K; ++k)
+        if (z->g_pos[k] < my) kb = k;
+    u128 S0 = 0;
+    if (cnt > 0) {
+        if (has_start && kb + 1 < K && z->g_pos[kb + 1] == my) {
+            S0 = z->g_end[kb + 1];
+        } else if (kb >= 0) {
+            const int e = z->g_e[kb];
+            const u128 F = z->g_first[kb];
+            S0 = F + ((u128)finc(excl, (int)((F >> e) & 1)) << e);
+        }
+    }
+    const double s0 = u128_to_double(S0);
+    sh.start[t] = s0;
+    cluster.sync();
+    // ---- (3) exact replay in IEEE doubles from shared memory; every join must hold
+    double sv = s0;
+    for (uint32_t j = 0; j < cnt; ++j) sv = __dadd_rn(sv, vals[lo + j]);
+    int jb = 0;
+    if (cnt > 0 && my + cnt < n) {
+        const double next = t + 1 < kBT ? sh.start[t + 1] : cluster.map_shared_rank(&sh, rank + 1)->start[0];
+        if (next != sv) jb = 1;
+    }
+    if (my == 0 && cnt > 0 && s0 != 0.0) jb = 1;
+    if (cnt > 0 && my + cnt == n) sh.final_sum = sv;
+    jb = __syncthreads_or(jb);
+    if (t == 0) sh.bad |= jb;
+    cluster.sync();
+    if (rank == 0 && t == 0) {
+        int b = 0;
+        unsigned long long csum = 0;
+        double sum = 0.0;
+        for (int r = 0; r < kCC; ++r) {
+            ClusterShared* o = cluster.map_shared_rank(&sh, r);
+            b |= o->bad;
+            csum += o->cta_cbo;
+            if (o->has_final) sum = o->final_sum;
+        }
+        double ml;
+        uint32_t fast = 1;
+        if (b) {
+            fast = 0;
+            double sl = 0.0;
+            for (uint32_t i = 0; i < n; ++i) sl = __dadd_rn(sl, lcom[i]);
+            ml = n ? __ddiv_rn(sl, (double)n) : 0.0;
+        } else {
+            ml = n ? __ddiv_rn(sum, (double)n) : 0.0;
+        }
+        double mc;
+        if (csum < (1ull << 53)) {
+            mc = n ? __ddiv_rn((double)csum, (double)n) : 0.0;
+        } else {
+            fast = 0;
+            double sc = 0.0;
+            for (uint32_t i = 0; i < n; ++i) sc = __dadd_rn(sc, cbo ? (double)cbo[i] : 0.0);
+            mc = n ? __ddiv_rn(sc, (double)n) : 0.0;
+        }
+        out->lcom = ml;
+        out->cbo = mc;
+        out->fast_path_ok = fast;
+    }
+    cluster.sync();  // CTA 0 read the others' shared memory: keep them resident until here
+}
+
 // Serial fallback kernel (n too large for one co-resident tile per CTA).
 // The sequential sums literally, by one warp: each 32-element chunk is loaded
 // coalesced, then every lane runs the same left-to-right chain over the
@@ -743,6 +1039,11 @@ __global__ void k_thresholds_serial(const double* __restrict__ lcom, const uint3
 }  // namespace
 
 constexpr int kMaxDevices = 64;
+
+bool getenv_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && v[0] == '1';
+}
 constexpr uint32_t kSerialMax = 2048;  // below this one warp's serial chain beats three grid syncs (measured)
 
 size_t thresholds_scratch_bytes(uint32_t n) {
@@ -768,6 +1069,19 @@ cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t 
     }
     if (n == 0 || (allow_serial && n <= kSerialMax)) {
         k_thresholds_serial<<<1, 32, 0, st>>>(lcom, cbo, n, out);
+        return cudaGetLastError();
+    }
+    if (n <= kClusterMax && !getenv_flag("MMGPU_THR_BLOCK")) {  // 8 CTAs of one cluster, values in shared memory
+        const uint32_t E = (n + kCC * kBT - 1) / (kCC * kBT);
+        const size_t dyn = sizeof(double) * kBT * E;
+        static std::atomic<size_t> configured[kMaxDevices];
+        if (dev < kMaxDevices && configured[dev].load(std::memory_order_relaxed) < dyn) {
+            const cudaError_t e = cudaFuncSetAttribute(k_thresholds_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)(sizeof(double) * kBT * kCPer));
+            if (e != cudaSuccess) return e;
+            configured[dev].store(sizeof(double) * kBT * kCPer, std::memory_order_relaxed);
+        }
+        k_thresholds_cluster<<<kCC, kBT, dyn, st>>>(lcom, cbo, n, out);
         return cudaGetLastError();
     }
     if (n <= kBlockMax) {  // one CTA, no grid syncs

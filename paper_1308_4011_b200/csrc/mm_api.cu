@@ -166,6 +166,7 @@ struct mm_ctx {
     DBuf<uint4> wide_cnt;  // top-k / all-candidates: pass counts of methods with >= 32 used classes
     DBuf<uint32_t> fallback;  // best-only screen: record-overflow positions
     bool no_screen = false;   // env MMGPU_NO_SCREEN=1: best-only mode on the per-thread kernel (A/B)
+    bool thr_side = false;    // env MMGPU_THR_SIDE=1: threshold means on the side stream
     DBuf<double> gate_lcom;
     DBuf<uint32_t> gate_cbo;
     bool gates_set = false;
@@ -386,6 +387,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     if (const char* v = std::getenv("MMGPU_GIANT_MIN")) ctx->giant_min = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_CK_MMA_MIN")) ctx->ck_mma_min = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_NO_SCREEN")) ctx->no_screen = v[0] == '1';
+    if (const char* v = std::getenv("MMGPU_THR_SIDE")) ctx->thr_side = v[0] == '1';
     *out = ctx;
     return MM_OK;
 }
@@ -859,18 +861,22 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
         return MM_OK;
     });
     if (st) return st;
-    // threshold means on the side stream: they overlap the candidate scoring,
-    // only the emission pass of the sweep waits for them
-    MM_CUDA(ctx, cudaEventRecord(ctx->ev_metrics, ctx->stream));
-    MM_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_metrics, 0));
+    // threshold means: on the main stream, ahead of the sweep (the cluster
+    // kernel takes 8 SMs for a few µs; launched beside the scoring kernel it
+    // could not be placed until whole SMs drained). MMGPU_THR_SIDE=1: on the
+    // side stream, overlapping the scoring (only the emission pass waits).
+    cudaStream_t ts = ctx->thr_side ? ctx->side : ctx->stream;
+    if (ctx->thr_side) {
+        MM_CUDA(ctx, cudaEventRecord(ctx->ev_metrics, ctx->stream));
+        MM_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_metrics, 0));
+    }
     cudaError_t te = cudaSuccess;
-    st = run_on(ctx, ctx->side, "thresholds", [&] {
-        te = launch_thresholds(ctx->lcom.p, ctx->cbo.p, ctx->C, &ctl->thr, ctx->thr_scratch.p, ctx->thr_scratch.n,
-                               ctx->side);
+    st = run_on(ctx, ts, "thresholds", [&] {
+        te = launch_thresholds(ctx->lcom.p, ctx->cbo.p, ctx->C, &ctl->thr, ctx->thr_scratch.p, ctx->thr_scratch.n, ts);
     });
     if (st) return st;
     if (te != cudaSuccess) return cuda_fail(ctx, te, "thresholds");
-    MM_CUDA(ctx, cudaEventRecord(ctx->ev_thr, ctx->side));
+    MM_CUDA(ctx, cudaEventRecord(ctx->ev_thr, ts));
     ctx->metrics_valid = true;
     ctx->sweep_valid = false;
     return MM_OK;

@@ -44,9 +44,14 @@ struct Nccl {
     const char* (*error_string)(ncclResult_t) = nullptr;
 
     bool load(std::string& err) {
+        // an NCCL already in the process (e.g. the one torch loaded) first: a
+        // second libnccl.so.2 of another version would shadow it by soname
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h)
+            if (const char* p = std::getenv("MMGPU_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_LOCAL);
         for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-            h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
             if (h) break;
+            h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
         }
         if (!h) {
             err = "NCCL not found (dlopen libnccl.so.2 failed)";

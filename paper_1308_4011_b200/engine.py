@@ -471,6 +471,12 @@ class Group:
     GPU's assembled list (= suggest_all's ordered list)."""
 
     def __init__(self, devices: Optional[Sequence[int]] = None, n: Optional[int] = None):
+        # mm_group dlopens libnccl.so.2 and reuses one already in the process:
+        # load torch's first when torch is present, so both share one NCCL
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         if devices is None:
             devices = list(range(n if n is not None else 1))
         arr = (C.c_int * max(1, len(devices)))(*devices)
