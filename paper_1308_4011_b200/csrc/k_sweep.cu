@@ -698,6 +698,175 @@ __global__ void __launch_bounds__(kSweepTile) k_screen(SweepArgs a) {
     if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
 }
 
+// Variant 2 of the screen (MMGPU_SCREEN=2): the same decisions with the
+// memory round trips overlapped — the origin's record is requested before the
+// candidate slots are built, the first round's destination records before the
+// origin's doubles are computed, and the Bloom words of every other used class
+// are requested together (predicated, no early exit), the U rows only probed
+// for Bloom positives.
+#ifndef MMGPU_SCREEN_MINB
+#define MMGPU_SCREEN_MINB 4
+#endif
+__device__ __forceinline__ bool bloom_word_test(const ClassRec* __restrict__ rec, uint32_t d, uint32_t X) {
+    const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
+    const uint32_t w1 = __ldg(rec[d].sig + (b1 >> 5)), w2 = __ldg(rec[d].sig + (b2 >> 5));
+    return ((w1 >> (b1 & 31)) & (w2 >> (b2 & 31)) & 1u) != 0;
+}
+
+__global__ void __launch_bounds__(kSweepTile, MMGPU_SCREEN_MINB) k_screen2(SweepArgs a) {
+    __shared__ ScreenSmem sm;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
+    const bool live = pos < a.pos_end;
+    uint32_t (*ent)[kRecMaxEnt] = sm.ent[warp];
+    uint8_t* cm = sm.cm[warp];
+    uint8_t* ck = sm.ck[warp];
+    double* kc = sm.kc[warp];
+    uint32_t* kp = sm.kp[warp];
+
+    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
+    uint32_t o = 0;
+    if (live) {
+        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
+        r0 = rp[0];
+        r1 = rp[1];
+        o = __ldg(a.pos_owner + pos);
+    }
+    const bool ovf = live && (r0.x & kRecOverflow);
+    const uint32_t n = (live && !ovf) ? rec_n(r0.x) : 0u;
+    // the origin's record and lcom: in flight while the slots are built
+    ClassRec ro{};
+    double dlo = 0.0;
+    if (n) {
+        ro = load_rec(a.rec, o);
+        dlo = __ldg(a.dlcom + o);
+    }
+    {
+        const uint32_t e7[kRecMaxEnt] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k) ent[lane][k] = e7[k];
+    }
+    uint32_t nc = 0;
+#pragma unroll
+    for (int k = 0; k < kRecMaxEnt; ++k) nc += (k < (int)n && (ent[lane][k] >> 8) != o);
+    uint32_t incl = nc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+    }
+    const uint32_t excl = incl - nc;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    {
+        uint32_t w = excl;
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k)
+            if (k < (int)n && (ent[lane][k] >> 8) != o) {
+                cm[w] = (uint8_t)lane;
+                ck[w] = (uint8_t)k;
+                ++w;
+            }
+    }
+    __syncwarp();
+    // the first round's destination: record and lcom requested before the origin math
+    uint32_t c = lane, m = 0, d = 0, hd = 0;
+    ClassRec rd{};
+    double dld = 0.0;
+    auto fetch = [&]() {
+        if (c < total) {
+            m = cm[c];
+            const uint32_t e = ent[m][ck[c]];
+            d = e >> 8;
+            hd = e & 0xffu;
+            rd = load_rec(a.rec, d);
+            dld = __ldg(a.dlcom + d);
+        }
+    };
+    fetch();
+    // origin (this lane's method)
+    bool coh_ok = false, can_coup = false;
+    double lo_a = 0.0;
+    if (n) {
+        const uint32_t h = rec_hown(r0.x);
+        const uint32_t removed = (r0.x & kRecRemovedValid) ? rec_removed(r0.x)
+                                                            : removed_from_list(ro, a.ux, a.un, a.dense, a.s.C,
+                                                                                ent[lane], n, o);
+        can_coup = removed > 0;
+        bool maybe = ro.A != 0 && ro.M != 0;
+        if (maybe && ro.M >= 2 && (uint64_t)ro.A * ro.M < kExact53) maybe = (uint64_t)h * ro.M < ro.H;
+        if (maybe) {
+            lo_a = lcom_of(ro.A, (uint64_t)ro.M - 1, (uint64_t)ro.H - h);
+            coh_ok = lo_a < dlo;
+        }
+    }
+    const uint32_t flags = (coh_ok ? 1u : 0u) | (can_coup ? 2u : 0u);
+    for (uint32_t c0 = 0; c0 < total; c0 += 32) {
+        const bool act = c < total;
+        const uint32_t mflags = __shfl_sync(0xffffffffu, flags, act ? m : 0);
+        const double m_lo_a = __shfl_sync(0xffffffffu, lo_a, act ? m : 0);
+        const uint32_t m_n = __shfl_sync(0xffffffffu, n, act ? m : 0);
+        if (act) {
+            double key = -1.0;
+            uint32_t kpv = kNone;
+            if ((mflags & 1u) && rd.A != 0 && rd.M != 0) {
+                const bool exact = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
+                if (!exact || (uint64_t)hd * rd.M > rd.H) {
+                    const double ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
+                    if (ld_a < dld) key = __dadd_rn(m_lo_a, ld_a);  // lcom_key, suggest.hpp:194-196
+                }
+            }
+            if (mflags & 2u) {
+                // every other used class must be in U[d]: all Bloom words at once
+                bool ok = true;
+                uint32_t probe = 0;
+                if (rd.dense != kNone) {
+#pragma unroll
+                    for (int j = 0; j < kRecMaxEnt; ++j)
+                        if (j < (int)m_n) {
+                            const uint32_t X = ent[m][j] >> 8;
+                            if (X != d) ok &= ((__ldg(a.dense + rd.dense + (X >> 5)) >> (X & 31)) & 1u) != 0;
+                        }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < kRecMaxEnt; ++j)
+                        if (j < (int)m_n) {
+                            const uint32_t X = ent[m][j] >> 8;
+                            if (X != d) {
+                                if (bloom_word_test(a.rec, d, X)) probe |= 1u << j;
+                                else ok = false;
+                            }
+                        }
+                    for (int j = 0; ok && probe; ++j, probe >>= 1)
+                        if (probe & 1u) ok = urow_find(a.ux, rd.ubase, rd.cbo, ent[m][j] >> 8) >= 0;
+                }
+                if (ok) kpv = rd.cbo;
+            }
+            kc[c] = key;
+            kp[c] = kpv;
+        }
+        c += 32;
+        fetch();
+    }
+    __syncwarp();
+    uint32_t bd_coh = kNone, bd_coup = kNone;
+    double bk = 0.0;
+    uint32_t bp = 0;
+    for (uint32_t j = 0; j < nc; ++j) {
+        const uint32_t slot = excl + j;
+        const double kcv = kc[slot];
+        const uint32_t kpv = kp[slot];
+        if (kcv >= 0.0 || kpv != kNone) {
+            const uint32_t dd = ent[lane][ck[slot]] >> 8;
+            if (kcv >= 0.0 && (bd_coh == kNone || kcv < bk)) { bd_coh = dd; bk = kcv; }
+            if (kpv != kNone && (bd_coup == kNone || kpv < bp)) { bd_coup = dd; bp = kpv; }
+        }
+    }
+    if (live && !ovf) a.res[pos] = make_uint4(bd_coh, bd_coup, nc, 0);
+    if (ovf) a.fallback[atomicAdd(a.n_fallback, 1u)] = (uint32_t)pos;
+    const uint32_t wc = __reduce_add_sync(0xffffffffu, nc);
+    if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
+}
+
 // Pass 2: apply the class gates (suggest.hpp:246, :273) and the criteria
 // merge (union / intersection, :315-341) to each method's pass-1 result,
 // then a tile scan + decoupled look-back gives every EMITTING method a slot in
@@ -1005,7 +1174,8 @@ __global__ void __launch_bounds__(kSweepTile) k_sim_emit(SweepArgs a, SimCrit sc
 void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st) {
     if (!n_tiles) return;
     if (a.mode == 0 && !a.no_screen) {
-        k_screen<<<n_tiles, kSweepTile, 0, st>>>(a);
+        if (a.screen_variant == 1) k_screen<<<n_tiles, kSweepTile, 0, st>>>(a);
+        else k_screen2<<<n_tiles, kSweepTile, 0, st>>>(a);
         if (fallback_tiles) {  // methods whose used list overflowed its record
             if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
             else k_score_thread<16, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);

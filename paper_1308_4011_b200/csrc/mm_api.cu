@@ -167,6 +167,7 @@ struct mm_ctx {
     DBuf<uint32_t> fallback;  // best-only screen: record-overflow positions
     bool no_screen = false;   // env MMGPU_NO_SCREEN=1: best-only mode on the per-thread kernel (A/B)
     bool thr_side = false;    // env MMGPU_THR_SIDE=1: threshold means on the side stream
+    uint32_t screen_variant = 2;  // env MMGPU_SCREEN (A/B of the best-only screen)
     DBuf<double> gate_lcom;
     DBuf<uint32_t> gate_cbo;
     bool gates_set = false;
@@ -388,6 +389,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     if (const char* v = std::getenv("MMGPU_CK_MMA_MIN")) ctx->ck_mma_min = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_NO_SCREEN")) ctx->no_screen = v[0] == '1';
     if (const char* v = std::getenv("MMGPU_THR_SIDE")) ctx->thr_side = v[0] == '1';
+    if (const char* v = std::getenv("MMGPU_SCREEN")) ctx->screen_variant = (uint32_t)std::strtoul(v, nullptr, 10);
     *out = ctx;
     return MM_OK;
 }
@@ -1384,6 +1386,7 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     a.fallback = ctx->fallback.p;
     a.n_fallback = &ctl->n_fallback;
     a.no_screen = ctx->no_screen ? 1u : 0u;
+    a.screen_variant = ctx->screen_variant;
     mm_status st = run(ctx, "score", [&] { launch_score(a, n_tiles, fallback_tiles, ctx->stream); });
     if (st) return st;
     if (a.thr_device)

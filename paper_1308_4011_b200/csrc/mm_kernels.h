@@ -58,6 +58,7 @@ struct SweepArgs {
     uint32_t* fallback;         // best-only screen: positions handed to the per-thread kernel
     uint32_t* n_fallback;
     uint32_t no_screen;         // 1: best-only mode on the per-thread kernel (A/B, MMGPU_NO_SCREEN)
+    uint32_t screen_variant;    // MMGPU_SCREEN: 1 plain, 2 overlapped round trips (default)
 };
 
 void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t* bad, cudaStream_t st);
