@@ -558,8 +558,8 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
 // other used class in U[d] (exact bitmap, or Bloom then the row). Per-method
 // argmin over (key, d) in ascending-d order with strict < (lowest d wins
 // ties, suggest.hpp:180-184) reads the candidates' results back from shared
-// memory. Methods whose used list did not fit their record go to the
-// per-thread kernel (k_score_thread<K, true>) through a short list.
+// memory. Methods whose used list did not fit their record are evaluated
+// afterwards by the whole warp, one at a time (screen_coop).
 constexpr int kScreenWarps = kSweepTile / 32;
 constexpr int kScreenSlots = 32 * kRecMaxEnt;  // candidates of one warp: ≤ 7 per method
 
@@ -571,7 +571,155 @@ struct ScreenSmem {
     uint32_t kp[kScreenWarps][kScreenSlots];      // coupling key cbo_d (passing) or kNone
 };
 
-__global__ void __launch_bounds__(kSweepTile) k_screen(SweepArgs a) {
+// ascending bitonic sort of buf[0, N) (N a power of two), one warp
+__device__ __forceinline__ void warp_sort_u32(uint32_t* buf, uint32_t N, int lane) {
+    for (uint32_t k = 2; k <= N; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = lane; i < N; i += 32) {
+                const uint32_t ixj = i ^ j;
+                if (ixj > i) {
+                    const uint32_t x = buf[i], y = buf[ixj];
+                    if ((x > y) == ((i & k) == 0)) { buf[i] = y; buf[ixj] = x; }
+                }
+            }
+            __syncwarp();
+        }
+}
+
+constexpr uint32_t kCoopMaxDeg = 128;  // methods with more edges (hubs) take one lane's streaming path
+
+// Best-only evaluation of ONE method whose used list did not fit its record,
+// by the whole warp (all lanes call it with the same pos): the used list from
+// the CSR (lane per edge, warp sort, run-length -> classes and own-access
+// counts), the origin's removed count over lanes, then one destination per
+// lane and a warp argmin over (key, list index). `scr` holds ≥ 3·kCoopMaxDeg
+// words of this warp's shared memory.
+__device__ __noinline__ void screen_coop(const SweepArgs& a, uint32_t pos, uint32_t* scr, int lane) {
+    const uint32_t p = __ldg(a.s.cls_methods + pos), o = __ldg(a.pos_owner + pos);
+    const uint32_t cb = __ldg(a.s.call_off + p), nc = __ldg(a.s.call_off + p + 1) - cb;
+    const uint32_t ab = __ldg(a.s.acc_off + p), na = __ldg(a.s.acc_off + p + 1) - ab;
+    const uint32_t deg = nc + na;
+    uint32_t* key = scr;                      // owner << 1 | is_access, sorted
+    uint32_t* LX = scr + kCoopMaxDeg;         // distinct used classes, ascending
+    uint32_t* LH = scr + 2 * kCoopMaxDeg;     // accesses of the method owned by each
+    uint32_t N = 32;
+    while (N < deg) N <<= 1;
+    for (uint32_t k = lane; k < N; k += 32) {
+        uint32_t v = kNone;
+        if (k < nc) v = __ldg(a.s.method_owner + __ldg(a.s.call_tgt + cb + k)) << 1;
+        else if (k < deg) v = (__ldg(a.s.attr_info + __ldg(a.s.acc_tgt + ab + (k - nc))).x << 1) | 1u;
+        key[k] = v;
+    }
+    __syncwarp();
+    warp_sort_u32(key, N, lane);
+    uint32_t n = 0;
+    for (uint32_t k0 = 0; k0 < deg; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const bool head = k < deg && (k == 0 || (key[k] >> 1) != (key[k - 1] >> 1));
+        const uint32_t hb = __ballot_sync(0xffffffffu, head);
+        if (head) {
+            const uint32_t X = key[k] >> 1;
+            uint32_t h = 0, e = k;
+            while (e < deg && (key[e] >> 1) == X) h += key[e++] & 1u;
+            const uint32_t idx = n + __popc(hb & ((1u << lane) - 1));
+            LX[idx] = X;
+            LH[idx] = h;
+        }
+        n += __popc(hb);
+    }
+    __syncwarp();
+    // origin: own-access count, removed count (U[o][X] == 1) over lanes
+    const ClassRec ro = load_rec(a.rec, o);
+    uint32_t hown = 0, removed = 0, own_used = 0;
+    for (uint32_t k = lane; k < n; k += 32) {
+        const uint32_t X = LX[k];
+        if (X == o) { hown = LH[k]; own_used = 1; continue; }
+        if (ro.dense != kNone) {
+            removed += (__ldg(a.dense + ro.dense + (a.s.C + 31) / 32 + (X >> 5)) >> (X & 31)) & 1u;
+        } else {
+            const int q = urow_find(a.ux, ro.ubase, ro.cbo, X);
+            if (q >= 0 && __ldg(a.un + ro.ubase + q) == 1u) ++removed;
+        }
+    }
+    hown = __reduce_max_sync(0xffffffffu, hown);
+    removed = __reduce_add_sync(0xffffffffu, removed);
+    own_used = __reduce_or_sync(0xffffffffu, own_used);
+    const Origin org = make_origin(ro, hown, removed);
+    const bool can_coup = org.co_a < org.co_b;
+    // destinations: one per lane
+    double bk = 0.0;
+    uint32_t bki = kNone, bp = 0, bpi = kNone;
+    if (org.coh_ok || can_coup)
+        for (uint32_t k = lane; k < n; k += 32) {
+            const uint32_t d = LX[k];
+            if (d == o) continue;
+            const ClassRec rd = load_rec(a.rec, d);
+            double ld_a;
+            if (org.coh_ok && coh_dest(rd, LH[k], ld_a)) {
+                const double kc = __dadd_rn(org.lo_a, ld_a);
+                if (bki == kNone || kc < bk) { bk = kc; bki = k; }
+            }
+            if (can_coup) {
+                bool ok = true;
+                for (uint32_t j = 0; j < n && ok; ++j) {
+                    const uint32_t X = LX[j];
+                    if (X != d && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ok = false;
+                }
+                if (ok && (bpi == kNone || rd.cbo < bp)) { bp = rd.cbo; bpi = k; }
+            }
+        }
+    // warp argmin over (key, list index): lowest d wins ties (suggest.hpp:180-184)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ok_ = __shfl_xor_sync(0xffffffffu, bk, off);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bki, off);
+        if (oi != kNone && (bki == kNone || ok_ < bk || (ok_ == bk && oi < bki))) { bk = ok_; bki = oi; }
+        const uint32_t op = __shfl_xor_sync(0xffffffffu, bp, off);
+        const uint32_t opi = __shfl_xor_sync(0xffffffffu, bpi, off);
+        if (opi != kNone && (bpi == kNone || op < bp || (op == bp && opi < bpi))) { bp = op; bpi = opi; }
+    }
+    if (lane == 0) {
+        const uint32_t cands = n - own_used;
+        a.res[pos] = make_uint4(bki == kNone ? kNone : LX[bki], bpi == kNone ? kNone : LX[bpi], cands, 0);
+        if (cands) atomicAdd(a.stats + 0, (unsigned long long)cands);
+    }
+    __syncwarp();
+}
+
+// one hub method (more than kCoopMaxDeg edges) on one lane, streaming used list
+__device__ __noinline__ void screen_stream_one(const SweepArgs& a, uint32_t ps, uint32_t pm) {
+    const uint32_t o = __ldg(a.pos_owner + ps);
+    StreamEnum sen;
+    sen.S.init(a.s, pm);
+    const ClassRec ro = load_rec(a.rec, o);
+    const Origin org = make_origin(ro, sen.hits(o), removed_count(ro, a.ux, a.un, a.dense, a.s.C, sen, o));
+    const MethodResult r = evaluate(a, sen, o, org, true, true);
+    a.res[ps] = make_uint4(r.bd_coh, r.bd_coup, r.cands, 0);
+    if (r.cands) atomicAdd(a.stats + 0, (unsigned long long)r.cands);
+}
+
+// the warp's methods whose used list did not fit their record (ovf lanes):
+// one at a time by the whole warp; hubs beyond kCoopMaxDeg edges by their own
+// lane on the streaming used list
+__device__ __forceinline__ void screen_overflow(const SweepArgs& a, bool ovf, uint64_t pos, uint32_t* scr, int lane) {
+    uint32_t ob = __ballot_sync(0xffffffffu, ovf);
+    while (ob) {
+        const int src = __ffs(ob) - 1;
+        ob &= ob - 1;
+        const uint32_t ps = __shfl_sync(0xffffffffu, (uint32_t)pos, src);
+        const uint32_t pm = __ldg(a.s.cls_methods + ps);
+        const uint32_t deg = (__ldg(a.s.call_off + pm + 1) - __ldg(a.s.call_off + pm)) +
+                             (__ldg(a.s.acc_off + pm + 1) - __ldg(a.s.acc_off + pm));
+        if (deg <= kCoopMaxDeg) {
+            screen_coop(a, ps, scr, lane);
+        } else if (lane == src) {
+            screen_stream_one(a, ps, pm);
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kSweepTile, 4) k_screen(SweepArgs a) {
     __shared__ ScreenSmem sm;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
@@ -693,9 +841,10 @@ __global__ void __launch_bounds__(kSweepTile) k_screen(SweepArgs a) {
         }
     }
     if (live && !ovf) a.res[pos] = make_uint4(bd_coh, bd_coup, nc, 0);
-    if (ovf) a.fallback[atomicAdd(a.n_fallback, 1u)] = (uint32_t)pos;
     const uint32_t wc = __reduce_add_sync(0xffffffffu, nc);
     if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
+    __syncwarp();
+    screen_overflow(a, ovf, pos, reinterpret_cast<uint32_t*>(kc), lane);  // kc: free after the argmin
 }
 
 // Variant 2 of the screen (MMGPU_SCREEN=2): the same decisions with the
@@ -862,9 +1011,10 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCREEN_MINB) k_screen2(Sweep
         }
     }
     if (live && !ovf) a.res[pos] = make_uint4(bd_coh, bd_coup, nc, 0);
-    if (ovf) a.fallback[atomicAdd(a.n_fallback, 1u)] = (uint32_t)pos;
     const uint32_t wc = __reduce_add_sync(0xffffffffu, nc);
     if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
+    __syncwarp();
+    screen_overflow(a, ovf, pos, reinterpret_cast<uint32_t*>(kc), lane);  // kc: free after the argmin
 }
 
 // Pass 2: apply the class gates (suggest.hpp:246, :273) and the criteria
@@ -1176,10 +1326,7 @@ void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles,
     if (a.mode == 0 && !a.no_screen) {
         if (a.screen_variant == 1) k_screen<<<n_tiles, kSweepTile, 0, st>>>(a);
         else k_screen2<<<n_tiles, kSweepTile, 0, st>>>(a);
-        if (fallback_tiles) {  // methods whose used list overflowed its record
-            if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
-            else k_score_thread<16, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
-        }
+        (void)fallback_tiles;  // record-overflow methods are handled inside the screen (warp-cooperative)
         return;
     }
     if (a.maxdeg_fast <= 8) k_score_thread<8><<<n_tiles, kSweepTile, 0, st>>>(a);

@@ -36,6 +36,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "mm_async.cuh"
 #include "mm_device.cuh"
 #include "mm_kernels.h"
 
@@ -722,8 +723,8 @@ k_thresholds_block(const double* __restrict__ lcom, const uint32_t* __restrict__
 // (hardware) between phases. Segment chaining (≤ kMaxSegs starts, in rank
 // order) is done by one thread of CTA 0, which publishes the chained states.
 constexpr int kCC = 8;                                  // CTAs per cluster (portable)
-constexpr int kCPer = 24;                               // values per thread (max)
-constexpr uint32_t kClusterMax = (uint32_t)kCC * kBT * kCPer;  // 196,608 values
+constexpr int kCPer = 17;                               // values per thread (max): (8 + 4) B each in shared memory
+constexpr uint32_t kClusterMax = (uint32_t)kCC * kBT * kCPer;  // 139,264 values
 
 struct ClusterShared {
     u128 warp_u128[kBT / 32];
@@ -744,6 +745,7 @@ struct ClusterShared {
     Fn final_total;   // the last segment's function (written by the CTA owning the last value)
     int has_final;
     double final_sum;
+    uint64_t bar;     // the bulk copies' mbarrier
     // cluster-wide chained segment table (filled in CTA 0, copied by every CTA)
     int g_n;
     uint32_t g_pos[kMaxSegs];
@@ -767,17 +769,31 @@ k_thresholds_cluster(const double* __restrict__ lcom, const uint32_t* __restrict
     const uint32_t lo = (uint32_t)t * E;                  // local chunk start
     const uint32_t cnt = lo < len ? min(E, len - lo) : 0u;
     const uint32_t my = base + lo;                        // global chunk start
-    if (t == 0) { sh.n_segs = 0; sh.bad = 0; sh.has_final = 0; }
-    // ---- load this CTA's values (coalesced) and its cbo sum
-    unsigned long long cs = 0;
-    for (uint32_t i = t; i < len; i += kBT) {
-        vals[i] = __ldg(lcom + base + i);
-        if (cbo) cs += __ldg(cbo + base + i);
+    // ---- this CTA's values and cbo counts into shared memory: one bulk (TMA)
+    // copy each, completing on an mbarrier; the odd tail by plain loads
+    uint32_t* cvals = reinterpret_cast<uint32_t*>(vals + (size_t)kBT * E);
+    const uint32_t lb = (len * 8u) & ~15u, cb = cbo ? (len * 4u) & ~15u : 0u;
+    if (t == 0) {
+        sh.n_segs = 0; sh.bad = 0; sh.has_final = 0;
+        mbar_init(&sh.bar, 1);
     }
+    __syncthreads();
+    if (t == 0) {
+        mbar_expect_tx(&sh.bar, lb + cb);
+        if (lb) bulk_g2s(vals, lcom + base, lb, &sh.bar);
+        if (cb) bulk_g2s(cvals, cbo + base, cb, &sh.bar);
+    }
+    for (uint32_t i = lb / 8 + t; i < len; i += kBT) vals[i] = __ldg(lcom + base + i);
+    if (cbo)
+        for (uint32_t i = cb / 4 + t; i < len; i += kBT) cvals[i] = __ldg(cbo + base + i);
+    mbar_wait(&sh.bar, 0);
+    __syncthreads();
+    unsigned long long cs = 0;
+    if (cbo)
+        for (uint32_t j = 0; j < cnt; ++j) cs += cvals[lo + j];
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) cs += __shfl_down_sync(0xffffffffu, cs, d);
     if (lane == 0) sh.warp_c[warp] = cs;
-    __syncthreads();
     // ---- (1) preconditions, exact chunk sums, cluster prefix
     u128 S = 0;
     int bad = 0;
@@ -940,18 +956,29 @@ k_thresholds_cluster(const double* __restrict__ lcom, const uint32_t* __restrict
         sh.bad = bad_seg;
     }
     cluster.sync();
-    ClusterShared* z = cluster.map_shared_rank(&sh, 0);
-    const int K = z->g_n;
+    if (rank != 0) {  // the chained table into this CTA's shared memory (one remote read each)
+        ClusterShared* z = cluster.map_shared_rank(&sh, 0);
+        const int K0 = z->g_n;
+        if (t == 0) sh.g_n = K0;
+        for (int k = t; k < K0; k += kBT) {
+            sh.g_pos[k] = z->g_pos[k];
+            sh.g_e[k] = z->g_e[k];
+            sh.g_first[k] = z->g_first[k];
+            sh.g_end[k + 1] = z->g_end[k + 1];
+        }
+        __syncthreads();
+    }
+    const int K = sh.g_n;
     int kb = -1;
     for (int k = 0; k < K; ++k)
-        if (z->g_pos[k] < my) kb = k;
+        if (sh.g_pos[k] < my) kb = k;
     u128 S0 = 0;
     if (cnt > 0) {
-        if (has_start && kb + 1 < K && z->g_pos[kb + 1] == my) {
-            S0 = z->g_end[kb + 1];
+        if (has_start && kb + 1 < K && sh.g_pos[kb + 1] == my) {
+            S0 = sh.g_end[kb + 1];
         } else if (kb >= 0) {
-            const int e = z->g_e[kb];
-            const u128 F = z->g_first[kb];
+            const int e = sh.g_e[kb];
+            const u128 F = sh.g_first[kb];
             S0 = F + ((u128)finc(excl, (int)((F >> e) & 1)) << e);
         }
     }
@@ -1073,13 +1100,13 @@ cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t 
     }
     if (n <= kClusterMax && !getenv_flag("MMGPU_THR_BLOCK")) {  // 8 CTAs of one cluster, values in shared memory
         const uint32_t E = (n + kCC * kBT - 1) / (kCC * kBT);
-        const size_t dyn = sizeof(double) * kBT * E;
+        const size_t dyn = (sizeof(double) + sizeof(uint32_t)) * kBT * E;
         static std::atomic<size_t> configured[kMaxDevices];
         if (dev < kMaxDevices && configured[dev].load(std::memory_order_relaxed) < dyn) {
             const cudaError_t e = cudaFuncSetAttribute(k_thresholds_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)(sizeof(double) * kBT * kCPer));
+                                                       (int)((sizeof(double) + sizeof(uint32_t)) * kBT * kCPer));
             if (e != cudaSuccess) return e;
-            configured[dev].store(sizeof(double) * kBT * kCPer, std::memory_order_relaxed);
+            configured[dev].store((sizeof(double) + sizeof(uint32_t)) * kBT * kCPer, std::memory_order_relaxed);
         }
         k_thresholds_cluster<<<kCC, kBT, dyn, st>>>(lcom, cbo, n, out);
         return cudaGetLastError();
