@@ -222,7 +222,7 @@ k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask
     const uint32_t nc = ce - cb, na = ae - ab, deg = nc + na;
     // edges in chunks of K: all targets of a chunk, then all their owner
     // gathers — two memory round trips per chunk instead of two per edge.
-    // The list keeps kRecMaxEnt + 1 slots: an 8th distinct class means the
+    // The list keeps kRecMaxEnt + 1 slots: a 9th distinct class means the
     // record cannot hold the list (consumers then read the CSR).
     UsedList<kRecMaxEnt + 1> L;
     L.clear();
@@ -281,8 +281,9 @@ k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask
         }
     if (fits) hdr = (uint32_t)L.n | (hown << kRecHownShift);
     uint4* dst = reinterpret_cast<uint4*>(recs + pos);
-    dst[0] = make_uint4(hdr, ent[0], ent[1], ent[2]);
-    dst[1] = make_uint4(ent[3], ent[4], ent[5], ent[6]);
+    dst[0] = make_uint4(ent[0], ent[1], ent[2], ent[3]);
+    dst[1] = make_uint4(ent[4], ent[5], ent[6], ent[7]);
+    rec_hdrs(recs, s.M)[pos] = hdr;
     own_mask[pos] = mask;
 }
 
@@ -353,19 +354,22 @@ k_class_small(DevModel s, const uint4* __restrict__ cplan, const uint32_t* __res
 
     UsedList<kSmallMaxDeg> L;  // only for overflowed records
     L.clear();
-    uint4 r0 = make_uint4(kRecOverflow, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
+    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
+    uint32_t hdr = kRecOverflow;
     uint64_t mask = 0;
     uint32_t hown = 0;
+    uint32_t* hdrs = rec_hdrs(recs, s.M);
     if (active) {
         const uint4* src = reinterpret_cast<const uint4*>(recs + pos);
         r0 = src[0];
         r1 = src[1];
+        hdr = hdrs[pos];
         mask = own_mask[pos];
     }
-    const bool ovf = active && (r0.x & kRecOverflow);
-    const uint32_t ent[kRecMaxEnt] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-    uint32_t nent = active && !ovf ? rec_n(r0.x) : 0;
-    if (active && !ovf) hown = rec_hown(r0.x);
+    const bool ovf = active && (hdr & kRecOverflow);
+    const uint32_t ent[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    uint32_t nent = active && !ovf ? rec_n(hdr) : 0;
+    if (active && !ovf) hown = rec_hown(hdr);
     if (ovf) {
         const uint32_t p = s.cls_methods[pos];
         const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
@@ -495,7 +499,7 @@ k_class_small(DevModel s, const uint4* __restrict__ cplan, const uint32_t* __res
     __syncwarp();
     removed_me = rem[lane];
     // per member: #{X ≠ c : U[c][X] == 1} — the sweep's cbo_origin_after
-    if (active && !ovf) recs[pos].hdr = r0.x | (removed_me << kRecRemovedShift) | kRecRemovedValid;
+    if (active && !ovf) hdrs[pos] = hdr | (removed_me << kRecRemovedShift) | kRecRemovedValid;
     if (lane == 0) {
         const double l = lcom_of(A, M, H);
         const uint64_t pairs = (uint64_t)M * (M - 1) / 2;
@@ -576,7 +580,7 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
 // enumeration of the CSR row when the record overflowed); f(X, h).
 template <class F>
 __device__ __forceinline__ void member_used(const DevModel& s, const MethRec* recs, uint32_t pos, uint32_t p, F f) {
-    const uint32_t hdr = recs[pos].hdr;
+    const uint32_t hdr = rec_hdrs(recs, s.M)[pos];
     if (!(hdr & kRecOverflow)) {
         for (uint32_t k = 0; k < rec_n(hdr); ++k) {
             const uint32_t e = recs[pos].ent[k];
@@ -699,10 +703,11 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
             member_used(s, recs, pos, p, [&](uint32_t X, uint32_t) {
                 if (X != c) keys[atomicAdd(&s_nk, 1u)] = X;
             });
-        if (A <= 64 && pl.ck_masks && !(recs[pos].hdr & kRecOverflow)) {
+        const uint32_t mh = rec_hdrs(recs, s.M)[pos];
+        if (A <= 64 && pl.ck_masks && !(mh & kRecOverflow)) {
             // the method pass already built this member's mask and own-hit count
             masks[i] = own_mask[pos];
-            hown += rec_hown(recs[pos].hdr);
+            hown += rec_hown(mh);
             continue;
         }
         const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
@@ -822,7 +827,8 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     // phase 3: per member, #{X ≠ c : U[c][X] == 1} into its method record
     for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) {
         MethRec* r = recs + mb + i;
-        const uint32_t hdr = r->hdr;
+        uint32_t* rh = rec_hdrs(recs, s.M) + mb + i;
+        const uint32_t hdr = *rh;
         if (hdr & kRecOverflow) continue;
         uint32_t removed = 0;
         for (uint32_t k = 0; k < rec_n(hdr); ++k) {
@@ -835,7 +841,7 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
                 removed += (lower_bound_u32(keys, nk, X + 1) - lo) == 1u;
             }
         }
-        r->hdr = hdr | (removed << kRecRemovedShift) | kRecRemovedValid;
+        *rh = hdr | (removed << kRecRemovedShift) | kRecRemovedValid;
     }
 
     // phase 4: LCOM-CK, Q = #pairs (i<j) sharing an own attribute. Classes

@@ -476,17 +476,18 @@ __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, ui
                                             SmemEnum& ren, StreamEnum& sen, Origin& org) {
     const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
     const uint4 r0 = rp[0], r1 = rp[1];
+    const uint32_t hdr = rec_hdrs(a.recs, a.s.M)[pos];
     const ClassRec ro = load_rec(a.rec, o);
-    if (!(r0.x & kRecOverflow)) {
-        const uint32_t ent[kRecMaxEnt] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-        const uint32_t n = rec_n(r0.x);
+    if (!(hdr & kRecOverflow)) {
+        const uint32_t ent[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        const uint32_t n = rec_n(hdr);
 #pragma unroll
         for (int k = 0; k < kRecMaxEnt; ++k)
             if (k < (int)n) { ren.X[k * kSweepTile] = ent[k] >> 8; ren.H[k * kSweepTile] = ent[k] & 0xffu; }
         ren.n = (int)n;
-        const uint32_t removed = (r0.x & kRecRemovedValid) ? rec_removed(r0.x)
-                                                            : removed_count(ro, a.ux, a.un, a.dense, a.s.C, ren, o);
-        org = make_origin(ro, rec_hown(r0.x), removed);
+        const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
+                                                           : removed_count(ro, a.ux, a.un, a.dense, a.s.C, ren, o);
+        org = make_origin(ro, rec_hown(hdr), removed);
         return true;
     }
     if (ren.build(a.s, p, K)) {  // ≤ K distinct classes (any degree): shared-memory list
@@ -561,7 +562,7 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
 // memory. Methods whose used list did not fit their record are evaluated
 // afterwards by the whole warp, one at a time (screen_coop).
 constexpr int kScreenWarps = kSweepTile / 32;
-constexpr int kScreenSlots = 32 * kRecMaxEnt;  // candidates of one warp: ≤ 7 per method
+constexpr int kScreenSlots = 32 * kRecMaxEnt;  // candidates of one warp: ≤ 8 per method
 
 struct ScreenSmem {
     uint32_t ent[kScreenWarps][32][kRecMaxEnt];   // the methods' used lists (X << 8 | h), own class included
@@ -732,17 +733,18 @@ __global__ void __launch_bounds__(kSweepTile, 4) k_screen(SweepArgs a) {
 
     // ---- per method (this lane)
     uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
-    uint32_t o = 0;
+    uint32_t o = 0, hdr = 0;
     if (live) {
         const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
         r0 = rp[0];
         r1 = rp[1];
+        hdr = rec_hdrs(a.recs, a.s.M)[pos];
         o = __ldg(a.pos_owner + pos);
     }
-    const bool ovf = live && (r0.x & kRecOverflow);
-    const uint32_t n = (live && !ovf) ? rec_n(r0.x) : 0u;
+    const bool ovf = live && (hdr & kRecOverflow);
+    const uint32_t n = (live && !ovf) ? rec_n(hdr) : 0u;
     {
-        const uint32_t e7[kRecMaxEnt] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        const uint32_t e7[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
         for (int k = 0; k < kRecMaxEnt; ++k) ent[lane][k] = e7[k];
     }
@@ -754,8 +756,8 @@ __global__ void __launch_bounds__(kSweepTile, 4) k_screen(SweepArgs a) {
     double lo_a = 0.0;
     if (n) {
         const ClassRec ro = load_rec(a.rec, o);
-        const uint32_t h = rec_hown(r0.x);
-        const uint32_t removed = (r0.x & kRecRemovedValid) ? rec_removed(r0.x)
+        const uint32_t h = rec_hown(hdr);
+        const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
                                                             : removed_from_list(ro, a.ux, a.un, a.dense, a.s.C,
                                                                                 ent[lane], n, o);
         can_coup = removed > 0;  // cbo_origin_after < cbo_origin_before
@@ -874,15 +876,16 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCREEN_MINB) k_screen2(Sweep
     uint32_t* kp = sm.kp[warp];
 
     uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
-    uint32_t o = 0;
+    uint32_t o = 0, hdr = 0;
     if (live) {
         const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
         r0 = rp[0];
         r1 = rp[1];
+        hdr = rec_hdrs(a.recs, a.s.M)[pos];
         o = __ldg(a.pos_owner + pos);
     }
-    const bool ovf = live && (r0.x & kRecOverflow);
-    const uint32_t n = (live && !ovf) ? rec_n(r0.x) : 0u;
+    const bool ovf = live && (hdr & kRecOverflow);
+    const uint32_t n = (live && !ovf) ? rec_n(hdr) : 0u;
     // the origin's record and lcom: in flight while the slots are built
     ClassRec ro{};
     double dlo = 0.0;
@@ -891,7 +894,7 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCREEN_MINB) k_screen2(Sweep
         dlo = __ldg(a.dlcom + o);
     }
     {
-        const uint32_t e7[kRecMaxEnt] = {r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        const uint32_t e7[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
         for (int k = 0; k < kRecMaxEnt; ++k) ent[lane][k] = e7[k];
     }
@@ -936,8 +939,8 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCREEN_MINB) k_screen2(Sweep
     bool coh_ok = false, can_coup = false;
     double lo_a = 0.0;
     if (n) {
-        const uint32_t h = rec_hown(r0.x);
-        const uint32_t removed = (r0.x & kRecRemovedValid) ? rec_removed(r0.x)
+        const uint32_t h = rec_hown(hdr);
+        const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
                                                             : removed_from_list(ro, a.ux, a.un, a.dense, a.s.C,
                                                                                 ent[lane], n, o);
         can_coup = removed > 0;

@@ -766,7 +766,8 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         ctx->grows_words = 0;
     }
     // derived tables
-    MM_CUDA(ctx, ctx->recs.ensure(M ? M : 1));
+    // M 32-byte records, then their M 32-bit headers (rec_hdrs)
+    MM_CUDA(ctx, ctx->recs.ensure(M ? M + (M + 7) / 8 : 1));
     MM_CUDA(ctx, ctx->own_mask.ensure(M ? M : 1));
     MM_CUDA(ctx, ctx->rec.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->lcom.ensure(C ? C : 1));

@@ -70,17 +70,25 @@ __device__ __forceinline__ uint32_t bloom_h2(uint32_t x) {
 // Compact per-method record, stored at the method's class-order position by
 // the method pass (one 32-byte sector): the sorted used list (owner classes
 // of calls ∪ accesses, own class included) packed as X << 8 | h, with h the
-// number of accesses owned by X.
+// number of accesses owned by X — up to 8 classes, so a method with ≤ 8
+// edges (every method of the k ≤ 4 + 4 generator configs) always fits. The
+// record's 32-bit header lives in a separate array right after the records
+// (rec_hdrs): readers load it coalesced beside the entries.
+constexpr int kRecMaxEnt = 8;
 struct __align__(32) MethRec {
-    uint32_t hdr;      // see kRec* below
-    uint32_t ent[7];
+    uint32_t ent[kRecMaxEnt];
 };
-constexpr uint32_t kRecN = 0xfu;            // bits 0-3   number of entries (≤ 7)
+__host__ __device__ __forceinline__ uint32_t* rec_hdrs(MethRec* recs, uint32_t M) {
+    return reinterpret_cast<uint32_t*>(recs + M);
+}
+__host__ __device__ __forceinline__ const uint32_t* rec_hdrs(const MethRec* recs, uint32_t M) {
+    return reinterpret_cast<const uint32_t*>(recs + M);
+}
+constexpr uint32_t kRecN = 0xfu;            // bits 0-3   number of entries (≤ 8)
 constexpr int kRecHownShift = 8;            // bits 8-15  |acc(p) ∩ attrs(own)|
 constexpr int kRecRemovedShift = 16;        // bits 16-23 #{X ≠ own : U[own][X] == 1} (class pass)
 constexpr uint32_t kRecOverflow = 1u << 24; // list not representable: consumers use the CSR
 constexpr uint32_t kRecRemovedValid = 1u << 25;
-constexpr int kRecMaxEnt = 7;
 
 __device__ __forceinline__ uint32_t rec_n(uint32_t hdr) { return hdr & kRecN; }
 __device__ __forceinline__ uint32_t rec_hown(uint32_t hdr) { return (hdr >> kRecHownShift) & 0xffu; }
