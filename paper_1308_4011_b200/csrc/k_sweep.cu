@@ -595,7 +595,7 @@ constexpr uint32_t kCoopMaxDeg = 128;  // methods with more edges (hubs) take on
 // counts), the origin's removed count over lanes, then one destination per
 // lane and a warp argmin over (key, list index). `scr` holds ≥ 3·kCoopMaxDeg
 // words of this warp's shared memory.
-__device__ __noinline__ void screen_coop(const SweepArgs& a, uint32_t pos, uint32_t* scr, int lane) {
+__device__ __noinline__ void screen_coop(const SweepArgs& a, uint32_t pos, uint32_t* scr, int lane, uint4& out) {
     const uint32_t p = __ldg(a.s.cls_methods + pos), o = __ldg(a.pos_owner + pos);
     const uint32_t cb = __ldg(a.s.call_off + p), nc = __ldg(a.s.call_off + p + 1) - cb;
     const uint32_t ab = __ldg(a.s.acc_off + p), na = __ldg(a.s.acc_off + p + 1) - ab;
@@ -679,30 +679,28 @@ __device__ __noinline__ void screen_coop(const SweepArgs& a, uint32_t pos, uint3
         const uint32_t opi = __shfl_xor_sync(0xffffffffu, bpi, off);
         if (opi != kNone && (bpi == kNone || op < bp || (op == bp && opi < bpi))) { bp = op; bpi = opi; }
     }
-    if (lane == 0) {
-        const uint32_t cands = n - own_used;
-        a.res[pos] = make_uint4(bki == kNone ? kNone : LX[bki], bpi == kNone ? kNone : LX[bpi], cands, 0);
-        if (cands) atomicAdd(a.stats + 0, (unsigned long long)cands);
-    }
+    out = make_uint4(bki == kNone ? kNone : LX[bki], bpi == kNone ? kNone : LX[bpi], n - own_used, 0);
     __syncwarp();
 }
 
 // one hub method (more than kCoopMaxDeg edges) on one lane, streaming used list
-__device__ __noinline__ void screen_stream_one(const SweepArgs& a, uint32_t ps, uint32_t pm) {
+__device__ __noinline__ uint4 screen_stream_one(const SweepArgs& a, uint32_t ps, uint32_t pm) {
     const uint32_t o = __ldg(a.pos_owner + ps);
     StreamEnum sen;
     sen.S.init(a.s, pm);
     const ClassRec ro = load_rec(a.rec, o);
     const Origin org = make_origin(ro, sen.hits(o), removed_count(ro, a.ux, a.un, a.dense, a.s.C, sen, o));
     const MethodResult r = evaluate(a, sen, o, org, true, true);
-    a.res[ps] = make_uint4(r.bd_coh, r.bd_coup, r.cands, 0);
-    if (r.cands) atomicAdd(a.stats + 0, (unsigned long long)r.cands);
+    return make_uint4(r.bd_coh, r.bd_coup, r.cands, 0);
 }
 
 // the warp's methods whose used list did not fit their record (ovf lanes):
 // one at a time by the whole warp; hubs beyond kCoopMaxDeg edges by their own
-// lane on the streaming used list
-__device__ __forceinline__ void screen_overflow(const SweepArgs& a, bool ovf, uint64_t pos, uint32_t* scr, int lane) {
+// lane on the streaming used list. Returns this lane's (bd_coh, bd_coup,
+// candidates) when it is an ovf lane.
+__device__ __forceinline__ uint4 screen_overflow(const SweepArgs& a, bool ovf, uint64_t pos, uint32_t* scr,
+                                                 int lane) {
+    uint4 mine = make_uint4(kNone, kNone, 0, 0);
     uint32_t ob = __ballot_sync(0xffffffffu, ovf);
     while (ob) {
         const int src = __ffs(ob) - 1;
@@ -712,12 +710,15 @@ __device__ __forceinline__ void screen_overflow(const SweepArgs& a, bool ovf, ui
         const uint32_t deg = (__ldg(a.s.call_off + pm + 1) - __ldg(a.s.call_off + pm)) +
                              (__ldg(a.s.acc_off + pm + 1) - __ldg(a.s.acc_off + pm));
         if (deg <= kCoopMaxDeg) {
-            screen_coop(a, ps, scr, lane);
+            uint4 r;
+            screen_coop(a, ps, scr, lane, r);
+            if (lane == src) mine = r;
         } else if (lane == src) {
-            screen_stream_one(a, ps, pm);
+            mine = screen_stream_one(a, ps, pm);
         }
         __syncwarp();
     }
+    return mine;
 }
 
 __global__ void __launch_bounds__(kSweepTile, 4) k_screen(SweepArgs a) {
@@ -846,7 +847,11 @@ __global__ void __launch_bounds__(kSweepTile, 4) k_screen(SweepArgs a) {
     const uint32_t wc = __reduce_add_sync(0xffffffffu, nc);
     if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
     __syncwarp();
-    screen_overflow(a, ovf, pos, reinterpret_cast<uint32_t*>(kc), lane);  // kc: free after the argmin
+    const uint4 ov = screen_overflow(a, ovf, pos, reinterpret_cast<uint32_t*>(kc), lane);  // kc: free now
+    if (ovf) {
+        a.res[pos] = ov;
+        if (ov.z) atomicAdd(a.stats + 0, (unsigned long long)ov.z);
+    }
 }
 
 // Variant 2 of the screen (MMGPU_SCREEN=2): the same decisions with the
@@ -1017,7 +1022,312 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCREEN_MINB) k_screen2(Sweep
     const uint32_t wc = __reduce_add_sync(0xffffffffu, nc);
     if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
     __syncwarp();
-    screen_overflow(a, ovf, pos, reinterpret_cast<uint32_t*>(kc), lane);  // kc: free after the argmin
+    const uint4 ov = screen_overflow(a, ovf, pos, reinterpret_cast<uint32_t*>(kc), lane);  // kc: free now
+    if (ovf) {
+        a.res[pos] = ov;
+        if (ov.z) atomicAdd(a.stats + 0, (unsigned long long)ov.z);
+    }
+}
+
+// ---- best-only mode, fused: screen + gates + offsets + records in one pass
+//
+// The class gates need the threshold means, which the metric pass now
+// computes before the sweep, so the whole best-only sweep runs as one kernel:
+// each CTA takes the next 256 class-order positions (dynamic tile id), screens
+// them exactly as k_screen, applies the gates (suggest.hpp:246, :273) and the
+// criteria merge (:315-341) per method, scans the record counts over the CTA
+// and a decoupled look-back over the preceding tiles (relaxed gpu-scope
+// 64-bit words: flag | emitters << 32 | records), publishes its inclusive
+// prefix, and only then writes its records (what-if values recomputed from the
+// class tables, suggest.hpp:87-122): emission never delays a successor's
+// look-back. No per-method result array, no emitter list, no extra launch.
+
+// decoupled look-back by warp 0 of the CTA: returns (lane 0) the exclusive
+// prefix of this tile and publishes tile_state[tile] = prefix | (excl + agg)
+__device__ __forceinline__ unsigned long long tile_lookback(const SweepArgs& a, uint32_t tile, unsigned long long agg,
+                                                            int lane) {
+    unsigned long long excl = 0;
+    if (tile == 0) {
+        if (lane == 0) st_relaxed_u64(a.tile_state, kFlagPrefix | agg);
+        return 0;
+    }
+    if (lane == 0) st_relaxed_u64(a.tile_state + tile, kFlagAgg | agg);
+    int base = (int)tile - 1;
+    while (true) {
+        const int j = base - lane;
+        const unsigned long long v = j >= 0 ? ld_relaxed_u64(a.tile_state + j) : kFlagPrefix;
+        const unsigned long long f = v & ~kValMask;
+        const uint32_t bP = __ballot_sync(0xffffffffu, f == kFlagPrefix);
+        const uint32_t bZ = __ballot_sync(0xffffffffu, f == 0);
+        const int lim = bP ? __ffs(bP) - 1 : 31;
+        const uint32_t need = lim == 31 ? 0xffffffffu : ((2u << lim) - 1);
+        if (bZ & need) continue;
+        unsigned long long part = lane <= lim ? (v & kValMask) : 0ull;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) part += __shfl_down_sync(0xffffffffu, part, d);
+        excl += __shfl_sync(0xffffffffu, part, 0);
+        if (bP) break;
+        base -= 32;
+    }
+    if (lane == 0) st_relaxed_u64(a.tile_state + tile, kFlagPrefix | (excl + agg));
+    return excl;
+}
+
+// one method's records (best-only; destinations bdc / bdp gated already) from
+// its packed used list; destinations ascending, suggest_all's tags
+__device__ __noinline__ void emit_best(const SweepArgs& a, uint32_t pos, uint32_t o, uint32_t hdr, const uint32_t* ent,
+                                       uint32_t n, uint32_t bdc, uint32_t bdp, bool inter, uint64_t at) {
+    const uint32_t p = __ldg(a.s.cls_methods + pos);
+    const ClassRec ro = load_rec(a.rec, o);
+    const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
+                                                       : removed_from_list(ro, a.ux, a.un, a.dense, a.s.C, ent, n, o);
+    const Origin org = make_origin(ro, rec_hown(hdr), removed);
+    uint32_t ds[2];
+    int nd = 0;
+    if (inter) {
+        ds[nd++] = bdc;  // bdc == bdp here
+    } else {
+        const uint32_t x = bdc < bdp ? bdc : bdp, y = bdc < bdp ? bdp : bdc;  // kNone sorts last
+        if (x != kNone) ds[nd++] = x;
+        if (y != kNone && y != x) ds[nd++] = y;
+    }
+    for (int i = 0; i < nd; ++i) {
+        const uint32_t d = ds[i];
+        uint32_t hd = 0;
+        for (uint32_t k = 0; k < n; ++k)
+            if ((ent[k] >> 8) == d) hd = ent[k] & 0xffu;
+        const ClassRec rd = load_rec(a.rec, d);
+        uint32_t miss = 0;
+        for (uint32_t k = 0; k < n; ++k) {
+            const uint32_t X = ent[k] >> 8;
+            if (X != d && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ++miss;
+        }
+        mm_suggestion r;
+        r.lcom_origin_before = org.lo_b;
+        r.lcom_origin_after = org.lo_a;
+        r.lcom_dest_before = lcom_of(rd.A, rd.M, rd.H);
+        r.lcom_dest_after = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
+        r.method = p;
+        r.origin = o;
+        r.destination = d;
+        r.cbo_origin_before = org.co_b;
+        r.cbo_origin_after = org.co_a;
+        r.cbo_dest_before = rd.cbo;
+        r.cbo_dest_after = rd.cbo + miss;
+        r.criteria = (uint8_t)((d == bdc ? MM_CRIT_COHESION : 0u) | (d == bdp ? MM_CRIT_COUPLING : 0u));
+        r.origin_degenerate_after = org.odeg;
+        r.dest_degenerate_after = rd.A == 0;
+        r.pad = 0;
+        store_record(a.out + at + i, r);
+    }
+}
+
+// the same for a method whose used list overflowed its record (streaming list)
+__device__ __noinline__ void emit_best_stream(const SweepArgs& a, uint32_t pos, uint32_t o, uint32_t bdc,
+                                              uint32_t bdp, uint64_t at) {
+    const uint32_t p = __ldg(a.s.cls_methods + pos);
+    StreamEnum sen;
+    sen.S.init(a.s, p);
+    const ClassRec ro = load_rec(a.rec, o);
+    const Origin org = make_origin(ro, sen.hits(o), removed_count(ro, a.ux, a.un, a.dense, a.s.C, sen, o));
+    MethodResult res{};
+    res.bd_coh = bdc;
+    res.bd_coup = bdp;
+    emit(a, sen, p, o, org, res, at);
+}
+
+__global__ void __launch_bounds__(kSweepTile, 4) k_sweep_best(SweepArgs a) {
+    __shared__ ScreenSmem sm;
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_warp[kScreenWarps], s_red[2][kScreenWarps];
+    __shared__ unsigned long long s_excl;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)tile * kSweepTile + threadIdx.x;
+    const bool live = pos < a.pos_end;
+    uint32_t (*ent)[kRecMaxEnt] = sm.ent[warp];
+    uint8_t* cm = sm.cm[warp];
+    uint8_t* ck = sm.ck[warp];
+    double* kc = sm.kc[warp];
+    uint32_t* kp = sm.kp[warp];
+
+    // ---- screen (as k_screen)
+    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
+    uint32_t o = 0, hdr = 0;
+    if (live) {
+        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
+        r0 = rp[0];
+        r1 = rp[1];
+        hdr = rec_hdrs(a.recs, a.s.M)[pos];
+        o = __ldg(a.pos_owner + pos);
+    }
+    const bool ovf = live && (hdr & kRecOverflow);
+    const uint32_t n = (live && !ovf) ? rec_n(hdr) : 0u;
+    {
+        const uint32_t e8[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k) ent[lane][k] = e8[k];
+    }
+    uint32_t nc = 0;
+#pragma unroll
+    for (int k = 0; k < kRecMaxEnt; ++k) nc += (k < (int)n && (ent[lane][k] >> 8) != o);
+    bool coh_ok = false, can_coup = false;
+    double lo_a = 0.0;
+    if (n) {
+        const ClassRec ro = load_rec(a.rec, o);
+        const uint32_t h = rec_hown(hdr);
+        const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
+                                                           : removed_from_list(ro, a.ux, a.un, a.dense, a.s.C,
+                                                                               ent[lane], n, o);
+        can_coup = removed > 0;
+        bool maybe = ro.A != 0 && ro.M != 0;
+        if (maybe && ro.M >= 2 && (uint64_t)ro.A * ro.M < kExact53) maybe = (uint64_t)h * ro.M < ro.H;
+        if (maybe) {
+            lo_a = lcom_of(ro.A, (uint64_t)ro.M - 1, (uint64_t)ro.H - h);
+            coh_ok = lo_a < __ldg(a.dlcom + o);
+        }
+    }
+    uint32_t incl = nc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+    }
+    const uint32_t excl_c = incl - nc;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    {
+        uint32_t w = excl_c;
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k)
+            if (k < (int)n && (ent[lane][k] >> 8) != o) {
+                cm[w] = (uint8_t)lane;
+                ck[w] = (uint8_t)k;
+                ++w;
+            }
+    }
+    const uint32_t flags = (coh_ok ? 1u : 0u) | (can_coup ? 2u : 0u);
+    __syncwarp();
+    for (uint32_t c0 = 0; c0 < total; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        const bool act = c < total;
+        const uint32_t m = act ? cm[c] : 0u;
+        const uint32_t mflags = __shfl_sync(0xffffffffu, flags, m);
+        const double m_lo_a = __shfl_sync(0xffffffffu, lo_a, m);
+        const uint32_t m_n = __shfl_sync(0xffffffffu, n, m);
+        if (!act) continue;
+        const uint32_t e = ent[m][ck[c]];
+        const uint32_t d = e >> 8, hd = e & 0xffu;
+        double key = -1.0;
+        uint32_t kpv = kNone;
+        if (mflags) {
+            const ClassRec rd = load_rec(a.rec, d);
+            if ((mflags & 1u) && rd.A != 0 && rd.M != 0) {
+                const bool exact = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
+                if (!exact || (uint64_t)hd * rd.M > rd.H) {
+                    const double ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
+                    if (ld_a < __ldg(a.dlcom + d)) key = __dadd_rn(m_lo_a, ld_a);
+                }
+            }
+            if (mflags & 2u) {
+                bool ok = true;
+                for (uint32_t j = 0; j < m_n && ok; ++j) {
+                    const uint32_t X = ent[m][j] >> 8;
+                    if (X != d && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ok = false;
+                }
+                if (ok) kpv = rd.cbo;
+            }
+        }
+        kc[c] = key;
+        kp[c] = kpv;
+    }
+    __syncwarp();
+    uint32_t bdc = kNone, bdp = kNone;
+    {
+        double bk = 0.0;
+        uint32_t bp = 0;
+        for (uint32_t j = 0; j < nc; ++j) {
+            const uint32_t slot = excl_c + j;
+            const double kcv = kc[slot];
+            const uint32_t kpv = kp[slot];
+            if (kcv >= 0.0 || kpv != kNone) {
+                const uint32_t dd = ent[lane][ck[slot]] >> 8;
+                if (kcv >= 0.0 && (bdc == kNone || kcv < bk)) { bdc = dd; bk = kcv; }
+                if (kpv != kNone && (bdp == kNone || kpv < bp)) { bdp = dd; bp = kpv; }
+            }
+        }
+    }
+    __syncwarp();
+    uint32_t cands = nc;
+    {
+        const uint4 ov = screen_overflow(a, ovf, pos, reinterpret_cast<uint32_t*>(kc), lane);
+        if (ovf) { bdc = ov.x; bdp = ov.y; cands = ov.z; }
+    }
+    // ---- gates and the criteria merge
+    double thr_l = a.thr_lcom, thr_c = a.thr_cbo;
+    if (a.thr_device) { thr_l = a.dthr->lcom; thr_c = a.dthr->cbo; }
+    const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
+    const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
+    uint32_t count = 0;
+    unsigned long long gated = 0;
+    if (live) {
+        const bool gcoh = (a.crit & MM_CRIT_COHESION) && __ldg(a.lcom + o) > thr_l;
+        const bool gcoup = (a.crit & MM_CRIT_COUPLING) && (double)__ldg(a.cbo + o) > thr_c;
+        gated = (unsigned long long)cands * ((gcoh ? 1u : 0u) + (gcoup ? 1u : 0u));
+        if (!gcoh) bdc = kNone;
+        if (!gcoup) bdp = kNone;
+        const bool same = bdc != kNone && bdc == bdp;
+        count = inter ? (same ? 1u : 0u) : (uint32_t)(bdc != kNone) + (uint32_t)(bdp != kNone) - (same ? 1u : 0u);
+    }
+    // ---- CTA scan of (emitters << 32 | records), look-back, publish
+    const unsigned long long mine = count + (count ? (1ull << 32) : 0ull);
+    unsigned long long inc = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    {
+        unsigned long long g0 = gated, g1 = cands;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            g0 += __shfl_down_sync(0xffffffffu, g0, d);
+            g1 += __shfl_down_sync(0xffffffffu, g1, d);
+        }
+        if (lane == 0) { s_red[0][warp] = g0; s_red[1][warp] = g1; }
+    }
+    __syncthreads();
+    unsigned long long before = 0, agg = 0;
+#pragma unroll
+    for (int w = 0; w < kScreenWarps; ++w) {
+        if (w < warp) before += s_warp[w];
+        agg += s_warp[w];
+    }
+    if (warp == 0) {
+        const unsigned long long ex = tile_lookback(a, tile, agg, lane);
+        if (lane == 0) {
+            s_excl = ex;
+            unsigned long long t0 = 0, t1 = 0;
+            for (int w = 0; w < kScreenWarps; ++w) { t0 += s_red[0][w]; t1 += s_red[1][w]; }
+            if (t1) atomicAdd(a.stats + 0, t1);
+            if (t0) atomicAdd(a.stats + 1, t0);
+            if (agg & 0xffffffffull) atomicAdd(a.stats + 2, agg & 0xffffffffull);
+            const uint64_t t0pos = (uint64_t)a.pos_begin + (uint64_t)tile * kSweepTile;
+            const uint64_t rest = a.pos_end > t0pos ? a.pos_end - t0pos : 0;
+            const uint64_t nvalid = rest < kSweepTile ? rest : (uint64_t)kSweepTile;
+            atomicAdd(a.stats + 3, (unsigned long long)nvalid);
+            atomicAdd(a.n_emit, (uint32_t)(agg >> 32));
+        }
+    }
+    __syncthreads();
+    // ---- records (the tile's prefix is already published)
+    if (count) {
+        const uint64_t at = (s_excl + before + inc - mine) & 0xffffffffull;
+        if (!ovf) emit_best(a, (uint32_t)pos, o, hdr, ent[lane], n, bdc, bdp, inter, at);
+        else emit_best_stream(a, (uint32_t)pos, o, bdc, bdp, at);
+    }
 }
 
 // Pass 2: apply the class gates (suggest.hpp:246, :273) and the criteria
@@ -1323,6 +1633,11 @@ __global__ void __launch_bounds__(kSweepTile) k_sim_emit(SweepArgs a, SimCrit sc
 }
 
 }  // namespace
+
+void launch_sweep_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
+    if (!n_tiles) return;
+    k_sweep_best<<<n_tiles, kSweepTile, 0, st>>>(a);
+}
 
 void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st) {
     if (!n_tiles) return;

@@ -168,6 +168,7 @@ struct mm_ctx {
     bool no_screen = false;   // env MMGPU_NO_SCREEN=1: best-only mode on the per-thread kernel (A/B)
     bool thr_side = false;    // env MMGPU_THR_SIDE=1: threshold means on the side stream
     uint32_t screen_variant = 2;  // env MMGPU_SCREEN (A/B of the best-only screen)
+    bool fused_best = true;       // env MMGPU_FUSED=0: best-only mode as screen + offsets + write
     DBuf<double> gate_lcom;
     DBuf<uint32_t> gate_cbo;
     bool gates_set = false;
@@ -390,6 +391,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     if (const char* v = std::getenv("MMGPU_NO_SCREEN")) ctx->no_screen = v[0] == '1';
     if (const char* v = std::getenv("MMGPU_THR_SIDE")) ctx->thr_side = v[0] == '1';
     if (const char* v = std::getenv("MMGPU_SCREEN")) ctx->screen_variant = (uint32_t)std::strtoul(v, nullptr, 10);
+    if (const char* v = std::getenv("MMGPU_FUSED")) ctx->fused_best = v[0] != '0';
     *out = ctx;
     return MM_OK;
 }
@@ -1333,7 +1335,10 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     MM_CUDA(ctx, ctx->out.ensure(cap));
     const uint32_t n_tiles = (uint32_t)((npos + kSweepTile - 1) / kSweepTile);
     const uint32_t n_off = offsets_tiles(npos);
-    MM_CUDA(ctx, ctx->tile_state.ensure(n_off ? n_off : 1));
+    // best-only mode runs fused (screen + gates + offsets + records in one pass)
+    const bool fused = mode == 0 && !ctx->no_screen && ctx->fused_best;
+    const uint32_t n_state = fused ? n_tiles : n_off;
+    MM_CUDA(ctx, ctx->tile_state.ensure(n_state ? n_state : 1));
     MM_CUDA(ctx, ctx->res.ensure(npos ? npos : 1));
     MM_CUDA(ctx, ctx->emit_list.ensure(npos ? npos : 1));
     const void* wide_before = ctx->wide_cnt.p;
@@ -1348,7 +1353,7 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
         before[3] != ctx->emit_list.p)
         ++ctx->layout_gen;
     Ctl* ctl = ctx->ctl.p;
-    if (n_off) MM_CUDA(ctx, cudaMemsetAsync(ctx->tile_state.p, 0, 8ull * n_off, ctx->stream));
+    if (n_state) MM_CUDA(ctx, cudaMemsetAsync(ctx->tile_state.p, 0, 8ull * n_state, ctx->stream));
     // tile_counter, err, n_emit, n_wide, n_fallback, n_hideg (rezeroed: unused here), stats
     MM_CUDA(ctx, cudaMemsetAsync(&ctl->tile_counter, 0, offsetof(Ctl, thr) - offsetof(Ctl, tile_counter),
                                  ctx->stream));
@@ -1388,6 +1393,19 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     a.n_fallback = &ctl->n_fallback;
     a.no_screen = ctx->no_screen ? 1u : 0u;
     a.screen_variant = ctx->screen_variant;
+    if (fused) {
+        if (a.thr_device)
+            if (mm_status s2 = join_thresholds(ctx)) return s2;
+        mm_status st = run(ctx, "sweep_best", [&] { launch_sweep_best(a, n_tiles, ctx->stream); });
+        if (st) return st;
+        ctx->sweep_valid = true;
+        if (n_out) {
+            mm_sweep_stats ss;
+            if (mm_status s2 = mm_sweep_stats_get(ctx, &ss)) return s2;
+            *n_out = ss.suggestions;
+        }
+        return MM_OK;
+    }
     mm_status st = run(ctx, "score", [&] { launch_score(a, n_tiles, fallback_tiles, ctx->stream); });
     if (st) return st;
     if (a.thr_device)

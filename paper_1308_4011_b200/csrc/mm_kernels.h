@@ -122,6 +122,8 @@ size_t thresholds_scratch_bytes(uint32_t n);
 cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
                               void* scratch, size_t scratch_bytes, cudaStream_t st, bool allow_serial = true);
 void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st);
+// best-only mode in one pass (screen + gates + offsets + records); thresholds must be ready
+void launch_sweep_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 uint32_t offsets_tiles(uint64_t npos);
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
