@@ -56,6 +56,19 @@ def build_lib(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variant(name: str, defines) -> Path:
+    """A/B build of the same sources with extra -D flags (development only):
+    paper_1308_4011_b200/_variants/libmmgpu_<name>.so, selected at run time by
+    MMGPU_LIB=<path> (the product is always libmmgpu.so)."""
+    out = PKG / "_variants" / f"libmmgpu_{name}.so"
+    out.parent.mkdir(exist_ok=True)
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", str(out), *map(str, _sources())]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(res.stdout + res.stderr)
+    return out
+
+
 def build_oracle() -> None:
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
 

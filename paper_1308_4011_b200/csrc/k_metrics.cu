@@ -134,6 +134,37 @@ __global__ void k_expand(DevModel s, uint32_t* __restrict__ mo_out, uint32_t* __
     }
 }
 
+// Upload-time layout: the call / access rows in class order. Degrees by
+// position (then an exclusive scan gives the offsets), then one thread per
+// position copies its row. Indices are bounds-checked (runs before the
+// validation verdict is known).
+__global__ void k_pos_degrees(DevModel s, uint32_t* __restrict__ dc, uint32_t* __restrict__ da) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > s.M) return;
+    if (k == s.M) { dc[k] = 0; da[k] = 0; return; }
+    const uint32_t p = s.cls_methods[k];
+    const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
+    if (p >= s.M) { dc[k] = 0; da[k] = 0; return; }
+    const uint32_t cb = min(s.call_off[p], Ec), ce = min(max(s.call_off[p + 1], cb), Ec);
+    const uint32_t ab = min(s.acc_off[p], Ea), ae = min(max(s.acc_off[p + 1], ab), Ea);
+    dc[k] = ce - cb;
+    da[k] = ae - ab;
+}
+
+__global__ void k_pos_rows(DevModel s, uint32_t* __restrict__ pc_tgt, uint32_t* __restrict__ pa_tgt) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= s.M) return;
+    const uint32_t p = s.cls_methods[k];
+    if (p >= s.M) return;
+    const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
+    const uint32_t cb = min(s.call_off[p], Ec), ce = min(max(s.call_off[p + 1], cb), Ec);
+    const uint32_t ab = min(s.acc_off[p], Ea), ae = min(max(s.acc_off[p + 1], ab), Ea);
+    uint32_t o = s.pc_off[k];
+    for (uint32_t e = cb; e < ce && o < Ec; ++e) pc_tgt[o++] = s.call_tgt[e];
+    o = s.pa_off[k];
+    for (uint32_t e = ab; e < ae && o < Ea; ++e) pa_tgt[o++] = s.acc_tgt[e];
+}
+
 // classify into the warp path (small) or the CTA path (large)
 __global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg, const uint32_t* __restrict__ foreign,
                                uint4* __restrict__ cplan, uint32_t* __restrict__ large_list,
@@ -179,9 +210,8 @@ k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask
         const bool live = pos < s.M;
         uint32_t nch = 0;
         if (live) {
-            const uint32_t q = __ldg(s.cls_methods + pos);
-            const uint32_t d = (__ldg(s.call_off + q + 1) - __ldg(s.call_off + q)) +
-                               (__ldg(s.acc_off + q + 1) - __ldg(s.acc_off + q));
+            const uint32_t d = (__ldg(s.pc_off + pos + 1) - __ldg(s.pc_off + pos)) +
+                               (__ldg(s.pa_off + pos + 1) - __ldg(s.pa_off + pos));
             nch = (d + K - 1) / K;
         }
         if (threadIdx.x < kChunkBuckets) s_cnt[threadIdx.x] = 0;
@@ -209,10 +239,10 @@ k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask
         }
     }
     if (pos >= s.M) return;
-    const uint32_t p = __ldg(s.cls_methods + pos);
     const uint32_t own = __ldg(pos_owner + pos);
-    const uint32_t cb = __ldg(s.call_off + p), ce = __ldg(s.call_off + p + 1);
-    const uint32_t ab = __ldg(s.acc_off + p), ae = __ldg(s.acc_off + p + 1);
+    // this position's rows, laid out in class order at upload: coalesced
+    const uint32_t cb = __ldg(s.pc_off + pos), ce = __ldg(s.pc_off + pos + 1);
+    const uint32_t ab = __ldg(s.pa_off + pos), ae = __ldg(s.pa_off + pos + 1);
     const uint32_t oab = __ldg(s.cls_aoff + own), oae = __ldg(s.cls_aoff + own + 1);
     uint32_t hdr = kRecOverflow;
     uint32_t ent[kRecMaxEnt];
@@ -236,7 +266,7 @@ k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask
         for (int k = 0; k < K; ++k) {
             const uint32_t e = e0 + k;
             const bool isc = e < nc, isa = !isc && e < deg;
-            tg[k] = isc ? __ldg(s.call_tgt + cb + e) : (isa ? __ldg(s.acc_tgt + ab + (e - nc)) : 0u);
+            tg[k] = isc ? __ldg(s.pc_tgt + cb + e) : (isa ? __ldg(s.pa_tgt + ab + (e - nc)) : 0u);
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -1015,6 +1045,17 @@ void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cp
     k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, cmaxdeg, foreign, cplan, large_list, n_large, big_list,
                                                        n_big, max_deg);
 }
+void launch_pos_rows(const DevModel& s, uint32_t* pc_off, uint32_t* pc_tgt, uint32_t* pa_off, uint32_t* pa_tgt,
+                     uint32_t* totals, uint32_t* grand, cudaStream_t st) {
+    k_pos_degrees<<<(s.M + 1 + 255) / 256, 256, 0, st>>>(s, pc_off, pa_off);
+    launch_scan(pc_off, pc_off, s.M + 1, totals, grand, st);
+    launch_scan(pa_off, pa_off, s.M + 1, totals, grand, st);
+    DevModel t = s;
+    t.pc_off = pc_off;
+    t.pa_off = pa_off;
+    if (s.M) k_pos_rows<<<(s.M + 255) / 256, 256, 0, st>>>(t, pc_tgt, pa_tgt);
+}
+
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
                    uint32_t max_deg, cudaStream_t st) {
     if (!s.M) return;

@@ -132,14 +132,41 @@ __device__ __forceinline__ Origin make_origin(const ClassRec& ro, uint32_t ho, u
     return g;
 }
 
+// The origin for scoring only (best / top-k / all-passing decisions): the
+// exact-rational pre-test decides "lcom(origin) cannot drop" without a
+// division (A == 0, or M ≥ 2 with exact denominators and H ≤ h·M); otherwise
+// lo_a by the reference's formula and lo_b = lcom[o] from the metric pass
+// (the same double). Emission uses make_origin (every field exact).
+__device__ __forceinline__ Origin make_origin_score(const ClassRec& ro, uint32_t ho, uint32_t removed,
+                                                   const double* __restrict__ dlcom, uint32_t o) {
+    Origin g;
+    g.ro = ro;
+    g.lo_b = 0.0;
+    g.lo_a = 0.0;
+    g.coh_ok = false;
+    bool maybe = ro.A != 0 && ro.M != 0;
+    if (maybe && ro.M >= 2 && (uint64_t)ro.A * ro.M < kExact53) maybe = (uint64_t)ho * ro.M < ro.H;
+    if (maybe) {
+        g.lo_a = lcom_of(ro.A, (uint64_t)ro.M - 1, (uint64_t)ro.H - ho);
+        g.lo_b = __ldg(dlcom + o);
+        g.coh_ok = g.lo_a < g.lo_b;
+    }
+    g.co_b = ro.cbo;
+    g.co_a = ro.cbo - removed;
+    g.odeg = ro.M <= 1 || ro.A == 0;
+    return g;
+}
+
 // lcom(A_d, M_d+1, H_d+h) < lcom(A_d, M_d, H_d): integer pre-test h·M > H
 // (q_after > q_before), doubles only when it holds.
-__device__ __forceinline__ bool coh_dest(const ClassRec& rd, uint32_t h, double& ld_a) {
+__device__ __forceinline__ bool coh_dest(const ClassRec& rd, uint32_t h, double& ld_a,
+                                         const double* __restrict__ dlcom = nullptr, uint32_t d = 0) {
     if (rd.A == 0 || rd.M == 0) return false;  // before is 0.0 (degenerate): nothing is < 0
     const bool exact_denoms = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
     if (exact_denoms && !((uint64_t)h * rd.M > rd.H)) return false;
     ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + h);
-    return ld_a < lcom_of(rd.A, rd.M, rd.H);
+    // lcom_dest_before: the metric pass's lcom[d] (the same double) when given
+    return ld_a < (dlcom ? __ldg(dlcom + d) : lcom_of(rd.A, rd.M, rd.H));
 }
 
 // X ∈ U[d]? Exact bitmap for dense rows; else the Bloom signature (a clear
@@ -234,7 +261,7 @@ __device__ __forceinline__ void score(const SweepArgs& a, const E& en, const Ori
     if (!org.coh_ok && org.co_a >= org.co_b) return;  // neither criterion can pass
     const ClassRec rd = load_rec(a.rec, d);
     double ld_a;
-    if (org.coh_ok && coh_dest(rd, hd, ld_a)) {
+    if (org.coh_ok && coh_dest(rd, hd, ld_a, a.dlcom, d)) {
         pcoh = true;
         kcoh = __dadd_rn(org.lo_a, ld_a);  // lcom_key, suggest.hpp:194-196
     }
@@ -471,7 +498,7 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 // Fills `ren` (shared-memory list) or `sen` (streaming) with method p's used
 // list and returns the origin-side values. Record path when the method pass
 // could pack the list; CSR otherwise.
-template <int K>
+template <int K, bool SCORE = false>
 __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, uint32_t p, uint32_t o,
                                             SmemEnum& ren, StreamEnum& sen, Origin& org) {
     const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
@@ -487,7 +514,7 @@ __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, ui
         ren.n = (int)n;
         const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
                                                            : removed_count(ro, a.ux, a.un, a.dense, a.s.C, ren, o);
-        org = make_origin(ro, rec_hown(hdr), removed);
+        org = SCORE ? make_origin_score(ro, rec_hown(hdr), removed, a.dlcom, o) : make_origin(ro, rec_hown(hdr), removed);
         return true;
     }
     if (ren.build(a.s, p, K)) {  // ≤ K distinct classes (any degree): shared-memory list
@@ -527,7 +554,7 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
         StreamEnum sen;
         Origin org;
         MethodResult r;
-        if (load_method<K>(a, (uint32_t)pos, p, o, ren, sen, org)) r = evaluate(a, ren, o, org, true, true);
+        if (load_method<K, true>(a, (uint32_t)pos, p, o, ren, sen, org)) r = evaluate(a, ren, o, org, true, true);
         else r = evaluate(a, sen, o, org, true, true);
         cands = r.cands;
         uint4 out;

@@ -161,12 +161,13 @@ struct mm_ctx {
     uint64_t sim_n = 0;
     bool sim_valid = false;
     DBuf<uint32_t> pos_owner;
+    DBuf<uint32_t> pc_off, pc_tgt, pa_off, pa_tgt, pos_scan;  // dependency rows in class order (+ scan scratch)
     DBuf<uint4> res;
     DBuf<uint4> emit_list;  // compact emitter records (k_offsets -> k_write)
     DBuf<uint4> wide_cnt;  // top-k / all-candidates: pass counts of methods with >= 32 used classes
     DBuf<uint32_t> fallback;  // best-only screen: record-overflow positions
-    bool no_screen = false;   // env MMGPU_NO_SCREEN=1: best-only mode on the per-thread kernel (A/B)
-    bool thr_side = false;    // env MMGPU_THR_SIDE=1: threshold means on the side stream
+    bool no_screen = true;    // env MMGPU_NO_SCREEN=0: best-only mode on the flattened screen (A/B; slower in situ)
+    bool thr_side = true;     // env MMGPU_THR_SIDE=0: threshold means on the main stream, ahead of the sweep
     uint32_t screen_variant = 2;  // env MMGPU_SCREEN (A/B of the best-only screen)
     bool fused_best = true;       // env MMGPU_FUSED=0: best-only mode as screen + offsets + write
     DBuf<double> gate_lcom;
@@ -199,6 +200,8 @@ struct mm_ctx {
         s.call_off = call_off.p; s.call_tgt = call_tgt.p;
         s.acc_off = acc_off.p; s.acc_tgt = acc_tgt.p;
         s.attr_info = attr_info.p;
+        s.pc_off = pc_off.p; s.pc_tgt = pc_tgt.p;
+        s.pa_off = pa_off.p; s.pa_tgt = pa_tgt.p;
         return s;
     }
 };
@@ -293,6 +296,7 @@ void free_model(mm_ctx* c) {
     c->simc_u32.release();
     c->simc_out.release();
     c->pos_owner.release();
+    for (DBuf<uint32_t>* b : {&c->pc_off, &c->pc_tgt, &c->pa_off, &c->pa_tgt, &c->pos_scan}) b->release();
     c->cplan.release();
     c->big_list.release();
     c->plans.release();
@@ -388,8 +392,8 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     if (const char* v = std::getenv("MMGPU_HIST_MAX_BYTES")) ctx->hist_max_bytes = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_GIANT_MIN")) ctx->giant_min = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_CK_MMA_MIN")) ctx->ck_mma_min = std::strtoull(v, nullptr, 10);
-    if (const char* v = std::getenv("MMGPU_NO_SCREEN")) ctx->no_screen = v[0] == '1';
-    if (const char* v = std::getenv("MMGPU_THR_SIDE")) ctx->thr_side = v[0] == '1';
+    if (const char* v = std::getenv("MMGPU_NO_SCREEN")) ctx->no_screen = v[0] != '0';
+    if (const char* v = std::getenv("MMGPU_THR_SIDE")) ctx->thr_side = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_SCREEN")) ctx->screen_variant = (uint32_t)std::strtoul(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_FUSED")) ctx->fused_best = v[0] != '0';
     *out = ctx;
@@ -573,6 +577,17 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         return st;
     MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[0], vs));
     MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[0], 0));
+    // the dependency rows in class order (the method pass streams them)
+    MM_CUDA(ctx, ctx->pc_off.ensure(M + 1ull));
+    MM_CUDA(ctx, ctx->pa_off.ensure(M + 1ull));
+    MM_CUDA(ctx, ctx->pc_tgt.ensure(Ec ? Ec : 1));
+    MM_CUDA(ctx, ctx->pa_tgt.ensure(Ea ? Ea : 1));
+    MM_CUDA(ctx, ctx->pos_scan.ensure((M + 1ull + 1023) / 1024 + 2));
+    st = run(ctx, "upload_rows", [&] {
+        launch_pos_rows(ctx->dev(), ctx->pc_off.p, ctx->pc_tgt.p, ctx->pa_off.p, ctx->pa_tgt.p, ctx->pos_scan.p,
+                        ctx->pos_scan.p + (M + 1ull + 1023) / 1024 + 1, ctx->stream);
+    });
+    if (st) return st;
 
     // class plan (bounds-checked, so it is safe on a model validation rejects):
     // warp path vs CTA path, scratch for the CTA path. One sync for both.

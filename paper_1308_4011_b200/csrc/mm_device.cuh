@@ -41,6 +41,13 @@ struct DevModel {
     const uint32_t* __restrict__ acc_off;
     const uint32_t* __restrict__ acc_tgt;
     const uint2* __restrict__ attr_info;  // derived at upload: (owner, position in the owner's attribute list)
+    // the dependency rows again, in class order (row k = the method at
+    // class-order position k), laid out at upload so the method pass streams
+    // them coalesced: offsets [M+1], targets [E]
+    const uint32_t* __restrict__ pc_off;
+    const uint32_t* __restrict__ pc_tgt;
+    const uint32_t* __restrict__ pa_off;
+    const uint32_t* __restrict__ pa_tgt;
 };
 
 constexpr int kSigWords = 10;               // 320-bit Bloom signature

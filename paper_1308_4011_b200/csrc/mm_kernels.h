@@ -69,6 +69,9 @@ void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, u
 void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint32_t* large_list,
                          uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,
                          uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st);
+// upload: the dependency rows in class order (DevModel::pc_* / pa_*)
+void launch_pos_rows(const DevModel& s, uint32_t* pc_off, uint32_t* pc_tgt, uint32_t* pa_off, uint32_t* pa_tgt,
+                     uint32_t* totals, uint32_t* grand, cudaStream_t st);
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
                    uint32_t max_deg, cudaStream_t st);
 void launch_class_small(const DevModel& s, const uint4* cplan, const uint32_t* big_list, uint32_t n_big,
