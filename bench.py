@@ -93,14 +93,27 @@ def algorithmic_bytes(sys_, nnz_u: int, n_sugg: int, rank_share: float = 1.0) ->
     large = (msz > 32) | (asz > 64) | (maxdeg > 16)
     m_l, c_l, a_l = int(msz[large].sum()), int(large.sum()), int(asz[large].sum())
     e_l = int(deg[sys_.class_methods][np.repeat(large, msz)].sum())
+    c_lean = c - c_l  # (the listed warp-path classes are counted as lean here: a small share)
+    m_lean, a_lean = m - m_l, a - a_l
+    e_lean = E - e_l
     k = {
+        # fused method + class pass of the lean classes: plan + edge ranges,
+        # edge targets + member bytes, owner tables, records + headers, class
+        # records + metrics, U rows
+        "class_lean": 32 * c_lean + 5 * e_lean + 4 * m_lean + 8 * a_lean + 36 * m_lean + 84 * c_lean + 8 * nnz_u,
+        # the same outputs from groups of lean classes per warp: plan, member
+        # rows (offsets + class), edge targets, owner tables, records +
+        # headers, class records + metrics, U rows
+        "class_group": 16 * c_lean + 12 * m_lean + 4 * e_lean + 4 * m_lean + 8 * a_lean + 36 * m_lean
+        + 84 * c_lean + 8 * nnz_u,
         "class_large": 36 * m_l + 8 * e_l + 8 * a_l + 93 * c_l + 8 * nnz_u,
         "method": 64 * m + 8 * a + 4 * E + 4 * c,
         "class_small": 44 * m + 93 * c + 8 * nnz_u,
         "thresholds": 12 * c,
         "score": 56 * ms + 64 * c + 4 * nnz_u,
         "offsets": 36 * ms + 12 * c,
-        "write": 20 * ms + 96 * n_sugg,
+        # emitters, method records, class records (origin + destination), records
+        "write": 16 * n_sugg + 36 * n_sugg + 48 * n_sugg + 64 * n_sugg,
     }
     # the class pass: the warp path and the CTA-path tiers, concurrent on their streams
     k["class_pass"] = k["class_large"] + k["class_small"] - 8 * nnz_u
@@ -453,7 +466,11 @@ def run_ours(args) -> None:
                 "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s"}
-    recompute_us = sum(kern.get(k, {}).get("avg_us", 0.0) for k in ("method", "class_pass"))
+    # the metric pass: the lean-class kernel runs beside method + class pass when
+    # both kinds of class exist, ahead of the class pass when every class is lean
+    t_lean = kern.get("class_lean", {}).get("avg_us", 0.0)
+    t_rest = sum(kern.get(k, {}).get("avg_us", 0.0) for k in ("method", "class_pass"))
+    recompute_us = max(t_lean, t_rest) if "method" in kern else t_lean + t_rest
 
     # e2e through the public API: pinned host CSR -> H2D upload -> pass -> sweep -> D2H results
     e2e = None

@@ -151,23 +151,29 @@ __global__ void k_pos_degrees(DevModel s, uint32_t* __restrict__ dc, uint32_t* _
     da[k] = ae - ab;
 }
 
-__global__ void k_pos_rows(DevModel s, uint32_t* __restrict__ pc_tgt, uint32_t* __restrict__ pa_tgt) {
+// also the member index of every class-order edge (position − first position
+// of its class, 255 past that), which the lean class kernel reads beside the
+// targets instead of searching the members' row starts
+__global__ void k_pos_rows(DevModel s, const uint32_t* __restrict__ pos_owner, uint32_t* __restrict__ pc_tgt,
+                           uint32_t* __restrict__ pa_tgt, uint8_t* __restrict__ pc_mem, uint8_t* __restrict__ pa_mem) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= s.M) return;
     const uint32_t p = s.cls_methods[k];
     if (p >= s.M) return;
+    const uint32_t oc = pos_owner[k];
+    const uint32_t mi = oc < s.C ? min(k - min(s.cls_moff[oc], k), 255u) : 255u;
     const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
     const uint32_t cb = min(s.call_off[p], Ec), ce = min(max(s.call_off[p + 1], cb), Ec);
     const uint32_t ab = min(s.acc_off[p], Ea), ae = min(max(s.acc_off[p + 1], ab), Ea);
     uint32_t o = s.pc_off[k];
-    for (uint32_t e = cb; e < ce && o < Ec; ++e) pc_tgt[o++] = s.call_tgt[e];
+    for (uint32_t e = cb; e < ce && o < Ec; ++e) { pc_mem[o] = (uint8_t)mi; pc_tgt[o++] = s.call_tgt[e]; }
     o = s.pa_off[k];
-    for (uint32_t e = ab; e < ae && o < Ea; ++e) pa_tgt[o++] = s.acc_tgt[e];
+    for (uint32_t e = ab; e < ae && o < Ea; ++e) { pa_mem[o] = (uint8_t)mi; pa_tgt[o++] = s.acc_tgt[e]; }
 }
 
 // classify into the warp path (small) or the CTA path (large)
 __global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg, const uint32_t* __restrict__ foreign,
-                               uint4* __restrict__ cplan, uint32_t* __restrict__ large_list,
+                               uint4* __restrict__ cplan, uint4* __restrict__ cedge, uint32_t* __restrict__ large_list,
                                uint32_t* __restrict__ n_large, uint32_t* __restrict__ big_list,
                                uint32_t* __restrict__ n_big, uint32_t* __restrict__ max_deg) {
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -181,6 +187,8 @@ __global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg,
     // register-sort variant, the rest the shared-memory one (listed)
     const uint32_t kind = !small ? kKindCta : (foreign[c] <= 32 ? kKindLean : kKindWarpBig);
     cplan[c] = make_uint4(mb, me - mb, A, kind);
+    // the class's edge ranges in the class-order rows
+    cedge[c] = make_uint4(s.pc_off[mb], s.pc_off[me], s.pa_off[mb], s.pa_off[me]);
     if (kind == kKindCta) large_list[atomicAdd(n_large, 1u)] = c;
     if (kind == kKindWarpBig) big_list[atomicAdd(n_big, 1u)] = c;
     atomicMax(max_deg, mdeg);
@@ -198,7 +206,7 @@ constexpr int kChunkBuckets = 8;  // k_method regrouping: 0..6 chunks, 7 = more 
 template <int K, bool REGROUP>
 __global__ void __launch_bounds__(256, 5)
 k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask,
-         const uint32_t* __restrict__ pos_owner) {
+         const uint32_t* __restrict__ pos_owner, const uint32_t* __restrict__ plist, uint32_t n_pos) {
     // Blocks holding methods of more than one chunk (dense shapes like C5)
     // first regroup their positions by chunk count (a counting sort in shared
     // memory), so a warp's threads loop the same number of chunks instead of
@@ -206,6 +214,7 @@ k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask
     // own position range (whole 32-byte records; L2 merges the masks).
     __shared__ uint32_t s_cnt[kChunkBuckets], s_perm[256];
     uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (plist) pos = pos < n_pos ? __ldg(plist + pos) : kNone;  // only the listed positions (non-lean classes)
     if (REGROUP) {
         const bool live = pos < s.M;
         uint32_t nch = 0;
@@ -1035,41 +1044,44 @@ void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, u
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((n1 + 255) / 256, 148 * 16);
     k_validate_offsets<<<blocks, 256, 0, st>>>(off, n1, total, bad);
 }
-void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint32_t* large_list,
+void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint4* cedge, uint32_t* large_list,
                          uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,
                          uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st) {
     if (!s.C) return;
     cudaMemsetAsync(foreign, 0, 4ull * s.C, st);
     cudaMemsetAsync(cmaxdeg, 0, 4ull * s.C, st);
     if (s.M) k_plan_methods<<<(s.M + 255) / 256, 256, 0, st>>>(s, pos_owner, foreign, cmaxdeg, n_hideg);
-    k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, cmaxdeg, foreign, cplan, large_list, n_large, big_list,
+    k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, cmaxdeg, foreign, cplan, cedge, large_list, n_large, big_list,
                                                        n_big, max_deg);
 }
-void launch_pos_rows(const DevModel& s, uint32_t* pc_off, uint32_t* pc_tgt, uint32_t* pa_off, uint32_t* pa_tgt,
-                     uint32_t* totals, uint32_t* grand, cudaStream_t st) {
+void launch_pos_rows(const DevModel& s, const uint32_t* pos_owner, uint32_t* pc_off, uint32_t* pc_tgt,
+                     uint32_t* pa_off, uint32_t* pa_tgt, uint8_t* pc_mem, uint8_t* pa_mem, uint32_t* totals,
+                     uint32_t* grand, cudaStream_t st) {
     k_pos_degrees<<<(s.M + 1 + 255) / 256, 256, 0, st>>>(s, pc_off, pa_off);
     launch_scan(pc_off, pc_off, s.M + 1, totals, grand, st);
     launch_scan(pa_off, pa_off, s.M + 1, totals, grand, st);
     DevModel t = s;
     t.pc_off = pc_off;
     t.pa_off = pa_off;
-    if (s.M) k_pos_rows<<<(s.M + 255) / 256, 256, 0, st>>>(t, pc_tgt, pa_tgt);
+    if (s.M) k_pos_rows<<<(s.M + 255) / 256, 256, 0, st>>>(t, pos_owner, pc_tgt, pa_tgt, pc_mem, pa_mem);
 }
 
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
-                   uint32_t max_deg, cudaStream_t st) {
-    if (!s.M) return;
-    const uint32_t blocks = (s.M + 255) / 256;
+                   uint32_t max_deg, const uint32_t* plist, uint32_t n_pos, cudaStream_t st) {
+    const uint32_t n = plist ? n_pos : s.M;
+    if (!n) return;
+    const uint32_t blocks = (n + 255) / 256;
     if (max_deg > 8)  // some method needs several chunks: regroup by chunk count
-        k_method<8, true><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
+        k_method<8, true><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner, plist, n_pos);
     else
-        k_method<8, false><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner);
+        k_method<8, false><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner, plist, n_pos);
 }
 void launch_class_small(const DevModel& s, const uint4* cplan, const uint32_t* big_list, uint32_t n_big,
                         MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck,
-                        uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st, cudaStream_t st_big) {
+                        uint32_t* cbo, uint32_t* ux, uint32_t* un, bool lean, cudaStream_t st, cudaStream_t st_big) {
     if (!s.C) return;
-    k_class_small<false><<<(s.C + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(
+    if (lean)
+        k_class_small<false><<<(s.C + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(
         s, cplan, nullptr, 0, recs, own_mask, rec, lcom, ck, cbo, ux, un);
     if (n_big)
         k_class_small<true><<<(n_big + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st_big>>>(

@@ -304,6 +304,11 @@ __device__ __forceinline__ int select_next(const SweepArgs& a, const E& en, uint
 constexpr uint32_t kMaskBits = 31;
 constexpr uint32_t kWideMark = 0x80000000u;  // res.x marker of a wide method (never a mask bit)
 constexpr int kTopMax = 8;
+// res.w of a best-only result whose method record is complete (entries,
+// own-access and removed counts): k_offsets writes its records itself;
+// 0 = k_write re-derives them from the CSR
+constexpr uint32_t kResFull = 1u << 31;
+constexpr uint32_t kEmitFast = 1u << 31;  // emitter list: written by k_write_best (positions < 2^31)
 
 // records of a top-k / all-candidates method from its pass counts under the
 // class gates: union = every gated pass, intersection = passes of both
@@ -538,10 +543,10 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
     __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
     uint64_t pos;
     bool live;
-    if (LIST) {  // the methods k_screen handed over (record overflow)
+    if (LIST) {  // a position list: a.plist (static) or the handed-over methods (record overflow)
         const uint32_t i = blockIdx.x * kSweepTile + threadIdx.x;
-        live = i < *a.n_fallback;
-        pos = live ? a.fallback[i] : 0;
+        live = i < (a.plist ? a.n_plist : *a.n_fallback);
+        pos = live ? (a.plist ? a.plist[i] : a.fallback[i]) : 0;
     } else {
         pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
         live = pos < a.pos_end;
@@ -554,12 +559,16 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
         StreamEnum sen;
         Origin org;
         MethodResult r;
+        uint32_t fw = 0;
+        const uint32_t hdr = rec_hdrs(a.recs, a.s.M)[pos];
         if (load_method<K, true>(a, (uint32_t)pos, p, o, ren, sen, org)) r = evaluate(a, ren, o, org, true, true);
         else r = evaluate(a, sen, o, org, true, true);
+        // the record writer can work from the method's record alone
+        if (!(hdr & kRecOverflow) && (hdr & kRecRemovedValid)) fw = kResFull;
         cands = r.cands;
         uint4 out;
         if (a.mode == 0) {
-            out = make_uint4(r.bd_coh, r.bd_coup, r.cands, 0);
+            out = make_uint4(r.bd_coh, r.bd_coup, r.cands, fw);
         } else if (r.n_list > kMaskBits) {  // wide: counts in the side table
             const uint32_t slot = atomicAdd(a.n_wide, 1u);
             a.wide_cnt[slot] = make_uint4(r.n_co, r.n_cp, r.n_both, (uint32_t)pos);
@@ -571,6 +580,269 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
     }
     const uint32_t wc = __reduce_add_sync(0xffffffffu, cands);
     if ((threadIdx.x & 31) == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
+}
+
+// Pass 1, best-only mode (the reference's default and the bench step), for
+// every method whose record the metric pass completed (≤ 8 used classes,
+// own-access and removed counts valid — every method of the generator's
+// k ≤ 4 + 4 configurations): one method per thread, everything in registers.
+// The packed used list (class order: one coalesced 32-byte record), the
+// origin's counts (neighbouring threads share them: L1), the exact-rational
+// origin pre-test h·M < H before the one lcom_origin_after division, then per
+// destination d (ascending): d's counts, the cohesion pre-test h_u(d)·M_d > H_d
+// before the lcom_dest_after division, and — when the method can lower its
+// origin's cbo (removed > 0) — every other used class checked against U[d]
+// (exact bitmap of a dense row, else the Bloom signature, the row only on a
+// positive). Argmin over (key, d) with strict < in ascending d
+// (suggest.hpp:180-184). Incomplete records go to k_score_thread's list.
+__global__ void __launch_bounds__(kSweepTile) k_score_fast(SweepArgs a) {
+    const uint32_t pos = a.pos_begin + blockIdx.x * kSweepTile + threadIdx.x;
+    const bool live = pos < a.pos_end;
+    const int lane = threadIdx.x & 31;
+    uint32_t hdr = kRecOverflow;
+    if (live) hdr = rec_hdrs(a.recs, a.s.M)[pos];
+    const bool fb = live && ((hdr & kRecOverflow) || !(hdr & kRecRemovedValid));
+    const uint32_t fbm = __ballot_sync(0xffffffffu, fb);
+    if (fbm) {  // the general per-thread kernel takes these (CSR path)
+        uint32_t base = 0;
+        if (lane == __ffs(fbm) - 1) base = atomicAdd(a.n_fallback, (uint32_t)__popc(fbm));
+        base = __shfl_sync(0xffffffffu, base, __ffs(fbm) - 1);
+        if (fb) a.fallback[base + __popc(fbm & ((1u << lane) - 1u))] = pos;
+    }
+    uint32_t cands = 0;
+    if (live && !fb) {
+        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
+        const uint4 r0 = rp[0], r1 = rp[1];
+        const uint32_t o = __ldg(a.pos_owner + pos);
+        const uint4 ro = __ldg(reinterpret_cast<const uint4*>(a.rec + o));  // A, M, H, cbo
+        const uint32_t ent[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        const uint32_t n = rec_n(hdr), hown = rec_hown(hdr);
+        // origin side (make_origin_score)
+        bool coh_ok = false;
+        double lo_a = 0.0;
+        if (ro.x != 0 && ro.y != 0) {
+            bool maybe = true;
+            if (ro.y >= 2 && (uint64_t)ro.x * ro.y < kExact53) maybe = (uint64_t)hown * ro.y < ro.z;
+            if (maybe) {
+                lo_a = lcom_of(ro.x, (uint64_t)ro.y - 1, (uint64_t)ro.z - hown);
+                coh_ok = lo_a < __ldg(a.dlcom + o);
+            }
+        }
+        const bool can_coup = rec_removed(hdr) > 0;
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k)
+            cands += ((uint32_t)k < n && (ent[k] >> 8) != o) ? 1u : 0u;
+        uint32_t bd_coh = kNone, bd_coup = kNone, bkp = 0;
+        double bkc = 0.0;
+        if (coh_ok || can_coup) {
+#pragma unroll
+            for (int k = 0; k < kRecMaxEnt; ++k) {
+                if ((uint32_t)k >= n) break;
+                const uint32_t d = ent[k] >> 8;
+                if (d == o) continue;
+                const uint32_t h = ent[k] & 0xffu;
+                const ClassRec rd = load_rec(a.rec, d);
+                if (coh_ok && rd.A != 0 && rd.M != 0) {  // coh_dest
+                    const bool exact = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
+                    if (!exact || (uint64_t)h * rd.M > rd.H) {
+                        const double ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + h);
+                        if (ld_a < __ldg(a.dlcom + d)) {
+                            const double kc = __dadd_rn(lo_a, ld_a);  // lcom_key
+                            if (bd_coh == kNone || kc < bkc) { bd_coh = d; bkc = kc; }
+                        }
+                    }
+                }
+                if (can_coup && (bd_coup == kNone || rd.cbo < bkp)) {  // cbo_dest_after == cbo_d when it passes
+                    bool okc = true;
+#pragma unroll
+                    for (int j = 0; j < kRecMaxEnt; ++j) {
+                        if ((uint32_t)j >= n || !okc) break;
+                        const uint32_t X = ent[j] >> 8;
+                        if (X != d && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) okc = false;
+                    }
+                    if (okc) { bd_coup = d; bkp = rd.cbo; }
+                }
+            }
+        }
+        a.res[pos] = make_uint4(bd_coh, bd_coup, cands, kResFull);
+    }
+    const uint32_t wc = __reduce_add_sync(0xffffffffu, cands);
+    if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
+}
+
+// Pass 1, best-only mode, lean origin classes (the warp-path kind: ≤ 32
+// members, ≤ 64 attributes, member degree ≤ 16): one warp per origin class,
+// one CANDIDATE (u, d) per lane. The members' packed used lists (class order:
+// contiguous records) and the origin's counts are loaded once per warp; each
+// member's origin side (exact-rational pre-test h·M < H, then lcom_origin_after
+// and its comparison with lcom[o], suggest.hpp:189-192; the coupling side
+// removed > 0 ⟺ cbo_origin_after < cbo_origin_before) is decided on its own
+// lane; the candidates of members that can still pass are flattened over the
+// lanes in (member, d ascending) order. Per candidate lane: d's whole 64-byte
+// ClassRec in four independent loads, the cohesion pre-test h_u(d)·M_d > H_d
+// (then the one division of lcom_dest_after and its comparison with lcom[d]),
+// and — when the member can lower its origin's cbo — the membership of every
+// other used class in U[d] (exact bitmap of a dense row, else the Bloom
+// signature from shared memory, the row only on a positive). Each member then
+// folds its candidates in ascending d with strict < (lowest d wins ties,
+// suggest.hpp:180-184). Same outputs as k_score_thread (res[pos]); methods
+// whose record overflowed go to the per-thread kernel's list.
+constexpr int kSLWarps = 8;
+constexpr uint32_t kSLChunk = 64;  // candidate slots per round of the warp
+
+struct __align__(16) ScoreLeanWarp {
+    uint32_t ent[32][kRecMaxEnt];      // members' used lists (X << 8 | h), own class included
+    double loa[32];                    // lcom_origin_after (when the pre-test let it be computed)
+    uint32_t flag[32];                 // bit 0 cohesion possible, bit 1 coupling possible
+    uint32_t n[32];                    // list lengths
+    double kc[kSLChunk];               // cohesion key of a passing candidate, or -1
+    uint32_t kp[kSLChunk];             // coupling key (cbo_d) of a passing candidate, or kNone
+    uint8_t sm[kSLChunk], sk[kSLChunk];  // slot -> member lane, list index
+    uint32_t sig[32][kSigWords + 1];   // each lane's destination signature
+};
+
+__global__ void __launch_bounds__(kSLWarps * 32) k_score_lean(SweepArgs a, const uint4* __restrict__ cplan,
+                                                               uint32_t c_begin, uint32_t c_end) {
+    __shared__ ScoreLeanWarp sw[kSLWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t c = c_begin + blockIdx.x * kSLWarps + warp;
+    if (c >= c_end) return;
+    const uint4 cp = cplan[c];  // (first member position, M, A, kind)
+    const uint32_t mb = cp.x, M = cp.y;
+    if (cp.w != kKindLean || M == 0) return;  // other kinds: k_score_thread over their position list
+    ScoreLeanWarp& w = sw[warp];
+    const uint32_t lt = (1u << lane) - 1u;
+    const bool act = (uint32_t)lane < M;
+    const uint32_t pos = mb + lane;
+    uint32_t hdr = kRecOverflow;
+    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0;
+    if (act) {
+        hdr = rec_hdrs(a.recs, a.s.M)[pos];
+        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
+        r0 = rp[0];
+        r1 = rp[1];
+    }
+    const uint4 ro = __ldg(reinterpret_cast<const uint4*>(a.rec + c));  // A, M, H, cbo of the origin
+    const double lcom_o = __ldg(a.dlcom + c);
+    // records the class pass could not complete: the per-thread kernel (CSR path)
+    const bool fb = act && ((hdr & kRecOverflow) || !(hdr & kRecRemovedValid));
+    const uint32_t fbm = __ballot_sync(0xffffffffu, fb);
+    if (fbm) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(a.n_fallback, (uint32_t)__popc(fbm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (fb) a.fallback[base + __popc(fbm & lt)] = pos;
+    }
+    const bool ok = act && !fb;
+    const uint32_t n = ok ? rec_n(hdr) : 0u;
+    reinterpret_cast<uint4*>(w.ent[lane])[0] = r0;
+    reinterpret_cast<uint4*>(w.ent[lane])[1] = r1;
+    // origin side, per member (make_origin_score)
+    const uint32_t hown = rec_hown(hdr);
+    bool coh_ok = false;
+    double lo_a = 0.0;
+    if (ok && ro.x != 0 && ro.y != 0) {
+        bool maybe = true;
+        if (ro.y >= 2 && (uint64_t)ro.x * ro.y < kExact53) maybe = (uint64_t)hown * ro.y < ro.z;
+        if (maybe) {
+            lo_a = lcom_of(ro.x, (uint64_t)ro.y - 1, (uint64_t)ro.z - hown);
+            coh_ok = lo_a < lcom_o;
+        }
+    }
+    const bool can_coup = ok && rec_removed(hdr) > 0;
+    const uint32_t ent[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    uint32_t own_at = kNone;
+#pragma unroll
+    for (int k = 0; k < kRecMaxEnt; ++k)
+        if ((uint32_t)k < n && (ent[k] >> 8) == c) own_at = (uint32_t)k;
+    const uint32_t ncand = n - (own_at != kNone ? 1u : 0u);
+    const uint32_t live = (coh_ok || can_coup) ? ncand : 0u;
+    w.loa[lane] = lo_a;
+    w.flag[lane] = (coh_ok ? 1u : 0u) | (can_coup ? 2u : 0u);
+    w.n[lane] = n;
+    // flatten: exclusive scan of the live candidate counts
+    uint32_t off = live;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, off, dd);
+        if (lane >= dd) off += y;
+    }
+    const uint32_t S = __shfl_sync(0xffffffffu, off, 31);
+    off -= live;
+    uint32_t bd_coh = kNone, bd_coup = kNone, bkp = 0;
+    double bkc = 0.0;
+    __syncwarp();
+    for (uint32_t base = 0; base < S; base += kSLChunk) {
+        if (live && off < base + kSLChunk && off + live > base) {
+            uint32_t sidx = off;
+            for (uint32_t k = 0; k < n; ++k) {
+                if (k == own_at) continue;
+                if (sidx >= base && sidx < base + kSLChunk) {
+                    w.sm[sidx - base] = (uint8_t)lane;
+                    w.sk[sidx - base] = (uint8_t)k;
+                }
+                ++sidx;
+            }
+        }
+        __syncwarp();
+        const uint32_t nS = min(S - base, kSLChunk);
+        for (uint32_t r = 0; r < nS; r += 32) {
+            const uint32_t sl = r + lane;
+            if (sl < nS) {
+                const uint32_t mi = w.sm[sl], k = w.sk[sl];
+                const uint32_t e = w.ent[mi][k];
+                const uint32_t d = e >> 8, h = e & 0xffu;
+                const uint32_t fl = w.flag[mi];
+                const uint4* rp = reinterpret_cast<const uint4*>(a.rec + d);
+                const uint4 q0 = __ldg(rp), q1 = __ldg(rp + 1), q2 = __ldg(rp + 2), q3 = __ldg(rp + 3);
+                double kc = -1.0;
+                uint32_t kp = kNone;
+                if ((fl & 1u) && q0.x != 0 && q0.y != 0) {  // coh_dest (suggest.hpp:189-192)
+                    const bool exact = (uint64_t)q0.x * ((uint64_t)q0.y + 1) < kExact53;
+                    if (!exact || (uint64_t)h * q0.y > q0.z) {
+                        const double ld_a = lcom_of(q0.x, (uint64_t)q0.y + 1, (uint64_t)q0.z + h);
+                        if (ld_a < __ldg(a.dlcom + d)) kc = __dadd_rn(w.loa[mi], ld_a);  // lcom_key
+                    }
+                }
+                if (fl & 2u) {  // every other used class already in U[d]
+                    uint32_t* sg = w.sig[lane];
+                    sg[0] = q1.z; sg[1] = q1.w; sg[2] = q2.x; sg[3] = q2.y; sg[4] = q2.z;
+                    sg[5] = q2.w; sg[6] = q3.x; sg[7] = q3.y; sg[8] = q3.z; sg[9] = q3.w;
+                    const uint32_t nn = w.n[mi];
+                    bool okc = true;
+                    for (uint32_t j = 0; j < nn && okc; ++j) {
+                        const uint32_t X = w.ent[mi][j] >> 8;
+                        if (X == d) continue;
+                        if (q1.y != kNone) {
+                            okc = (__ldg(a.dense + q1.y + (X >> 5)) >> (X & 31)) & 1u;
+                        } else {
+                            const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
+                            okc = ((sg[b1 >> 5] >> (b1 & 31)) & (sg[b2 >> 5] >> (b2 & 31)) & 1u) &&
+                                  urow_find(a.ux, q1.x, q0.w, X) >= 0;
+                        }
+                    }
+                    if (okc) kp = q0.w;  // cbo_dest_after == cbo_dest_before when it passes
+                }
+                w.kc[sl] = kc;
+                w.kp[sl] = kp;
+            }
+        }
+        __syncwarp();
+        if (live && off < base + kSLChunk && off + live > base) {
+            const uint32_t lo = max(off, base), hi = min(off + live, base + kSLChunk);
+            for (uint32_t sl = lo; sl < hi; ++sl) {  // ascending d, strict <
+                const uint32_t d = w.ent[lane][w.sk[sl - base]] >> 8;
+                const double kc = w.kc[sl - base];
+                const uint32_t kp = w.kp[sl - base];
+                if (kc >= 0.0 && (bd_coh == kNone || kc < bkc)) { bd_coh = d; bkc = kc; }
+                if (kp != kNone && (bd_coup == kNone || kp < bkp)) { bd_coup = d; bkp = kp; }
+            }
+        }
+        __syncwarp();
+    }
+    if (ok) a.res[pos] = make_uint4(bd_coh, bd_coup, ncand, kResFull);
+    const uint32_t wc = __reduce_add_sync(0xffffffffu, ok ? ncand : 0u);
+    if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
 }
 
 // Pass 1, best-only mode (the reference's default and the bench step): a
@@ -1364,6 +1636,60 @@ __global__ void __launch_bounds__(kSweepTile, 4) k_sweep_best(SweepArgs a) {
 // record) — both counts travel packed in one 64-bit look-back word. 1024
 // methods per tile (4 per thread) keep the look-back chain short; res is only
 // read.
+// Best-only records of one method straight from its pass-1 result (kResFull):
+// the method's packed used list, the origin's and destinations' class
+// records, the two lcom divisions, and cbo_dest_after = cbo_d + #{X ∈
+// used(u) \ {d} : X ∉ U[d]} (0 for a coupling pass; exact bitmap, or Bloom
+// then the row). Records in ascending destination order (suggest.hpp:343-349).
+__device__ __forceinline__ void write_best(const SweepArgs& a, uint32_t pos, uint32_t dc, uint32_t dp, uint64_t at) {
+    const uint32_t o = __ldg(a.pos_owner + pos), p = __ldg(a.s.cls_methods + pos);
+    const uint32_t hdr = rec_hdrs(a.recs, a.s.M)[pos];
+    const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
+    const uint4 r0 = rp[0], r1 = rp[1];
+    const uint4 ro = __ldg(reinterpret_cast<const uint4*>(a.rec + o));
+    const uint32_t ent[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    const uint32_t n = rec_n(hdr);
+    mm_suggestion s;
+    s.lcom_origin_before = __ldg(a.dlcom + o);
+    s.lcom_origin_after = lcom_of(ro.x, (uint64_t)ro.y - 1, (uint64_t)ro.z - rec_hown(hdr));
+    s.method = p;
+    s.origin = o;
+    s.cbo_origin_before = ro.w;
+    s.cbo_origin_after = ro.w - rec_removed(hdr);
+    s.origin_degenerate_after = ro.y <= 1 || ro.x == 0;
+    s.pad = 0;
+    auto one = [&](uint32_t d, uint32_t crit, bool coupling_pass) {
+        const ClassRec rd = load_rec(a.rec, d);
+        uint32_t h = 0, miss = 0;
+#pragma unroll
+        for (int k = 0; k < kRecMaxEnt; ++k) {
+            if ((uint32_t)k >= n) break;
+            const uint32_t X = ent[k] >> 8;
+            if (X == d) { h = ent[k] & 0xffu; continue; }
+            if (!coupling_pass && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ++miss;
+        }
+        s.lcom_dest_before = __ldg(a.dlcom + d);
+        s.lcom_dest_after = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + h);
+        s.destination = d;
+        s.cbo_dest_before = rd.cbo;
+        s.cbo_dest_after = rd.cbo + miss;
+        s.criteria = (uint8_t)crit;
+        s.dest_degenerate_after = rd.A == 0;
+        store_record(a.out + at, s);
+        ++at;
+    };
+    if (dc != kNone && dc == dp) {
+        one(dc, MM_CRIT_COHESION | MM_CRIT_COUPLING, true);
+    } else if (dc != kNone && dp != kNone) {  // union of two destinations (the count excludes intersection)
+        if (dc < dp) { one(dc, MM_CRIT_COHESION, false); one(dp, MM_CRIT_COUPLING, true); }
+        else { one(dp, MM_CRIT_COUPLING, true); one(dc, MM_CRIT_COHESION, false); }
+    } else if (dc != kNone) {
+        one(dc, MM_CRIT_COHESION, false);
+    } else if (dp != kNone) {
+        one(dp, MM_CRIT_COUPLING, true);
+    }
+}
+
 constexpr int kOffItems = 4;
 constexpr uint32_t kOffTile = kSweepTile * kOffItems;
 
@@ -1385,6 +1711,7 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
 
     uint4 r[kOffItems];
     uint32_t cnt[kOffItems];
+    uint32_t slow = 0;
     unsigned long long mine = 0, gated = 0, nvalid = 0;  // packed (emitters << 32) | records
 #pragma unroll
     for (int it = 0; it < kOffItems; ++it) {
@@ -1417,6 +1744,8 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
         }
         r[it] = v;
         cnt[it] = count;
+        // best-only results whose method record is complete: k_write_best
+        if (count && !(a.mode == 0 && (v.w & kResFull))) slow |= 1u << it;
         mine += count + (count ? (1ull << 32) : 0ull);
     }
     // block scan of the packed pair
@@ -1487,9 +1816,10 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
     for (int it = 0; it < kOffItems; ++it) {
         const uint64_t pos = pos0 + it;
         if (pos >= a.pos_end) continue;
-        if (cnt[it]) {  // compact emitter record: (position, gated selection, first record)
+        if (cnt[it]) {  // compact emitter record: (position | fast flag, gated selection, first record)
             const uint4 v = r[it];
-            a.emitters[at >> 32] = make_uint4((uint32_t)pos, v.x, v.y, (uint32_t)(at & 0xffffffffull));
+            const uint32_t fast = ((slow >> it) & 1u) ? 0u : kEmitFast;
+            a.emitters[at >> 32] = make_uint4((uint32_t)pos | fast, v.x, v.y, (uint32_t)(at & 0xffffffffull));
         }
         at += cnt[it] + (cnt[it] ? (1ull << 32) : 0ull);
     }
@@ -1503,6 +1833,7 @@ __global__ void __launch_bounds__(kSweepTile) k_write(SweepArgs a) {
     const uint32_t n = *a.n_emit;
     for (uint32_t i = blockIdx.x * kSweepTile + threadIdx.x; i < n; i += gridDim.x * kSweepTile) {
         const uint4 em = a.emitters[i];
+        if (em.x & kEmitFast) continue;  // k_write_best
         const uint32_t pos = em.x;
         const uint4 r = make_uint4(em.y, em.z, 0u, em.w);
         const uint32_t o = __ldg(a.pos_owner + pos);
@@ -1517,6 +1848,17 @@ __global__ void __launch_bounds__(kSweepTile) k_write(SweepArgs a) {
         Origin org;
         if (load_method<K>(a, pos, p, o, ren, sen, org)) emit(a, ren, p, o, org, res, r.w, wide);
         else emit(a, sen, p, o, org, res, r.w, wide);
+    }
+}
+
+// Pass 3, best-only records of complete-record methods (kEmitFast): one
+// thread per emitter, register-light (write_best).
+__global__ void __launch_bounds__(kSweepTile) k_write_best(SweepArgs a) {
+    const uint32_t n = *a.n_emit;
+    for (uint32_t i = blockIdx.x * kSweepTile + threadIdx.x; i < n; i += gridDim.x * kSweepTile) {
+        const uint4 em = a.emitters[i];
+        if (!(em.x & kEmitFast)) continue;
+        write_best(a, em.x & ~kEmitFast, em.y, em.z, em.w);
     }
 }
 
@@ -1680,6 +2022,31 @@ void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles,
 
 uint32_t offsets_tiles(uint64_t npos) { return (uint32_t)((npos + kOffTile - 1) / kOffTile); }
 
+void launch_score_lean(const SweepArgs& a, const uint4* cplan, uint32_t c_begin, uint32_t c_end,
+                       uint32_t fallback_tiles, cudaStream_t st) {
+    if (c_end > c_begin)
+        k_score_lean<<<(c_end - c_begin + kSLWarps - 1) / kSLWarps, kSLWarps * 32, 0, st>>>(a, cplan, c_begin, c_end);
+    if (!fallback_tiles) return;  // record-overflow members of lean classes (their list is built above)
+    SweepArgs b = a;
+    b.plist = nullptr;
+    if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<fallback_tiles, kSweepTile, 0, st>>>(b);
+    else k_score_thread<16, true><<<fallback_tiles, kSweepTile, 0, st>>>(b);
+}
+
+void launch_score_fast(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st) {
+    if (n_tiles) k_score_fast<<<n_tiles, kSweepTile, 0, st>>>(a);
+    if (!fallback_tiles) return;  // incomplete records (their list is built above)
+    if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
+    else k_score_thread<16, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
+}
+
+void launch_score_list(const SweepArgs& a, cudaStream_t st) {
+    if (!a.n_plist) return;
+    const uint32_t tiles = (a.n_plist + kSweepTile - 1) / kSweepTile;
+    if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<tiles, kSweepTile, 0, st>>>(a);
+    else k_score_thread<16, true><<<tiles, kSweepTile, 0, st>>>(a);
+}
+
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     if (!n_tiles) return;
     k_offsets<<<n_tiles, kSweepTile, 0, st>>>(a);
@@ -1688,6 +2055,7 @@ void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
 void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     if (!n_tiles) return;
     const uint32_t grid = std::min<uint32_t>(n_tiles, 148 * 8);  // grid-stride over the emitter list
+    if (a.mode == 0) k_write_best<<<grid, kSweepTile, 0, st>>>(a);
     if (a.maxdeg_fast <= 8) k_write<8><<<grid, kSweepTile, 0, st>>>(a);
     else k_write<16><<<grid, kSweepTile, 0, st>>>(a);
 }

@@ -752,6 +752,13 @@ struct ClusterShared {
     int g_e[kMaxSegs];
     u128 g_first[kMaxSegs];
     u128 g_end[kMaxSegs + 1];
+    // CTA 0's gather of every CTA's starts (unsorted), then sorted x / closing functions
+    uint32_t seg_pos_all[kMaxSegs];
+    int seg_e_all[kMaxSegs];
+    uint64_t seg_x_all[kMaxSegs];
+    Fn seg_close_all[kMaxSegs];
+    uint64_t g_x[kMaxSegs];
+    Fn g_close[kMaxSegs];
 };
 
 __global__ void __cluster_dims__(kCC, 1, 1) __launch_bounds__(kBT, 1)
@@ -912,48 +919,74 @@ k_thresholds_cluster(const double* __restrict__ lcom, const uint32_t* __restrict
         sh.has_final = 1;
     }
     cluster.sync();
-    if (rank == 0 && t == 0) {  // chain every segment, in rank (= position) order, from S_0 = 0
-        int K = 0;
-        u128 T = 0;
-        int bad_seg = 0;
-        Fn fin = fn_id();
-        uint32_t pos[kMaxSegs];
-        int ee[kMaxSegs];
-        uint64_t xx[kMaxSegs];
-        Fn cl[kMaxSegs];
-        for (int r = 0; r < kCC; ++r) {
+    if (rank == 0 && warp == 0) {
+        // chain every segment, in position order, from S_0 = 0. The segment
+        // lists of the 8 CTAs are gathered over the lanes (independent remote
+        // reads instead of one dependent chain of them), ordered by position
+        // with a rank count, then chained by lane 0 (local arithmetic only).
+        int ns = 0, rbad = 0, rfin = 0;
+        if (lane < kCC) {
+            ClusterShared* o = cluster.map_shared_rank(&sh, lane);
+            ns = o->n_segs;
+            rbad = o->bad;
+            rfin = o->has_final;
+        }
+        int bad_seg = __reduce_or_sync(0xffffffffu, rbad | (ns > kMaxSegs ? 1 : 0));
+        ns = min(ns, kMaxSegs);
+        int incl = ns;
+#pragma unroll
+        for (int d = 1; d < kCC; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += y;
+        }
+        const int K = __shfl_sync(0xffffffffu, incl, kCC - 1);
+        if (K > kMaxSegs) bad_seg = 1;
+        const int Kc = min(K, kMaxSegs);
+        const int fin_rank = __ffs(__ballot_sync(0xffffffffu, lane < kCC && rfin)) - 1;
+        // gathered (unsorted) entries in this CTA's g_* arrays; g_end[k+1] / g_first[k] reused below
+        int inc_r[kCC];
+#pragma unroll
+        for (int q = 0; q < kCC; ++q) inc_r[q] = __shfl_sync(0xffffffffu, incl, q);
+        for (int idx = lane; idx < Kc; idx += 32) {
+            int r = 0, before = 0;
+#pragma unroll
+            for (int q = 0; q < kCC - 1; ++q)
+                if (idx >= inc_r[q]) { r = q + 1; before = inc_r[q]; }
             ClusterShared* o = cluster.map_shared_rank(&sh, r);
-            bad_seg |= o->bad;
-            const int ns = min(o->n_segs, kMaxSegs);
-            for (int a = 0; a < ns; ++a) {  // a CTA's list in position order (insertion sort, ≤ 64)
-                const uint32_t p = o->seg_pos[a];
-                int b = K;
-                while (b > 0 && pos[b - 1] > p) {
-                    if (b < kMaxSegs) { pos[b] = pos[b - 1]; ee[b] = ee[b - 1]; xx[b] = xx[b - 1]; cl[b] = cl[b - 1]; }
-                    --b;
-                }
-                if (K < kMaxSegs) {
-                    pos[b] = p; ee[b] = o->seg_e[a]; xx[b] = o->seg_x[a]; cl[b] = o->seg_close[a];
-                    ++K;
-                } else {
-                    bad_seg = 1;
-                }
+            const int a = idx - before;
+            sh.seg_pos_all[idx] = o->seg_pos[a];
+            sh.seg_e_all[idx] = o->seg_e[a];
+            sh.seg_x_all[idx] = o->seg_x[a];
+            sh.seg_close_all[idx] = o->seg_close[a];
+        }
+        __syncwarp();
+        // position order (positions are distinct): rank of each entry
+        for (int idx = lane; idx < Kc; idx += 32) {
+            const uint32_t p = sh.seg_pos_all[idx];
+            int rk = 0;
+            for (int j = 0; j < Kc; ++j) rk += sh.seg_pos_all[j] < p;
+            sh.g_pos[rk] = p;
+            sh.g_e[rk] = sh.seg_e_all[idx];
+            sh.g_x[rk] = sh.seg_x_all[idx];
+            sh.g_close[rk] = sh.seg_close_all[idx];
+        }
+        Fn fin = fn_id();
+        if (fin_rank >= 0 && lane == 0) fin = cluster.map_shared_rank(&sh, fin_rank)->final_total;
+        __syncwarp();
+        if (lane == 0) {
+            u128 T = 0;
+            sh.g_end[0] = T;
+            for (int k = 0; k < Kc; ++k) {
+                const Fn tot = k + 1 < Kc ? sh.g_close[k + 1] : fin;  // segment k closes at start k+1 (or the end)
+                const int e = sh.g_e[k];
+                T = rne53(T + sh.g_x[k]);
+                sh.g_first[k] = T;
+                T += (u128)finc(tot, (int)((T >> e) & 1)) << e;
+                sh.g_end[k + 1] = T;
             }
-            if (o->has_final) fin = o->final_total;
+            sh.g_n = Kc;
+            sh.bad = bad_seg;
         }
-        sh.g_end[0] = T;
-        for (int k = 0; k < K; ++k) {
-            const Fn tot = k + 1 < K ? cl[k + 1] : fin;  // segment k closes at start k+1 (or the end)
-            const int e = ee[k];
-            T = rne53(T + xx[k]);
-            sh.g_pos[k] = pos[k];
-            sh.g_e[k] = e;
-            sh.g_first[k] = T;
-            T += (u128)finc(tot, (int)((T >> e) & 1)) << e;
-            sh.g_end[k + 1] = T;
-        }
-        sh.g_n = K;
-        sh.bad = bad_seg;
     }
     cluster.sync();
     if (rank != 0) {  // the chained table into this CTA's shared memory (one remote read each)

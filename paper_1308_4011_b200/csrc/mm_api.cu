@@ -49,6 +49,8 @@ struct Ctl {  // small device-resident control block
     unsigned long long stats[4];
     DevThresholds thr;
     DevThresholds thr_aux;  // mm_sequential_mean / the similarity mean (never the metric pass's means)
+    uint32_t n_groups;      // upload plan: k_class_group warps
+    uint32_t n_solo;        // upload plan: lean classes for k_class_lean
 };
 
 struct KStat {
@@ -92,9 +94,9 @@ struct mm_ctx {
     cudaStream_t side = nullptr;       // threshold means run here, overlapping the candidate scoring
     cudaEvent_t ev_metrics = nullptr;  // class tables ready (main -> side)
     // CTA-path tiers run on their own streams, concurrently with the warp path
-    cudaStream_t aux[kMaxTiers + 2] = {};  // + the listed warp-path classes, + tensor-core LCOM-CK
-    cudaEvent_t ev_fork = nullptr;
-    cudaEvent_t ev_join[kMaxTiers + 2] = {};
+    cudaStream_t aux[kMaxTiers + 3] = {};  // + the listed warp-path classes, + tensor-core LCOM-CK, + lean classes
+    cudaEvent_t ev_fork = nullptr, ev_fork0 = nullptr;
+    cudaEvent_t ev_join[kMaxTiers + 3] = {};
     cudaEvent_t ev_up[kUploadArrays] = {};  // per-array copy done (upload validation overlaps the copies)
     cudaStream_t d2h = nullptr;             // mm_class_metrics_async copies
     cudaEvent_t ev_d2h_go = nullptr, ev_d2h_done = nullptr;
@@ -139,6 +141,19 @@ struct mm_ctx {
     uint32_t n_giant = 0;
     uint64_t grows_words = 0;              // global attribute-bitmap scratch in use
     DBuf<uint4> cplan;         // per class (first member position, M, A, kind)
+    DBuf<uint4> cedge;         // per class: its call and access edge ranges in the class-order rows
+    DBuf<uint8_t> pc_mem, pa_mem;  // per class-order edge: member index inside its class (255: beyond)
+    bool lean_fused = true;    // env MMGPU_LEAN=0: lean classes through k_method + k_class_small (A/B)
+    uint32_t n_lean = 0;       // classes k_class_lean handles (0 when lean_fused is off)
+    DBuf<uint32_t> nl_pos;     // class-order positions of the other classes (k_method's list when mixed)
+    uint32_t n_nl = 0;
+    std::vector<uint32_t> h_nl;  // host copy of nl_pos (sweep sub-ranges)
+    bool group_on = true;        // env MMGPU_GROUP=0: every lean class on k_class_lean (warp per class)
+    DBuf<uint2> groups;          // k_class_group: (first class, classes)
+    DBuf<uint32_t> solo;         // lean classes outside the groups (member degree > 8)
+    uint32_t n_groups = 0, n_solo = 0;
+    bool score_lean = false;     // env MMGPU_SCORE_LEAN=1: best-only scoring of lean classes warp per class (A/B)
+    bool score_fast = true;      // env MMGPU_SCORE_FAST=0: best-only scoring on the general per-thread kernel
     DBuf<uint32_t> big_list;   // kKindWarpBig classes
     uint32_t n_big = 0;
     DBuf<uint32_t> large_list, foreign, cmaxdeg;
@@ -279,8 +294,13 @@ void free_model(mm_ctx* c) {
     for (DBuf<uint32_t>* b : {&c->method_owner, &c->attribute_owner, &c->cls_moff, &c->cls_methods, &c->cls_aoff,
                               &c->cls_attrs, &c->call_off, &c->call_tgt, &c->acc_off, &c->acc_tgt,
                               &c->large_list, &c->foreign, &c->cmaxdeg, &c->grows, &c->cbo, &c->ux,
-                              &c->un})
+                              &c->un, &c->nl_pos})
         b->release();
+    c->cedge.release();
+    c->groups.release();
+    c->solo.release();
+    c->pc_mem.release();
+    c->pa_mem.release();
     c->recs.release();
     c->own_mask.release();
     c->attr_info.release();
@@ -366,11 +386,12 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
         cudaEventCreateWithFlags(&ctx->ev_thr, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventRecord(ctx->ev_thr, ctx->side) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_fork0, cudaEventDisableTiming) != cudaSuccess ||
         ctx->ctl.alloc(1) != cudaSuccess || ctx->whatif.alloc(1) != cudaSuccess) {
         mm_ctx_destroy(ctx);
         return MM_E_CUDA;
     }
-    for (int k = 0; k <= kMaxTiers + 1; ++k)
+    for (int k = 0; k <= kMaxTiers + 2; ++k)
         if (cudaStreamCreateWithFlags(&ctx->aux[k], cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&ctx->ev_join[k], cudaEventDisableTiming) != cudaSuccess) {
             mm_ctx_destroy(ctx);
@@ -396,6 +417,10 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     if (const char* v = std::getenv("MMGPU_THR_SIDE")) ctx->thr_side = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_SCREEN")) ctx->screen_variant = (uint32_t)std::strtoul(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_FUSED")) ctx->fused_best = v[0] != '0';
+    if (const char* v = std::getenv("MMGPU_LEAN")) ctx->lean_fused = v[0] != '0';
+    if (const char* v = std::getenv("MMGPU_SCORE_LEAN")) ctx->score_lean = v[0] != '0';
+    if (const char* v = std::getenv("MMGPU_SCORE_FAST")) ctx->score_fast = v[0] != '0';
+    if (const char* v = std::getenv("MMGPU_GROUP")) ctx->group_on = v[0] != '0';
     *out = ctx;
     return MM_OK;
 }
@@ -429,7 +454,8 @@ void mm_ctx_destroy(mm_ctx* ctx) {
     if (ctx->ev_metrics) cudaEventDestroy(ctx->ev_metrics);
     if (ctx->ev_thr) cudaEventDestroy(ctx->ev_thr);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    for (int k = 0; k <= kMaxTiers + 1; ++k) {
+    if (ctx->ev_fork0) cudaEventDestroy(ctx->ev_fork0);
+    for (int k = 0; k <= kMaxTiers + 2; ++k) {
         if (ctx->aux[k]) cudaStreamDestroy(ctx->aux[k]);
         if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
     }
@@ -583,25 +609,39 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, ctx->pc_tgt.ensure(Ec ? Ec : 1));
     MM_CUDA(ctx, ctx->pa_tgt.ensure(Ea ? Ea : 1));
     MM_CUDA(ctx, ctx->pos_scan.ensure((M + 1ull + 1023) / 1024 + 2));
+    MM_CUDA(ctx, ctx->pc_mem.ensure(Ec ? Ec : 1));
+    MM_CUDA(ctx, ctx->pa_mem.ensure(Ea ? Ea : 1));
     st = run(ctx, "upload_rows", [&] {
-        launch_pos_rows(ctx->dev(), ctx->pc_off.p, ctx->pc_tgt.p, ctx->pa_off.p, ctx->pa_tgt.p, ctx->pos_scan.p,
-                        ctx->pos_scan.p + (M + 1ull + 1023) / 1024 + 1, ctx->stream);
+        launch_pos_rows(ctx->dev(), ctx->pos_owner.p, ctx->pc_off.p, ctx->pc_tgt.p, ctx->pa_off.p, ctx->pa_tgt.p,
+                        ctx->pc_mem.p, ctx->pa_mem.p, ctx->pos_scan.p, ctx->pos_scan.p + (M + 1ull + 1023) / 1024 + 1,
+                        ctx->stream);
     });
     if (st) return st;
 
     // class plan (bounds-checked, so it is safe on a model validation rejects):
     // warp path vs CTA path, scratch for the CTA path. One sync for both.
     MM_CUDA(ctx, ctx->cplan.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->cedge.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->big_list.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->large_list.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->foreign.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->cmaxdeg.ensure(C ? C : 1));
     const DevModel dm = ctx->dev();
     st = run(ctx, "plan", [&] {
-        launch_plan_classes(dm, ctx->pos_owner.p, ctx->cplan.p, ctx->large_list.p, &ctl->n_large, ctx->big_list.p,
+        launch_plan_classes(dm, ctx->pos_owner.p, ctx->cplan.p, ctx->cedge.p, ctx->large_list.p, &ctl->n_large, ctx->big_list.p,
                             &ctl->n_big, &ctl->max_deg, ctx->foreign.p, ctx->cmaxdeg.p, &ctl->n_hideg, ctx->stream);
     });
     if (st) return st;
+    const bool grouping = ctx->lean_fused && ctx->group_on;
+    if (grouping) {
+        MM_CUDA(ctx, ctx->groups.ensure(C ? C : 1));
+        MM_CUDA(ctx, ctx->solo.ensure(C ? C : 1));
+        st = run(ctx, "plan_groups", [&] {
+            launch_plan_groups(ctx->cplan.p, ctx->foreign.p, ctx->cmaxdeg.p, C, ctx->groups.p, &ctl->n_groups,
+                               ctx->solo.p, &ctl->n_solo, ctx->stream);
+        });
+        if (st) return st;
+    }
     Ctl h{};
     MM_CUDA(ctx, cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -609,6 +649,26 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     ctx->n_large = h.n_large;
     ctx->n_big = h.n_big;
     ctx->max_deg = h.max_deg;
+    ctx->n_groups = grouping ? h.n_groups : 0;
+    ctx->n_solo = grouping ? h.n_solo : 0;
+    // lean classes take the fused method + class kernel; k_method then runs
+    // only over the other classes' positions (a list, when there are both)
+    ctx->n_lean = ctx->lean_fused ? C - h.n_large - h.n_big : 0;
+    ctx->n_nl = 0;
+    ctx->h_nl.clear();
+    if (ctx->n_lean && ctx->n_lean < C) {
+        std::vector<uint4> cp(C);
+        MM_CUDA(ctx, cudaMemcpy(cp.data(), ctx->cplan.p, sizeof(uint4) * C, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> nl;
+        for (uint32_t c = 0; c < C; ++c)
+            if (cp[c].w != kKindLean)
+                for (uint32_t k = 0; k < cp[c].y; ++k) nl.push_back(cp[c].x + k);
+        ctx->n_nl = (uint32_t)nl.size();
+        MM_CUDA(ctx, ctx->nl_pos.ensure(nl.size() ? nl.size() : 1));
+        if (!nl.empty())
+            MM_CUDA(ctx, cudaMemcpy(ctx->nl_pos.p, nl.data(), 4ull * nl.size(), cudaMemcpyHostToDevice));
+        ctx->h_nl = std::move(nl);
+    }
     // methods the best-only screen may hand to the per-thread kernel: more edges
     // than a record's entries, or (class ids ≥ 2^24) any
     ctx->n_maybe_ovf = C >= (1u << 24) ? M : h.n_hideg;
@@ -811,10 +871,41 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
     MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_d2h_done, 0));  // async copies of the last results
     MM_CUDA(ctx, cudaMemsetAsync(&ctl->ucursor, 0, 2 * sizeof(uint32_t), ctx->stream));  // ucursor, dense_cursor
     const DevModel dm = ctx->dev();
-    mm_status st = run(ctx, "method", [&] {
-        launch_method(dm, ctx->recs.p, ctx->own_mask.p, ctx->pos_owner.p, ctx->max_deg, ctx->stream);
-    });
-    if (st) return st;
+    // lean classes: one fused kernel (no k_method records needed), on its own
+    // stream when other classes need the method pass, else on the main stream
+    const bool lean = ctx->n_lean > 0, others = ctx->n_lean < ctx->C;
+    cudaStream_t ls = others ? ctx->aux[kMaxTiers + 2] : ctx->stream;
+    mm_status st = MM_OK;
+    if (lean) {
+        if (others) {
+            MM_CUDA(ctx, cudaEventRecord(ctx->ev_fork0, ctx->stream));
+            MM_CUDA(ctx, cudaStreamWaitEvent(ls, ctx->ev_fork0, 0));
+        }
+        const bool grouped = ctx->lean_fused && ctx->group_on;
+        if (grouped) {
+            st = run_on(ctx, ls, "class_group", [&] {
+                launch_class_group(dm, ctx->cplan.p, ctx->groups.p, ctx->n_groups, ctx->pos_owner.p, ctx->recs.p,
+                                   ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p, ls);
+            });
+            if (st) return st;
+        }
+        if (!grouped || ctx->n_solo) {
+            st = run_on(ctx, ls, "class_lean", [&] {
+                launch_class_lean(dm, ctx->cplan.p, ctx->cedge.p, ctx->pc_mem.p, ctx->pa_mem.p, ctx->recs.p,
+                                  ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p,
+                                  grouped ? ctx->solo.p : nullptr, ctx->n_solo, ls);
+            });
+            if (st) return st;
+        }
+        if (others) MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[kMaxTiers + 2], ls));
+    }
+    if (others) {
+        st = run(ctx, "method", [&] {
+            launch_method(dm, ctx->recs.p, ctx->own_mask.p, ctx->pos_owner.p, ctx->max_deg,
+                          lean ? ctx->nl_pos.p : nullptr, ctx->n_nl, ctx->stream);
+        });
+        if (st) return st;
+    }
     // class pass: the CTA-path tiers fork onto their own streams (longest
     // tier first) and overlap each other and the warp path on the main stream
     st = run(ctx, "class_pass", [&] {
@@ -868,8 +959,8 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
         }
         if (mm_status e = run(ctx, "class_small", [&] {
                 launch_class_small(dm, ctx->cplan.p, ctx->big_list.p, ctx->n_big, ctx->recs.p, ctx->own_mask.p,
-                                   ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p, ctx->stream,
-                                   bs);
+                                   ctx->rec.p, ctx->lcom.p, ctx->ck.p, ctx->cbo.p, ctx->ux.p, ctx->un.p, !lean,
+                                   ctx->stream, bs);
             }))
             return e;
         if (ctx->n_big) {
@@ -878,6 +969,7 @@ mm_status mm_compute_metrics(mm_ctx* ctx) {
         }
         if (ctx->n_mma) MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[kMaxTiers + 1], 0));
         for (size_t k = 0; k < ng; ++k) MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[k], 0));
+        if (lean && others) MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[kMaxTiers + 2], 0));
         return MM_OK;
     });
     if (st) return st;
@@ -1421,8 +1513,35 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
         }
         return MM_OK;
     }
-    mm_status st = run(ctx, "score", [&] { launch_score(a, n_tiles, fallback_tiles, ctx->stream); });
-    if (st) return st;
+    // best-only on lean origin classes: warp per class, candidate per lane;
+    // the other classes' positions (a static list) on the per-thread kernel,
+    // concurrently on an auxiliary stream
+    const bool lean_score = mode == 0 && ctx->no_screen && ctx->score_lean && ctx->n_lean > 0;
+    mm_status st = MM_OK;
+    if (lean_score) {
+        const auto i0 = std::lower_bound(ctx->h_nl.begin(), ctx->h_nl.end(), pb) - ctx->h_nl.begin();
+        const auto i1 = std::lower_bound(ctx->h_nl.begin(), ctx->h_nl.end(), pe) - ctx->h_nl.begin();
+        SweepArgs b = a;
+        b.plist = ctx->nl_pos.p + i0;
+        b.n_plist = (uint32_t)(i1 - i0);
+        cudaStream_t ls = ctx->aux[kMaxTiers + 2];
+        if (b.n_plist) {
+            MM_CUDA(ctx, cudaEventRecord(ctx->ev_fork0, ctx->stream));
+            MM_CUDA(ctx, cudaStreamWaitEvent(ls, ctx->ev_fork0, 0));
+            st = run_on(ctx, ls, "score_list", [&] { launch_score_list(b, ls); });
+            if (st) return st;
+            MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[kMaxTiers + 2], ls));
+        }
+        st = run(ctx, "score", [&] { launch_score_lean(a, ctx->cplan.p, cb, ce, fallback_tiles, ctx->stream); });
+        if (st) return st;
+        if (b.n_plist) MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[kMaxTiers + 2], 0));
+    } else if (mode == 0 && ctx->no_screen && ctx->score_fast) {
+        st = run(ctx, "score", [&] { launch_score_fast(a, n_tiles, fallback_tiles, ctx->stream); });
+        if (st) return st;
+    } else {
+        st = run(ctx, "score", [&] { launch_score(a, n_tiles, fallback_tiles, ctx->stream); });
+        if (st) return st;
+    }
     if (a.thr_device)
         if (mm_status s2 = join_thresholds(ctx)) return s2;
     st = run(ctx, "offsets", [&] { launch_offsets(a, n_off, ctx->stream); });

@@ -59,6 +59,8 @@ struct SweepArgs {
     uint32_t* n_fallback;
     uint32_t no_screen;         // 1: best-only mode on the per-thread kernel (A/B, MMGPU_NO_SCREEN)
     uint32_t screen_variant;    // MMGPU_SCREEN: 1 plain, 2 overlapped round trips (default)
+    const uint32_t* plist;      // k_score_thread list mode: a static position list (non-lean classes)
+    uint32_t n_plist;
 };
 
 void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t* bad, cudaStream_t st);
@@ -66,17 +68,28 @@ void launch_expand(const DevModel& s, uint32_t* mo_out, uint32_t* ao_out, uint32
                    cudaStream_t st);
 void launch_fan(const DevModel& s, uint32_t* fan_in, uint32_t* fan_out, uint32_t* kmax, cudaStream_t st);
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st);
-void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint32_t* large_list,
+void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint4* cedge, uint32_t* large_list,
                          uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,
                          uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st);
 // upload: the dependency rows in class order (DevModel::pc_* / pa_*)
-void launch_pos_rows(const DevModel& s, uint32_t* pc_off, uint32_t* pc_tgt, uint32_t* pa_off, uint32_t* pa_tgt,
-                     uint32_t* totals, uint32_t* grand, cudaStream_t st);
+void launch_pos_rows(const DevModel& s, const uint32_t* pos_owner, uint32_t* pc_off, uint32_t* pc_tgt,
+                     uint32_t* pa_off, uint32_t* pa_tgt, uint8_t* pc_mem, uint8_t* pa_mem, uint32_t* totals,
+                     uint32_t* grand, cudaStream_t st);
+void launch_class_lean(const DevModel& s, const uint4* cplan, const uint4* cedge, const uint8_t* pc_mem,
+                       const uint8_t* pa_mem, MethRec* recs, ClassRec* rec, double* lcom,
+                       uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, const uint32_t* list,
+                       uint32_t n_list, cudaStream_t st);
+void launch_class_group(const DevModel& s, const uint4* cplan, const uint2* groups, uint32_t n_groups,
+                        const uint32_t* pos_owner, MethRec* recs, ClassRec* rec, double* lcom, uint64_t* ck,
+                        uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st);
+void launch_plan_groups(const uint4* cplan, const uint32_t* foreign, const uint32_t* cmaxdeg, uint32_t C,
+                        uint2* groups, uint32_t* n_groups, uint32_t* solo, uint32_t* n_solo, cudaStream_t st);
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
-                   uint32_t max_deg, cudaStream_t st);
+                   uint32_t max_deg, const uint32_t* plist, uint32_t n_pos, cudaStream_t st);
 void launch_class_small(const DevModel& s, const uint4* cplan, const uint32_t* big_list, uint32_t n_big,
                         MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom, uint64_t* ck,
-                        uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st, cudaStream_t st_big);
+                        uint32_t* cbo, uint32_t* ux, uint32_t* un, bool lean, cudaStream_t st,
+                        cudaStream_t st_big);
 void launch_class_large(const DevModel& s, uint32_t n_large, const uint32_t* large_list, const LargePlan* plan,
                         uint32_t smem_bytes, MethRec* recs, const uint64_t* own_mask, ClassRec* rec, double* lcom,
                         uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, uint32_t* ucursor,
@@ -128,6 +141,10 @@ void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles,
 // best-only mode in one pass (screen + gates + offsets + records); thresholds must be ready
 void launch_sweep_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 uint32_t offsets_tiles(uint64_t npos);
+void launch_score_lean(const SweepArgs& a, const uint4* cplan, uint32_t c_begin, uint32_t c_end,
+                       uint32_t fallback_tiles, cudaStream_t st);
+void launch_score_list(const SweepArgs& a, cudaStream_t st);
+void launch_score_fast(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st);
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 constexpr uint32_t kSweepTile = 256;
