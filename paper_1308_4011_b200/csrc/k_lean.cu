@@ -218,23 +218,21 @@ k_class_lean(DevModel s, const uint4* __restrict__ cplan, const uint4* __restric
 //     and run-length encoded into the sorted used list with own-access counts
 //     (used_classes + intersection_count, suggest.hpp:152-159,
 //     metrics.hpp:121-123) — no per-method insertion sorts;
-//   * every (class, foreign X) pair of the group counted once per member in a
-//     128-slot shared-memory hash table: the group's U rows with U[c][X]
-//     (metrics.hpp:167-185), the Bloom signatures, and per member the number
-//     of classes it alone uses (the sweep's cbo_origin_after);
+//   * every (class, foreign X, member) key of the group (≤ 64) sorted by one
+//     bitonic network over the warp's registers (two keys per lane): runs of
+//     (class, X) are the group's U rows in ascending X with U[c][X] = run
+//     length (metrics.hpp:167-185), their Bloom signatures, and a run of one
+//     names the member that alone uses X (the sweep's cbo_origin_after);
 //   * H, LCOM-CK (pairwise own-mask ANDs inside each class's lane segment,
 //     metrics.hpp:135-157) and lcom (metrics.hpp:114-126) per class.
 // Outputs are the same arrays k_class_lean writes (records, headers, class
 // records, lcom / LCOM-CK / cbo, U rows at 16·(first member position)).
 constexpr int kGroupWarps = 4;
-constexpr uint32_t kHashSlots = 128;
-constexpr uint32_t kHashEmpty = 0xffffffffu;
+constexpr uint32_t kGroupKeys = 64;  // (class, foreign X, member) keys per group (the plan bounds foreign edges)
 
 struct __align__(16) GroupWarp {
     uint32_t ent[32][kRecMaxEnt];      // member records
-    uint32_t hkey[kHashSlots];         // (class index << 27) | X
-    uint32_t hcnt[kHashSlots];         // members using X
-    uint32_t huser[kHashSlots];        // the member that inserted it (the only one when the count is 1)
+    uint32_t keys[kGroupKeys];         // (class index << 27) | (X << 5) | member, before the sort
     uint32_t csig[32][kSigWords];      // per class of the group: Bloom signature
     unsigned long long mask[32];       // member own-attribute masks
     uint32_t ccnt[32], cH[32], cQ[32], cmb[32];  // per class: U-row length, H, LCOM-CK pairs, first position
@@ -274,15 +272,11 @@ k_class_group(DevModel s, const uint4* __restrict__ cplan, const uint2* __restri
         c = __ldg(pos_owner + pos);
     }
     // shared state
-#pragma unroll
-    for (int k = 0; k < (int)(kHashSlots / 32); ++k) {
-        w.hkey[lane + 32 * k] = kHashEmpty;
-        w.hcnt[lane + 32 * k] = 0;
-    }
+    w.keys[lane] = kNone;
+    w.keys[lane + 32] = kNone;
     w.ccnt[lane] = 0; w.cH[lane] = 0; w.cQ[lane] = 0; w.rem[lane] = 0;
     w.cmb[lane] = cp.x;
-#pragma unroll
-    for (int k = 0; k < kSigWords; ++k) w.csig[lane][k] = 0;
+    for (uint32_t j = lane; j < nc * kSigWords; j += 32) (&w.csig[0][0])[j] = 0;
     reinterpret_cast<uint4*>(w.ent[lane])[0] = make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4*>(w.ent[lane])[1] = make_uint4(0, 0, 0, 0);
     // ---- edges: all targets, then all owners ----
@@ -326,41 +320,86 @@ k_class_group(DevModel s, const uint4* __restrict__ cplan, const uint2* __restri
         if (k + 1 < kRecMaxEnt && key[k + 1] != kNone && (key[k + 1] >> 1) == X) continue;  // run continues
         w.ent[lane][n++] = (X << 8) | h;
         ovf |= X >= (1u << 24);
-        if (X == c) {
-            hown = h;
-        } else {  // (class, X) once per member
-            const uint32_t hk = (ci << 27) | X;
-            uint32_t slot = (hk * 0x9E3779B1u) >> 25;
-            for (;;) {
-                const uint32_t old = atomicCAS(&w.hkey[slot], kHashEmpty, hk);
-                if (old == kHashEmpty || old == hk) break;
-                slot = (slot + 1) & (kHashSlots - 1);
-            }
-            if (atomicAdd(&w.hcnt[slot], 1u) == 0) w.huser[slot] = (uint32_t)lane;
-        }
+        if (X == c) hown = h;
         h = 0;
+    }
+    // every (class, foreign X, member) once: compacted into 64 slots
+    uint32_t nf = 0;
+#pragma unroll 1
+    for (uint32_t k = 0; k < n; ++k) nf += (w.ent[lane][k] >> 8) != c;
+    uint32_t fo = nf;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, fo, d);
+        if (lane >= d) fo += y;
+    }
+    fo -= nf;
+#pragma unroll 1
+    for (uint32_t k = 0; k < n; ++k) {
+        const uint32_t X = w.ent[lane][k] >> 8;
+        if (X == c) continue;
+        if (fo < kGroupKeys) w.keys[fo] = (ci << 27) | (X << 5) | (uint32_t)lane;
+        ++fo;
     }
     if (act) {
         atomicAdd(&w.cH[ci], hown);
         w.mask[lane] = mask;
     }
     __syncwarp();
-    // ---- the group's U rows, Bloom signatures, sole users ----
+    // ---- bitonic sort of the 64 keys over the warp (element e = lane + 32 r) ----
+    uint32_t v0 = w.keys[lane], v1 = w.keys[lane + 32];
 #pragma unroll
-    for (int k = 0; k < (int)(kHashSlots / 32); ++k) {
-        const uint32_t sl = lane + 32 * k;
-        const uint32_t hk = w.hkey[sl];
-        if (hk != kHashEmpty) {
-            const uint32_t cj = hk >> 27, X = hk & ((1u << 27) - 1u), cnt = w.hcnt[sl];
-            const uint32_t idx = atomicAdd(&w.ccnt[cj], 1u);
-            const uint32_t ub = kSmallRowCap * w.cmb[cj];
-            ux[ub + idx] = X;
-            un[ub + idx] = cnt;
-            if (cnt == 1) atomicAdd(&w.rem[w.huser[sl]], 1u);
-            const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
-            atomicOr(&w.csig[cj][b1 >> 5], 1u << (b1 & 31u));
-            atomicOr(&w.csig[cj][b2 >> 5], 1u << (b2 & 31u));
+    for (uint32_t k = 2; k <= kGroupKeys; k <<= 1) {
+#pragma unroll
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {  // partner in the same lane (only for k == 64: ascending)
+                const uint32_t lo = min(v0, v1), hi = max(v0, v1);
+                v0 = lo;
+                v1 = hi;
+            } else {
+                const uint32_t p0 = __shfl_xor_sync(kFull, v0, j), p1 = __shfl_xor_sync(kFull, v1, j);
+                const bool lower = ((uint32_t)lane & j) == 0;
+                const bool up0 = ((uint32_t)lane & k) == 0, up1 = (((uint32_t)lane + 32u) & k) == 0;
+                v0 = (lower == up0) ? min(v0, p0) : max(v0, p0);
+                v1 = (lower == up1) ? min(v1, p1) : max(v1, p1);
+            }
         }
+    }
+    // ---- runs of (class, X): U rows (ascending X), counts, Bloom, sole users ----
+    const uint32_t prev0 = __shfl_up_sync(kFull, v0, 1), last0 = __shfl_sync(kFull, v0, 31);
+    const uint32_t prev1 = __shfl_up_sync(kFull, v1, 1);
+    const bool val0 = v0 != kNone, val1 = v1 != kNone;
+    const bool hd0 = val0 && (lane == 0 || (prev0 >> 5) != (v0 >> 5));
+    const bool hd1 = val1 && ((lane == 0 ? last0 : prev1) >> 5) != (v1 >> 5);
+    const bool ch0 = val0 && (lane == 0 || (prev0 >> 27) != (v0 >> 27));   // first key of its class
+    const bool ch1 = val1 && ((lane == 0 ? last0 : prev1) >> 27) != (v1 >> 27);
+    const unsigned long long H = (unsigned long long)__ballot_sync(kFull, hd0) |
+                                 ((unsigned long long)__ballot_sync(kFull, hd1) << 32);
+    const unsigned long long CH = (unsigned long long)__ballot_sync(kFull, ch0) |
+                                  ((unsigned long long)__ballot_sync(kFull, ch1) << 32);
+    const uint32_t F = min(__shfl_sync(kFull, fo, 31), kGroupKeys);  // keys in use
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const bool hd = r ? hd1 : hd0;
+        if (!hd) continue;
+        const uint32_t v = r ? v1 : v0;
+        const uint32_t e = (uint32_t)lane + 32u * r;
+        const unsigned long long below = (1ull << e) - 1ull;
+        const unsigned long long after = H & ~(below | (1ull << e));
+        const uint32_t next = after ? (uint32_t)(__ffsll((long long)after) - 1) : F;
+        const uint32_t cnt = next - e;                           // members using X
+        const unsigned long long cb = CH & (below | (1ull << e));
+        const uint32_t cs = 63u - (uint32_t)__clzll((long long)cb);  // the class's first key
+        const uint32_t idx = (uint32_t)__popcll(H & below) - (uint32_t)__popcll(H & ((1ull << cs) - 1ull));
+        const uint32_t cj = v >> 27, X = (v >> 5) & ((1u << 22) - 1u);
+        const uint32_t ub = kSmallRowCap * w.cmb[cj];
+        ux[ub + idx] = X;
+        un[ub + idx] = cnt;
+        atomicAdd(&w.ccnt[cj], 1u);
+        if (cnt == 1) atomicAdd(&w.rem[v & 31u], 1u);
+        const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
+        atomicOr(&w.csig[cj][b1 >> 5], 1u << (b1 & 31u));
+        atomicOr(&w.csig[cj][b2 >> 5], 1u << (b2 & 31u));
     }
     // ---- LCOM-CK: pairs inside each class's lane segment ----
     const uint32_t seg0 = act ? w.cmb[ci] - P0 : (uint32_t)lane;
@@ -401,7 +440,8 @@ k_class_group(DevModel s, const uint4* __restrict__ cplan, const uint2* __restri
 }
 
 // Upload plan: runs of consecutive lean classes per warp of k_class_group
-// (≤ 32 members, ≤ 64 foreign edges, ≤ 32 classes, member degree ≤ 8),
+// (≤ 32 members, ≤ 64 foreign edges, ≤ 32 classes, member degree ≤ 8, fewer
+// than 2^22 classes),
 // greedily inside blocks of 16 classes (one thread per block); lean classes
 // with a member of degree 9..16 go to k_class_lean's list.
 __global__ void k_plan_groups(const uint4* __restrict__ cplan, const uint32_t* __restrict__ foreign,
@@ -419,13 +459,29 @@ __global__ void k_plan_groups(const uint4* __restrict__ cplan, const uint32_t* _
     for (uint32_t c = cb; c < ce; ++c) {
         const uint4 cp = cplan[c];
         if (cp.w != kKindLean) { close(); continue; }
-        if (cmaxdeg[c] > (uint32_t)kRecMaxEnt) { close(); solo[atomicAdd(n_solo, 1u)] = c; continue; }
+        // (group keys pack the class id in 22 bits)
+        if (cmaxdeg[c] > (uint32_t)kRecMaxEnt || C >= (1u << 22)) { close(); solo[atomicAdd(n_solo, 1u)] = c; continue; }
         const uint32_t f = foreign[c];
         if (gn && (gm + cp.y > 32u || gf + f > 64u || gn == 32u)) close();
         if (!gn) g0 = c;
         ++gn; gm += cp.y; gf += f;
     }
     close();
+}
+
+// Upload plan: the class-order positions of every class that is not lean
+// (k_method's list when both kinds exist), compacted on the device.
+__global__ void k_nl_positions(const uint32_t* __restrict__ pos_owner, const uint4* __restrict__ cplan, uint32_t M,
+                               uint32_t* __restrict__ out, uint32_t* __restrict__ n) {
+    const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool keep = pos < M && cplan[pos_owner[pos]].w != kKindLean;
+    const uint32_t b = __ballot_sync(kFull, keep);
+    if (!b) return;
+    const int lane = threadIdx.x & 31, lead = __ffs(b) - 1;
+    uint32_t base = 0;
+    if (lane == lead) base = atomicAdd(n, (uint32_t)__popc(b));
+    base = __shfl_sync(kFull, base, lead);
+    if (keep) out[base + __popc(b & ((1u << lane) - 1u))] = pos;
 }
 
 }  // namespace
@@ -446,6 +502,11 @@ void launch_class_lean(const DevModel& s, const uint4* cplan, const uint4* cedge
     k_class_lean<<<(n + kLeanWarps - 1) / kLeanWarps, kLeanWarps * 32, 0, st>>>(s, cplan, cedge, pc_mem, pa_mem,
                                                                                   recs, rec, lcom, ck, cbo, ux, un,
                                                                                   list, n_list);
+}
+
+void launch_nl_positions(const uint32_t* pos_owner, const uint4* cplan, uint32_t M, uint32_t* out, uint32_t* n,
+                         cudaStream_t st) {
+    if (M) k_nl_positions<<<(M + 255) / 256, 256, 0, st>>>(pos_owner, cplan, M, out, n);
 }
 
 void launch_plan_groups(const uint4* cplan, const uint32_t* foreign, const uint32_t* cmaxdeg, uint32_t C,

@@ -543,10 +543,10 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
     __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
     uint64_t pos;
     bool live;
-    if (LIST) {  // a position list: a.plist (static) or the handed-over methods (record overflow)
+    if (LIST) {  // the methods k_score_fast / k_screen handed over (record overflow)
         const uint32_t i = blockIdx.x * kSweepTile + threadIdx.x;
-        live = i < (a.plist ? a.n_plist : *a.n_fallback);
-        pos = live ? (a.plist ? a.plist[i] : a.fallback[i]) : 0;
+        live = i < *a.n_fallback;
+        pos = live ? a.fallback[i] : 0;
     } else {
         pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
         live = pos < a.pos_end;
@@ -596,6 +596,10 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
 // positive). Argmin over (key, d) with strict < in ascending d
 // (suggest.hpp:180-184). Incomplete records go to k_score_thread's list.
 __global__ void __launch_bounds__(kSweepTile) k_score_fast(SweepArgs a) {
+    // the used list column-major in shared memory (thread t's k-th entry at
+    // [k][t]: conflict-free), so the candidate and membership loops stay
+    // rolled: small code, lanes of a warp in step
+    __shared__ uint32_t s_ent[kRecMaxEnt][kSweepTile];
     const uint32_t pos = a.pos_begin + blockIdx.x * kSweepTile + threadIdx.x;
     const bool live = pos < a.pos_end;
     const int lane = threadIdx.x & 31;
@@ -615,8 +619,10 @@ __global__ void __launch_bounds__(kSweepTile) k_score_fast(SweepArgs a) {
         const uint4 r0 = rp[0], r1 = rp[1];
         const uint32_t o = __ldg(a.pos_owner + pos);
         const uint4 ro = __ldg(reinterpret_cast<const uint4*>(a.rec + o));  // A, M, H, cbo
-        const uint32_t ent[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
         const uint32_t n = rec_n(hdr), hown = rec_hown(hdr);
+        uint32_t* E = &s_ent[0][threadIdx.x];
+        E[0 * kSweepTile] = r0.x; E[1 * kSweepTile] = r0.y; E[2 * kSweepTile] = r0.z; E[3 * kSweepTile] = r0.w;
+        E[4 * kSweepTile] = r1.x; E[5 * kSweepTile] = r1.y; E[6 * kSweepTile] = r1.z; E[7 * kSweepTile] = r1.w;
         // origin side (make_origin_score)
         bool coh_ok = false;
         double lo_a = 0.0;
@@ -629,219 +635,39 @@ __global__ void __launch_bounds__(kSweepTile) k_score_fast(SweepArgs a) {
             }
         }
         const bool can_coup = rec_removed(hdr) > 0;
-#pragma unroll
-        for (int k = 0; k < kRecMaxEnt; ++k)
-            cands += ((uint32_t)k < n && (ent[k] >> 8) != o) ? 1u : 0u;
         uint32_t bd_coh = kNone, bd_coup = kNone, bkp = 0;
         double bkc = 0.0;
-        if (coh_ok || can_coup) {
-#pragma unroll
-            for (int k = 0; k < kRecMaxEnt; ++k) {
-                if ((uint32_t)k >= n) break;
-                const uint32_t d = ent[k] >> 8;
-                if (d == o) continue;
-                const uint32_t h = ent[k] & 0xffu;
-                const ClassRec rd = load_rec(a.rec, d);
-                if (coh_ok && rd.A != 0 && rd.M != 0) {  // coh_dest
-                    const bool exact = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
-                    if (!exact || (uint64_t)h * rd.M > rd.H) {
-                        const double ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + h);
-                        if (ld_a < __ldg(a.dlcom + d)) {
-                            const double kc = __dadd_rn(lo_a, ld_a);  // lcom_key
-                            if (bd_coh == kNone || kc < bkc) { bd_coh = d; bkc = kc; }
-                        }
+#pragma unroll 1
+        for (uint32_t k = 0; k < n; ++k) {
+            const uint32_t d = E[k * kSweepTile] >> 8;
+            if (d == o) continue;
+            ++cands;
+            if (!coh_ok && !can_coup) continue;
+            const uint32_t h = E[k * kSweepTile] & 0xffu;
+            const ClassRec rd = load_rec(a.rec, d);
+            if (coh_ok && rd.A != 0 && rd.M != 0) {  // coh_dest
+                const bool exact = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
+                if (!exact || (uint64_t)h * rd.M > rd.H) {
+                    const double ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + h);
+                    if (ld_a < __ldg(a.dlcom + d)) {
+                        const double kc = __dadd_rn(lo_a, ld_a);  // lcom_key
+                        if (bd_coh == kNone || kc < bkc) { bd_coh = d; bkc = kc; }
                     }
                 }
-                if (can_coup && (bd_coup == kNone || rd.cbo < bkp)) {  // cbo_dest_after == cbo_d when it passes
-                    bool okc = true;
-#pragma unroll
-                    for (int j = 0; j < kRecMaxEnt; ++j) {
-                        if ((uint32_t)j >= n || !okc) break;
-                        const uint32_t X = ent[j] >> 8;
-                        if (X != d && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) okc = false;
-                    }
-                    if (okc) { bd_coup = d; bkp = rd.cbo; }
+            }
+            if (can_coup && (bd_coup == kNone || rd.cbo < bkp)) {  // cbo_dest_after == cbo_d when it passes
+                bool okc = true;
+#pragma unroll 1
+                for (uint32_t j = 0; j < n && okc; ++j) {
+                    const uint32_t X = E[j * kSweepTile] >> 8;
+                    if (X != d) okc = in_urow(a.rec, d, rd, a.ux, a.dense, X);
                 }
+                if (okc) { bd_coup = d; bkp = rd.cbo; }
             }
         }
         a.res[pos] = make_uint4(bd_coh, bd_coup, cands, kResFull);
     }
     const uint32_t wc = __reduce_add_sync(0xffffffffu, cands);
-    if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
-}
-
-// Pass 1, best-only mode, lean origin classes (the warp-path kind: ≤ 32
-// members, ≤ 64 attributes, member degree ≤ 16): one warp per origin class,
-// one CANDIDATE (u, d) per lane. The members' packed used lists (class order:
-// contiguous records) and the origin's counts are loaded once per warp; each
-// member's origin side (exact-rational pre-test h·M < H, then lcom_origin_after
-// and its comparison with lcom[o], suggest.hpp:189-192; the coupling side
-// removed > 0 ⟺ cbo_origin_after < cbo_origin_before) is decided on its own
-// lane; the candidates of members that can still pass are flattened over the
-// lanes in (member, d ascending) order. Per candidate lane: d's whole 64-byte
-// ClassRec in four independent loads, the cohesion pre-test h_u(d)·M_d > H_d
-// (then the one division of lcom_dest_after and its comparison with lcom[d]),
-// and — when the member can lower its origin's cbo — the membership of every
-// other used class in U[d] (exact bitmap of a dense row, else the Bloom
-// signature from shared memory, the row only on a positive). Each member then
-// folds its candidates in ascending d with strict < (lowest d wins ties,
-// suggest.hpp:180-184). Same outputs as k_score_thread (res[pos]); methods
-// whose record overflowed go to the per-thread kernel's list.
-constexpr int kSLWarps = 8;
-constexpr uint32_t kSLChunk = 64;  // candidate slots per round of the warp
-
-struct __align__(16) ScoreLeanWarp {
-    uint32_t ent[32][kRecMaxEnt];      // members' used lists (X << 8 | h), own class included
-    double loa[32];                    // lcom_origin_after (when the pre-test let it be computed)
-    uint32_t flag[32];                 // bit 0 cohesion possible, bit 1 coupling possible
-    uint32_t n[32];                    // list lengths
-    double kc[kSLChunk];               // cohesion key of a passing candidate, or -1
-    uint32_t kp[kSLChunk];             // coupling key (cbo_d) of a passing candidate, or kNone
-    uint8_t sm[kSLChunk], sk[kSLChunk];  // slot -> member lane, list index
-    uint32_t sig[32][kSigWords + 1];   // each lane's destination signature
-};
-
-__global__ void __launch_bounds__(kSLWarps * 32) k_score_lean(SweepArgs a, const uint4* __restrict__ cplan,
-                                                               uint32_t c_begin, uint32_t c_end) {
-    __shared__ ScoreLeanWarp sw[kSLWarps];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t c = c_begin + blockIdx.x * kSLWarps + warp;
-    if (c >= c_end) return;
-    const uint4 cp = cplan[c];  // (first member position, M, A, kind)
-    const uint32_t mb = cp.x, M = cp.y;
-    if (cp.w != kKindLean || M == 0) return;  // other kinds: k_score_thread over their position list
-    ScoreLeanWarp& w = sw[warp];
-    const uint32_t lt = (1u << lane) - 1u;
-    const bool act = (uint32_t)lane < M;
-    const uint32_t pos = mb + lane;
-    uint32_t hdr = kRecOverflow;
-    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0;
-    if (act) {
-        hdr = rec_hdrs(a.recs, a.s.M)[pos];
-        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
-        r0 = rp[0];
-        r1 = rp[1];
-    }
-    const uint4 ro = __ldg(reinterpret_cast<const uint4*>(a.rec + c));  // A, M, H, cbo of the origin
-    const double lcom_o = __ldg(a.dlcom + c);
-    // records the class pass could not complete: the per-thread kernel (CSR path)
-    const bool fb = act && ((hdr & kRecOverflow) || !(hdr & kRecRemovedValid));
-    const uint32_t fbm = __ballot_sync(0xffffffffu, fb);
-    if (fbm) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(a.n_fallback, (uint32_t)__popc(fbm));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (fb) a.fallback[base + __popc(fbm & lt)] = pos;
-    }
-    const bool ok = act && !fb;
-    const uint32_t n = ok ? rec_n(hdr) : 0u;
-    reinterpret_cast<uint4*>(w.ent[lane])[0] = r0;
-    reinterpret_cast<uint4*>(w.ent[lane])[1] = r1;
-    // origin side, per member (make_origin_score)
-    const uint32_t hown = rec_hown(hdr);
-    bool coh_ok = false;
-    double lo_a = 0.0;
-    if (ok && ro.x != 0 && ro.y != 0) {
-        bool maybe = true;
-        if (ro.y >= 2 && (uint64_t)ro.x * ro.y < kExact53) maybe = (uint64_t)hown * ro.y < ro.z;
-        if (maybe) {
-            lo_a = lcom_of(ro.x, (uint64_t)ro.y - 1, (uint64_t)ro.z - hown);
-            coh_ok = lo_a < lcom_o;
-        }
-    }
-    const bool can_coup = ok && rec_removed(hdr) > 0;
-    const uint32_t ent[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-    uint32_t own_at = kNone;
-#pragma unroll
-    for (int k = 0; k < kRecMaxEnt; ++k)
-        if ((uint32_t)k < n && (ent[k] >> 8) == c) own_at = (uint32_t)k;
-    const uint32_t ncand = n - (own_at != kNone ? 1u : 0u);
-    const uint32_t live = (coh_ok || can_coup) ? ncand : 0u;
-    w.loa[lane] = lo_a;
-    w.flag[lane] = (coh_ok ? 1u : 0u) | (can_coup ? 2u : 0u);
-    w.n[lane] = n;
-    // flatten: exclusive scan of the live candidate counts
-    uint32_t off = live;
-#pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, off, dd);
-        if (lane >= dd) off += y;
-    }
-    const uint32_t S = __shfl_sync(0xffffffffu, off, 31);
-    off -= live;
-    uint32_t bd_coh = kNone, bd_coup = kNone, bkp = 0;
-    double bkc = 0.0;
-    __syncwarp();
-    for (uint32_t base = 0; base < S; base += kSLChunk) {
-        if (live && off < base + kSLChunk && off + live > base) {
-            uint32_t sidx = off;
-            for (uint32_t k = 0; k < n; ++k) {
-                if (k == own_at) continue;
-                if (sidx >= base && sidx < base + kSLChunk) {
-                    w.sm[sidx - base] = (uint8_t)lane;
-                    w.sk[sidx - base] = (uint8_t)k;
-                }
-                ++sidx;
-            }
-        }
-        __syncwarp();
-        const uint32_t nS = min(S - base, kSLChunk);
-        for (uint32_t r = 0; r < nS; r += 32) {
-            const uint32_t sl = r + lane;
-            if (sl < nS) {
-                const uint32_t mi = w.sm[sl], k = w.sk[sl];
-                const uint32_t e = w.ent[mi][k];
-                const uint32_t d = e >> 8, h = e & 0xffu;
-                const uint32_t fl = w.flag[mi];
-                const uint4* rp = reinterpret_cast<const uint4*>(a.rec + d);
-                const uint4 q0 = __ldg(rp), q1 = __ldg(rp + 1), q2 = __ldg(rp + 2), q3 = __ldg(rp + 3);
-                double kc = -1.0;
-                uint32_t kp = kNone;
-                if ((fl & 1u) && q0.x != 0 && q0.y != 0) {  // coh_dest (suggest.hpp:189-192)
-                    const bool exact = (uint64_t)q0.x * ((uint64_t)q0.y + 1) < kExact53;
-                    if (!exact || (uint64_t)h * q0.y > q0.z) {
-                        const double ld_a = lcom_of(q0.x, (uint64_t)q0.y + 1, (uint64_t)q0.z + h);
-                        if (ld_a < __ldg(a.dlcom + d)) kc = __dadd_rn(w.loa[mi], ld_a);  // lcom_key
-                    }
-                }
-                if (fl & 2u) {  // every other used class already in U[d]
-                    uint32_t* sg = w.sig[lane];
-                    sg[0] = q1.z; sg[1] = q1.w; sg[2] = q2.x; sg[3] = q2.y; sg[4] = q2.z;
-                    sg[5] = q2.w; sg[6] = q3.x; sg[7] = q3.y; sg[8] = q3.z; sg[9] = q3.w;
-                    const uint32_t nn = w.n[mi];
-                    bool okc = true;
-                    for (uint32_t j = 0; j < nn && okc; ++j) {
-                        const uint32_t X = w.ent[mi][j] >> 8;
-                        if (X == d) continue;
-                        if (q1.y != kNone) {
-                            okc = (__ldg(a.dense + q1.y + (X >> 5)) >> (X & 31)) & 1u;
-                        } else {
-                            const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
-                            okc = ((sg[b1 >> 5] >> (b1 & 31)) & (sg[b2 >> 5] >> (b2 & 31)) & 1u) &&
-                                  urow_find(a.ux, q1.x, q0.w, X) >= 0;
-                        }
-                    }
-                    if (okc) kp = q0.w;  // cbo_dest_after == cbo_dest_before when it passes
-                }
-                w.kc[sl] = kc;
-                w.kp[sl] = kp;
-            }
-        }
-        __syncwarp();
-        if (live && off < base + kSLChunk && off + live > base) {
-            const uint32_t lo = max(off, base), hi = min(off + live, base + kSLChunk);
-            for (uint32_t sl = lo; sl < hi; ++sl) {  // ascending d, strict <
-                const uint32_t d = w.ent[lane][w.sk[sl - base]] >> 8;
-                const double kc = w.kc[sl - base];
-                const uint32_t kp = w.kp[sl - base];
-                if (kc >= 0.0 && (bd_coh == kNone || kc < bkc)) { bd_coh = d; bkc = kc; }
-                if (kp != kNone && (bd_coup == kNone || kp < bkp)) { bd_coup = d; bkp = kp; }
-            }
-        }
-        __syncwarp();
-    }
-    if (ok) a.res[pos] = make_uint4(bd_coh, bd_coup, ncand, kResFull);
-    const uint32_t wc = __reduce_add_sync(0xffffffffu, ok ? ncand : 0u);
     if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
 }
 
@@ -1642,15 +1468,25 @@ __global__ void __launch_bounds__(kSweepTile, 4) k_sweep_best(SweepArgs a) {
 // used(u) \ {d} : X ∉ U[d]} (0 for a coupling pass; exact bitmap, or Bloom
 // then the row). Records in ascending destination order (suggest.hpp:343-349).
 __device__ __forceinline__ void write_best(const SweepArgs& a, uint32_t pos, uint32_t dc, uint32_t dp, uint64_t at) {
+    // every load that depends only on the emitter first (one memory round trip)
     const uint32_t o = __ldg(a.pos_owner + pos), p = __ldg(a.s.cls_methods + pos);
     const uint32_t hdr = rec_hdrs(a.recs, a.s.M)[pos];
     const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
     const uint4 r0 = rp[0], r1 = rp[1];
+    const uint32_t d1 = dc != kNone ? dc : dp;                       // first destination in the record order
+    const uint32_t d2 = (dc != kNone && dp != kNone && dc != dp) ? dp : kNone;
+    const uint32_t da = (d2 != kNone && d2 < d1) ? d2 : d1, db = (d2 != kNone && d2 < d1) ? d1 : d2;
+    const ClassRec ra = load_rec(a.rec, da);
+    ClassRec rb = ra;
+    double lb_b = 0.0;
+    if (db != kNone) { rb = load_rec(a.rec, db); lb_b = __ldg(a.dlcom + db); }
+    const double la_b = __ldg(a.dlcom + da);
     const uint4 ro = __ldg(reinterpret_cast<const uint4*>(a.rec + o));
+    const double lo_b = __ldg(a.dlcom + o);
     const uint32_t ent[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
     const uint32_t n = rec_n(hdr);
     mm_suggestion s;
-    s.lcom_origin_before = __ldg(a.dlcom + o);
+    s.lcom_origin_before = lo_b;
     s.lcom_origin_after = lcom_of(ro.x, (uint64_t)ro.y - 1, (uint64_t)ro.z - rec_hown(hdr));
     s.method = p;
     s.origin = o;
@@ -1658,40 +1494,57 @@ __device__ __forceinline__ void write_best(const SweepArgs& a, uint32_t pos, uin
     s.cbo_origin_after = ro.w - rec_removed(hdr);
     s.origin_degenerate_after = ro.y <= 1 || ro.x == 0;
     s.pad = 0;
-    auto one = [&](uint32_t d, uint32_t crit, bool coupling_pass) {
-        const ClassRec rd = load_rec(a.rec, d);
+    auto one = [&](uint32_t d, const ClassRec& rd, double ld_b) {
+        const bool coh = d == dc, coup = d == dp;
         uint32_t h = 0, miss = 0;
 #pragma unroll
         for (int k = 0; k < kRecMaxEnt; ++k) {
             if ((uint32_t)k >= n) break;
             const uint32_t X = ent[k] >> 8;
             if (X == d) { h = ent[k] & 0xffu; continue; }
-            if (!coupling_pass && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ++miss;
+            if (!coup && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ++miss;  // a coupling pass has none
         }
-        s.lcom_dest_before = __ldg(a.dlcom + d);
+        s.lcom_dest_before = ld_b;
         s.lcom_dest_after = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + h);
         s.destination = d;
         s.cbo_dest_before = rd.cbo;
         s.cbo_dest_after = rd.cbo + miss;
-        s.criteria = (uint8_t)crit;
+        s.criteria = (uint8_t)((coh ? MM_CRIT_COHESION : 0u) | (coup ? MM_CRIT_COUPLING : 0u));
         s.dest_degenerate_after = rd.A == 0;
         store_record(a.out + at, s);
         ++at;
     };
-    if (dc != kNone && dc == dp) {
-        one(dc, MM_CRIT_COHESION | MM_CRIT_COUPLING, true);
-    } else if (dc != kNone && dp != kNone) {  // union of two destinations (the count excludes intersection)
-        if (dc < dp) { one(dc, MM_CRIT_COHESION, false); one(dp, MM_CRIT_COUPLING, true); }
-        else { one(dp, MM_CRIT_COUPLING, true); one(dc, MM_CRIT_COHESION, false); }
-    } else if (dc != kNone) {
-        one(dc, MM_CRIT_COHESION, false);
-    } else if (dp != kNone) {
-        one(dp, MM_CRIT_COUPLING, true);
-    }
+    // records in ascending destination order (suggest.hpp:343-349); the count
+    // k_offsets made excludes the intersection case where dc != dp
+    one(da, ra, la_b);
+    if (db != kNone) one(db, rb, lb_b);
 }
 
-constexpr int kOffItems = 4;
+constexpr int kOffItems = 16;  // 4096-position tiles: ≤ 245 tiles for 1M methods, one resident wave
 constexpr uint32_t kOffTile = kSweepTile * kOffItems;
+
+// one method's pass-1 result under the class gates and the criteria merge:
+// the emitter's selection words and the record count
+__device__ __forceinline__ uint4 gate_result(const SweepArgs& a, uint4 v, bool gcoh, bool gcoup, bool inter,
+                                             uint32_t& count) {
+    if (a.mode == 0) {
+        const uint32_t bc = gcoh ? v.x : kNone, bp = gcoup ? v.y : kNone;
+        const bool same = bc != kNone && bc == bp;
+        count = inter ? (same ? 1u : 0u) : (uint32_t)(bc != kNone) + (uint32_t)(bp != kNone) - (same ? 1u : 0u);
+        v.x = bc;
+        v.y = bp;
+    } else if (v.x & kWideMark) {
+        const uint4 wc = a.wide_cnt[v.x & ~kWideMark];
+        count = wide_count(wc.x, wc.y, wc.z, gcoh, gcoup, inter);
+        v.x = kWideMark | (gcoh ? 1u : 0u);  // k_write re-derives the destinations under these gates
+        v.y = gcoup ? 1u : 0u;
+    } else {
+        v.x = gcoh ? v.x : 0u;
+        v.y = gcoup ? v.y : 0u;
+        count = __popc(inter ? (v.x & v.y) : (v.x | v.y));
+    }
+    return v;
+}
 
 __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
     __shared__ uint32_t s_tile;
@@ -1709,46 +1562,29 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
     const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
     const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
 
-    uint4 r[kOffItems];
+    // pass A: counts (the gated results are recomputed in pass C from the
+    // same reads — cache hits — instead of holding 16 of them in registers)
     uint32_t cnt[kOffItems];
-    uint32_t slow = 0;
+    uint32_t gates = 0;  // bit 2·it: cohesion gate, bit 2·it + 1: coupling gate
     unsigned long long mine = 0, gated = 0, nvalid = 0;  // packed (emitters << 32) | records
 #pragma unroll
     for (int it = 0; it < kOffItems; ++it) {
         const uint64_t pos = pos0 + it;
         cnt[it] = 0;
-        r[it] = make_uint4(0, 0, 0, 0);
         if (pos >= a.pos_end) continue;
         ++nvalid;
-        uint4 v = a.res[pos];
+        const uint4 v = a.res[pos];
         const uint32_t o = __ldg(a.pos_owner + pos);
         const bool gcoh = (a.crit & MM_CRIT_COHESION) && __ldg(a.lcom + o) > thr_l;
         const bool gcoup = (a.crit & MM_CRIT_COUPLING) && (double)__ldg(a.cbo + o) > thr_c;
+        gates |= ((gcoh ? 1u : 0u) | (gcoup ? 2u : 0u)) << (2 * it);
         gated += v.z * ((gcoh ? 1u : 0u) + (gcoup ? 1u : 0u));
         uint32_t count;
-        if (a.mode == 0) {
-            const uint32_t bc = gcoh ? v.x : kNone, bp = gcoup ? v.y : kNone;
-            const bool same = bc != kNone && bc == bp;
-            count = inter ? (same ? 1u : 0u) : (uint32_t)(bc != kNone) + (uint32_t)(bp != kNone) - (same ? 1u : 0u);
-            v.x = bc;
-            v.y = bp;
-        } else if (v.x & kWideMark) {
-            const uint4 wc = a.wide_cnt[v.x & ~kWideMark];
-            count = wide_count(wc.x, wc.y, wc.z, gcoh, gcoup, inter);
-            v.x = kWideMark | (gcoh ? 1u : 0u);  // k_write re-derives the destinations under these gates
-            v.y = gcoup ? 1u : 0u;
-        } else {
-            v.x = gcoh ? v.x : 0u;
-            v.y = gcoup ? v.y : 0u;
-            count = __popc(inter ? (v.x & v.y) : (v.x | v.y));
-        }
-        r[it] = v;
+        gate_result(a, v, gcoh, gcoup, inter, count);
         cnt[it] = count;
-        // best-only results whose method record is complete: k_write_best
-        if (count && !(a.mode == 0 && (v.w & kResFull))) slow |= 1u << it;
         mine += count + (count ? (1ull << 32) : 0ull);
     }
-    // block scan of the packed pair
+    // pass B: block scan of the packed pair, decoupled look-back
     unsigned long long inc = mine;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -1773,8 +1609,8 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
         agg += s_warp[w];
     }
     const unsigned long long texcl = before + inc - mine;
-    // decoupled look-back: warp 0 inspects 32 predecessor tiles per step
-    // (relaxed gpu-scope loads; flag and value share one 64-bit word)
+    // warp 0 inspects 32 predecessor tiles per step (relaxed gpu-scope loads;
+    // flag and value share one 64-bit word)
     if (warp == 0) {
         unsigned long long excl = 0;
         if (tile == 0) {
@@ -1811,17 +1647,158 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
         }
     }
     __syncthreads();
+    // pass C: the emitters' compact records
     unsigned long long at = s_excl + texcl;
 #pragma unroll
     for (int it = 0; it < kOffItems; ++it) {
         const uint64_t pos = pos0 + it;
         if (pos >= a.pos_end) continue;
-        if (cnt[it]) {  // compact emitter record: (position | fast flag, gated selection, first record)
-            const uint4 v = r[it];
-            const uint32_t fast = ((slow >> it) & 1u) ? 0u : kEmitFast;
+        if (cnt[it]) {  // (position | fast flag, gated selection, first record)
+            uint32_t count;
+            const uint4 v = gate_result(a, a.res[pos], (gates >> (2 * it)) & 1u, (gates >> (2 * it + 1)) & 1u, inter,
+                                        count);
+            // best-only results whose method record is complete: k_write_best
+            const uint32_t fast = (a.mode == 0 && (v.w & kResFull)) ? kEmitFast : 0u;
             a.emitters[at >> 32] = make_uint4((uint32_t)pos | fast, v.x, v.y, (uint32_t)(at & 0xffffffffull));
         }
         at += cnt[it] + (cnt[it] ? (1ull << 32) : 0ull);
+    }
+}
+
+// Best-only mode (the bench step) without a look-back chain: pass 2a counts
+// each 4096-position tile's records under the class gates (one word per
+// tile), pass 2b gives every tile its prefix by summing its predecessors'
+// words (≤ a few hundred, one block reduction), re-derives the per-method
+// counts, scans them inside the block, and writes the records of complete-
+// record methods itself (write_best, balanced over the block through a
+// shared-memory list); the rest go to k_write's emitter list.
+__device__ __forceinline__ uint32_t best_count(const SweepArgs& a, uint64_t pos, double thr_l, double thr_c, bool inter,
+                                               uint4& v, bool& fast, unsigned long long* gated) {
+    v = a.res[pos];
+    const uint32_t o = __ldg(a.pos_owner + pos);
+    const bool gcoh = (a.crit & MM_CRIT_COHESION) && __ldg(a.lcom + o) > thr_l;
+    const bool gcoup = (a.crit & MM_CRIT_COUPLING) && (double)__ldg(a.cbo + o) > thr_c;
+    if (gated) *gated += v.z * ((gcoh ? 1u : 0u) + (gcoup ? 1u : 0u));
+    uint32_t count;
+    v = gate_result(a, v, gcoh, gcoup, inter, count);
+    fast = (v.w & kResFull) != 0;
+    return count;
+}
+
+__global__ void __launch_bounds__(kSweepTile) k_tile_counts(SweepArgs a) {
+    __shared__ unsigned long long s_red[3][kSweepTile / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t pos0 = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kOffTile + (uint64_t)threadIdx.x * kOffItems;
+    double thr_l = a.thr_lcom, thr_c = a.thr_cbo;
+    if (a.thr_device) { thr_l = a.dthr->lcom; thr_c = a.dthr->cbo; }
+    const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
+    const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
+    unsigned long long mine = 0, gated = 0, nvalid = 0;  // (slow emitters << 32) | records
+#pragma unroll
+    for (int it = 0; it < kOffItems; ++it) {
+        const uint64_t pos = pos0 + it;
+        if (pos >= a.pos_end) continue;
+        ++nvalid;
+        uint4 v;
+        bool fast;
+        const uint32_t count = best_count(a, pos, thr_l, thr_c, inter, v, fast, &gated);
+        mine += count + ((count && !fast) ? (1ull << 32) : 0ull);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        mine += __shfl_down_sync(0xffffffffu, mine, d);
+        gated += __shfl_down_sync(0xffffffffu, gated, d);
+        nvalid += __shfl_down_sync(0xffffffffu, nvalid, d);
+    }
+    if (lane == 0) { s_red[0][warp] = mine; s_red[1][warp] = gated; s_red[2][warp] = nvalid; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t0 = 0, t1 = 0, t2 = 0;
+        for (int w = 0; w < kSweepTile / 32; ++w) { t0 += s_red[0][w]; t1 += s_red[1][w]; t2 += s_red[2][w]; }
+        a.tile_state[blockIdx.x] = t0;
+        atomicAdd(a.stats + 1, t1);
+        atomicAdd(a.stats + 2, t0 & 0xffffffffull);
+        atomicAdd(a.stats + 3, t2);
+        atomicAdd(a.n_emit, (uint32_t)(t0 >> 32));
+    }
+}
+
+constexpr uint32_t kEmitCap = 1024;  // write_best jobs a block balances through shared memory
+
+__global__ void __launch_bounds__(kSweepTile) k_emit_best(SweepArgs a) {
+    __shared__ unsigned long long s_warp[kSweepTile / 32];
+    __shared__ unsigned long long s_base;
+    __shared__ uint32_t s_n;
+    __shared__ uint4 s_job[kEmitCap];  // (position, cohesion d, coupling d, first record)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tile = blockIdx.x;
+    // the tile's prefix: its predecessors' (slow emitters, records) words
+    unsigned long long pre = 0;
+    for (uint32_t j = threadIdx.x; j < tile; j += kSweepTile) pre += a.tile_state[j];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) pre += __shfl_down_sync(0xffffffffu, pre, d);
+    if (lane == 0) s_warp[warp] = pre;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < kSweepTile / 32; ++w) t += s_warp[w];
+        s_base = t;
+    }
+    const uint64_t pos0 = (uint64_t)a.pos_begin + (uint64_t)tile * kOffTile + (uint64_t)threadIdx.x * kOffItems;
+    double thr_l = a.thr_lcom, thr_c = a.thr_cbo;
+    if (a.thr_device) { thr_l = a.dthr->lcom; thr_c = a.dthr->cbo; }
+    const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
+    const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
+    uint32_t cnt[kOffItems];
+    uint32_t fastm = 0;
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int it = 0; it < kOffItems; ++it) {
+        const uint64_t pos = pos0 + it;
+        cnt[it] = 0;
+        if (pos >= a.pos_end) continue;
+        uint4 v;
+        bool fast;
+        cnt[it] = best_count(a, pos, thr_l, thr_c, inter, v, fast, nullptr);
+        if (fast) fastm |= 1u << it;
+        mine += cnt[it] + ((cnt[it] && !fast) ? (1ull << 32) : 0ull);
+    }
+    unsigned long long inc = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+    }
+    __syncthreads();  // s_warp reused
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    unsigned long long at = s_base + inc - mine;
+#pragma unroll
+    for (int w = 0; w < kSweepTile / 32; ++w)
+        if (w < warp) at += s_warp[w];
+#pragma unroll
+    for (int it = 0; it < kOffItems; ++it) {
+        const uint64_t pos = pos0 + it;
+        if (!cnt[it]) continue;
+        uint4 v;
+        bool fast;
+        best_count(a, pos, thr_l, thr_c, inter, v, fast, nullptr);
+        const uint32_t first = (uint32_t)(at & 0xffffffffull);
+        if ((fastm >> it) & 1u) {
+            const uint32_t k = atomicAdd(&s_n, 1u);
+            if (k < kEmitCap) s_job[k] = make_uint4((uint32_t)pos, v.x, v.y, first);
+            else write_best(a, (uint32_t)pos, v.x, v.y, first);  // (a dense tile: past the shared list)
+        } else {
+            a.emitters[at >> 32] = make_uint4((uint32_t)pos, v.x, v.y, first);  // k_write
+        }
+        at += cnt[it] + (((fastm >> it) & 1u) ? 0ull : (1ull << 32));
+    }
+    __syncthreads();
+    const uint32_t n = min(s_n, kEmitCap);
+    for (uint32_t k = threadIdx.x; k < n; k += kSweepTile) {
+        const uint4 j = s_job[k];
+        write_best(a, j.x, j.y, j.z, j.w);
     }
 }
 
@@ -2022,17 +1999,6 @@ void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles,
 
 uint32_t offsets_tiles(uint64_t npos) { return (uint32_t)((npos + kOffTile - 1) / kOffTile); }
 
-void launch_score_lean(const SweepArgs& a, const uint4* cplan, uint32_t c_begin, uint32_t c_end,
-                       uint32_t fallback_tiles, cudaStream_t st) {
-    if (c_end > c_begin)
-        k_score_lean<<<(c_end - c_begin + kSLWarps - 1) / kSLWarps, kSLWarps * 32, 0, st>>>(a, cplan, c_begin, c_end);
-    if (!fallback_tiles) return;  // record-overflow members of lean classes (their list is built above)
-    SweepArgs b = a;
-    b.plist = nullptr;
-    if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<fallback_tiles, kSweepTile, 0, st>>>(b);
-    else k_score_thread<16, true><<<fallback_tiles, kSweepTile, 0, st>>>(b);
-}
-
 void launch_score_fast(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st) {
     if (n_tiles) k_score_fast<<<n_tiles, kSweepTile, 0, st>>>(a);
     if (!fallback_tiles) return;  // incomplete records (their list is built above)
@@ -2040,11 +2006,10 @@ void launch_score_fast(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_t
     else k_score_thread<16, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
 }
 
-void launch_score_list(const SweepArgs& a, cudaStream_t st) {
-    if (!a.n_plist) return;
-    const uint32_t tiles = (a.n_plist + kSweepTile - 1) / kSweepTile;
-    if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<tiles, kSweepTile, 0, st>>>(a);
-    else k_score_thread<16, true><<<tiles, kSweepTile, 0, st>>>(a);
+void launch_emit_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
+    if (!n_tiles) return;
+    k_tile_counts<<<n_tiles, kSweepTile, 0, st>>>(a);
+    k_emit_best<<<n_tiles, kSweepTile, 0, st>>>(a);
 }
 
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
@@ -2052,10 +2017,10 @@ void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     k_offsets<<<n_tiles, kSweepTile, 0, st>>>(a);
 }
 
-void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
+void launch_write(const SweepArgs& a, uint32_t n_tiles, bool fast_list, cudaStream_t st) {
     if (!n_tiles) return;
     const uint32_t grid = std::min<uint32_t>(n_tiles, 148 * 8);  // grid-stride over the emitter list
-    if (a.mode == 0) k_write_best<<<grid, kSweepTile, 0, st>>>(a);
+    if (a.mode == 0 && fast_list) k_write_best<<<grid, kSweepTile, 0, st>>>(a);
     if (a.maxdeg_fast <= 8) k_write<8><<<grid, kSweepTile, 0, st>>>(a);
     else k_write<16><<<grid, kSweepTile, 0, st>>>(a);
 }

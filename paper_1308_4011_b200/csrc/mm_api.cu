@@ -51,6 +51,7 @@ struct Ctl {  // small device-resident control block
     DevThresholds thr_aux;  // mm_sequential_mean / the similarity mean (never the metric pass's means)
     uint32_t n_groups;      // upload plan: k_class_group warps
     uint32_t n_solo;        // upload plan: lean classes for k_class_lean
+    uint32_t n_nl;          // upload plan: positions of the classes that are not lean
 };
 
 struct KStat {
@@ -147,13 +148,13 @@ struct mm_ctx {
     uint32_t n_lean = 0;       // classes k_class_lean handles (0 when lean_fused is off)
     DBuf<uint32_t> nl_pos;     // class-order positions of the other classes (k_method's list when mixed)
     uint32_t n_nl = 0;
-    std::vector<uint32_t> h_nl;  // host copy of nl_pos (sweep sub-ranges)
     bool group_on = true;        // env MMGPU_GROUP=0: every lean class on k_class_lean (warp per class)
     DBuf<uint2> groups;          // k_class_group: (first class, classes)
     DBuf<uint32_t> solo;         // lean classes outside the groups (member degree > 8)
     uint32_t n_groups = 0, n_solo = 0;
-    bool score_lean = false;     // env MMGPU_SCORE_LEAN=1: best-only scoring of lean classes warp per class (A/B)
     bool score_fast = true;      // env MMGPU_SCORE_FAST=0: best-only scoring on the general per-thread kernel
+    int prio_lo = 0, prio_hi = 0;  // stream priority range of the device
+    bool emit_best = true;         // env MMGPU_EMIT_BEST=0: best-only emission through the look-back scan
     DBuf<uint32_t> big_list;   // kKindWarpBig classes
     uint32_t n_big = 0;
     DBuf<uint32_t> large_list, foreign, cmaxdeg;
@@ -381,7 +382,11 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     ctx->device = device;
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+        // the side stream (threshold means beside the scoring kernel) at the
+        // highest priority: its cluster launch must not wait for the scoring
+        // kernel's blocks to drain
+        cudaDeviceGetStreamPriorityRange(&ctx->prio_lo, &ctx->prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, ctx->prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_metrics, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->ev_thr, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventRecord(ctx->ev_thr, ctx->side) != cudaSuccess ||
@@ -418,9 +423,9 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     if (const char* v = std::getenv("MMGPU_SCREEN")) ctx->screen_variant = (uint32_t)std::strtoul(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_FUSED")) ctx->fused_best = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_LEAN")) ctx->lean_fused = v[0] != '0';
-    if (const char* v = std::getenv("MMGPU_SCORE_LEAN")) ctx->score_lean = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_SCORE_FAST")) ctx->score_fast = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_GROUP")) ctx->group_on = v[0] != '0';
+    if (const char* v = std::getenv("MMGPU_EMIT_BEST")) ctx->emit_best = v[0] != '0';
     *out = ctx;
     return MM_OK;
 }
@@ -633,6 +638,13 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     });
     if (st) return st;
     const bool grouping = ctx->lean_fused && ctx->group_on;
+    if (ctx->lean_fused) {  // k_method's position list (classes that are not lean)
+        MM_CUDA(ctx, ctx->nl_pos.ensure(M ? M : 1));
+        st = run(ctx, "plan_nl", [&] {
+            launch_nl_positions(ctx->pos_owner.p, ctx->cplan.p, M, ctx->nl_pos.p, &ctl->n_nl, ctx->stream);
+        });
+        if (st) return st;
+    }
     if (grouping) {
         MM_CUDA(ctx, ctx->groups.ensure(C ? C : 1));
         MM_CUDA(ctx, ctx->solo.ensure(C ? C : 1));
@@ -654,21 +666,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     // lean classes take the fused method + class kernel; k_method then runs
     // only over the other classes' positions (a list, when there are both)
     ctx->n_lean = ctx->lean_fused ? C - h.n_large - h.n_big : 0;
-    ctx->n_nl = 0;
-    ctx->h_nl.clear();
-    if (ctx->n_lean && ctx->n_lean < C) {
-        std::vector<uint4> cp(C);
-        MM_CUDA(ctx, cudaMemcpy(cp.data(), ctx->cplan.p, sizeof(uint4) * C, cudaMemcpyDeviceToHost));
-        std::vector<uint32_t> nl;
-        for (uint32_t c = 0; c < C; ++c)
-            if (cp[c].w != kKindLean)
-                for (uint32_t k = 0; k < cp[c].y; ++k) nl.push_back(cp[c].x + k);
-        ctx->n_nl = (uint32_t)nl.size();
-        MM_CUDA(ctx, ctx->nl_pos.ensure(nl.size() ? nl.size() : 1));
-        if (!nl.empty())
-            MM_CUDA(ctx, cudaMemcpy(ctx->nl_pos.p, nl.data(), 4ull * nl.size(), cudaMemcpyHostToDevice));
-        ctx->h_nl = std::move(nl);
-    }
+    ctx->n_nl = ctx->lean_fused ? h.n_nl : 0;
     // methods the best-only screen may hand to the per-thread kernel: more edges
     // than a record's entries, or (class ids ≥ 2^24) any
     ctx->n_maybe_ovf = C >= (1u << 24) ? M : h.n_hideg;
@@ -1513,29 +1511,10 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
         }
         return MM_OK;
     }
-    // best-only on lean origin classes: warp per class, candidate per lane;
-    // the other classes' positions (a static list) on the per-thread kernel,
-    // concurrently on an auxiliary stream
-    const bool lean_score = mode == 0 && ctx->no_screen && ctx->score_lean && ctx->n_lean > 0;
     mm_status st = MM_OK;
-    if (lean_score) {
-        const auto i0 = std::lower_bound(ctx->h_nl.begin(), ctx->h_nl.end(), pb) - ctx->h_nl.begin();
-        const auto i1 = std::lower_bound(ctx->h_nl.begin(), ctx->h_nl.end(), pe) - ctx->h_nl.begin();
-        SweepArgs b = a;
-        b.plist = ctx->nl_pos.p + i0;
-        b.n_plist = (uint32_t)(i1 - i0);
-        cudaStream_t ls = ctx->aux[kMaxTiers + 2];
-        if (b.n_plist) {
-            MM_CUDA(ctx, cudaEventRecord(ctx->ev_fork0, ctx->stream));
-            MM_CUDA(ctx, cudaStreamWaitEvent(ls, ctx->ev_fork0, 0));
-            st = run_on(ctx, ls, "score_list", [&] { launch_score_list(b, ls); });
-            if (st) return st;
-            MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[kMaxTiers + 2], ls));
-        }
-        st = run(ctx, "score", [&] { launch_score_lean(a, ctx->cplan.p, cb, ce, fallback_tiles, ctx->stream); });
-        if (st) return st;
-        if (b.n_plist) MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[kMaxTiers + 2], 0));
-    } else if (mode == 0 && ctx->no_screen && ctx->score_fast) {
+    if (mode == 0 && ctx->no_screen && ctx->score_fast && (uint64_t)ctx->n_maybe_ovf * 8 <= npos) {
+        // (when many records may overflow — dense shapes — the general kernel
+        // in one pass beats the fast pass plus its fallback list)
         st = run(ctx, "score", [&] { launch_score_fast(a, n_tiles, fallback_tiles, ctx->stream); });
         if (st) return st;
     } else {
@@ -1544,10 +1523,17 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     }
     if (a.thr_device)
         if (mm_status s2 = join_thresholds(ctx)) return s2;
-    st = run(ctx, "offsets", [&] { launch_offsets(a, n_off, ctx->stream); });
-    if (st) return st;
-    st = run(ctx, "write", [&] { launch_write(a, n_tiles, ctx->stream); });
-    if (st) return st;
+    if (mode == 0 && ctx->emit_best) {  // best-only: tile counts + in-block emission, no look-back chain
+        st = run(ctx, "offsets", [&] { launch_emit_best(a, n_off, ctx->stream); });
+        if (st) return st;
+        st = run(ctx, "write", [&] { launch_write(a, n_tiles, false, ctx->stream); });
+        if (st) return st;
+    } else {
+        st = run(ctx, "offsets", [&] { launch_offsets(a, n_off, ctx->stream); });
+        if (st) return st;
+        st = run(ctx, "write", [&] { launch_write(a, n_tiles, true, ctx->stream); });
+        if (st) return st;
+    }
     ctx->sweep_valid = true;
     if (n_out) {
         mm_sweep_stats ss;
@@ -1610,7 +1596,7 @@ mm_status mm_run(mm_ctx* ctx, const mm_sweep_params* p) {
     ctx->capturing = false;
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
-    if (s2 || e != cudaSuccess || !g || cudaGraphInstantiate(&ctx->graph_exec, g, 0) != cudaSuccess) {
+    if (s2 || e != cudaSuccess || !g || cudaGraphInstantiate(&ctx->graph_exec, g, cudaGraphInstantiateFlagUseNodePriority) != cudaSuccess) {
         ctx->graph_disabled = true;  // keep running eagerly (the result above stands)
         ctx->graph_exec = nullptr;
         cudaGetLastError();

@@ -59,8 +59,6 @@ struct SweepArgs {
     uint32_t* n_fallback;
     uint32_t no_screen;         // 1: best-only mode on the per-thread kernel (A/B, MMGPU_NO_SCREEN)
     uint32_t screen_variant;    // MMGPU_SCREEN: 1 plain, 2 overlapped round trips (default)
-    const uint32_t* plist;      // k_score_thread list mode: a static position list (non-lean classes)
-    uint32_t n_plist;
 };
 
 void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t* bad, cudaStream_t st);
@@ -82,6 +80,8 @@ void launch_class_lean(const DevModel& s, const uint4* cplan, const uint4* cedge
 void launch_class_group(const DevModel& s, const uint4* cplan, const uint2* groups, uint32_t n_groups,
                         const uint32_t* pos_owner, MethRec* recs, ClassRec* rec, double* lcom, uint64_t* ck,
                         uint32_t* cbo, uint32_t* ux, uint32_t* un, cudaStream_t st);
+void launch_nl_positions(const uint32_t* pos_owner, const uint4* cplan, uint32_t M, uint32_t* out, uint32_t* n,
+                         cudaStream_t st);
 void launch_plan_groups(const uint4* cplan, const uint32_t* foreign, const uint32_t* cmaxdeg, uint32_t C,
                         uint2* groups, uint32_t* n_groups, uint32_t* solo, uint32_t* n_solo, cudaStream_t st);
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
@@ -141,12 +141,10 @@ void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles,
 // best-only mode in one pass (screen + gates + offsets + records); thresholds must be ready
 void launch_sweep_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 uint32_t offsets_tiles(uint64_t npos);
-void launch_score_lean(const SweepArgs& a, const uint4* cplan, uint32_t c_begin, uint32_t c_end,
-                       uint32_t fallback_tiles, cudaStream_t st);
-void launch_score_list(const SweepArgs& a, cudaStream_t st);
 void launch_score_fast(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st);
+void launch_emit_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
-void launch_write(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
+void launch_write(const SweepArgs& a, uint32_t n_tiles, bool fast_list, cudaStream_t st);
 constexpr uint32_t kSweepTile = 256;
 void launch_what_if(const DevModel& s, const ClassRec* rec, const uint32_t* ux, const uint32_t* un,
                     const uint32_t* dense, uint32_t u, uint32_t o, uint32_t d, mm_whatif* out, cudaStream_t st);
