@@ -126,6 +126,54 @@ def algorithmic_bytes(sys_, nnz_u: int, n_sugg: int, rank_share: float = 1.0) ->
     return k
 
 
+def tensor_roofline(sys_, ck_us: float) -> dict:
+    """k_ck_mma (classes with 128 ≤ M ≤ 3328 members and A ≤ 64 attributes): useful
+    int8 operations = 2·64 per member pair (the dot product of two 64-byte 0/1 rows),
+    executed = every 128×64×64 half-tile UMMA of the upper triangle."""
+    msz = np.diff(sys_.class_method_off).astype(np.int64)
+    asz = np.diff(sys_.class_attr_off).astype(np.int64)
+    sel = (msz >= 128) & (msz <= 3328) & (asz <= 64)
+    M = msz[sel]
+    useful = float((2 * 64 * M * (M - 1) // 2).sum())
+    T = (M + 127) // 128
+    executed = float((T * (T + 1) * 2 * 128 * 64 * 64).sum())
+    pk = ROOT / "profiles" / "r2_peaks.json"
+    peak = json.loads(pk.read_text()).get("i8_mma_tops") if pk.exists() else None
+    ach = useful / (ck_us * 1e-6) / 1e12
+    return {"kernel": "ck_mma", "bound": "tensor", "unit": "TOPS (int8)", "achieved": ach,
+            "executed": executed / (ck_us * 1e-6) / 1e12, "peak": peak,
+            "frac": (ach / peak) if peak else None, "classes": int(sel.sum()),
+            "peak_source": "profiles/r2_peaks.json (tools/peaks.cu: tcgen05.mma kind::i8 128x256x32, all SMs)",
+            "note": "in situ (concurrent with k_class_large on its own stream); the drain of the TMEM accumulator "
+                    "(one compare per pair) bounds it, not the tensor core"}
+
+
+def cpp_dropin_e2e():
+    """The C++ drop-in end to end (tools/e2e_cpp.cpp): the reference's SystemModel +
+    DependencyTable -> gpu::parallel_class_metrics + gpu::compute_thresholds +
+    gpu::suggest_all (free functions: one upload per call, as the reference takes
+    the model by const& each time) and the same calls on one resident gpu::Engine;
+    wall clock around complete calls (host vectors out), median of 10 steps."""
+    exe = ROOT / "tools" / "_build" / "e2e_cpp"
+    if not exe.exists():
+        return {"unavailable": "tools/_build/e2e_cpp not built (needs the reference headers at build time)"}
+    try:
+        r = subprocess.run([str(exe), "--steps", "10", "--warmup", "3"], capture_output=True, text=True, timeout=600)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except (subprocess.SubprocessError, ValueError, IndexError) as exc:
+        return {"unavailable": f"e2e_cpp failed: {exc}"}
+    if "error" in d:
+        return {"unavailable": d["error"]}
+    cand = d["candidates"]
+    return {"free_functions": {"ms_per_step": d["free_functions_ms"], "value": cand / (d["free_functions_ms"] / 1e3),
+                               "unit": UNIT, "uploads_per_step": 2},
+            "engine": {"ms_per_step": d["engine_ms"], "value": cand / (d["engine_ms"] / 1e3), "unit": UNIT,
+                       "uploads_per_step": 1},
+            "suggestions": d["suggestions"],
+            "path": "reference generate() -> SystemModel/DependencyTable -> gpu.hpp (flattening to CSR, H2D, "
+                    "metric pass, D2H, device means, sweep, D2H, std::vector<MoveSuggestion>)"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons around the timed region (B200_PROFILING.md).
 
@@ -466,6 +514,10 @@ def run_ours(args) -> None:
                 "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": dom_bytes,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6.65 TB/s"}
+    # the tensor-core LCOM-CK of dense classes against the measured tcgen05 kind::i8
+    # peak (tools/peaks.cu, profiles/r2_peaks.json)
+    if "ck_mma" in kern:
+        roofline["tensor"] = tensor_roofline(s, kern["ck_mma"]["avg_us"])
     # the metric pass: the lean-class kernel runs beside method + class pass when
     # both kinds of class exist, ahead of the class pass when every class is lean
     t_lean = kern.get("class_lean", {}).get("avg_us", 0.0)
@@ -476,6 +528,8 @@ def run_ours(args) -> None:
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather if world > 1 else None)
+        if e2e is not None and rank == 0 and world == 1 and args.config == "c4":
+            e2e["cpp_dropin"] = cpp_dropin_e2e()
 
     cb = None
     ingest = None

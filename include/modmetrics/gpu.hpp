@@ -33,10 +33,12 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <exception>
 #include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <modmetrics/metrics.hpp>
@@ -66,47 +68,148 @@ inline void check(mm_status st, const mm_ctx* ctx, const char* what) {
 }
 
 // SystemModel + DependencyTable -> CSR (mm_system points into this object)
+// Pinned host memory (mm_pinned_alloc), grown on demand and reused: the
+// flattened system is staged here so the upload copies at the link's full
+// rate instead of through the driver's pageable bounce buffers.
+class PinnedArena {
+public:
+    PinnedArena() = default;
+    PinnedArena(const PinnedArena&) = delete;
+    PinnedArena& operator=(const PinnedArena&) = delete;
+    PinnedArena(PinnedArena&& o) noexcept : p_(o.p_), cap_(o.cap_) { o.p_ = nullptr; o.cap_ = 0; }
+    PinnedArena& operator=(PinnedArena&& o) noexcept {
+        if (this != &o) {
+            if (p_) mm_pinned_free(p_);
+            p_ = o.p_; cap_ = o.cap_;
+            o.p_ = nullptr; o.cap_ = 0;
+        }
+        return *this;
+    }
+    ~PinnedArena() { if (p_) mm_pinned_free(p_); }
+    // n u32 slots per array, each array 64-byte aligned inside one block
+    uint32_t* reserve(const size_t* counts, size_t n_arrays, uint32_t** out) {
+        size_t total = 0;
+        for (size_t k = 0; k < n_arrays; ++k) total += (counts[k] + 15) & ~size_t(15);
+        if (total * 4 > cap_) {
+            if (p_) mm_pinned_free(p_);
+            p_ = nullptr;
+            cap_ = 0;
+            void* q = nullptr;
+            if (mm_pinned_alloc(total * 4 + (total * 4) / 8, &q) != MM_OK) throw std::bad_alloc();
+            p_ = q;
+            cap_ = total * 4 + (total * 4) / 8;
+        }
+        uint32_t* at = static_cast<uint32_t*>(p_);
+        for (size_t k = 0; k < n_arrays; ++k) {
+            out[k] = at;
+            at += (counts[k] + 15) & ~size_t(15);
+        }
+        return static_cast<uint32_t*>(p_);
+    }
+
+private:
+    void* p_ = nullptr;
+    size_t cap_ = 0;
+};
+
+// for_each over [0, n) on up to 16 host threads (worker exceptions rethrown
+// after every started thread joined)
+template <class Fn>
+inline void parallel_ranges(size_t n, Fn&& fn) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const size_t T = n >= (size_t(1) << 15) ? std::min<size_t>(16, hw ? hw : 1) : 1;
+    if (T <= 1) { fn(size_t(0), n); return; }
+    std::vector<std::exception_ptr> errs(T);
+    std::vector<std::thread> th;
+    th.reserve(T);
+    std::exception_ptr spawn_err;
+    for (size_t k = 0; k < T && !spawn_err; ++k) {
+        try {
+            th.emplace_back([&, k] {
+                try { fn(n * k / T, n * (k + 1) / T); } catch (...) { errs[k] = std::current_exception(); }
+            });
+        } catch (...) {
+            spawn_err = std::current_exception();
+        }
+    }
+    for (std::thread& t : th) t.join();
+    if (spawn_err) std::rethrow_exception(spawn_err);
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+}
+
+// The reference's vector-of-vectors model flattened to the CSR mm_upload
+// takes: exact sizes first, then every row copied in parallel straight into
+// pinned staging (arena) — or into owned vectors when no arena is given.
 struct Csr {
-    std::vector<uint32_t> cmo, cm, cao, ca, co, ct, ao, at;
+    std::vector<uint32_t> own;  // backing store without an arena
     mm_system sys{};
 
-    Csr(const SystemModel& model, const DependencyTable& deps) {
-        cmo.reserve(model.classes.size() + 1);
-        cao.reserve(model.classes.size() + 1);
-        cmo.push_back(0);
-        cao.push_back(0);
-        for (const ClassRecord& c : model.classes) {
-            cm.insert(cm.end(), c.method_ids.begin(), c.method_ids.end());
-            ca.insert(ca.end(), c.attribute_ids.begin(), c.attribute_ids.end());
-            cmo.push_back(static_cast<uint32_t>(cm.size()));
-            cao.push_back(static_cast<uint32_t>(ca.size()));
-        }
-        const size_t m = model.method_count();
+    Csr(const SystemModel& model, const DependencyTable& deps, PinnedArena* arena = nullptr) {
+        const size_t C = model.classes.size(), m = model.method_count(), A = model.attribute_count();
         if (deps.calls.size() != m || deps.accesses.size() != m)
             throw std::invalid_argument("gpu: dependency table rows != method count");
-        co.reserve(m + 1);
-        ao.reserve(m + 1);
-        co.push_back(0);
-        ao.push_back(0);
-        for (size_t p = 0; p < m; ++p) {
-            ct.insert(ct.end(), deps.calls[p].begin(), deps.calls[p].end());
-            at.insert(at.end(), deps.accesses[p].begin(), deps.accesses[p].end());
-            co.push_back(static_cast<uint32_t>(ct.size()));
-            ao.push_back(static_cast<uint32_t>(at.size()));
+        // offsets (sizes, then an exclusive scan)
+        std::vector<uint32_t> cmo(C + 1), cao(C + 1), co(m + 1), ao(m + 1);
+        parallel_ranges(C, [&](size_t b, size_t e) {
+            for (size_t c = b; c < e; ++c) {
+                cmo[c + 1] = static_cast<uint32_t>(model.classes[c].method_ids.size());
+                cao[c + 1] = static_cast<uint32_t>(model.classes[c].attribute_ids.size());
+            }
+        });
+        parallel_ranges(m, [&](size_t b, size_t e) {
+            for (size_t p = b; p < e; ++p) {
+                co[p + 1] = static_cast<uint32_t>(deps.calls[p].size());
+                ao[p + 1] = static_cast<uint32_t>(deps.accesses[p].size());
+            }
+        });
+        for (size_t c = 0; c < C; ++c) { cmo[c + 1] += cmo[c]; cao[c + 1] += cao[c]; }
+        for (size_t p = 0; p < m; ++p) { co[p + 1] += co[p]; ao[p + 1] += ao[p]; }
+        const size_t counts[10] = {C + 1, cmo[C], C + 1, cao[C], m + 1, co[m], m + 1, ao[m], m, A};
+        uint32_t* a[10];
+        if (arena) {
+            arena->reserve(counts, 10, a);
+        } else {
+            size_t total = 0;
+            for (size_t k = 0; k < 10; ++k) total += counts[k];
+            own.resize(total ? total : 1);
+            uint32_t* at = own.data();
+            for (size_t k = 0; k < 10; ++k) { a[k] = at; at += counts[k]; }
         }
-        sys.n_classes = static_cast<uint32_t>(model.classes.size());
+        std::copy(cmo.begin(), cmo.end(), a[0]);
+        std::copy(cao.begin(), cao.end(), a[2]);
+        std::copy(co.begin(), co.end(), a[4]);
+        std::copy(ao.begin(), ao.end(), a[6]);
+        parallel_ranges(C, [&](size_t b, size_t e) {
+            for (size_t c = b; c < e; ++c) {
+                const ClassRecord& r = model.classes[c];
+                std::copy(r.method_ids.begin(), r.method_ids.end(), a[1] + cmo[c]);
+                std::copy(r.attribute_ids.begin(), r.attribute_ids.end(), a[3] + cao[c]);
+            }
+        });
+        parallel_ranges(m, [&](size_t b, size_t e) {
+            for (size_t p = b; p < e; ++p) {
+                std::copy(deps.calls[p].begin(), deps.calls[p].end(), a[5] + co[p]);
+                std::copy(deps.accesses[p].begin(), deps.accesses[p].end(), a[7] + ao[p]);
+            }
+            std::copy(model.method_owner.begin() + b, model.method_owner.begin() + e, a[8] + b);
+        });
+        parallel_ranges(A, [&](size_t b, size_t e) {
+            std::copy(model.attribute_owner.begin() + b, model.attribute_owner.begin() + e, a[9] + b);
+        });
+        sys.n_classes = static_cast<uint32_t>(C);
         sys.n_methods = static_cast<uint32_t>(m);
-        sys.n_attributes = static_cast<uint32_t>(model.attribute_count());
-        sys.method_owner = model.method_owner.data();
-        sys.attribute_owner = model.attribute_owner.data();
-        sys.class_method_off = cmo.data();
-        sys.class_methods = cm.data();
-        sys.class_attr_off = cao.data();
-        sys.class_attrs = ca.data();
-        sys.call_off = co.data();
-        sys.call_tgt = ct.data();
-        sys.acc_off = ao.data();
-        sys.acc_tgt = at.data();
+        sys.n_attributes = static_cast<uint32_t>(A);
+        sys.class_method_off = a[0];
+        sys.class_methods = a[1];
+        sys.class_attr_off = a[2];
+        sys.class_attrs = a[3];
+        sys.call_off = a[4];
+        sys.call_tgt = a[5];
+        sys.acc_off = a[6];
+        sys.acc_tgt = a[7];
+        sys.method_owner = a[8];
+        sys.attribute_owner = a[9];
     }
 };
 
@@ -148,7 +251,7 @@ public:
 
     // Uploads (copies) the system into HBM; the model may be destroyed afterwards.
     void upload(const SystemModel& model, const DependencyTable& deps) {
-        const detail::Csr csr(model, deps);
+        const detail::Csr csr(model, deps, &stage_);
         detail::check(mm_upload(ctx_.get(), &csr.sys), ctx_.get(), "mm_upload");
         n_classes_ = csr.sys.n_classes;
         n_methods_ = csr.sys.n_methods;
@@ -343,7 +446,10 @@ public:
                           ctx_.get(), "suggest_by_similarity");
         std::vector<MoveSuggestion> out;
         out.reserve(raw.size());
-        for (const mm_suggestion& r : raw) out.push_back(detail::to_suggestion(r));
+        out.resize(raw.size());
+        detail::parallel_ranges(raw.size(), [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) out[i] = detail::to_suggestion(raw[i]);
+        });
         return out;
     }
 
@@ -373,6 +479,7 @@ private:
         void operator()(mm_ctx* c) const { mm_ctx_destroy(c); }
     };
     std::unique_ptr<mm_ctx, Del> ctx_;
+    detail::PinnedArena stage_;  // pinned staging of the flattened system, reused across uploads
     uint32_t n_classes_ = 0;
     uint32_t n_methods_ = 0;
 
@@ -396,7 +503,10 @@ private:
         detail::check(mm_set_gates(ctx_.get(), nullptr, nullptr), ctx_.get(), "mm_set_gates");
         std::vector<MoveSuggestion> out;
         out.reserve(raw.size());
-        for (const mm_suggestion& r : raw) out.push_back(detail::to_suggestion(r));
+        out.resize(raw.size());
+        detail::parallel_ranges(raw.size(), [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) out[i] = detail::to_suggestion(raw[i]);
+        });
         return out;
     }
 
@@ -462,7 +572,10 @@ public:
         if (n) check(mm_group_copy_suggestions(g_.get(), raw.data(), n, &n), "mm_group_copy_suggestions");
         std::vector<MoveSuggestion> out;
         out.reserve(raw.size());
-        for (const mm_suggestion& r : raw) out.push_back(detail::to_suggestion(r));
+        out.resize(raw.size());
+        detail::parallel_ranges(raw.size(), [&](size_t b, size_t e) {
+            for (size_t i = b; i < e; ++i) out[i] = detail::to_suggestion(raw[i]);
+        });
         return out;
     }
 

@@ -245,7 +245,10 @@ __device__ __forceinline__ void cas_sort(uint32_t& a, uint32_t& b) {
     b = hi;
 }
 
-__global__ void __launch_bounds__(kGroupWarps * 32)
+#ifndef MMGPU_GROUP_MINB
+#define MMGPU_GROUP_MINB 12
+#endif
+__global__ void __launch_bounds__(kGroupWarps * 32, MMGPU_GROUP_MINB)
 k_class_group(DevModel s, const uint4* __restrict__ cplan, const uint2* __restrict__ groups, uint32_t n_groups,
               const uint32_t* __restrict__ pos_owner, MethRec* __restrict__ recs, ClassRec* __restrict__ rec,
               double* __restrict__ lcom_out, uint64_t* __restrict__ ck_out, uint32_t* __restrict__ cbo_out,
@@ -279,27 +282,26 @@ k_class_group(DevModel s, const uint4* __restrict__ cplan, const uint2* __restri
     for (uint32_t j = lane; j < nc * kSigWords; j += 32) (&w.csig[0][0])[j] = 0;
     reinterpret_cast<uint4*>(w.ent[lane])[0] = make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4*>(w.ent[lane])[1] = make_uint4(0, 0, 0, 0);
-    // ---- edges: all targets, then all owners ----
+    // ---- edges: all targets, then all owners (branch-free: selected addresses, predicated loads) ----
     const uint32_t ncall = co1 - co, deg = ncall + (ao1 - ao);
     uint32_t key[kRecMaxEnt];
 #pragma unroll
     for (int k = 0; k < kRecMaxEnt; ++k) {
         const uint32_t e = (uint32_t)k;
-        key[k] = e < ncall ? __ldg(s.pc_tgt + co + e) : (e < deg ? __ldg(s.pa_tgt + ao + (e - ncall)) : 0u);
+        const uint32_t* src = e < ncall ? s.pc_tgt + co + e : s.pa_tgt + ao + (e - ncall);
+        key[k] = 0;
+        if (e < deg) key[k] = __ldg(src);
     }
     unsigned long long mask = 0;
 #pragma unroll
     for (int k = 0; k < kRecMaxEnt; ++k) {
         const uint32_t e = (uint32_t)k;
-        if (e < ncall) {
-            key[k] = __ldg(s.method_owner + key[k]) << 1;
-        } else if (e < deg) {
-            const uint2 ai = __ldg(s.attr_info + key[k]);
-            if (ai.x == c) mask |= 1ull << ai.y;  // lean: A ≤ 64
-            key[k] = (ai.x << 1) | 1u;
-        } else {
-            key[k] = kNone;
-        }
+        const bool isa = e >= ncall;
+        uint2 ai = make_uint2(kNone, 0u);
+        if (e < ncall) ai.x = __ldg(s.method_owner + key[k]);
+        if (isa && e < deg) ai = __ldg(s.attr_info + key[k]);
+        if (isa && ai.x == c) mask |= 1ull << ai.y;  // lean: A ≤ 64
+        key[k] = e < deg ? (ai.x << 1) | (isa ? 1u : 0u) : kNone;
     }
     // ---- sort (19-comparator network for 8), run-length encode ----
     cas_sort(key[0], key[2]); cas_sort(key[1], key[3]); cas_sort(key[4], key[6]); cas_sort(key[5], key[7]);
@@ -310,7 +312,7 @@ k_class_group(DevModel s, const uint4* __restrict__ cplan, const uint2* __restri
     cas_sort(key[1], key[2]); cas_sort(key[3], key[4]); cas_sort(key[5], key[6]);
     __syncwarp();
     const uint32_t ci = c - c0;
-    uint32_t n = 0, hown = 0, h = 0;
+    uint32_t n = 0, hown = 0, h = 0, own_seen = 0;
     bool ovf = false;
 #pragma unroll
     for (int k = 0; k < kRecMaxEnt; ++k) {
@@ -320,13 +322,11 @@ k_class_group(DevModel s, const uint4* __restrict__ cplan, const uint2* __restri
         if (k + 1 < kRecMaxEnt && key[k + 1] != kNone && (key[k + 1] >> 1) == X) continue;  // run continues
         w.ent[lane][n++] = (X << 8) | h;
         ovf |= X >= (1u << 24);
-        if (X == c) hown = h;
+        if (X == c) { hown = h; own_seen = 1; }
         h = 0;
     }
     // every (class, foreign X, member) once: compacted into 64 slots
-    uint32_t nf = 0;
-#pragma unroll 1
-    for (uint32_t k = 0; k < n; ++k) nf += (w.ent[lane][k] >> 8) != c;
+    const uint32_t nf = n - own_seen;
     uint32_t fo = nf;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {

@@ -30,6 +30,12 @@
 #ifndef MMGPU_SCORE_MINB
 #define MMGPU_SCORE_MINB 6
 #endif
+#ifndef MMGPU_FAST_FULLREC
+#define MMGPU_FAST_FULLREC 0
+#endif
+#ifndef MMGPU_FAST_MINB
+#define MMGPU_FAST_MINB 8
+#endif
 namespace mmg {
 
 namespace {
@@ -595,7 +601,7 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
 // (exact bitmap of a dense row, else the Bloom signature, the row only on a
 // positive). Argmin over (key, d) with strict < in ascending d
 // (suggest.hpp:180-184). Incomplete records go to k_score_thread's list.
-__global__ void __launch_bounds__(kSweepTile) k_score_fast(SweepArgs a) {
+__global__ void __launch_bounds__(kSweepTile, MMGPU_FAST_MINB) k_score_fast(SweepArgs a) {
     // the used list column-major in shared memory (thread t's k-th entry at
     // [k][t]: conflict-free), so the candidate and membership loops stay
     // rolled: small code, lanes of a warp in step
@@ -657,11 +663,36 @@ __global__ void __launch_bounds__(kSweepTile) k_score_fast(SweepArgs a) {
             }
             if (can_coup && (bd_coup == kNone || rd.cbo < bkp)) {  // cbo_dest_after == cbo_d when it passes
                 bool okc = true;
+#if MMGPU_FAST_FULLREC
+                // the signature words with the record's first half: one round trip
+                const uint4* qp = reinterpret_cast<const uint4*>(a.rec + d);
+                const uint4 q1 = __ldg(qp + 1), q2 = __ldg(qp + 2), q3 = __ldg(qp + 3);
+                const uint32_t sg[kSigWords] = {q1.z, q1.w, q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
+                auto word = [&](uint32_t w) {
+                    uint32_t v = sg[0];
+#pragma unroll
+                    for (int k = 1; k < kSigWords; ++k) v = (w == (uint32_t)k) ? sg[k] : v;
+                    return v;
+                };
+#pragma unroll 1
+                for (uint32_t j = 0; j < n && okc; ++j) {
+                    const uint32_t X = E[j * kSweepTile] >> 8;
+                    if (X == d) continue;
+                    if (rd.dense != kNone) {
+                        okc = (__ldg(a.dense + rd.dense + (X >> 5)) >> (X & 31)) & 1u;
+                    } else {
+                        const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
+                        okc = ((word(b1 >> 5) >> (b1 & 31)) & (word(b2 >> 5) >> (b2 & 31)) & 1u) &&
+                              urow_find(a.ux, rd.ubase, rd.cbo, X) >= 0;
+                    }
+                }
+#else
 #pragma unroll 1
                 for (uint32_t j = 0; j < n && okc; ++j) {
                     const uint32_t X = E[j * kSweepTile] >> 8;
                     if (X != d) okc = in_urow(a.rec, d, rd, a.ux, a.dense, X);
                 }
+#endif
                 if (okc) { bd_coup = d; bkp = rd.cbo; }
             }
         }
@@ -1665,143 +1696,6 @@ __global__ void __launch_bounds__(kSweepTile) k_offsets(SweepArgs a) {
     }
 }
 
-// Best-only mode (the bench step) without a look-back chain: pass 2a counts
-// each 4096-position tile's records under the class gates (one word per
-// tile), pass 2b gives every tile its prefix by summing its predecessors'
-// words (≤ a few hundred, one block reduction), re-derives the per-method
-// counts, scans them inside the block, and writes the records of complete-
-// record methods itself (write_best, balanced over the block through a
-// shared-memory list); the rest go to k_write's emitter list.
-__device__ __forceinline__ uint32_t best_count(const SweepArgs& a, uint64_t pos, double thr_l, double thr_c, bool inter,
-                                               uint4& v, bool& fast, unsigned long long* gated) {
-    v = a.res[pos];
-    const uint32_t o = __ldg(a.pos_owner + pos);
-    const bool gcoh = (a.crit & MM_CRIT_COHESION) && __ldg(a.lcom + o) > thr_l;
-    const bool gcoup = (a.crit & MM_CRIT_COUPLING) && (double)__ldg(a.cbo + o) > thr_c;
-    if (gated) *gated += v.z * ((gcoh ? 1u : 0u) + (gcoup ? 1u : 0u));
-    uint32_t count;
-    v = gate_result(a, v, gcoh, gcoup, inter, count);
-    fast = (v.w & kResFull) != 0;
-    return count;
-}
-
-__global__ void __launch_bounds__(kSweepTile) k_tile_counts(SweepArgs a) {
-    __shared__ unsigned long long s_red[3][kSweepTile / 32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t pos0 = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kOffTile + (uint64_t)threadIdx.x * kOffItems;
-    double thr_l = a.thr_lcom, thr_c = a.thr_cbo;
-    if (a.thr_device) { thr_l = a.dthr->lcom; thr_c = a.dthr->cbo; }
-    const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
-    const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
-    unsigned long long mine = 0, gated = 0, nvalid = 0;  // (slow emitters << 32) | records
-#pragma unroll
-    for (int it = 0; it < kOffItems; ++it) {
-        const uint64_t pos = pos0 + it;
-        if (pos >= a.pos_end) continue;
-        ++nvalid;
-        uint4 v;
-        bool fast;
-        const uint32_t count = best_count(a, pos, thr_l, thr_c, inter, v, fast, &gated);
-        mine += count + ((count && !fast) ? (1ull << 32) : 0ull);
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        mine += __shfl_down_sync(0xffffffffu, mine, d);
-        gated += __shfl_down_sync(0xffffffffu, gated, d);
-        nvalid += __shfl_down_sync(0xffffffffu, nvalid, d);
-    }
-    if (lane == 0) { s_red[0][warp] = mine; s_red[1][warp] = gated; s_red[2][warp] = nvalid; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long t0 = 0, t1 = 0, t2 = 0;
-        for (int w = 0; w < kSweepTile / 32; ++w) { t0 += s_red[0][w]; t1 += s_red[1][w]; t2 += s_red[2][w]; }
-        a.tile_state[blockIdx.x] = t0;
-        atomicAdd(a.stats + 1, t1);
-        atomicAdd(a.stats + 2, t0 & 0xffffffffull);
-        atomicAdd(a.stats + 3, t2);
-        atomicAdd(a.n_emit, (uint32_t)(t0 >> 32));
-    }
-}
-
-constexpr uint32_t kEmitCap = 1024;  // write_best jobs a block balances through shared memory
-
-__global__ void __launch_bounds__(kSweepTile) k_emit_best(SweepArgs a) {
-    __shared__ unsigned long long s_warp[kSweepTile / 32];
-    __shared__ unsigned long long s_base;
-    __shared__ uint32_t s_n;
-    __shared__ uint4 s_job[kEmitCap];  // (position, cohesion d, coupling d, first record)
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t tile = blockIdx.x;
-    // the tile's prefix: its predecessors' (slow emitters, records) words
-    unsigned long long pre = 0;
-    for (uint32_t j = threadIdx.x; j < tile; j += kSweepTile) pre += a.tile_state[j];
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) pre += __shfl_down_sync(0xffffffffu, pre, d);
-    if (lane == 0) s_warp[warp] = pre;
-    if (threadIdx.x == 0) s_n = 0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long t = 0;
-        for (int w = 0; w < kSweepTile / 32; ++w) t += s_warp[w];
-        s_base = t;
-    }
-    const uint64_t pos0 = (uint64_t)a.pos_begin + (uint64_t)tile * kOffTile + (uint64_t)threadIdx.x * kOffItems;
-    double thr_l = a.thr_lcom, thr_c = a.thr_cbo;
-    if (a.thr_device) { thr_l = a.dthr->lcom; thr_c = a.dthr->cbo; }
-    const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
-    const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
-    uint32_t cnt[kOffItems];
-    uint32_t fastm = 0;
-    unsigned long long mine = 0;
-#pragma unroll
-    for (int it = 0; it < kOffItems; ++it) {
-        const uint64_t pos = pos0 + it;
-        cnt[it] = 0;
-        if (pos >= a.pos_end) continue;
-        uint4 v;
-        bool fast;
-        cnt[it] = best_count(a, pos, thr_l, thr_c, inter, v, fast, nullptr);
-        if (fast) fastm |= 1u << it;
-        mine += cnt[it] + ((cnt[it] && !fast) ? (1ull << 32) : 0ull);
-    }
-    unsigned long long inc = mine;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += y;
-    }
-    __syncthreads();  // s_warp reused
-    if (lane == 31) s_warp[warp] = inc;
-    __syncthreads();
-    unsigned long long at = s_base + inc - mine;
-#pragma unroll
-    for (int w = 0; w < kSweepTile / 32; ++w)
-        if (w < warp) at += s_warp[w];
-#pragma unroll
-    for (int it = 0; it < kOffItems; ++it) {
-        const uint64_t pos = pos0 + it;
-        if (!cnt[it]) continue;
-        uint4 v;
-        bool fast;
-        best_count(a, pos, thr_l, thr_c, inter, v, fast, nullptr);
-        const uint32_t first = (uint32_t)(at & 0xffffffffull);
-        if ((fastm >> it) & 1u) {
-            const uint32_t k = atomicAdd(&s_n, 1u);
-            if (k < kEmitCap) s_job[k] = make_uint4((uint32_t)pos, v.x, v.y, first);
-            else write_best(a, (uint32_t)pos, v.x, v.y, first);  // (a dense tile: past the shared list)
-        } else {
-            a.emitters[at >> 32] = make_uint4((uint32_t)pos, v.x, v.y, first);  // k_write
-        }
-        at += cnt[it] + (((fastm >> it) & 1u) ? 0ull : (1ull << 32));
-    }
-    __syncthreads();
-    const uint32_t n = min(s_n, kEmitCap);
-    for (uint32_t k = threadIdx.x; k < n; k += kSweepTile) {
-        const uint4 j = s_job[k];
-        write_best(a, j.x, j.y, j.z, j.w);
-    }
-}
-
 // Pass 3: the emitting methods (compact list from pass 2) write their
 // records — exact what-if values — at their offsets. One thread per emitter.
 template <int K>
@@ -2004,12 +1898,6 @@ void launch_score_fast(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_t
     if (!fallback_tiles) return;  // incomplete records (their list is built above)
     if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
     else k_score_thread<16, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
-}
-
-void launch_emit_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
-    if (!n_tiles) return;
-    k_tile_counts<<<n_tiles, kSweepTile, 0, st>>>(a);
-    k_emit_best<<<n_tiles, kSweepTile, 0, st>>>(a);
 }
 
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {

@@ -154,7 +154,6 @@ struct mm_ctx {
     uint32_t n_groups = 0, n_solo = 0;
     bool score_fast = true;      // env MMGPU_SCORE_FAST=0: best-only scoring on the general per-thread kernel
     int prio_lo = 0, prio_hi = 0;  // stream priority range of the device
-    bool emit_best = true;         // env MMGPU_EMIT_BEST=0: best-only emission through the look-back scan
     DBuf<uint32_t> big_list;   // kKindWarpBig classes
     uint32_t n_big = 0;
     DBuf<uint32_t> large_list, foreign, cmaxdeg;
@@ -425,7 +424,6 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     if (const char* v = std::getenv("MMGPU_LEAN")) ctx->lean_fused = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_SCORE_FAST")) ctx->score_fast = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_GROUP")) ctx->group_on = v[0] != '0';
-    if (const char* v = std::getenv("MMGPU_EMIT_BEST")) ctx->emit_best = v[0] != '0';
     *out = ctx;
     return MM_OK;
 }
@@ -1523,17 +1521,10 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     }
     if (a.thr_device)
         if (mm_status s2 = join_thresholds(ctx)) return s2;
-    if (mode == 0 && ctx->emit_best) {  // best-only: tile counts + in-block emission, no look-back chain
-        st = run(ctx, "offsets", [&] { launch_emit_best(a, n_off, ctx->stream); });
-        if (st) return st;
-        st = run(ctx, "write", [&] { launch_write(a, n_tiles, false, ctx->stream); });
-        if (st) return st;
-    } else {
-        st = run(ctx, "offsets", [&] { launch_offsets(a, n_off, ctx->stream); });
-        if (st) return st;
-        st = run(ctx, "write", [&] { launch_write(a, n_tiles, true, ctx->stream); });
-        if (st) return st;
-    }
+    st = run(ctx, "offsets", [&] { launch_offsets(a, n_off, ctx->stream); });
+    if (st) return st;
+    st = run(ctx, "write", [&] { launch_write(a, n_tiles, true, ctx->stream); });
+    if (st) return st;
     ctx->sweep_valid = true;
     if (n_out) {
         mm_sweep_stats ss;

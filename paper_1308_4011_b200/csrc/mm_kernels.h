@@ -142,7 +142,6 @@ void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles,
 void launch_sweep_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 uint32_t offsets_tiles(uint64_t npos);
 void launch_score_fast(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st);
-void launch_emit_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 void launch_write(const SweepArgs& a, uint32_t n_tiles, bool fast_list, cudaStream_t st);
 constexpr uint32_t kSweepTile = 256;
