@@ -74,49 +74,78 @@ def dist_env():
     return rank, world, local
 
 
-def algorithmic_bytes(sys_, nnz_u: int, n_sugg: int, rank_share: float = 1.0) -> dict:
+def algorithmic_bytes(sys_, cbo, n_sugg: int, rank_share: float = 1.0) -> dict:
     """Compulsory bytes per launch of each kernel: every array the kernel must
-    touch, read or written once (DESIGN.md §4 derives each line). m, c, a =
+    touch, read or written once (DESIGN.md §4 derives each line), over the
+    classes that kernel actually serves (the upload plan's kinds, restated
+    here: CTA path M > 32 | A > 64 | member degree > 16; lean = the rest with
+    ≤ 32 foreign edges; group = lean with member degree ≤ 8). m, c, a =
     methods, classes, attributes; E = call + access edges; nnz = Σ cbo (U row
-    entries); S = emitted suggestion records; the sweep kernels scale with the
-    rank's share of methods."""
+    entries) of the kind; S = emitted suggestion records; the sweep kernels
+    scale with the rank's share of methods."""
     m, c, a = sys_.n_methods, sys_.n_classes, sys_.n_attributes
     E = sys_.n_calls + sys_.n_accesses
     ms = int(m * rank_share)
-    # classes on the CTA path (M > 32, A > 64 or a member of degree > 16), as mm_upload plans them
+    cbo = np.asarray(cbo, dtype=np.int64)
+    nnz_u = int(cbo.sum())
     msz = np.diff(sys_.class_method_off).astype(np.int64)
     asz = np.diff(sys_.class_attr_off).astype(np.int64)
     deg = (np.diff(sys_.call_off) + np.diff(sys_.acc_off)).astype(np.int64)
-    owner_of_pos = np.repeat(np.arange(c), msz)
+    pos_cls = np.repeat(np.arange(c), msz)                 # class of each class-order position
+    pdeg = deg[sys_.class_methods]
     maxdeg = np.zeros(c, np.int64)
-    np.maximum.at(maxdeg, owner_of_pos, deg[sys_.class_methods])
+    np.maximum.at(maxdeg, pos_cls, pdeg)
+    # foreign edges per class (owner of the target != own class)
+    own_of_method = np.empty(m, np.int64)
+    own_of_method[sys_.class_methods] = pos_cls
+    ce = np.repeat(np.arange(m), np.diff(sys_.call_off))
+    ae = np.repeat(np.arange(m), np.diff(sys_.acc_off))
+    fc = own_of_method[sys_.call_tgt] != own_of_method[ce]
+    aown = np.empty(a, np.int64)
+    aown[sys_.class_attrs] = np.repeat(np.arange(c), asz)
+    fa = aown[sys_.acc_tgt] != own_of_method[ae]
+    foreign = np.bincount(own_of_method[ce[fc]], minlength=c) + np.bincount(own_of_method[ae[fa]], minlength=c)
     large = (msz > 32) | (asz > 64) | (maxdeg > 16)
-    m_l, c_l, a_l = int(msz[large].sum()), int(large.sum()), int(asz[large].sum())
-    e_l = int(deg[sys_.class_methods][np.repeat(large, msz)].sum())
-    c_lean = c - c_l  # (the listed warp-path classes are counted as lean here: a small share)
-    m_lean, a_lean = m - m_l, a - a_l
-    e_lean = E - e_l
+    lean = ~large & (foreign <= 32)
+    big = ~large & ~lean
+    group = lean & (maxdeg <= 8)
+
+    def kind(sel):
+        mem = np.repeat(sel, msz)
+        return int(sel.sum()), int(msz[sel].sum()), int(asz[sel].sum()), int(pdeg[mem].sum()), int(cbo[sel].sum())
+
+    c_l, m_l, a_l, e_l, n_l = kind(large)
+    c_b, m_b, a_b, e_b, n_b = kind(big)
+    c_n, m_n, a_n, e_n, n_n = kind(lean)
+    c_g, m_g, a_g, e_g, n_g = kind(group)
     k = {
         # fused method + class pass of the lean classes: plan + edge ranges,
         # edge targets + member bytes, owner tables, records + headers, class
         # records + metrics, U rows
-        "class_lean": 32 * c_lean + 5 * e_lean + 4 * m_lean + 8 * a_lean + 36 * m_lean + 84 * c_lean + 8 * nnz_u,
+        "class_lean": 32 * c_n + 5 * e_n + 4 * m + 8 * a + 36 * m_n + 84 * c_n + 8 * n_n,
         # the same outputs from groups of lean classes per warp: plan, member
-        # rows (offsets + class), edge targets, owner tables, records +
-        # headers, class records + metrics, U rows
-        "class_group": 16 * c_lean + 12 * m_lean + 4 * e_lean + 4 * m_lean + 8 * a_lean + 36 * m_lean
-        + 84 * c_lean + 8 * nnz_u,
-        "class_large": 36 * m_l + 8 * e_l + 8 * a_l + 93 * c_l + 8 * nnz_u,
-        "method": 64 * m + 8 * a + 4 * E + 4 * c,
-        "class_small": 44 * m + 93 * c + 8 * nnz_u,
+        # rows (offsets + class), edge targets, owner tables (method owner,
+        # attr_info), records + headers, class records + metrics, U rows
+        "class_group": 16 * c_g + 12 * m_g + 4 * e_g + 4 * m + 8 * a + 36 * m_g + 84 * c_g + 8 * n_g,
+        # CTA path: member records + headers + own masks, plans / class
+        # records / metrics, U rows (CSR rows only for overflowed records)
+        "class_large": 44 * m_l + 93 * c_l + 8 * n_l,
+        # method pass over the classes that are not lean
+        "method": 64 * (m_l + m_b) + 8 * a + 4 * (e_l + e_b) + 4 * (c_l + c_b),
+        # listed warp path (the big warp-path classes)
+        "class_small": 44 * m_b + 93 * c_b + 8 * n_b,
         "thresholds": 12 * c,
         "score": 56 * ms + 64 * c + 4 * nnz_u,
         "offsets": 36 * ms + 12 * c,
         # emitters, method records, class records (origin + destination), records
         "write": 16 * n_sugg + 36 * n_sugg + 48 * n_sugg + 64 * n_sugg,
+        # tensor-core LCOM-CK reads each member's own mask once
+        "ck_mma": 8 * int(msz[(msz >= 128) & (msz <= 3328) & (asz <= 64)].sum()),
     }
-    # the class pass: the warp path and the CTA-path tiers, concurrent on their streams
-    k["class_pass"] = k["class_large"] + k["class_small"] - 8 * nnz_u
+    # the class pass: the CTA-path tiers, the listed warp path and the
+    # tensor-core LCOM-CK, concurrent on their streams
+    k["class_pass"] = k["class_large"] + k["class_small"] + k["ck_mma"]
+    k["plan_kinds"] = {"large": c_l, "big": c_b, "lean": c_n, "group": c_g}
     # SURVEY.md §8d layout-independent totals, for reference
     b_in = 4 * (2 * (m + 1) + E + m + a)
     b_cls = 4 * ((c + 1) + m + (c + 1) + a) + 24 * c
@@ -497,11 +526,11 @@ def run_ours(args) -> None:
     lcom, ck, cbo = eng.class_metrics_all()
     nnz_u = int(cbo.astype(np.int64).sum())
     share = 1.0 / world
-    ab = algorithmic_bytes(s, nnz_u, n_sugg_local, share)
+    ab = algorithmic_bytes(s, cbo, n_sugg_local, share)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     # the dominant unit per step: one kernel, or the class pass whose kernels overlap
-    units = [k for k in kern if k in ab and k not in ("class_small", "class_large")]
+    units = [k for k in kern if k in ab and k not in ("class_small", "class_large", "ck_mma")]
     dom = max(units, key=lambda k: kern[k]["avg_us"] * kern[k]["launches"])
     dom_bytes = ab[dom]
     dom_us = kern[dom]["avg_us"]

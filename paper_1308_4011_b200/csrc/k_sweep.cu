@@ -30,9 +30,6 @@
 #ifndef MMGPU_SCORE_MINB
 #define MMGPU_SCORE_MINB 6
 #endif
-#ifndef MMGPU_FAST_FULLREC
-#define MMGPU_FAST_FULLREC 0
-#endif
 #ifndef MMGPU_FAST_MINB
 #define MMGPU_FAST_MINB 8
 #endif
@@ -663,36 +660,11 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_FAST_MINB) k_score_fast(Swee
             }
             if (can_coup && (bd_coup == kNone || rd.cbo < bkp)) {  // cbo_dest_after == cbo_d when it passes
                 bool okc = true;
-#if MMGPU_FAST_FULLREC
-                // the signature words with the record's first half: one round trip
-                const uint4* qp = reinterpret_cast<const uint4*>(a.rec + d);
-                const uint4 q1 = __ldg(qp + 1), q2 = __ldg(qp + 2), q3 = __ldg(qp + 3);
-                const uint32_t sg[kSigWords] = {q1.z, q1.w, q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
-                auto word = [&](uint32_t w) {
-                    uint32_t v = sg[0];
-#pragma unroll
-                    for (int k = 1; k < kSigWords; ++k) v = (w == (uint32_t)k) ? sg[k] : v;
-                    return v;
-                };
-#pragma unroll 1
-                for (uint32_t j = 0; j < n && okc; ++j) {
-                    const uint32_t X = E[j * kSweepTile] >> 8;
-                    if (X == d) continue;
-                    if (rd.dense != kNone) {
-                        okc = (__ldg(a.dense + rd.dense + (X >> 5)) >> (X & 31)) & 1u;
-                    } else {
-                        const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
-                        okc = ((word(b1 >> 5) >> (b1 & 31)) & (word(b2 >> 5) >> (b2 & 31)) & 1u) &&
-                              urow_find(a.ux, rd.ubase, rd.cbo, X) >= 0;
-                    }
-                }
-#else
 #pragma unroll 1
                 for (uint32_t j = 0; j < n && okc; ++j) {
                     const uint32_t X = E[j * kSweepTile] >> 8;
                     if (X != d) okc = in_urow(a.rec, d, rd, a.ux, a.dense, X);
                 }
-#endif
                 if (okc) { bd_coup = d; bkp = rd.cbo; }
             }
         }

@@ -45,6 +45,9 @@ def main(rep, launches, out):
         tot = sum(v for _, v in st) or 1
         top = ", ".join(f"{k} {100 * v / tot:.0f}%" for k, v in sorted(st, key=lambda x: -x[1])[:3])
         lines.append(f"| {name} | " + " | ".join(vals) + f" | {top} |")
+    if launches == "-":  # no launch list for this capture
+        open(out, "w").write("\n".join(lines) + "\n")
+        return
     # launch list: per-kernel share of the serialized step
     per = defaultdict(list)
     rows = list(csv.reader(open(launches)))
