@@ -173,15 +173,33 @@ __global__ void __launch_bounds__(256) k_ck_mma(DevModel s, const uint32_t* __re
                 if (I == J && c0 + 32 <= 32 * quarter) continue;
                 uint32_t v[32];
                 tmem_ld32(tmem + ((32u * quarter) << 16) + c0, v);
-                if (I != J && c0 + 32 <= jlim) {
+                // every entry of the chunk counts: inside the valid columns and, on a
+                // diagonal tile, right of all of this warp's rows (warp-uniform)
+                if (c0 + 32 <= jlim && (I != J || c0 >= 32 * (quarter + 1))) {
+                    // nonzero count as Σ min(v, 1): two IMNMX and one IADD3 per pair of
+                    // entries instead of a compare and an add per entry
 #pragma unroll
-                    for (int t = 0; t < 32; ++t) qt += v[t] != 0u;
+                    for (int t = 0; t < 32; t += 2) {
+                        uint32_t a, b;  // (PTX min: kept as IMNMX, not re-derived into compares)
+                        asm("min.u32 %0, %1, 1;" : "=r"(a) : "r"(v[t]));
+                        asm("min.u32 %0, %1, 1;" : "=r"(b) : "r"(v[t + 1]));
+                        qt += a + b;
+                    }
                 } else {
+                    // this lane's valid columns t ∈ [lo, hi): j < jlim and, on a diagonal
+                    // tile, j > i; the nonzero pattern as a bit mask (IMNMX + LEA per
+                    // entry), counted once
+                    const uint32_t lo = (I == J) ? min(max(il + 1, c0) - c0, 32u) : 0u;
+                    const uint32_t hi = jlim > c0 ? min(jlim - c0, 32u) : 0u;
+                    const uint32_t keep = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((lo >= 32) ? 0xffffffffu : ((1u << lo) - 1u));
+                    uint32_t nz = 0;
 #pragma unroll
                     for (int t = 0; t < 32; ++t) {
-                        const uint32_t jl = c0 + t;
-                        qt += (v[t] != 0u && jl < jlim && (I != J || jl > il)) ? 1u : 0u;
+                        uint32_t a;
+                        asm("min.u32 %0, %1, 1;" : "=r"(a) : "r"(v[t]));
+                        nz += a << t;
                     }
+                    qt += __popc(nz & keep);
                 }
             }
             q += i < M ? qt : 0u;

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "mm_device.cuh"
 #include "mm_kernels.h"

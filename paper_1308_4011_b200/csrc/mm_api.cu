@@ -153,7 +153,6 @@ struct mm_ctx {
     DBuf<uint32_t> solo;         // lean classes outside the groups (member degree > 8)
     uint32_t n_groups = 0, n_solo = 0;
     bool score_fast = true;      // env MMGPU_SCORE_FAST=0: best-only scoring on the general per-thread kernel
-    bool score_fast_force = false;  // env MMGPU_SCORE_FAST=2: the fast kernel whatever the overflow bound
     int prio_lo = 0, prio_hi = 0;  // stream priority range of the device
     DBuf<uint32_t> big_list;   // kKindWarpBig classes
     uint32_t n_big = 0;
@@ -423,10 +422,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     if (const char* v = std::getenv("MMGPU_SCREEN")) ctx->screen_variant = (uint32_t)std::strtoul(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_FUSED")) ctx->fused_best = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_LEAN")) ctx->lean_fused = v[0] != '0';
-    if (const char* v = std::getenv("MMGPU_SCORE_FAST")) {
-        ctx->score_fast = v[0] != '0';
-        ctx->score_fast_force = v[0] == '2';
-    }
+    if (const char* v = std::getenv("MMGPU_SCORE_FAST")) ctx->score_fast = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_GROUP")) ctx->group_on = v[0] != '0';
     *out = ctx;
     return MM_OK;
@@ -1514,8 +1510,7 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
         return MM_OK;
     }
     mm_status st = MM_OK;
-    if (mode == 0 && ctx->no_screen && ctx->score_fast &&
-        (ctx->score_fast_force || (uint64_t)ctx->n_maybe_ovf * 8 <= npos)) {
+    if (mode == 0 && ctx->no_screen && ctx->score_fast && (uint64_t)ctx->n_maybe_ovf * 8 <= npos) {
         // (when many records may overflow — dense shapes — the general kernel
         // in one pass beats the fast pass plus its fallback list)
         st = run(ctx, "score", [&] { launch_score_fast(a, n_tiles, fallback_tiles, ctx->stream); });
