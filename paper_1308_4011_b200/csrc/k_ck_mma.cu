@@ -16,6 +16,8 @@
 // between 8-row groups (descriptor fields per cute/arch/mma_sm100_desc.hpp).
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cstdint>
 
 #include "mm_device.cuh"
@@ -226,8 +228,18 @@ uint32_t ck_mma_smem_bytes(uint32_t max_members) {
     return ((max_members + kTile - 1) / kTile) * kTile * kRowBytes;
 }
 
+// The attribute belongs to the function, process-wide, not to a context: a
+// later upload of a smaller system (another engine, another thread) must not
+// lower it under a launch planned with more. Raised only, never lowered.
 cudaError_t set_ck_mma_smem(uint32_t bytes) {
-    return cudaFuncSetAttribute(k_ck_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    static std::atomic<int> granted{0};
+    int cur = granted.load(std::memory_order_relaxed);
+    while ((int)bytes > cur) {
+        const cudaError_t e = cudaFuncSetAttribute(k_ck_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return e;
+        if (granted.compare_exchange_weak(cur, (int)bytes, std::memory_order_relaxed)) break;
+    }
+    return cudaSuccess;
 }
 
 void launch_ck_mma(const DevModel& s, const uint32_t* list, uint32_t n, uint32_t smem_bytes,

@@ -456,12 +456,29 @@ __global__ void k_plan_groups(const uint4* __restrict__ cplan, const uint32_t* _
         if (gn) groups[atomicAdd(n_groups, 1u)] = make_uint2(g0, gn);
         gn = gm = gf = 0;
     };
-    for (uint32_t c = cb; c < ce; ++c) {
-        const uint4 cp = cplan[c];
-        if (cp.w != kKindLean) { close(); continue; }
+    // the block's 16 plans first (independent loads), then the greedy walk on registers
+    uint32_t kind[16], mem[16], fr[16], md[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t c = cb + k;
+        kind[k] = kNone;
+        if (c < ce) {
+            const uint4 cp = cplan[c];
+            kind[k] = cp.w;
+            mem[k] = cp.y;
+            fr[k] = foreign[c];
+            md[k] = cmaxdeg[c];
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint32_t c = cb + k;
+        if (c >= ce) break;
+        if (kind[k] != kKindLean) { close(); continue; }
         // (group keys pack the class id in 22 bits)
-        if (cmaxdeg[c] > (uint32_t)kRecMaxEnt || C >= (1u << 22)) { close(); solo[atomicAdd(n_solo, 1u)] = c; continue; }
-        const uint32_t f = foreign[c];
+        if (md[k] > (uint32_t)kRecMaxEnt || C >= (1u << 22)) { close(); solo[atomicAdd(n_solo, 1u)] = c; continue; }
+        const uint4 cp = make_uint4(0, mem[k], 0, 0);
+        const uint32_t f = fr[k];
         if (gn && (gm + cp.y > 32u || gf + f > 64u || gn == 32u)) close();
         if (!gn) g0 = c;
         ++gn; gm += cp.y; gf += f;

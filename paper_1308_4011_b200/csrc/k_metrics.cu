@@ -14,6 +14,8 @@
 //             (metrics.hpp:167-185), built as the sorted U row with counts.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -1112,8 +1114,18 @@ void launch_giant_p1(const DevModel& s, const uint32_t* large_list, const LargeP
     if (!n_items) return;
     k_giant_p1<<<n_items, kGiantChunk, 0, st>>>(s, large_list, plan, items, recs, gcnt, gH, grows);
 }
+// The attribute belongs to the function, process-wide, not to a context: a
+// later upload of a smaller system (another engine, another thread) must not
+// lower it under a launch planned with more. Raised only, never lowered.
 cudaError_t set_class_large_smem(uint32_t bytes) {
-    return cudaFuncSetAttribute(k_class_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    static std::atomic<int> granted{0};
+    int cur = granted.load(std::memory_order_relaxed);
+    while ((int)bytes > cur) {
+        const cudaError_t e = cudaFuncSetAttribute(k_class_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return e;
+        if (granted.compare_exchange_weak(cur, (int)bytes, std::memory_order_relaxed)) break;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace mmg

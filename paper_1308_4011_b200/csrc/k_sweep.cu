@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(S
     __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
     uint64_t pos;
     bool live;
-    if (LIST) {  // the methods k_score_fast / k_screen handed over (record overflow)
+    if (LIST) {  // the methods k_score_fast handed over (record overflow)
         const uint32_t i = blockIdx.x * kSweepTile + threadIdx.x;
         live = i < *a.n_fallback;
         pos = live ? a.fallback[i] : 0;
@@ -672,790 +672,6 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_FAST_MINB) k_score_fast(Swee
     }
     const uint32_t wc = __reduce_add_sync(0xffffffffu, cands);
     if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
-}
-
-// Pass 1, best-only mode (the reference's default and the bench step): a
-// flattened candidate screen. Each warp takes 32 consecutive class-order
-// positions (one method per lane) and then spreads the warp's candidates
-// (u, d) over its lanes, one candidate per lane and iteration, so lanes never
-// idle on a neighbour's longer list. Per method (its own lane): the packed
-// used list from the method pass's record, the origin's counts, and — only
-// when the exact-rational pre-test h·M < H allows lcom(origin) to drop — the
-// two origin doubles. Per candidate lane: d's counts and lcom, the integer
-// pre-test h_u(d)·M_d > H_d (then the one fp64 division of lcom_dest_after),
-// and, if the method can lower the origin's cbo, the membership of every
-// other used class in U[d] (exact bitmap, or Bloom then the row). Per-method
-// argmin over (key, d) in ascending-d order with strict < (lowest d wins
-// ties, suggest.hpp:180-184) reads the candidates' results back from shared
-// memory. Methods whose used list did not fit their record are evaluated
-// afterwards by the whole warp, one at a time (screen_coop).
-constexpr int kScreenWarps = kSweepTile / 32;
-constexpr int kScreenSlots = 32 * kRecMaxEnt;  // candidates of one warp: ≤ 8 per method
-
-struct ScreenSmem {
-    uint32_t ent[kScreenWarps][32][kRecMaxEnt];   // the methods' used lists (X << 8 | h), own class included
-    uint8_t cm[kScreenWarps][kScreenSlots];       // candidate slot -> method lane
-    uint8_t ck[kScreenWarps][kScreenSlots];       // candidate slot -> list index
-    double kc[kScreenWarps][kScreenSlots];        // cohesion key (passing) or -1
-    uint32_t kp[kScreenWarps][kScreenSlots];      // coupling key cbo_d (passing) or kNone
-};
-
-// ascending bitonic sort of buf[0, N) (N a power of two), one warp
-__device__ __forceinline__ void warp_sort_u32(uint32_t* buf, uint32_t N, int lane) {
-    for (uint32_t k = 2; k <= N; k <<= 1)
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = lane; i < N; i += 32) {
-                const uint32_t ixj = i ^ j;
-                if (ixj > i) {
-                    const uint32_t x = buf[i], y = buf[ixj];
-                    if ((x > y) == ((i & k) == 0)) { buf[i] = y; buf[ixj] = x; }
-                }
-            }
-            __syncwarp();
-        }
-}
-
-constexpr uint32_t kCoopMaxDeg = 128;  // methods with more edges (hubs) take one lane's streaming path
-
-// Best-only evaluation of ONE method whose used list did not fit its record,
-// by the whole warp (all lanes call it with the same pos): the used list from
-// the CSR (lane per edge, warp sort, run-length -> classes and own-access
-// counts), the origin's removed count over lanes, then one destination per
-// lane and a warp argmin over (key, list index). `scr` holds ≥ 3·kCoopMaxDeg
-// words of this warp's shared memory.
-__device__ __noinline__ void screen_coop(const SweepArgs& a, uint32_t pos, uint32_t* scr, int lane, uint4& out) {
-    const uint32_t p = __ldg(a.s.cls_methods + pos), o = __ldg(a.pos_owner + pos);
-    const uint32_t cb = __ldg(a.s.call_off + p), nc = __ldg(a.s.call_off + p + 1) - cb;
-    const uint32_t ab = __ldg(a.s.acc_off + p), na = __ldg(a.s.acc_off + p + 1) - ab;
-    const uint32_t deg = nc + na;
-    uint32_t* key = scr;                      // owner << 1 | is_access, sorted
-    uint32_t* LX = scr + kCoopMaxDeg;         // distinct used classes, ascending
-    uint32_t* LH = scr + 2 * kCoopMaxDeg;     // accesses of the method owned by each
-    uint32_t N = 32;
-    while (N < deg) N <<= 1;
-    for (uint32_t k = lane; k < N; k += 32) {
-        uint32_t v = kNone;
-        if (k < nc) v = __ldg(a.s.method_owner + __ldg(a.s.call_tgt + cb + k)) << 1;
-        else if (k < deg) v = (__ldg(a.s.attr_info + __ldg(a.s.acc_tgt + ab + (k - nc))).x << 1) | 1u;
-        key[k] = v;
-    }
-    __syncwarp();
-    warp_sort_u32(key, N, lane);
-    uint32_t n = 0;
-    for (uint32_t k0 = 0; k0 < deg; k0 += 32) {
-        const uint32_t k = k0 + lane;
-        const bool head = k < deg && (k == 0 || (key[k] >> 1) != (key[k - 1] >> 1));
-        const uint32_t hb = __ballot_sync(0xffffffffu, head);
-        if (head) {
-            const uint32_t X = key[k] >> 1;
-            uint32_t h = 0, e = k;
-            while (e < deg && (key[e] >> 1) == X) h += key[e++] & 1u;
-            const uint32_t idx = n + __popc(hb & ((1u << lane) - 1));
-            LX[idx] = X;
-            LH[idx] = h;
-        }
-        n += __popc(hb);
-    }
-    __syncwarp();
-    // origin: own-access count, removed count (U[o][X] == 1) over lanes
-    const ClassRec ro = load_rec(a.rec, o);
-    uint32_t hown = 0, removed = 0, own_used = 0;
-    for (uint32_t k = lane; k < n; k += 32) {
-        const uint32_t X = LX[k];
-        if (X == o) { hown = LH[k]; own_used = 1; continue; }
-        if (ro.dense != kNone) {
-            removed += (__ldg(a.dense + ro.dense + (a.s.C + 31) / 32 + (X >> 5)) >> (X & 31)) & 1u;
-        } else {
-            const int q = urow_find(a.ux, ro.ubase, ro.cbo, X);
-            if (q >= 0 && __ldg(a.un + ro.ubase + q) == 1u) ++removed;
-        }
-    }
-    hown = __reduce_max_sync(0xffffffffu, hown);
-    removed = __reduce_add_sync(0xffffffffu, removed);
-    own_used = __reduce_or_sync(0xffffffffu, own_used);
-    const Origin org = make_origin(ro, hown, removed);
-    const bool can_coup = org.co_a < org.co_b;
-    // destinations: one per lane
-    double bk = 0.0;
-    uint32_t bki = kNone, bp = 0, bpi = kNone;
-    if (org.coh_ok || can_coup)
-        for (uint32_t k = lane; k < n; k += 32) {
-            const uint32_t d = LX[k];
-            if (d == o) continue;
-            const ClassRec rd = load_rec(a.rec, d);
-            double ld_a;
-            if (org.coh_ok && coh_dest(rd, LH[k], ld_a)) {
-                const double kc = __dadd_rn(org.lo_a, ld_a);
-                if (bki == kNone || kc < bk) { bk = kc; bki = k; }
-            }
-            if (can_coup) {
-                bool ok = true;
-                for (uint32_t j = 0; j < n && ok; ++j) {
-                    const uint32_t X = LX[j];
-                    if (X != d && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ok = false;
-                }
-                if (ok && (bpi == kNone || rd.cbo < bp)) { bp = rd.cbo; bpi = k; }
-            }
-        }
-    // warp argmin over (key, list index): lowest d wins ties (suggest.hpp:180-184)
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const double ok_ = __shfl_xor_sync(0xffffffffu, bk, off);
-        const uint32_t oi = __shfl_xor_sync(0xffffffffu, bki, off);
-        if (oi != kNone && (bki == kNone || ok_ < bk || (ok_ == bk && oi < bki))) { bk = ok_; bki = oi; }
-        const uint32_t op = __shfl_xor_sync(0xffffffffu, bp, off);
-        const uint32_t opi = __shfl_xor_sync(0xffffffffu, bpi, off);
-        if (opi != kNone && (bpi == kNone || op < bp || (op == bp && opi < bpi))) { bp = op; bpi = opi; }
-    }
-    out = make_uint4(bki == kNone ? kNone : LX[bki], bpi == kNone ? kNone : LX[bpi], n - own_used, 0);
-    __syncwarp();
-}
-
-// one hub method (more than kCoopMaxDeg edges) on one lane, streaming used list
-__device__ __noinline__ uint4 screen_stream_one(const SweepArgs& a, uint32_t ps, uint32_t pm) {
-    const uint32_t o = __ldg(a.pos_owner + ps);
-    StreamEnum sen;
-    sen.S.init(a.s, pm);
-    const ClassRec ro = load_rec(a.rec, o);
-    const Origin org = make_origin(ro, sen.hits(o), removed_count(ro, a.ux, a.un, a.dense, a.s.C, sen, o));
-    const MethodResult r = evaluate(a, sen, o, org, true, true);
-    return make_uint4(r.bd_coh, r.bd_coup, r.cands, 0);
-}
-
-// the warp's methods whose used list did not fit their record (ovf lanes):
-// one at a time by the whole warp; hubs beyond kCoopMaxDeg edges by their own
-// lane on the streaming used list. Returns this lane's (bd_coh, bd_coup,
-// candidates) when it is an ovf lane.
-__device__ __forceinline__ uint4 screen_overflow(const SweepArgs& a, bool ovf, uint64_t pos, uint32_t* scr,
-                                                 int lane) {
-    uint4 mine = make_uint4(kNone, kNone, 0, 0);
-    uint32_t ob = __ballot_sync(0xffffffffu, ovf);
-    while (ob) {
-        const int src = __ffs(ob) - 1;
-        ob &= ob - 1;
-        const uint32_t ps = __shfl_sync(0xffffffffu, (uint32_t)pos, src);
-        const uint32_t pm = __ldg(a.s.cls_methods + ps);
-        const uint32_t deg = (__ldg(a.s.call_off + pm + 1) - __ldg(a.s.call_off + pm)) +
-                             (__ldg(a.s.acc_off + pm + 1) - __ldg(a.s.acc_off + pm));
-        if (deg <= kCoopMaxDeg) {
-            uint4 r;
-            screen_coop(a, ps, scr, lane, r);
-            if (lane == src) mine = r;
-        } else if (lane == src) {
-            mine = screen_stream_one(a, ps, pm);
-        }
-        __syncwarp();
-    }
-    return mine;
-}
-
-__global__ void __launch_bounds__(kSweepTile, 4) k_screen(SweepArgs a) {
-    __shared__ ScreenSmem sm;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
-    const bool live = pos < a.pos_end;
-    uint32_t (*ent)[kRecMaxEnt] = sm.ent[warp];
-    uint8_t* cm = sm.cm[warp];
-    uint8_t* ck = sm.ck[warp];
-    double* kc = sm.kc[warp];
-    uint32_t* kp = sm.kp[warp];
-
-    // ---- per method (this lane)
-    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
-    uint32_t o = 0, hdr = 0;
-    if (live) {
-        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
-        r0 = rp[0];
-        r1 = rp[1];
-        hdr = rec_hdrs(a.recs, a.s.M)[pos];
-        o = __ldg(a.pos_owner + pos);
-    }
-    const bool ovf = live && (hdr & kRecOverflow);
-    const uint32_t n = (live && !ovf) ? rec_n(hdr) : 0u;
-    {
-        const uint32_t e7[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-        for (int k = 0; k < kRecMaxEnt; ++k) ent[lane][k] = e7[k];
-    }
-    uint32_t nc = 0;  // candidates: list entries other than the own class
-#pragma unroll
-    for (int k = 0; k < kRecMaxEnt; ++k) nc += (k < (int)n && (ent[lane][k] >> 8) != o);
-    // origin
-    bool coh_ok = false, can_coup = false;
-    double lo_a = 0.0;
-    if (n) {
-        const ClassRec ro = load_rec(a.rec, o);
-        const uint32_t h = rec_hown(hdr);
-        const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
-                                                            : removed_from_list(ro, a.ux, a.un, a.dense, a.s.C,
-                                                                                ent[lane], n, o);
-        can_coup = removed > 0;  // cbo_origin_after < cbo_origin_before
-        // lcom(A, M-1, H-h) < lcom(A, M, H): impossible when A == 0 (both 0.0)
-        // or, with exact denominators and M ≥ 2, when (H-h)·M ≤ H·(M-1)
-        bool maybe = ro.A != 0 && ro.M != 0;
-        if (maybe && ro.M >= 2 && (uint64_t)ro.A * ro.M < kExact53) maybe = (uint64_t)h * ro.M < ro.H;
-        if (maybe) {
-            lo_a = lcom_of(ro.A, (uint64_t)ro.M - 1, (uint64_t)ro.H - h);
-            coh_ok = lo_a < __ldg(a.dlcom + o);
-        }
-    }
-    // candidate slots: this method's at [excl, excl + nc), list order (d ascending)
-    uint32_t incl = nc;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += y;
-    }
-    const uint32_t excl = incl - nc;
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    {
-        uint32_t w = excl;
-#pragma unroll
-        for (int k = 0; k < kRecMaxEnt; ++k)
-            if (k < (int)n && (ent[lane][k] >> 8) != o) {
-                cm[w] = (uint8_t)lane;
-                ck[w] = (uint8_t)k;
-                ++w;
-            }
-    }
-    const uint32_t flags = (coh_ok ? 1u : 0u) | (can_coup ? 2u : 0u);
-    __syncwarp();
-
-    // ---- per candidate (one per lane and round)
-    for (uint32_t c0 = 0; c0 < total; c0 += 32) {
-        const uint32_t c = c0 + lane;
-        const bool act = c < total;
-        const uint32_t m = act ? cm[c] : 0u;
-        const uint32_t mflags = __shfl_sync(0xffffffffu, flags, m);
-        const double m_lo_a = __shfl_sync(0xffffffffu, lo_a, m);
-        const uint32_t m_n = __shfl_sync(0xffffffffu, n, m);
-        if (!act) continue;
-        const uint32_t e = ent[m][ck[c]];
-        const uint32_t d = e >> 8, hd = e & 0xffu;
-        double key = -1.0;
-        uint32_t kpv = kNone;
-        if (mflags) {
-            const ClassRec rd = load_rec(a.rec, d);
-            if ((mflags & 1u) && rd.A != 0 && rd.M != 0) {
-                const bool exact = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
-                if (!exact || (uint64_t)hd * rd.M > rd.H) {
-                    const double ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
-                    if (ld_a < __ldg(a.dlcom + d)) key = __dadd_rn(m_lo_a, ld_a);  // lcom_key, suggest.hpp:194-196
-                }
-            }
-            if (mflags & 2u) {
-                bool ok = true;
-                for (uint32_t j = 0; j < m_n && ok; ++j) {
-                    const uint32_t X = ent[m][j] >> 8;
-                    if (X != d && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ok = false;
-                }
-                if (ok) kpv = rd.cbo;  // cbo_dest_after == cbo_dest_before when it passes
-            }
-        }
-        kc[c] = key;
-        kp[c] = kpv;
-    }
-    __syncwarp();
-
-    // ---- per method: argmin over its slots (d ascending, strict <)
-    uint32_t bd_coh = kNone, bd_coup = kNone;
-    double bk = 0.0;
-    uint32_t bp = 0;
-    for (uint32_t j = 0; j < nc; ++j) {
-        const uint32_t slot = excl + j;
-        const double kcv = kc[slot];
-        const uint32_t kpv = kp[slot];
-        if (kcv >= 0.0 || kpv != kNone) {
-            const uint32_t d = ent[lane][ck[slot]] >> 8;
-            if (kcv >= 0.0 && (bd_coh == kNone || kcv < bk)) { bd_coh = d; bk = kcv; }
-            if (kpv != kNone && (bd_coup == kNone || kpv < bp)) { bd_coup = d; bp = kpv; }
-        }
-    }
-    if (live && !ovf) a.res[pos] = make_uint4(bd_coh, bd_coup, nc, 0);
-    const uint32_t wc = __reduce_add_sync(0xffffffffu, nc);
-    if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
-    __syncwarp();
-    const uint4 ov = screen_overflow(a, ovf, pos, reinterpret_cast<uint32_t*>(kc), lane);  // kc: free now
-    if (ovf) {
-        a.res[pos] = ov;
-        if (ov.z) atomicAdd(a.stats + 0, (unsigned long long)ov.z);
-    }
-}
-
-// Variant 2 of the screen (MMGPU_SCREEN=2): the same decisions with the
-// memory round trips overlapped — the origin's record is requested before the
-// candidate slots are built, the first round's destination records before the
-// origin's doubles are computed, and the Bloom words of every other used class
-// are requested together (predicated, no early exit), the U rows only probed
-// for Bloom positives.
-#ifndef MMGPU_SCREEN_MINB
-#define MMGPU_SCREEN_MINB 4
-#endif
-__device__ __forceinline__ bool bloom_word_test(const ClassRec* __restrict__ rec, uint32_t d, uint32_t X) {
-    const uint32_t b1 = bloom_h1(X), b2 = bloom_h2(X);
-    const uint32_t w1 = __ldg(rec[d].sig + (b1 >> 5)), w2 = __ldg(rec[d].sig + (b2 >> 5));
-    return ((w1 >> (b1 & 31)) & (w2 >> (b2 & 31)) & 1u) != 0;
-}
-
-__global__ void __launch_bounds__(kSweepTile, MMGPU_SCREEN_MINB) k_screen2(SweepArgs a) {
-    __shared__ ScreenSmem sm;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
-    const bool live = pos < a.pos_end;
-    uint32_t (*ent)[kRecMaxEnt] = sm.ent[warp];
-    uint8_t* cm = sm.cm[warp];
-    uint8_t* ck = sm.ck[warp];
-    double* kc = sm.kc[warp];
-    uint32_t* kp = sm.kp[warp];
-
-    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
-    uint32_t o = 0, hdr = 0;
-    if (live) {
-        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
-        r0 = rp[0];
-        r1 = rp[1];
-        hdr = rec_hdrs(a.recs, a.s.M)[pos];
-        o = __ldg(a.pos_owner + pos);
-    }
-    const bool ovf = live && (hdr & kRecOverflow);
-    const uint32_t n = (live && !ovf) ? rec_n(hdr) : 0u;
-    // the origin's record and lcom: in flight while the slots are built
-    ClassRec ro{};
-    double dlo = 0.0;
-    if (n) {
-        ro = load_rec(a.rec, o);
-        dlo = __ldg(a.dlcom + o);
-    }
-    {
-        const uint32_t e7[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-        for (int k = 0; k < kRecMaxEnt; ++k) ent[lane][k] = e7[k];
-    }
-    uint32_t nc = 0;
-#pragma unroll
-    for (int k = 0; k < kRecMaxEnt; ++k) nc += (k < (int)n && (ent[lane][k] >> 8) != o);
-    uint32_t incl = nc;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += y;
-    }
-    const uint32_t excl = incl - nc;
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    {
-        uint32_t w = excl;
-#pragma unroll
-        for (int k = 0; k < kRecMaxEnt; ++k)
-            if (k < (int)n && (ent[lane][k] >> 8) != o) {
-                cm[w] = (uint8_t)lane;
-                ck[w] = (uint8_t)k;
-                ++w;
-            }
-    }
-    __syncwarp();
-    // the first round's destination: record and lcom requested before the origin math
-    uint32_t c = lane, m = 0, d = 0, hd = 0;
-    ClassRec rd{};
-    double dld = 0.0;
-    auto fetch = [&]() {
-        if (c < total) {
-            m = cm[c];
-            const uint32_t e = ent[m][ck[c]];
-            d = e >> 8;
-            hd = e & 0xffu;
-            rd = load_rec(a.rec, d);
-            dld = __ldg(a.dlcom + d);
-        }
-    };
-    fetch();
-    // origin (this lane's method)
-    bool coh_ok = false, can_coup = false;
-    double lo_a = 0.0;
-    if (n) {
-        const uint32_t h = rec_hown(hdr);
-        const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
-                                                            : removed_from_list(ro, a.ux, a.un, a.dense, a.s.C,
-                                                                                ent[lane], n, o);
-        can_coup = removed > 0;
-        bool maybe = ro.A != 0 && ro.M != 0;
-        if (maybe && ro.M >= 2 && (uint64_t)ro.A * ro.M < kExact53) maybe = (uint64_t)h * ro.M < ro.H;
-        if (maybe) {
-            lo_a = lcom_of(ro.A, (uint64_t)ro.M - 1, (uint64_t)ro.H - h);
-            coh_ok = lo_a < dlo;
-        }
-    }
-    const uint32_t flags = (coh_ok ? 1u : 0u) | (can_coup ? 2u : 0u);
-    for (uint32_t c0 = 0; c0 < total; c0 += 32) {
-        const bool act = c < total;
-        const uint32_t mflags = __shfl_sync(0xffffffffu, flags, act ? m : 0);
-        const double m_lo_a = __shfl_sync(0xffffffffu, lo_a, act ? m : 0);
-        const uint32_t m_n = __shfl_sync(0xffffffffu, n, act ? m : 0);
-        if (act) {
-            double key = -1.0;
-            uint32_t kpv = kNone;
-            if ((mflags & 1u) && rd.A != 0 && rd.M != 0) {
-                const bool exact = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
-                if (!exact || (uint64_t)hd * rd.M > rd.H) {
-                    const double ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
-                    if (ld_a < dld) key = __dadd_rn(m_lo_a, ld_a);  // lcom_key, suggest.hpp:194-196
-                }
-            }
-            if (mflags & 2u) {
-                // every other used class must be in U[d]: all Bloom words at once
-                bool ok = true;
-                uint32_t probe = 0;
-                if (rd.dense != kNone) {
-#pragma unroll
-                    for (int j = 0; j < kRecMaxEnt; ++j)
-                        if (j < (int)m_n) {
-                            const uint32_t X = ent[m][j] >> 8;
-                            if (X != d) ok &= ((__ldg(a.dense + rd.dense + (X >> 5)) >> (X & 31)) & 1u) != 0;
-                        }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < kRecMaxEnt; ++j)
-                        if (j < (int)m_n) {
-                            const uint32_t X = ent[m][j] >> 8;
-                            if (X != d) {
-                                if (bloom_word_test(a.rec, d, X)) probe |= 1u << j;
-                                else ok = false;
-                            }
-                        }
-                    for (int j = 0; ok && probe; ++j, probe >>= 1)
-                        if (probe & 1u) ok = urow_find(a.ux, rd.ubase, rd.cbo, ent[m][j] >> 8) >= 0;
-                }
-                if (ok) kpv = rd.cbo;
-            }
-            kc[c] = key;
-            kp[c] = kpv;
-        }
-        c += 32;
-        fetch();
-    }
-    __syncwarp();
-    uint32_t bd_coh = kNone, bd_coup = kNone;
-    double bk = 0.0;
-    uint32_t bp = 0;
-    for (uint32_t j = 0; j < nc; ++j) {
-        const uint32_t slot = excl + j;
-        const double kcv = kc[slot];
-        const uint32_t kpv = kp[slot];
-        if (kcv >= 0.0 || kpv != kNone) {
-            const uint32_t dd = ent[lane][ck[slot]] >> 8;
-            if (kcv >= 0.0 && (bd_coh == kNone || kcv < bk)) { bd_coh = dd; bk = kcv; }
-            if (kpv != kNone && (bd_coup == kNone || kpv < bp)) { bd_coup = dd; bp = kpv; }
-        }
-    }
-    if (live && !ovf) a.res[pos] = make_uint4(bd_coh, bd_coup, nc, 0);
-    const uint32_t wc = __reduce_add_sync(0xffffffffu, nc);
-    if (lane == 0 && wc) atomicAdd(a.stats + 0, (unsigned long long)wc);
-    __syncwarp();
-    const uint4 ov = screen_overflow(a, ovf, pos, reinterpret_cast<uint32_t*>(kc), lane);  // kc: free now
-    if (ovf) {
-        a.res[pos] = ov;
-        if (ov.z) atomicAdd(a.stats + 0, (unsigned long long)ov.z);
-    }
-}
-
-// ---- best-only mode, fused: screen + gates + offsets + records in one pass
-//
-// The class gates need the threshold means, which the metric pass now
-// computes before the sweep, so the whole best-only sweep runs as one kernel:
-// each CTA takes the next 256 class-order positions (dynamic tile id), screens
-// them exactly as k_screen, applies the gates (suggest.hpp:246, :273) and the
-// criteria merge (:315-341) per method, scans the record counts over the CTA
-// and a decoupled look-back over the preceding tiles (relaxed gpu-scope
-// 64-bit words: flag | emitters << 32 | records), publishes its inclusive
-// prefix, and only then writes its records (what-if values recomputed from the
-// class tables, suggest.hpp:87-122): emission never delays a successor's
-// look-back. No per-method result array, no emitter list, no extra launch.
-
-// decoupled look-back by warp 0 of the CTA: returns (lane 0) the exclusive
-// prefix of this tile and publishes tile_state[tile] = prefix | (excl + agg)
-__device__ __forceinline__ unsigned long long tile_lookback(const SweepArgs& a, uint32_t tile, unsigned long long agg,
-                                                            int lane) {
-    unsigned long long excl = 0;
-    if (tile == 0) {
-        if (lane == 0) st_relaxed_u64(a.tile_state, kFlagPrefix | agg);
-        return 0;
-    }
-    if (lane == 0) st_relaxed_u64(a.tile_state + tile, kFlagAgg | agg);
-    int base = (int)tile - 1;
-    while (true) {
-        const int j = base - lane;
-        const unsigned long long v = j >= 0 ? ld_relaxed_u64(a.tile_state + j) : kFlagPrefix;
-        const unsigned long long f = v & ~kValMask;
-        const uint32_t bP = __ballot_sync(0xffffffffu, f == kFlagPrefix);
-        const uint32_t bZ = __ballot_sync(0xffffffffu, f == 0);
-        const int lim = bP ? __ffs(bP) - 1 : 31;
-        const uint32_t need = lim == 31 ? 0xffffffffu : ((2u << lim) - 1);
-        if (bZ & need) continue;
-        unsigned long long part = lane <= lim ? (v & kValMask) : 0ull;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) part += __shfl_down_sync(0xffffffffu, part, d);
-        excl += __shfl_sync(0xffffffffu, part, 0);
-        if (bP) break;
-        base -= 32;
-    }
-    if (lane == 0) st_relaxed_u64(a.tile_state + tile, kFlagPrefix | (excl + agg));
-    return excl;
-}
-
-// one method's records (best-only; destinations bdc / bdp gated already) from
-// its packed used list; destinations ascending, suggest_all's tags
-__device__ __noinline__ void emit_best(const SweepArgs& a, uint32_t pos, uint32_t o, uint32_t hdr, const uint32_t* ent,
-                                       uint32_t n, uint32_t bdc, uint32_t bdp, bool inter, uint64_t at) {
-    const uint32_t p = __ldg(a.s.cls_methods + pos);
-    const ClassRec ro = load_rec(a.rec, o);
-    const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
-                                                       : removed_from_list(ro, a.ux, a.un, a.dense, a.s.C, ent, n, o);
-    const Origin org = make_origin(ro, rec_hown(hdr), removed);
-    uint32_t ds[2];
-    int nd = 0;
-    if (inter) {
-        ds[nd++] = bdc;  // bdc == bdp here
-    } else {
-        const uint32_t x = bdc < bdp ? bdc : bdp, y = bdc < bdp ? bdp : bdc;  // kNone sorts last
-        if (x != kNone) ds[nd++] = x;
-        if (y != kNone && y != x) ds[nd++] = y;
-    }
-    for (int i = 0; i < nd; ++i) {
-        const uint32_t d = ds[i];
-        uint32_t hd = 0;
-        for (uint32_t k = 0; k < n; ++k)
-            if ((ent[k] >> 8) == d) hd = ent[k] & 0xffu;
-        const ClassRec rd = load_rec(a.rec, d);
-        uint32_t miss = 0;
-        for (uint32_t k = 0; k < n; ++k) {
-            const uint32_t X = ent[k] >> 8;
-            if (X != d && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ++miss;
-        }
-        mm_suggestion r;
-        r.lcom_origin_before = org.lo_b;
-        r.lcom_origin_after = org.lo_a;
-        r.lcom_dest_before = lcom_of(rd.A, rd.M, rd.H);
-        r.lcom_dest_after = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
-        r.method = p;
-        r.origin = o;
-        r.destination = d;
-        r.cbo_origin_before = org.co_b;
-        r.cbo_origin_after = org.co_a;
-        r.cbo_dest_before = rd.cbo;
-        r.cbo_dest_after = rd.cbo + miss;
-        r.criteria = (uint8_t)((d == bdc ? MM_CRIT_COHESION : 0u) | (d == bdp ? MM_CRIT_COUPLING : 0u));
-        r.origin_degenerate_after = org.odeg;
-        r.dest_degenerate_after = rd.A == 0;
-        r.pad = 0;
-        store_record(a.out + at + i, r);
-    }
-}
-
-// the same for a method whose used list overflowed its record (streaming list)
-__device__ __noinline__ void emit_best_stream(const SweepArgs& a, uint32_t pos, uint32_t o, uint32_t bdc,
-                                              uint32_t bdp, uint64_t at) {
-    const uint32_t p = __ldg(a.s.cls_methods + pos);
-    StreamEnum sen;
-    sen.S.init(a.s, p);
-    const ClassRec ro = load_rec(a.rec, o);
-    const Origin org = make_origin(ro, sen.hits(o), removed_count(ro, a.ux, a.un, a.dense, a.s.C, sen, o));
-    MethodResult res{};
-    res.bd_coh = bdc;
-    res.bd_coup = bdp;
-    emit(a, sen, p, o, org, res, at);
-}
-
-__global__ void __launch_bounds__(kSweepTile, 4) k_sweep_best(SweepArgs a) {
-    __shared__ ScreenSmem sm;
-    __shared__ uint32_t s_tile;
-    __shared__ unsigned long long s_warp[kScreenWarps], s_red[2][kScreenWarps];
-    __shared__ unsigned long long s_excl;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint64_t pos = (uint64_t)a.pos_begin + (uint64_t)tile * kSweepTile + threadIdx.x;
-    const bool live = pos < a.pos_end;
-    uint32_t (*ent)[kRecMaxEnt] = sm.ent[warp];
-    uint8_t* cm = sm.cm[warp];
-    uint8_t* ck = sm.ck[warp];
-    double* kc = sm.kc[warp];
-    uint32_t* kp = sm.kp[warp];
-
-    // ---- screen (as k_screen)
-    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = make_uint4(0, 0, 0, 0);
-    uint32_t o = 0, hdr = 0;
-    if (live) {
-        const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
-        r0 = rp[0];
-        r1 = rp[1];
-        hdr = rec_hdrs(a.recs, a.s.M)[pos];
-        o = __ldg(a.pos_owner + pos);
-    }
-    const bool ovf = live && (hdr & kRecOverflow);
-    const uint32_t n = (live && !ovf) ? rec_n(hdr) : 0u;
-    {
-        const uint32_t e8[kRecMaxEnt] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-        for (int k = 0; k < kRecMaxEnt; ++k) ent[lane][k] = e8[k];
-    }
-    uint32_t nc = 0;
-#pragma unroll
-    for (int k = 0; k < kRecMaxEnt; ++k) nc += (k < (int)n && (ent[lane][k] >> 8) != o);
-    bool coh_ok = false, can_coup = false;
-    double lo_a = 0.0;
-    if (n) {
-        const ClassRec ro = load_rec(a.rec, o);
-        const uint32_t h = rec_hown(hdr);
-        const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
-                                                           : removed_from_list(ro, a.ux, a.un, a.dense, a.s.C,
-                                                                               ent[lane], n, o);
-        can_coup = removed > 0;
-        bool maybe = ro.A != 0 && ro.M != 0;
-        if (maybe && ro.M >= 2 && (uint64_t)ro.A * ro.M < kExact53) maybe = (uint64_t)h * ro.M < ro.H;
-        if (maybe) {
-            lo_a = lcom_of(ro.A, (uint64_t)ro.M - 1, (uint64_t)ro.H - h);
-            coh_ok = lo_a < __ldg(a.dlcom + o);
-        }
-    }
-    uint32_t incl = nc;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += y;
-    }
-    const uint32_t excl_c = incl - nc;
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    {
-        uint32_t w = excl_c;
-#pragma unroll
-        for (int k = 0; k < kRecMaxEnt; ++k)
-            if (k < (int)n && (ent[lane][k] >> 8) != o) {
-                cm[w] = (uint8_t)lane;
-                ck[w] = (uint8_t)k;
-                ++w;
-            }
-    }
-    const uint32_t flags = (coh_ok ? 1u : 0u) | (can_coup ? 2u : 0u);
-    __syncwarp();
-    for (uint32_t c0 = 0; c0 < total; c0 += 32) {
-        const uint32_t c = c0 + lane;
-        const bool act = c < total;
-        const uint32_t m = act ? cm[c] : 0u;
-        const uint32_t mflags = __shfl_sync(0xffffffffu, flags, m);
-        const double m_lo_a = __shfl_sync(0xffffffffu, lo_a, m);
-        const uint32_t m_n = __shfl_sync(0xffffffffu, n, m);
-        if (!act) continue;
-        const uint32_t e = ent[m][ck[c]];
-        const uint32_t d = e >> 8, hd = e & 0xffu;
-        double key = -1.0;
-        uint32_t kpv = kNone;
-        if (mflags) {
-            const ClassRec rd = load_rec(a.rec, d);
-            if ((mflags & 1u) && rd.A != 0 && rd.M != 0) {
-                const bool exact = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
-                if (!exact || (uint64_t)hd * rd.M > rd.H) {
-                    const double ld_a = lcom_of(rd.A, (uint64_t)rd.M + 1, (uint64_t)rd.H + hd);
-                    if (ld_a < __ldg(a.dlcom + d)) key = __dadd_rn(m_lo_a, ld_a);
-                }
-            }
-            if (mflags & 2u) {
-                bool ok = true;
-                for (uint32_t j = 0; j < m_n && ok; ++j) {
-                    const uint32_t X = ent[m][j] >> 8;
-                    if (X != d && !in_urow(a.rec, d, rd, a.ux, a.dense, X)) ok = false;
-                }
-                if (ok) kpv = rd.cbo;
-            }
-        }
-        kc[c] = key;
-        kp[c] = kpv;
-    }
-    __syncwarp();
-    uint32_t bdc = kNone, bdp = kNone;
-    {
-        double bk = 0.0;
-        uint32_t bp = 0;
-        for (uint32_t j = 0; j < nc; ++j) {
-            const uint32_t slot = excl_c + j;
-            const double kcv = kc[slot];
-            const uint32_t kpv = kp[slot];
-            if (kcv >= 0.0 || kpv != kNone) {
-                const uint32_t dd = ent[lane][ck[slot]] >> 8;
-                if (kcv >= 0.0 && (bdc == kNone || kcv < bk)) { bdc = dd; bk = kcv; }
-                if (kpv != kNone && (bdp == kNone || kpv < bp)) { bdp = dd; bp = kpv; }
-            }
-        }
-    }
-    __syncwarp();
-    uint32_t cands = nc;
-    {
-        const uint4 ov = screen_overflow(a, ovf, pos, reinterpret_cast<uint32_t*>(kc), lane);
-        if (ovf) { bdc = ov.x; bdp = ov.y; cands = ov.z; }
-    }
-    // ---- gates and the criteria merge
-    double thr_l = a.thr_lcom, thr_c = a.thr_cbo;
-    if (a.thr_device) { thr_l = a.dthr->lcom; thr_c = a.dthr->cbo; }
-    const bool both = (a.crit & MM_CRIT_COHESION) && (a.crit & MM_CRIT_COUPLING);
-    const bool inter = a.combine == MM_COMBINE_INTERSECTION && both;
-    uint32_t count = 0;
-    unsigned long long gated = 0;
-    if (live) {
-        const bool gcoh = (a.crit & MM_CRIT_COHESION) && __ldg(a.lcom + o) > thr_l;
-        const bool gcoup = (a.crit & MM_CRIT_COUPLING) && (double)__ldg(a.cbo + o) > thr_c;
-        gated = (unsigned long long)cands * ((gcoh ? 1u : 0u) + (gcoup ? 1u : 0u));
-        if (!gcoh) bdc = kNone;
-        if (!gcoup) bdp = kNone;
-        const bool same = bdc != kNone && bdc == bdp;
-        count = inter ? (same ? 1u : 0u) : (uint32_t)(bdc != kNone) + (uint32_t)(bdp != kNone) - (same ? 1u : 0u);
-    }
-    // ---- CTA scan of (emitters << 32 | records), look-back, publish
-    const unsigned long long mine = count + (count ? (1ull << 32) : 0ull);
-    unsigned long long inc = mine;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += y;
-    }
-    if (lane == 31) s_warp[warp] = inc;
-    {
-        unsigned long long g0 = gated, g1 = cands;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            g0 += __shfl_down_sync(0xffffffffu, g0, d);
-            g1 += __shfl_down_sync(0xffffffffu, g1, d);
-        }
-        if (lane == 0) { s_red[0][warp] = g0; s_red[1][warp] = g1; }
-    }
-    __syncthreads();
-    unsigned long long before = 0, agg = 0;
-#pragma unroll
-    for (int w = 0; w < kScreenWarps; ++w) {
-        if (w < warp) before += s_warp[w];
-        agg += s_warp[w];
-    }
-    if (warp == 0) {
-        const unsigned long long ex = tile_lookback(a, tile, agg, lane);
-        if (lane == 0) {
-            s_excl = ex;
-            unsigned long long t0 = 0, t1 = 0;
-            for (int w = 0; w < kScreenWarps; ++w) { t0 += s_red[0][w]; t1 += s_red[1][w]; }
-            if (t1) atomicAdd(a.stats + 0, t1);
-            if (t0) atomicAdd(a.stats + 1, t0);
-            if (agg & 0xffffffffull) atomicAdd(a.stats + 2, agg & 0xffffffffull);
-            const uint64_t t0pos = (uint64_t)a.pos_begin + (uint64_t)tile * kSweepTile;
-            const uint64_t rest = a.pos_end > t0pos ? a.pos_end - t0pos : 0;
-            const uint64_t nvalid = rest < kSweepTile ? rest : (uint64_t)kSweepTile;
-            atomicAdd(a.stats + 3, (unsigned long long)nvalid);
-            atomicAdd(a.n_emit, (uint32_t)(agg >> 32));
-        }
-    }
-    __syncthreads();
-    // ---- records (the tile's prefix is already published)
-    if (count) {
-        const uint64_t at = (s_excl + before + inc - mine) & 0xffffffffull;
-        if (!ovf) emit_best(a, (uint32_t)pos, o, hdr, ent[lane], n, bdc, bdp, inter, at);
-        else emit_best_stream(a, (uint32_t)pos, o, bdc, bdp, at);
-    }
 }
 
 // Pass 2: apply the class gates (suggest.hpp:246, :273) and the criteria
@@ -1846,19 +1062,8 @@ __global__ void __launch_bounds__(kSweepTile) k_sim_emit(SweepArgs a, SimCrit sc
 
 }  // namespace
 
-void launch_sweep_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
+void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     if (!n_tiles) return;
-    k_sweep_best<<<n_tiles, kSweepTile, 0, st>>>(a);
-}
-
-void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st) {
-    if (!n_tiles) return;
-    if (a.mode == 0 && !a.no_screen) {
-        if (a.screen_variant == 1) k_screen<<<n_tiles, kSweepTile, 0, st>>>(a);
-        else k_screen2<<<n_tiles, kSweepTile, 0, st>>>(a);
-        (void)fallback_tiles;  // record-overflow methods are handled inside the screen (warp-cooperative)
-        return;
-    }
     if (a.maxdeg_fast <= 8) k_score_thread<8><<<n_tiles, kSweepTile, 0, st>>>(a);
     else k_score_thread<16><<<n_tiles, kSweepTile, 0, st>>>(a);
 }

@@ -44,7 +44,7 @@ struct Ctl {  // small device-resident control block
     uint32_t err;
     uint32_t n_emit;
     uint32_t n_wide;    // top-k / all-candidates methods with >= 32 used classes (side table)
-    uint32_t n_fallback;  // best-only screen: methods handed to the per-thread kernel
+    uint32_t n_fallback;  // best-only: methods k_score_fast handed to the per-thread kernel
     uint32_t n_hideg;     // upload plan: methods with more than kRecMaxEnt edges
     unsigned long long stats[4];
     DevThresholds thr;
@@ -180,11 +180,8 @@ struct mm_ctx {
     DBuf<uint4> res;
     DBuf<uint4> emit_list;  // compact emitter records (k_offsets -> k_write)
     DBuf<uint4> wide_cnt;  // top-k / all-candidates: pass counts of methods with >= 32 used classes
-    DBuf<uint32_t> fallback;  // best-only screen: record-overflow positions
-    bool no_screen = true;    // env MMGPU_NO_SCREEN=0: best-only mode on the flattened screen (A/B; slower in situ)
+    DBuf<uint32_t> fallback;  // best-only: record-overflow positions (k_score_fast -> k_score_thread)
     bool thr_side = true;     // env MMGPU_THR_SIDE=0: threshold means on the main stream, ahead of the sweep
-    uint32_t screen_variant = 2;  // env MMGPU_SCREEN (A/B of the best-only screen)
-    bool fused_best = true;       // env MMGPU_FUSED=0: best-only mode as screen + offsets + write
     DBuf<double> gate_lcom;
     DBuf<uint32_t> gate_cbo;
     bool gates_set = false;
@@ -417,10 +414,7 @@ mm_status mm_ctx_create(int device, mm_ctx** out) {
     if (const char* v = std::getenv("MMGPU_HIST_MAX_BYTES")) ctx->hist_max_bytes = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_GIANT_MIN")) ctx->giant_min = std::strtoull(v, nullptr, 10);
     if (const char* v = std::getenv("MMGPU_CK_MMA_MIN")) ctx->ck_mma_min = std::strtoull(v, nullptr, 10);
-    if (const char* v = std::getenv("MMGPU_NO_SCREEN")) ctx->no_screen = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_THR_SIDE")) ctx->thr_side = v[0] != '0';
-    if (const char* v = std::getenv("MMGPU_SCREEN")) ctx->screen_variant = (uint32_t)std::strtoul(v, nullptr, 10);
-    if (const char* v = std::getenv("MMGPU_FUSED")) ctx->fused_best = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_LEAN")) ctx->lean_fused = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_SCORE_FAST")) ctx->score_fast = v[0] != '0';
     if (const char* v = std::getenv("MMGPU_GROUP")) ctx->group_on = v[0] != '0';
@@ -665,7 +659,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     // only over the other classes' positions (a list, when there are both)
     ctx->n_lean = ctx->lean_fused ? C - h.n_large - h.n_big : 0;
     ctx->n_nl = ctx->lean_fused ? h.n_nl : 0;
-    // methods the best-only screen may hand to the per-thread kernel: more edges
+    // methods k_score_fast may hand to the per-thread kernel: more edges
     // than a record's entries, or (class ids ≥ 2^24) any
     ctx->n_maybe_ovf = C >= (1u << 24) ? M : h.n_hideg;
     if (ctx->n_large) {
@@ -1438,9 +1432,7 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     MM_CUDA(ctx, ctx->out.ensure(cap));
     const uint32_t n_tiles = (uint32_t)((npos + kSweepTile - 1) / kSweepTile);
     const uint32_t n_off = offsets_tiles(npos);
-    // best-only mode runs fused (screen + gates + offsets + records in one pass)
-    const bool fused = mode == 0 && !ctx->no_screen && ctx->fused_best;
-    const uint32_t n_state = fused ? n_tiles : n_off;
+    const uint32_t n_state = n_off;
     MM_CUDA(ctx, ctx->tile_state.ensure(n_state ? n_state : 1));
     MM_CUDA(ctx, ctx->res.ensure(npos ? npos : 1));
     MM_CUDA(ctx, ctx->emit_list.ensure(npos ? npos : 1));
@@ -1494,29 +1486,14 @@ mm_status mm_sweep(mm_ctx* ctx, const mm_sweep_params* p, uint64_t* n_out) {
     a.dlcom = ctx->lcom.p;
     a.fallback = ctx->fallback.p;
     a.n_fallback = &ctl->n_fallback;
-    a.no_screen = ctx->no_screen ? 1u : 0u;
-    a.screen_variant = ctx->screen_variant;
-    if (fused) {
-        if (a.thr_device)
-            if (mm_status s2 = join_thresholds(ctx)) return s2;
-        mm_status st = run(ctx, "sweep_best", [&] { launch_sweep_best(a, n_tiles, ctx->stream); });
-        if (st) return st;
-        ctx->sweep_valid = true;
-        if (n_out) {
-            mm_sweep_stats ss;
-            if (mm_status s2 = mm_sweep_stats_get(ctx, &ss)) return s2;
-            *n_out = ss.suggestions;
-        }
-        return MM_OK;
-    }
     mm_status st = MM_OK;
-    if (mode == 0 && ctx->no_screen && ctx->score_fast && (uint64_t)ctx->n_maybe_ovf * 8 <= npos) {
+    if (mode == 0 && ctx->score_fast && (uint64_t)ctx->n_maybe_ovf * 8 <= npos) {
         // (when many records may overflow — dense shapes — the general kernel
         // in one pass beats the fast pass plus its fallback list)
         st = run(ctx, "score", [&] { launch_score_fast(a, n_tiles, fallback_tiles, ctx->stream); });
         if (st) return st;
     } else {
-        st = run(ctx, "score", [&] { launch_score(a, n_tiles, fallback_tiles, ctx->stream); });
+        st = run(ctx, "score", [&] { launch_score(a, n_tiles, ctx->stream); });
         if (st) return st;
     }
     if (a.thr_device)

@@ -55,10 +55,8 @@ struct SweepArgs {
     uint4* wide_cnt;            // top-k / all modes: counts of methods with ≥ 32 used classes
     uint32_t* n_wide;           // their number
     const double* dlcom;        // the metric pass's lcom per class (lcom_normalized; not the gates)
-    uint32_t* fallback;         // best-only screen: positions handed to the per-thread kernel
+    uint32_t* fallback;         // best-only: positions k_score_fast handed to the per-thread kernel
     uint32_t* n_fallback;
-    uint32_t no_screen;         // 1: best-only mode on the per-thread kernel (A/B, MMGPU_NO_SCREEN)
-    uint32_t screen_variant;    // MMGPU_SCREEN: 1 plain, 2 overlapped round trips (default)
 };
 
 void launch_validate_ids(const uint32_t* v, uint64_t n, uint32_t bound, uint32_t* bad, cudaStream_t st);
@@ -137,9 +135,7 @@ size_t thresholds_scratch_bytes(uint32_t n);
 // allow_serial: small n may take the one-warp serial kernel (faster there)
 cudaError_t launch_thresholds(const double* lcom, const uint32_t* cbo, uint32_t n, DevThresholds* out,
                               void* scratch, size_t scratch_bytes, cudaStream_t st, bool allow_serial = true);
-void launch_score(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st);
-// best-only mode in one pass (screen + gates + offsets + records); thresholds must be ready
-void launch_sweep_best(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
+void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);
 uint32_t offsets_tiles(uint64_t npos);
 void launch_score_fast(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st);
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st);

@@ -694,3 +694,26 @@ def test_gpu_report_thresholds_random(gpu_engine):
         assert (a.similarity, a.lcom, a.cbo) == (b.similarity, b.lcom, b.cbo), n
     a = gpu_engine.report_thresholds(rng.random(10), rng.integers(0, 9, 7).astype(np.uint32), None)
     assert a.similarity == 0.0
+
+
+@pytest.mark.parametrize("env", [{}, {"MMGPU_GROUP": "0"}, {"MMGPU_LEAN": "0"}, {"MMGPU_SCORE_FAST": "0"}],
+                         ids=["default", "warp-per-class", "method+class-small", "general-scorer"])
+def test_gpu_metric_pass_and_scorer_variants(monkeypatch, env):
+    """Every route a small class can take through the metric pass — groups of
+    whole classes per warp (k_class_group), one warp per class (k_class_lean:
+    the solo list of members with degree 9..16, and everything under
+    MMGPU_GROUP=0), the round-1 k_method + k_class_small chain (MMGPU_LEAN=0)
+    — and both best-only scorers, against the oracle on systems whose member
+    degrees reach 16 (so solo classes, record overflow and listed warp-path
+    classes all occur)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    with Engine(0) as e:
+        for seed in range(10):
+            rng = np.random.default_rng(4100 + seed)
+            cfg = dict(seed=seed, n_classes=int(rng.integers(20, 300)), n_methods=int(rng.integers(200, 4000)),
+                       n_attributes=int(rng.integers(100, 6000)), k_max_calls=int(rng.integers(0, 9)),
+                       k_max_accesses=int(rng.integers(0, 9)), intra_class_bias=float(rng.random()))
+            s = System.generate(**cfg)
+            check_against_oracle(e, s, f"{env} seed {seed}",
+                                 modes=((COH | COUP, 0, False), (COH | COUP, 1, False), (COH | COUP, 0, True)))
