@@ -6,7 +6,7 @@
 // ownership (:109-122), per-method call/access counts uniform in [0, k]
 // (:131, :141), intra-class bias coin (:133, :143), pick rules
 // pick_excluding / pick_foreign (:57-84), skipped draws and sort+unique
-// (:155-160). tests/test_generate_oracle.py pins it against the reference
+// (:155-160). tests/test_abi_cpu.py:50-71 pins it against the reference
 // compiled in oracle/_ref and against committed golden hashes.
 //
 // zipf_s > 0 is the skewed variant used for config C3: class

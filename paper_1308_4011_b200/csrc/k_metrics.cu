@@ -206,8 +206,11 @@ __global__ void k_plan_classes(DevModel s, const uint32_t* __restrict__ cmaxdeg,
 // own class (classes with ≤ 64 attributes).
 constexpr int kChunkBuckets = 8;  // k_method regrouping: 0..6 chunks, 7 = more or past the end
 
+#ifndef MMGPU_METHOD_MINB
+#define MMGPU_METHOD_MINB 4
+#endif
 template <int K, bool REGROUP>
-__global__ void __launch_bounds__(256, 5)
+__global__ void __launch_bounds__(256, MMGPU_METHOD_MINB)
 k_method(DevModel s, MethRec* __restrict__ recs, uint64_t* __restrict__ own_mask,
          const uint32_t* __restrict__ pos_owner, const uint32_t* __restrict__ plist, uint32_t n_pos) {
     // Blocks holding methods of more than one chunk (dense shapes like C5)

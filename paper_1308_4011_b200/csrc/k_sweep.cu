@@ -28,10 +28,10 @@
 #include "mm_kernels.h"
 
 #ifndef MMGPU_SCORE_MINB
-#define MMGPU_SCORE_MINB 6
+#define MMGPU_SCORE_MINB 4
 #endif
 #ifndef MMGPU_FAST_MINB
-#define MMGPU_FAST_MINB 8
+#define MMGPU_FAST_MINB 6
 #endif
 namespace mmg {
 
@@ -647,6 +647,20 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_FAST_MINB) k_score_fast(Swee
             ++cands;
             if (!coh_ok && !can_coup) continue;
             const uint32_t h = E[k * kSweepTile] & 0xffu;
+            // the first other used class's two signature words requested with d's
+            // record (their addresses need only d and X): the common coupling
+            // rejection then costs one memory round trip, not two
+            uint32_t X0 = kNone, sw1 = 0, sw2 = 0, sb1 = 0, sb2 = 0;
+            if (can_coup) {
+                X0 = E[0] >> 8;
+                if (X0 == d) X0 = n > 1 ? E[kSweepTile] >> 8 : kNone;
+                if (X0 != kNone) {
+                    sb1 = bloom_h1(X0);
+                    sb2 = bloom_h2(X0);
+                    sw1 = __ldg(a.rec[d].sig + (sb1 >> 5));
+                    sw2 = __ldg(a.rec[d].sig + (sb2 >> 5));
+                }
+            }
             const ClassRec rd = load_rec(a.rec, d);
             if (coh_ok && rd.A != 0 && rd.M != 0) {  // coh_dest
                 const bool exact = (uint64_t)rd.A * ((uint64_t)rd.M + 1) < kExact53;
@@ -659,7 +673,8 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_FAST_MINB) k_score_fast(Swee
                 }
             }
             if (can_coup && (bd_coup == kNone || rd.cbo < bkp)) {  // cbo_dest_after == cbo_d when it passes
-                bool okc = true;
+                // a clear prefetched Bloom bit proves X0 ∉ U[d] (Bloom rows only)
+                bool okc = X0 == kNone || rd.dense != kNone || (((sw1 >> (sb1 & 31)) & (sw2 >> (sb2 & 31)) & 1u) != 0);
 #pragma unroll 1
                 for (uint32_t j = 0; j < n && okc; ++j) {
                     const uint32_t X = E[j * kSweepTile] >> 8;
