@@ -44,15 +44,26 @@ def build_lib(force: bool = False, verbose: bool = False) -> Path:
     deps = _sources() + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [ROOT / "include" / "mmgpu.h", ROOT / "include" / "mmfacts.h"]
     if not force and not _stale(LIB, deps):
         return LIB
-    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-o", str(LIB), *map(str, _sources())]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    # one nvcc per translation unit, in parallel (no device code crosses
+    # units), then one link
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    srcs = _sources()
+    objs = [objdir / (s.name + ".o") for s in srcs]
+    cmds = [[NVCC, *NVCC_FLAGS, "-c", "-o", str(o), str(s)] for s, o in zip(srcs, objs)]
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB), *map(str, objs)]
+    if all(r.returncode == 0 for r in results):
+        results.append(subprocess.run(link, capture_output=True, text=True))
     log = PKG / "build.log"
-    log.write_text(" ".join(cmd) + "\n\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+    log.write_text("\n\n".join(" ".join(c) + "\n" + r.stdout + r.stderr for c, r in zip(cmds + [link], results)))
+    if any(r.returncode != 0 for r in results):
+        sys.stderr.write("".join(r.stdout + r.stderr for r in results if r.returncode != 0))
         raise RuntimeError(f"nvcc failed building {LIB.name} (see {log})")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("".join(r.stderr for r in results))
     return LIB
 
 

@@ -47,38 +47,6 @@ __global__ void k_validate_offsets(const uint32_t* __restrict__ off, uint64_t n_
     }
 }
 
-// Per class: member/attribute counts, Σ degree, max degree, foreign-edge
-// count; classify into the warp path (small) or the CTA path (large).
-// Upload-time plan, method-parallel (a class-per-thread loop serialises on
-// Zipf giants): per member, its degree and foreign-edge count, folded into its
-// class with atomics. Every index is bounds-checked: this runs before the
-// validation result is known.
-__global__ void k_plan_methods(DevModel s, const uint32_t* __restrict__ pos_owner, uint32_t* __restrict__ foreign,
-                               uint32_t* __restrict__ cmaxdeg, uint32_t* __restrict__ n_hideg) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= s.M) return;
-    const uint32_t c = pos_owner[i];
-    const uint32_t p = s.cls_methods[i];
-    if (p >= s.M || c >= s.C) return;
-    const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
-    const uint32_t cb = min(s.call_off[p], Ec), ce = min(max(s.call_off[p + 1], cb), Ec);
-    const uint32_t ab = min(s.acc_off[p], Ea), ae = min(max(s.acc_off[p + 1], ab), Ea);
-    uint32_t fr = 0;
-    for (uint32_t e = cb; e < ce; ++e) {
-        const uint32_t t = s.call_tgt[e];
-        fr += t >= s.M || s.method_owner[t] != c;
-    }
-    for (uint32_t e = ab; e < ae; ++e) {
-        const uint32_t t = s.acc_tgt[e];
-        fr += t >= s.A || s.attribute_owner[t] != c;
-    }
-    if (fr) atomicAdd(foreign + c, fr);
-    atomicMax(cmaxdeg + c, (ce - cb) + (ae - ab));
-    // a used list longer than a method record holds needs more than kRecMaxEnt edges
-    const uint32_t hi = __ballot_sync(__activemask(), (ce - cb) + (ae - ab) > (uint32_t)kRecMaxEnt);
-    if (hi && (threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(n_hideg, __popc(hi));
-}
-
 // fan_out[p] = |calls(p)| (metrics.hpp:87-93); fan_in[t] += 1 per call-list
 // occurrence of t (metrics.hpp:79-85) — integer atomics, so the counts are
 // exact and order-free. Thread per method: its own row, then its targets.
@@ -104,8 +72,10 @@ __global__ void k_fan(DevModel s, uint32_t* __restrict__ fan_in, uint32_t* __res
     }
 }
 
-// Upload-time expansion of the membership lists, one warp per class (lanes
-// over the class's list positions, coalesced; no per-position searches):
+// Upload-time expansion of the membership lists, one thread per list
+// position (method positions, then attribute positions), its class found by a
+// binary search of the class offsets (warps hold consecutive positions, so
+// they walk the same search path; a warp per class serialised Zipf giants):
 //   pos_owner[k]  = class of method position k (the class-order owner table
 //                   every pass reads instead of gathering method_owner)
 //   attr_info[t]  = (owner(t), position of t in its owner's attribute list):
@@ -114,64 +84,198 @@ __global__ void k_fan(DevModel s, uint32_t* __restrict__ fan_in, uint32_t* __res
 //   method_owner / attribute_owner, when the caller omitted them
 // Every index is clamped or bounds-checked: this runs before validation's
 // verdict is known.
+__device__ __forceinline__ uint32_t class_of(const uint32_t* __restrict__ off, uint32_t C, uint32_t k) {
+    uint32_t lo = 0, hi = C - 1;  // the largest c with off[c] <= k
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(off + mid) <= k) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
 __global__ void k_expand(DevModel s, uint32_t* __restrict__ mo_out, uint32_t* __restrict__ ao_out,
                          uint32_t* __restrict__ pos_owner, uint2* __restrict__ info) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < s.C; c += nw) {
-        const uint32_t mb = min(s.cls_moff[c], s.M), me = min(max(s.cls_moff[c + 1], mb), s.M);
-        for (uint32_t k = mb + lane; k < me; k += 32) {
+    const uint64_t n = (uint64_t)s.M + s.A;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (i < s.M) {
+            const uint32_t k = (uint32_t)i;
+            const uint32_t c = class_of(s.cls_moff, s.C, k);
             pos_owner[k] = c;
             if (mo_out) {
                 const uint32_t p = s.cls_methods[k];
                 if (p < s.M) mo_out[p] = c;
             }
-        }
-        const uint32_t ab = min(s.cls_aoff[c], s.A), ae = min(max(s.cls_aoff[c + 1], ab), s.A);
-        for (uint32_t k = ab + lane; k < ae; k += 32) {
+        } else {
+            const uint32_t k = (uint32_t)(i - s.M);
+            const uint32_t c = class_of(s.cls_aoff, s.C, k);
             const uint32_t t = s.cls_attrs[k];
             if (t >= s.A) continue;
             if (ao_out) ao_out[t] = c;
-            info[t] = make_uint2(ao_out ? c : s.attribute_owner[t], k - ab);
+            info[t] = make_uint2(ao_out ? c : s.attribute_owner[t], k - min(__ldg(s.cls_aoff + c), k));
         }
     }
 }
 
-// Upload-time layout: the call / access rows in class order. Degrees by
-// position (then an exclusive scan gives the offsets), then one thread per
-// position copies its row. Indices are bounds-checked (runs before the
-// validation verdict is known).
-__global__ void k_pos_degrees(DevModel s, uint32_t* __restrict__ dc, uint32_t* __restrict__ da) {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k > s.M) return;
-    if (k == s.M) { dc[k] = 0; da[k] = 0; return; }
-    const uint32_t p = s.cls_methods[k];
-    const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
-    if (p >= s.M) { dc[k] = 0; da[k] = 0; return; }
-    const uint32_t cb = min(s.call_off[p], Ec), ce = min(max(s.call_off[p + 1], cb), Ec);
-    const uint32_t ab = min(s.acc_off[p], Ea), ae = min(max(s.acc_off[p + 1], ab), Ea);
-    dc[k] = ce - cb;
-    da[k] = ae - ab;
+// Upload-time layout: the call / access rows in class order, in three
+// kernels over 256-position tiles: per-tile degree sums, one block scanning
+// the tile sums, then the row pass below (its block scan + the tile base give
+// the class-order offsets, written beside the rows). Indices are
+// bounds-checked (this runs before the validation verdict is known).
+constexpr uint32_t kPosTile = 256;
+
+struct PosRow {
+    uint32_t p, cb, ce, ab, ae;
+};
+__device__ __forceinline__ PosRow pos_row(const DevModel& s, uint32_t k, uint32_t Ec, uint32_t Ea) {
+    PosRow r{s.M, 0, 0, 0, 0};
+    if (k >= s.M) return r;
+    r.p = s.cls_methods[k];
+    if (r.p >= s.M) return r;
+    r.cb = min(s.call_off[r.p], Ec); r.ce = min(max(s.call_off[r.p + 1], r.cb), Ec);
+    r.ab = min(s.acc_off[r.p], Ea); r.ae = min(max(s.acc_off[r.p + 1], r.ab), Ea);
+    return r;
 }
 
-// also the member index of every class-order edge (position − first position
-// of its class, 255 past that), which the lean class kernel reads beside the
-// targets instead of searching the members' row starts
-__global__ void k_pos_rows(DevModel s, const uint32_t* __restrict__ pos_owner, uint32_t* __restrict__ pc_tgt,
-                           uint32_t* __restrict__ pa_tgt, uint8_t* __restrict__ pc_mem, uint8_t* __restrict__ pa_mem) {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= s.M) return;
-    const uint32_t p = s.cls_methods[k];
-    if (p >= s.M) return;
-    const uint32_t oc = pos_owner[k];
-    const uint32_t mi = oc < s.C ? min(k - min(s.cls_moff[oc], k), 255u) : 255u;
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= (uint32_t)d) v += u;
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(kPosTile) k_pos_tile_sums(DevModel s, uint32_t* __restrict__ tsum) {
+    __shared__ uint32_t ws[2][kPosTile / 32];
     const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
-    const uint32_t cb = min(s.call_off[p], Ec), ce = min(max(s.call_off[p + 1], cb), Ec);
-    const uint32_t ab = min(s.acc_off[p], Ea), ae = min(max(s.acc_off[p + 1], ab), Ea);
-    uint32_t o = s.pc_off[k];
-    for (uint32_t e = cb; e < ce && o < Ec; ++e) { pc_mem[o] = (uint8_t)mi; pc_tgt[o++] = s.call_tgt[e]; }
-    o = s.pa_off[k];
-    for (uint32_t e = ab; e < ae && o < Ea; ++e) { pa_mem[o] = (uint8_t)mi; pa_tgt[o++] = s.acc_tgt[e]; }
+    const PosRow r = pos_row(s, blockIdx.x * kPosTile + threadIdx.x, Ec, Ea);
+    const uint32_t sc = __reduce_add_sync(0xffffffffu, r.ce - r.cb), sa = __reduce_add_sync(0xffffffffu, r.ae - r.ab);
+    if ((threadIdx.x & 31) == 0) { ws[0][threadIdx.x >> 5] = sc; ws[1][threadIdx.x >> 5] = sa; }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        uint32_t v = 0;
+        for (int w = 0; w < (int)(kPosTile / 32); ++w) v += ws[threadIdx.x][w];
+        tsum[threadIdx.x * gridDim.x + blockIdx.x] = v;
+    }
+}
+
+// one block: exclusive scans of both tile-sum arrays in place, and the totals
+// into pc_off[M] / pa_off[M]
+__global__ void __launch_bounds__(1024) k_pos_tile_scan(uint32_t* __restrict__ tsum, uint32_t ntiles,
+                                                        uint32_t* __restrict__ pc_off, uint32_t* __restrict__ pa_off,
+                                                        uint32_t M) {
+    __shared__ uint32_t ws[32];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int arr = 0; arr < 2; ++arr) {
+        uint32_t* a = tsum + arr * ntiles;
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < ntiles; base += 1024) {
+            const uint32_t i = base + threadIdx.x;
+            const uint32_t v = i < ntiles ? a[i] : 0u;
+            const uint32_t incl = warp_incl_scan(v, lane);
+            if (lane == 31) ws[w] = incl;
+            __syncthreads();
+            if (w == 0) ws[lane] = warp_incl_scan(ws[lane], lane);
+            __syncthreads();
+            const uint32_t x = carry + (w ? ws[w - 1] : 0u) + incl - v;
+            if (i < ntiles) a[i] = x;
+            carry += ws[31];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) (arr ? pa_off : pc_off)[M] = carry;
+    }
+}
+
+// The row pass: one warp per 32 consecutive class-order positions, whose rows
+// are flattened (warp scan of the degrees) and copied one element per lane
+// (two per iteration, loads issued before use), so the class-order writes are
+// fully coalesced and short rows do not idle lanes. Beside each target: the
+// member index of its position within the class (255 past that), which the
+// lean class kernel reads instead of searching the members' row starts. The
+// same pass folds the class plan's per-member inputs (formerly a separate
+// per-method pass): the foreign-edge count and the largest degree per class,
+// and the number of methods whose used list can outgrow a method record.
+__device__ __forceinline__ uint32_t flat_pos(uint32_t excl, uint32_t i) {
+    uint32_t j = 0;  // the position holding element i: the largest j with excl_j <= i
+#pragma unroll
+    for (int step = 16; step; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, excl, j + step);
+        if (v <= i) j += step;
+    }
+    return j;
+}
+__device__ __forceinline__ void flat_rows(uint32_t lane, uint32_t b, uint32_t excl, uint32_t total, uint32_t dst0,
+                                          uint32_t limit, const uint32_t* __restrict__ src,
+                                          const uint32_t* __restrict__ owner, uint32_t bound, uint32_t c,
+                                          uint32_t mi, uint32_t* __restrict__ tgt, uint8_t* __restrict__ mem,
+                                          uint32_t* __restrict__ fr) {
+    for (uint32_t base = 0; base < total; base += 64) {
+        const uint32_t i0 = base + lane, i1 = i0 + 32;
+        const uint32_t j0 = flat_pos(excl, i0), j1 = flat_pos(excl, i1);
+        const uint32_t e0 = __shfl_sync(0xffffffffu, excl, j0), e1 = __shfl_sync(0xffffffffu, excl, j1);
+        const uint32_t b0 = __shfl_sync(0xffffffffu, b, j0), b1 = __shfl_sync(0xffffffffu, b, j1);
+        const uint32_t c0 = __shfl_sync(0xffffffffu, c, j0), c1 = __shfl_sync(0xffffffffu, c, j1);
+        const uint32_t m0 = __shfl_sync(0xffffffffu, mi, j0), m1 = __shfl_sync(0xffffffffu, mi, j1);
+        const uint32_t o0 = dst0 + i0, o1 = dst0 + i1;
+        const bool v0 = i0 < total && o0 < limit, v1 = i1 < total && o1 < limit;
+        const uint32_t x0 = v0 ? __ldg(src + b0 + (i0 - e0)) : 0u;
+        const uint32_t x1 = v1 ? __ldg(src + b1 + (i1 - e1)) : 0u;
+        const uint32_t w0 = v0 && x0 < bound ? __ldg(owner + x0) : kNone;
+        const uint32_t w1 = v1 && x1 < bound ? __ldg(owner + x1) : kNone;
+        if (v0) {
+            tgt[o0] = x0;
+            mem[o0] = (uint8_t)m0;
+            if (w0 != c0) atomicAdd_block(fr + j0, 1u);
+        }
+        if (v1) {
+            tgt[o1] = x1;
+            mem[o1] = (uint8_t)m1;
+            if (w1 != c1) atomicAdd_block(fr + j1, 1u);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kPosTile) k_pos_rows(DevModel s, const uint32_t* __restrict__ pos_owner,
+                                                       const uint32_t* __restrict__ tsum, uint32_t* __restrict__ pc_off,
+                                                       uint32_t* __restrict__ pa_off, uint32_t* __restrict__ pc_tgt,
+                                                       uint32_t* __restrict__ pa_tgt, uint8_t* __restrict__ pc_mem,
+                                                       uint8_t* __restrict__ pa_mem, uint32_t* __restrict__ foreign,
+                                                       uint32_t* __restrict__ cmaxdeg, uint32_t* __restrict__ n_hideg) {
+    __shared__ uint32_t fr_s[kPosTile / 32][32];
+    __shared__ uint32_t ws[2][kPosTile / 32];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint32_t k = blockIdx.x * kPosTile + threadIdx.x;
+    uint32_t* fr = fr_s[wib];
+    fr[lane] = 0;
+    const uint32_t Ec = s.call_off[s.M], Ea = s.acc_off[s.M];
+    const PosRow r = pos_row(s, k, Ec, Ea);
+    uint32_t c = kNone, mi = 255u;
+    if (k < s.M) {
+        c = pos_owner[k];
+        mi = c < s.C ? min(k - min(s.cls_moff[c], k), 255u) : 255u;
+    }
+    const uint32_t nc = r.ce - r.cb, na = r.ae - r.ab;
+    const uint32_t ic = warp_incl_scan(nc, lane), ia = warp_incl_scan(na, lane);
+    if (lane == 31) { ws[0][wib] = ic; ws[1][wib] = ia; }
+    __syncthreads();
+    uint32_t wc = tsum[blockIdx.x], wa = tsum[gridDim.x + blockIdx.x];
+    for (uint32_t w = 0; w < wib; ++w) { wc += ws[0][w]; wa += ws[1][w]; }
+    if (k < s.M) { pc_off[k] = wc + ic - nc; pa_off[k] = wa + ia - na; }
+    const uint32_t tc = __shfl_sync(0xffffffffu, ic, 31), ta = __shfl_sync(0xffffffffu, ia, 31);
+    flat_rows(lane, r.cb, ic - nc, tc, wc, Ec, s.call_tgt, s.method_owner, s.M, c, mi, pc_tgt, pc_mem, fr);
+    flat_rows(lane, r.ab, ia - na, ta, wa, Ea, s.acc_tgt, s.attribute_owner, s.A, c, mi, pa_tgt, pa_mem, fr);
+    __syncwarp();
+    // plan inputs, one atomic per class present in the warp
+    const bool member = k < s.M && r.p < s.M && c < s.C;
+    const uint32_t deg = nc + na;
+    const uint32_t hi = __ballot_sync(0xffffffffu, member && deg > (uint32_t)kRecMaxEnt);
+    if (hi && lane == 0) atomicAdd(n_hideg, __popc(hi));
+    const uint32_t grp = __match_any_sync(0xffffffffu, member ? c : kNone);
+    const uint32_t fsum = __reduce_add_sync(grp, member ? fr[lane] : 0u);
+    const uint32_t dmax = __reduce_max_sync(grp, member ? deg : 0u);
+    if (member && lane == (uint32_t)(__ffs(grp) - 1)) {
+        if (fsum) atomicAdd(foreign + c, fsum);
+        atomicMax(cmaxdeg + c, dmax);
+    }
 }
 
 // classify into the warp path (small) or the CTA path (large)
@@ -1037,8 +1141,9 @@ void launch_expand(const DevModel& s, uint32_t* mo_out, uint32_t* ao_out, uint32
     if (!s.C) return;
     if (mo_out && s.M) cudaMemsetAsync(mo_out, 0xff, 4ull * s.M, st);  // unowned ids fail validation
     if (ao_out && s.A) cudaMemsetAsync(ao_out, 0xff, 4ull * s.A, st);
-    const uint32_t blocks = std::min<uint32_t>((s.C + 7) / 8, 148 * 8);
-    k_expand<<<blocks, 256, 0, st>>>(s, mo_out, ao_out, pos_owner, info);
+    const uint64_t n = (uint64_t)s.M + s.A;
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+    if (n) k_expand<<<blocks, 256, 0, st>>>(s, mo_out, ao_out, pos_owner, info);
 }
 void launch_fan(const DevModel& s, uint32_t* fan_in, uint32_t* fan_out, uint32_t* kmax, cudaStream_t st) {
     if (kmax) cudaMemsetAsync(kmax, 0, 8, st);
@@ -1050,26 +1155,30 @@ void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, u
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((n1 + 255) / 256, 148 * 16);
     k_validate_offsets<<<blocks, 256, 0, st>>>(off, n1, total, bad);
 }
-void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint4* cedge, uint32_t* large_list,
-                         uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,
-                         uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st) {
+void launch_plan_classes(const DevModel& s, uint4* cplan, uint4* cedge, uint32_t* large_list,
+                         uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg,
+                         const uint32_t* foreign, const uint32_t* cmaxdeg, cudaStream_t st) {
     if (!s.C) return;
-    cudaMemsetAsync(foreign, 0, 4ull * s.C, st);
-    cudaMemsetAsync(cmaxdeg, 0, 4ull * s.C, st);
-    if (s.M) k_plan_methods<<<(s.M + 255) / 256, 256, 0, st>>>(s, pos_owner, foreign, cmaxdeg, n_hideg);
     k_plan_classes<<<(s.C + 127) / 128, 128, 0, st>>>(s, cmaxdeg, foreign, cplan, cedge, large_list, n_large, big_list,
                                                        n_big, max_deg);
 }
 void launch_pos_rows(const DevModel& s, const uint32_t* pos_owner, uint32_t* pc_off, uint32_t* pc_tgt,
                      uint32_t* pa_off, uint32_t* pa_tgt, uint8_t* pc_mem, uint8_t* pa_mem, uint32_t* totals,
-                     uint32_t* grand, cudaStream_t st) {
-    k_pos_degrees<<<(s.M + 1 + 255) / 256, 256, 0, st>>>(s, pc_off, pa_off);
-    launch_scan(pc_off, pc_off, s.M + 1, totals, grand, st);
-    launch_scan(pa_off, pa_off, s.M + 1, totals, grand, st);
-    DevModel t = s;
-    t.pc_off = pc_off;
-    t.pa_off = pa_off;
-    if (s.M) k_pos_rows<<<(s.M + 255) / 256, 256, 0, st>>>(t, pos_owner, pc_tgt, pa_tgt, pc_mem, pa_mem);
+                     uint32_t* grand, uint32_t* foreign, uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st) {
+    if (s.C) {
+        cudaMemsetAsync(foreign, 0, 4ull * s.C, st);
+        cudaMemsetAsync(cmaxdeg, 0, 4ull * s.C, st);
+    }
+    const uint32_t ntiles = (s.M + kPosTile - 1) / kPosTile;
+    if (!ntiles) {  // no positions: empty rows
+        cudaMemsetAsync(pc_off, 0, 4, st);
+        cudaMemsetAsync(pa_off, 0, 4, st);
+        return;
+    }
+    k_pos_tile_sums<<<ntiles, kPosTile, 0, st>>>(s, totals);
+    k_pos_tile_scan<<<1, 1024, 0, st>>>(totals, ntiles, pc_off, pa_off, s.M);
+    k_pos_rows<<<ntiles, kPosTile, 0, st>>>(s, pos_owner, totals, pc_off, pa_off, pc_tgt, pa_tgt, pc_mem, pa_mem,
+                                            foreign, cmaxdeg, n_hideg);
 }
 
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,

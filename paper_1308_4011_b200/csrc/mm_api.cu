@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstddef>
 #include <cstdlib>
 #include <cstdio>
@@ -86,6 +87,27 @@ struct DBuf {  // owning device buffer (freed on release() or destruction)
     }
 };
 
+template <class T>
+struct HBuf {  // owning pinned host buffer, grown on demand (upload-time staging)
+    T* p = nullptr;
+    size_t n = 0;
+    HBuf() = default;
+    HBuf(const HBuf&) = delete;
+    HBuf& operator=(const HBuf&) = delete;
+    ~HBuf() { release(); }
+    cudaError_t ensure(size_t count) {
+        if (count <= n && p) return cudaSuccess;
+        release();
+        n = count ? count : 1;
+        return cudaMallocHost(reinterpret_cast<void**>(&p), n * sizeof(T));
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
 }  // namespace
 
 struct mm_ctx {
@@ -113,6 +135,11 @@ struct mm_ctx {
     uint32_t C = 0, M = 0, A = 0;
     uint64_t Ec = 0, Ea = 0;
     std::vector<uint32_t> h_cls_moff;
+    // upload-time pinned staging: the CTA-path list and foreign counts (D2H),
+    // the host-built plan tables (H2D, asynchronous: the next upload syncs
+    // the stream before reusing it)
+    HBuf<uint32_t> hs_list, hs_fr;
+    HBuf<unsigned char> hs_up;
     DBuf<uint32_t> method_owner, attribute_owner, cls_moff, cls_methods, cls_aoff, cls_attrs, call_off, call_tgt,
         acc_off, acc_tgt;
     // plan
@@ -522,9 +549,53 @@ uint64_t mm_system_bytes(const mm_system* s) {
                    2ull * (s->n_classes + 1) + 2ull * (s->n_methods + 1) + Ec + Ea);
 }
 
+// MMGPU_UPLOAD_TRACE=1: per-phase times of mm_upload on stderr (events on the
+// main stream + host clock); a diagnostic, off by default
+struct UploadTrace {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    std::vector<cudaEvent_t> ev;
+    std::vector<const char*> name;
+    std::vector<std::pair<const char*, double>> host;
+    std::chrono::steady_clock::time_point h0;
+    void init(cudaStream_t s) {
+        static const bool env = std::getenv("MMGPU_UPLOAD_TRACE") != nullptr;
+        on = env;
+        st = s;
+        if (on) h0 = std::chrono::steady_clock::now();
+    }
+    void mark(const char* n) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        ev.push_back(e);
+        name.push_back(n);
+    }
+    void hmark(const char* n) {
+        if (on) host.push_back({n, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count()});
+    }
+    ~UploadTrace() {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        std::fprintf(stderr, "[mm_upload trace] device (us since %s):", ev.empty() ? "-" : name[0]);
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[0], ev[i]);
+            std::fprintf(stderr, " %s=%.1f", name[i], ms * 1e3);
+        }
+        std::fprintf(stderr, " | host (us since entry):");
+        for (auto& h : host) std::fprintf(stderr, " %s=%.1f", h.first, h.second);
+        std::fprintf(stderr, "\n");
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
 mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     if (!ctx || !s) return MM_E_ARG;
     if (mm_status st = set_device(ctx)) return st;
+    UploadTrace tr;
+    tr.init(ctx->stream);
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->side));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     // device buffers are reused across uploads (grown on demand, never shrunk)
@@ -545,6 +616,8 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     Ctl* ctl = ctx->ctl.p;
     uint32_t* bad = &ctl->bad;
     MM_CUDA(ctx, cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx->stream));
+    tr.hmark("synced");
+    tr.mark("start");
     cudaStream_t vs = ctx->aux[0];
     int n_up = 0;
     auto up = [&](DBuf<uint32_t>& d, const uint32_t* h, size_t n, const char* what, auto&& validate) -> mm_status {
@@ -598,22 +671,28 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         (st = up(ctx->acc_off, s->acc_off, M + 1ull, "acc_off", offs(M + 1ull, (uint32_t)Ea))) ||
         (st = up(ctx->acc_tgt, s->acc_tgt, Ea, "acc_tgt", ids(Ea, A))))
         return st;
+    tr.mark("copies");
+    tr.hmark("copies_issued");
     MM_CUDA(ctx, cudaEventRecord(ctx->ev_join[0], vs));
     MM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join[0], 0));
+    tr.mark("validated");
     // the dependency rows in class order (the method pass streams them)
     MM_CUDA(ctx, ctx->pc_off.ensure(M + 1ull));
     MM_CUDA(ctx, ctx->pa_off.ensure(M + 1ull));
     MM_CUDA(ctx, ctx->pc_tgt.ensure(Ec ? Ec : 1));
     MM_CUDA(ctx, ctx->pa_tgt.ensure(Ea ? Ea : 1));
-    MM_CUDA(ctx, ctx->pos_scan.ensure((M + 1ull + 1023) / 1024 + 2));
+    MM_CUDA(ctx, ctx->pos_scan.ensure(2ull * ((M + 255ull) / 256) + 2));  // per-tile degree sums (pc, pa)
     MM_CUDA(ctx, ctx->pc_mem.ensure(Ec ? Ec : 1));
     MM_CUDA(ctx, ctx->pa_mem.ensure(Ea ? Ea : 1));
+    MM_CUDA(ctx, ctx->foreign.ensure(C ? C : 1));
+    MM_CUDA(ctx, ctx->cmaxdeg.ensure(C ? C : 1));
     st = run(ctx, "upload_rows", [&] {
         launch_pos_rows(ctx->dev(), ctx->pos_owner.p, ctx->pc_off.p, ctx->pc_tgt.p, ctx->pa_off.p, ctx->pa_tgt.p,
                         ctx->pc_mem.p, ctx->pa_mem.p, ctx->pos_scan.p, ctx->pos_scan.p + (M + 1ull + 1023) / 1024 + 1,
-                        ctx->stream);
+                        ctx->foreign.p, ctx->cmaxdeg.p, &ctl->n_hideg, ctx->stream);
     });
     if (st) return st;
+    tr.mark("pos_rows");
 
     // class plan (bounds-checked, so it is safe on a model validation rejects):
     // warp path vs CTA path, scratch for the CTA path. One sync for both.
@@ -621,12 +700,10 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, ctx->cedge.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->big_list.ensure(C ? C : 1));
     MM_CUDA(ctx, ctx->large_list.ensure(C ? C : 1));
-    MM_CUDA(ctx, ctx->foreign.ensure(C ? C : 1));
-    MM_CUDA(ctx, ctx->cmaxdeg.ensure(C ? C : 1));
     const DevModel dm = ctx->dev();
     st = run(ctx, "plan", [&] {
-        launch_plan_classes(dm, ctx->pos_owner.p, ctx->cplan.p, ctx->cedge.p, ctx->large_list.p, &ctl->n_large, ctx->big_list.p,
-                            &ctl->n_big, &ctl->max_deg, ctx->foreign.p, ctx->cmaxdeg.p, &ctl->n_hideg, ctx->stream);
+        launch_plan_classes(dm, ctx->cplan.p, ctx->cedge.p, ctx->large_list.p, &ctl->n_large, ctx->big_list.p,
+                            &ctl->n_big, &ctl->max_deg, ctx->foreign.p, ctx->cmaxdeg.p, ctx->stream);
     });
     if (st) return st;
     const bool grouping = ctx->lean_fused && ctx->group_on;
@@ -646,9 +723,11 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         });
         if (st) return st;
     }
+    tr.mark("plans");
     Ctl h{};
     MM_CUDA(ctx, cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
     MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    tr.hmark("ctl_synced");
     if (h.bad) return fail(ctx, MM_E_ARG, (h.bad & 2u) ? "mm_upload: malformed offsets" : "mm_upload: id out of range");
     ctx->n_large = h.n_large;
     ctx->n_big = h.n_big;
@@ -663,10 +742,26 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     // than a record's entries, or (class ids ≥ 2^24) any
     ctx->n_maybe_ovf = C >= (1u << 24) ? M : h.n_hideg;
     if (ctx->n_large) {
-        std::vector<uint32_t> list(ctx->n_large), fr(C);
-        MM_CUDA(ctx, cudaMemcpy(list.data(), ctx->large_list.p, 4ull * ctx->n_large, cudaMemcpyDeviceToHost));
-        MM_CUDA(ctx, cudaMemcpy(fr.data(), ctx->foreign.p, 4ull * C, cudaMemcpyDeviceToHost));
-        std::sort(list.begin(), list.end());
+        MM_CUDA(ctx, ctx->hs_list.ensure(ctx->n_large));
+        MM_CUDA(ctx, ctx->hs_fr.ensure(C));
+        MM_CUDA(ctx, cudaMemcpyAsync(ctx->hs_list.p, ctx->large_list.p, 4ull * ctx->n_large, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+        MM_CUDA(ctx, cudaMemcpyAsync(ctx->hs_fr.p, ctx->foreign.p, 4ull * C, cudaMemcpyDeviceToHost, ctx->stream));
+        MM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        tr.hmark("lists_d2h");
+        // the list in class order (the device appends it in atomic order): a
+        // pass over a class bitmap, O(C), instead of a comparison sort
+        std::vector<uint32_t> list(ctx->n_large);
+        {
+            std::vector<uint8_t> mark(C, 0);
+            for (uint32_t i = 0; i < ctx->n_large; ++i)
+                if (ctx->hs_list.p[i] < C) mark[ctx->hs_list.p[i]] = 1;
+            uint32_t k = 0;
+            for (uint32_t c = 0; c < C && k < ctx->n_large; ++c)
+                if (mark[c]) list[k++] = c;
+            if (k != ctx->n_large) return fail(ctx, MM_E_ARG, "mm_upload: malformed class plan");
+        }
+        const uint32_t* fr = ctx->hs_fr.p;
         int dev_smem = 0;
         cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
         const uint64_t budget = dev_smem > 8192 ? (uint64_t)dev_smem - 8192 : 40 * 1024;
@@ -725,11 +820,14 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
             while (need[i] > tiers[tier]) ++tier;
             gkey[i] = 2 * tier + ((tier >= 3 || Mc >= kBigCtaMembers) ? 1 : 0);
         }
+        // stable counting sort by group key (class order within a group)
         std::vector<uint32_t> order(ctx->n_large);
-        for (uint32_t i = 0; i < ctx->n_large; ++i) order[i] = i;
-        std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
-            return gkey[x] != gkey[y] ? gkey[x] < gkey[y] : need[x] < need[y];
-        });
+        {
+            uint32_t start[2 * 4 + 1] = {};
+            for (uint32_t i = 0; i < ctx->n_large; ++i) ++start[gkey[i] + 1];
+            for (int g = 0; g < 2 * 4; ++g) start[g + 1] += start[g];
+            for (uint32_t i = 0; i < ctx->n_large; ++i) order[start[gkey[i]]++] = i;
+        }
         std::vector<uint32_t> list2(ctx->n_large);
         std::vector<LargePlan> plans2(ctx->n_large);
         uint64_t koff = 0, roff = 0;
@@ -786,16 +884,17 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         MM_CUDA(ctx, ctx->giant_items.ensure(gitems.size() ? gitems.size() : 1));
         MM_CUDA(ctx, ctx->gcnt.ensure(n_giant ? (size_t)n_giant * C : 1));
         MM_CUDA(ctx, ctx->gH.ensure(n_giant ? n_giant : 1));
-        if (!gitems.empty())
-            MM_CUDA(ctx, cudaMemcpy(ctx->giant_items.p, gitems.data(), sizeof(uint2) * gitems.size(),
-                                    cudaMemcpyHostToDevice));
+        tr.hmark("host_plan");
+        // every host-built table travels in one pinned staging block, asynchronously
+        struct Part { void* dst; const void* src; size_t bytes; };
+        std::vector<Part> parts;
+        auto stage = [&](void* dst, const void* src, size_t bytes) { if (bytes) parts.push_back({dst, src, bytes}); };
+        stage(ctx->giant_items.p, gitems.data(), sizeof(uint2) * gitems.size());
         MM_CUDA(ctx, ctx->ck_items.ensure(items.size() ? items.size() : 1));
         MM_CUDA(ctx, ctx->split_list.ensure(split.size() ? split.size() : 1));
-        if (!items.empty()) {
-            MM_CUDA(ctx, cudaMemcpy(ctx->ck_items.p, items.data(), sizeof(uint2) * items.size(), cudaMemcpyHostToDevice));
-            MM_CUDA(ctx, cudaMemcpy(ctx->split_list.p, split.data(), 4 * split.size(), cudaMemcpyHostToDevice));
-        }
-        MM_CUDA(ctx, cudaMemcpy(ctx->large_list.p, list2.data(), 4ull * ctx->n_large, cudaMemcpyHostToDevice));
+        stage(ctx->ck_items.p, items.data(), sizeof(uint2) * items.size());
+        stage(ctx->split_list.p, split.data(), 4 * split.size());
+        stage(ctx->large_list.p, list2.data(), 4ull * ctx->n_large);
         std::vector<uint32_t> mma;
         uint32_t mma_max = 0;
         for (uint32_t j = 0; j < ctx->n_large; ++j)
@@ -806,13 +905,22 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         ctx->n_mma = (uint32_t)mma.size();
         MM_CUDA(ctx, ctx->mma_list.ensure(mma.size() ? mma.size() : 1));
         if (!mma.empty()) {
-            MM_CUDA(ctx, cudaMemcpy(ctx->mma_list.p, mma.data(), 4 * mma.size(), cudaMemcpyHostToDevice));
+            stage(ctx->mma_list.p, mma.data(), 4 * mma.size());
             ctx->mma_smem = ck_mma_smem_bytes(mma_max);
             MM_CUDA(ctx, set_ck_mma_smem(ctx->mma_smem));
         }
         MM_CUDA(ctx, ctx->plans.ensure(ctx->n_large));
-        MM_CUDA(ctx, cudaMemcpy(ctx->plans.p, plans2.data(), sizeof(LargePlan) * ctx->n_large,
-                                cudaMemcpyHostToDevice));
+        stage(ctx->plans.p, plans2.data(), sizeof(LargePlan) * ctx->n_large);
+        size_t total = 0;
+        for (const Part& q : parts) total += (q.bytes + 15) & ~size_t(15);
+        MM_CUDA(ctx, ctx->hs_up.ensure(total));
+        size_t at = 0;
+        for (const Part& q : parts) {
+            std::memcpy(ctx->hs_up.p + at, q.src, q.bytes);
+            MM_CUDA(ctx, cudaMemcpyAsync(q.dst, ctx->hs_up.p + at, q.bytes, cudaMemcpyHostToDevice, ctx->stream));
+            at += (q.bytes + 15) & ~size_t(15);
+        }
+        tr.hmark("plans_h2d");
         MM_CUDA(ctx, ctx->gkeys.ensure(koff ? koff : 1));
         MM_CUDA(ctx, ctx->grows.ensure(roff ? roff : 1));
         ctx->grows_words = roff;
@@ -847,6 +955,8 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
         return fail(ctx, MM_E_RANGE, "mm_upload: system too large for 32-bit U-row offsets");
     MM_CUDA(ctx, ctx->ux.ensure((size_t)kSmallRowCap * M + Ec + Ea + 1));
     MM_CUDA(ctx, ctx->un.ensure((size_t)kSmallRowCap * M + Ec + Ea + 1));
+    tr.hmark("done");
+    tr.mark("end");
     ctx->have_model = true;
     ctx->metrics_valid = false;
     ctx->sweep_valid = false;

@@ -64,13 +64,14 @@ void launch_expand(const DevModel& s, uint32_t* mo_out, uint32_t* ao_out, uint32
                    cudaStream_t st);
 void launch_fan(const DevModel& s, uint32_t* fan_in, uint32_t* fan_out, uint32_t* kmax, cudaStream_t st);
 void launch_validate_offsets(const uint32_t* off, uint64_t n1, uint32_t total, uint32_t* bad, cudaStream_t st);
-void launch_plan_classes(const DevModel& s, const uint32_t* pos_owner, uint4* cplan, uint4* cedge, uint32_t* large_list,
-                         uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg, uint32_t* foreign,
-                         uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st);
-// upload: the dependency rows in class order (DevModel::pc_* / pa_*)
+void launch_plan_classes(const DevModel& s, uint4* cplan, uint4* cedge, uint32_t* large_list,
+                         uint32_t* n_large, uint32_t* big_list, uint32_t* n_big, uint32_t* max_deg,
+                         const uint32_t* foreign, const uint32_t* cmaxdeg, cudaStream_t st);
+// upload: the dependency rows in class order (DevModel::pc_* / pa_*), and the
+// class plan's per-class foreign-edge counts / largest degree / n_hideg
 void launch_pos_rows(const DevModel& s, const uint32_t* pos_owner, uint32_t* pc_off, uint32_t* pc_tgt,
                      uint32_t* pa_off, uint32_t* pa_tgt, uint8_t* pc_mem, uint8_t* pa_mem, uint32_t* totals,
-                     uint32_t* grand, cudaStream_t st);
+                     uint32_t* grand, uint32_t* foreign, uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st);
 void launch_class_lean(const DevModel& s, const uint4* cplan, const uint4* cedge, const uint8_t* pc_mem,
                        const uint8_t* pa_mem, MethRec* recs, ClassRec* rec, double* lcom,
                        uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, const uint32_t* list,
