@@ -44,35 +44,37 @@ constexpr unsigned long long kValMask = (1ull << 62) - 1;
 // Per-thread used list staged in shared memory (column-major over the tile
 // so thread t's k-th entry sits at [k * kSweepTile + t]: conflict-free).
 // Dynamic loops keep the kernel small and its register count low.
-struct SmemEnum {
+template <int S>
+struct SmemEnumT {  // a method's used list in shared memory, stride S (the block size)
+    static constexpr int kStride = S;
     uint32_t* X;
     uint32_t* H;
     int n;
     template <class F>
     __device__ __forceinline__ void each(F f) const {
 #pragma unroll 1
-        for (int k = 0; k < n; ++k) f(k, X[k * kSweepTile], H[k * kSweepTile]);
+        for (int k = 0; k < n; ++k) f(k, X[k * S], H[k * S]);
     }
     __device__ __forceinline__ uint32_t hits(uint32_t v) const {
         for (int k = 0; k < n; ++k)
-            if (X[k * kSweepTile] == v) return H[k * kSweepTile];
+            if (X[k * S] == v) return H[k * S];
         return 0;
     }
     // returns false when a new class would exceed `cap` distinct entries
     __device__ __forceinline__ bool insert(uint32_t v, uint32_t acc, int cap) {
         int k = 0;
-        while (k < n && X[k * kSweepTile] < v) ++k;
-        if (k < n && X[k * kSweepTile] == v) {
-            H[k * kSweepTile] += acc;
+        while (k < n && X[k * S] < v) ++k;
+        if (k < n && X[k * S] == v) {
+            H[k * S] += acc;
             return true;
         }
         if (n >= cap) return false;
         for (int j = n; j > k; --j) {
-            X[j * kSweepTile] = X[(j - 1) * kSweepTile];
-            H[j * kSweepTile] = H[(j - 1) * kSweepTile];
+            X[j * S] = X[(j - 1) * S];
+            H[j * S] = H[(j - 1) * S];
         }
-        X[k * kSweepTile] = v;
-        H[k * kSweepTile] = acc;
+        X[k * S] = v;
+        H[k * S] = acc;
         ++n;
         return true;
     }
@@ -88,6 +90,7 @@ struct SmemEnum {
         return true;
     }
 };
+using SmemEnum = SmemEnumT<kSweepTile>;
 
 struct StreamEnum {
     StreamUsed S;
@@ -506,9 +509,9 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 // Fills `ren` (shared-memory list) or `sen` (streaming) with method p's used
 // list and returns the origin-side values. Record path when the method pass
 // could pack the list; CSR otherwise.
-template <int K, bool SCORE = false>
+template <int K, bool SCORE = false, class REN>
 __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, uint32_t p, uint32_t o,
-                                            SmemEnum& ren, StreamEnum& sen, Origin& org) {
+                                            REN& ren, StreamEnum& sen, Origin& org) {
     const uint4* rp = reinterpret_cast<const uint4*>(a.recs + pos);
     const uint4 r0 = rp[0], r1 = rp[1];
     const uint32_t hdr = rec_hdrs(a.recs, a.s.M)[pos];
@@ -518,7 +521,7 @@ __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, ui
         const uint32_t n = rec_n(hdr);
 #pragma unroll
         for (int k = 0; k < kRecMaxEnt; ++k)
-            if (k < (int)n) { ren.X[k * kSweepTile] = ent[k] >> 8; ren.H[k * kSweepTile] = ent[k] & 0xffu; }
+            if (k < (int)n) { ren.X[k * REN::kStride] = ent[k] >> 8; ren.H[k * REN::kStride] = ent[k] & 0xffu; }
         ren.n = (int)n;
         const uint32_t removed = (hdr & kRecRemovedValid) ? rec_removed(hdr)
                                                            : removed_count(ro, a.ux, a.un, a.dense, a.s.C, ren, o);
@@ -540,25 +543,34 @@ __device__ __forceinline__ bool load_method(const SweepArgs& a, uint32_t pos, ui
 // One method per thread, its used list in shared memory: small per-thread
 // state and high occupancy measured faster on C4 than a warp-flattened
 // variant (one candidate per lane), the round-1 profiles show why — every
-// kernel here is latency-bound, so resident warps matter most.
+// kernel here is latency-bound, so resident warps matter most. Blocks of
+// kScoreTile threads: per-method work is uneven (C5: up to 16 used classes,
+// each destination checked against the others), and a block keeps its shared
+// memory and registers until its slowest warp ends, so small blocks keep more
+// warps resident (C5 at 256 threads: 14.8 of 32 possible warps per SM).
+#ifndef MMGPU_SCORE_TILE
+#define MMGPU_SCORE_TILE 64
+#endif
+constexpr int kScoreTile = MMGPU_SCORE_TILE;
+static_assert(kSweepTile % kScoreTile == 0, "score tile divides the sweep tile");
 template <int K, bool LIST = false>
-__global__ void __launch_bounds__(kSweepTile, MMGPU_SCORE_MINB) k_score_thread(SweepArgs a) {
-    __shared__ uint32_t s_X[K * kSweepTile], s_H[K * kSweepTile];
+__global__ void __launch_bounds__(kScoreTile, MMGPU_SCORE_MINB * (kSweepTile / kScoreTile)) k_score_thread(SweepArgs a) {
+    __shared__ uint32_t s_X[K * kScoreTile], s_H[K * kScoreTile];
     uint64_t pos;
     bool live;
     if (LIST) {  // the methods k_score_fast handed over (record overflow)
-        const uint32_t i = blockIdx.x * kSweepTile + threadIdx.x;
+        const uint32_t i = blockIdx.x * kScoreTile + threadIdx.x;
         live = i < *a.n_fallback;
         pos = live ? a.fallback[i] : 0;
     } else {
-        pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kSweepTile + threadIdx.x;
+        pos = (uint64_t)a.pos_begin + (uint64_t)blockIdx.x * kScoreTile + threadIdx.x;
         live = pos < a.pos_end;
     }
     uint32_t cands = 0;
     if (live) {
         const uint32_t p = __ldg(a.s.cls_methods + pos);
         const uint32_t o = __ldg(a.pos_owner + pos);
-        SmemEnum ren{s_X + threadIdx.x, s_H + threadIdx.x, 0};
+        SmemEnumT<kScoreTile> ren{s_X + threadIdx.x, s_H + threadIdx.x, 0};
         StreamEnum sen;
         Origin org;
         MethodResult r;
@@ -1079,8 +1091,9 @@ __global__ void __launch_bounds__(kSweepTile) k_sim_emit(SweepArgs a, SimCrit sc
 
 void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
     if (!n_tiles) return;
-    if (a.maxdeg_fast <= 8) k_score_thread<8><<<n_tiles, kSweepTile, 0, st>>>(a);
-    else k_score_thread<16><<<n_tiles, kSweepTile, 0, st>>>(a);
+    const uint32_t blocks = n_tiles * (kSweepTile / kScoreTile);
+    if (a.maxdeg_fast <= 8) k_score_thread<8><<<blocks, kScoreTile, 0, st>>>(a);
+    else k_score_thread<16><<<blocks, kScoreTile, 0, st>>>(a);
 }
 
 uint32_t offsets_tiles(uint64_t npos) { return (uint32_t)((npos + kOffTile - 1) / kOffTile); }
@@ -1088,8 +1101,9 @@ uint32_t offsets_tiles(uint64_t npos) { return (uint32_t)((npos + kOffTile - 1) 
 void launch_score_fast(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st) {
     if (n_tiles) k_score_fast<<<n_tiles, kSweepTile, 0, st>>>(a);
     if (!fallback_tiles) return;  // incomplete records (their list is built above)
-    if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
-    else k_score_thread<16, true><<<fallback_tiles, kSweepTile, 0, st>>>(a);
+    const uint32_t blocks = fallback_tiles * (kSweepTile / kScoreTile);
+    if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<blocks, kScoreTile, 0, st>>>(a);
+    else k_score_thread<16, true><<<blocks, kScoreTile, 0, st>>>(a);
 }
 
 void launch_offsets(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
