@@ -697,7 +697,7 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
     out = {"value": n_cand / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h[0]),
            "ms_per_step": dt * 1e3, "steps": n, "latency_ms": dt * 1e3, "path": path}
     if world == 1 and not args.e2e_serial:
-        # request pipelining, as a serving host runs it: two engines (two
+        # request pipelining, as a serving host runs it: several engines (
         # contexts with their own streams and device copies of the model),
         # each driven by its own host thread through the same public calls, so
         # one request's H2D overlaps the other's kernels and D2H (PCIe is full
@@ -705,7 +705,8 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
         # its whole input from pinned host memory and reads its results back.
         import threading
         from paper_1308_4011_b200 import Engine
-        eng2 = Engine(dev.index if dev.index is not None else 0)
+        extra = [Engine(dev.index if dev.index is not None else 0) for _ in range(max(1, args.e2e_engines) - 1)]
+        engines = [eng] + extra
         counts = {}
 
         def request(e):
@@ -717,31 +718,32 @@ def run_e2e(args, s, eng, dev, stream, n_cand, world, shard, gather):
             e.synchronize()
             counts[id(e)] = len(recs)
 
-        for e in (eng, eng2):
+        for e in engines:
             request(e)
         n_each = max(2, min(args.steps, 10))
-        gate = threading.Barrier(3)
+        gate = threading.Barrier(len(engines) + 1)
 
         def worker(e):
             gate.wait()
             for _ in range(n_each):
                 request(e)
 
-        ths = [threading.Thread(target=worker, args=(e,)) for e in (eng, eng2)]
+        ths = [threading.Thread(target=worker, args=(e,)) for e in engines]
         for th in ths:
             th.start()
         gate.wait()
         t0 = time.perf_counter()
         for th in ths:
             th.join()
-        dtp = (time.perf_counter() - t0) / (2 * n_each)
-        eng2.close()
+        dtp = (time.perf_counter() - t0) / (len(engines) * n_each)
+        for e in extra:
+            e.close()
         if len(set(counts.values())) != 1:
             raise RuntimeError(f"pipelined e2e: engines disagree on the suggestion count {counts}")
-        out.update({"value": n_cand / dtp, "ms_per_step": dtp * 1e3, "steps": 2 * n_each,
-                    "serial_value": n_cand / dt,
-                    "path": path + "; two engines on two host threads, requests pipelined (one request's H2D "
-                                   "under the other's kernels and D2H); latency_ms = one request alone"})
+        out.update({"value": n_cand / dtp, "ms_per_step": dtp * 1e3, "steps": len(engines) * n_each,
+                    "serial_value": n_cand / dt, "engines": len(engines),
+                    "path": path + f"; {len(engines)} engines on {len(engines)} host threads, requests pipelined "
+                                   "(one request's H2D under another's kernels and D2H); latency_ms = one request alone"})
     return out
 
 
@@ -781,6 +783,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-serial", action="store_true", help="e2e without request pipelining (one engine)")
+    ap.add_argument("--e2e-engines", type=int, default=3, help="engines (host threads) pipelining e2e requests")
     ap.add_argument("--traffic-bytes", type=float, default=None,
                     help="dram bytes per launch of the dominant kernel from an ncu --set full capture")
     args = ap.parse_args()

@@ -158,30 +158,49 @@ __global__ void __launch_bounds__(kPosTile) k_pos_tile_sums(DevModel s, uint32_t
     }
 }
 
-// one block: exclusive scans of both tile-sum arrays in place, and the totals
-// into pc_off[M] / pa_off[M]
+// one block: exclusive scans of both tile-sum arrays in place (4 consecutive
+// tiles per thread, both arrays in the same pass), and the totals into
+// pc_off[M] / pa_off[M]
 __global__ void __launch_bounds__(1024) k_pos_tile_scan(uint32_t* __restrict__ tsum, uint32_t ntiles,
                                                         uint32_t* __restrict__ pc_off, uint32_t* __restrict__ pa_off,
                                                         uint32_t M) {
-    __shared__ uint32_t ws[32];
+    __shared__ uint32_t ws[2][32];
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int arr = 0; arr < 2; ++arr) {
-        uint32_t* a = tsum + arr * ntiles;
-        uint32_t carry = 0;
-        for (uint32_t base = 0; base < ntiles; base += 1024) {
-            const uint32_t i = base + threadIdx.x;
-            const uint32_t v = i < ntiles ? a[i] : 0u;
-            const uint32_t incl = warp_incl_scan(v, lane);
-            if (lane == 31) ws[w] = incl;
-            __syncthreads();
-            if (w == 0) ws[lane] = warp_incl_scan(ws[lane], lane);
-            __syncthreads();
-            const uint32_t x = carry + (w ? ws[w - 1] : 0u) + incl - v;
-            if (i < ntiles) a[i] = x;
-            carry += ws[31];
-            __syncthreads();
+    uint32_t carry[2] = {0u, 0u};
+    for (uint32_t base = 0; base < ntiles; base += 4096) {
+        const uint32_t i0 = base + 4 * threadIdx.x;
+        uint32_t v[2][4], s[2] = {0u, 0u};
+#pragma unroll
+        for (int arr = 0; arr < 2; ++arr)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                v[arr][j] = i0 + j < ntiles ? tsum[arr * ntiles + i0 + j] : 0u;
+                s[arr] += v[arr][j];
+            }
+        uint32_t incl[2];
+#pragma unroll
+        for (int arr = 0; arr < 2; ++arr) {
+            incl[arr] = warp_incl_scan(s[arr], lane);
+            if (lane == 31) ws[arr][w] = incl[arr];
         }
-        if (threadIdx.x == 0) (arr ? pa_off : pc_off)[M] = carry;
+        __syncthreads();
+        if (w < 2) ws[w][lane] = warp_incl_scan(ws[w][lane], lane);
+        __syncthreads();
+#pragma unroll
+        for (int arr = 0; arr < 2; ++arr) {
+            uint32_t x = carry[arr] + (w ? ws[arr][w - 1] : 0u) + incl[arr] - s[arr];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (i0 + j < ntiles) tsum[arr * ntiles + i0 + j] = x;
+                x += v[arr][j];
+            }
+            carry[arr] += ws[arr][31];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        pc_off[M] = carry[0];
+        pa_off[M] = carry[1];
     }
 }
 
