@@ -1200,12 +1200,153 @@ void launch_pos_rows(const DevModel& s, const uint32_t* pos_owner, uint32_t* pc_
                                             foreign, cmaxdeg, n_hideg);
 }
 
+// The method pass for rows longer than one chunk (dense shapes like C5:
+// up to 36 edges per method), flattened: one warp per 32 listed positions,
+// their edges spread over the lanes (warp scan of the degrees, two edges per
+// lane per round, loads issued before use), so every round reads 32
+// consecutive class-order targets and no lane idles behind the warp's
+// longest row. Per position, in shared memory: the distinct foreign classes
+// (first-fit atomicCAS slots, an access adds 1 to its class's count), the
+// own-attribute mask, the own-access count. Each lane then sorts its
+// position's list (own class included) and writes the same MethRec, header
+// and mask as k_method (a list longer than a record holds is flagged
+// overflow; consumers then read the CSR and ignore the entries).
+#ifndef MMGPU_METHOD_FLAT
+#define MMGPU_METHOD_FLAT 1
+#endif
+constexpr int kFlatSlots = kRecMaxEnt + 1;  // a 9th distinct class proves overflow
+
+__global__ void __launch_bounds__(256) k_method_flat(DevModel s, MethRec* __restrict__ recs,
+                                                     uint64_t* __restrict__ own_mask,
+                                                     const uint32_t* __restrict__ pos_owner,
+                                                     const uint32_t* __restrict__ plist, uint32_t n_pos) {
+    __shared__ uint32_t sX[8][kFlatSlots][32], sH[8][kFlatSlots][32];
+    __shared__ unsigned long long sMask[8][32];
+    __shared__ uint32_t sHown[8][32], sFlag[8][32];  // flag: 1 own class used, 2 more classes than slots
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t n = plist ? n_pos : s.M;
+    uint32_t pos = kNone;
+    if (idx < n) pos = plist ? __ldg(plist + idx) : idx;
+    if (pos >= s.M) pos = kNone;
+    if (__all_sync(0xffffffffu, pos == kNone)) return;  // whole warps only
+#pragma unroll
+    for (int k = 0; k < kFlatSlots; ++k) { sX[w][k][lane] = kNone; sH[w][k][lane] = 0; }
+    sMask[w][lane] = 0;
+    sHown[w][lane] = 0;
+    sFlag[w][lane] = 0;
+    uint32_t own = kNone, cb = 0, nc = 0, ab = 0, na = 0, small = 0;
+    if (pos != kNone) {
+        own = __ldg(pos_owner + pos);
+        cb = __ldg(s.pc_off + pos); nc = __ldg(s.pc_off + pos + 1) - cb;
+        ab = __ldg(s.pa_off + pos); na = __ldg(s.pa_off + pos + 1) - ab;
+        small = __ldg(s.cls_aoff + own + 1) - __ldg(s.cls_aoff + own) <= 64;  // masks feed LCOM-CK (A ≤ 64)
+    }
+    const uint32_t deg = nc + na, incl = warp_incl_scan(deg, lane), excl = incl - deg;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    auto insert = [&](uint32_t j, uint32_t X, uint32_t inc) {
+#pragma unroll 1
+        for (int k = 0; k < kFlatSlots; ++k) {
+            const uint32_t old = atomicCAS(&sX[w][k][j], kNone, X);
+            if (old == kNone || old == X) {
+                if (inc) atomicAdd(&sH[w][k][j], inc);
+                return;
+            }
+        }
+        atomicOr(&sFlag[w][j], 2u);
+    };
+    for (uint32_t base = 0; base < total; base += 64) {
+        uint32_t j[2], X[2], rk[2];
+        bool v[2], isc[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const uint32_t i = base + 32u * u + lane;
+            j[u] = flat_pos(excl, i);
+            const uint32_t ej = __shfl_sync(0xffffffffu, excl, j[u]);
+            const uint32_t cj = __shfl_sync(0xffffffffu, cb, j[u]), ncj = __shfl_sync(0xffffffffu, nc, j[u]);
+            const uint32_t aj = __shfl_sync(0xffffffffu, ab, j[u]);
+            v[u] = i < total;
+            const uint32_t e = i - ej;
+            isc[u] = e < ncj;
+            X[u] = v[u] ? (isc[u] ? __ldg(s.pc_tgt + cj + e) : __ldg(s.pa_tgt + aj + (e - ncj))) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            rk[u] = 0;
+            if (v[u]) {
+                if (isc[u]) {
+                    X[u] = __ldg(s.method_owner + X[u]);
+                } else {
+                    const uint2 ai = __ldg(s.attr_info + X[u]);
+                    X[u] = ai.x;
+                    rk[u] = ai.y;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const uint32_t oj = __shfl_sync(0xffffffffu, own, j[u]), sj = __shfl_sync(0xffffffffu, small, j[u]);
+            if (!v[u]) continue;
+            if (X[u] == oj) {  // own class: counted, inserted once at the end
+                atomicOr(&sFlag[w][j[u]], 1u);
+                if (!isc[u]) {
+                    atomicAdd(&sHown[w][j[u]], 1u);
+                    if (sj) atomicOr(&sMask[w][j[u]], 1ull << rk[u]);
+                }
+            } else {
+                insert(j[u], X[u], isc[u] ? 0u : 1u);
+            }
+        }
+    }
+    __syncwarp();
+    if (pos == kNone) return;
+    // this position's list (foreign slots, then the own class), sorted by class
+    unsigned long long key[kFlatSlots + 1];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kFlatSlots; ++k) {
+        const uint32_t x = sX[w][k][lane];
+        key[k] = x != kNone ? ((unsigned long long)x << 32) | sH[w][k][lane] : ~0ull;
+        cnt += x != kNone;
+    }
+    const uint32_t flag = sFlag[w][lane], hown = sHown[w][lane];
+    key[kFlatSlots] = (flag & 1u) ? ((unsigned long long)own << 32) | hown : ~0ull;
+    cnt += flag & 1u;
+#pragma unroll
+    for (int a = 1; a <= kFlatSlots; ++a)
+#pragma unroll
+        for (int b = a; b > 0; --b) {
+            const unsigned long long lo = min(key[b - 1], key[b]), hi = max(key[b - 1], key[b]);
+            key[b - 1] = lo;
+            key[b] = hi;
+        }
+    bool fits = !(flag & 2u) && cnt <= (uint32_t)kRecMaxEnt && hown < 256;
+    uint32_t ent[kRecMaxEnt];
+#pragma unroll
+    for (int k = 0; k < kRecMaxEnt; ++k) {
+        ent[k] = 0;
+        if ((uint32_t)k < cnt) {
+            const uint32_t x = (uint32_t)(key[k] >> 32), h = (uint32_t)key[k];
+            fits = fits && x < (1u << 24) && h < 256;
+            ent[k] = (x << 8) | h;
+        }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(recs + pos);
+    dst[0] = make_uint4(ent[0], ent[1], ent[2], ent[3]);
+    dst[1] = make_uint4(ent[4], ent[5], ent[6], ent[7]);
+    rec_hdrs(recs, s.M)[pos] = fits ? cnt | (hown << kRecHownShift) : kRecOverflow;
+    own_mask[pos] = sMask[w][lane];
+}
+
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
                    uint32_t max_deg, const uint32_t* plist, uint32_t n_pos, cudaStream_t st) {
     const uint32_t n = plist ? n_pos : s.M;
     if (!n) return;
     const uint32_t blocks = (n + 255) / 256;
-    if (max_deg > 8)  // some method needs several chunks: regroup by chunk count
+    if (max_deg > 8 && MMGPU_METHOD_FLAT)  // rows longer than a chunk: edges flattened over the lanes
+        k_method_flat<<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner, plist, n_pos);
+    else if (max_deg > 8)  // some method needs several chunks: regroup by chunk count
         k_method<8, true><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner, plist, n_pos);
     else
         k_method<8, false><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner, plist, n_pos);
