@@ -893,10 +893,28 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
     const uint32_t dwords = (s.C + 31) / 32;
     uint32_t nx = 0, ubase = 0, nk = 0;
     if (pl.hist) {
-        // phase 2 (histogram): the nonzero counts, in class order, are the U row
-        uint32_t mine = 0;
-        for (uint32_t k = threadIdx.x; k < s.C; k += blockDim.x) mine += cnt[k] != 0u;
-        nx = (uint32_t)block_sum_u64(mine, red64);
+        // phase 2 (histogram): the nonzero counts, in class order, are the U
+        // row. Each warp owns a contiguous range of whole 32-class words:
+        // it counts its nonzeros (ballots), one barrier publishes the warp
+        // counts (their prefix = the warp's offset in the row), and the warp
+        // writes its entries in order — two barriers per class, not two per
+        // blockDim classes (C5: 5000 classes scanned by 256 threads had 40)
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+        const uint32_t seg = (s.C + 32u * nwarps - 1) / (32u * nwarps) * 32u;
+        const uint32_t k0 = min(s.C, (uint32_t)warp * seg), k1 = min(s.C, k0 + seg);
+        uint32_t wcnt = 0;
+        for (uint32_t b = k0; b < k1; b += 32) {
+            const uint32_t k = b + lane;
+            wcnt += __popc(__ballot_sync(0xffffffffu, k < k1 && cnt[k] != 0u));
+        }
+        if (lane == 0) red32[warp] = wcnt;
+        __syncthreads();
+        uint32_t woff = 0;
+        for (int w2 = 0; w2 < nwarps; ++w2) {
+            const uint32_t c2 = red32[w2];
+            woff += w2 < warp ? c2 : 0u;
+            nx += c2;
+        }
         if (threadIdx.x == 0) {
             s_ubase = kSmallRowCap * s.M + (nx ? atomicAdd(ucursor, nx) : 0u);
             s_dense = kNone;
@@ -908,29 +926,27 @@ k_class_large(DevModel s, const uint32_t* __restrict__ large_list, const LargePl
         __syncthreads();
         ubase = s_ubase;
         const uint32_t dn = s_dense;
-        const int lane = threadIdx.x & 31;
-        uint32_t xcarry = 0;
-        for (uint32_t b = 0; b < s.C; b += blockDim.x) {
-            const uint32_t k = b + threadIdx.x;
-            const uint32_t v = k < s.C ? cnt[k] : 0u;
-            uint32_t tot;
-            const uint32_t ex = block_excl_scan(v != 0u ? 1u : 0u, red32, &tot);
+        uint32_t run = woff;
+        for (uint32_t b = k0; b < k1; b += 32) {
+            const uint32_t k = b + lane;
+            const uint32_t v = k < k1 ? cnt[k] : 0u;
+            const uint32_t m = __ballot_sync(0xffffffffu, v != 0u);
             if (v) {
-                ux[ubase + xcarry + ex] = k;
-                un[ubase + xcarry + ex] = v;
+                const uint32_t at = ubase + run + __popc(m & ((1u << lane) - 1u));
+                ux[at] = k;
+                un[at] = v;
                 const uint32_t b1 = bloom_h1(k), b2 = bloom_h2(k);
                 atomicOr(s_sig + (b1 >> 5), 1u << (b1 & 31));
                 atomicOr(s_sig + (b2 >> 5), 1u << (b2 & 31));
             }
-            if (dn != kNone) {  // warps cover whole 32-class words: membership, singletons
-                const uint32_t m = __ballot_sync(0xffffffffu, v != 0u);
+            if (dn != kNone) {  // whole 32-class words: membership, singletons
                 const uint32_t one = __ballot_sync(0xffffffffu, v == 1u);
-                if (lane == 0 && (k >> 5) < dwords) {
-                    dense[dn + (k >> 5)] = m;
-                    dense[dn + dwords + (k >> 5)] = one;
+                if (lane == 0) {
+                    dense[dn + (b >> 5)] = m;
+                    dense[dn + dwords + (b >> 5)] = one;
                 }
             }
-            xcarry += tot;
+            run += __popc(m);
         }
     } else {
         nk = s_nk;
@@ -1200,153 +1216,12 @@ void launch_pos_rows(const DevModel& s, const uint32_t* pos_owner, uint32_t* pc_
                                             foreign, cmaxdeg, n_hideg);
 }
 
-// The method pass for rows longer than one chunk (dense shapes like C5:
-// up to 36 edges per method), flattened: one warp per 32 listed positions,
-// their edges spread over the lanes (warp scan of the degrees, two edges per
-// lane per round, loads issued before use), so every round reads 32
-// consecutive class-order targets and no lane idles behind the warp's
-// longest row. Per position, in shared memory: the distinct foreign classes
-// (first-fit atomicCAS slots, an access adds 1 to its class's count), the
-// own-attribute mask, the own-access count. Each lane then sorts its
-// position's list (own class included) and writes the same MethRec, header
-// and mask as k_method (a list longer than a record holds is flagged
-// overflow; consumers then read the CSR and ignore the entries).
-#ifndef MMGPU_METHOD_FLAT
-#define MMGPU_METHOD_FLAT 1
-#endif
-constexpr int kFlatSlots = kRecMaxEnt + 1;  // a 9th distinct class proves overflow
-
-__global__ void __launch_bounds__(256) k_method_flat(DevModel s, MethRec* __restrict__ recs,
-                                                     uint64_t* __restrict__ own_mask,
-                                                     const uint32_t* __restrict__ pos_owner,
-                                                     const uint32_t* __restrict__ plist, uint32_t n_pos) {
-    __shared__ uint32_t sX[8][kFlatSlots][32], sH[8][kFlatSlots][32];
-    __shared__ unsigned long long sMask[8][32];
-    __shared__ uint32_t sHown[8][32], sFlag[8][32];  // flag: 1 own class used, 2 more classes than slots
-    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t n = plist ? n_pos : s.M;
-    uint32_t pos = kNone;
-    if (idx < n) pos = plist ? __ldg(plist + idx) : idx;
-    if (pos >= s.M) pos = kNone;
-    if (__all_sync(0xffffffffu, pos == kNone)) return;  // whole warps only
-#pragma unroll
-    for (int k = 0; k < kFlatSlots; ++k) { sX[w][k][lane] = kNone; sH[w][k][lane] = 0; }
-    sMask[w][lane] = 0;
-    sHown[w][lane] = 0;
-    sFlag[w][lane] = 0;
-    uint32_t own = kNone, cb = 0, nc = 0, ab = 0, na = 0, small = 0;
-    if (pos != kNone) {
-        own = __ldg(pos_owner + pos);
-        cb = __ldg(s.pc_off + pos); nc = __ldg(s.pc_off + pos + 1) - cb;
-        ab = __ldg(s.pa_off + pos); na = __ldg(s.pa_off + pos + 1) - ab;
-        small = __ldg(s.cls_aoff + own + 1) - __ldg(s.cls_aoff + own) <= 64;  // masks feed LCOM-CK (A ≤ 64)
-    }
-    const uint32_t deg = nc + na, incl = warp_incl_scan(deg, lane), excl = incl - deg;
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    __syncwarp();
-    auto insert = [&](uint32_t j, uint32_t X, uint32_t inc) {
-#pragma unroll 1
-        for (int k = 0; k < kFlatSlots; ++k) {
-            const uint32_t old = atomicCAS(&sX[w][k][j], kNone, X);
-            if (old == kNone || old == X) {
-                if (inc) atomicAdd(&sH[w][k][j], inc);
-                return;
-            }
-        }
-        atomicOr(&sFlag[w][j], 2u);
-    };
-    for (uint32_t base = 0; base < total; base += 64) {
-        uint32_t j[2], X[2], rk[2];
-        bool v[2], isc[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const uint32_t i = base + 32u * u + lane;
-            j[u] = flat_pos(excl, i);
-            const uint32_t ej = __shfl_sync(0xffffffffu, excl, j[u]);
-            const uint32_t cj = __shfl_sync(0xffffffffu, cb, j[u]), ncj = __shfl_sync(0xffffffffu, nc, j[u]);
-            const uint32_t aj = __shfl_sync(0xffffffffu, ab, j[u]);
-            v[u] = i < total;
-            const uint32_t e = i - ej;
-            isc[u] = e < ncj;
-            X[u] = v[u] ? (isc[u] ? __ldg(s.pc_tgt + cj + e) : __ldg(s.pa_tgt + aj + (e - ncj))) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            rk[u] = 0;
-            if (v[u]) {
-                if (isc[u]) {
-                    X[u] = __ldg(s.method_owner + X[u]);
-                } else {
-                    const uint2 ai = __ldg(s.attr_info + X[u]);
-                    X[u] = ai.x;
-                    rk[u] = ai.y;
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const uint32_t oj = __shfl_sync(0xffffffffu, own, j[u]), sj = __shfl_sync(0xffffffffu, small, j[u]);
-            if (!v[u]) continue;
-            if (X[u] == oj) {  // own class: counted, inserted once at the end
-                atomicOr(&sFlag[w][j[u]], 1u);
-                if (!isc[u]) {
-                    atomicAdd(&sHown[w][j[u]], 1u);
-                    if (sj) atomicOr(&sMask[w][j[u]], 1ull << rk[u]);
-                }
-            } else {
-                insert(j[u], X[u], isc[u] ? 0u : 1u);
-            }
-        }
-    }
-    __syncwarp();
-    if (pos == kNone) return;
-    // this position's list (foreign slots, then the own class), sorted by class
-    unsigned long long key[kFlatSlots + 1];
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int k = 0; k < kFlatSlots; ++k) {
-        const uint32_t x = sX[w][k][lane];
-        key[k] = x != kNone ? ((unsigned long long)x << 32) | sH[w][k][lane] : ~0ull;
-        cnt += x != kNone;
-    }
-    const uint32_t flag = sFlag[w][lane], hown = sHown[w][lane];
-    key[kFlatSlots] = (flag & 1u) ? ((unsigned long long)own << 32) | hown : ~0ull;
-    cnt += flag & 1u;
-#pragma unroll
-    for (int a = 1; a <= kFlatSlots; ++a)
-#pragma unroll
-        for (int b = a; b > 0; --b) {
-            const unsigned long long lo = min(key[b - 1], key[b]), hi = max(key[b - 1], key[b]);
-            key[b - 1] = lo;
-            key[b] = hi;
-        }
-    bool fits = !(flag & 2u) && cnt <= (uint32_t)kRecMaxEnt && hown < 256;
-    uint32_t ent[kRecMaxEnt];
-#pragma unroll
-    for (int k = 0; k < kRecMaxEnt; ++k) {
-        ent[k] = 0;
-        if ((uint32_t)k < cnt) {
-            const uint32_t x = (uint32_t)(key[k] >> 32), h = (uint32_t)key[k];
-            fits = fits && x < (1u << 24) && h < 256;
-            ent[k] = (x << 8) | h;
-        }
-    }
-    uint4* dst = reinterpret_cast<uint4*>(recs + pos);
-    dst[0] = make_uint4(ent[0], ent[1], ent[2], ent[3]);
-    dst[1] = make_uint4(ent[4], ent[5], ent[6], ent[7]);
-    rec_hdrs(recs, s.M)[pos] = fits ? cnt | (hown << kRecHownShift) : kRecOverflow;
-    own_mask[pos] = sMask[w][lane];
-}
-
 void launch_method(const DevModel& s, MethRec* recs, uint64_t* own_mask, const uint32_t* pos_owner,
                    uint32_t max_deg, const uint32_t* plist, uint32_t n_pos, cudaStream_t st) {
     const uint32_t n = plist ? n_pos : s.M;
     if (!n) return;
     const uint32_t blocks = (n + 255) / 256;
-    if (max_deg > 8 && MMGPU_METHOD_FLAT)  // rows longer than a chunk: edges flattened over the lanes
-        k_method_flat<<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner, plist, n_pos);
-    else if (max_deg > 8)  // some method needs several chunks: regroup by chunk count
+    if (max_deg > 8)  // some method needs several chunks: regroup by chunk count
         k_method<8, true><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner, plist, n_pos);
     else
         k_method<8, false><<<blocks, 256, 0, st>>>(s, recs, own_mask, pos_owner, plist, n_pos);

@@ -766,7 +766,10 @@ __device__ __forceinline__ void write_best(const SweepArgs& a, uint32_t pos, uin
     if (db != kNone) one(db, rb, lb_b);
 }
 
-constexpr int kOffItems = 16;  // 4096-position tiles: ≤ 245 tiles for 1M methods, one resident wave
+#ifndef MMGPU_OFF_ITEMS
+#define MMGPU_OFF_ITEMS 16
+#endif
+constexpr int kOffItems = MMGPU_OFF_ITEMS;  // 16: 4096-position tiles, ≤ 245 tiles for 1M methods, one resident wave
 constexpr uint32_t kOffTile = kSweepTile * kOffItems;
 
 // one method's pass-1 result under the class gates and the criteria merge:
