@@ -13,8 +13,9 @@
  * relative to /root/reference/proj/include/modmetrics/).
  *
  * Threading: one mm_ctx == one CUDA device + one CUDA stream. A context is
- * not thread-safe; distinct contexts (one per GPU) may be driven from
- * distinct host threads or processes.
+ * not thread-safe; distinct contexts — one per GPU, or several on one GPU to
+ * pipeline requests — may be driven from distinct host threads or processes
+ * (tests/test_gpu_concurrency.py).
  */
 #ifndef MMGPU_H
 #define MMGPU_H
