@@ -610,12 +610,17 @@ __global__ void __launch_bounds__(kScoreTile, MMGPU_SCORE_MINB * (kSweepTile / k
 // (exact bitmap of a dense row, else the Bloom signature, the row only on a
 // positive). Argmin over (key, d) with strict < in ascending d
 // (suggest.hpp:180-184). Incomplete records go to k_score_thread's list.
-__global__ void __launch_bounds__(kSweepTile, MMGPU_FAST_MINB) k_score_fast(SweepArgs a) {
+#ifndef MMGPU_FAST_TILE
+#define MMGPU_FAST_TILE 64
+#endif
+constexpr int kFastTile = MMGPU_FAST_TILE;  // block size of k_score_fast (64: C4 scoring 62.5 -> 60 us against 256, uneven per-method work)
+static_assert(kSweepTile % kFastTile == 0, "fast-score tile divides the sweep tile");
+__global__ void __launch_bounds__(kFastTile, MMGPU_FAST_MINB * (kSweepTile / kFastTile)) k_score_fast(SweepArgs a) {
     // the used list column-major in shared memory (thread t's k-th entry at
     // [k][t]: conflict-free), so the candidate and membership loops stay
     // rolled: small code, lanes of a warp in step
-    __shared__ uint32_t s_ent[kRecMaxEnt][kSweepTile];
-    const uint32_t pos = a.pos_begin + blockIdx.x * kSweepTile + threadIdx.x;
+    __shared__ uint32_t s_ent[kRecMaxEnt][kFastTile];
+    const uint32_t pos = a.pos_begin + blockIdx.x * kFastTile + threadIdx.x;
     const bool live = pos < a.pos_end;
     const int lane = threadIdx.x & 31;
     uint32_t hdr = kRecOverflow;
@@ -636,8 +641,8 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_FAST_MINB) k_score_fast(Swee
         const uint4 ro = __ldg(reinterpret_cast<const uint4*>(a.rec + o));  // A, M, H, cbo
         const uint32_t n = rec_n(hdr), hown = rec_hown(hdr);
         uint32_t* E = &s_ent[0][threadIdx.x];
-        E[0 * kSweepTile] = r0.x; E[1 * kSweepTile] = r0.y; E[2 * kSweepTile] = r0.z; E[3 * kSweepTile] = r0.w;
-        E[4 * kSweepTile] = r1.x; E[5 * kSweepTile] = r1.y; E[6 * kSweepTile] = r1.z; E[7 * kSweepTile] = r1.w;
+        E[0 * kFastTile] = r0.x; E[1 * kFastTile] = r0.y; E[2 * kFastTile] = r0.z; E[3 * kFastTile] = r0.w;
+        E[4 * kFastTile] = r1.x; E[5 * kFastTile] = r1.y; E[6 * kFastTile] = r1.z; E[7 * kFastTile] = r1.w;
         // origin side (make_origin_score)
         bool coh_ok = false;
         double lo_a = 0.0;
@@ -654,18 +659,18 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_FAST_MINB) k_score_fast(Swee
         double bkc = 0.0;
 #pragma unroll 1
         for (uint32_t k = 0; k < n; ++k) {
-            const uint32_t d = E[k * kSweepTile] >> 8;
+            const uint32_t d = E[k * kFastTile] >> 8;
             if (d == o) continue;
             ++cands;
             if (!coh_ok && !can_coup) continue;
-            const uint32_t h = E[k * kSweepTile] & 0xffu;
+            const uint32_t h = E[k * kFastTile] & 0xffu;
             // the first other used class's two signature words requested with d's
             // record (their addresses need only d and X): the common coupling
             // rejection then costs one memory round trip, not two
             uint32_t X0 = kNone, sw1 = 0, sw2 = 0, sb1 = 0, sb2 = 0;
             if (can_coup) {
                 X0 = E[0] >> 8;
-                if (X0 == d) X0 = n > 1 ? E[kSweepTile] >> 8 : kNone;
+                if (X0 == d) X0 = n > 1 ? E[kFastTile] >> 8 : kNone;
                 if (X0 != kNone) {
                     sb1 = bloom_h1(X0);
                     sb2 = bloom_h2(X0);
@@ -689,7 +694,7 @@ __global__ void __launch_bounds__(kSweepTile, MMGPU_FAST_MINB) k_score_fast(Swee
                 bool okc = X0 == kNone || rd.dense != kNone || (((sw1 >> (sb1 & 31)) & (sw2 >> (sb2 & 31)) & 1u) != 0);
 #pragma unroll 1
                 for (uint32_t j = 0; j < n && okc; ++j) {
-                    const uint32_t X = E[j * kSweepTile] >> 8;
+                    const uint32_t X = E[j * kFastTile] >> 8;
                     if (X != d) okc = in_urow(a.rec, d, rd, a.ux, a.dense, X);
                 }
                 if (okc) { bd_coup = d; bkp = rd.cbo; }
@@ -1102,7 +1107,7 @@ void launch_score(const SweepArgs& a, uint32_t n_tiles, cudaStream_t st) {
 uint32_t offsets_tiles(uint64_t npos) { return (uint32_t)((npos + kOffTile - 1) / kOffTile); }
 
 void launch_score_fast(const SweepArgs& a, uint32_t n_tiles, uint32_t fallback_tiles, cudaStream_t st) {
-    if (n_tiles) k_score_fast<<<n_tiles, kSweepTile, 0, st>>>(a);
+    if (n_tiles) k_score_fast<<<n_tiles * (kSweepTile / kFastTile), kFastTile, 0, st>>>(a);
     if (!fallback_tiles) return;  // incomplete records (their list is built above)
     const uint32_t blocks = fallback_tiles * (kSweepTile / kScoreTile);
     if (a.maxdeg_fast <= 8) k_score_thread<8, true><<<blocks, kScoreTile, 0, st>>>(a);
