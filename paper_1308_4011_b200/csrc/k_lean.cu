@@ -227,7 +227,10 @@ k_class_lean(DevModel s, const uint4* __restrict__ cplan, const uint4* __restric
 //     metrics.hpp:135-157) and lcom (metrics.hpp:114-126) per class.
 // Outputs are the same arrays k_class_lean writes (records, headers, class
 // records, lcom / LCOM-CK / cbo, U rows at 16·(first member position)).
-constexpr int kGroupWarps = 4;
+#ifndef MMGPU_GROUP_WARPS
+#define MMGPU_GROUP_WARPS 4
+#endif
+constexpr int kGroupWarps = MMGPU_GROUP_WARPS;
 constexpr uint32_t kGroupKeys = 64;  // (class, foreign X, member) keys per group (the plan bounds foreign edges)
 
 struct __align__(16) GroupWarp {
