@@ -1199,7 +1199,7 @@ void launch_plan_classes(const DevModel& s, uint4* cplan, uint4* cedge, uint32_t
 }
 void launch_pos_rows(const DevModel& s, const uint32_t* pos_owner, uint32_t* pc_off, uint32_t* pc_tgt,
                      uint32_t* pa_off, uint32_t* pa_tgt, uint8_t* pc_mem, uint8_t* pa_mem, uint32_t* totals,
-                     uint32_t* grand, uint32_t* foreign, uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st) {
+                     uint32_t* foreign, uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st) {
     if (s.C) {
         cudaMemsetAsync(foreign, 0, 4ull * s.C, st);
         cudaMemsetAsync(cmaxdeg, 0, 4ull * s.C, st);

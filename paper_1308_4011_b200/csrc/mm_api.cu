@@ -688,8 +688,7 @@ mm_status mm_upload(mm_ctx* ctx, const mm_system* s) {
     MM_CUDA(ctx, ctx->cmaxdeg.ensure(C ? C : 1));
     st = run(ctx, "upload_rows", [&] {
         launch_pos_rows(ctx->dev(), ctx->pos_owner.p, ctx->pc_off.p, ctx->pc_tgt.p, ctx->pa_off.p, ctx->pa_tgt.p,
-                        ctx->pc_mem.p, ctx->pa_mem.p, ctx->pos_scan.p, ctx->pos_scan.p + (M + 1ull + 1023) / 1024 + 1,
-                        ctx->foreign.p, ctx->cmaxdeg.p, &ctl->n_hideg, ctx->stream);
+                        ctx->pc_mem.p, ctx->pa_mem.p, ctx->pos_scan.p, ctx->foreign.p, ctx->cmaxdeg.p, &ctl->n_hideg, ctx->stream);
     });
     if (st) return st;
     tr.mark("pos_rows");

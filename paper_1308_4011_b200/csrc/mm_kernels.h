@@ -71,7 +71,7 @@ void launch_plan_classes(const DevModel& s, uint4* cplan, uint4* cedge, uint32_t
 // class plan's per-class foreign-edge counts / largest degree / n_hideg
 void launch_pos_rows(const DevModel& s, const uint32_t* pos_owner, uint32_t* pc_off, uint32_t* pc_tgt,
                      uint32_t* pa_off, uint32_t* pa_tgt, uint8_t* pc_mem, uint8_t* pa_mem, uint32_t* totals,
-                     uint32_t* grand, uint32_t* foreign, uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st);
+                     uint32_t* foreign, uint32_t* cmaxdeg, uint32_t* n_hideg, cudaStream_t st);  // totals: 2 per 256-position tile
 void launch_class_lean(const DevModel& s, const uint4* cplan, const uint4* cedge, const uint8_t* pc_mem,
                        const uint8_t* pa_mem, MethRec* recs, ClassRec* rec, double* lcom,
                        uint64_t* ck, uint32_t* cbo, uint32_t* ux, uint32_t* un, const uint32_t* list,
